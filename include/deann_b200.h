@@ -1,0 +1,173 @@
+/*
+ * deann_b200.h — C-ABI of the B200-native DEANN KDE query path.
+ *
+ * This is the drop-in boundary under the Python estimator API of the
+ * reference package `deann` (arXiv 2107.02736).  The reference is pure
+ * Python/NumPy and has no FFI of its own; each entry point below names the
+ * reference function whose contract it implements (paths relative to
+ * /root/reference/pkg/src/deann/).  The binding a maintainer would add to the
+ * reference package is shown in INTEGRATION.md (ctypes).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Every array pointer may be HOST or
+ *     DEVICE memory; the library inspects it (cudaPointerGetAttributes) and
+ *     stages host arrays through its own device workspace.  Outputs follow
+ *     the same rule.
+ *   - Row-major, C-contiguous.  Dataset rows are fp32 (reference Dataset
+ *     stores float32, data.py:55); queries are fp64 (the reference casts
+ *     queries to float64, estimators.py:129,156,333).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *     Calls are stream-ordered; when any output pointer is host memory the
+ *     call synchronises the stream before returning.
+ *   - Every function returns a dk_status; on failure dk_last_error() returns
+ *     a thread-local message.  Argument errors (DK_EINVAL) are raised for
+ *     exactly the preconditions the reference raises ValueError for.
+ *   - A handle is read-only after dk_fit; concurrent calls on one handle
+ *     must use distinct handles (the workspace is per handle).
+ */
+#ifndef DEANN_B200_H
+#define DEANN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DK_OK = 0,
+  DK_EINVAL = 1,    /* argument/range/dimension error  -> ValueError          */
+  DK_ECUDA = 2,     /* CUDA runtime/driver failure     -> RuntimeError        */
+  DK_ENOMEM = 3,    /* device allocation failed        -> MemoryError         */
+  DK_EINEXACT = 4,  /* k-NN certificate failed (see dk_knn)                   */
+  DK_ENODEV = 5     /* no sm_100 device                                       */
+} dk_status;
+
+/* Kernel families, same order/meaning as kernels.py:22-39
+ * (gaussian -> squared L2, exponential -> L2, laplacian -> L1). */
+typedef enum {
+  DK_GAUSSIAN = 0,
+  DK_EXPONENTIAL = 1,
+  DK_LAPLACIAN = 2
+} dk_family;
+
+/* Operand precision for the tensor-core distance tile (dk_fit_opts.precision). */
+typedef enum {
+  DK_PREC_AUTO = 0,    /* exact fp16 when rows and queries are small integers, else split3 */
+  DK_PREC_SPLIT3 = 1,  /* fp16 hi/lo, K-concatenated [Qh|Qh|Ql]x[Xh|Xl|Xh] (~2^-22 rel)   */
+  DK_PREC_FP16 = 2     /* single-pass fp16 (fast, ~1e-3..1e-5 rel; opt-in only)           */
+} dk_precision;
+
+typedef struct dk_dataset* dk_handle;
+
+typedef struct {
+  int32_t device;        /* CUDA device ordinal                                   */
+  int32_t precision;     /* dk_precision                                          */
+  int64_t global_offset; /* dataset-sharded mode: global index of local row 0     */
+  int64_t global_n;      /* dataset-sharded mode: total rows over all shards (0 = n) */
+} dk_fit_opts;
+
+/* Flags for dk_naive / dk_sample. */
+#define DK_OUT_SUM 1u    /* write per-query kernel SUMS (fp64) instead of means  */
+
+/* ---- version / errors ---------------------------------------------------- */
+int32_t dk_version(void);
+const char* dk_last_error(void);
+int32_t dk_device_ok(int32_t device);   /* 1 if `device` is sm_100 (B200) */
+
+/* ---- fit ------------------------------------------------------------------
+ * Replaces Dataset.from_array + data64() + sq_norms (data.py:53-83) and
+ * BruteForceIndex(ds) (ann.py:114-118): copies X (n x d fp32) to the device,
+ * validates finiteness (ValueError at data.py:61-62), computes fp64 row norms
+ * (data.py:63-64) and the tensor-core operand encodings. */
+dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts,
+                 dk_handle* out);
+dk_status dk_free(dk_handle h);
+dk_status dk_info(dk_handle h, int64_t* n, int32_t* d, int64_t* global_offset,
+                  int64_t* global_n, int32_t* exact_mode);
+/* fp64 squared row norms (n), cf. Dataset.sq_norms (data.py:64). */
+dk_status dk_sq_norms(dk_handle h, double* out, void* stream);
+
+/* ---- exact KDE ------------------------------------------------------------
+ * naive_kde (estimators.py:122-149): out[j] = (1/n) sum_i K_h(q_j, x_i), fp64.
+ * Gaussian/exponential run the fused tcgen05 distance-tile + exp + row-sum;
+ * laplacian runs the CUDA-core L1 kernel.  With DK_OUT_SUM the un-normalised
+ * local sum is written (dataset-sharded partials). */
+dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family,
+                   double bandwidth, uint32_t flags, double* out, void* stream);
+
+/* ---- exact k-NN -----------------------------------------------------------
+ * brute_force_knn (ann.py:105-111) / BruteForceIndex.query (ann.py:120-121)
+ * for a batch: idx_out (nq x k, int64, GLOBAL row ids), d2_out (nq x k, fp64
+ * squared L2 by direct difference), each row sorted by (d2, idx) — ties to the
+ * lower index as in _smallest_k (ann.py:82-102).  Requires 1 <= k <= n
+ * (ValueError at ann.py:107-108).  Candidates are selected on tensor-core
+ * distance tiles and re-ranked exactly in fp64; a per-query certificate
+ * proves the set; DK_EINEXACT if it could not be proven (never observed). */
+dk_status dk_knn(dk_handle h, const double* Q, int64_t nq, int32_t k,
+                 int64_t* idx_out, double* d2_out, void* stream);
+
+/* Merge of per-shard top-k lists for dataset-sharded mode: `parts` lists of
+ * (idx, d2) per query laid out [part][query][k], each sorted by (d2, idx);
+ * writes the global top-k.  Pure device work. */
+dk_status dk_merge_topk(int32_t parts, int64_t nq, int32_t k,
+                        const int64_t* idx_in, const double* d2_in,
+                        int64_t* idx_out, double* d2_out, void* stream);
+
+/* ---- sampling (RS / DEANN residual) ---------------------------------------
+ * rs_kde (estimators.py:152-164) and _rs_excluding (estimators.py:203-233):
+ * for query j, draw t = 0,1,2,... gives row
+ *   r_t = mulhi64(philox4x32_10(key=seed, ctr={t, j+query_base, 0, 0}) as u64, N)
+ * over the GLOBAL index space N (= global_n); the first m draws NOT in the
+ * exclusion list excl[j*excl_stride .. +excl_cnt[j]) (any order) are accepted
+ * ("first m accepted of the stream" = the reference's effective rule).  For
+ * accepted rows inside this shard the kernel value is computed in fp64 (direct
+ * difference) and summed: z_sum[j].  Optionally exports accepted row ids
+ * (nq x m) and the number of draws consumed per query.  excl may be NULL
+ * (plain RS).  m >= 1. */
+dk_status dk_sample(dk_handle h, const double* Q, int64_t nq, int32_t family,
+                    double bandwidth, int32_t m, uint64_t seed, int64_t query_base,
+                    const int64_t* excl, const int32_t* excl_cnt, int32_t excl_stride,
+                    double* z_sum, int64_t* accepted_idx_out, int64_t* draws_out,
+                    void* stream);
+
+/* Kernel sums over explicit rows: out[j] = sum_{c<cnt} K(q_j, x_rows[j*stride+c]),
+ * fp64 direct difference (cf. _kernel_rows, estimators.py:106-119).  Rows are
+ * GLOBAL ids; rows outside this shard contribute 0.  Used for Z1 of the
+ * laplacian family (estimators.py:346-348) and for parity with explicit ids. */
+dk_status dk_eval_rows(dk_handle h, const double* Q, int64_t nq, int32_t family,
+                       double bandwidth, const int64_t* rows, const int32_t* cnt,
+                       int32_t stride, double* out, void* stream);
+
+/* kernel_from_distance (kernels.py:65-83) on the device: out[i] =
+ * exp(-dist[i]/(2h^2)) for gaussian (dist = squared L2), exp(-dist[i]/h) for
+ * exponential (L2) and laplacian (L1); fp64.  Non-finite or negative
+ * distances -> DK_EINVAL (kernels.py:74-77). */
+dk_status dk_kernel_values(int32_t family, double bandwidth, const double* dist, int64_t count, double* out,
+                           void* stream);
+
+/* ---- DEANN (single GPU, whole dataset) -------------------------------------
+ * deann (estimators.py:306-379) with ann = exact brute force and the uniform
+ * sampler, batched over nq queries (deann_batch, estimators.py:382-410):
+ *   value = (k/n) Z1 + ((n-k)/n) Z2,  Z1 from the exact neighbour distances
+ * (L2 families, estimators.py:349-351) or recomputed L1 (laplacian, :346-348).
+ * k == 0 -> pure RS (no k-NN); m == 0 -> truncated (k/n) Z1.  Preconditions as
+ * estimators.py:322-335.  Optional exports: neighbours (nq x k), accepted
+ * sample ids (nq x m). */
+dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family,
+                   double bandwidth, int32_t k, int32_t m, uint64_t seed,
+                   int64_t query_base, double* value_out, int64_t* nbr_idx_out,
+                   double* nbr_d2_out, int64_t* sample_idx_out, void* stream);
+
+/* Timing support for bench.py: average device duration (ms) of the LAST launch
+ * of the dominant kernel of the last call on this handle (CUDA events on the
+ * launching stream) and its algorithmic work. */
+dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* bytes);
+dk_status dk_set_profiling(dk_handle h, int32_t on);
+/* Number of this library's kernels launched by the last API call. */
+dk_status dk_last_launch_count(dk_handle h, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEANN_B200_H */

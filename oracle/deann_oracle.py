@@ -1,0 +1,261 @@
+"""CPU oracle for the DEANN KDE query path — TEST INFRASTRUCTURE ONLY.
+
+This module is the checker, never the product: only tests/, the smoke() of
+__graft_entry__.py and bench.py's cpu_baseline / --impl reference arm may
+import it.  It restates, in plain NumPy (fp64 throughout), the algorithms of
+the reference package `deann` 0.1.0 (/root/reference/pkg/src/deann/), each
+function citing the lines it follows.  It is pinned against golden vectors
+produced by importing the real reference (tests/golden/make_golden.py ->
+tests/golden/*.npz, checked by tests/test_oracle.py).
+
+The arithmetic dependency of the reference is NumPy/OpenBLAS (unpinned,
+`numpy>=1.24`, pyproject.toml:10): DGEMM in batch_sqdist, einsum norms,
+np.exp, argpartition/lexsort, PCG64 Generator.integers.  This restatement
+uses the same NumPy calls for the same steps, so agreement with the
+reference is at the 1e-15 level.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+__all__ = [
+    "row_norms", "batch_sqdist", "kernel_from_distance", "kernel_from_sql2", "kernel_rows", "naive_kde",
+    "rs_kde", "rs_excluding", "smallest_k", "brute_force_knn", "deann", "deann_batch", "kernel_pair",
+]
+
+BLOCK_ENTRIES = 4_000_000  # estimators.py:54
+CLAMP_REL = 1e-3           # distance.py:25
+
+
+class NormConsistencyError(RuntimeError):
+    """distance.py:28-29"""
+
+
+def as_rows(data) -> np.ndarray:
+    """Dataset.from_array storage: C-contiguous float32 (data.py:55)."""
+    return np.ascontiguousarray(data, dtype=np.float32)
+
+
+def row_norms(x32: np.ndarray) -> np.ndarray:
+    """fp64 squared row norms via einsum (data.py:63-64)."""
+    d64 = x32.astype(np.float64)
+    return np.einsum("ij,ij->i", d64, d64)
+
+
+def kernel_from_distance(family: str, h: float, dist):
+    """kernels.py:65-83: validates finite & >= 0, then exp(-d/(2h^2)) or exp(-d/h)."""
+    scalar = np.isscalar(dist) or np.ndim(dist) == 0
+    d = np.asarray(dist, dtype=np.float64)
+    if not np.all(np.isfinite(d)):
+        raise ValueError("distance must be finite")
+    if np.any(d < 0.0):
+        raise ValueError("distance must be nonnegative")
+    out = np.exp(-d / (2.0 * h * h)) if family == "gaussian" else np.exp(-d / h)
+    return float(out) if scalar else out
+
+
+def kernel_pair(family: str, h: float, x, y) -> float:
+    """kernels.py:86-106: scalar oracle with the family's own metric."""
+    diff = np.asarray(x, dtype=np.float64).ravel() - np.asarray(y, dtype=np.float64).ravel()
+    if family == "gaussian":
+        dist = float(diff @ diff)
+    elif family == "exponential":
+        dist = math.sqrt(float(diff @ diff))
+    else:
+        dist = float(np.abs(diff).sum())
+    return kernel_from_distance(family, h, dist)
+
+
+def _clamp(d2: np.ndarray, scale: float) -> np.ndarray:
+    """distance.py:58-66"""
+    tol = CLAMP_REL * max(scale, 1.0)
+    worst = d2.min() if d2.size else 0.0
+    if worst < -tol:
+        raise NormConsistencyError(f"batch distance {worst:g} below clamp tolerance {-tol:g}")
+    np.maximum(d2, 0.0, out=d2)
+    return d2
+
+
+def batch_sqdist(q: np.ndarray, x64: np.ndarray, sq_norms: np.ndarray) -> np.ndarray:
+    """distance.py:69-85: ||q||^2 + ||x||^2 - 2 q.x in fp64, clamped."""
+    q = np.atleast_2d(np.asarray(q, dtype=np.float64))
+    q_norms = np.einsum("ij,ij->i", q, q)
+    d2 = q @ x64.T
+    d2 *= -2.0
+    d2 += q_norms[:, None]
+    d2 += sq_norms[None, :]
+    scale = float(q_norms.max(initial=0.0) + sq_norms.max(initial=0.0))
+    return _clamp(d2, scale)
+
+
+def kernel_from_sql2(family: str, h: float, d2: np.ndarray) -> np.ndarray:
+    """estimators.py:99-103"""
+    if family == "gaussian":
+        return kernel_from_distance(family, h, d2)
+    return kernel_from_distance(family, h, np.sqrt(d2))
+
+
+def kernel_rows(x64: np.ndarray, sq_norms: np.ndarray, family: str, h: float, rows: np.ndarray,
+                y: np.ndarray) -> np.ndarray:
+    """estimators.py:106-119"""
+    if len(rows) == 0:
+        return np.empty(0, dtype=np.float64)
+    x = x64[rows]
+    if family == "laplacian":
+        return kernel_from_distance(family, h, np.abs(x - y).sum(axis=1))
+    d2 = x @ y
+    d2 *= -2.0
+    d2 += sq_norms[rows]
+    d2 += float(y @ y)
+    np.maximum(d2, 0.0, out=d2)
+    return kernel_from_sql2(family, h, d2)
+
+
+class Data:
+    """Oracle-side dataset: fp32 rows, fp64 copy, fp64 norms (data.py:45-83)."""
+
+    def __init__(self, data):
+        self.x32 = as_rows(data)
+        self.x64 = self.x32.astype(np.float64)
+        self.sq_norms = row_norms(self.x32)
+
+    @property
+    def n(self) -> int:
+        return self.x32.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self.x32.shape[1]
+
+
+def naive_kde(data: Data, family: str, h: float, queries) -> np.ndarray:
+    """estimators.py:122-149 (L2 via blocked batch_sqdist, L1 via per-query row blocks)."""
+    q = np.atleast_2d(np.asarray(queries, dtype=np.float64))
+    if q.shape[1] != data.d:
+        raise ValueError(f"dimension mismatch: queries d={q.shape[1]}, dataset d={data.d}")
+    n = data.n
+    values = np.empty(q.shape[0], dtype=np.float64)
+    if family == "laplacian":
+        step = max(1, BLOCK_ENTRIES // data.d)
+        for j, y in enumerate(q):
+            acc = 0.0
+            for lo in range(0, n, step):
+                dist = np.abs(data.x64[lo: lo + step] - y).sum(axis=1)
+                acc += float(kernel_from_distance(family, h, dist).sum())
+            values[j] = acc / n
+        return values
+    block = max(1, BLOCK_ENTRIES // n)
+    for lo in range(0, q.shape[0], block):
+        hi = min(q.shape[0], lo + block)
+        d2 = batch_sqdist(q[lo:hi], data.x64, data.sq_norms)
+        values[lo:hi] = kernel_from_sql2(family, h, d2).mean(axis=1)
+    return values
+
+
+def rs_kde(data: Data, family: str, h: float, query, m: int, rng) -> float:
+    """estimators.py:152-164 (rng: anything with .integers(low, high, size))."""
+    if m < 1:
+        raise ValueError(f"m={m} must be >= 1")
+    y = np.asarray(query, dtype=np.float64).ravel()
+    draws = rng.integers(0, data.n, size=m)
+    return float(kernel_rows(data.x64, data.sq_norms, family, h, draws, y).mean())
+
+
+def rs_excluding(data: Data, family: str, h: float, y: np.ndarray, m: int, rng, exclude, n_excluded: int):
+    """estimators.py:203-233: first-m-accepted rejection sampling restricted to X \\ X1."""
+    n = data.n
+    total = 0.0
+    accepted = 0
+    while accepted < m:
+        need = m - accepted
+        if n_excluded == 0:
+            batch = need
+        else:
+            batch = min(math.ceil(need * n / (n - n_excluded)) + 8, max(4 * need, 65536))
+        draws = rng.integers(0, n, size=batch)
+        if n_excluded:
+            draws = draws[~exclude[draws]]
+        draws = draws[:need]
+        if len(draws) == 0:
+            continue
+        total += float(kernel_rows(data.x64, data.sq_norms, family, h, draws, y).sum())
+        accepted += len(draws)
+    return total / m, m
+
+
+def smallest_k(d2: np.ndarray, ids: np.ndarray, k: int):
+    """ann.py:82-102: k smallest, boundary widening, stable argsort, lexsort on ties."""
+    k = min(k, len(d2))
+    if k < len(d2):
+        part = np.argpartition(d2, k - 1)[:k]
+        boundary = d2[part].max()
+        cand = np.flatnonzero(d2 <= boundary)
+        cd = d2[cand]
+    else:
+        cand = np.arange(len(d2))
+        cd = d2
+    order = np.argsort(cd, kind="stable")
+    if len(order) > 1 and np.any(np.diff(cd[order]) == 0.0):
+        order = np.lexsort((ids[cand], cd))
+    sel = cand[order[:k]]
+    return ids[sel], d2[sel]
+
+
+def brute_force_knn(data: Data, query, k: int):
+    """ann.py:105-111 -> (indices int64, sq_distances fp64)."""
+    if not 1 <= k <= data.n:
+        raise ValueError(f"k={k} out of range [1, {data.n}]")
+    d2 = batch_sqdist(np.asarray(query, dtype=np.float64).reshape(1, -1), data.x64, data.sq_norms)[0]
+    return smallest_k(d2, np.arange(data.n, dtype=np.int64), k)
+
+
+def deann(data: Data, family: str, h: float, neighbors, query, k: int, m: int, rng=None):
+    """estimators.py:306-379 with the uniform sampler.
+
+    `neighbors` is a callable (y, k) -> (indices, sq_distances) (the AnnIndex
+    black box, e.g. brute_force_knn or a replay of GPU neighbours).
+    Returns (value, kernel_evals, k_hat, samples_used, truncated).
+    """
+    n = data.n
+    if not 0 <= k <= n:
+        raise ValueError(f"k={k} out of range [0, {n}]")
+    if m < 0:
+        raise ValueError(f"m={m} must be >= 0")
+    if m > 0 and k >= n:
+        raise ValueError("m > 0 requires k + 1 <= n so the remainder is nonempty")
+    if m > 0 and rng is None:
+        raise ValueError("give exactly one of rng= or rsp_state= when m > 0")
+    y = np.asarray(query, dtype=np.float64).ravel()
+    if y.shape[0] != data.d:
+        raise ValueError(f"dimension mismatch: query d={y.shape[0]}, dataset d={data.d}")
+    if k > 0:
+        idx, sqd = neighbors(y, k)
+        x1 = np.asarray(idx, dtype=np.int64)
+    else:
+        x1, sqd = np.empty(0, dtype=np.int64), None
+    k_hat = len(x1)
+    if k_hat == 0:
+        z1 = 0.0
+    elif family == "laplacian":
+        z1 = float(kernel_rows(data.x64, data.sq_norms, family, h, x1, y).mean())
+    else:
+        z1 = float(kernel_from_sql2(family, h, np.asarray(sqd, dtype=np.float64)).mean())
+    if m == 0:
+        return (k_hat / n) * z1, k_hat, k_hat, 0, k_hat < n
+    if k_hat:
+        exclude = np.zeros(n, dtype=bool)
+        exclude[x1] = True
+    else:
+        exclude = None
+    z2, used = rs_excluding(data, family, h, y, m, rng, exclude, k_hat)
+    value = (k_hat / n) * z1 + ((n - k_hat) / n) * z2
+    return value, k_hat + used, k_hat, used, False
+
+
+def deann_batch(data: Data, family: str, h: float, neighbors, queries, k: int, m: int, rng=None):
+    """estimators.py:382-410 (uniform sampler): a loop of deann in query order."""
+    q = np.atleast_2d(np.asarray(queries, dtype=np.float64))
+    return [deann(data, family, h, neighbors, q[j], k, m, rng=rng)[0] for j in range(q.shape[0])]

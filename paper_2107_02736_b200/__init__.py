@@ -1,0 +1,36 @@
+"""B200-native KDE query path of DEANN (arXiv 2107.02736).
+
+Drop-in for the estimator API of the reference package ``deann``
+(/root/reference/pkg/src/deann/__init__.py:8-43, hot-path subset):
+``Dataset``, ``KernelFamily``/``KernelSpec``, ``naive_kde``, ``rs_kde``,
+``deann``, ``deann_batch``, ``Estimate``/``BatchKde``, ``NeighborList``,
+``AnnIndex``/``BruteForceIndex`` (GPU brute force) and ``brute_force_knn``.
+All arithmetic runs in hand-written sm_100a kernels behind the C-ABI in
+``include/deann_b200.h``; see DESIGN.md.
+"""
+
+from .ann import AnnIndex, BruteForceIndex, GpuBruteForceIndex, NeighborList, brute_force_knn, knn_batch
+from .bandwidth import fit_bandwidth, NoBandwidthError
+from .data import Dataset, as_gpu_dataset
+from .estimators import (
+    BatchKde,
+    Estimate,
+    deann,
+    deann_arrays,
+    deann_batch,
+    kernel_from_distance,
+    naive_kde,
+    naive_kde_into,
+    rs_kde,
+)
+from .kernels import KernelFamily, KernelSpec
+from .sampler import PhiloxSampler
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AnnIndex", "BruteForceIndex", "GpuBruteForceIndex", "NeighborList", "brute_force_knn", "knn_batch",
+    "fit_bandwidth", "NoBandwidthError", "Dataset", "as_gpu_dataset", "BatchKde", "Estimate", "deann",
+    "deann_arrays", "deann_batch", "kernel_from_distance", "naive_kde", "naive_kde_into", "rs_kde",
+    "KernelFamily", "KernelSpec", "PhiloxSampler",
+]

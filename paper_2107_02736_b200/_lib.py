@@ -1,0 +1,135 @@
+"""ctypes binding of the C-ABI library ``libdeann_b200.so`` (include/deann_b200.h).
+
+The product path has no CPU fallback: if the library is missing or no sm_100
+device is present, every estimator raises.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``make`` in
+``paper_2107_02736_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdeann_b200.so")
+
+DK_OK, DK_EINVAL, DK_ECUDA, DK_ENOMEM, DK_EINEXACT, DK_ENODEV = range(6)
+DK_GAUSSIAN, DK_EXPONENTIAL, DK_LAPLACIAN = 0, 1, 2
+DK_PREC_AUTO, DK_PREC_SPLIT3, DK_PREC_FP16 = 0, 1, 2
+DK_OUT_SUM = 1
+
+# every symbol include/deann_b200.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "dk_version", "dk_last_error", "dk_device_ok", "dk_fit", "dk_free", "dk_info", "dk_sq_norms",
+    "dk_naive", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
+    "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count",
+)
+
+
+class DeannGpuError(RuntimeError):
+    """A CUDA / device failure reported by the C-ABI (status DK_ECUDA / DK_ENODEV)."""
+
+
+class FitOpts(ctypes.Structure):
+    _fields_ = [
+        ("device", ctypes.c_int32),
+        ("precision", ctypes.c_int32),
+        ("global_offset", ctypes.c_int64),
+        ("global_n", ctypes.c_int64),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u32 = ctypes.c_uint32
+_u64 = ctypes.c_uint64
+_f64 = ctypes.c_double
+
+
+def _declare(lib):
+    sig = {
+        "dk_version": (_i32, []),
+        "dk_last_error": (ctypes.c_char_p, []),
+        "dk_device_ok": (_i32, [_i32]),
+        "dk_fit": (_i32, [_vp, _i64, _i32, ctypes.POINTER(FitOpts), ctypes.POINTER(_vp)]),
+        "dk_free": (_i32, [_vp]),
+        "dk_info": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),
+                            ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
+        "dk_sq_norms": (_i32, [_vp, _vp, _vp]),
+        "dk_naive": (_i32, [_vp, _vp, _i64, _i32, _f64, _u32, _vp, _vp]),
+        "dk_knn": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp]),
+        "dk_merge_topk": (_i32, [_i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+        "dk_sample": (_i32, [_vp, _vp, _i64, _i32, _f64, _i32, _u64, _i64, _vp, _vp, _i32, _vp, _vp, _vp, _vp]),
+        "dk_eval_rows": (_i32, [_vp, _vp, _i64, _i32, _f64, _vp, _vp, _i32, _vp, _vp]),
+        "dk_kernel_values": (_i32, [_i32, _f64, _vp, _i64, _vp, _vp]),
+        "dk_deann": (_i32, [_vp, _vp, _i64, _i32, _f64, _i32, _i32, _u64, _i64, _vp, _vp, _vp, _vp, _vp]),
+        "dk_last_kernel_ms": (_i32, [_vp, ctypes.POINTER(_f64), ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
+        "dk_set_profiling": (_i32, [_vp, _i32]),
+        "dk_last_launch_count": (_i32, [_vp, ctypes.POINTER(_i64)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def load():
+    """Load the C-ABI library (raises ImportError when it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} not found: the CUDA extension is not built "
+                    "(run `make -C paper_2107_02736_b200/csrc` or __graft_entry__.build())"
+                )
+            _lib = _declare(ctypes.CDLL(LIB_PATH))
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == DK_OK:
+        return
+    msg = load().dk_last_error().decode(errors="replace")
+    if status == DK_EINVAL:
+        raise ValueError(msg)
+    if status == DK_ENOMEM:
+        raise MemoryError(msg)
+    raise DeannGpuError(f"[status {status}] {msg}")
+
+
+def ptr(obj) -> int | None:
+    """Raw address of a numpy array or torch tensor (None passes through)."""
+    if obj is None:
+        return None
+    if isinstance(obj, np.ndarray):
+        return obj.ctypes.data
+    if hasattr(obj, "data_ptr"):
+        return obj.data_ptr()
+    raise TypeError(f"cannot take the address of {type(obj)!r}")
+
+
+def current_stream():
+    """cudaStream_t of torch's current stream when torch is loaded, else the default stream."""
+    import sys
+
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+        return torch.cuda.current_stream().cuda_stream
+    return None
+
+
+def family_code(family) -> int:
+    v = getattr(family, "value", family)
+    return {"gaussian": DK_GAUSSIAN, "exponential": DK_EXPONENTIAL, "laplacian": DK_LAPLACIAN}[str(v)]

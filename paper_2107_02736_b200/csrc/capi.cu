@@ -1,0 +1,857 @@
+// capi.cu — the extern "C" boundary (include/deann_b200.h).
+//
+// Host orchestration of the device kernels: argument validation with the
+// reference's preconditions, host<->device staging, per-handle workspace,
+// operand-encoding choice, k-NN batching/certificates and profiling events.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <limits>
+#include <memory>
+#include <mutex>
+
+#include "internal.h"
+#include "tile_kernel.cuh"
+
+namespace dk {
+
+std::atomic<long long> g_launches{0};
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+void Workspace::reserve(size_t bytes) {
+  off = 0;
+  if (bytes <= cap) return;
+  if (base) {
+    DK_CUDA(cudaDeviceSynchronize());
+    DK_CUDA(cudaFree(base));
+    base = nullptr;
+    cap = 0;
+  }
+  const size_t want = std::max(bytes + bytes / 4, size_t(64) << 20);
+  DK_CUDA(cudaMalloc(&base, want));
+  cap = want;
+}
+Workspace::~Workspace() {
+  if (base) cudaFree(base);
+}
+
+namespace {
+
+struct Plan {
+  size_t off = 0;
+  template <class T>
+  size_t add(size_t count) {
+    const size_t a = (off + 255) & ~size_t(255);
+    off = a + std::max<size_t>(count, 1) * sizeof(T);
+    return a;
+  }
+};
+template <class T>
+T* at(Workspace& ws, size_t o) {
+  return reinterpret_cast<T*>(ws.base + o);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <class F>
+dk_status guard(F&& f) {
+  try {
+    f();
+    return DK_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return DK_ENOMEM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return DK_ECUDA;
+  }
+}
+
+constexpr int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+void check_family_bw(int32_t family, double bw) {
+  DK_REQUIRE(family == DK_GAUSSIAN || family == DK_EXPONENTIAL || family == DK_LAPLACIAN,
+             "unknown kernel family " + std::to_string(family));
+  DK_REQUIRE(std::isfinite(bw) && bw > 0.0, "bandwidth must be positive and finite, got " + std::to_string(bw));
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) DK_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// ------------------------------------------------------------------ encodings
+Encoding& enc_slot(dk_dataset* h, int mode) {
+  return mode == 0 ? h->enc_exact : (mode == 1 ? h->enc_split : h->enc_fp16);
+}
+
+void ensure_mu(dk_dataset* h, cudaStream_t s) {
+  if (h->mu) return;
+  DK_CUDA(cudaMalloc(&h->mu, size_t(h->d) * sizeof(double)));
+  const int32_t row_blocks = int32_t(std::min<int64_t>(1024, h->n));
+  double* partial = nullptr;
+  DK_CUDA(cudaMalloc(&partial, size_t(row_blocks) * h->d * sizeof(double)));
+  launch_column_mean(h->X, h->n, h->d, partial, row_blocks, h->mu, s);
+  DK_CUDA(cudaStreamSynchronize(s));
+  DK_CUDA(cudaFree(partial));
+}
+
+const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
+  Encoding& e = enc_slot(h, mode);
+  if (e.mode == mode) return e;
+  const int32_t d = h->d;
+  e.Kp = int32_t(round_up(mode == 1 ? 3 * int64_t(d) : d, kBK));
+  if (mode != 0) ensure_mu(h, s);
+  e.mu = mode == 0 ? nullptr : h->mu;
+  DK_CUDA(cudaMalloc(&e.B, size_t(h->n_pad) * e.Kp * sizeof(__half)));
+  DK_CUDA(cudaMalloc(&e.xn, size_t(h->n_pad) * sizeof(float)));
+  DK_CUDA(cudaMalloc(&e.sx, 2 * sizeof(float)));
+  uint32_t* maxabs = reinterpret_cast<uint32_t*>(e.sx + 1);
+  launch_encode_rows(h->X, h->n, h->n_pad, d, mode, e.mu, e.Kp, e.B, e.xn, e.sx, maxabs, s);
+  std::vector<float> xn(static_cast<size_t>(h->n));
+  DK_CUDA(cudaMemcpyAsync(xn.data(), e.xn, xn.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
+  DK_CUDA(cudaStreamSynchronize(s));
+  float mx = 0.f;
+  for (float v : xn) mx = std::max(mx, v);
+  e.xn_max = mx;
+  const double u = std::ldexp(1.0, -24);
+  if (mode == 0) e.eps_rel = 0.f;                                           // bit-exact integers
+  else if (mode == 1) e.eps_rel = float(8 * u + double(e.Kp) * u + 6 * u);  // hi/lo split + fp32 sums
+  else e.eps_rel = float(std::ldexp(1.0, -9) + double(e.Kp) * u);           // single fp16 pass
+  e.tmap = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN));
+  e.mode = mode;
+  return e;
+}
+
+void free_encoding(Encoding& e) {
+  if (e.B) cudaFree(e.B);
+  if (e.xn) cudaFree(e.xn);
+  if (e.sx) cudaFree(e.sx);
+  e = Encoding{};
+}
+
+// ------------------------------------------------------------------ query staging
+struct Staged {
+  const double* Q = nullptr;  // device fp64 queries
+};
+
+const double* stage_queries(dk_dataset* h, const double* Q, int64_t nq, size_t off, cudaStream_t s) {
+  if (is_device_ptr(Q)) return Q;
+  double* dst = at<double>(h->ws, off);
+  DK_CUDA(cudaMemcpyAsync(dst, Q, size_t(nq) * h->d * sizeof(double), cudaMemcpyHostToDevice, s));
+  return dst;
+}
+
+// choose the encoding for this query batch (may synchronise for the integrality check)
+int choose_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cudaStream_t s) {
+  if (h->precision == DK_PREC_SPLIT3) return 1;
+  if (h->precision == DK_PREC_FP16) return 2;
+  if (!h->int_exact) return 1;
+  DK_CUDA(cudaMemsetAsync(flags, 0, sizeof(uint32_t), s));
+  launch_query_check(Qd, nq, h->d, flags, s);
+  uint32_t f = 0;
+  DK_CUDA(cudaMemcpyAsync(&f, flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  DK_CUDA(cudaStreamSynchronize(s));
+  DK_REQUIRE(!(f & 1u), "queries must be finite");
+  return (f & 6u) ? 1 : 0;
+}
+
+QueryOperand encode_queries(dk_dataset* h, const Encoding& e, const double* Qd, int64_t nq, int32_t nq_pad,
+                            __half* A, float* qn, float* scal, cudaStream_t s) {
+  QueryOperand q;
+  q.nq = int32_t(nq);
+  q.nq_pad = nq_pad;
+  q.A = A;
+  q.qn = qn;
+  q.m2s = scal;
+  launch_encode_queries(Qd, nq, nq_pad, h->d, e.mode, e.mu, e.Kp, e.sx, A, qn, scal,
+                        reinterpret_cast<uint32_t*>(scal + 1), s);
+  q.tmap = make_tmap_2d_f16(A, uint64_t(nq_pad), uint64_t(e.Kp), uint32_t(kBM));
+  return q;
+}
+
+void copy_out(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (dst == src || bytes == 0) return;
+  DK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+}
+
+struct ProfScope {
+  dk_dataset* h;
+  cudaStream_t s;
+  cudaEvent_t e1 = nullptr;
+  ProfScope(dk_dataset* hh, cudaStream_t ss, double flops, double bytes) : h(hh), s(ss) {
+    if (!h->profiling) return;
+    if (h->prof_used == h->prof_events.size()) {
+      cudaEvent_t a, b;
+      DK_CUDA(cudaEventCreate(&a));
+      DK_CUDA(cudaEventCreate(&b));
+      h->prof_events.emplace_back(a, b);
+    }
+    auto& pr = h->prof_events[h->prof_used++];
+    DK_CUDA(cudaEventRecord(pr.first, s));
+    e1 = pr.second;
+    h->last_flops = flops;
+    h->last_bytes = bytes;
+  }
+  ~ProfScope() {
+    if (e1) cudaEventRecord(e1, s);
+  }
+};
+
+struct LaunchCount {
+  dk_dataset* h;
+  long long start;
+  explicit LaunchCount(dk_dataset* hh) : h(hh), start(g_launches.load()) {}
+  ~LaunchCount() { h->launches = g_launches.load() - start; }
+};
+
+// ------------------------------------------------------------------ k-NN core
+struct KnnPlan {
+  int32_t kprime = 0, stride = 1, nseg = 0, cap = 0, batch = 0;
+  bool tau_inf = false;
+};
+
+KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
+  KnnPlan p;
+  p.kprime = int32_t(std::min<int64_t>(h->n, int64_t(k) + std::max<int32_t>(32, k / 4)));
+  const int64_t ntiles = h->n_pad / kBN;
+  if (h->n <= 4096 || 2 * ntiles < p.kprime) {
+    p.tau_inf = true;
+    p.cap = int32_t(h->n);
+    p.stride = 1;
+    p.nseg = 0;
+  } else {
+    const int64_t target = std::clamp<int64_t>(16 * int64_t(p.kprime), 2048, 8192);
+    p.stride = int32_t(std::max<int64_t>(1, (2 * ntiles + target - 1) / target));
+    while (p.stride > 1 && 2 * ((ntiles + p.stride - 1) / p.stride) < 4 * p.kprime) --p.stride;
+    p.nseg = int32_t(2 * ((ntiles + p.stride - 1) / p.stride));
+    int64_t cap = 2048;
+    while (cap < 3 * int64_t(p.stride) * p.kprime && cap < 16384) cap <<= 1;
+    p.cap = int32_t(cap);
+  }
+  const int64_t budget = int64_t(1) << 31;  // bytes of candidate storage per batch
+  int64_t b = budget / (int64_t(p.cap) * 8 + int64_t(p.nseg) * 4 + 64);
+  b = std::max<int64_t>(kBM, std::min<int64_t>(16384, b)) / kBM * kBM;
+  p.batch = int32_t(std::min<int64_t>(b, round_up(nq, kBM)));
+  return p;
+}
+
+// k-NN for nq queries already on the device; idx/d2 outputs on the device.
+void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t* idx_d, double* d2_d,
+                cudaStream_t s, size_t ws_off_base) {
+  const KnnPlan kp = plan_knn(h, k, nq);
+  // encoding: decided once for the whole query set
+  Plan pl;
+  pl.off = ws_off_base;
+  const size_t o_flags = pl.add<uint32_t>(4);
+  uint32_t* flags = at<uint32_t>(h->ws, o_flags);
+  const int mode = choose_mode(h, Qd, nq, flags, s);
+  const Encoding& e = ensure_encoding(h, mode, s);
+  const int32_t bpad = kp.batch;
+  const size_t o_A = pl.add<__half>(size_t(bpad) * e.Kp);
+  const size_t o_qn = pl.add<float>(bpad);
+  const size_t o_scal = pl.add<float>(4);
+  const size_t o_tmin = pl.add<float>(size_t(std::max(kp.nseg, 1)) * bpad);
+  const size_t o_tau = pl.add<float>(bpad);
+  const size_t o_cnt = pl.add<uint32_t>(bpad);
+  const size_t o_cand = pl.add<unsigned long long>(size_t(kp.cap) * bpad);
+  const size_t o_status = pl.add<int32_t>(bpad);
+  const size_t o_ovf = pl.add<int32_t>(bpad + 1);
+  const size_t o_Qc = pl.add<double>(size_t(bpad) * h->d);
+  const size_t o_A2 = pl.add<__half>(size_t(bpad) * e.Kp);
+  const size_t o_qn2 = pl.add<float>(bpad);
+  const size_t o_tau2 = pl.add<float>(bpad);
+  const size_t o_scal2 = pl.add<float>(4);
+  if (pl.off > h->ws.cap) throw Error{DK_ECUDA, "internal: k-NN workspace under-reserved"};
+  const float inf = std::numeric_limits<float>::infinity();
+  for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
+    const int64_t bn = std::min<int64_t>(bpad, nq - b0);
+    const int32_t bn_pad = int32_t(round_up(bn, kBM));
+    const double* Qb = Qd + b0 * h->d;
+    QueryOperand q = encode_queries(h, e, Qb, bn, bn_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
+                                    at<float>(h->ws, o_scal), s);
+    float* tau = at<float>(h->ws, o_tau);
+    uint32_t* cnt = at<uint32_t>(h->ws, o_cnt);
+    unsigned long long* cand = at<unsigned long long>(h->ws, o_cand);
+    if (kp.tau_inf) {
+      launch_fill_float(tau, bn, inf, s);
+    } else {
+      SweepArgs a{};
+      a.mode = MODE_TILEMIN;
+      a.qop = &q;
+      a.enc = &e;
+      a.n = h->n;
+      a.n_pad = h->n_pad;
+      a.tile_stride = kp.stride;
+      a.tmin = at<float>(h->ws, o_tmin);
+      launch_sweep(a, h->num_sms, s);
+      launch_tau_from_tmin(a.tmin, kp.nseg, bn_pad, bn, kp.kprime, tau, s);
+    }
+    launch_fill_float(tau + bn, bn_pad - bn, -inf, s);
+    DK_CUDA(cudaMemsetAsync(cnt, 0, size_t(bn_pad) * sizeof(uint32_t), s));
+    {
+      SweepArgs a{};
+      a.mode = MODE_FILTER;
+      a.qop = &q;
+      a.enc = &e;
+      a.n = h->n;
+      a.n_pad = h->n_pad;
+      a.tile_stride = 1;
+      a.tau = tau;
+      a.cand_cnt = cnt;
+      a.cand = cand;
+      a.cap = kp.cap;
+      ProfScope ps(h, s, 2.0 * double(h->d) * double(bn) * double(h->n), double(h->n_pad) * e.Kp * 2);
+      launch_sweep(a, h->num_sms, s);
+    }
+    // overflow: tighten tau on the stored candidates and sweep those queries again
+    int32_t* ovf = at<int32_t>(h->ws, o_ovf);
+    for (int iter = 0;; ++iter) {
+      DK_CUDA(cudaMemsetAsync(ovf + bpad, 0, sizeof(int32_t), s));
+      launch_tau_from_cand(cand, cnt, kp.cap, bn, kp.kprime, tau, ovf, ovf + bpad, s);
+      int32_t novf = 0;
+      DK_CUDA(cudaMemcpyAsync(&novf, ovf + bpad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaStreamSynchronize(s));
+      if (novf == 0) break;
+      if (iter >= 8) throw Error{DK_EINEXACT, "k-NN candidate overflow did not converge"};
+      std::vector<int32_t> list(static_cast<size_t>(novf));
+      DK_CUDA(cudaMemcpy(list.data(), ovf, size_t(novf) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      std::sort(list.begin(), list.end());
+      DK_CUDA(cudaMemcpyAsync(ovf, list.data(), size_t(novf) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      // compact the overflowing queries (+ their tightened tau), reset their counters
+      double* Qc = at<double>(h->ws, o_Qc);
+      float* tau2 = at<float>(h->ws, o_tau2);
+      std::vector<float> tau_h(static_cast<size_t>(bn));
+      DK_CUDA(cudaMemcpyAsync(tau_h.data(), tau, size_t(bn) * sizeof(float), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaStreamSynchronize(s));
+      const int32_t nc_pad = int32_t(round_up(novf, kBM));
+      std::vector<float> tau2_h(size_t(nc_pad), -inf);
+      for (int32_t i = 0; i < novf; ++i) {
+        DK_CUDA(cudaMemcpyAsync(Qc + size_t(i) * h->d, Qb + size_t(list[i]) * h->d, size_t(h->d) * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+        tau2_h[i] = tau_h[list[i]];
+        DK_CUDA(cudaMemsetAsync(cnt + list[i], 0, sizeof(uint32_t), s));
+      }
+      DK_CUDA(cudaMemcpyAsync(tau2, tau2_h.data(), size_t(nc_pad) * sizeof(float), cudaMemcpyHostToDevice, s));
+      QueryOperand qc = encode_queries(h, e, Qc, novf, nc_pad, at<__half>(h->ws, o_A2), at<float>(h->ws, o_qn2),
+                                       at<float>(h->ws, o_scal2), s);
+      SweepArgs a{};
+      a.mode = MODE_FILTER;
+      a.qop = &qc;
+      a.enc = &e;
+      a.n = h->n;
+      a.n_pad = h->n_pad;
+      a.tile_stride = 1;
+      a.tau = tau2;
+      a.cand_cnt = cnt;
+      a.cand = cand;
+      a.cap = kp.cap;
+      a.row_map = ovf;
+      launch_sweep(a, h->num_sms, s);
+      DK_CUDA(cudaStreamSynchronize(s));
+    }
+    int32_t* status = at<int32_t>(h->ws, o_status);
+    launch_select_rerank(h->X, h->global_offset, h->d, Qb, bn, k, kp.kprime, cand, cnt, kp.cap, tau, q.qn, e.xn_max,
+                         e.eps_rel, idx_d + b0 * k, d2_d + b0 * k, status, s);
+    std::vector<int32_t> st(static_cast<size_t>(bn));
+    DK_CUDA(cudaMemcpyAsync(st.data(), status, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    DK_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> fail;
+    for (int64_t i = 0; i < bn; ++i)
+      if (st[size_t(i)]) fail.push_back(int32_t(i));
+    if (!fail.empty()) {
+      DK_CUDA(cudaMemcpyAsync(ovf, fail.data(), fail.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, ovf, int32_t(fail.size()), k, idx_d + b0 * k,
+                                d2_d + b0 * k, s);
+      DK_CUDA(cudaStreamSynchronize(s));
+    }
+  }
+}
+
+size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
+  const KnnPlan kp = plan_knn(h, k, nq);
+  const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
+  Plan pl;
+  pl.add<uint32_t>(4);
+  pl.add<__half>(size_t(kp.batch) * Kp_max);
+  pl.add<float>(kp.batch);
+  pl.add<float>(4);
+  pl.add<float>(size_t(std::max(kp.nseg, 1)) * kp.batch);
+  pl.add<float>(kp.batch);
+  pl.add<uint32_t>(kp.batch);
+  pl.add<unsigned long long>(size_t(kp.cap) * kp.batch);
+  pl.add<int32_t>(kp.batch);
+  pl.add<int32_t>(kp.batch + 1);
+  pl.add<double>(size_t(kp.batch) * h->d);
+  pl.add<__half>(size_t(kp.batch) * Kp_max);
+  pl.add<float>(kp.batch);
+  pl.add<float>(kp.batch);
+  pl.add<float>(4);
+  return pl.off + 4096;
+}
+
+}  // namespace
+}  // namespace dk
+
+using namespace dk;
+
+extern "C" {
+
+int32_t dk_version(void) { return 10000; }
+
+const char* dk_last_error(void) { return g_err.c_str(); }
+
+int32_t dk_device_ok(int32_t device) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return prop.major == 10 ? 1 : 0;
+}
+
+dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts, dk_handle* out) {
+  return guard([&] {
+    DK_REQUIRE(out != nullptr, "out handle pointer is NULL");
+    *out = nullptr;
+    DK_REQUIRE(n >= 1 && d >= 1, "dataset must have n >= 1 and d >= 1, got " + std::to_string(n) + " x " +
+                                     std::to_string(d));
+    DK_REQUIRE(X != nullptr, "dataset pointer is NULL");
+    const int device = opts ? opts->device : 0;
+    int ndev = 0;
+    DK_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Error{DK_ENODEV, "no CUDA device " + std::to_string(device)};
+    cudaDeviceProp prop;
+    DK_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw Error{DK_ENODEV, std::string("device is not sm_100 (B200): ") + prop.name};
+    DeviceGuard g(device);
+    auto h = std::make_unique<dk_dataset>();
+    h->device = device;
+    h->num_sms = prop.multiProcessorCount;
+    h->n = n;
+    h->d = d;
+    h->n_pad = round_up(n, kBN);
+    h->global_offset = opts ? opts->global_offset : 0;
+    h->global_n = (opts && opts->global_n > 0) ? opts->global_n : n;
+    h->precision = opts ? opts->precision : DK_PREC_AUTO;
+    DK_REQUIRE(h->precision >= 0 && h->precision <= 2, "unknown precision mode");
+    DK_REQUIRE(h->global_offset >= 0 && h->global_offset + n <= h->global_n, "shard outside [0, global_n)");
+    cudaStream_t s = nullptr;
+    DK_CUDA(cudaMalloc(&h->X, size_t(n) * d * sizeof(float)));
+    DK_CUDA(cudaMemcpy(h->X, X, size_t(n) * d * sizeof(float), cudaMemcpyDefault));
+    DK_CUDA(cudaMalloc(&h->xn64, size_t(n) * sizeof(double)));
+    uint32_t* flags_d = nullptr;
+    DK_CUDA(cudaMalloc(&flags_d, sizeof(uint32_t)));
+    DK_CUDA(cudaMemset(flags_d, 0, sizeof(uint32_t)));
+    launch_row_stats(h->X, n, d, h->xn64, flags_d, s);
+    uint32_t flags = 0;
+    DK_CUDA(cudaMemcpy(&flags, flags_d, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    cudaFree(flags_d);
+    DK_REQUIRE(!(flags & 1u), "dataset entries must be finite");
+    h->int_exact = (flags & 6u) == 0;
+    if (h->precision == DK_PREC_AUTO) ensure_encoding(h.get(), h->int_exact ? 0 : 1, s);
+    else if (h->precision == DK_PREC_SPLIT3) ensure_encoding(h.get(), 1, s);
+    else ensure_encoding(h.get(), 2, s);
+    DK_CUDA(cudaDeviceSynchronize());
+    *out = h.release();
+  });
+}
+
+dk_status dk_free(dk_handle h) {
+  return guard([&] {
+    if (!h) return;
+    DeviceGuard g(h->device);
+    cudaDeviceSynchronize();
+    free_encoding(h->enc_exact);
+    free_encoding(h->enc_split);
+    free_encoding(h->enc_fp16);
+    if (h->X) cudaFree(h->X);
+    if (h->xn64) cudaFree(h->xn64);
+    if (h->mu) cudaFree(h->mu);
+    for (auto& pr : h->prof_events) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    delete h;
+  });
+}
+
+dk_status dk_info(dk_handle h, int64_t* n, int32_t* d, int64_t* go, int64_t* gn, int32_t* exact) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    if (n) *n = h->n;
+    if (d) *d = h->d;
+    if (go) *go = h->global_offset;
+    if (gn) *gn = h->global_n;
+    if (exact) *exact = h->int_exact ? 1 : 0;
+  });
+}
+
+dk_status dk_sq_norms(dk_handle h, double* out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr && out != nullptr, "NULL argument");
+    DeviceGuard g(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DK_CUDA(cudaMemcpyAsync(out, h->xn64, size_t(h->n) * sizeof(double), cudaMemcpyDefault, s));
+    if (!is_device_ptr(out)) DK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth, uint32_t flags,
+                   double* out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    check_family_bw(family, bandwidth);
+    DK_REQUIRE(nq >= 0, "negative query count");
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && out != nullptr, "NULL query or output pointer");
+    DeviceGuard g(h->device);
+    LaunchCount lc(h);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool out_dev = is_device_ptr(out);
+    const double scale = (flags & DK_OUT_SUM) ? 1.0 : 1.0 / double(h->n);
+    Plan pl;
+    const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
+    const size_t o_out = pl.add<double>(size_t(nq));
+    const size_t o_flags = pl.add<uint32_t>(4);
+    if (family == DK_LAPLACIAN) {
+      const size_t o_part = pl.add<double>(l1_part_count(h->n, int32_t(nq)));
+      h->ws.reserve(pl.off);
+      const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+      int32_t nparts = 0;
+      double* part = at<double>(h->ws, o_part);
+      double* od = out_dev ? out : at<double>(h->ws, o_out);
+      {
+        ProfScope ps(h, s, 3.0 * double(h->d) * double(nq) * double(h->n), double(h->n) * h->d * 4);
+        launch_l1_kde(h->X, h->n, h->d, Qd, nq, 1.0 / bandwidth, part, &nparts, nullptr, s);
+      }
+      launch_reduce_partials(part, nparts, int32_t((nq + 63) / 64 * 64), nq, scale, od, s);
+      if (!out_dev) {
+        copy_out(out, od, size_t(nq) * sizeof(double), s);
+        DK_CUDA(cudaStreamSynchronize(s));
+      }
+      return;
+    }
+    const int32_t nq_pad = int32_t(round_up(nq, kBM));
+    const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
+    const size_t o_A = pl.add<__half>(size_t(nq_pad) * Kp_max);
+    const size_t o_qn = pl.add<float>(nq_pad);
+    const size_t o_scal = pl.add<float>(4);
+    const size_t o_part = pl.add<double>(sweep_part_count(h->n_pad, nq_pad, h->num_sms));
+    h->ws.reserve(pl.off);
+    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+    const int mode = choose_mode(h, Qd, nq, at<uint32_t>(h->ws, o_flags), s);
+    const Encoding& e = ensure_encoding(h, mode, s);
+    QueryOperand q = encode_queries(h, e, Qd, nq, nq_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
+                                    at<float>(h->ws, o_scal), s);
+    SweepArgs a{};
+    a.mode = family == DK_GAUSSIAN ? MODE_KDE_GAUSS : MODE_KDE_EXP;
+    a.qop = &q;
+    a.enc = &e;
+    a.n = h->n;
+    a.n_pad = h->n_pad;
+    a.tile_stride = 1;
+    const double log2e = 1.4426950408889634;
+    a.negc = float(family == DK_GAUSSIAN ? -log2e / (2.0 * bandwidth * bandwidth) : -log2e / bandwidth);
+    a.part = at<double>(h->ws, o_part);
+    int32_t ncc = 0;
+    a.ncc_out = &ncc;
+    {
+      ProfScope ps(h, s, 2.0 * double(h->d) * double(nq) * double(h->n), double(h->n_pad) * e.Kp * 2);
+      launch_sweep(a, h->num_sms, s);
+    }
+    double* od = out_dev ? out : at<double>(h->ws, o_out);
+    launch_reduce_partials(a.part, ncc * 2, nq_pad, nq, scale, od, s);
+    if (!out_dev) {
+      copy_out(out, od, size_t(nq) * sizeof(double), s);
+      DK_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+dk_status dk_knn(dk_handle h, const double* Q, int64_t nq, int32_t k, int64_t* idx_out, double* d2_out,
+                 void* stream) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    DK_REQUIRE(k >= 1 && int64_t(k) <= h->n,
+               "k=" + std::to_string(k) + " out of range [1, " + std::to_string(h->n) + "]");
+    DK_REQUIRE(k <= 4096, "k > 4096 is not supported by the GPU k-NN selection");
+    DK_REQUIRE(nq >= 0, "negative query count");
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && idx_out != nullptr && d2_out != nullptr, "NULL argument");
+    DeviceGuard g(h->device);
+    LaunchCount lc(h);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool idx_dev = is_device_ptr(idx_out), d2_dev = is_device_ptr(d2_out);
+    Plan pl;
+    const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
+    const size_t o_idx = pl.add<int64_t>(size_t(nq) * k);
+    const size_t o_d2 = pl.add<double>(size_t(nq) * k);
+    const size_t base = pl.off;
+    h->ws.reserve(base + knn_ws_bytes(h, k, nq));
+    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+    int64_t* idx_d = idx_dev ? idx_out : at<int64_t>(h->ws, o_idx);
+    double* d2_d = d2_dev ? d2_out : at<double>(h->ws, o_d2);
+    knn_device(h, Qd, nq, k, idx_d, d2_d, s, base);
+    if (!idx_dev) copy_out(idx_out, idx_d, size_t(nq) * k * sizeof(int64_t), s);
+    if (!d2_dev) copy_out(d2_out, d2_d, size_t(nq) * k * sizeof(double), s);
+    if (!idx_dev || !d2_dev) DK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+dk_status dk_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_in, const double* d2_in,
+                        int64_t* idx_out, double* d2_out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(parts >= 1 && parts <= 64 && k >= 1 && nq >= 0, "bad merge arguments");
+    if (nq == 0) return;
+    DK_REQUIRE(is_device_ptr(idx_in) && is_device_ptr(d2_in) && is_device_ptr(idx_out) && is_device_ptr(d2_out),
+               "dk_merge_topk expects device pointers");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    launch_merge_topk(parts, nq, k, idx_in, d2_in, idx_out, d2_out, s);
+  });
+}
+
+dk_status dk_sample(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t m,
+                    uint64_t seed, int64_t query_base, const int64_t* excl, const int32_t* excl_cnt,
+                    int32_t excl_stride, double* z_sum, int64_t* accepted_idx_out, int64_t* draws_out,
+                    void* stream) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    check_family_bw(family, bandwidth);
+    DK_REQUIRE(m >= 1, "m=" + std::to_string(m) + " must be >= 1");
+    DK_REQUIRE(nq >= 0, "negative query count");
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && z_sum != nullptr, "NULL argument");
+    DK_REQUIRE(!excl || excl_stride >= 1, "excl_stride must be >= 1");
+    DeviceGuard g(h->device);
+    LaunchCount lc(h);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Plan pl;
+    const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
+    const size_t o_ex = pl.add<int64_t>(excl ? size_t(nq) * excl_stride : 1);
+    const size_t o_exs = pl.add<int64_t>(excl ? size_t(nq) * excl_stride : 1);
+    const size_t o_cnt = pl.add<int32_t>(excl_cnt ? size_t(nq) : 1);
+    const size_t o_z = pl.add<double>(size_t(nq));
+    const size_t o_acc = pl.add<int64_t>(accepted_idx_out ? size_t(nq) * m : 1);
+    const size_t o_dr = pl.add<int64_t>(size_t(nq));
+    h->ws.reserve(pl.off);
+    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+    const int64_t* ex_sorted = nullptr;
+    const int32_t* cnt_d = nullptr;
+    if (excl) {
+      int64_t* ex_d = at<int64_t>(h->ws, o_ex);
+      DK_CUDA(cudaMemcpyAsync(ex_d, excl, size_t(nq) * excl_stride * sizeof(int64_t), cudaMemcpyDefault, s));
+      if (excl_cnt) {
+        int32_t* c = at<int32_t>(h->ws, o_cnt);
+        DK_CUDA(cudaMemcpyAsync(c, excl_cnt, size_t(nq) * sizeof(int32_t), cudaMemcpyDefault, s));
+        cnt_d = c;
+      }
+      int64_t* srt = at<int64_t>(h->ws, o_exs);
+      launch_sort_excl(ex_d, cnt_d, excl_stride, nq, srt, s);
+      ex_sorted = srt;
+    }
+    const bool z_dev = is_device_ptr(z_sum);
+    double* zd = z_dev ? z_sum : at<double>(h->ws, o_z);
+    const bool acc_dev = accepted_idx_out && is_device_ptr(accepted_idx_out);
+    int64_t* accd = accepted_idx_out ? (acc_dev ? accepted_idx_out : at<int64_t>(h->ws, o_acc)) : nullptr;
+    const bool dr_dev = draws_out && is_device_ptr(draws_out);
+    int64_t* drd = draws_out ? (dr_dev ? draws_out : at<int64_t>(h->ws, o_dr)) : nullptr;
+    {
+      ProfScope ps(h, s, 0.0, double(nq) * m * h->d * 4.0);
+      launch_sample(h->X, h->n, h->global_offset, h->global_n, h->d, Qd, nq, family, bandwidth, m, seed, query_base,
+                    ex_sorted, cnt_d, excl ? excl_stride : 0, zd, accd, drd, s);
+    }
+    bool sync = false;
+    if (!z_dev) { copy_out(z_sum, zd, size_t(nq) * sizeof(double), s); sync = true; }
+    if (accd && !acc_dev) { copy_out(accepted_idx_out, accd, size_t(nq) * m * sizeof(int64_t), s); sync = true; }
+    if (drd && !dr_dev) { copy_out(draws_out, drd, size_t(nq) * sizeof(int64_t), s); sync = true; }
+    if (sync) DK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+dk_status dk_eval_rows(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth,
+                       const int64_t* rows, const int32_t* cnt, int32_t stride, double* out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    check_family_bw(family, bandwidth);
+    DK_REQUIRE(nq >= 0 && stride >= 0, "negative size");
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && out != nullptr && (rows != nullptr || stride == 0), "NULL argument");
+    DeviceGuard g(h->device);
+    LaunchCount lc(h);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Plan pl;
+    const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
+    const size_t o_r = pl.add<int64_t>(size_t(nq) * std::max(stride, 1));
+    const size_t o_c = pl.add<int32_t>(size_t(nq));
+    const size_t o_o = pl.add<double>(size_t(nq));
+    h->ws.reserve(pl.off);
+    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+    const int64_t* rd = rows;
+    if (rows && !is_device_ptr(rows)) {
+      int64_t* r = at<int64_t>(h->ws, o_r);
+      DK_CUDA(cudaMemcpyAsync(r, rows, size_t(nq) * stride * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      rd = r;
+    }
+    const int32_t* cd = cnt;
+    if (cnt && !is_device_ptr(cnt)) {
+      int32_t* c = at<int32_t>(h->ws, o_c);
+      DK_CUDA(cudaMemcpyAsync(c, cnt, size_t(nq) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      cd = c;
+    }
+    const bool od = is_device_ptr(out);
+    double* o = od ? out : at<double>(h->ws, o_o);
+    launch_eval_rows(h->X, h->n, h->global_offset, h->d, Qd, nq, family, bandwidth, rd, cd, stride, o, s);
+    if (!od) {
+      copy_out(out, o, size_t(nq) * sizeof(double), s);
+      DK_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+dk_status dk_kernel_values(int32_t family, double bandwidth, const double* dist, int64_t count, double* out,
+                           void* stream) {
+  return guard([&] {
+    check_family_bw(family, bandwidth);
+    DK_REQUIRE(count >= 0, "negative count");
+    if (count == 0) return;
+    DK_REQUIRE(dist != nullptr && out != nullptr, "NULL argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool din = is_device_ptr(dist), dout = is_device_ptr(out);
+    double *dd = nullptr, *od = nullptr;
+    uint32_t* bad = nullptr;
+    DK_CUDA(cudaMalloc(&bad, sizeof(uint32_t) + 2 * size_t(count) * sizeof(double)));
+    dd = reinterpret_cast<double*>(bad + 2);
+    od = dd + count;
+    DK_CUDA(cudaMemsetAsync(bad, 0, sizeof(uint32_t), s));
+    DK_CUDA(cudaMemcpyAsync(dd, dist, size_t(count) * sizeof(double), cudaMemcpyDefault, s));
+    launch_kernel_values(family, bandwidth, dd, count, od, bad, s);
+    uint32_t b = 0;
+    DK_CUDA(cudaMemcpyAsync(&b, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    DK_CUDA(cudaMemcpyAsync(out, od, size_t(count) * sizeof(double), cudaMemcpyDefault, s));
+    DK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(bad);
+    (void)din;
+    (void)dout;
+    DK_REQUIRE(!(b & 1u), "distance must be finite");
+    DK_REQUIRE(!(b & 2u), "distance must be nonnegative");
+  });
+}
+
+dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m,
+                   uint64_t seed, int64_t query_base, double* value_out, int64_t* nbr_idx_out, double* nbr_d2_out,
+                   int64_t* sample_idx_out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    check_family_bw(family, bandwidth);
+    const int64_t n = h->n;
+    DK_REQUIRE(h->global_offset == 0 && h->global_n == n,
+               "dk_deann runs on an unsharded handle; use dk_knn/dk_sample per shard");
+    DK_REQUIRE(k >= 0 && int64_t(k) <= n, "k=" + std::to_string(k) + " out of range [0, " + std::to_string(n) + "]");
+    DK_REQUIRE(m >= 0, "m=" + std::to_string(m) + " must be >= 0");
+    DK_REQUIRE(!(m > 0 && int64_t(k) >= n), "m > 0 requires k + 1 <= n so the remainder is nonempty");
+    DK_REQUIRE(k <= 4096, "k > 4096 is not supported by the GPU k-NN selection");
+    DK_REQUIRE(nq >= 0, "negative query count");
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && value_out != nullptr, "NULL argument");
+    DeviceGuard g(h->device);
+    LaunchCount lc(h);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int32_t ks = std::max(k, 1);
+    Plan pl;
+    const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
+    const size_t o_idx = pl.add<int64_t>(size_t(nq) * ks);
+    const size_t o_d2 = pl.add<double>(size_t(nq) * ks);
+    const size_t o_srt = pl.add<int64_t>(size_t(nq) * ks);
+    const size_t o_z1 = pl.add<double>(size_t(nq));
+    const size_t o_z2 = pl.add<double>(size_t(nq));
+    const size_t o_val = pl.add<double>(size_t(nq));
+    const size_t o_acc = pl.add<int64_t>(sample_idx_out ? size_t(nq) * std::max(m, 1) : 1);
+    const size_t base = pl.off;
+    h->ws.reserve(base + (k > 0 ? knn_ws_bytes(h, k, nq) : 0));
+    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+    int64_t* idx = at<int64_t>(h->ws, o_idx);
+    double* d2 = at<double>(h->ws, o_d2);
+    double* z1 = at<double>(h->ws, o_z1);
+    double* z2 = at<double>(h->ws, o_z2);
+    if (k > 0) {
+      knn_device(h, Qd, nq, k, idx, d2, s, base);
+      if (family == DK_LAPLACIAN)
+        launch_eval_rows(h->X, h->n, 0, h->d, Qd, nq, family, bandwidth, idx, nullptr, k, z1, s);
+    }
+    const bool acc_dev = sample_idx_out && is_device_ptr(sample_idx_out);
+    int64_t* accd = sample_idx_out ? (acc_dev ? sample_idx_out : at<int64_t>(h->ws, o_acc)) : nullptr;
+    if (m > 0) {
+      const int64_t* ex = nullptr;
+      if (k > 0) {
+        int64_t* srt = at<int64_t>(h->ws, o_srt);
+        launch_sort_excl(idx, nullptr, k, nq, srt, s);
+        ex = srt;
+      }
+      ProfScope ps(h, s, 0.0, double(nq) * (m + k) * h->d * 4.0);
+      launch_sample(h->X, h->n, 0, n, h->d, Qd, nq, family, bandwidth, m, seed, query_base, ex, nullptr,
+                    k > 0 ? k : 0, z2, accd, nullptr, s);
+    }
+    const bool v_dev = is_device_ptr(value_out);
+    double* vd = v_dev ? value_out : at<double>(h->ws, o_val);
+    launch_deann_combine(nq, family, bandwidth, k, m, n, d2, z1, z2, vd, s);
+    bool sync = false;
+    if (!v_dev) { copy_out(value_out, vd, size_t(nq) * sizeof(double), s); sync = true; }
+    if (k > 0 && nbr_idx_out) { copy_out(nbr_idx_out, idx, size_t(nq) * k * sizeof(int64_t), s); sync = true; }
+    if (k > 0 && nbr_d2_out) { copy_out(nbr_d2_out, d2, size_t(nq) * k * sizeof(double), s); sync = true; }
+    if (accd && !acc_dev && m > 0) { copy_out(sample_idx_out, accd, size_t(nq) * m * sizeof(int64_t), s); sync = true; }
+    if (sync) DK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+dk_status dk_set_profiling(dk_handle h, int32_t on) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    h->profiling = on != 0;
+    h->prof_used = 0;
+  });
+}
+
+dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* bytes) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    DeviceGuard g(h->device);
+    double tot = 0.0;
+    for (size_t i = 0; i < h->prof_used; ++i) {
+      DK_CUDA(cudaEventSynchronize(h->prof_events[i].second));
+      float t = 0.f;
+      DK_CUDA(cudaEventElapsedTime(&t, h->prof_events[i].first, h->prof_events[i].second));
+      tot += t;
+    }
+    if (ms) *ms = h->prof_used ? tot / double(h->prof_used) : 0.0;
+    if (flops) *flops = h->last_flops;
+    if (bytes) *bytes = h->last_bytes;
+  });
+}
+
+dk_status dk_last_launch_count(dk_handle h, int64_t* count) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr && count != nullptr, "NULL argument");
+    *count = h->launches;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,185 @@
+// internal.h — host-side internals shared by the C-ABI translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/deann_b200.h"
+
+namespace dk {
+
+void set_error(const std::string& msg);
+
+struct Error {
+  dk_status code;
+  std::string msg;
+};
+
+#define DK_CUDA(call)                                                                           \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess) {                                                                    \
+      throw ::dk::Error{e_ == cudaErrorMemoryAllocation ? DK_ENOMEM : DK_ECUDA,                 \
+                        std::string(#call) + ": " + cudaGetErrorString(e_) + " at " + __FILE__ + \
+                            ":" + std::to_string(__LINE__)};                                    \
+    }                                                                                           \
+  } while (0)
+
+extern std::atomic<long long> g_launches;  // kernels launched by this library
+#define DK_CHECK_LAUNCH()                         \
+  do {                                            \
+    ::dk::g_launches.fetch_add(1);                \
+    DK_CUDA(cudaGetLastError());                  \
+  } while (0)
+
+#define DK_REQUIRE(cond, msg)                          \
+  do {                                                 \
+    if (!(cond)) throw ::dk::Error{DK_EINVAL, (msg)};  \
+  } while (0)
+
+// One operand encoding of the dataset for the tensor-core tile.
+struct Encoding {
+  int mode = -1;            // 0 exact fp16, 1 split3, 2 fp16 single (lossy)
+  int32_t Kp = 0;           // padded K (multiple of 64)
+  __half* B = nullptr;      // [n_pad][Kp]
+  float* xn = nullptr;      // [n_pad] |x - mu|^2 in fp32
+  double* mu = nullptr;     // [d] centring (nullptr = none)
+  float* sx = nullptr;      // device scalar: power-of-two scale applied to x
+  float xn_max = 0.f;       // max of xn (host copy, k-NN certificate)
+  float eps_rel = 0.f;      // |approx d2 - exact d2| <= eps_rel * (|q|^2 + xn_max)
+  CUtensorMap tmap;
+};
+
+// Growable device scratch, carved per call.
+struct Workspace {
+  uint8_t* base = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+  void reserve(size_t bytes);
+  void reset() { off = 0; }
+  template <class T>
+  T* take(size_t count) {
+    size_t a = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + a);
+    off = a + count * sizeof(T);
+    if (off > cap) throw Error{DK_ECUDA, "workspace overflow (internal sizing bug)"};
+    return p;
+  }
+  ~Workspace();
+};
+
+}  // namespace dk
+
+struct dk_dataset {
+  int device = 0;
+  int num_sms = 148;
+  int64_t n = 0, n_pad = 0;
+  int32_t d = 0;
+  int64_t global_offset = 0, global_n = 0;
+  int precision = 0;
+  bool int_exact = false;   // rows are small integers: exact fp16 encoding valid
+  float* X = nullptr;       // [n][d] fp32 rows
+  double* xn64 = nullptr;   // [n]
+  dk::Encoding enc_exact;   // mode 0 (only if int_exact)
+  dk::Encoding enc_split;   // mode 1 (built lazily when needed)
+  dk::Encoding enc_fp16;    // mode 2 (opt-in)
+  dk::Workspace ws;
+  double* mu = nullptr;     // [d] column means (split/fp16 centring)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  size_t prof_used = 0;
+  bool profiling = false;
+  double last_flops = 0, last_bytes = 0;
+  int64_t launches = 0;
+};
+
+namespace dk {
+
+// ---- launchers (prep.cu / tile.cu / sample.cu / l1.cu / knn.cu) ----------
+struct QueryOperand {
+  int32_t nq = 0, nq_pad = 0;
+  __half* A = nullptr;        // [nq_pad][Kp]
+  float* qn = nullptr;        // [nq_pad]
+  float* m2s = nullptr;       // device scalar
+  CUtensorMap tmap;
+};
+
+CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint32_t box_rows);
+
+// dataset prep
+void launch_check_finite_rows(const float* X, int64_t count, uint32_t* flags, cudaStream_t s);
+void launch_row_stats(const float* X, int64_t n, int32_t d, double* xn64, uint32_t* flags, cudaStream_t s);
+void launch_column_mean(const float* X, int64_t n, int32_t d, double* partial, int32_t row_blocks, double* mu,
+                        cudaStream_t s);
+void launch_encode_rows(const float* X, int64_t n, int64_t n_pad, int32_t d, int mode, const double* mu,
+                        int32_t Kp, __half* B, float* xn, float* scale, uint32_t* maxabs_bits, cudaStream_t s);
+// queries
+void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags, cudaStream_t s);
+void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
+                           int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
+                           cudaStream_t s);
+void launch_reduce_partials(const double* part, int32_t nparts, int32_t nq_pad, int64_t nq, double scale,
+                            double* out, cudaStream_t s);
+
+// tcgen05 tile sweep
+struct SweepArgs {
+  int mode;                   // TileMode
+  const QueryOperand* qop;
+  const Encoding* enc;
+  int64_t n, n_pad;
+  int32_t tile_stride;        // 1 = all tiles
+  float negc;
+  double* part;               // out partials (KDE)
+  int32_t* ncc_out;           // number of column chunks used (KDE)
+  float* tmin;                // TILEMIN output
+  const float* tau;
+  uint32_t* cand_cnt;
+  unsigned long long* cand;
+  int32_t cap;
+  const int32_t* row_map;
+};
+size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms);  // doubles needed for KDE partials
+void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
+
+// L1 / laplacian exact KDE on CUDA cores
+size_t l1_part_count(int64_t n, int32_t nq);
+void launch_l1_kde(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, double inv_h, double* part,
+                   int32_t* nparts, float* q32, cudaStream_t s);
+
+// sampling / explicit rows (fp64 direct difference)
+void launch_sample(const float* X, int64_t n_local, int64_t global_offset, int64_t global_n, int32_t d,
+                   const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t m, uint64_t seed,
+                   int64_t query_base, const int64_t* excl_sorted, const int32_t* excl_cnt, int32_t excl_stride,
+                   double* z_sum, int64_t* acc_idx, int64_t* draws, cudaStream_t s);
+void launch_sort_excl(const int64_t* excl, const int32_t* excl_cnt, int32_t stride, int64_t nq, int64_t* sorted,
+                      cudaStream_t s);
+void launch_eval_rows(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q, int64_t nq,
+                      int32_t family, double bandwidth, const int64_t* rows, const int32_t* cnt, int32_t stride,
+                      double* out, cudaStream_t s);
+
+// k-NN selection
+void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t kprime, float* tau,
+                          cudaStream_t s);
+void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s);
+void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
+                          int32_t kprime, const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap,
+                          const float* tau, const float* qn, float xn_max, float eps_rel, int64_t* idx_out,
+                          double* d2_out, int32_t* status, cudaStream_t s);
+void launch_tau_from_cand(const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, int64_t nq,
+                          int32_t kprime, float* tau, int32_t* overflow_list, int32_t* n_overflow, cudaStream_t s);
+void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
+                               const int32_t* qlist, int32_t nlist, int32_t k, int64_t* idx_out, double* d2_out,
+                               cudaStream_t s);
+void launch_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_in, const double* d2_in,
+                       int64_t* idx_out, double* d2_out, cudaStream_t s);
+void launch_kernel_values(int32_t family, double h, const double* dist, int64_t count, double* out, uint32_t* bad,
+                          cudaStream_t s);
+void launch_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m, int64_t n_total,
+                          const double* nbr_d2, const double* z1_l1_sum, const double* z2_sum, double* value,
+                          cudaStream_t s);
+
+}  // namespace dk

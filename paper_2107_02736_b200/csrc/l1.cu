@@ -1,0 +1,122 @@
+// l1.cu — exact laplacian KDE on CUDA cores (K4).
+//
+// Reference: naive_kde's L1 branch (estimators.py:134-143): for each query,
+// sum_i exp(-sum_k |x_ik - y_k| / h) over row blocks, then / n.  L1 is not a
+// contraction, so it cannot use the tensor cores; this is a register-tiled
+// SIMT kernel: a 64-query x 128-row tile per block, 4x8 outputs per thread,
+// 32-dimension smem chunks, fp32 |a-b| accumulation with per-chunk partial
+// sums, ex2.approx epilogue, fp32 per-tile row sums folded into fp64.
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace dk {
+
+namespace {
+
+constexpr int TQ = 64, TX = 128, DK = 32, XPAD = 4;
+constexpr int kTilesPerBlock = 8;
+
+__global__ void __launch_bounds__(256) l1_kde_kernel(const float* __restrict__ X, int64_t n, int32_t d,
+                                                      const double* __restrict__ Q, int64_t nq, int32_t nq_pad,
+                                                      float negc, double* __restrict__ part) {
+  __shared__ __align__(16) float Qs[DK][TQ];
+  __shared__ __align__(16) float Xs[DK][TX + XPAD];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t q0 = int64_t(blockIdx.x) * TQ;
+  const int64_t tile0 = int64_t(blockIdx.y) * kTilesPerBlock;
+  double qacc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int xt = 0; xt < kTilesPerBlock; ++xt) {
+    const int64_t x0 = (tile0 + xt) * TX;
+    if (x0 >= n) break;
+    float acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int k0 = 0; k0 < d; k0 += DK) {
+      // stage Q (fp64 -> fp32) and X chunks, transposed to [k][row]
+#pragma unroll
+      for (int r = 0; r < (TQ * DK) / 256; ++r) {
+        const int e = r * 256 + threadIdx.x;
+        const int qq = e / DK, kk = e % DK;
+        const int64_t qi = q0 + qq;
+        Qs[kk][qq] = (qi < nq && k0 + kk < d) ? float(Q[qi * d + k0 + kk]) : 0.f;
+      }
+#pragma unroll
+      for (int r = 0; r < (TX * DK) / 256; ++r) {
+        const int e = r * 256 + threadIdx.x;
+        const int xx = e / DK, kk = e % DK;
+        const int64_t xi = x0 + xx;
+        Xs[kk][xx] = (xi < n && k0 + kk < d) ? __ldg(X + xi * d + k0 + kk) : 0.f;
+      }
+      __syncthreads();
+      float part_acc[4][8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) part_acc[i][j] = 0.f;
+#pragma unroll 4
+      for (int kk = 0; kk < DK; ++kk) {
+        const float4 qv = *reinterpret_cast<const float4*>(&Qs[kk][ty * 4]);
+        const float4 xa = *reinterpret_cast<const float4*>(&Xs[kk][tx * 8]);
+        const float4 xb = *reinterpret_cast<const float4*>(&Xs[kk][tx * 8 + 4]);
+        const float qs[4] = {qv.x, qv.y, qv.z, qv.w};
+        const float xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) part_acc[i][j] += fabsf(qs[i] - xs[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] += part_acc[i][j];
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float rs = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool valid = x0 + tx * 8 + j < n;
+        const float e = ex2_approx(acc[i][j] * negc);
+        rs += valid ? e : 0.f;
+      }
+      qacc[i] += double(rs);
+    }
+  }
+  // reduce over the 16 tx lanes (same ty within a warp half)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double v = qacc[i];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    qacc[i] = v;
+  }
+  if (tx == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) part[size_t(blockIdx.y) * nq_pad + q0 + ty * 4 + i] = qacc[i];
+  }
+}
+
+}  // namespace
+
+static int64_t l1_chunks(int64_t n) { return (n + int64_t(TX) * kTilesPerBlock - 1) / (int64_t(TX) * kTilesPerBlock); }
+
+size_t l1_part_count(int64_t n, int32_t nq) {
+  const int64_t nq_pad = (int64_t(nq) + TQ - 1) / TQ * TQ;
+  return size_t(l1_chunks(n)) * size_t(nq_pad);
+}
+
+void launch_l1_kde(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, double inv_h, double* part,
+                   int32_t* nparts, float* /*q32*/, cudaStream_t s) {
+  const int32_t nq_pad = int32_t((nq + TQ - 1) / TQ * TQ);
+  const int64_t chunks = l1_chunks(n);
+  dim3 grid(unsigned(nq_pad / TQ), unsigned(chunks));
+  const float negc = float(-inv_h * 1.4426950408889634);
+  l1_kde_kernel<<<grid, 256, 0, s>>>(X, n, d, Q, nq, nq_pad, negc, part);
+  DK_CHECK_LAUNCH();
+  *nparts = int32_t(chunks);
+}
+
+}  // namespace dk

@@ -1,0 +1,280 @@
+// sample.cu — Philox-indexed gather kernels (K3): RS, DEANN residual, explicit rows.
+//
+// Reference: rs_kde (estimators.py:152-164), _rs_excluding (:203-233),
+// _kernel_rows (:106-119), deann's value formula (:372).
+//
+// Stream semantics.  For query j (global position j + query_base) the t-th
+// draw is
+//     r = philox4x32_10(ctr = {t_lo, t_hi, j_lo, j_hi}, key = {seed_lo, seed_hi})
+//     row_t = mulhi64((r.y << 32) | r.x, N)                    (N = global n)
+// i.e. uniform with replacement over [0, N).  The first m draws whose row is
+// NOT in the query's exclusion list (its k-NN set X1) are accepted — exactly
+// the effective rule of _rs_excluding ("keep the first `need` non-excluded
+// draws of each batch", estimators.py:225-228), so feeding this stream to the
+// reference through a replaying `rng.integers` reproduces its estimate.
+//
+// One warp per query; 32 consecutive draws per iteration; accepted draws are
+// compacted with a ballot so acceptance order == draw order.  Each accepted
+// row is evaluated by the lane that drew it: fp32 row loads (float4 when
+// aligned), fp64 direct-difference distance, fp64 exp (parity ~1e-15 with
+// the reference's fp64 arithmetic).
+#include "internal.h"
+
+namespace dk {
+
+namespace {
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k.x += W0; k.y += W1; }
+    const uint32_t lo0 = M0 * c.x, hi0 = __umulhi(M0, c.x);
+    const uint32_t lo1 = M1 * c.z, hi1 = __umulhi(M1, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+__device__ __forceinline__ int64_t draw_row(uint64_t seed, uint64_t t, uint64_t jg, uint64_t N) {
+  const uint4 r = philox4x32_10(make_uint4(uint32_t(t), uint32_t(t >> 32), uint32_t(jg), uint32_t(jg >> 32)),
+                                make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
+  const uint64_t v = (uint64_t(r.y) << 32) | uint64_t(r.x);
+  return int64_t(__umul64hi(v, N));
+}
+
+__device__ __forceinline__ bool in_sorted(const int64_t* __restrict__ a, int cnt, int64_t v) {
+  int lo = 0, hi = cnt;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const int64_t x = a[mid];
+    if (x < v) lo = mid + 1; else hi = mid;
+  }
+  return lo < cnt && a[lo] == v;
+}
+
+// fp64 kernel value between the query (fp64, in smem) and one fp32 dataset row
+__device__ __forceinline__ double row_kernel(const float* __restrict__ x, const double* __restrict__ q, int d,
+                                             int family, double c) {
+  double acc = 0.0;
+  if ((d & 3) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int k4 = 0; k4 < (d >> 2); ++k4) {
+      const float4 v = __ldg(x4 + k4);
+      const double t0 = double(v.x) - q[4 * k4 + 0], t1 = double(v.y) - q[4 * k4 + 1];
+      const double t2 = double(v.z) - q[4 * k4 + 2], t3 = double(v.w) - q[4 * k4 + 3];
+      if (family == DK_LAPLACIAN) {
+        acc += (fabs(t0) + fabs(t1)) + (fabs(t2) + fabs(t3));
+      } else {
+        acc = fma(t0, t0, acc); acc = fma(t1, t1, acc); acc = fma(t2, t2, acc); acc = fma(t3, t3, acc);
+      }
+    }
+  } else {
+    for (int k = 0; k < d; ++k) {
+      const double t = double(__ldg(x + k)) - q[k];
+      acc = family == DK_LAPLACIAN ? acc + fabs(t) : fma(t, t, acc);
+    }
+  }
+  // c = 1/(2h^2) for gaussian (exp(-d2*c)), 1/h otherwise
+  if (family == DK_EXPONENTIAL) acc = sqrt(acc);
+  return exp(-acc * c);
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int64_t global_offset, int64_t N,
+                              int32_t d, const double* __restrict__ Q, int64_t nq, int32_t family, double c,
+                              int32_t m, uint64_t seed, int64_t query_base, const int64_t* __restrict__ excl,
+                              const int32_t* __restrict__ excl_cnt, int32_t excl_stride, double* __restrict__ z_sum,
+                              int64_t* __restrict__ acc_idx, int64_t* __restrict__ draws) {
+  extern __shared__ double sq[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
+  if (j >= nq) return;
+  double* q = sq + size_t(wib) * d;
+  for (int k = lane; k < d; k += 32) q[k] = Q[size_t(j) * d + k];
+  __syncwarp();
+  const int ecnt = excl ? (excl_cnt ? excl_cnt[j] : excl_stride) : 0;
+  const int64_t* ex = excl ? excl + size_t(j) * excl_stride : nullptr;
+  const uint64_t jg = uint64_t(j + query_base);
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  double zsum = 0.0;
+  int accepted = 0;
+  uint64_t t_base = 0;
+  int64_t last_t = -1;
+  while (accepted < m) {
+    const uint64_t t = t_base + lane;
+    const int64_t row = draw_row(seed, t, jg, uint64_t(N));
+    const bool ok = ecnt == 0 || !in_sorted(ex, ecnt, row);
+    const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
+    const int rank = __popc(ballot & lt_mask);
+    const bool take = ok && (accepted + rank < m);
+    if (take) {
+      const int64_t loc = row - global_offset;
+      if (loc >= 0 && loc < n_local) zsum += row_kernel(X + size_t(loc) * d, q, d, family, c);
+      if (acc_idx) acc_idx[size_t(j) * m + accepted + rank] = row;
+    }
+    const uint32_t took = __ballot_sync(0xffffffffu, take);
+    if (took) last_t = int64_t(t_base) + 31 - __clz(took);
+    accepted += __popc(took);
+    t_base += 32;
+  }
+  zsum = warp_sum_d(zsum);
+  if (lane == 0) {
+    z_sum[j] = zsum;
+    if (draws) draws[j] = last_t + 1;
+  }
+}
+
+// per-query ascending sort of the exclusion list (block per query, bitonic in smem)
+__global__ void sort_excl_kernel(const int64_t* __restrict__ excl, const int32_t* __restrict__ cnt, int32_t stride,
+                                 int32_t B, int64_t* __restrict__ sorted) {
+  extern __shared__ long long sb[];
+  const int64_t q = blockIdx.x;
+  const int c = cnt ? cnt[q] : stride;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) sb[i] = i < c ? excl[size_t(q) * stride + i] : LLONG_MAX;
+  for (int k = 2; k <= B; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < B; i += blockDim.x) {
+        const int ixj = i ^ jj;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const long long a = sb[i], b = sb[ixj];
+          if ((a > b) == up) { sb[i] = b; sb[ixj] = a; }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < c; i += blockDim.x) sorted[size_t(q) * stride + i] = sb[i];
+}
+
+// explicit rows: out[j] = sum_c K(q_j, x_rows[j*stride + c])   (one warp per query)
+__global__ void eval_rows_kernel(const float* __restrict__ X, int64_t n_local, int64_t global_offset, int32_t d,
+                                 const double* __restrict__ Q, int64_t nq, int32_t family, double c,
+                                 const int64_t* __restrict__ rows, const int32_t* __restrict__ cnt, int32_t stride,
+                                 double* __restrict__ out) {
+  extern __shared__ double sq[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
+  if (j >= nq) return;
+  double* q = sq + size_t(wib) * d;
+  for (int k = lane; k < d; k += 32) q[k] = Q[size_t(j) * d + k];
+  __syncwarp();
+  const int r = cnt ? cnt[j] : stride;
+  double s = 0.0;
+  for (int i = lane; i < r; i += 32) {
+    const int64_t loc = rows[size_t(j) * stride + i] - global_offset;
+    if (loc >= 0 && loc < n_local) s += row_kernel(X + size_t(loc) * d, q, d, family, c);
+  }
+  s = warp_sum_d(s);
+  if (lane == 0) out[j] = s;
+}
+
+// value = (k/n) Z1 + ((n-k)/n) Z2   (estimators.py:344-372), one thread per query
+__global__ void deann_combine_kernel(int64_t nq, int32_t family, double c, int32_t k, int32_t m, int64_t n,
+                                     const double* __restrict__ nbr_d2, const double* __restrict__ z1_l1_sum,
+                                     const double* __restrict__ z2_sum, double* __restrict__ value) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= nq) return;
+  double z1 = 0.0;
+  if (k > 0) {
+    if (family == DK_LAPLACIAN) {
+      z1 = z1_l1_sum[j] / double(k);
+    } else {
+      double s = 0.0;
+      for (int i = 0; i < k; ++i) {
+        double dd = nbr_d2[size_t(j) * k + i];
+        if (family == DK_EXPONENTIAL) dd = sqrt(dd);
+        s += exp(-dd * c);
+      }
+      z1 = s / double(k);
+    }
+  }
+  double v = (double(k) / double(n)) * z1;
+  if (m > 0) v += (double(n - k) / double(n)) * (z2_sum[j] / double(m));
+  value[j] = v;
+}
+
+__global__ void kernel_values_kernel(int32_t family, double h, const double* __restrict__ dist, int64_t count,
+                                     double* __restrict__ out, uint32_t* __restrict__ bad) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double v = dist[i];
+  if (!isfinite(v)) atomicOr(bad, 1u);
+  else if (v < 0.0) atomicOr(bad, 2u);
+  out[i] = family == DK_GAUSSIAN ? exp(-v / (2.0 * h * h)) : exp(-v / h);
+}
+
+double family_c(int32_t family, double h) { return family == DK_GAUSSIAN ? 1.0 / (2.0 * h * h) : 1.0 / h; }
+
+}  // namespace
+
+void launch_sample(const float* X, int64_t n_local, int64_t global_offset, int64_t global_n, int32_t d,
+                   const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t m, uint64_t seed,
+                   int64_t query_base, const int64_t* excl_sorted, const int32_t* excl_cnt, int32_t excl_stride,
+                   double* z_sum, int64_t* acc_idx, int64_t* draws, cudaStream_t s) {
+  const int wpb = 8;
+  const size_t smem = size_t(wpb) * d * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    DK_CUDA(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    attr = true;
+  }
+  if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the sampling kernel"};
+  sample_kernel<<<unsigned((nq + wpb - 1) / wpb), wpb * 32, smem, s>>>(
+      X, n_local, global_offset, global_n, d, Q, nq, family, family_c(family, bandwidth), m, seed, query_base,
+      excl_sorted, excl_cnt, excl_stride, z_sum, acc_idx, draws);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_sort_excl(const int64_t* excl, const int32_t* excl_cnt, int32_t stride, int64_t nq, int64_t* sorted,
+                      cudaStream_t s) {
+  int B = 1;
+  while (B < stride) B <<= 1;
+  const size_t smem = size_t(B) * 8;
+  if (smem > 232448) throw Error{DK_EINVAL, "exclusion list too long (k > 29000) for the sampling path"};
+  static bool attr = false;
+  if (!attr) {
+    DK_CUDA(cudaFuncSetAttribute(sort_excl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    attr = true;
+  }
+  sort_excl_kernel<<<unsigned(nq), 256, smem, s>>>(excl, excl_cnt, stride, B, sorted);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_eval_rows(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q, int64_t nq,
+                      int32_t family, double bandwidth, const int64_t* rows, const int32_t* cnt, int32_t stride,
+                      double* out, cudaStream_t s) {
+  const int wpb = 8;
+  const size_t smem = size_t(wpb) * d * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    DK_CUDA(cudaFuncSetAttribute(eval_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    attr = true;
+  }
+  eval_rows_kernel<<<unsigned((nq + wpb - 1) / wpb), wpb * 32, smem, s>>>(
+      X, n_local, global_offset, d, Q, nq, family, family_c(family, bandwidth), rows, cnt, stride, out);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_kernel_values(int32_t family, double h, const double* dist, int64_t count, double* out, uint32_t* bad,
+                          cudaStream_t s) {
+  kernel_values_kernel<<<unsigned((count + 255) / 256), 256, 0, s>>>(family, h, dist, count, out, bad);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m, int64_t n_total,
+                          const double* nbr_d2, const double* z1_l1_sum, const double* z2_sum, double* value,
+                          cudaStream_t s) {
+  deann_combine_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(nq, family, family_c(family, bandwidth), k, m,
+                                                                  n_total, nbr_d2, z1_l1_sum, z2_sum, value);
+  DK_CHECK_LAUNCH();
+}
+
+}  // namespace dk

@@ -1,0 +1,142 @@
+// tile.cu — host launcher for the tcgen05 tile sweep (tile_kernel.cuh).
+#include <algorithm>
+#include <mutex>
+
+#include "internal.h"
+#include "tile_kernel.cuh"
+
+namespace dk {
+
+namespace {
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t get_encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  if (!fn) throw Error{DK_ECUDA, "cuTensorMapEncodeTiled entry point unavailable"};
+  return fn;
+}
+
+constexpr size_t kMaxSmem = 232448;  // sm_100 opt-in dynamic shared memory per block
+
+struct Plan {
+  int a_resident, stages, tiles_per_unit, ncc;
+  size_t smem;
+};
+
+Plan make_plan(int kblocks, int ntiles, int nqb, int num_sms) {
+  Plan pl{};
+  // keep the query block resident when it fits next to a >=3-stage ring
+  size_t a_bytes = size_t(kblocks) * kABlockBytes;
+  if (tile_smem_bytes(kblocks, 1, 3) <= kMaxSmem) {
+    pl.a_resident = 1;
+    int st = 3;
+    while (st < 8 && tile_smem_bytes(kblocks, 1, st + 1) <= kMaxSmem) ++st;
+    pl.stages = st;
+  } else {
+    pl.a_resident = 0;
+    int st = 2;
+    while (st < 6 && tile_smem_bytes(kblocks, 0, st + 1) <= kMaxSmem) ++st;
+    pl.stages = st;
+  }
+  (void)a_bytes;
+  // ~16+ units per CTA for balance; at least 1 tile per unit
+  const int64_t total_tiles = int64_t(ntiles) * nqb;
+  int64_t tpu = total_tiles / (int64_t(num_sms) * 16);
+  tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, ntiles));
+  pl.tiles_per_unit = int(tpu);
+  pl.ncc = int((ntiles + tpu - 1) / tpu);
+  pl.smem = tile_smem_bytes(kblocks, pl.a_resident, pl.stages);
+  return pl;
+}
+
+template <int MODE>
+void launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const TileParams& p, int grid, size_t smem,
+                 cudaStream_t s) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxSmem));
+  });
+  DK_CUDA(attr_err);
+  tile_kernel<MODE><<<grid, kThreads, smem, s>>>(ta, tb, p);
+  DK_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {kp, rows};
+  cuuint64_t strides[1] = {kp * 2};
+  cuuint32_t box[2] = {uint32_t(kBK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error{DK_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r))};
+  return m;
+}
+
+size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms) {
+  const int ntiles = int(n_pad / kBN);
+  const Plan pl = make_plan(1, ntiles, nq_pad / kBM, num_sms);
+  return size_t(pl.ncc) * 2 * size_t(nq_pad);
+}
+
+void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
+  const QueryOperand& q = *a.qop;
+  const Encoding& e = *a.enc;
+  const int kblocks = e.Kp / kBK;
+  const int ntiles_all = int(a.n_pad / kBN);
+  const int ntiles = (ntiles_all + a.tile_stride - 1) / a.tile_stride;
+  const int nqb = q.nq_pad / kBM;
+  const Plan pl = make_plan(kblocks, ntiles, nqb, num_sms);
+
+  TileParams p{};
+  p.nq = q.nq;
+  p.nq_pad = q.nq_pad;
+  p.nqb = nqb;
+  p.n = a.n;
+  p.ntiles = ntiles;
+  p.tile_stride = a.tile_stride;
+  p.tiles_per_unit = pl.tiles_per_unit;
+  p.ncc = pl.ncc;
+  p.kblocks = kblocks;
+  p.a_resident = pl.a_resident;
+  p.stages = pl.stages;
+  p.xn = e.xn;
+  p.qn = q.qn;
+  p.m2s = q.m2s;
+  p.negc = a.negc;
+  p.part = a.part;
+  p.tmin = a.tmin;
+  p.tau = a.tau;
+  p.cand_cnt = a.cand_cnt;
+  p.cand = a.cand;
+  p.cap = a.cap;
+  p.row_map = a.row_map;
+  if (a.ncc_out) *a.ncc_out = pl.ncc;
+
+  const int nunits = nqb * pl.ncc;
+  const int grid = std::min(nunits, num_sms);
+  switch (a.mode) {
+    case MODE_KDE_GAUSS: launch_mode<MODE_KDE_GAUSS>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
+    case MODE_KDE_EXP: launch_mode<MODE_KDE_EXP>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
+    case MODE_TILEMIN: launch_mode<MODE_TILEMIN>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
+    case MODE_FILTER: launch_mode<MODE_FILTER>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
+    default: throw Error{DK_EINVAL, "bad tile mode"};
+  }
+}
+
+}  // namespace dk

@@ -1,0 +1,244 @@
+"""KDE estimators on the GPU — drop-in for reference estimators.py.
+
+Same names, signatures, return types and ValueError preconditions as
+``naive_kde`` (estimators.py:122-149), ``rs_kde`` (:152-164), ``deann``
+(:306-379) and ``deann_batch`` (:382-410).  The arithmetic runs in the CUDA
+kernels behind the C-ABI:
+
+* naive_kde  -> dk_naive: fused tcgen05 distance tile + exp + row sum
+  (gaussian/exponential) or the CUDA-core L1 kernel (laplacian);
+* rs_kde     -> dk_sample without exclusions (Philox-indexed gather);
+* deann      -> dk_deann (exact k-NN + exclusion sampling + combine) when the
+  index is the GPU brute force; any other AnnIndex is queried as a black box
+  and its neighbours drive dk_sample / dk_eval_rows / dk_kernel_values.
+
+Differences to the reference, by design: the uniform sampler is a
+counter-based Philox stream per query (sampler.py) instead of numpy's PCG64,
+and ``rsp_state`` (the permuted sampler) is not accelerated
+yet and raises NotImplementedError.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .ann import GpuBruteForceIndex
+from .data import Dataset, as_gpu_dataset
+from .kernels import KernelFamily, as_spec
+from .sampler import resolve_sampler
+
+__all__ = [
+    "Estimate", "BatchKde", "naive_kde", "rs_kde", "deann", "deann_batch",
+    "naive_kde_into", "deann_arrays", "kernel_from_distance",
+]
+
+
+@dataclass
+class Estimate:
+    """A single KDE estimate plus its cost counters (estimators.py:57-72)."""
+
+    value: float
+    kernel_evals: int
+    neighbors_used: int
+    samples_used: int
+    truncated: bool = False
+    clamped: bool = False
+
+
+@dataclass
+class BatchKde:
+    """Exact KDE values for a query batch plus the total kernel-eval count (estimators.py:75-80)."""
+
+    values: np.ndarray
+    kernel_evals: int
+
+
+def _queries64(queries, d: int) -> np.ndarray:
+    q = np.ascontiguousarray(np.atleast_2d(np.asarray(queries, dtype=np.float64)))
+    if q.shape[1] != d:
+        raise ValueError(f"dimension mismatch: queries d={q.shape[1]}, dataset d={d}")
+    return q
+
+
+def _query64(query, d: int) -> np.ndarray:
+    y = np.ascontiguousarray(np.asarray(query, dtype=np.float64).ravel())
+    if y.shape[0] != d:
+        raise ValueError(f"dimension mismatch: query d={y.shape[0]}, dataset d={d}")
+    return y
+
+
+# ---------------------------------------------------------------- exact
+
+
+def naive_kde_into(dataset: Dataset, kernel, queries, out, *, sums: bool = False, stream=None) -> None:
+    """Exact KDE into a caller buffer.  ``queries`` (nq, d) fp64 and ``out`` (nq,)
+    fp64 may be numpy arrays or torch CUDA tensors (device buffers skip all copies)."""
+    spec = as_spec(kernel)
+    nq = int(queries.shape[0])
+    _lib.check(_lib.load().dk_naive(dataset.handle, _lib.ptr(queries), nq, _lib.family_code(spec.family),
+                                    spec.bandwidth, _lib.DK_OUT_SUM if sums else 0, _lib.ptr(out),
+                                    stream if stream is not None else _lib.current_stream()))
+
+
+def naive_kde(dataset, kernel, queries) -> BatchKde:
+    """Exact KDE of every query against the full dataset (estimators.py:122-149)."""
+    ds = as_gpu_dataset(dataset)
+    spec = as_spec(kernel)
+    q = _queries64(queries, ds.d)
+    values = np.empty(q.shape[0], dtype=np.float64)
+    naive_kde_into(ds, spec, q, values)
+    return BatchKde(values=values, kernel_evals=q.shape[0] * ds.n)
+
+
+def kernel_from_distance(kernel, dist):
+    """Kernel values from precomputed family distances (kernels.py:65-83), on the GPU."""
+    spec = as_spec(kernel)
+    scalar = np.isscalar(dist) or np.ndim(dist) == 0
+    d = np.ascontiguousarray(np.asarray(dist, dtype=np.float64).ravel())
+    if not np.all(np.isfinite(d)):
+        raise ValueError("distance must be finite")
+    if np.any(d < 0.0):
+        raise ValueError("distance must be nonnegative")
+    out = np.empty_like(d)
+    if d.size:
+        _lib.check(_lib.load().dk_kernel_values(_lib.family_code(spec.family), spec.bandwidth, d.ctypes.data,
+                                                d.size, out.ctypes.data, None))
+    if scalar:
+        return float(out[0])
+    return out.reshape(np.shape(dist))
+
+
+# ---------------------------------------------------------------- sampling
+
+
+def _sample_sums(ds: Dataset, spec, q: np.ndarray, m: int, seed: int, base: int, excl=None, excl_cnt=None,
+                 stride: int = 0, export: bool = False):
+    nq = q.shape[0]
+    z = np.empty(nq, dtype=np.float64)
+    acc = np.empty((nq, m), dtype=np.int64) if export else None
+    _lib.check(_lib.load().dk_sample(ds.handle, q.ctypes.data, nq, _lib.family_code(spec.family), spec.bandwidth,
+                                     m, seed, base, _lib.ptr(excl), _lib.ptr(excl_cnt), stride, z.ctypes.data,
+                                     _lib.ptr(acc), None, None))
+    return z, acc
+
+
+def rs_kde(dataset, kernel, query, m: int, rng) -> Estimate:
+    """Uniform sampling with replacement: mean kernel value over m draws (estimators.py:152-164)."""
+    if m < 1:
+        raise ValueError(f"m={m} must be >= 1")
+    ds = as_gpu_dataset(dataset)
+    spec = as_spec(kernel)
+    y = _query64(query, ds.d).reshape(1, -1)
+    seed, base = resolve_sampler(rng).take(1)
+    z, _ = _sample_sums(ds, spec, y, m, seed, base)
+    return Estimate(value=float(z[0] / m), kernel_evals=m, neighbors_used=0, samples_used=m)
+
+
+# ---------------------------------------------------------------- DEANN
+
+
+def _validate(n: int, d: int, k: int, m: int, rng, rsp_state):
+    # estimators.py:322-335, same order and messages
+    if not 0 <= k <= n:
+        raise ValueError(f"k={k} out of range [0, {n}]")
+    if m < 0:
+        raise ValueError(f"m={m} must be >= 0")
+    if m > 0 and k >= n:
+        raise ValueError("m > 0 requires k + 1 <= n so the remainder is nonempty")
+    if m > 0 and (rng is None) == (rsp_state is None):
+        raise ValueError("give exactly one of rng= or rsp_state= when m > 0")
+    if rsp_state is not None and rsp_state.n != n:
+        raise ValueError("rsp_state was built for a different dataset size")
+
+
+def _is_gpu_bruteforce(ann, ds: Dataset) -> bool:
+    if isinstance(ann, GpuBruteForceIndex):
+        return ann.dataset is ds
+    # the reference's own BruteForceIndex over the same rows is also exact brute force
+    cls = type(ann)
+    if cls.__name__ == "BruteForceIndex" and hasattr(ann, "dataset"):
+        try:
+            return as_gpu_dataset(ann.dataset) is ds
+        except TypeError:
+            return False
+    return False
+
+
+def deann_arrays(dataset, kernel, queries, k: int, m: int, *, seed: int, query_base: int = 0,
+                 export_neighbors: bool = False, export_samples: bool = False):
+    """Batch DEANN with exact GPU brute force + Philox sampling.
+
+    Returns (values (nq,), neighbor_idx (nq, k) or None, sample_idx (nq, m) or None).
+    """
+    ds = as_gpu_dataset(dataset)
+    spec = as_spec(kernel)
+    q = _queries64(queries, ds.d)
+    nq = q.shape[0]
+    values = np.empty(nq, dtype=np.float64)
+    nbr = np.empty((nq, k), dtype=np.int64) if (export_neighbors and k > 0) else None
+    smp = np.empty((nq, m), dtype=np.int64) if (export_samples and m > 0) else None
+    _lib.check(_lib.load().dk_deann(ds.handle, q.ctypes.data, nq, _lib.family_code(spec.family), spec.bandwidth,
+                                    k, m, int(seed), int(query_base), values.ctypes.data, _lib.ptr(nbr), None,
+                                    _lib.ptr(smp), _lib.current_stream()))
+    return values, nbr, smp
+
+
+def deann(dataset, kernel, ann, query, k: int, m: int, *, rng=None, rsp_state=None) -> Estimate:
+    """Combined estimator: exact near part from the index, sampled far part (estimators.py:306-379)."""
+    ds = as_gpu_dataset(dataset)
+    spec = as_spec(kernel)
+    n = ds.n
+    _validate(n, ds.d, k, m, rng, rsp_state)
+    y = _query64(query, ds.d)
+    if rsp_state is not None and m > 0:
+        raise NotImplementedError("the permuted sampler (rsp_state=) is not GPU-accelerated yet (SURVEY §8 f1)")
+    seed, base = resolve_sampler(rng).take(1) if (m > 0) else (0, 0)
+    if k == 0 or _is_gpu_bruteforce(ann, ds):
+        values, _, _ = deann_arrays(ds, spec, y.reshape(1, -1), k, m, seed=seed, query_base=base)
+        k_hat = k
+        return Estimate(value=float(values[0]), kernel_evals=k_hat + m, neighbors_used=k_hat, samples_used=m,
+                        truncated=(m == 0 and k_hat < n))
+    # black-box index: neighbours from `ann`, everything else on the GPU
+    neighbors = ann.query(y, k)
+    x1 = np.ascontiguousarray(np.asarray(neighbors.indices, dtype=np.int64))
+    k_hat = len(x1)
+    if k_hat == 0:
+        z1 = 0.0
+    elif spec.family is KernelFamily.LAPLACIAN:
+        out = np.empty(1, dtype=np.float64)
+        _lib.check(_lib.load().dk_eval_rows(ds.handle, y.ctypes.data, 1, _lib.DK_LAPLACIAN, spec.bandwidth,
+                                            x1.ctypes.data, None, k_hat, out.ctypes.data, None))
+        z1 = float(out[0] / k_hat)
+    else:
+        d2 = np.asarray(neighbors.sq_distances, dtype=np.float64)
+        dist = d2 if spec.family is KernelFamily.GAUSSIAN else np.sqrt(d2)
+        z1 = float(np.mean(kernel_from_distance(spec, dist)))
+    if m == 0:
+        return Estimate(value=(k_hat / n) * z1, kernel_evals=k_hat, neighbors_used=k_hat, samples_used=0,
+                        truncated=k_hat < n)
+    excl = x1.reshape(1, -1) if k_hat else None
+    z, _ = _sample_sums(ds, spec, y.reshape(1, -1), m, seed, base, excl=excl, stride=max(k_hat, 1))
+    z2 = float(z[0] / m)
+    value = (k_hat / n) * z1 + ((n - k_hat) / n) * z2
+    return Estimate(value=value, kernel_evals=k_hat + m, neighbors_used=k_hat, samples_used=m)
+
+
+def deann_batch(dataset, kernel, ann, queries, k: int, m: int, *, rng=None, rsp_state=None,
+                independent_cursors: bool = False) -> list[Estimate]:
+    """Evaluate a query batch (estimators.py:382-410); one fused GPU call for brute force."""
+    ds = as_gpu_dataset(dataset)
+    spec = as_spec(kernel)
+    q = _queries64(queries, ds.d)
+    n = ds.n
+    _validate(n, ds.d, k, m, rng, rsp_state)
+    if rsp_state is not None and m > 0:
+        raise NotImplementedError("the permuted sampler (rsp_state=) is not GPU-accelerated yet (SURVEY §8 f1)")
+    if k == 0 or _is_gpu_bruteforce(ann, ds):
+        seed, base = resolve_sampler(rng).take(q.shape[0]) if m > 0 else (0, 0)
+        values, _, _ = deann_arrays(ds, spec, q, k, m, seed=seed, query_base=base)
+        return [Estimate(value=float(v), kernel_evals=k + m, neighbors_used=k, samples_used=m,
+                         truncated=(m == 0 and k < n)) for v in values]
+    return [deann(ds, spec, ann, q[j], k, m, rng=rng, rsp_state=rsp_state) for j in range(q.shape[0])]
