@@ -232,16 +232,16 @@ KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
   KnnPlan p;
   p.kprime = int32_t(std::min<int64_t>(h->n, int64_t(k) + std::max<int32_t>(32, k / 4)));
   const int64_t ntiles = h->n_pad / kBN;
-  if (h->n <= 4096 || 2 * ntiles < p.kprime) {
+  if (h->n <= 4096 || kColGroups * ntiles < p.kprime) {
     p.tau_inf = true;
     p.cap = int32_t(h->n);
     p.stride = 1;
     p.nseg = 0;
   } else {
     const int64_t target = std::clamp<int64_t>(16 * int64_t(p.kprime), 2048, 8192);
-    p.stride = int32_t(std::max<int64_t>(1, (2 * ntiles + target - 1) / target));
-    while (p.stride > 1 && 2 * ((ntiles + p.stride - 1) / p.stride) < 4 * p.kprime) --p.stride;
-    p.nseg = int32_t(2 * ((ntiles + p.stride - 1) / p.stride));
+    p.stride = int32_t(std::max<int64_t>(1, (kColGroups * ntiles + target - 1) / target));
+    while (p.stride > 1 && kColGroups * ((ntiles + p.stride - 1) / p.stride) < 4 * p.kprime) --p.stride;
+    p.nseg = int32_t(kColGroups * ((ntiles + p.stride - 1) / p.stride));
     int64_t cap = 2048;
     while (cap < 3 * int64_t(p.stride) * p.kprime && cap < 16384) cap <<= 1;
     p.cap = int32_t(cap);
@@ -579,7 +579,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       launch_sweep(a, h->num_sms, s);
     }
     double* od = out_dev ? out : at<double>(h->ws, o_out);
-    launch_reduce_partials(a.part, ncc * 2, nq_pad, nq, scale, od, s);
+    launch_reduce_partials(a.part, ncc * kColGroups, nq_pad, nq, scale, od, s);
     if (!out_dev) {
       copy_out(out, od, size_t(nq) * sizeof(double), s);
       DK_CUDA(cudaStreamSynchronize(s));

@@ -37,7 +37,6 @@ struct Plan {
 Plan make_plan(int kblocks, int ntiles, int nqb, int num_sms) {
   Plan pl{};
   // keep the query block resident when it fits next to a >=3-stage ring
-  size_t a_bytes = size_t(kblocks) * kABlockBytes;
   if (tile_smem_bytes(kblocks, 1, 3) <= kMaxSmem) {
     pl.a_resident = 1;
     int st = 3;
@@ -49,7 +48,6 @@ Plan make_plan(int kblocks, int ntiles, int nqb, int num_sms) {
     while (st < 6 && tile_smem_bytes(kblocks, 0, st + 1) <= kMaxSmem) ++st;
     pl.stages = st;
   }
-  (void)a_bytes;
   // ~16+ units per CTA for balance; at least 1 tile per unit
   const int64_t total_tiles = int64_t(ntiles) * nqb;
   int64_t tpu = total_tiles / (int64_t(num_sms) * 16);
@@ -91,7 +89,7 @@ CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint3
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms) {
   const int ntiles = int(n_pad / kBN);
   const Plan pl = make_plan(1, ntiles, nq_pad / kBM, num_sms);
-  return size_t(pl.ncc) * 2 * size_t(nq_pad);
+  return size_t(pl.ncc) * kColGroups * size_t(nq_pad);
 }
 
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {

@@ -8,15 +8,16 @@
 //   warp 1      MMA issuer (one lane): tcgen05.mma kind::f16, M=128 N=256,
 //               fp32 accumulator in TMEM, 2 accumulator buffers x 256 cols.
 //   warp 2      TMEM allocator.
-//   warps 4-11  epilogue: warp w reads TMEM lane quarter (w%4) and column half
-//               (w-4)/4 with tcgen05.ld; each thread owns ONE query row, so the
-//               per-query row sum needs no shuffles.
+//   warps 4-19  epilogue: warp w reads TMEM lane quarter (w%4) and column
+//               quarter (w-4)/4 (64 columns) with tcgen05.ld; each thread owns
+//               ONE query row, so the per-query row sum needs no shuffles.
+//               The tile's 256 column norms are TMA-staged in smem (1 KB ring).
 // The S = Q X^T tile never leaves the SM: the epilogue turns it into
 //   d2 = |q|^2 + |x|^2 - 2 S          (fp32, exact for the integer encoding)
 // and then, by mode,
 //   KDE_GAUSS  sum exp2(d2 * -log2e/(2h^2))       -> naive_kde gaussian
 //   KDE_EXP    sum exp2(sqrt(d2) * -log2e/h)       -> naive_kde exponential
-//   TILEMIN    min d2 over each 128-column half tile (k-NN threshold pass)
+//   TILEMIN    min d2 over each 64-column quarter tile (k-NN threshold pass)
 //   FILTER     append (d2, col) when d2 <= tau[row]  (k-NN candidate pass)
 // Reference: naive_kde estimators.py:144-149 -> batch_sqdist distance.py:69-85
 // -> kernel_from_distance kernels.py:65-83 -> .mean(axis=1); brute_force_knn
@@ -36,9 +37,11 @@ constexpr int kBN = 256;           // dataset columns per tile (UMMA N)
 constexpr int kBK = 64;            // K elements per block (128 B rows, SWIZZLE_128B)
 constexpr int kABlockBytes = kBM * kBK * 2;   // 16 KB
 constexpr int kBBlockBytes = kBN * kBK * 2;   // 32 KB
-constexpr int kThreads = 384;      // 12 warps
 constexpr int kEpiWarp0 = 4;
-constexpr int kNumEpiWarps = 8;
+constexpr int kNumEpiWarps = 16;
+constexpr int kThreads = 32 * (kEpiWarp0 + kNumEpiWarps);  // 640
+constexpr int kColGroups = 4;      // 64-column groups per tile (one per epilogue warp of a lane quarter)
+constexpr int kXnSlots = 4;        // column-norm staging ring (1 KB per tile)
 constexpr uint32_t kTmemCols = 512;  // 2 accumulator buffers x 256 fp32 columns
 
 struct TileParams {
@@ -57,8 +60,8 @@ struct TileParams {
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
   float negc;              // exp2 scale: gaussian -log2e/(2h^2); exponential -log2e/h
-  double* part;            // KDE: [ncc*2][nq_pad] partial sums
-  float* tmin;             // TILEMIN: [ntiles*2][nq_pad]
+  double* part;            // KDE: [ncc*kColGroups][nq_pad] partial sums
+  float* tmin;             // TILEMIN: [ntiles*kColGroups][nq_pad]
   const float* tau;        // FILTER: [nq_pad] thresholds
   uint32_t* cand_cnt;      // FILTER: [nq_pad]
   unsigned long long* cand;  // FILTER: [nq_pad][cap] keys (f32 bits << 32 | col)
@@ -69,7 +72,67 @@ struct TileParams {
 __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages) {
   size_t a = a_resident ? size_t(kblocks) * kABlockBytes : size_t(stages) * kABlockBytes;
   size_t b = size_t(stages) * kBBlockBytes;
-  return 1024 /*align slack*/ + a + b + 256 /*barriers*/;
+  return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + 512 /*barriers*/;
+}
+
+template <int MODE>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* __restrict__ xs_smem, float qn,
+                                          float m2s, float negc, float tau, bool full, int64_t cbase, int64_t n,
+                                          float& s0, float& s1, float& s2, float& s3, float& mn, const TileParams& p,
+                                          int row) {
+  const float4* x4 = reinterpret_cast<const float4*>(xs_smem);
+  if (full) {
+#pragma unroll
+    for (int j4 = 0; j4 < 8; ++j4) {
+      const float4 xv = x4[j4];
+      const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = j4 * 4 + jj;
+        const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs[jj]);
+        if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
+          float e;
+          if constexpr (MODE == MODE_KDE_GAUSS) e = ex2_approx(d2 * negc);
+          else e = ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
+          if (jj == 0) s0 += e; else if (jj == 1) s1 += e; else if (jj == 2) s2 += e; else s3 += e;
+        } else if constexpr (MODE == MODE_TILEMIN) {
+          mn = fminf(mn, d2);
+        } else {
+          if (d2 <= tau) {
+            const int slot = p.row_map ? p.row_map[row] : row;
+            const uint32_t pos = atomicAdd(&p.cand_cnt[slot], 1u);
+            if (pos < uint32_t(p.cap))
+              p.cand[size_t(slot) * p.cap + pos] =
+                  (static_cast<unsigned long long>(__float_as_uint(fmaxf(d2, 0.f))) << 32) |
+                  static_cast<unsigned long long>(cbase + j);
+          }
+        }
+      }
+    }
+  } else {
+    const int lim = int(min(int64_t(32), n - cbase));
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j >= lim) continue;
+      const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs_smem[j]);
+      if constexpr (MODE == MODE_KDE_GAUSS) {
+        s0 += ex2_approx(d2 * negc);
+      } else if constexpr (MODE == MODE_KDE_EXP) {
+        s0 += ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
+      } else if constexpr (MODE == MODE_TILEMIN) {
+        mn = fminf(mn, d2);
+      } else {
+        if (d2 <= tau) {
+          const int slot = p.row_map ? p.row_map[row] : row;
+          const uint32_t pos = atomicAdd(&p.cand_cnt[slot], 1u);
+          if (pos < uint32_t(p.cap))
+            p.cand[size_t(slot) * p.cap + pos] =
+                (static_cast<unsigned long long>(__float_as_uint(fmaxf(d2, 0.f))) << 32) |
+                static_cast<unsigned long long>(cbase + j);
+        }
+      }
+    }
+  }
 }
 
 template <int MODE>
@@ -81,14 +144,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stages = p.stages;
   uint8_t* smemA = smem;
   uint8_t* smemB = smem + (p.a_resident ? size_t(p.kblocks) * kABlockBytes : size_t(stages) * kABlockBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smemB + size_t(stages) * kBBlockBytes);
+  float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBBlockBytes);  // [kXnSlots][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smemX + kXnSlots * kBN);
   uint64_t* full_bar = bars;                 // [stages]
   uint64_t* empty_bar = bars + stages;       // [stages]
   uint64_t* tfull_bar = bars + 2 * stages;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;      // [2]
   uint64_t* afull_bar = tempty_bar + 2;      // [1]
   uint64_t* aempty_bar = afull_bar + 1;      // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty_bar + 1);
+  uint64_t* xfull_bar = aempty_bar + 1;      // [kXnSlots]
+  uint64_t* xempty_bar = xfull_bar + kXnSlots;  // [kXnSlots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty_bar + kXnSlots);
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
@@ -107,6 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(afull_bar, 1);
     mbar_init(aempty_bar, 1);
+    for (int x = 0; x < kXnSlots; ++x) {
+      mbar_init(&xfull_bar[x], 1);
+      mbar_init(&xempty_bar[x], kNumEpiWarps);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -123,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int uiter = 0;
+      uint32_t titer = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++uiter) {
         const int qb = u % p.nqb, cc = u / p.nqb;
         const int t0 = cc * p.tiles_per_unit;
@@ -133,8 +204,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < p.kblocks; ++kb)
             tma_load_2d(smemA + size_t(kb) * kABlockBytes, &tmapA, afull_bar, kb * kBK, qb * kBM, pol_a);
         }
-        for (int t = t0; t < t1; ++t) {
+        for (int t = t0; t < t1; ++t, ++titer) {
           const int col0 = t * p.tile_stride * kBN;
+          {  // column norms of this tile -> smem ring slot
+            const uint32_t xs = titer % kXnSlots;
+            mbar_wait(&xempty_bar[xs], ((titer / kXnSlots) & 1) ^ 1);
+            mbar_arrive_expect_tx(&xfull_bar[xs], kBN * 4);
+            bulk_load(smemX + xs * kBN, p.xn + col0, kBN * 4, &xfull_bar[xs]);
+          }
           for (int kb = 0; kb < p.kblocks; ++kb) {
             mbar_wait(&empty_bar[stage], phase ^ 1);
             if (p.a_resident) {
@@ -194,82 +271,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== epilogue =====================
     const int ew = int(warp) - kEpiWarp0;
     const int quarter = int(warp & 3);
-    const int half = ew >> 2;
+    const int cg = ew >> 2;  // 64-column group of the tile
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t titer = 0;
+    const float m2s = *p.m2s;
+    const float negc = p.negc;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       const int qb = u % p.nqb, cc = u / p.nqb;
       const int t0 = cc * p.tiles_per_unit;
       const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
       const int row = qb * kBM + quarter * 32 + int(lane);
       const float qn = p.qn[row];
-      const float m2s = *p.m2s;
       float tau = 0.f;
       if constexpr (MODE == MODE_FILTER) tau = p.tau[row];
       double usum = 0.0;
-      for (int t = t0; t < t1; ++t) {
+      for (int t = t0; t < t1; ++t, ++titer) {
+        const uint32_t xs = titer % kXnSlots;
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
-        const int64_t colh = int64_t(t) * p.tile_stride * kBN + half * 128;
-        const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN + half * 128);
+        const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN + cg * 64);
+        uint32_t r0[32], r1[32];
+        tmem_ld32(taddr, r0);
+        tmem_ld32(taddr + 32u, r1);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
+        const int64_t cbase = int64_t(t) * p.tile_stride * kBN + cg * 64;
+        const float* xsm = smemX + xs * kBN + cg * 64;
+        const bool full = cbase + 64 <= p.n;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         float mn = __int_as_float(0x7f800000);
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + uint32_t(c * 32), r);
-          tmem_ld_wait();
-          if (c == 3) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-          }
-          const int64_t cbase = colh + c * 32;
-          const float4* xv4 = reinterpret_cast<const float4*>(p.xn + cbase);
-          const bool full = cbase + 32 <= p.n;
-#pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 xv = __ldg(xv4 + j4);
-            const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const int j = j4 * 4 + jj;
-              const float u2 = qn + xs[jj];
-              float d2 = fmaf(__uint_as_float(r[j]), m2s, u2);
-              const bool valid = full || (cbase + j < p.n);
-              if constexpr (MODE == MODE_KDE_GAUSS) {
-                float e = ex2_approx(d2 * p.negc);
-                e = valid ? e : 0.f;
-                if (jj == 0) s0 += e; else if (jj == 1) s1 += e; else if (jj == 2) s2 += e; else s3 += e;
-              } else if constexpr (MODE == MODE_KDE_EXP) {
-                float e = ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * p.negc);
-                e = valid ? e : 0.f;
-                if (jj == 0) s0 += e; else if (jj == 1) s1 += e; else if (jj == 2) s2 += e; else s3 += e;
-              } else if constexpr (MODE == MODE_TILEMIN) {
-                mn = valid ? fminf(mn, d2) : mn;
-              } else {  // FILTER
-                if (valid && d2 <= tau) {
-                  const int slot = p.row_map ? p.row_map[row] : row;
-                  const uint32_t pos = atomicAdd(&p.cand_cnt[slot], 1u);
-                  if (pos < uint32_t(p.cap)) {
-                    const uint32_t key = __float_as_uint(fmaxf(d2, 0.f));
-                    p.cand[size_t(slot) * p.cap + pos] =
-                        (static_cast<unsigned long long>(key) << 32) | static_cast<unsigned long long>(cbase + j);
-                  }
-                }
-              }
-            }
-          }
-        }
+        epi_chunk<MODE>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, s0, s1, s2, s3, mn, p, row);
+        epi_chunk<MODE>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n, s0, s1, s2, s3, mn, p, row);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
           usum += double((s0 + s1) + (s2 + s3));
         } else if constexpr (MODE == MODE_TILEMIN) {
-          p.tmin[(size_t(t) * 2 + half) * p.nq_pad + row] = mn;
+          p.tmin[(size_t(t) * kColGroups + cg) * p.nq_pad + row] = mn;
         }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
-        p.part[(size_t(cc) * 2 + half) * p.nq_pad + row] = usum;
+        p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
       }
     }
   }
