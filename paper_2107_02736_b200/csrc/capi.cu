@@ -70,6 +70,7 @@ dk_status guard(F&& f) {
     return DK_OK;
   } catch (const Error& e) {
     set_error(e.msg);
+    cudaGetLastError();  // do not leak a non-sticky error into the next call
     return e.code;
   } catch (const std::bad_alloc&) {
     set_error("host allocation failed");
@@ -323,6 +324,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     }
     // overflow: tighten tau on the stored candidates and sweep those queries again
     int32_t* ovf = at<int32_t>(h->ws, o_ovf);
+    std::vector<int32_t> unresolved;  // still overflowing after two tightenings -> exact scan
     for (int iter = 0;; ++iter) {
       DK_CUDA(cudaMemsetAsync(ovf + bpad, 0, sizeof(int32_t), s));
       launch_tau_from_cand(cand, cnt, kp.cap, bn, kp.kprime, tau, ovf, ovf + bpad, s);
@@ -330,10 +332,13 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       DK_CUDA(cudaMemcpyAsync(&novf, ovf + bpad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaStreamSynchronize(s));
       if (novf == 0) break;
-      if (iter >= 8) throw Error{DK_EINEXACT, "k-NN candidate overflow did not converge"};
       std::vector<int32_t> list(static_cast<size_t>(novf));
       DK_CUDA(cudaMemcpy(list.data(), ovf, size_t(novf) * sizeof(int32_t), cudaMemcpyDeviceToHost));
       std::sort(list.begin(), list.end());
+      if (iter >= 2) {  // massive ties at the threshold: tightening cannot shrink the set
+        unresolved = list;
+        break;
+      }
       DK_CUDA(cudaMemcpyAsync(ovf, list.data(), size_t(novf) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
       // compact the overflowing queries (+ their tightened tau), reset their counters
       double* Qc = at<double>(h->ws, o_Qc);
@@ -373,9 +378,10 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     std::vector<int32_t> st(static_cast<size_t>(bn));
     DK_CUDA(cudaMemcpyAsync(st.data(), status, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     DK_CUDA(cudaStreamSynchronize(s));
-    std::vector<int32_t> fail;
+    std::vector<int32_t> fail = unresolved;
     for (int64_t i = 0; i < bn; ++i)
-      if (st[size_t(i)]) fail.push_back(int32_t(i));
+      if (st[size_t(i)] && !std::binary_search(unresolved.begin(), unresolved.end(), int32_t(i)))
+        fail.push_back(int32_t(i));
     if (!fail.empty()) {
       DK_CUDA(cudaMemcpyAsync(ovf, fail.data(), fail.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
       launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, ovf, int32_t(fail.size()), k, idx_d + b0 * k,
@@ -738,7 +744,7 @@ dk_status dk_kernel_values(int32_t family, double bandwidth, const double* dist,
     const bool din = is_device_ptr(dist), dout = is_device_ptr(out);
     double *dd = nullptr, *od = nullptr;
     uint32_t* bad = nullptr;
-    DK_CUDA(cudaMalloc(&bad, sizeof(uint32_t) + 2 * size_t(count) * sizeof(double)));
+    DK_CUDA(cudaMalloc(&bad, 2 * sizeof(uint32_t) + 2 * size_t(count) * sizeof(double)));
     dd = reinterpret_cast<double*>(bad + 2);
     od = dd + count;
     DK_CUDA(cudaMemsetAsync(bad, 0, sizeof(uint32_t), s));
