@@ -164,6 +164,11 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family,
  * launching stream) and its algorithmic work. */
 dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* bytes);
 dk_status dk_set_profiling(dk_handle h, int32_t on);
+/* k-NN diagnostics accumulated on this handle (counted when DK_KNN_STATS is set
+ * in the environment at fit time; fallbacks always): queries, total and max
+ * candidates per query, queries that took the exact-scan fallback. */
+dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t* cand_max,
+                       int64_t* fallbacks);
 /* Number of this library's kernels launched by the last API call. */
 dk_status dk_last_launch_count(dk_handle h, int64_t* count);
 

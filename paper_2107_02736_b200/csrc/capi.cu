@@ -5,6 +5,7 @@
 // operand-encoding choice, k-NN batching/certificates and profiling events.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <limits>
@@ -133,9 +134,12 @@ const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
   for (float v : xn) mx = std::max(mx, v);
   e.xn_max = mx;
   const double u = std::ldexp(1.0, -24);
-  if (mode == 0) e.eps_rel = 0.f;                                           // bit-exact integers
-  else if (mode == 1) e.eps_rel = float(8 * u + double(e.Kp) * u + 6 * u);  // hi/lo split + fp32 sums
-  else e.eps_rel = float(std::ldexp(1.0, -9) + double(e.Kp) * u);           // single fp16 pass
+  // |approx d2 - d2| <= eps_rel * (|q|^2 + max|x|^2): operand rounding (2u_op |q||x|, u_op the
+  // unit roundoff of the encoding), fp32 accumulation over Kp terms, fp32 epilogue (norm
+  // rounding, the add and the fma), using 2|q||x| <= |q|^2 + |x|^2.
+  if (mode == 0) e.eps_rel = 0.f;                                                        // exact integers
+  else if (mode == 1) e.eps_rel = float(1.01 * (4.0 * std::ldexp(1.0, -22) + double(e.Kp + 4) * u));  // split3
+  else e.eps_rel = float(1.01 * (2.002 * std::ldexp(1.0, -11) + double(e.Kp + 4) * u));             // fp16
   e.tmap = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN));
   e.mode = mode;
   return e;
@@ -224,46 +228,59 @@ struct LaunchCount {
 };
 
 // ------------------------------------------------------------------ k-NN core
+constexpr int32_t kKnnCap = 8192;  // candidates per query before the exact-scan fallback
+
 struct KnnPlan {
-  int32_t kprime = 0, stride = 1, nseg = 0, cap = 0, batch = 0;
+  int32_t seg_tiles = 1, nseg = 0, cap = 0, batch = 0;
   bool tau_inf = false;
 };
 
 KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
   KnnPlan p;
-  p.kprime = int32_t(std::min<int64_t>(h->n, int64_t(k) + std::max<int32_t>(32, k / 4)));
   const int64_t ntiles = h->n_pad / kBN;
-  if (h->n <= 4096 || kColGroups * ntiles < p.kprime) {
-    p.tau_inf = true;
+  const int64_t target = std::clamp<int64_t>(4 * int64_t(k), 256, 2048);  // ~4k segments: tight tau
+  if (h->n <= kKnnCap) {
+    p.tau_inf = true;  // every row is a candidate
     p.cap = int32_t(h->n);
-    p.stride = 1;
-    p.nseg = 0;
-  } else {
-    const int64_t target = std::clamp<int64_t>(16 * int64_t(p.kprime), 2048, 8192);
-    p.stride = int32_t(std::max<int64_t>(1, (kColGroups * ntiles + target - 1) / target));
-    while (p.stride > 1 && kColGroups * ((ntiles + p.stride - 1) / p.stride) < 4 * p.kprime) --p.stride;
-    p.nseg = int32_t(kColGroups * ((ntiles + p.stride - 1) / p.stride));
-    int64_t cap = 2048;
-    while (cap < 3 * int64_t(p.stride) * p.kprime && cap < 16384) cap <<= 1;
-    p.cap = int32_t(cap);
+  } else if (ntiles >= target) {
+    p.seg_tiles = int32_t((ntiles + target - 1) / target);
+    p.nseg = int32_t((ntiles + p.seg_tiles - 1) / p.seg_tiles);
+    p.cap = kKnnCap;
+  } else {  // one segment per 64-column group of every tile
+    p.seg_tiles = 0;
+    p.nseg = int32_t(ntiles * kColGroups);
+    p.cap = kKnnCap;
   }
-  const int64_t budget = int64_t(1) << 31;  // bytes of candidate storage per batch
+  if (!p.tau_inf && p.nseg < k) {  // cannot bound the k-th distance: keep every row
+    p.tau_inf = true;
+    p.seg_tiles = 1;
+    p.nseg = 0;
+    p.cap = int32_t(std::min<int64_t>(h->n, int64_t(1) << 20));
+  }
+  const int64_t budget = int64_t(1) << 30;  // bytes of candidate storage per batch
   int64_t b = budget / (int64_t(p.cap) * 8 + int64_t(p.nseg) * 4 + 64);
   b = std::max<int64_t>(kBM, std::min<int64_t>(16384, b)) / kBM * kBM;
   p.batch = int32_t(std::min<int64_t>(b, round_up(nq, kBM)));
   return p;
 }
 
+// encoding for the k-NN sweeps: exact integers when possible, else single-pass
+// fp16 (its error is bounded by eps_rel and absorbed by the threshold), unless
+// the caller pinned split3.
+int knn_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cudaStream_t s) {
+  if (h->precision == DK_PREC_SPLIT3) return 1;
+  const int m = choose_mode(h, Qd, nq, flags, s);
+  return m == 0 ? 0 : 2;
+}
+
 // k-NN for nq queries already on the device; idx/d2 outputs on the device.
 void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t* idx_d, double* d2_d,
                 cudaStream_t s, size_t ws_off_base) {
   const KnnPlan kp = plan_knn(h, k, nq);
-  // encoding: decided once for the whole query set
   Plan pl;
   pl.off = ws_off_base;
   const size_t o_flags = pl.add<uint32_t>(4);
-  uint32_t* flags = at<uint32_t>(h->ws, o_flags);
-  const int mode = choose_mode(h, Qd, nq, flags, s);
+  const int mode = knn_mode(h, Qd, nq, at<uint32_t>(h->ws, o_flags), s);
   const Encoding& e = ensure_encoding(h, mode, s);
   const int32_t bpad = kp.batch;
   const size_t o_A = pl.add<__half>(size_t(bpad) * e.Kp);
@@ -274,12 +291,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
   const size_t o_cnt = pl.add<uint32_t>(bpad);
   const size_t o_cand = pl.add<unsigned long long>(size_t(kp.cap) * bpad);
   const size_t o_status = pl.add<int32_t>(bpad);
-  const size_t o_ovf = pl.add<int32_t>(bpad + 1);
-  const size_t o_Qc = pl.add<double>(size_t(bpad) * h->d);
-  const size_t o_A2 = pl.add<__half>(size_t(bpad) * e.Kp);
-  const size_t o_qn2 = pl.add<float>(bpad);
-  const size_t o_tau2 = pl.add<float>(bpad);
-  const size_t o_scal2 = pl.add<float>(4);
+  const size_t o_list = pl.add<int32_t>(bpad);
   if (pl.off > h->ws.cap) throw Error{DK_ECUDA, "internal: k-NN workspace under-reserved"};
   const float inf = std::numeric_limits<float>::infinity();
   for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
@@ -294,16 +306,19 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     if (kp.tau_inf) {
       launch_fill_float(tau, bn, inf, s);
     } else {
+      float* tmin = at<float>(h->ws, o_tmin);
+      launch_fill_float(tmin, int64_t(kp.nseg) * bn_pad, inf, s);
       SweepArgs a{};
       a.mode = MODE_TILEMIN;
       a.qop = &q;
       a.enc = &e;
       a.n = h->n;
       a.n_pad = h->n_pad;
-      a.tile_stride = kp.stride;
-      a.tmin = at<float>(h->ws, o_tmin);
+      a.tile_stride = 1;
+      a.seg_tiles = kp.seg_tiles;
+      a.tmin = tmin;
       launch_sweep(a, h->num_sms, s);
-      launch_tau_from_tmin(a.tmin, kp.nseg, bn_pad, bn, kp.kprime, tau, s);
+      launch_tau_from_tmin(tmin, kp.nseg, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau, s);
     }
     launch_fill_float(tau + bn, bn_pad - bn, -inf, s);
     DK_CUDA(cudaMemsetAsync(cnt, 0, size_t(bn_pad) * sizeof(uint32_t), s));
@@ -322,72 +337,33 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       ProfScope ps(h, s, 2.0 * double(h->d) * double(bn) * double(h->n), double(h->n_pad) * e.Kp * 2);
       launch_sweep(a, h->num_sms, s);
     }
-    // overflow: tighten tau on the stored candidates and sweep those queries again
-    int32_t* ovf = at<int32_t>(h->ws, o_ovf);
-    std::vector<int32_t> unresolved;  // still overflowing after two tightenings -> exact scan
-    for (int iter = 0;; ++iter) {
-      DK_CUDA(cudaMemsetAsync(ovf + bpad, 0, sizeof(int32_t), s));
-      launch_tau_from_cand(cand, cnt, kp.cap, bn, kp.kprime, tau, ovf, ovf + bpad, s);
-      int32_t novf = 0;
-      DK_CUDA(cudaMemcpyAsync(&novf, ovf + bpad, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (h->knn_stats) {
+      std::vector<uint32_t> c(static_cast<size_t>(bn));
+      DK_CUDA(cudaMemcpyAsync(c.data(), cnt, size_t(bn) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaStreamSynchronize(s));
-      if (novf == 0) break;
-      std::vector<int32_t> list(static_cast<size_t>(novf));
-      DK_CUDA(cudaMemcpy(list.data(), ovf, size_t(novf) * sizeof(int32_t), cudaMemcpyDeviceToHost));
-      std::sort(list.begin(), list.end());
-      if (iter >= 2) {  // massive ties at the threshold: tightening cannot shrink the set
-        unresolved = list;
-        break;
+      for (uint32_t v : c) {
+        h->knn_cand_sum += v;
+        h->knn_cand_max = std::max<int64_t>(h->knn_cand_max, v);
       }
-      DK_CUDA(cudaMemcpyAsync(ovf, list.data(), size_t(novf) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      // compact the overflowing queries (+ their tightened tau), reset their counters
-      double* Qc = at<double>(h->ws, o_Qc);
-      float* tau2 = at<float>(h->ws, o_tau2);
-      std::vector<float> tau_h(static_cast<size_t>(bn));
-      DK_CUDA(cudaMemcpyAsync(tau_h.data(), tau, size_t(bn) * sizeof(float), cudaMemcpyDeviceToHost, s));
-      DK_CUDA(cudaStreamSynchronize(s));
-      const int32_t nc_pad = int32_t(round_up(novf, kBM));
-      std::vector<float> tau2_h(size_t(nc_pad), -inf);
-      for (int32_t i = 0; i < novf; ++i) {
-        DK_CUDA(cudaMemcpyAsync(Qc + size_t(i) * h->d, Qb + size_t(list[i]) * h->d, size_t(h->d) * sizeof(double),
-                                cudaMemcpyDeviceToDevice, s));
-        tau2_h[i] = tau_h[list[i]];
-        DK_CUDA(cudaMemsetAsync(cnt + list[i], 0, sizeof(uint32_t), s));
-      }
-      DK_CUDA(cudaMemcpyAsync(tau2, tau2_h.data(), size_t(nc_pad) * sizeof(float), cudaMemcpyHostToDevice, s));
-      QueryOperand qc = encode_queries(h, e, Qc, novf, nc_pad, at<__half>(h->ws, o_A2), at<float>(h->ws, o_qn2),
-                                       at<float>(h->ws, o_scal2), s);
-      SweepArgs a{};
-      a.mode = MODE_FILTER;
-      a.qop = &qc;
-      a.enc = &e;
-      a.n = h->n;
-      a.n_pad = h->n_pad;
-      a.tile_stride = 1;
-      a.tau = tau2;
-      a.cand_cnt = cnt;
-      a.cand = cand;
-      a.cap = kp.cap;
-      a.row_map = ovf;
-      launch_sweep(a, h->num_sms, s);
-      DK_CUDA(cudaStreamSynchronize(s));
+      h->knn_queries += bn;
     }
     int32_t* status = at<int32_t>(h->ws, o_status);
-    launch_select_rerank(h->X, h->global_offset, h->d, Qb, bn, k, kp.kprime, cand, cnt, kp.cap, tau, q.qn, e.xn_max,
-                         e.eps_rel, idx_d + b0 * k, d2_d + b0 * k, status, s);
+    launch_select_rerank(h->X, h->global_offset, h->d, Qb, bn, k, cand, cnt, kp.cap, q.qn, e.xn_max, e.eps_rel,
+                         idx_d + b0 * k, d2_d + b0 * k, status, s);
     std::vector<int32_t> st(static_cast<size_t>(bn));
     DK_CUDA(cudaMemcpyAsync(st.data(), status, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     DK_CUDA(cudaStreamSynchronize(s));
-    std::vector<int32_t> fail = unresolved;
+    std::vector<int32_t> fail;
     for (int64_t i = 0; i < bn; ++i)
-      if (st[size_t(i)] && !std::binary_search(unresolved.begin(), unresolved.end(), int32_t(i)))
-        fail.push_back(int32_t(i));
+      if (st[size_t(i)]) fail.push_back(int32_t(i));
     if (!fail.empty()) {
-      DK_CUDA(cudaMemcpyAsync(ovf, fail.data(), fail.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, ovf, int32_t(fail.size()), k, idx_d + b0 * k,
-                                d2_d + b0 * k, s);
+      int32_t* list = at<int32_t>(h->ws, o_list);
+      DK_CUDA(cudaMemcpyAsync(list, fail.data(), fail.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, list, int32_t(fail.size()), k,
+                                idx_d + b0 * k, d2_d + b0 * k, s);
       DK_CUDA(cudaStreamSynchronize(s));
     }
+    h->knn_fallbacks += int64_t(fail.size());
   }
 }
 
@@ -404,12 +380,7 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
   pl.add<uint32_t>(kp.batch);
   pl.add<unsigned long long>(size_t(kp.cap) * kp.batch);
   pl.add<int32_t>(kp.batch);
-  pl.add<int32_t>(kp.batch + 1);
-  pl.add<double>(size_t(kp.batch) * h->d);
-  pl.add<__half>(size_t(kp.batch) * Kp_max);
-  pl.add<float>(kp.batch);
-  pl.add<float>(kp.batch);
-  pl.add<float>(4);
+  pl.add<int32_t>(kp.batch);
   return pl.off + 4096;
 }
 
@@ -458,6 +429,7 @@ dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts, 
     h->global_offset = opts ? opts->global_offset : 0;
     h->global_n = (opts && opts->global_n > 0) ? opts->global_n : n;
     h->precision = opts ? opts->precision : DK_PREC_AUTO;
+    h->knn_stats = std::getenv("DK_KNN_STATS") != nullptr;
     DK_REQUIRE(h->precision >= 0 && h->precision <= 2, "unknown precision mode");
     DK_REQUIRE(h->global_offset >= 0 && h->global_offset + n <= h->global_n, "shard outside [0, global_n)");
     cudaStream_t s = nullptr;
@@ -850,6 +822,16 @@ dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* byte
     if (ms) *ms = h->prof_used ? tot / double(h->prof_used) : 0.0;
     if (flops) *flops = h->last_flops;
     if (bytes) *bytes = h->last_bytes;
+  });
+}
+
+dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t* cand_max, int64_t* fallbacks) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    if (queries) *queries = h->knn_queries;
+    if (cand_sum) *cand_sum = h->knn_cand_sum;
+    if (cand_max) *cand_max = h->knn_cand_max;
+    if (fallbacks) *fallbacks = h->knn_fallbacks;
   });
 }
 

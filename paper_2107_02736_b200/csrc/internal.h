@@ -37,6 +37,18 @@ extern std::atomic<long long> g_launches;  // kernels launched by this library
     DK_CUDA(cudaGetLastError());                  \
   } while (0)
 
+// Opt a kernel into `bytes` of dynamic shared memory (only ever raises the limit).
+template <class K>
+inline void set_dynamic_smem(K* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  cudaFuncAttributes fa;
+  DK_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  if (size_t(fa.maxDynamicSharedSizeBytes) >= bytes) return;
+  if (bytes + fa.sharedSizeBytes > 232448)
+    throw Error{DK_EINVAL, "kernel needs " + std::to_string(bytes) + " B of shared memory (> 227 KB)"};
+  DK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
 #define DK_REQUIRE(cond, msg)                          \
   do {                                                 \
     if (!(cond)) throw ::dk::Error{DK_EINVAL, (msg)};  \
@@ -95,6 +107,9 @@ struct dk_dataset {
   bool profiling = false;
   double last_flops = 0, last_bytes = 0;
   int64_t launches = 0;
+  // k-NN diagnostics (DK_KNN_STATS=1 in the environment): candidates per query, fallbacks
+  bool knn_stats = false;
+  int64_t knn_queries = 0, knn_cand_sum = 0, knn_cand_max = 0, knn_fallbacks = 0;
 };
 
 namespace dk {
@@ -140,7 +155,7 @@ struct SweepArgs {
   uint32_t* cand_cnt;
   unsigned long long* cand;
   int32_t cap;
-  const int32_t* row_map;
+  int32_t seg_tiles;          // TILEMIN: tiles per segment
 };
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms);  // doubles needed for KDE partials
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
@@ -162,15 +177,13 @@ void launch_eval_rows(const float* X, int64_t n_local, int64_t global_offset, in
                       double* out, cudaStream_t s);
 
 // k-NN selection
-void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t kprime, float* tau,
-                          cudaStream_t s);
+void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
+                          float xn_max, float eps_rel, float* tau, cudaStream_t s);
 void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s);
 void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
-                          int32_t kprime, const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap,
-                          const float* tau, const float* qn, float xn_max, float eps_rel, int64_t* idx_out,
-                          double* d2_out, int32_t* status, cudaStream_t s);
-void launch_tau_from_cand(const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, int64_t nq,
-                          int32_t kprime, float* tau, int32_t* overflow_list, int32_t* n_overflow, cudaStream_t s);
+                          const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
+                          float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* status,
+                          cudaStream_t s);
 void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
                                const int32_t* qlist, int32_t nlist, int32_t k, int64_t* idx_out, double* d2_out,
                                cudaStream_t s);

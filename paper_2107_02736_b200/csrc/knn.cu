@@ -4,18 +4,21 @@
 // _smallest_k (:82-102): the k smallest fp64 squared distances, ties broken by
 // the lower row index, sorted by (d2, idx); NeighborList invariants (:49-67).
 //
-// Pipeline per query batch (host side in capi.cu):
-//   1. TILEMIN sweep over every S-th tile: min approx d2 per 128-column segment.
-//      tau_q = K'-th smallest segment minimum is an UPPER bound on the K'-th
-//      smallest approx d2 of the whole set (each minimum is a distinct point).
-//   2. FILTER sweep: append every (approx d2, col) with approx d2 <= tau_q.
-//      Overflowing queries tighten tau to the K'-th of their first `cap`
-//      candidates (still a valid bound) and are swept again.
-//   3. select_rerank: K' smallest candidates by approx d2 -> exact fp64 direct
-//      difference d2 -> sort by (d2, idx) -> top k.  Certificate: with
-//      |approx - exact| <= eps, every non-selected point has exact d2 >
-//      boundary - eps; the set is proven when D_k < boundary - eps.
-//   4. queries whose certificate fails take an exact fp64 full scan.
+// Pipeline per query batch (host side in capi.cu).  Distances are computed on
+// the tensor-core tile from an operand encoding whose error is bounded:
+// |d2_approx - d2| <= eps_q = eps_rel * (|q|^2 + max|x|^2) (eps_rel = 0 for the
+// exact integer encoding, ~1e-3 for single-pass fp16).
+//   1. TILEMIN sweep: min approx d2 per segment of `seg_tiles` tiles (atomicMin).
+//      The k-th smallest segment minimum t_q is >= the k-th smallest approx d2
+//      (segments hold distinct points), so tau_q = t_q + 2 eps_q bounds the
+//      approx d2 of every point whose EXACT d2 is <= the exact k-th distance.
+//   2. FILTER sweep: keep every (approx d2, col) with approx d2 <= tau_q.  The
+//      candidate set provably contains all points at or inside the exact k-th
+//      distance, including every tie there.
+//   3. select_rerank: candidates sorted by approx d2, re-ranked exactly (fp64
+//      direct difference) in that order until the next approx d2 - eps_q
+//      exceeds the current exact k-th distance; output sorted by (d2, idx).
+//   4. queries whose candidate list overflowed take an exact fp64 full scan.
 #include <cfloat>
 
 #include "internal.h"
@@ -72,60 +75,31 @@ __host__ __device__ inline int pow2_ceil(int v) {
   return p;
 }
 
-// Streaming selection of the Kp smallest u64 keys out of `cnt` keys fetched by `get(i)`.
-// buf has B entries (B > Kp, both powers of two); on return buf[0..Kp) is sorted ascending.
-template <class Get>
-__device__ void stream_topk_u64(unsigned long long* buf, int B, int Kp, int64_t cnt, Get get) {
-  for (int i = threadIdx.x; i < Kp; i += blockDim.x) buf[i] = ~0ull;
-  const int chunk = B - Kp;
-  for (int64_t pos = 0; pos < cnt || pos == 0; pos += chunk) {
-    for (int i = threadIdx.x; i < chunk; i += blockDim.x) {
-      const int64_t src = pos + i;
-      buf[Kp + i] = src < cnt ? get(src) : ~0ull;
-    }
-    bitonic_u64(buf, B);
-    if (cnt == 0) break;
-  }
-}
-
-// tau_q = K'-th smallest tile-minimum (fp32 bits in the high word, segment id low)
+// tau_q = k-th smallest segment minimum + 2 eps_q
 __global__ void tau_from_tmin_kernel(const float* __restrict__ tmin, int32_t nseg, int32_t nq_pad, int64_t nq,
-                                     int32_t kprime, int32_t B, float* __restrict__ tau) {
+                                     int32_t k, int32_t B, const float* __restrict__ qn, float xn_max,
+                                     float eps_rel, float* __restrict__ tau) {
   extern __shared__ unsigned long long sbuf[];
   const int64_t q = blockIdx.x;
   if (q >= nq) return;
-  const int Kp = pow2_ceil(kprime);
-  stream_topk_u64(sbuf, B, Kp, nseg, [&](int64_t s) {
-    float v = tmin[size_t(s) * nq_pad + q];
-    v = fmaxf(v, 0.f);  // order-preserving on clamped values; tau only loosens
-    return (static_cast<unsigned long long>(__float_as_uint(v)) << 32) | static_cast<unsigned long long>(s);
-  });
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    unsigned long long key = ~0ull;
+    if (i < nseg) {
+      const float v = fmaxf(tmin[size_t(i) * nq_pad + q], 0.f);
+      key = (static_cast<unsigned long long>(__float_as_uint(v)) << 32) | static_cast<unsigned long long>(i);
+    }
+    sbuf[i] = key;
+  }
+  bitonic_u64(sbuf, B);
   if (threadIdx.x == 0) {
     float t = __int_as_float(0x7f800000);
-    if (nseg >= kprime) {
-      const unsigned long long kk = sbuf[kprime - 1];
-      t = __uint_as_float(uint32_t(kk >> 32));
-      if (t == 0.f) t = 0.f;
+    if (nseg >= k) {
+      const float v = __uint_as_float(uint32_t(sbuf[k - 1] >> 32));
+      const float eps = eps_rel * (qn[q] + xn_max);
+      t = v + 2.f * eps;
+      t = __fmul_ru(t, 1.0f + 2.4e-7f);  // absorb the rounding of the addition itself
     }
     tau[q] = t;
-  }
-}
-
-// queries whose candidate list overflowed: tau' = K'-th smallest of the stored `cap` keys
-__global__ void tau_from_cand_kernel(const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt,
-                                     int32_t cap, int64_t nq, int32_t kprime, int32_t B, float* __restrict__ tau,
-                                     int32_t* __restrict__ overflow_list, int32_t* __restrict__ n_overflow) {
-  extern __shared__ unsigned long long sbuf[];
-  const int64_t q = blockIdx.x;
-  if (q >= nq) return;
-  if (cnt[q] <= uint32_t(cap)) return;
-  const int Kp = pow2_ceil(kprime);
-  const unsigned long long* keys = cand + size_t(q) * cap;
-  stream_topk_u64(sbuf, B, Kp, cap, [&](int64_t i) { return keys[i]; });
-  if (threadIdx.x == 0) {
-    tau[q] = __uint_as_float(uint32_t(sbuf[kprime - 1] >> 32));
-    const int slot = atomicAdd(n_overflow, 1);
-    overflow_list[slot] = int32_t(q);
   }
 }
 
@@ -141,56 +115,65 @@ __device__ __forceinline__ double exact_d2_warp(const float* __restrict__ x, con
   return s;
 }
 
-// K' smallest candidates by approx key -> exact fp64 re-rank -> top k + certificate
+// exact re-rank of the candidates in increasing approx order with early termination
 __global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global_offset, int32_t d,
-                                     const double* __restrict__ Q, int64_t nq, int32_t k, int32_t kprime,
+                                     const double* __restrict__ Q, int64_t nq, int32_t k,
                                      const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt,
-                                     int32_t cap, const float* __restrict__ tau, const float* __restrict__ qn,
-                                     float xn_max, float eps_rel, int32_t B, int64_t* __restrict__ idx_out,
-                                     double* __restrict__ d2_out, int32_t* __restrict__ status) {
+                                     int32_t cap, const float* __restrict__ qn, float xn_max, float eps_rel,
+                                     int32_t B, int64_t* __restrict__ idx_out, double* __restrict__ d2_out,
+                                     int32_t* __restrict__ status) {
   extern __shared__ unsigned long long sbuf[];
   const int64_t q = blockIdx.x;
   if (q >= nq) return;
-  const int Kp = pow2_ceil(kprime);
-  const int64_t c = min(int64_t(cnt[q]), int64_t(cap));
+  const uint32_t craw = cnt[q];
+  if (craw > uint32_t(cap)) {  // overflow -> exact scan on the host's request
+    if (threadIdx.x == 0) status[q] = 1;
+    return;
+  }
+  const int c = int(craw);
+  const int Kp = max(32, pow2_ceil(k));
+  const int W = Kp;  // candidates re-ranked per round; Kp + W is a power of two for the bitonic merge
+  int Bc = 1;
+  while (Bc < c) Bc <<= 1;
+  Bc = max(Bc, 2);
   const unsigned long long* keys = cand + size_t(q) * cap;
-  stream_topk_u64(sbuf, B, Kp, c, [&](int64_t i) { return keys[i]; });
-  // exact re-rank of the first T entries
-  const int T = int(min(c, int64_t(kprime)));
-  Key128* ex = reinterpret_cast<Key128*>(sbuf + B);  // [Kp]
-  const double* qv = Q + size_t(q) * d;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int i = warp; i < Kp; i += nwarps) {
-    Key128 key{~0ull, ~0ull};
-    if (i < T) {
-      const unsigned long long col = sbuf[i] & 0xffffffffull;
-      const double dd = exact_d2_warp(X + size_t(col) * d, qv, d, lane);
-      key.hi = static_cast<unsigned long long>(__double_as_longlong(dd));
-      key.lo = col;
-    }
-    if (lane == 0) ex[i] = key;
-  }
-  bitonic_k128(ex, Kp);
-  if (threadIdx.x == 0) {
-    int ok = 1;
-    if (T < k) {
-      ok = 0;
-    } else {
-      const double Dk = __longlong_as_double(static_cast<long long>(ex[k - 1].hi));
-      const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max)) + 1e-30;
-      if (c > kprime) {
-        const double a = double(__uint_as_float(uint32_t(sbuf[kprime - 1] >> 32)));
-        ok = Dk < a - eps;
-      } else {
-        const double t = double(tau[q]);
-        ok = isinf(t) ? 1 : (Dk <= t - eps);
-      }
-    }
-    status[q] = ok ? 0 : 1;
-  }
+  for (int i = threadIdx.x; i < Bc; i += blockDim.x) sbuf[i] = i < c ? keys[i] : ~0ull;
+  bitonic_u64(sbuf, Bc);
+  Key128* top = reinterpret_cast<Key128*>(sbuf + B);  // [Kp + W]
+  for (int i = threadIdx.x; i < Kp + W; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
   __syncthreads();
+  const double* qv = Q + size_t(q) * d;
+  const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  __shared__ int s_stop;
+  for (int pos = 0; pos < c; pos += W) {
+    for (int i = warp; i < W; i += nwarps) {
+      Key128 key{~0ull, ~0ull};
+      if (pos + i < c) {
+        const unsigned long long col = sbuf[pos + i] & 0xffffffffull;
+        const double dd = exact_d2_warp(X + size_t(col) * d, qv, d, lane);
+        key.hi = static_cast<unsigned long long>(__double_as_longlong(dd));
+        key.lo = col;
+      }
+      if (lane == 0) top[Kp + i] = key;
+    }
+    bitonic_k128(top, Kp + W);
+    if (threadIdx.x == 0) {
+      int stop = 0;
+      if (pos + W < c && top[k - 1].hi != ~0ull) {
+        const double Dk = __longlong_as_double(static_cast<long long>(top[k - 1].hi));
+        const double next = double(__uint_as_float(uint32_t(sbuf[pos + W] >> 32)));
+        stop = (next - eps > Dk) ? 1 : 0;
+      }
+      s_stop = stop;
+    }
+    __syncthreads();
+    if (s_stop) break;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) status[q] = (c < k) ? 1 : 0;
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    const Key128 key = ex[i];
+    const Key128 key = top[i];
     idx_out[size_t(q) * k + i] = key.lo == ~0ull ? -1 : int64_t(key.lo) + global_offset;
     d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(key.hi));
   }
@@ -261,58 +244,33 @@ __global__ void fill_float_kernel(float* p, int64_t count, float v) {
 
 }  // namespace
 
-static int topk_buffer(int kprime) {
-  const int Kp = pow2_ceil(kprime);
-  return std::max(2048, 2 * Kp);
-}
-
 void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s) {
   if (count <= 0) return;
   fill_float_kernel<<<unsigned((count + 255) / 256), 256, 0, s>>>(p, count, v);
   DK_CHECK_LAUNCH();
 }
 
-void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t kprime, float* tau,
-                          cudaStream_t s) {
-  const int B = topk_buffer(kprime);
+void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
+                          float xn_max, float eps_rel, float* tau, cudaStream_t s) {
+  const int B = std::max(2, pow2_ceil(nseg));
   const size_t smem = size_t(B) * 8;
-  static bool attr = false;
-  if (!attr) {
-    DK_CUDA(cudaFuncSetAttribute(tau_from_tmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
-  tau_from_tmin_kernel<<<unsigned(nq), 256, smem, s>>>(tmin, nseg, nq_pad, nq, kprime, B, tau);
-  DK_CHECK_LAUNCH();
-}
-
-void launch_tau_from_cand(const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, int64_t nq,
-                          int32_t kprime, float* tau, int32_t* overflow_list, int32_t* n_overflow, cudaStream_t s) {
-  const int B = topk_buffer(kprime);
-  static bool attr = false;
-  if (!attr) {
-    DK_CUDA(cudaFuncSetAttribute(tau_from_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
-  tau_from_cand_kernel<<<unsigned(nq), 256, size_t(B) * 8, s>>>(cand, cand_cnt, cap, nq, kprime, B, tau,
-                                                                overflow_list, n_overflow);
+  if (smem > 232448) throw Error{DK_EINVAL, "too many k-NN segments"};
+  set_dynamic_smem(tau_from_tmin_kernel, smem);
+  tau_from_tmin_kernel<<<unsigned(nq), 256, smem, s>>>(tmin, nseg, nq_pad, nq, k, B, qn, xn_max, eps_rel, tau);
   DK_CHECK_LAUNCH();
 }
 
 void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
-                          int32_t kprime, const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap,
-                          const float* tau, const float* qn, float xn_max, float eps_rel, int64_t* idx_out,
-                          double* d2_out, int32_t* status, cudaStream_t s) {
-  const int B = topk_buffer(kprime);
-  const int Kp = pow2_ceil(kprime);
-  const size_t smem = size_t(B) * 8 + size_t(Kp) * sizeof(Key128);
-  static bool attr = false;
-  if (!attr) {
-    DK_CUDA(cudaFuncSetAttribute(select_rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
-  if (smem > 232448) throw Error{DK_EINVAL, "k too large for the k-NN selection buffer"};
-  select_rerank_kernel<<<unsigned(nq), 256, smem, s>>>(X, global_offset, d, Q, nq, k, kprime, cand, cand_cnt, cap,
-                                                       tau, qn, xn_max, eps_rel, B, idx_out, d2_out, status);
+                          const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
+                          float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* status,
+                          cudaStream_t s) {
+  const int B = std::max(2, pow2_ceil(cap));
+  const int Kp = std::max(32, pow2_ceil(k));
+  const size_t smem = size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128);
+  set_dynamic_smem(select_rerank_kernel, smem);
+  if (smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
+  select_rerank_kernel<<<unsigned(nq), 256, smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,
+                                                       xn_max, eps_rel, B, idx_out, d2_out, status);
   DK_CHECK_LAUNCH();
 }
 
@@ -323,11 +281,7 @@ void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_o
   const int Kp = pow2_ceil(k);
   const int B = std::max(1024, 2 * Kp);
   const size_t smem = size_t(B) * sizeof(Key128);
-  static bool attr = false;
-  if (!attr) {
-    DK_CUDA(cudaFuncSetAttribute(exact_knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
+  set_dynamic_smem(exact_knn_kernel, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "k too large for the exact k-NN fallback"};
   exact_knn_kernel<<<unsigned(nlist), 256, smem, s>>>(X, n_local, global_offset, d, Q, qlist, k, B, idx_out, d2_out);
   DK_CHECK_LAUNCH();

@@ -221,11 +221,7 @@ void launch_sample(const float* X, int64_t n_local, int64_t global_offset, int64
                    double* z_sum, int64_t* acc_idx, int64_t* draws, cudaStream_t s) {
   const int wpb = 8;
   const size_t smem = size_t(wpb) * d * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    DK_CUDA(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
+  set_dynamic_smem(sample_kernel, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the sampling kernel"};
   sample_kernel<<<unsigned((nq + wpb - 1) / wpb), wpb * 32, smem, s>>>(
       X, n_local, global_offset, global_n, d, Q, nq, family, family_c(family, bandwidth), m, seed, query_base,
@@ -239,11 +235,7 @@ void launch_sort_excl(const int64_t* excl, const int32_t* excl_cnt, int32_t stri
   while (B < stride) B <<= 1;
   const size_t smem = size_t(B) * 8;
   if (smem > 232448) throw Error{DK_EINVAL, "exclusion list too long (k > 29000) for the sampling path"};
-  static bool attr = false;
-  if (!attr) {
-    DK_CUDA(cudaFuncSetAttribute(sort_excl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
+  set_dynamic_smem(sort_excl_kernel, smem);
   sort_excl_kernel<<<unsigned(nq), 256, smem, s>>>(excl, excl_cnt, stride, B, sorted);
   DK_CHECK_LAUNCH();
 }
@@ -253,11 +245,7 @@ void launch_eval_rows(const float* X, int64_t n_local, int64_t global_offset, in
                       double* out, cudaStream_t s) {
   const int wpb = 8;
   const size_t smem = size_t(wpb) * d * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    DK_CUDA(cudaFuncSetAttribute(eval_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
+  set_dynamic_smem(eval_rows_kernel, smem);
   eval_rows_kernel<<<unsigned((nq + wpb - 1) / wpb), wpb * 32, smem, s>>>(
       X, n_local, global_offset, d, Q, nq, family, family_c(family, bandwidth), rows, cnt, stride, out);
   DK_CHECK_LAUNCH();

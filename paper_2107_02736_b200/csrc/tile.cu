@@ -34,18 +34,18 @@ struct Plan {
   size_t smem;
 };
 
-Plan make_plan(int kblocks, int ntiles, int nqb, int num_sms) {
+Plan make_plan(int kblocks, int ntiles, int nqb, int num_sms, int mode) {
   Plan pl{};
   // keep the query block resident when it fits next to a >=3-stage ring
-  if (tile_smem_bytes(kblocks, 1, 3) <= kMaxSmem) {
+  if (tile_smem_bytes(kblocks, 1, 3, mode) <= kMaxSmem) {
     pl.a_resident = 1;
     int st = 3;
-    while (st < 8 && tile_smem_bytes(kblocks, 1, st + 1) <= kMaxSmem) ++st;
+    while (st < 8 && tile_smem_bytes(kblocks, 1, st + 1, mode) <= kMaxSmem) ++st;
     pl.stages = st;
   } else {
     pl.a_resident = 0;
     int st = 2;
-    while (st < 6 && tile_smem_bytes(kblocks, 0, st + 1) <= kMaxSmem) ++st;
+    while (st < 6 && tile_smem_bytes(kblocks, 0, st + 1, mode) <= kMaxSmem) ++st;
     pl.stages = st;
   }
   // ~16+ units per CTA for balance; at least 1 tile per unit
@@ -54,7 +54,7 @@ Plan make_plan(int kblocks, int ntiles, int nqb, int num_sms) {
   tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, ntiles));
   pl.tiles_per_unit = int(tpu);
   pl.ncc = int((ntiles + tpu - 1) / tpu);
-  pl.smem = tile_smem_bytes(kblocks, pl.a_resident, pl.stages);
+  pl.smem = tile_smem_bytes(kblocks, pl.a_resident, pl.stages, mode);
   return pl;
 }
 
@@ -88,7 +88,7 @@ CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint3
 
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms) {
   const int ntiles = int(n_pad / kBN);
-  const Plan pl = make_plan(1, ntiles, nq_pad / kBM, num_sms);
+  const Plan pl = make_plan(1, ntiles, nq_pad / kBM, num_sms, MODE_KDE_GAUSS);
   return size_t(pl.ncc) * kColGroups * size_t(nq_pad);
 }
 
@@ -99,7 +99,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const int ntiles_all = int(a.n_pad / kBN);
   const int ntiles = (ntiles_all + a.tile_stride - 1) / a.tile_stride;
   const int nqb = q.nq_pad / kBM;
-  const Plan pl = make_plan(kblocks, ntiles, nqb, num_sms);
+  const Plan pl = make_plan(kblocks, ntiles, nqb, num_sms, a.mode);
 
   TileParams p{};
   p.nq = q.nq;
@@ -123,7 +123,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.cand_cnt = a.cand_cnt;
   p.cand = a.cand;
   p.cap = a.cap;
-  p.row_map = a.row_map;
+  p.seg_tiles = a.seg_tiles;
   if (a.ncc_out) *a.ncc_out = pl.ncc;
 
   const int nunits = nqb * pl.ncc;

@@ -4,21 +4,25 @@
 // (chunk of 256-column dataset tiles).  Roles:
 //   warp 0      TMA producer (one elected lane): A = query block (resident in
 //               smem for the whole unit when it fits), B = 256x64 dataset
-//               K-blocks through a multi-stage mbarrier ring.
+//               K-blocks through a multi-stage mbarrier ring, plus the tile's
+//               256 column norms (1 KB bulk copy into a 4-slot ring).
 //   warp 1      MMA issuer (one lane): tcgen05.mma kind::f16, M=128 N=256,
 //               fp32 accumulator in TMEM, 2 accumulator buffers x 256 cols.
 //   warp 2      TMEM allocator.
-//   warps 4-19  epilogue: warp w reads TMEM lane quarter (w%4) and column
-//               quarter (w-4)/4 (64 columns) with tcgen05.ld; each thread owns
-//               ONE query row, so the per-query row sum needs no shuffles.
-//               The tile's 256 column norms are TMA-staged in smem (1 KB ring).
+//   warps 4-19  epilogue: warp w reads TMEM lane quarter (w%4) and 64-column
+//               group (w-4)/4 with tcgen05.ld; each thread owns ONE query row,
+//               so the per-query row sum needs no shuffles.
 // The S = Q X^T tile never leaves the SM: the epilogue turns it into
 //   d2 = |q|^2 + |x|^2 - 2 S          (fp32, exact for the integer encoding)
 // and then, by mode,
 //   KDE_GAUSS  sum exp2(d2 * -log2e/(2h^2))       -> naive_kde gaussian
 //   KDE_EXP    sum exp2(sqrt(d2) * -log2e/h)       -> naive_kde exponential
-//   TILEMIN    min d2 over each 64-column quarter tile (k-NN threshold pass)
-//   FILTER     append (d2, col) when d2 <= tau[row]  (k-NN candidate pass)
+//   TILEMIN    min d2 over segments of `seg_tiles` tiles (k-NN threshold pass)
+//   FILTER     keep (d2, col) with d2 <= tau[row]    (k-NN candidate pass)
+// The gaussian epilogue does the per-element arithmetic on packed f32x2
+// (FADD2 / FFMA2 / FMUL2) and evaluates a fixed fraction of the exponentials
+// with a polynomial on the FMA pipe instead of MUFU.EX2, balancing the two
+// pipes (the SFU alone would bound the kernel).
 // Reference: naive_kde estimators.py:144-149 -> batch_sqdist distance.py:69-85
 // -> kernel_from_distance kernels.py:65-83 -> .mean(axis=1); brute_force_knn
 // ann.py:105-111.
@@ -43,6 +47,7 @@ constexpr int kThreads = 32 * (kEpiWarp0 + kNumEpiWarps);  // 640
 constexpr int kColGroups = 4;      // 64-column groups per tile (one per epilogue warp of a lane quarter)
 constexpr int kXnSlots = 4;        // column-norm staging ring (1 KB per tile)
 constexpr uint32_t kTmemCols = 512;  // 2 accumulator buffers x 256 fp32 columns
+constexpr int kStageCap = 32;      // FILTER: per-row smem candidate staging (entries)
 
 struct TileParams {
   int32_t nq;              // valid query rows
@@ -56,56 +61,157 @@ struct TileParams {
   int32_t kblocks;         // Kp / 64
   int32_t a_resident;      // 1: query block loaded once per unit
   int32_t stages;          // B ring depth
+  int32_t seg_tiles;       // TILEMIN: tiles per segment (0: one segment per 64-column group)
   const float* xn;         // [n_pad] |x|^2 (encoding-consistent)
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
   float negc;              // exp2 scale: gaussian -log2e/(2h^2); exponential -log2e/h
   double* part;            // KDE: [ncc*kColGroups][nq_pad] partial sums
-  float* tmin;             // TILEMIN: [ntiles*kColGroups][nq_pad]
+  float* tmin;             // TILEMIN: [nseg][nq_pad], pre-filled with +inf (atomicMin on int bits)
   const float* tau;        // FILTER: [nq_pad] thresholds
   uint32_t* cand_cnt;      // FILTER: [nq_pad]
   unsigned long long* cand;  // FILTER: [nq_pad][cap] keys (f32 bits << 32 | col)
   int32_t cap;
-  const int32_t* row_map;  // FILTER subset rerun: query row -> output slot (nullptr = identity)
 };
 
-__host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages) {
+__host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode) {
   size_t a = a_resident ? size_t(kblocks) * kABlockBytes : size_t(stages) * kABlockBytes;
   size_t b = size_t(stages) * kBBlockBytes;
-  return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + 512 /*barriers*/;
+  size_t stage = mode == MODE_FILTER ? size_t(kBM) * kStageCap * 8 + kBM * 4 : 0;
+  return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + stage + 512 /*barriers*/;
 }
 
+// ---------------------------------------------------------------- packed f32x2 helpers
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 c;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(reinterpret_cast<uint64_t&>(c))
+      : "l"(reinterpret_cast<uint64_t&>(a)), "l"(reinterpret_cast<uint64_t&>(b)));
+  return c;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 c;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(reinterpret_cast<uint64_t&>(c))
+      : "l"(reinterpret_cast<uint64_t&>(a)), "l"(reinterpret_cast<uint64_t&>(b)));
+  return c;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(reinterpret_cast<uint64_t&>(d))
+      : "l"(reinterpret_cast<uint64_t&>(a)), "l"(reinterpret_cast<uint64_t&>(b)),
+        "l"(reinterpret_cast<uint64_t&>(c)));
+  return d;
+}
+
+// 2^t for a pair, t <= 0, on the FMA pipe: t = j + f (j = round(t), |f| <= 1/2),
+// 2^f by a degree-5 polynomial (relative error < 2.4e-7 on |f| <= 1/2, i.e. at the
+// level of ex2.approx), exponent j added to the float bits.  t is clamped at -126
+// (ex2.approx.ftz flushes below 2^-126 as well).
+__device__ __forceinline__ float2 exp2_poly2(float2 t) {
+  t.x = fmaxf(t.x, -126.f);
+  t.y = fmaxf(t.y, -126.f);
+  const float2 tr = add2(t, make_float2(12582912.f, 12582912.f));  // 1.5 * 2^23: round to integer
+  const float2 jf = add2(tr, make_float2(-12582912.f, -12582912.f));
+  const float2 f = add2(t, make_float2(-jf.x, -jf.y));
+  // near-minimax (relative error) fit of 2^f on [-1/2, 1/2]: max rel err 2.3e-7 in fp32 Horner
+  float2 p = make_float2(1.3276207e-3f, 1.3276207e-3f);
+  p = fma2(p, f, make_float2(9.6754571e-3f, 9.6754571e-3f));
+  p = fma2(p, f, make_float2(5.5507135e-2f, 5.5507135e-2f));
+  p = fma2(p, f, make_float2(2.4022122e-1f, 2.4022122e-1f));
+  p = fma2(p, f, make_float2(6.9314694e-1f, 6.9314694e-1f));
+  p = fma2(p, f, make_float2(1.0000001f, 1.0000001f));
+  float2 r;
+  r.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(tr.x) << 23));
+  r.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(tr.y) << 23));
+  return r;
+}
+
+__device__ __forceinline__ void candidate(float d2, int64_t col, int row, const TileParams& p, uint32_t* scnt,
+                                          unsigned long long* sbuf, int lrow) {
+  const unsigned long long key =
+      (static_cast<unsigned long long>(__float_as_uint(fmaxf(d2, 0.f))) << 32) | static_cast<unsigned long long>(col);
+  const uint32_t pos = atomicAdd(&scnt[lrow], 1u);
+  if (pos < uint32_t(kStageCap)) {
+    sbuf[lrow * kStageCap + pos] = key;
+  } else {  // dense region: spill straight to the global list
+    const uint32_t g = atomicAdd(&p.cand_cnt[row], 1u);
+    if (g < uint32_t(p.cap)) p.cand[size_t(row) * p.cap + g] = key;
+  }
+}
+
+// One 32-column chunk of the epilogue.  `full` = all 32 columns valid (warp-uniform).
 template <int MODE>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* __restrict__ xs_smem, float qn,
                                           float m2s, float negc, float tau, bool full, int64_t cbase, int64_t n,
-                                          float& s0, float& s1, float& s2, float& s3, float& mn, const TileParams& p,
-                                          int row) {
+                                          float2& acc0, float2& acc1, float& mn, const TileParams& p, int row,
+                                          uint32_t* scnt, unsigned long long* sbuf, int lrow) {
   const float4* x4 = reinterpret_cast<const float4*>(xs_smem);
-  if (full) {
+  if (full || MODE == MODE_TILEMIN || MODE == MODE_FILTER) {
+    if constexpr (MODE == MODE_KDE_GAUSS) {
+      const float2 q2 = make_float2(qn, qn), m2 = make_float2(m2s, m2s), c2 = make_float2(negc, negc);
 #pragma unroll
-    for (int j4 = 0; j4 < 8; ++j4) {
-      const float4 xv = x4[j4];
-      const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float4 xv = x4[j4];
+        const float2 ua = add2(q2, make_float2(xv.x, xv.y));
+        const float2 ub = add2(q2, make_float2(xv.z, xv.w));
+        const float2 da = fma2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), m2, ua);
+        const float2 db = fma2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), m2, ub);
+        const float2 ta = mul2(da, c2), tb = mul2(db, c2);
+        const float2 ea = make_float2(ex2_approx(ta.x), ex2_approx(ta.y));
+        // every other group of 4: one pair on the FMA pipe (25% of the exponentials)
+        const float2 eb = (j4 & 1) ? exp2_poly2(tb) : make_float2(ex2_approx(tb.x), ex2_approx(tb.y));
+        acc0 = add2(acc0, ea);
+        acc1 = add2(acc1, eb);
+      }
+    } else if constexpr (MODE == MODE_KDE_EXP) {
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = j4 * 4 + jj;
-        const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs[jj]);
-        if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
-          float e;
-          if constexpr (MODE == MODE_KDE_GAUSS) e = ex2_approx(d2 * negc);
-          else e = ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
-          if (jj == 0) s0 += e; else if (jj == 1) s1 += e; else if (jj == 2) s2 += e; else s3 += e;
-        } else if constexpr (MODE == MODE_TILEMIN) {
-          mn = fminf(mn, d2);
-        } else {
-          if (d2 <= tau) {
-            const int slot = p.row_map ? p.row_map[row] : row;
-            const uint32_t pos = atomicAdd(&p.cand_cnt[slot], 1u);
-            if (pos < uint32_t(p.cap))
-              p.cand[size_t(slot) * p.cap + pos] =
-                  (static_cast<unsigned long long>(__float_as_uint(fmaxf(d2, 0.f))) << 32) |
-                  static_cast<unsigned long long>(cbase + j);
-          }
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float4 xv = x4[j4];
+        const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = j4 * 4 + jj;
+          const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs[jj]);
+          const float e = ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
+          if (jj & 1) acc0.y += e; else acc0.x += e;
+        }
+      }
+    } else {
+      // k-NN passes: packed distance arithmetic, branch-free hit mask
+      const float2 q2 = make_float2(qn, qn), m2 = make_float2(m2s, m2s);
+      float d2v[32];
+#pragma unroll
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float4 xv = x4[j4];
+        const float2 da = fma2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), m2,
+                               add2(q2, make_float2(xv.x, xv.y)));
+        const float2 db = fma2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), m2,
+                               add2(q2, make_float2(xv.z, xv.w)));
+        d2v[4 * j4] = da.x; d2v[4 * j4 + 1] = da.y; d2v[4 * j4 + 2] = db.x; d2v[4 * j4 + 3] = db.y;
+      }
+      if (!full) {  // columns past n: +inf never wins a min and never passes the threshold
+        const int lim = int(min(int64_t(32), n - cbase));
+#pragma unroll
+        for (int j = 0; j < 32; ++j) d2v[j] = j < lim ? d2v[j] : __int_as_float(0x7f800000);
+      }
+      if constexpr (MODE == MODE_TILEMIN) {
+        float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[2], m3 = d2v[3];
+#pragma unroll
+        for (int j = 4; j < 32; j += 4) {
+          m0 = fminf(m0, d2v[j]); m1 = fminf(m1, d2v[j + 1]);
+          m2_ = fminf(m2_, d2v[j + 2]); m3 = fminf(m3, d2v[j + 3]);
+        }
+        mn = fminf(mn, fminf(fminf(m0, m1), fminf(m2_, m3)));
+      } else {
+        uint32_t hits = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hits |= (d2v[j] <= tau ? 1u : 0u) << j;
+        while (hits) {  // rare: appended candidates
+          const int j = __ffs(hits) - 1;
+          hits &= hits - 1;
+          float dj = d2v[0];
+#pragma unroll
+          for (int i = 1; i < 32; ++i) dj = (i == j) ? d2v[i] : dj;
+          candidate(dj, cbase + j, row, p, scnt, sbuf, lrow);
         }
       }
     }
@@ -116,36 +222,31 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
       if (j >= lim) continue;
       const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs_smem[j]);
       if constexpr (MODE == MODE_KDE_GAUSS) {
-        s0 += ex2_approx(d2 * negc);
-      } else if constexpr (MODE == MODE_KDE_EXP) {
-        s0 += ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
-      } else if constexpr (MODE == MODE_TILEMIN) {
-        mn = fminf(mn, d2);
+        acc0.x += ex2_approx(d2 * negc);
       } else {
-        if (d2 <= tau) {
-          const int slot = p.row_map ? p.row_map[row] : row;
-          const uint32_t pos = atomicAdd(&p.cand_cnt[slot], 1u);
-          if (pos < uint32_t(p.cap))
-            p.cand[size_t(slot) * p.cap + pos] =
-                (static_cast<unsigned long long>(__float_as_uint(fmaxf(d2, 0.f))) << 32) |
-                static_cast<unsigned long long>(cbase + j);
-        }
+        acc0.x += ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
       }
     }
   }
 }
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32) : "memory"); }
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                 const TileParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the shared pointer itself, so the
+  // compiler keeps the shared address space (LDS/ATOMS instead of generic LD/ATOM)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
   uint8_t* smemA = smem;
   uint8_t* smemB = smem + (p.a_resident ? size_t(p.kblocks) * kABlockBytes : size_t(stages) * kABlockBytes);
   float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBBlockBytes);  // [kXnSlots][256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smemX + kXnSlots * kBN);
+  unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smemX + kXnSlots * kBN);  // FILTER staging
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (MODE == MODE_FILTER ? kBM * kStageCap : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scnt + (MODE == MODE_FILTER ? kBM : 0));
   uint64_t* full_bar = bars;                 // [stages]
   uint64_t* empty_bar = bars + stages;       // [stages]
   uint64_t* tfull_bar = bars + 2 * stages;   // [2]
@@ -178,6 +279,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&xempty_bar[x], kNumEpiWarps);
     }
     fence_mbar_init();
+  }
+  if constexpr (MODE == MODE_FILTER) {
+    for (int i = threadIdx.x; i < kBM; i += blockDim.x) scnt[i] = 0;
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -272,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = int(warp) - kEpiWarp0;
     const int quarter = int(warp & 3);
     const int cg = ew >> 2;  // 64-column group of the tile
+    const int lrow = quarter * 32 + int(lane);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t titer = 0;
@@ -281,13 +386,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int qb = u % p.nqb, cc = u / p.nqb;
       const int t0 = cc * p.tiles_per_unit;
       const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
-      const int row = qb * kBM + quarter * 32 + int(lane);
+      const int row = qb * kBM + lrow;
       const float qn = p.qn[row];
       float tau = 0.f;
       if constexpr (MODE == MODE_FILTER) tau = p.tau[row];
       double usum = 0.0;
+      float mn = __int_as_float(0x7f800000);
+      // TILEMIN segments: seg_tiles > 0 -> groups of seg_tiles whole tiles; seg_tiles == 0 -> one
+      // segment per (tile, 64-column group)
+      const int segdiv = p.seg_tiles > 0 ? p.seg_tiles : 1;
+      int seg = MODE == MODE_TILEMIN ? t0 / segdiv : 0;
       for (int t = t0; t < t1; ++t, ++titer) {
         const uint32_t xs = titer % kXnSlots;
+        if constexpr (MODE == MODE_TILEMIN) {
+          if (p.seg_tiles > 0 && t / segdiv != seg) {
+            atomicMin(reinterpret_cast<int*>(&p.tmin[size_t(seg) * p.nq_pad + row]), __float_as_int(fmaxf(mn, 0.f)));
+            seg = t / segdiv;
+            mn = __int_as_float(0x7f800000);
+          }
+        }
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN + cg * 64);
@@ -303,20 +420,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t cbase = int64_t(t) * p.tile_stride * kBN + cg * 64;
         const float* xsm = smemX + xs * kBN + cg * 64;
         const bool full = cbase + 64 <= p.n;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        float mn = __int_as_float(0x7f800000);
-        epi_chunk<MODE>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, s0, s1, s2, s3, mn, p, row);
-        epi_chunk<MODE>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n, s0, s1, s2, s3, mn, p, row);
+        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+        epi_chunk<MODE>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf, lrow);
+        epi_chunk<MODE>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n, a0, a1, mn, p, row, scnt, sbuf,
+                        lrow);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
-          usum += double((s0 + s1) + (s2 + s3));
+          usum += double((a0.x + a0.y) + (a1.x + a1.y));
         } else if constexpr (MODE == MODE_TILEMIN) {
-          p.tmin[(size_t(t) * kColGroups + cg) * p.nq_pad + row] = mn;
+          if (p.seg_tiles == 0) {
+            p.tmin[(size_t(t) * kColGroups + cg) * p.nq_pad + row] = fmaxf(mn, 0.f);
+            mn = __int_as_float(0x7f800000);
+          }
         }
       }
       if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
         p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
+      } else if constexpr (MODE == MODE_TILEMIN) {
+        if (t1 > t0 && p.seg_tiles > 0)
+          atomicMin(reinterpret_cast<int*>(&p.tmin[size_t(seg) * p.nq_pad + row]), __float_as_int(fmaxf(mn, 0.f)));
+      } else {
+        // flush the unit's staged candidates: one global atomic per row
+        epi_bar();
+        if (cg == 0) {
+          const uint32_t c = min(scnt[lrow], uint32_t(kStageCap));
+          if (c) {
+            const uint32_t base = atomicAdd(&p.cand_cnt[row], c);
+            for (uint32_t i = 0; i < c; ++i)
+              if (base + i < uint32_t(p.cap)) p.cand[size_t(row) * p.cap + base + i] = sbuf[lrow * kStageCap + i];
+          }
+          scnt[lrow] = 0;
+        }
+        epi_bar();
       }
     }
   }
