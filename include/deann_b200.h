@@ -54,7 +54,7 @@ typedef enum {
 /* Operand precision for the tensor-core distance tile (dk_fit_opts.precision). */
 typedef enum {
   DK_PREC_AUTO = 0,    /* exact fp16 when rows and queries are small integers, else split3 */
-  DK_PREC_SPLIT3 = 1,  /* fp16 hi/lo, K-concatenated [Qh|Qh|Ql]x[Xh|Xl|Xh] (~2^-22 rel)   */
+  DK_PREC_SPLIT3 = 1,  /* fp16 hi/lo, K-concatenated [Qh|Ql|Qh]x[Xl|Xh|Xh] (~2^-22 rel)   */
   DK_PREC_FP16 = 2     /* single-pass fp16 (fast, ~1e-3..1e-5 rel; opt-in only)           */
 } dk_precision;
 

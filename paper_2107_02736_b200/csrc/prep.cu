@@ -6,8 +6,8 @@
 //   exact  : fp16 copies of small-integer rows (bit-exact products, fp32 sums
 //            exact below 2^24)  -> Kp = roundup(d, 64)
 //   split3 : centred, power-of-two scaled fp16 hi/lo pairs, K-concatenated
-//            A=[Qh|Qh|Ql], B=[Xh|Xl|Xh] so one MMA chain with K = 3d gives
-//            Qh.Xh + Qh.Xl + Ql.Xh (~2^-22 relative)     -> Kp = roundup(3d, 64)
+//            A=[Qh|Ql|Qh], B=[Xl|Xh|Xh] so one MMA chain with K = 3d gives
+//            Qh.Xl + Ql.Xh + Qh.Xh (~2^-22 relative)     -> Kp = roundup(3d, 64)
 //   fp16   : single-pass scaled fp16 (opt-in, lossy)       -> Kp = roundup(d, 64)
 #include "internal.h"
 
@@ -132,7 +132,10 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
   double nrm = 0.0;
   for (int k = lane; k < Kp; k += 32) {
     if (mode == 1) {
-      const int blk = k / d;                 // 0: hi, 1: (A) hi | (B) lo, 2: (A) lo | (B) hi
+      // K-concatenation A=[Qh|Ql|Qh], B=[Xl|Xh|Xh]: the two small cross terms are accumulated
+      // first and the large hi*hi term last, so the fp32 accumulator spends the fewest MMA
+      // steps at full magnitude (its rounding error grows with steps x |S|)
+      const int blk = k / d;
       const int kk = k - blk * d;
       if (blk >= 3) { o[k] = __float2half_rn(0.f); continue; }
       double x = double(v[kk]);
@@ -141,12 +144,11 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
       const double xs = x * double(s);
       const __half h = __float2half_rn(float(xs));
       const __half l = __float2half_rn(float(xs - double(__half2float(h))));
-      // rows encode B=[h|l|h]; queries (other_scale != nullptr) encode A=[h|h|l]
       const bool is_query = (other_scale != nullptr);
       __half w;
-      if (blk == 0) w = h;
-      else if (blk == 1) w = is_query ? h : l;
-      else w = is_query ? l : h;
+      if (blk == 0) w = is_query ? h : l;
+      else if (blk == 1) w = is_query ? l : h;
+      else w = h;
       o[k] = w;
     } else {
       if (k >= d) { o[k] = __float2half_rn(0.f); continue; }
