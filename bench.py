@@ -294,7 +294,7 @@ def run_ours(args):
     tpath = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("c2_kde_gauss")
+            traffic = json.load(f).get("c2_kde_gauss", {}).get("dram_bytes_per_launch")
     line = {
         "metric": METRIC, "value": nq / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
