@@ -169,6 +169,11 @@ dk_status dk_set_profiling(dk_handle h, int32_t on);
  * candidates per query, queries that took the exact-scan fallback. */
 dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t* cand_max,
                        int64_t* fallbacks);
+/* Diagnostics: time (ms, CUDA events) of one tile sweep of the given mode
+ * (0 KDE-gauss, 1 KDE-exp, 2 segment-min, 3 filter, 4 null epilogue) with the
+ * given operand encoding (0 exact, 1 split3, 2 fp16) — a pipeline probe. */
+dk_status dk_sweep_probe(dk_handle h, const double* Q, int64_t nq, int32_t mode, int32_t encoding,
+                         double* ms);
 /* Number of this library's kernels launched by the last API call. */
 dk_status dk_last_launch_count(dk_handle h, int64_t* count);
 

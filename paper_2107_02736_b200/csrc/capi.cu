@@ -825,6 +825,60 @@ dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* byte
   });
 }
 
+dk_status dk_sweep_probe(dk_handle h, const double* Q, int64_t nq, int32_t mode, int32_t encoding, double* ms) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr && Q != nullptr && ms != nullptr && nq > 0, "bad probe arguments");
+    DK_REQUIRE(mode >= MODE_KDE_GAUSS && mode <= MODE_NULL && encoding >= 0 && encoding <= 2, "bad probe mode");
+    DeviceGuard g(h->device);
+    cudaStream_t s = nullptr;
+    const Encoding& e = ensure_encoding(h, encoding, s);
+    const int32_t nq_pad = int32_t(round_up(nq, kBM));
+    Plan pl;
+    const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
+    const size_t o_A = pl.add<__half>(size_t(nq_pad) * e.Kp);
+    const size_t o_qn = pl.add<float>(nq_pad);
+    const size_t o_scal = pl.add<float>(4);
+    const size_t o_part = pl.add<double>(sweep_part_count(h->n_pad, nq_pad, h->num_sms));
+    const size_t o_tmin = pl.add<float>(size_t(nq_pad) * 4 * size_t(h->n_pad / kBN));
+    const size_t o_tau = pl.add<float>(nq_pad);
+    const size_t o_cnt = pl.add<uint32_t>(nq_pad);
+    const size_t o_cand = pl.add<unsigned long long>(size_t(nq_pad) * 64);
+    h->ws.reserve(pl.off);
+    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+    QueryOperand q = encode_queries(h, e, Qd, nq, nq_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
+                                    at<float>(h->ws, o_scal), s);
+    SweepArgs a{};
+    a.mode = mode;
+    a.qop = &q;
+    a.enc = &e;
+    a.n = h->n;
+    a.n_pad = h->n_pad;
+    a.tile_stride = 1;
+    a.negc = -1e-3f;
+    a.part = at<double>(h->ws, o_part);
+    a.tmin = at<float>(h->ws, o_tmin);
+    a.seg_tiles = 0;
+    a.tau = at<float>(h->ws, o_tau);
+    launch_fill_float(at<float>(h->ws, o_tau), nq_pad, -1.f, s);
+    a.cand_cnt = at<uint32_t>(h->ws, o_cnt);
+    a.cand = at<unsigned long long>(h->ws, o_cand);
+    a.cap = 64;
+    cudaEvent_t e0, e1;
+    DK_CUDA(cudaEventCreate(&e0));
+    DK_CUDA(cudaEventCreate(&e1));
+    launch_sweep(a, h->num_sms, s);  // warm
+    DK_CUDA(cudaEventRecord(e0, s));
+    launch_sweep(a, h->num_sms, s);
+    DK_CUDA(cudaEventRecord(e1, s));
+    DK_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    DK_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
 dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t* cand_max, int64_t* fallbacks) {
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");

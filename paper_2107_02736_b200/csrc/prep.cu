@@ -187,8 +187,17 @@ __global__ void reduce_partials_kernel(const double* __restrict__ part, int32_t 
                                        double scale, double* __restrict__ out) {
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= nq) return;
+  // fixed summation order (deterministic); loads issued 8 ahead of the adds (latency-bound otherwise)
   double s = 0.0;
-  for (int j = 0; j < nparts; ++j) s += part[size_t(j) * nq_pad + q];
+  int j = 0;
+  for (; j + 8 <= nparts; j += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = part[size_t(j + u) * nq_pad + q];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; j < nparts; ++j) s += part[size_t(j) * nq_pad + q];
   out[q] = s * scale;
 }
 
@@ -248,7 +257,7 @@ void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t 
 
 void launch_reduce_partials(const double* part, int32_t nparts, int32_t nq_pad, int64_t nq, double scale, double* out,
                             cudaStream_t s) {
-  reduce_partials_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(part, nparts, nq_pad, nq, scale, out);
+  reduce_partials_kernel<<<unsigned((nq + 63) / 64), 64, 0, s>>>(part, nparts, nq_pad, nq, scale, out);
   DK_CHECK_LAUNCH();
 }
 

@@ -14,10 +14,10 @@
 // reference through a replaying `rng.integers` reproduces its estimate.
 //
 // One warp per query; 32 consecutive draws per iteration; accepted draws are
-// compacted with a ballot so acceptance order == draw order.  Each accepted
-// row is evaluated by the lane that drew it: fp32 row loads (float4 when
-// aligned), fp64 direct-difference distance, fp64 exp (parity ~1e-15 with
-// the reference's fp64 arithmetic).
+// compacted with a ballot so acceptance order == draw order.  Accepted rows
+// are evaluated by groups of G lanes (coalesced float4 row loads), fp64
+// direct-difference distance, fp64 exp (parity ~1e-15 with the reference's
+// fp64 arithmetic).
 #include "internal.h"
 
 namespace dk {
@@ -86,22 +86,55 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// Accepted rows are evaluated by groups of G lanes (G = 1..32 chosen from d):
+// each group reads one row with G-wide coalesced float4 loads and reduces its
+// fp64 partial with shuffles, so rows of any width stream at full sector use.
+template <int G>
+__device__ __forceinline__ double group_row_kernel(const float* __restrict__ x, const double* __restrict__ q, int d,
+                                                   int family, double c, int gl) {
+  double acc = 0.0;
+  if ((d & 3) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int k4 = gl; k4 < (d >> 2); k4 += G) {
+      const float4 v = __ldg(x4 + k4);
+      const double t0 = double(v.x) - q[4 * k4 + 0], t1 = double(v.y) - q[4 * k4 + 1];
+      const double t2 = double(v.z) - q[4 * k4 + 2], t3 = double(v.w) - q[4 * k4 + 3];
+      if (family == DK_LAPLACIAN) acc += (fabs(t0) + fabs(t1)) + (fabs(t2) + fabs(t3));
+      else { acc = fma(t0, t0, acc); acc = fma(t1, t1, acc); acc = fma(t2, t2, acc); acc = fma(t3, t3, acc); }
+    }
+  } else {
+    for (int k = gl; k < d; k += G) {
+      const double t = double(__ldg(x + k)) - q[k];
+      acc = family == DK_LAPLACIAN ? acc + fabs(t) : fma(t, t, acc);
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (family == DK_EXPONENTIAL) acc = sqrt(acc);
+  return exp(-acc * c);
+}
+
+template <int G>
 __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int64_t global_offset, int64_t N,
                               int32_t d, const double* __restrict__ Q, int64_t nq, int32_t family, double c,
                               int32_t m, uint64_t seed, int64_t query_base, const int64_t* __restrict__ excl,
                               const int32_t* __restrict__ excl_cnt, int32_t excl_stride, double* __restrict__ z_sum,
                               int64_t* __restrict__ acc_idx, int64_t* __restrict__ draws) {
   extern __shared__ double sq[];
+  constexpr int R = 32 / G;  // rows evaluated per warp step
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
+  const int nw = blockDim.x >> 5;
+  const int64_t j = int64_t(blockIdx.x) * nw + wib;
   if (j >= nq) return;
   double* q = sq + size_t(wib) * d;
+  int64_t* rows_s = reinterpret_cast<int64_t*>(sq + size_t(nw) * d) + wib * 32;
   for (int k = lane; k < d; k += 32) q[k] = Q[size_t(j) * d + k];
   __syncwarp();
   const int ecnt = excl ? (excl_cnt ? excl_cnt[j] : excl_stride) : 0;
   const int64_t* ex = excl ? excl + size_t(j) * excl_stride : nullptr;
   const uint64_t jg = uint64_t(j + query_base);
   const uint32_t lt_mask = (1u << lane) - 1u;
+  const int grp = lane / G, gl = lane % G;
   double zsum = 0.0;
   int accepted = 0;
   uint64_t t_base = 0;
@@ -114,13 +147,23 @@ __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int6
     const int rank = __popc(ballot & lt_mask);
     const bool take = ok && (accepted + rank < m);
     if (take) {
-      const int64_t loc = row - global_offset;
-      if (loc >= 0 && loc < n_local) zsum += row_kernel(X + size_t(loc) * d, q, d, family, c);
+      rows_s[rank] = row;
       if (acc_idx) acc_idx[size_t(j) * m + accepted + rank] = row;
     }
     const uint32_t took = __ballot_sync(0xffffffffu, take);
+    const int ntook = __popc(took);
+    __syncwarp();
+    for (int r0 = 0; r0 < ntook; r0 += R) {
+      const int r = r0 + grp;
+      const int64_t loc = r < ntook ? rows_s[r] - global_offset : -1;
+      const bool mine = loc >= 0 && loc < n_local;
+      // groups with no row still take part in the shuffles (G-lane reduction is warp-synchronous)
+      const double v = group_row_kernel<G>(X + size_t(mine ? loc : 0) * d, q, d, family, c, gl);
+      if (mine && gl == 0) zsum += v;
+    }
+    __syncwarp();
     if (took) last_t = int64_t(t_base) + 31 - __clz(took);
-    accepted += __popc(took);
+    accepted += ntook;
     t_base += 32;
   }
   zsum = warp_sum_d(zsum);
@@ -220,12 +263,26 @@ void launch_sample(const float* X, int64_t n_local, int64_t global_offset, int64
                    int64_t query_base, const int64_t* excl_sorted, const int32_t* excl_cnt, int32_t excl_stride,
                    double* z_sum, int64_t* acc_idx, int64_t* draws, cudaStream_t s) {
   const int wpb = 8;
-  const size_t smem = size_t(wpb) * d * sizeof(double);
-  set_dynamic_smem(sample_kernel, smem);
+  const size_t smem = size_t(wpb) * d * sizeof(double) + size_t(wpb) * 32 * sizeof(int64_t);
   if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the sampling kernel"};
-  sample_kernel<<<unsigned((nq + wpb - 1) / wpb), wpb * 32, smem, s>>>(
-      X, n_local, global_offset, global_n, d, Q, nq, family, family_c(family, bandwidth), m, seed, query_base,
-      excl_sorted, excl_cnt, excl_stride, z_sum, acc_idx, draws);
+  const double c = family_c(family, bandwidth);
+  const unsigned grid = unsigned((nq + wpb - 1) / wpb);
+  // lanes per row: enough that one float4 sweep of the row covers >= ~1/2 of its 16 B chunks
+  const int chunks = (d + 3) / 4;
+#define DK_SAMPLE_LAUNCH(G)                                                                                   \
+  do {                                                                                                        \
+    set_dynamic_smem(sample_kernel<G>, smem);                                                                 \
+    sample_kernel<G><<<grid, wpb * 32, smem, s>>>(X, n_local, global_offset, global_n, d, Q, nq, family, c, m, \
+                                                  seed, query_base, excl_sorted, excl_cnt, excl_stride, z_sum,  \
+                                                  acc_idx, draws);                                            \
+  } while (0)
+  if (chunks >= 64) DK_SAMPLE_LAUNCH(32);
+  else if (chunks >= 32) DK_SAMPLE_LAUNCH(16);
+  else if (chunks >= 16) DK_SAMPLE_LAUNCH(8);
+  else if (chunks >= 8) DK_SAMPLE_LAUNCH(4);
+  else if (chunks >= 4) DK_SAMPLE_LAUNCH(2);
+  else DK_SAMPLE_LAUNCH(1);
+#undef DK_SAMPLE_LAUNCH
   DK_CHECK_LAUNCH();
 }
 

@@ -133,6 +133,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
     case MODE_KDE_EXP: launch_mode<MODE_KDE_EXP>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
     case MODE_TILEMIN: launch_mode<MODE_TILEMIN>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
     case MODE_FILTER: launch_mode<MODE_FILTER>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
+    case MODE_NULL: launch_mode<MODE_NULL>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
     default: throw Error{DK_EINVAL, "bad tile mode"};
   }
 }

@@ -34,7 +34,7 @@
 
 namespace dk {
 
-enum TileMode : int { MODE_KDE_GAUSS = 0, MODE_KDE_EXP = 1, MODE_TILEMIN = 2, MODE_FILTER = 3 };
+enum TileMode : int { MODE_KDE_GAUSS = 0, MODE_KDE_EXP = 1, MODE_TILEMIN = 2, MODE_FILTER = 3, MODE_NULL = 4 };
 
 constexpr int kBM = 128;           // query rows per tile (UMMA M)
 constexpr int kBN = 256;           // dataset columns per tile (UMMA N)
@@ -417,6 +417,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&tempty_bar[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
+        if constexpr (MODE == MODE_NULL) {  // pipeline probe: consume the accumulator, no epilogue math
+          uint32_t x = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) x ^= r0[j] ^ r1[j];
+          if (x == 0x9e3779b9u) p.tmin[row] = 0.f;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xempty_bar[xs]);
+          continue;
+        }
         const int64_t cbase = int64_t(t) * p.tile_stride * kBN + cg * 64;
         const float* xsm = smemX + xs * kBN + cg * 64;
         const bool full = cbase + 64 <= p.n;
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if constexpr (MODE == MODE_TILEMIN) {
         if (t1 > t0 && p.seg_tiles > 0)
           atomicMin(reinterpret_cast<int*>(&p.tmin[size_t(seg) * p.nq_pad + row]), __float_as_int(fmaxf(mn, 0.f)));
-      } else {
+      } else if constexpr (MODE == MODE_FILTER) {
         // flush the unit's staged candidates: one global atomic per row
         epi_bar();
         if (cg == 0) {
