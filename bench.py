@@ -48,31 +48,54 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled every ~5 ms during the timed region (NVML;
+    nvidia-smi as a fallback).  Reported as the recipe's clocks line."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons_bitmask)
         self._stop = threading.Event()
         self._t = None
+        self.nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        if self.nvml is not None:
+            p = self.nvml
+            sm = p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM)
+            reasons = p.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            return float(sm), float(self.max_mhz), int(reasons)
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+        sm, mx = (float(v) for v in out.strip().split(","))
+        return sm, mx, 0
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
+                self.samples.append(self._poll())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.005 if self.nvml is not None else 0.2)
 
     def __enter__(self):
+        try:
+            self.samples.append(self._poll())
+        except Exception:
+            pass
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -84,14 +107,17 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
-                          and "Not" not in s[3 + i]})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [x[0] for x in self.samples]
+        reasons = set()
+        if self.nvml is not None:
+            for name, const in self.REASONS:
+                bit = getattr(self.nvml, const, 0)
+                if any(x[2] & bit for x in self.samples):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": sorted(reasons), "samples": len(self.samples),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def _dist_env():
@@ -122,9 +148,9 @@ def cpu_oracle_rate(X, Q, h, budget_s=12.0, max_q=1024, threads=None):
         O.naive_kde(data, "gaussian", h, blk)
         done += len(blk)
     el = time.perf_counter() - t0
-    if ctx is not None:
-        ctx.unregister() if hasattr(ctx, "unregister") else None
-    return done / el, cores, done, el
+    if ctx is not None and hasattr(ctx, "unregister"):
+        ctx.unregister()
+    return done / el, cores, done, el, data
 
 
 def run_reference(args):
@@ -316,19 +342,65 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if ws == 1 and not args.no_secondary:
+        line["secondary"] = measure_deann_c3(args, local)
     if ws == 1 and not args.no_cpu_baseline:
-        rate, cores, done, el = cpu_oracle_rate(W.X, W.Q, h)
+        rate, cores, done, el, odata = cpu_oracle_rate(W.X, W.Q, h)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"first {done} of the 10,000 queries over all n=1,000,000 rows "
                                           f"({el:.1f} s), oracle/deann_oracle.naive_kde, NumPy/OpenBLAS fp64"}
-        # parity of the timed path on the same sample
-        ref = __import__("oracle.deann_oracle", fromlist=["x"]).naive_kde(
-            __import__("oracle.deann_oracle", fromlist=["x"]).Data(W.X), "gaussian", h, W.Q[:8])
-        got = out[:8].cpu().numpy()
+        # parity of the timed device output against the oracle on a query sample
+        from oracle import deann_oracle as O
+
+        ref = O.naive_kde(odata, "gaussian", h, W.Q[:16])
+        got = out[:16].cpu().numpy()
         line["parity_max_rel"] = float(np.max(np.abs(got - ref) / ref))
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def measure_deann_c3(args, local):
+    """Secondary line: DEANN (exact k=100 NN + m=1000 Philox samples) on config 3, device-resident."""
+    import ctypes
+
+    import torch
+
+    import paper_2107_02736_b200 as g
+    import workloads
+    from paper_2107_02736_b200 import _lib
+
+    W = workloads.make("c3")
+    h = _bandwidth_cpu_free(W)
+    ds = g.Dataset.from_array(W.X, device=local)
+    Qd = torch.from_numpy(W.Q).to(f"cuda:{local}")
+    out = torch.empty(W.Q.shape[0], dtype=torch.float64, device=f"cuda:{local}")
+    lib = _lib.load()
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        _lib.check(lib.dk_deann(ds.handle, Qd.data_ptr(), Qd.shape[0], _lib.DK_GAUSSIAN, h, W.k, W.m, 1234 + i, 0,
+                                out.data_ptr(), None, None, None, stream.cuda_stream))
+
+    for i in range(max(2, args.warmup)):
+        step(i)
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        step(100 + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    cnt = ctypes.c_int64()
+    _lib.check(lib.dk_last_launch_count(ds.handle, ctypes.byref(cnt)))
+    ds.free()
+    return {"metric": "DEANN queries/sec (exact k=100 NN + m=1000 samples, gaussian) at n=1.2M, d=100",
+            "value": W.Q.shape[0] / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "gpu_launches_per_step": int(cnt.value),
+            "config": {"workload": "c3: 1,200,000 x 100 L2-normalised rows, 10,000 queries, h by median-1e-3 rule",
+                       "bandwidth": h, "k": W.k, "m": W.m}}
 
 
 def fit_manifest():
@@ -364,6 +436,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the c3 DEANN secondary measurement")
     ap.add_argument("--fit-bandwidth", action="store_true", help="(re)write tests/golden/bandwidths.json")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
