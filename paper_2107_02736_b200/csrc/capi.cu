@@ -83,6 +83,9 @@ dk_status guard(F&& f) {
 }
 
 constexpr int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+// query rows padded to whole 128-row blocks, and to an even block count beyond one block so the
+// tile sweep can run as 2-CTA pairs (cta_group::2, M = 256)
+constexpr int64_t query_pad(int64_t nq) { return nq <= kBM ? kBM : round_up(nq, 2 * kBM); }
 
 void check_family_bw(int32_t family, double bw) {
   DK_REQUIRE(family == DK_GAUSSIAN || family == DK_EXPONENTIAL || family == DK_LAPLACIAN,
@@ -141,6 +144,7 @@ const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
   else if (mode == 1) e.eps_rel = float(1.01 * (4.0 * std::ldexp(1.0, -22) + double(e.Kp + 4) * u));  // split3
   else e.eps_rel = float(1.01 * (2.002 * std::ldexp(1.0, -11) + double(e.Kp + 4) * u));             // fp16
   e.tmap = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN));
+  e.tmap_half = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN / 2));
   e.mode = mode;
   return e;
 }
@@ -259,8 +263,8 @@ KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
   }
   const int64_t budget = int64_t(1) << 30;  // bytes of candidate storage per batch
   int64_t b = budget / (int64_t(p.cap) * 8 + int64_t(p.nseg) * 4 + 64);
-  b = std::max<int64_t>(kBM, std::min<int64_t>(16384, b)) / kBM * kBM;
-  p.batch = int32_t(std::min<int64_t>(b, round_up(nq, kBM)));
+  b = std::max<int64_t>(2 * kBM, std::min<int64_t>(16384, b)) / (2 * kBM) * (2 * kBM);
+  p.batch = int32_t(std::min<int64_t>(b, query_pad(nq)));
   return p;
 }
 
@@ -296,7 +300,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
   const float inf = std::numeric_limits<float>::infinity();
   for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
     const int64_t bn = std::min<int64_t>(bpad, nq - b0);
-    const int32_t bn_pad = int32_t(round_up(bn, kBM));
+    const int32_t bn_pad = int32_t(query_pad(bn));
     const double* Qb = Qd + b0 * h->d;
     QueryOperand q = encode_queries(h, e, Qb, bn, bn_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
                                     at<float>(h->ws, o_scal), s);
@@ -430,6 +434,7 @@ dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts, 
     h->global_n = (opts && opts->global_n > 0) ? opts->global_n : n;
     h->precision = opts ? opts->precision : DK_PREC_AUTO;
     h->knn_stats = std::getenv("DK_KNN_STATS") != nullptr;
+    if (const char* pv = std::getenv("DK_PAIR")) set_pair_enabled(std::atoi(pv) != 0);
     DK_REQUIRE(h->precision >= 0 && h->precision <= 2, "unknown precision mode");
     DK_REQUIRE(h->global_offset >= 0 && h->global_offset + n <= h->global_n, "shard outside [0, global_n)");
     cudaStream_t s = nullptr;
@@ -528,7 +533,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       }
       return;
     }
-    const int32_t nq_pad = int32_t(round_up(nq, kBM));
+    const int32_t nq_pad = int32_t(query_pad(nq));
     const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
     const size_t o_A = pl.add<__half>(size_t(nq_pad) * Kp_max);
     const size_t o_qn = pl.add<float>(nq_pad);
@@ -832,7 +837,7 @@ dk_status dk_sweep_probe(dk_handle h, const double* Q, int64_t nq, int32_t mode,
     DeviceGuard g(h->device);
     cudaStream_t s = nullptr;
     const Encoding& e = ensure_encoding(h, encoding, s);
-    const int32_t nq_pad = int32_t(round_up(nq, kBM));
+    const int32_t nq_pad = int32_t(query_pad(nq));
     Plan pl;
     const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
     const size_t o_A = pl.add<__half>(size_t(nq_pad) * e.Kp);

@@ -64,7 +64,8 @@ struct Encoding {
   float* sx = nullptr;      // device scalar: power-of-two scale applied to x
   float xn_max = 0.f;       // max of xn (host copy, k-NN certificate)
   float eps_rel = 0.f;      // |approx d2 - exact d2| <= eps_rel * (|q|^2 + xn_max)
-  CUtensorMap tmap;
+  CUtensorMap tmap;         // B boxes of 256 rows (single-CTA sweep)
+  CUtensorMap tmap_half;    // B boxes of 128 rows (2-CTA pair sweep: each CTA loads half)
 };
 
 // Growable device scratch, carved per call.
@@ -159,6 +160,7 @@ struct SweepArgs {
 };
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms);  // doubles needed for KDE partials
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
+void set_pair_enabled(bool on);  // 2-CTA (cta_group::2) sweeps; off by default (DK_PAIR=1)
 
 // L1 / laplacian exact KDE on CUDA cores
 size_t l1_part_count(int64_t n, int32_t nq);

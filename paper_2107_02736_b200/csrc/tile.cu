@@ -34,42 +34,64 @@ struct Plan {
   size_t smem;
 };
 
-Plan make_plan(int kblocks, int ntiles, int nqb, int num_sms, int mode) {
+Plan make_plan(int kblocks, int ntiles, int ngroups, int nslots, int mode, bool pair) {
   Plan pl{};
   // keep the query block resident when it fits next to a >=3-stage ring
-  if (tile_smem_bytes(kblocks, 1, 3, mode) <= kMaxSmem) {
+  if (tile_smem_bytes(kblocks, 1, 3, mode, pair) <= kMaxSmem) {
     pl.a_resident = 1;
     int st = 3;
-    while (st < 8 && tile_smem_bytes(kblocks, 1, st + 1, mode) <= kMaxSmem) ++st;
+    while (st < 10 && tile_smem_bytes(kblocks, 1, st + 1, mode, pair) <= kMaxSmem) ++st;
     pl.stages = st;
   } else {
     pl.a_resident = 0;
     int st = 2;
-    while (st < 6 && tile_smem_bytes(kblocks, 0, st + 1, mode) <= kMaxSmem) ++st;
+    while (st < 6 && tile_smem_bytes(kblocks, 0, st + 1, mode, pair) <= kMaxSmem) ++st;
     pl.stages = st;
   }
-  // ~16+ units per CTA for balance; at least 1 tile per unit
-  const int64_t total_tiles = int64_t(ntiles) * nqb;
-  int64_t tpu = total_tiles / (int64_t(num_sms) * 16);
+  // ~16+ units per CTA (pair) for balance; at least 1 tile per unit
+  const int64_t total_tiles = int64_t(ntiles) * ngroups;
+  int64_t tpu = total_tiles / (int64_t(nslots) * 16);
   tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, ntiles));
   pl.tiles_per_unit = int(tpu);
   pl.ncc = int((ntiles + tpu - 1) / tpu);
-  pl.smem = tile_smem_bytes(kblocks, pl.a_resident, pl.stages, mode);
+  pl.smem = tile_smem_bytes(kblocks, pl.a_resident, pl.stages, mode, pair);
   return pl;
 }
 
-template <int MODE>
+template <int MODE, bool kPair>
 void launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const TileParams& p, int grid, size_t smem,
                  cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxSmem));
+    attr_err = cudaFuncSetAttribute(tile_kernel<MODE, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kMaxSmem));
   });
   DK_CUDA(attr_err);
-  tile_kernel<MODE><<<grid, kThreads, smem, s>>>(ta, tb, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DK_CUDA(cudaLaunchKernelEx(&cfg, tile_kernel<MODE, kPair>, ta, tb, p));
   DK_CHECK_LAUNCH();
 }
+
+template <int MODE>
+void launch_any(bool pair, const CUtensorMap& ta, const CUtensorMap& tb, const TileParams& p, int grid, size_t smem,
+                cudaStream_t s) {
+  if (pair) launch_mode<MODE, true>(ta, tb, p, grid, smem, s);
+  else launch_mode<MODE, false>(ta, tb, p, grid, smem, s);
+}
+
+bool g_pair_enabled = false;  // DK_PAIR=1 enables: measured slower (CTA coupling), see DESIGN.md
 
 }  // namespace
 
@@ -86,11 +108,17 @@ CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint3
   return m;
 }
 
+static bool use_pair(int nqb) { return g_pair_enabled && nqb >= 2 && nqb % 2 == 0; }
+
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms) {
   const int ntiles = int(n_pad / kBN);
-  const Plan pl = make_plan(1, ntiles, nq_pad / kBM, num_sms, MODE_KDE_GAUSS);
+  const int nqb = nq_pad / kBM;
+  const bool pr = use_pair(nqb);
+  const Plan pl = make_plan(1, ntiles, pr ? nqb / 2 : nqb, pr ? num_sms / 2 : num_sms, MODE_KDE_GAUSS, pr);
   return size_t(pl.ncc) * kColGroups * size_t(nq_pad);
 }
+
+void set_pair_enabled(bool on) { g_pair_enabled = on; }
 
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const QueryOperand& q = *a.qop;
@@ -99,7 +127,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const int ntiles_all = int(a.n_pad / kBN);
   const int ntiles = (ntiles_all + a.tile_stride - 1) / a.tile_stride;
   const int nqb = q.nq_pad / kBM;
-  const Plan pl = make_plan(kblocks, ntiles, nqb, num_sms, a.mode);
+  const bool pr = use_pair(nqb);
+  const int ngroups = pr ? nqb / 2 : nqb;
+  const int nslots = pr ? num_sms / 2 : num_sms;  // CTAs (or CTA pairs) resident at once
+  const Plan pl = make_plan(kblocks, ntiles, ngroups, nslots, a.mode, pr);
 
   TileParams p{};
   p.nq = q.nq;
@@ -126,14 +157,15 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.seg_tiles = a.seg_tiles;
   if (a.ncc_out) *a.ncc_out = pl.ncc;
 
-  const int nunits = nqb * pl.ncc;
-  const int grid = std::min(nunits, num_sms);
+  const int nunits = ngroups * pl.ncc;
+  const int grid = std::min(nunits, nslots) * (pr ? 2 : 1);
+  const CUtensorMap& tb = pr ? e.tmap_half : e.tmap;
   switch (a.mode) {
-    case MODE_KDE_GAUSS: launch_mode<MODE_KDE_GAUSS>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
-    case MODE_KDE_EXP: launch_mode<MODE_KDE_EXP>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
-    case MODE_TILEMIN: launch_mode<MODE_TILEMIN>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
-    case MODE_FILTER: launch_mode<MODE_FILTER>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
-    case MODE_NULL: launch_mode<MODE_NULL>(q.tmap, e.tmap, p, grid, pl.smem, s); break;
+    case MODE_KDE_GAUSS: launch_any<MODE_KDE_GAUSS>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_KDE_EXP: launch_any<MODE_KDE_EXP>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_TILEMIN: launch_any<MODE_TILEMIN>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_FILTER: launch_any<MODE_FILTER>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_NULL: launch_any<MODE_NULL>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     default: throw Error{DK_EINVAL, "bad tile mode"};
   }
 }

@@ -74,9 +74,9 @@ struct TileParams {
   int32_t cap;
 };
 
-__host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode) {
+__host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode, bool pair) {
   size_t a = a_resident ? size_t(kblocks) * kABlockBytes : size_t(stages) * kABlockBytes;
-  size_t b = size_t(stages) * kBBlockBytes;
+  size_t b = size_t(stages) * (pair ? kBBlockBytes / 2 : kBBlockBytes);
   size_t stage = mode == MODE_FILTER ? size_t(kBM) * kStageCap * 8 + kBM * 4 : 0;
   return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + stage + 512 /*barriers*/;
 }
@@ -232,7 +232,14 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32) : "memory"); }
 
-template <int MODE>
+// kPair: a 2-CTA cluster runs tcgen05.mma.cta_group::2 with M = 256 — the two CTAs
+// own two query blocks (128 rows each, A resident in each CTA) and each TMA-loads one
+// half (128 rows) of every 256-row dataset K-block.  Each SM then streams half the B
+// bytes and reads half the B operand per MMA from its shared memory, which is what
+// keeps a single-CTA M=128 sweep below the tensor peak (smem bandwidth).  The leader
+// (rank 0) issues every MMA; stage / accumulator / A releases are multicast commits to
+// both CTAs; both CTAs' epilogue warps arrive on the leader's accumulator-empty barrier.
+template <int MODE, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                 const TileParams p) {
@@ -241,16 +248,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   // compiler keeps the shared address space (LDS/ATOMS instead of generic LD/ATOM)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
+  constexpr int kBStage = kPair ? kBBlockBytes / 2 : kBBlockBytes;  // B bytes per CTA per stage
   uint8_t* smemA = smem;
   uint8_t* smemB = smem + (p.a_resident ? size_t(p.kblocks) * kABlockBytes : size_t(stages) * kABlockBytes);
-  float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBBlockBytes);  // [kXnSlots][256]
+  float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBStage);  // [kXnSlots][256]
   unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smemX + kXnSlots * kBN);  // FILTER staging
   uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (MODE == MODE_FILTER ? kBM * kStageCap : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(scnt + (MODE == MODE_FILTER ? kBM : 0));
-  uint64_t* full_bar = bars;                 // [stages]
+  uint64_t* full_bar = bars;                 // [stages]   (leader's counts both CTAs' bytes)
   uint64_t* empty_bar = bars + stages;       // [stages]
   uint64_t* tfull_bar = bars + 2 * stages;   // [2]
-  uint64_t* tempty_bar = tfull_bar + 2;      // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;      // [2]        (leader's counts both CTAs' warps)
   uint64_t* afull_bar = tempty_bar + 2;      // [1]
   uint64_t* aempty_bar = afull_bar + 1;      // [1]
   uint64_t* xfull_bar = aempty_bar + 1;      // [kXnSlots]
@@ -259,7 +267,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
-  const int nunits = p.nqb * p.ncc;
+  const uint32_t crank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = crank == 0;
+  // work units: (query-block group, column chunk); a pair owns 2 query blocks
+  const int ngroups = kPair ? p.nqb / 2 : p.nqb;
+  const int nunits = ngroups * p.ncc;
+  const int first_unit = kPair ? int(blockIdx.x) / 2 : int(blockIdx.x);
+  const int unit_step = kPair ? int(gridDim.x) / 2 : int(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmapA);
@@ -270,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], kNumEpiWarps);
+      mbar_init(&tempty_bar[a], kPair ? 2 * kNumEpiWarps : kNumEpiWarps);
     }
     mbar_init(afull_bar, 1);
     mbar_init(aempty_bar, 1);
@@ -283,14 +297,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (MODE == MODE_FILTER) {
     for (int i = threadIdx.x; i < kBM; i += blockDim.x) scnt[i] = 0;
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (kPair) tmem_alloc_pair<kTmemCols>(tmem_slot);
+    else tmem_alloc<kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // both CTAs' barriers live before any remote arrive / TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (each CTA) =====================
     if (lane == 0) {
       const uint64_t pol_b = policy_evict_last();   // dataset tiles are re-read by other query blocks
       const uint64_t pol_a = policy_evict_last();
@@ -298,19 +316,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int uiter = 0;
       uint32_t titer = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++uiter) {
-        const int qb = u % p.nqb, cc = u / p.nqb;
+      for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
+        const int qb = (u % ngroups) * (kPair ? 2 : 1) + int(crank), cc = u / ngroups;
         const int t0 = cc * p.tiles_per_unit;
         const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
         if (p.a_resident) {
           mbar_wait(aempty_bar, (uiter & 1) ^ 1);
-          mbar_arrive_expect_tx(afull_bar, uint32_t(p.kblocks) * kABlockBytes);
-          for (int kb = 0; kb < p.kblocks; ++kb)
-            tma_load_2d(smemA + size_t(kb) * kABlockBytes, &tmapA, afull_bar, kb * kBK, qb * kBM, pol_a);
+          if constexpr (kPair) {
+            if (leader) mbar_arrive_expect_tx(afull_bar, 2u * uint32_t(p.kblocks) * kABlockBytes);
+            for (int kb = 0; kb < p.kblocks; ++kb)
+              tma_load_2d_pair(smemA + size_t(kb) * kABlockBytes, &tmapA, afull_bar, kb * kBK, qb * kBM, pol_a);
+          } else {
+            mbar_arrive_expect_tx(afull_bar, uint32_t(p.kblocks) * kABlockBytes);
+            for (int kb = 0; kb < p.kblocks; ++kb)
+              tma_load_2d(smemA + size_t(kb) * kABlockBytes, &tmapA, afull_bar, kb * kBK, qb * kBM, pol_a);
+          }
         }
         for (int t = t0; t < t1; ++t, ++titer) {
           const int col0 = t * p.tile_stride * kBN;
-          {  // column norms of this tile -> smem ring slot
+          {  // column norms of this tile -> own smem ring slot
             const uint32_t xs = titer % kXnSlots;
             mbar_wait(&xempty_bar[xs], ((titer / kXnSlots) & 1) ^ 1);
             mbar_arrive_expect_tx(&xfull_bar[xs], kBN * 4);
@@ -318,31 +342,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           for (int kb = 0; kb < p.kblocks; ++kb) {
             mbar_wait(&empty_bar[stage], phase ^ 1);
-            if (p.a_resident) {
-              mbar_arrive_expect_tx(&full_bar[stage], kBBlockBytes);
+            if constexpr (kPair) {
+              const uint32_t bytes = 2u * (kBStage + (p.a_resident ? 0u : uint32_t(kABlockBytes)));
+              if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
+              if (!p.a_resident)
+                tma_load_2d_pair(smemA + size_t(stage) * kABlockBytes, &tmapA, &full_bar[stage], kb * kBK,
+                                 qb * kBM, pol_a);
+              tma_load_2d_pair(smemB + size_t(stage) * kBStage, &tmapB, &full_bar[stage], kb * kBK,
+                               col0 + int(crank) * (kBN / 2), pol_b);
             } else {
-              mbar_arrive_expect_tx(&full_bar[stage], kBBlockBytes + kABlockBytes);
-              tma_load_2d(smemA + size_t(stage) * kABlockBytes, &tmapA, &full_bar[stage], kb * kBK, qb * kBM,
-                          pol_a);
+              if (p.a_resident) {
+                mbar_arrive_expect_tx(&full_bar[stage], kBBlockBytes);
+              } else {
+                mbar_arrive_expect_tx(&full_bar[stage], kBBlockBytes + kABlockBytes);
+                tma_load_2d(smemA + size_t(stage) * kABlockBytes, &tmapA, &full_bar[stage], kb * kBK, qb * kBM,
+                            pol_a);
+              }
+              tma_load_2d(smemB + size_t(stage) * kBBlockBytes, &tmapB, &full_bar[stage], kb * kBK, col0, pol_b);
             }
-            tma_load_2d(smemB + size_t(stage) * kBBlockBytes, &tmapB, &full_bar[stage], kb * kBK, col0, pol_b);
             if (++stage == stages) { stage = 0; phase ^= 1; }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32(kBM, kBN);
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_f16_f32(kPair ? 2 * kBM : kBM, kBN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       int uiter = 0;
       const uint32_t a0 = smem_u32(smemA), b0 = smem_u32(smemB);
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++uiter) {
-        const int cc = u / p.nqb;
+      for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
+        const int cc = u / ngroups;
         const int t0 = cc * p.tiles_per_unit;
         const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
         if (p.a_resident) {
@@ -357,22 +391,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
             const uint32_t abase = p.a_resident ? a0 + uint32_t(kb) * kABlockBytes : a0 + uint32_t(stage) * kABlockBytes;
-            const uint32_t bbase = b0 + uint32_t(stage) * kBBlockBytes;
+            const uint32_t bbase = b0 + uint32_t(stage) * kBStage;
             const uint64_t ad = sw128_kmajor_desc(abase), bd = sw128_kmajor_desc(bbase);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              mma_f16_ss(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
-            mma_commit(&empty_bar[stage]);
+            for (int k = 0; k < kBK / 16; ++k) {
+              if constexpr (kPair) mma_f16_ss_pair(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+              else mma_f16_ss(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+            }
+            if constexpr (kPair) mma_commit_pair_mc(&empty_bar[stage], uint16_t(0x3));
+            else mma_commit(&empty_bar[stage]);
             if (++stage == stages) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&tfull_bar[acc]);
+          if constexpr (kPair) mma_commit_pair_mc(&tfull_bar[acc], uint16_t(0x3));
+          else mma_commit(&tfull_bar[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        if (p.a_resident) mma_commit(aempty_bar);
+        if (p.a_resident) {
+          if constexpr (kPair) mma_commit_pair_mc(aempty_bar, uint16_t(0x3));
+          else mma_commit(aempty_bar);
+        }
       }
     }
   } else if (warp >= kEpiWarp0) {
-    // ===================== epilogue =====================
+    // ===================== epilogue (each CTA, its own 128 rows) =====================
     const int ew = int(warp) - kEpiWarp0;
     const int quarter = int(warp & 3);
     const int cg = ew >> 2;  // 64-column group of the tile
@@ -382,8 +423,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t titer = 0;
     const float m2s = *p.m2s;
     const float negc = p.negc;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      const int qb = u % p.nqb, cc = u / p.nqb;
+    for (int u = first_unit; u < nunits; u += unit_step) {
+      const int qb = (u % ngroups) * (kPair ? 2 : 1) + int(crank), cc = u / ngroups;
       const int t0 = cc * p.tiles_per_unit;
       const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
       const int row = qb * kBM + lrow;
@@ -414,7 +455,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_cluster(&tempty_bar[acc], 0u);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
         if constexpr (MODE == MODE_NULL) {  // pipeline probe: consume the accumulator, no epilogue math
@@ -466,11 +510,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // no remote arrive / MMA write may target an exited CTA
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    if constexpr (kPair) tmem_dealloc_pair<kTmemCols>(tmem_base);
+    else tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 
