@@ -159,6 +159,26 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family,
                    int64_t query_base, double* value_out, int64_t* nbr_idx_out,
                    double* nbr_d2_out, int64_t* sample_idx_out, void* stream);
 
+/* ---- permuted sampler (RSP / DEANNP) -----------------------
+ * RspState (estimators.py:83-96) on the device: `h` is a dataset fitted on the
+ * PERMUTED rows (row i = original row permutation[i], permute data.py:214-233);
+ * attach its inverse permutation (original id -> permuted position, n int64). */
+dk_status dk_rsp_attach(dk_handle h, const int64_t* inverse_permutation);
+
+/* Permuted-window sampler over a query batch: rsp_kde (estimators.py:180-200),
+ * _rsp_excluding (:249-303) and deann_batch's cursor threading (:394-409).
+ * Query j walks the permuted rows from its start, skipping rows whose ORIGINAL id
+ * is in excl[j*excl_stride ..+excl_stride) (nullable), until m rows are accepted
+ * or one full pass completes.  Starts: independent != 0 -> floor(j*n/nq)
+ * (independent_cursors=True); else start_0 = cursor_in, start_{j+1} = start_j +
+ * rows consumed by query j (mod n).  Outputs: z_sum[j] = fp64 kernel sum over the
+ * accepted rows, taken[j] = accepted count (< m: clamped to one full pass),
+ * *cursor_out = the shared cursor after the batch (cursor_in if independent). */
+dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth,
+                      int32_t m, const int64_t* excl, int32_t excl_stride, int64_t cursor_in,
+                      int32_t independent, double* z_sum, int32_t* taken, int64_t* cursor_out,
+                      void* stream);
+
 /* Timing support for bench.py: average device duration (ms) of the LAST launch
  * of the dominant kernel of the last call on this handle (CUDA events on the
  * launching stream) and its algorithmic work. */

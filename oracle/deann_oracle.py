@@ -259,3 +259,120 @@ def deann_batch(data: Data, family: str, h: float, neighbors, queries, k: int, m
     """estimators.py:382-410 (uniform sampler): a loop of deann in query order."""
     q = np.atleast_2d(np.asarray(queries, dtype=np.float64))
     return [deann(data, family, h, neighbors, q[j], k, m, rng=rng)[0] for j in range(q.shape[0])]
+
+
+# ---------------------------------------------------------------- permuted sampler (RSP / DEANNP)
+
+
+class Permuted:
+    """PermutedDataset + RspState cursor (data.py:103-117, 214-233; estimators.py:83-96)."""
+
+    def __init__(self, data: "Data", seed: int, cursor: int = 0):
+        rng = np.random.default_rng(seed)
+        self.perm = rng.permutation(data.n).astype(np.int64)        # data.py:226
+        self.inverse = np.empty_like(self.perm)
+        self.inverse[self.perm] = np.arange(data.n, dtype=np.int64)  # data.py:227-228
+        self.base = Data(data.x32[self.perm])                        # rows move with the permutation
+        self.cursor = int(cursor)
+
+    @property
+    def n(self) -> int:
+        return self.base.n
+
+
+def window_ranges(n: int, start: int, count: int):
+    """distance.py:88-98"""
+    if start + count <= n:
+        return [(start, start + count)]
+    return [(start, n), (0, start + count - n)]
+
+
+def _block_values(base: Data, family: str, h: float, y: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """estimators.py:236-246 (one matvec per contiguous block)."""
+    if family == "laplacian":
+        return kernel_from_distance(family, h, np.abs(base.x64[lo:hi] - y).sum(axis=1))
+    d2 = base.x64[lo:hi] @ y
+    d2 *= -2.0
+    d2 += base.sq_norms[lo:hi]
+    d2 += float(y @ y)
+    np.maximum(d2, 0.0, out=d2)
+    return kernel_from_sql2(family, h, d2)
+
+
+def rsp_kde(state: Permuted, family: str, h: float, query, m: int) -> float:
+    """estimators.py:180-200: mean over the next m permuted rows (wrapping); cursor += m."""
+    n = state.n
+    if not 1 <= m <= n:
+        raise ValueError(f"m={m} out of range [1, {n}]")
+    y = np.asarray(query, dtype=np.float64).ravel()
+    total = sum(float(_block_values(state.base, family, h, y, lo, hi).sum())
+                for lo, hi in window_ranges(n, state.cursor, m))
+    state.cursor = (state.cursor + m) % n
+    return total / m
+
+
+def rsp_excluding(state: Permuted, family: str, h: float, y, m: int, exclude, n_excluded: int):
+    """estimators.py:249-303: walk from the cursor skipping excluded ORIGINAL ids until m
+    rows are accepted or a full pass completes; the cursor advances past skipped rows."""
+    n = state.n
+    if n_excluded == 0:
+        count = min(m, n)
+        total = sum(float(_block_values(state.base, family, h, y, lo, hi).sum())
+                    for lo, hi in window_ranges(n, state.cursor, count))
+        state.cursor = (state.cursor + count) % n
+        return total / count, count, count < m
+    perm = state.perm
+    advanced = taken = 0
+    total = 0.0
+    while taken < m and advanced < n:
+        pos = (state.cursor + advanced) % n
+        chunk = min(n - advanced, max(m - taken + 64, 64))
+        consumed = chunk
+        for lo, hi in window_ranges(n, pos, chunk):
+            keep = ~exclude[perm[lo:hi]]
+            kept = int(np.count_nonzero(keep))
+            need = m - taken
+            if kept >= need:
+                cut = int(np.flatnonzero(keep)[need - 1]) + 1
+                keep = keep[:cut]
+                hi = lo + cut
+                consumed = (lo - pos) % n + cut
+                kept = need
+            if kept:
+                vals = _block_values(state.base, family, h, y, lo, hi)
+                total += float(vals[keep].sum())
+                taken += kept
+            if taken == m:
+                break
+        advanced += consumed
+    state.cursor = (state.cursor + advanced) % n
+    if taken == 0:
+        return 0.0, 0, True
+    return total / taken, taken, taken < m
+
+
+def deann_rsp(data: Data, family: str, h: float, neighbors, query, k: int, m: int, state: Permuted):
+    """estimators.py:306-379 with the permuted sampler.  Returns (value, evals, k_hat, used, truncated, clamped)."""
+    n = data.n
+    if state.n != n:
+        raise ValueError("rsp_state was built for a different dataset size")
+    y = np.asarray(query, dtype=np.float64).ravel()
+    if k > 0:
+        idx, sqd = neighbors(y, k)
+        x1 = np.asarray(idx, dtype=np.int64)
+    else:
+        x1, sqd = np.empty(0, dtype=np.int64), None
+    k_hat = len(x1)
+    if k_hat == 0:
+        z1 = 0.0
+    elif family == "laplacian":
+        z1 = float(kernel_rows(data.x64, data.sq_norms, family, h, x1, y).mean())
+    else:
+        z1 = float(kernel_from_sql2(family, h, np.asarray(sqd, dtype=np.float64)).mean())
+    if m == 0:
+        return (k_hat / n) * z1, k_hat, k_hat, 0, k_hat < n, False
+    exclude = np.zeros(n, dtype=bool)
+    exclude[x1] = True
+    z2, used, clamped = rsp_excluding(state, family, h, y, m, exclude if k_hat else None, k_hat)
+    value = (k_hat / n) * z1 + ((n - k_hat) / n) * z2
+    return value, k_hat + used, k_hat, used, False, clamped

@@ -11,10 +11,11 @@ All arithmetic runs in hand-written sm_100a kernels behind the C-ABI in
 
 from .ann import AnnIndex, BruteForceIndex, GpuBruteForceIndex, NeighborList, brute_force_knn, knn_batch
 from .bandwidth import fit_bandwidth, NoBandwidthError
-from .data import Dataset, as_gpu_dataset
+from .data import Dataset, PermutedDataset, as_gpu_dataset, permute
 from .estimators import (
     BatchKde,
     Estimate,
+    RspState,
     deann,
     deann_arrays,
     deann_batch,
@@ -22,6 +23,7 @@ from .estimators import (
     naive_kde,
     naive_kde_into,
     rs_kde,
+    rsp_kde,
 )
 from .kernels import KernelFamily, KernelSpec
 from .sampler import PhiloxSampler
@@ -30,7 +32,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AnnIndex", "BruteForceIndex", "GpuBruteForceIndex", "NeighborList", "brute_force_knn", "knn_batch",
-    "fit_bandwidth", "NoBandwidthError", "Dataset", "as_gpu_dataset", "BatchKde", "Estimate", "deann",
+    "fit_bandwidth", "NoBandwidthError", "Dataset", "PermutedDataset", "permute", "as_gpu_dataset", "BatchKde",
+    "Estimate", "RspState", "rsp_kde", "deann",
     "deann_arrays", "deann_batch", "kernel_from_distance", "naive_kde", "naive_kde_into", "rs_kde",
     "KernelFamily", "KernelSpec", "PhiloxSampler",
 ]

@@ -26,7 +26,7 @@ DK_OUT_SUM = 1
 EXPORTED = (
     "dk_version", "dk_last_error", "dk_device_ok", "dk_fit", "dk_free", "dk_info", "dk_sq_norms",
     "dk_naive", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
-    "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
+    "dk_rsp_attach", "dk_rsp_walk", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
 )
 
 
@@ -71,6 +71,9 @@ def _declare(lib):
         "dk_eval_rows": (_i32, [_vp, _vp, _i64, _i32, _f64, _vp, _vp, _i32, _vp, _vp]),
         "dk_kernel_values": (_i32, [_i32, _f64, _vp, _i64, _vp, _vp]),
         "dk_deann": (_i32, [_vp, _vp, _i64, _i32, _f64, _i32, _i32, _u64, _i64, _vp, _vp, _vp, _vp, _vp]),
+        "dk_rsp_attach": (_i32, [_vp, _vp]),
+        "dk_rsp_walk": (_i32, [_vp, _vp, _i64, _i32, _f64, _i32, _vp, _i32, _i64, _i32, _vp, _vp,
+                                ctypes.POINTER(_i64), _vp]),
         "dk_last_kernel_ms": (_i32, [_vp, ctypes.POINTER(_f64), ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
         "dk_set_profiling": (_i32, [_vp, _i32]),
         "dk_last_launch_count": (_i32, [_vp, ctypes.POINTER(_i64)]),

@@ -469,6 +469,7 @@ dk_status dk_free(dk_handle h) {
     if (h->X) cudaFree(h->X);
     if (h->xn64) cudaFree(h->xn64);
     if (h->mu) cudaFree(h->mu);
+    if (h->rsp_inverse) cudaFree(h->rsp_inverse);
     for (auto& pr : h->prof_events) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
@@ -802,6 +803,69 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     if (k > 0 && nbr_d2_out) { copy_out(nbr_d2_out, d2, size_t(nq) * k * sizeof(double), s); sync = true; }
     if (accd && !acc_dev && m > 0) { copy_out(sample_idx_out, accd, size_t(nq) * m * sizeof(int64_t), s); sync = true; }
     if (sync) DK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+dk_status dk_rsp_attach(dk_handle h, const int64_t* inverse_permutation) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr && inverse_permutation != nullptr, "NULL argument");
+    DeviceGuard g(h->device);
+    if (!h->rsp_inverse) DK_CUDA(cudaMalloc(&h->rsp_inverse, size_t(h->n) * sizeof(int64_t)));
+    DK_CUDA(cudaMemcpy(h->rsp_inverse, inverse_permutation, size_t(h->n) * sizeof(int64_t), cudaMemcpyDefault));
+  });
+}
+
+dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t m,
+                      const int64_t* excl, int32_t excl_stride, int64_t cursor_in, int32_t independent,
+                      double* z_sum, int32_t* taken, int64_t* cursor_out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    check_family_bw(family, bandwidth);
+    DK_REQUIRE(m >= 1, "m=" + std::to_string(m) + " must be >= 1");
+    DK_REQUIRE(cursor_in >= 0 && cursor_in < h->n, "cursor out of range [0, n)");
+    DK_REQUIRE(!excl || (excl_stride >= 1 && excl_stride < h->n), "exclusion list must hold 1..n-1 ids");
+    DK_REQUIRE(!excl || h->rsp_inverse != nullptr, "dk_rsp_attach must be called before excluding ids");
+    DK_REQUIRE(nq >= 0, "negative query count");
+    if (cursor_out) *cursor_out = cursor_in;
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && z_sum != nullptr, "NULL argument");
+    DeviceGuard g(h->device);
+    LaunchCount lc(h);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int32_t cnt = excl ? excl_stride : 0;
+    Plan pl;
+    const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
+    const size_t o_ex = pl.add<int64_t>(size_t(nq) * std::max(cnt, 1));
+    const size_t o_pos = pl.add<int64_t>(size_t(nq) * std::max(cnt, 1));
+    const size_t o_start = pl.add<int64_t>(size_t(nq));
+    const size_t o_len = pl.add<int64_t>(size_t(nq));
+    const size_t o_taken = pl.add<int32_t>(size_t(nq));
+    const size_t o_z = pl.add<double>(size_t(nq));
+    const size_t o_cur = pl.add<int64_t>(1);
+    h->ws.reserve(pl.off);
+    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
+    int64_t* pos = nullptr;
+    if (excl) {
+      int64_t* ex = at<int64_t>(h->ws, o_ex);
+      DK_CUDA(cudaMemcpyAsync(ex, excl, size_t(nq) * cnt * sizeof(int64_t), cudaMemcpyDefault, s));
+      pos = at<int64_t>(h->ws, o_pos);
+      launch_rsp_map_sort(ex, cnt, h->rsp_inverse, nq, pos, s);
+    }
+    int64_t* start = at<int64_t>(h->ws, o_start);
+    int64_t* len = at<int64_t>(h->ws, o_len);
+    int32_t* tk = at<int32_t>(h->ws, o_taken);
+    int64_t* cur = at<int64_t>(h->ws, o_cur);
+    launch_rsp_starts(pos, cnt, nq, h->n, m, cursor_in, independent != 0, start, len, tk, cur, s);
+    const bool z_dev = is_device_ptr(z_sum);
+    double* zd = z_dev ? z_sum : at<double>(h->ws, o_z);
+    {
+      ProfScope ps(h, s, 0.0, double(nq) * m * h->d * 4.0);
+      launch_rsp_eval(h->X, h->n, h->d, Qd, nq, family, bandwidth, pos, cnt, start, len, zd, s);
+    }
+    if (!z_dev) copy_out(z_sum, zd, size_t(nq) * sizeof(double), s);
+    if (taken) copy_out(taken, tk, size_t(nq) * sizeof(int32_t), s);
+    if (cursor_out && !independent) copy_out(cursor_out, cur, sizeof(int64_t), s);
+    DK_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -103,6 +103,7 @@ struct dk_dataset {
   dk::Encoding enc_fp16;    // mode 2 (opt-in)
   dk::Workspace ws;
   double* mu = nullptr;     // [d] column means (split/fp16 centring)
+  int64_t* rsp_inverse = nullptr;  // [n] original id -> permuted position (dk_rsp_attach)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   bool profiling = false;
@@ -193,6 +194,14 @@ void launch_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_
                        int64_t* idx_out, double* d2_out, cudaStream_t s);
 void launch_kernel_values(int32_t family, double h, const double* dist, int64_t count, double* out, uint32_t* bad,
                           cudaStream_t s);
+void launch_rsp_map_sort(const int64_t* excl, int32_t stride, const int64_t* inverse, int64_t nq, int64_t* pos,
+                         cudaStream_t s);
+void launch_rsp_starts(const int64_t* pos, int32_t cnt, int64_t nq, int64_t n, int64_t m, int64_t cursor_in,
+                       bool independent, int64_t* start, int64_t* len, int32_t* taken, int64_t* cursor_out,
+                       cudaStream_t s);
+void launch_rsp_eval(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, int32_t family,
+                     double bandwidth, const int64_t* pos, int32_t cnt, const int64_t* start, const int64_t* len,
+                     double* z_sum, cudaStream_t s);
 void launch_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m, int64_t n_total,
                           const double* nbr_d2, const double* z1_l1_sum, const double* z2_sum, double* value,
                           cudaStream_t s);

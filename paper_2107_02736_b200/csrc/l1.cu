@@ -4,7 +4,7 @@
 // sum_i exp(-sum_k |x_ik - y_k| / h) over row blocks, then / n.  L1 is not a
 // contraction, so it cannot use the tensor cores; this is a register-tiled
 // SIMT kernel: a 64-query x 128-row tile per block, 4x8 outputs per thread,
-// 32-dimension smem chunks, fp32 |a-b| accumulation with per-chunk partial
+// 16-dimension double-buffered smem chunks, fp32 |a-b| accumulation with per-chunk partial
 // sums, ex2.approx epilogue, fp32 per-tile row sums folded into fp64.
 #include "internal.h"
 #include "ptx.cuh"
@@ -13,17 +13,22 @@ namespace dk {
 
 namespace {
 
-constexpr int TQ = 64, TX = 128, DK = 32, XPAD = 4;
+constexpr int TQ = 64, TX = 128, DK = 16, XPAD = 4;
 constexpr int kTilesPerBlock = 8;
 
-__global__ void __launch_bounds__(256) l1_kde_kernel(const float* __restrict__ X, int64_t n, int32_t d,
-                                                      const double* __restrict__ Q, int64_t nq, int32_t nq_pad,
-                                                      float negc, double* __restrict__ part) {
-  __shared__ __align__(16) float Qs[DK][TQ];
-  __shared__ __align__(16) float Xs[DK][TX + XPAD];
+__global__ void __launch_bounds__(256, 2) l1_kde_kernel(const float* __restrict__ X, int64_t n, int32_t d,
+                                                         const double* __restrict__ Q, int64_t nq, int32_t nq_pad,
+                                                         float negc, double* __restrict__ part) {
+  // double-buffered smem tiles, transposed to [k][row] so each thread reads its 4 queries
+  // and 8 rows of one dimension with 3 LDS.128; the next chunk is fetched into registers
+  // while the current one is consumed
+  __shared__ __align__(16) float Qs[2][DK][TQ];
+  __shared__ __align__(16) float Xs[2][DK][TX + XPAD];
+  constexpr int QL = (TQ * DK) / 256, XL = (TX * DK) / 256;  // per-thread staged loads
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t q0 = int64_t(blockIdx.x) * TQ;
   const int64_t tile0 = int64_t(blockIdx.y) * kTilesPerBlock;
+  const int nchunks = (d + DK - 1) / DK;
   double qacc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int xt = 0; xt < kTilesPerBlock; ++xt) {
     const int64_t x0 = (tile0 + xt) * TX;
@@ -33,23 +38,41 @@ __global__ void __launch_bounds__(256) l1_kde_kernel(const float* __restrict__ X
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-    for (int k0 = 0; k0 < d; k0 += DK) {
-      // stage Q (fp64 -> fp32) and X chunks, transposed to [k][row]
+    float qreg[QL], xreg[XL];
+    auto fetch = [&](int k0) {
 #pragma unroll
-      for (int r = 0; r < (TQ * DK) / 256; ++r) {
+      for (int r = 0; r < QL; ++r) {
         const int e = r * 256 + threadIdx.x;
         const int qq = e / DK, kk = e % DK;
         const int64_t qi = q0 + qq;
-        Qs[kk][qq] = (qi < nq && k0 + kk < d) ? float(Q[qi * d + k0 + kk]) : 0.f;
+        qreg[r] = (qi < nq && k0 + kk < d) ? float(Q[qi * d + k0 + kk]) : 0.f;
       }
 #pragma unroll
-      for (int r = 0; r < (TX * DK) / 256; ++r) {
+      for (int r = 0; r < XL; ++r) {
         const int e = r * 256 + threadIdx.x;
         const int xx = e / DK, kk = e % DK;
         const int64_t xi = x0 + xx;
-        Xs[kk][xx] = (xi < n && k0 + kk < d) ? __ldg(X + xi * d + k0 + kk) : 0.f;
+        xreg[r] = (xi < n && k0 + kk < d) ? __ldg(X + xi * d + k0 + kk) : 0.f;
       }
-      __syncthreads();
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+      for (int r = 0; r < QL; ++r) {
+        const int e = r * 256 + threadIdx.x;
+        Qs[buf][e % DK][e / DK] = qreg[r];
+      }
+#pragma unroll
+      for (int r = 0; r < XL; ++r) {
+        const int e = r * 256 + threadIdx.x;
+        Xs[buf][e % DK][e / DK] = xreg[r];
+      }
+    };
+    fetch(0);
+    stash(0);
+    __syncthreads();
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      if (c + 1 < nchunks) fetch((c + 1) * DK);  // in flight during the compute below
       float part_acc[4][8];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -57,9 +80,9 @@ __global__ void __launch_bounds__(256) l1_kde_kernel(const float* __restrict__ X
         for (int j = 0; j < 8; ++j) part_acc[i][j] = 0.f;
 #pragma unroll 4
       for (int kk = 0; kk < DK; ++kk) {
-        const float4 qv = *reinterpret_cast<const float4*>(&Qs[kk][ty * 4]);
-        const float4 xa = *reinterpret_cast<const float4*>(&Xs[kk][tx * 8]);
-        const float4 xb = *reinterpret_cast<const float4*>(&Xs[kk][tx * 8 + 4]);
+        const float4 qv = *reinterpret_cast<const float4*>(&Qs[buf][kk][ty * 4]);
+        const float4 xa = *reinterpret_cast<const float4*>(&Xs[buf][kk][tx * 8]);
+        const float4 xb = *reinterpret_cast<const float4*>(&Xs[buf][kk][tx * 8 + 4]);
         const float qs[4] = {qv.x, qv.y, qv.z, qv.w};
         const float xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
@@ -71,6 +94,7 @@ __global__ void __launch_bounds__(256) l1_kde_kernel(const float* __restrict__ X
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] += part_acc[i][j];
+      if (c + 1 < nchunks) stash(buf ^ 1);
       __syncthreads();
     }
 #pragma unroll

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["Dataset", "as_gpu_dataset"]
+__all__ = ["Dataset", "as_gpu_dataset", "PermutedDataset", "permute", "as_gpu_permuted"]
 
 _PRECISION = {"auto": _lib.DK_PREC_AUTO, "split3": _lib.DK_PREC_SPLIT3, "fp16": _lib.DK_PREC_FP16}
 
@@ -125,3 +125,54 @@ def as_gpu_dataset(dataset) -> Dataset:
     except TypeError:
         pass
     return gpu
+
+
+class PermutedDataset:
+    """Rows reordered by a stored permutation (data.py:103-117), fitted on the device.
+
+    ``base`` holds row ``permutation[i]`` of the original at position i, so the
+    permuted sampler's windows are contiguous row ranges on the GPU; the inverse
+    permutation (original id -> position) is attached to the base handle for
+    excluding neighbour ids (dk_rsp_attach).
+    """
+
+    def __init__(self, base: Dataset, permutation: np.ndarray, inverse_permutation: np.ndarray):
+        self.base = base
+        self.permutation = permutation
+        self.inverse_permutation = inverse_permutation
+        inv = np.ascontiguousarray(inverse_permutation, dtype=np.int64)
+        _lib.check(_lib.load().dk_rsp_attach(base.handle, inv.ctypes.data))
+
+    @property
+    def n(self) -> int:
+        return self.base.n
+
+
+def permute(dataset, seed: int) -> PermutedDataset:
+    """Seeded Fisher-Yates reordering with numpy's PCG64, exactly as data.py:214-233."""
+    ds = as_gpu_dataset(dataset)
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(ds.n).astype(np.int64)
+    inverse = np.empty_like(perm)
+    inverse[perm] = np.arange(ds.n, dtype=np.int64)
+    perm.flags.writeable = False
+    inverse.flags.writeable = False
+    base = Dataset.from_array(ds.data[perm], device=ds.device, precision=ds.precision)
+    return PermutedDataset(base, perm, inverse)
+
+
+_PCACHE: "weakref.WeakKeyDictionary[object, PermutedDataset]" = weakref.WeakKeyDictionary()
+
+
+def as_gpu_permuted(permuted) -> PermutedDataset:
+    """This package's PermutedDataset, or a cached device fit of the reference's one."""
+    if isinstance(permuted, PermutedDataset):
+        return permuted
+    cached = _PCACHE.get(permuted)
+    if cached is not None:
+        return cached
+    base = Dataset.from_array(np.asarray(permuted.base.data))
+    out = PermutedDataset(base, np.asarray(permuted.permutation, dtype=np.int64),
+                          np.asarray(permuted.inverse_permutation, dtype=np.int64))
+    _PCACHE[permuted] = out
+    return out

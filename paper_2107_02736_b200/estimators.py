@@ -10,28 +10,33 @@ kernels behind the C-ABI:
 * rs_kde     -> dk_sample without exclusions (Philox-indexed gather);
 * deann      -> dk_deann (exact k-NN + exclusion sampling + combine) when the
   index is the GPU brute force; any other AnnIndex is queried as a black box
-  and its neighbours drive dk_sample / dk_eval_rows / dk_kernel_values.
+  and its neighbours drive dk_sample / dk_eval_rows / dk_kernel_values;
+* rsp_kde / deann(rsp_state=) -> dk_rsp_walk: the permuted sampler streams
+  contiguous windows of the device-resident permuted rows (rsp.cu), with the
+  reference's cursor semantics (shared threading or independent cursors).
 
-Differences to the reference, by design: the uniform sampler is a
-counter-based Philox stream per query (sampler.py) instead of numpy's PCG64,
-and ``rsp_state`` (the permuted sampler) is not accelerated
-yet and raises NotImplementedError.
+Difference to the reference, by design: the uniform sampler is a
+counter-based Philox stream per query (sampler.py) instead of numpy's PCG64.
+The permuted sampler is deterministic and matches the reference exactly
+(same PCG64 permutation, same cursor arithmetic).
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
 from .ann import GpuBruteForceIndex
-from .data import Dataset, as_gpu_dataset
+from .data import Dataset, PermutedDataset, as_gpu_dataset, as_gpu_permuted, permute
 from .kernels import KernelFamily, as_spec
 from .sampler import resolve_sampler
 
 __all__ = [
-    "Estimate", "BatchKde", "naive_kde", "rs_kde", "deann", "deann_batch",
+    "Estimate", "BatchKde", "RspState", "naive_kde", "rs_kde", "rsp_kde", "deann", "deann_batch",
     "naive_kde_into", "deann_arrays", "kernel_from_distance",
 ]
 
@@ -137,6 +142,68 @@ def rs_kde(dataset, kernel, query, m: int, rng) -> Estimate:
     return Estimate(value=float(z[0] / m), kernel_evals=m, neighbors_used=0, samples_used=m)
 
 
+# ---------------------------------------------------------------- permuted sampler
+
+
+@dataclass
+class RspState:
+    """Permuted copy of the data plus the running cursor (estimators.py:83-96)."""
+
+    permuted: PermutedDataset
+    cursor: int = 0
+
+    @classmethod
+    def from_dataset(cls, dataset, seed: int, cursor: int = 0) -> "RspState":
+        return cls(permuted=permute(dataset, seed), cursor=cursor)
+
+    @property
+    def n(self) -> int:
+        return self.permuted.n
+
+
+def _rsp_walk(state, spec, q: np.ndarray, m: int, excl, independent: bool):
+    """One dk_rsp_walk over a query batch; updates the shared cursor (unless independent)."""
+    pds = as_gpu_permuted(state.permuted)
+    nq = q.shape[0]
+    z = np.empty(nq, dtype=np.float64)
+    taken = np.empty(nq, dtype=np.int32)
+    cur = ctypes.c_int64()
+    ex = None if excl is None else np.ascontiguousarray(excl, dtype=np.int64)
+    _lib.check(_lib.load().dk_rsp_walk(pds.base.handle, q.ctypes.data, nq, _lib.family_code(spec.family),
+                                       spec.bandwidth, m, _lib.ptr(ex), 0 if ex is None else ex.shape[1],
+                                       int(state.cursor), 1 if independent else 0, z.ctypes.data, taken.ctypes.data,
+                                       ctypes.byref(cur), _lib.current_stream()))
+    if not independent:
+        state.cursor = int(cur.value)
+    return z, taken
+
+
+def rsp_kde(state, kernel, query, m: int) -> Estimate:
+    """Permuted contiguous sampling: mean over the next m permuted rows, cursor += m (estimators.py:180-200)."""
+    n = state.n
+    if not 1 <= m <= n:
+        raise ValueError(f"m={m} out of range [1, {n}]")
+    spec = as_spec(kernel)
+    pds = as_gpu_permuted(state.permuted)
+    y = _query64(query, pds.base.d).reshape(1, -1)
+    z, _ = _rsp_walk(state, spec, y, m, None, False)
+    return Estimate(value=float(z[0] / m), kernel_evals=m, neighbors_used=0, samples_used=m)
+
+
+def _z1_from_neighbors(ds: Dataset, spec, q: np.ndarray, idx: np.ndarray, d2: np.ndarray) -> np.ndarray:
+    """Z1 per query: kernel of the exact neighbour distances (L2 families, estimators.py:349-351)
+    or re-evaluated L1 (laplacian, :346-348), on the device."""
+    nq, k = idx.shape
+    if spec.family is KernelFamily.LAPLACIAN:
+        out = np.empty(nq, dtype=np.float64)
+        r = np.ascontiguousarray(idx, dtype=np.int64)
+        _lib.check(_lib.load().dk_eval_rows(ds.handle, q.ctypes.data, nq, _lib.DK_LAPLACIAN, spec.bandwidth,
+                                            r.ctypes.data, None, k, out.ctypes.data, None))
+        return out / k
+    dist = d2 if spec.family is KernelFamily.GAUSSIAN else np.sqrt(d2)
+    return kernel_from_distance(spec, dist).reshape(nq, k).mean(axis=1)
+
+
 # ---------------------------------------------------------------- DEANN
 
 
@@ -194,7 +261,7 @@ def deann(dataset, kernel, ann, query, k: int, m: int, *, rng=None, rsp_state=No
     _validate(n, ds.d, k, m, rng, rsp_state)
     y = _query64(query, ds.d)
     if rsp_state is not None and m > 0:
-        raise NotImplementedError("the permuted sampler (rsp_state=) is not GPU-accelerated yet (SURVEY §8 f1)")
+        return _deann_rsp(ds, spec, ann, y.reshape(1, -1), k, m, rsp_state, False)[0]
     seed, base = resolve_sampler(rng).take(1) if (m > 0) else (0, 0)
     if k == 0 or _is_gpu_bruteforce(ann, ds):
         values, _, _ = deann_arrays(ds, spec, y.reshape(1, -1), k, m, seed=seed, query_base=base)
@@ -235,10 +302,49 @@ def deann_batch(dataset, kernel, ann, queries, k: int, m: int, *, rng=None, rsp_
     n = ds.n
     _validate(n, ds.d, k, m, rng, rsp_state)
     if rsp_state is not None and m > 0:
-        raise NotImplementedError("the permuted sampler (rsp_state=) is not GPU-accelerated yet (SURVEY §8 f1)")
+        return _deann_rsp(ds, spec, ann, q, k, m, rsp_state, independent_cursors)
     if k == 0 or _is_gpu_bruteforce(ann, ds):
         seed, base = resolve_sampler(rng).take(q.shape[0]) if m > 0 else (0, 0)
         values, _, _ = deann_arrays(ds, spec, q, k, m, seed=seed, query_base=base)
         return [Estimate(value=float(v), kernel_evals=k + m, neighbors_used=k, samples_used=m,
                          truncated=(m == 0 and k < n)) for v in values]
     return [deann(ds, spec, ann, q[j], k, m, rng=rng, rsp_state=rsp_state) for j in range(q.shape[0])]
+
+
+def _deann_rsp(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, state, independent: bool) -> list[Estimate]:
+    """DEANN with the permuted sampler over a query batch (DEANNP; estimators.py:306-379, 249-303, 394-409)."""
+    n = ds.n
+    nq = q.shape[0]
+    if k > 0 and _is_gpu_bruteforce(ann, ds):
+        from .ann import knn_batch
+
+        idx, d2 = knn_batch(ds, q, k)
+        z1 = _z1_from_neighbors(ds, spec, q, idx, d2)
+        k_hat = np.full(nq, k)
+    elif k > 0:  # black-box index: one query at a time, lists may be shorter than k
+        if nq != 1:
+            return [_deann_rsp(ds, spec, ann, q[j:j + 1], k, m, state, False)[0] if not independent else
+                    _deann_rsp_indep(ds, spec, ann, q, j, k, m, state) for j in range(nq)]
+        nb = ann.query(q[0], k)
+        x1 = np.asarray(nb.indices, dtype=np.int64)
+        if len(x1) == 0:
+            return _deann_rsp(ds, spec, None, q, 0, m, state, independent)
+        idx = x1.reshape(1, -1)
+        d2 = np.asarray(nb.sq_distances, dtype=np.float64).reshape(1, -1)
+        z1 = _z1_from_neighbors(ds, spec, q, idx, d2)
+        k_hat = np.full(1, len(x1))
+    else:
+        idx, z1, k_hat = None, np.zeros(nq), np.zeros(nq, dtype=np.int64)
+    z, taken = _rsp_walk(state, spec, q, m, idx, independent)
+    out = []
+    for j in range(nq):
+        kh, t = int(k_hat[j]), int(taken[j])
+        z2 = z[j] / t if t else 0.0
+        value = (kh / n) * float(z1[j]) + ((n - kh) / n) * z2
+        out.append(Estimate(value=value, kernel_evals=kh + t, neighbors_used=kh, samples_used=t, clamped=t < m))
+    return out
+
+
+def _deann_rsp_indep(ds, spec, ann, q, j, k, m, state):
+    sub = RspState(permuted=as_gpu_permuted(state.permuted), cursor=(j * state.n) // q.shape[0])
+    return _deann_rsp(ds, spec, ann, q[j:j + 1], k, m, sub, False)[0]

@@ -121,6 +121,34 @@ def main():
     out["lim_naive"] = np.array([deann.naive_kde(ds, ks("gaussian", 1.4), q.reshape(1, -1)).values[0]])
     out["lim_kn"] = np.array([deann.deann(ds, ks("gaussian", 1.4), deann.BruteForceIndex(ds), q, 80, 0).value])
 
+    # --- permuted sampler: rsp_kde sequences, DEANNP with brute force, deann_batch cursors
+    X = _random_dataset(300, 5, 50)
+    Q = np.random.default_rng(51).normal(size=(5, 5))
+    ds = deann.Dataset.from_array(X)
+    bf = deann.BruteForceIndex(ds)
+    rsp_vals, rsp_cur, dp_vals, dp_cur, dp_used = [], [], [], [], []
+    for fi, (fam, h) in enumerate([("gaussian", 1.1), ("exponential", 0.8), ("laplacian", 2.3)]):
+        st = deann.RspState.from_dataset(ds, 60 + fi, cursor=37 * fi)
+        for j, q in enumerate(Q):
+            rsp_vals.append(deann.rsp_kde(st, ks(fam, h), q, [17, 100, 299, 1, 64][j]).value)
+            rsp_cur.append(st.cursor)
+        st = deann.RspState.from_dataset(ds, 70 + fi, cursor=290)
+        for j, q in enumerate(Q):
+            e = deann.deann(ds, ks(fam, h), bf, q, [10, 0, 25, 299, 5][j], [40, 30, 280, 1, 0][j], rsp_state=st)
+            dp_vals.append(e.value)
+            dp_used.append([e.samples_used, int(e.clamped), int(e.truncated)])
+            dp_cur.append(st.cursor)
+    shared = deann.RspState.from_dataset(ds, 80, cursor=123)
+    batch = deann.deann_batch(ds, ks("gaussian", 1.1), bf, Q, 12, 50, rsp_state=shared)
+    indep = deann.deann_batch(ds, ks("gaussian", 1.1), bf, Q, 12, 50, rsp_state=shared, independent_cursors=True)
+    out["rsp_X"], out["rsp_Q"] = X, Q
+    out["rsp_vals"], out["rsp_cursor"] = np.array(rsp_vals), np.array(rsp_cur)
+    out["dp_vals"], out["dp_cursor"], out["dp_used"] = np.array(dp_vals), np.array(dp_cur), np.array(dp_used)
+    out["dp_batch"] = np.array([e.value for e in batch])
+    out["dp_batch_cursor"] = np.array([shared.cursor])
+    out["dp_indep"] = np.array([e.value for e in indep])
+    out["rsp_perm80"] = deann.RspState.from_dataset(ds, 80).permuted.permutation.copy()
+
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", os.path.join(HERE, "reference_golden.npz"), len(out), "arrays")
 

@@ -131,3 +131,52 @@ def test_neighbor_replay():
     nr = NeighborReplay([3, 1, 2], [0.1, 0.2, 0.3])
     i, d2 = nr(None, 2)
     assert list(i) == [3, 1] and list(d2) == [0.1, 0.2]
+
+
+def _rsp_setup(golden):
+    d = O.Data(golden["rsp_X"])
+    return d, golden["rsp_Q"]
+
+
+def test_rsp_permutation_matches_reference(golden):
+    d, _ = _rsp_setup(golden)
+    np.testing.assert_array_equal(O.Permuted(d, 80).perm, golden["rsp_perm80"])
+
+
+def test_rsp_kde_sequences_match_reference(golden):
+    d, Q = _rsp_setup(golden)
+    it_v, it_c = iter(golden["rsp_vals"]), iter(golden["rsp_cursor"])
+    for fi, (fam, h) in enumerate([("gaussian", 1.1), ("exponential", 0.8), ("laplacian", 2.3)]):
+        st = O.Permuted(d, 60 + fi, cursor=37 * fi)
+        for j, q in enumerate(Q):
+            v = O.rsp_kde(st, fam, h, q, [17, 100, 299, 1, 64][j])
+            assert v == pytest.approx(next(it_v), rel=1e-12)
+            assert st.cursor == next(it_c)
+
+
+def test_deannp_matches_reference(golden):
+    d, Q = _rsp_setup(golden)
+    it_v, it_c, it_u = iter(golden["dp_vals"]), iter(golden["dp_cursor"]), iter(golden["dp_used"])
+    nb = lambda y, k: O.brute_force_knn(d, y, k)  # noqa: E731
+    for fi, (fam, h) in enumerate([("gaussian", 1.1), ("exponential", 0.8), ("laplacian", 2.3)]):
+        st = O.Permuted(d, 70 + fi, cursor=290)
+        for j, q in enumerate(Q):
+            v, _, _, used, trunc, clamped = O.deann_rsp(d, fam, h, nb, q, [10, 0, 25, 299, 5][j],
+                                                        [40, 30, 280, 1, 0][j], st)
+            assert v == pytest.approx(next(it_v), rel=1e-12)
+            assert st.cursor == next(it_c)
+            assert [used, int(clamped), int(trunc)] == list(next(it_u))
+
+
+def test_deannp_batch_cursor_threading(golden):
+    d, Q = _rsp_setup(golden)
+    nb = lambda y, k: O.brute_force_knn(d, y, k)  # noqa: E731
+    st = O.Permuted(d, 80, cursor=123)
+    vals = [O.deann_rsp(d, "gaussian", 1.1, nb, q, 12, 50, st)[0] for q in Q]
+    np.testing.assert_allclose(vals, golden["dp_batch"], rtol=1e-12)
+    assert st.cursor == golden["dp_batch_cursor"][0]
+    indep = []
+    for j, q in enumerate(Q):
+        s2 = O.Permuted(d, 80, cursor=(j * d.n) // len(Q))
+        indep.append(O.deann_rsp(d, "gaussian", 1.1, nb, q, 12, 50, s2)[0])
+    np.testing.assert_allclose(indep, golden["dp_indep"], rtol=1e-12)
