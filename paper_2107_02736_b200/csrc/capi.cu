@@ -268,6 +268,19 @@ KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
   return p;
 }
 
+// The tile path's selection keeps the candidate list and 2*pow2(k) keys in one
+// CTA's shared memory (knn.cu launch_select_rerank); plans that do not fit —
+// k > 4096, or every row a candidate because fewer segment minima than k exist
+// to bound tau — take the exact fp64 + radix-sort path instead (bigk.cu).
+bool use_bigk(const dk_dataset* h, int32_t k, int64_t nq) {
+  if (k > kSelectMaxK) return true;
+  const KnnPlan kp = plan_knn(h, k, nq);
+  int B = 2, Kp = 32;
+  while (B < kp.cap) B <<= 1;
+  while (Kp < k) Kp <<= 1;
+  return size_t(B) * 8 + size_t(2 * Kp) * 16 > 232448;
+}
+
 // encoding for the k-NN sweeps: exact integers when possible, else single-pass
 // fp16 (its error is bounded by eps_rel and absorbed by the threshold), unless
 // the caller pinned split3.
@@ -280,6 +293,12 @@ int knn_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cudaS
 // k-NN for nq queries already on the device; idx/d2 outputs on the device.
 void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t* idx_d, double* d2_d,
                 cudaStream_t s, size_t ws_off_base) {
+  if (use_bigk(h, k, nq)) {  // exact fp64 distances + stable radix sort (bigk.cu)
+    const size_t off = (ws_off_base + 255) & ~size_t(255);
+    launch_knn_bigk(h->X, h->n, h->global_offset, h->d, Qd, nq, k, idx_d, d2_d, h->ws.base + off,
+                    bigk_temp_bytes(h->n), s);
+    return;
+  }
   const KnnPlan kp = plan_knn(h, k, nq);
   Plan pl;
   pl.off = ws_off_base;
@@ -372,6 +391,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
 }
 
 size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
+  if (use_bigk(h, k, nq)) return bigk_temp_bytes(h->n) + 4096;
   const KnnPlan kp = plan_knn(h, k, nq);
   const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
   Plan pl;
@@ -577,7 +597,6 @@ dk_status dk_knn(dk_handle h, const double* Q, int64_t nq, int32_t k, int64_t* i
     DK_REQUIRE(h != nullptr, "NULL handle");
     DK_REQUIRE(k >= 1 && int64_t(k) <= h->n,
                "k=" + std::to_string(k) + " out of range [1, " + std::to_string(h->n) + "]");
-    DK_REQUIRE(k <= 4096, "k > 4096 is not supported by the GPU k-NN selection");
     DK_REQUIRE(nq >= 0, "negative query count");
     if (nq == 0) return;
     DK_REQUIRE(Q != nullptr && idx_out != nullptr && d2_out != nullptr, "NULL argument");
@@ -636,6 +655,9 @@ dk_status dk_sample(dk_handle h, const double* Q, int64_t nq, int32_t family, do
     const size_t o_z = pl.add<double>(size_t(nq));
     const size_t o_acc = pl.add<int64_t>(accepted_idx_out ? size_t(nq) * m : 1);
     const size_t o_dr = pl.add<int64_t>(size_t(nq));
+    const bool long_excl = excl && excl_stride > kSmemSortMax;
+    const size_t seg_bytes = long_excl ? seg_sort_temp_bytes(excl_stride, nq) : 0;
+    const size_t o_seg = pl.add<uint8_t>(seg_bytes);
     h->ws.reserve(pl.off);
     const double* Qd = stage_queries(h, Q, nq, o_Q, s);
     const int64_t* ex_sorted = nullptr;
@@ -649,7 +671,8 @@ dk_status dk_sample(dk_handle h, const double* Q, int64_t nq, int32_t family, do
         cnt_d = c;
       }
       int64_t* srt = at<int64_t>(h->ws, o_exs);
-      launch_sort_excl(ex_d, cnt_d, excl_stride, nq, srt, s);
+      if (long_excl) launch_seg_sort_i64(ex_d, srt, cnt_d, excl_stride, nq, at<uint8_t>(h->ws, o_seg), seg_bytes, s);
+      else launch_sort_excl(ex_d, cnt_d, excl_stride, nq, srt, s);
       ex_sorted = srt;
     }
     const bool z_dev = is_device_ptr(z_sum);
@@ -752,7 +775,6 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     DK_REQUIRE(k >= 0 && int64_t(k) <= n, "k=" + std::to_string(k) + " out of range [0, " + std::to_string(n) + "]");
     DK_REQUIRE(m >= 0, "m=" + std::to_string(m) + " must be >= 0");
     DK_REQUIRE(!(m > 0 && int64_t(k) >= n), "m > 0 requires k + 1 <= n so the remainder is nonempty");
-    DK_REQUIRE(k <= 4096, "k > 4096 is not supported by the GPU k-NN selection");
     DK_REQUIRE(nq >= 0, "negative query count");
     if (nq == 0) return;
     DK_REQUIRE(Q != nullptr && value_out != nullptr, "NULL argument");
@@ -769,6 +791,9 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     const size_t o_z2 = pl.add<double>(size_t(nq));
     const size_t o_val = pl.add<double>(size_t(nq));
     const size_t o_acc = pl.add<int64_t>(sample_idx_out ? size_t(nq) * std::max(m, 1) : 1);
+    const bool long_excl = m > 0 && k > kSmemSortMax;
+    const size_t seg_bytes = long_excl ? seg_sort_temp_bytes(k, nq) : 0;
+    const size_t o_seg = pl.add<uint8_t>(seg_bytes);
     const size_t base = pl.off;
     h->ws.reserve(base + (k > 0 ? knn_ws_bytes(h, k, nq) : 0));
     const double* Qd = stage_queries(h, Q, nq, o_Q, s);
@@ -787,7 +812,8 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       const int64_t* ex = nullptr;
       if (k > 0) {
         int64_t* srt = at<int64_t>(h->ws, o_srt);
-        launch_sort_excl(idx, nullptr, k, nq, srt, s);
+        if (long_excl) launch_seg_sort_i64(idx, srt, nullptr, k, nq, at<uint8_t>(h->ws, o_seg), seg_bytes, s);
+        else launch_sort_excl(idx, nullptr, k, nq, srt, s);
         ex = srt;
       }
       ProfScope ps(h, s, 0.0, double(nq) * (m + k) * h->d * 4.0);
@@ -842,6 +868,9 @@ dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, 
     const size_t o_taken = pl.add<int32_t>(size_t(nq));
     const size_t o_z = pl.add<double>(size_t(nq));
     const size_t o_cur = pl.add<int64_t>(1);
+    const bool long_excl = cnt > kSmemSortMax;
+    const size_t seg_bytes = long_excl ? seg_sort_temp_bytes(cnt, nq) : 0;
+    const size_t o_seg = pl.add<uint8_t>(seg_bytes);
     h->ws.reserve(pl.off);
     const double* Qd = stage_queries(h, Q, nq, o_Q, s);
     int64_t* pos = nullptr;
@@ -849,7 +878,12 @@ dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, 
       int64_t* ex = at<int64_t>(h->ws, o_ex);
       DK_CUDA(cudaMemcpyAsync(ex, excl, size_t(nq) * cnt * sizeof(int64_t), cudaMemcpyDefault, s));
       pos = at<int64_t>(h->ws, o_pos);
-      launch_rsp_map_sort(ex, cnt, h->rsp_inverse, nq, pos, s);
+      if (long_excl) {  // ids -> positions in place, then a segmented radix sort
+        launch_gather_positions(ex, h->rsp_inverse, nq * cnt, ex, s);
+        launch_seg_sort_i64(ex, pos, nullptr, cnt, nq, at<uint8_t>(h->ws, o_seg), seg_bytes, s);
+      } else {
+        launch_rsp_map_sort(ex, cnt, h->rsp_inverse, nq, pos, s);
+      }
     }
     int64_t* start = at<int64_t>(h->ws, o_start);
     int64_t* len = at<int64_t>(h->ws, o_len);

@@ -194,6 +194,16 @@ void launch_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_
                        int64_t* idx_out, double* d2_out, cudaStream_t s);
 void launch_kernel_values(int32_t family, double h, const double* dist, int64_t count, double* out, uint32_t* bad,
                           cudaStream_t s);
+// bigk.cu: exact k-NN for k > kSelectMaxK and CUB sorts of lists longer than kSmemSortMax
+constexpr int32_t kSelectMaxK = 4096;
+constexpr int32_t kSmemSortMax = 16384;
+size_t bigk_temp_bytes(int64_t n);
+void launch_knn_bigk(const float* X, int64_t n, int64_t offset, int32_t d, const double* Q, int64_t nq, int32_t k,
+                     int64_t* idx_out, double* d2_out, void* temp, size_t temp_bytes, cudaStream_t s);
+size_t seg_sort_temp_bytes(int32_t stride, int64_t nq);
+void launch_seg_sort_i64(const int64_t* in, int64_t* out, const int32_t* cnt, int32_t stride, int64_t nq, void* temp,
+                         size_t temp_bytes, cudaStream_t s);
+void launch_gather_positions(const int64_t* ids, const int64_t* inverse, int64_t count, int64_t* out, cudaStream_t s);
 void launch_rsp_map_sort(const int64_t* excl, int32_t stride, const int64_t* inverse, int64_t nq, int64_t* pos,
                          cudaStream_t s);
 void launch_rsp_starts(const int64_t* pos, int32_t cnt, int64_t nq, int64_t n, int64_t m, int64_t cursor_in,
