@@ -40,7 +40,9 @@ typedef enum {
   DK_ECUDA = 2,     /* CUDA runtime/driver failure     -> RuntimeError        */
   DK_ENOMEM = 3,    /* device allocation failed        -> MemoryError         */
   DK_EINEXACT = 4,  /* k-NN certificate failed (see dk_knn)                   */
-  DK_ENODEV = 5     /* no sm_100 device                                       */
+  DK_ENODEV = 5,    /* no sm_100 device                                       */
+  DK_EFORMAT = 6,   /* malformed dataset file          -> DatasetFormatError  */
+  DK_EIO = 7        /* file open/read failure          -> OSError             */
 } dk_status;
 
 /* Kernel families, same order/meaning as kernels.py:22-39
@@ -83,6 +85,20 @@ int32_t dk_device_ok(int32_t device);   /* 1 if `device` is sm_100 (B200) */
 dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts,
                  dk_handle* out);
 dk_status dk_free(dk_handle h);
+
+/* ---- load -----------------------------------------------------------------
+ * The DEANN1 binary format of data.py:1-15 (magic "DEANN1\0\0", u32 n, u32 d,
+ * n*d little-endian fp32, row-major).  dk_file_info validates the header and
+ * the payload size exactly as _load_binary (data.py:151-167) does, with the same
+ * messages (DK_EFORMAT).  dk_fit_file streams rows [row_begin, row_begin +
+ * row_count) of the file (row_count < 0: to the end) through pinned staging
+ * buffers straight into device memory — parallel pread threads overlapped with
+ * the host->device copies — and then fits like dk_fit.  Loading a proper row
+ * range without opts->global_n makes the handle a dataset shard whose global ids
+ * are the file's row ids (global_offset = row_begin, global_n = file n). */
+dk_status dk_file_info(const char* path, int64_t* n, int32_t* d);
+dk_status dk_fit_file(const char* path, int64_t row_begin, int64_t row_count,
+                      const dk_fit_opts* opts, dk_handle* out);
 dk_status dk_info(dk_handle h, int64_t* n, int32_t* d, int64_t* global_offset,
                   int64_t* global_n, int32_t* exact_mode);
 /* fp64 squared row norms (n), cf. Dataset.sq_norms (data.py:64). */

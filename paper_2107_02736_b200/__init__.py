@@ -11,7 +11,7 @@ All arithmetic runs in hand-written sm_100a kernels behind the C-ABI in
 
 from .ann import AnnIndex, BruteForceIndex, GpuBruteForceIndex, NeighborList, brute_force_knn, knn_batch
 from .bandwidth import fit_bandwidth, NoBandwidthError
-from .data import Dataset, PermutedDataset, as_gpu_dataset, permute
+from .data import Dataset, DatasetFormatError, PermutedDataset, as_gpu_dataset, file_info, load, permute, save
 from .estimators import (
     BatchKde,
     Estimate,
@@ -32,7 +32,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AnnIndex", "BruteForceIndex", "GpuBruteForceIndex", "NeighborList", "brute_force_knn", "knn_batch",
-    "fit_bandwidth", "NoBandwidthError", "Dataset", "PermutedDataset", "permute", "as_gpu_dataset", "BatchKde",
+    "fit_bandwidth", "NoBandwidthError", "Dataset", "DatasetFormatError", "PermutedDataset", "permute",
+    "as_gpu_dataset", "file_info", "load", "save", "BatchKde",
     "Estimate", "RspState", "rsp_kde", "deann",
     "deann_arrays", "deann_batch", "kernel_from_distance", "naive_kde", "naive_kde_into", "rs_kde",
     "KernelFamily", "KernelSpec", "PhiloxSampler",

@@ -15,16 +15,17 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdeann_b200.so")
+LIB_PATH = os.environ.get("DK_LIBRARY") or os.path.join(_HERE, "libdeann_b200.so")
 
-DK_OK, DK_EINVAL, DK_ECUDA, DK_ENOMEM, DK_EINEXACT, DK_ENODEV = range(6)
+DK_OK, DK_EINVAL, DK_ECUDA, DK_ENOMEM, DK_EINEXACT, DK_ENODEV, DK_EFORMAT, DK_EIO = range(8)
 DK_GAUSSIAN, DK_EXPONENTIAL, DK_LAPLACIAN = 0, 1, 2
 DK_PREC_AUTO, DK_PREC_SPLIT3, DK_PREC_FP16 = 0, 1, 2
 DK_OUT_SUM = 1
 
 # every symbol include/deann_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
-    "dk_version", "dk_last_error", "dk_device_ok", "dk_fit", "dk_free", "dk_info", "dk_sq_norms",
+    "dk_version", "dk_last_error", "dk_device_ok", "dk_fit", "dk_free", "dk_file_info", "dk_fit_file",
+    "dk_info", "dk_sq_norms",
     "dk_naive", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
     "dk_rsp_attach", "dk_rsp_walk", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
 )
@@ -32,6 +33,10 @@ EXPORTED = (
 
 class DeannGpuError(RuntimeError):
     """A CUDA / device failure reported by the C-ABI (status DK_ECUDA / DK_ENODEV)."""
+
+
+class DatasetFormatError(ValueError):
+    """A dataset file cannot be parsed (reference data.DatasetFormatError, data.py:41-42)."""
 
 
 class FitOpts(ctypes.Structure):
@@ -61,6 +66,8 @@ def _declare(lib):
         "dk_device_ok": (_i32, [_i32]),
         "dk_fit": (_i32, [_vp, _i64, _i32, ctypes.POINTER(FitOpts), ctypes.POINTER(_vp)]),
         "dk_free": (_i32, [_vp]),
+        "dk_file_info": (_i32, [ctypes.c_char_p, ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
+        "dk_fit_file": (_i32, [ctypes.c_char_p, _i64, _i64, ctypes.POINTER(FitOpts), ctypes.POINTER(_vp)]),
         "dk_info": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),
                             ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
         "dk_sq_norms": (_i32, [_vp, _vp, _vp]),
@@ -110,6 +117,10 @@ def check(status: int) -> None:
     msg = load().dk_last_error().decode(errors="replace")
     if status == DK_EINVAL:
         raise ValueError(msg)
+    if status == DK_EFORMAT:
+        raise DatasetFormatError(msg)
+    if status == DK_EIO:
+        raise OSError(msg)
     if status == DK_ENOMEM:
         raise MemoryError(msg)
     raise DeannGpuError(f"[status {status}] {msg}")

@@ -11,6 +11,12 @@
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <thread>
+
+#include <errno.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include "internal.h"
 #include "tile_kernel.cuh"
@@ -408,6 +414,221 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
   return pl.off + 4096;
 }
 
+
+// ------------------------------------------------------------------ fit
+struct HandleDeleter {
+  void operator()(dk_dataset* h) const { dk_free(h); }
+};
+using HandlePtr = std::unique_ptr<dk_dataset, HandleDeleter>;
+
+// Device checks and handle fields shared by dk_fit / dk_fit_file (rows not yet on the device).
+HandlePtr new_handle(int64_t n, int32_t d, const dk_fit_opts* opts) {
+  const int device = opts ? opts->device : 0;
+  int ndev = 0;
+  DK_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) throw Error{DK_ENODEV, "no CUDA device " + std::to_string(device)};
+  cudaDeviceProp prop;
+  DK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) throw Error{DK_ENODEV, std::string("device is not sm_100 (B200): ") + prop.name};
+  HandlePtr h(new dk_dataset());
+  h->device = device;
+  h->num_sms = prop.multiProcessorCount;
+  h->n = n;
+  h->d = d;
+  h->n_pad = round_up(n, kBN);
+  h->global_offset = opts ? opts->global_offset : 0;
+  h->global_n = (opts && opts->global_n > 0) ? opts->global_n : n;
+  h->precision = opts ? opts->precision : DK_PREC_AUTO;
+  h->knn_stats = std::getenv("DK_KNN_STATS") != nullptr;
+  if (const char* pv = std::getenv("DK_PAIR")) set_pair_enabled(std::atoi(pv) != 0);
+  DK_REQUIRE(h->precision >= 0 && h->precision <= 2, "unknown precision mode");
+  DK_REQUIRE(h->global_offset >= 0 && h->global_offset + n <= h->global_n, "shard outside [0, global_n)");
+  return h;
+}
+
+// Rows are in h->X: finiteness / integrality flags, fp64 norms, default encoding.
+void finish_fit(dk_dataset* h) {
+  cudaStream_t s = nullptr;
+  DK_CUDA(cudaMalloc(&h->xn64, size_t(h->n) * sizeof(double)));
+  uint32_t* flags_d = nullptr;
+  DK_CUDA(cudaMalloc(&flags_d, sizeof(uint32_t)));
+  DK_CUDA(cudaMemset(flags_d, 0, sizeof(uint32_t)));
+  launch_row_stats(h->X, h->n, h->d, h->xn64, flags_d, s);
+  uint32_t flags = 0;
+  DK_CUDA(cudaMemcpy(&flags, flags_d, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  cudaFree(flags_d);
+  DK_REQUIRE(!(flags & 1u), "dataset entries must be finite");
+  h->int_exact = (flags & 6u) == 0;
+  if (h->precision == DK_PREC_AUTO) ensure_encoding(h, h->int_exact ? 0 : 1, s);
+  else if (h->precision == DK_PREC_SPLIT3) ensure_encoding(h, 1, s);
+  else ensure_encoding(h, 2, s);
+  DK_CUDA(cudaDeviceSynchronize());
+}
+
+// ------------------------------------------------------------------ DEANN1 files (data.py:1-15, 151-167)
+constexpr int64_t kHeaderBytes = 16;  // magic[8] "DEANN1\0\0", u32 n, u32 d (little-endian)
+
+struct FileHeader {
+  int64_t n = 0;
+  int32_t d = 0;
+};
+
+struct Fd {
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) ::close(fd);
+  }
+};
+
+// Python's repr() of a bytes object (the reference formats the bad magic with !r).
+std::string py_bytes_repr(const unsigned char* b, size_t len) {
+  bool has_sq = false, has_dq = false;
+  for (size_t i = 0; i < len; ++i) {
+    has_sq |= b[i] == '\'';
+    has_dq |= b[i] == '"';
+  }
+  const char quote = (has_sq && !has_dq) ? '"' : '\'';
+  std::string r = "b";
+  r += quote;
+  static const char* hex = "0123456789abcdef";
+  for (size_t i = 0; i < len; ++i) {
+    const unsigned char c = b[i];
+    if (c == '\\' || c == static_cast<unsigned char>(quote)) {
+      r += '\\';
+      r += char(c);
+    } else if (c == '\t') {
+      r += "\\t";
+    } else if (c == '\n') {
+      r += "\\n";
+    } else if (c == '\r') {
+      r += "\\r";
+    } else if (c < 32 || c >= 127) {
+      r += "\\x";
+      r += hex[c >> 4];
+      r += hex[c & 15];
+    } else {
+      r += char(c);
+    }
+  }
+  r += quote;
+  return r;
+}
+
+// Same checks and messages as _load_binary (data.py:151-167); status DK_EFORMAT.
+FileHeader read_header(const char* path) {
+  Fd f;
+  f.fd = ::open(path, O_RDONLY | O_CLOEXEC);
+  if (f.fd < 0) throw Error{DK_EIO, std::string(path) + ": " + std::strerror(errno)};
+  unsigned char hdr[kHeaderBytes];
+  ssize_t got = 0;
+  while (got < kHeaderBytes) {
+    const ssize_t r = ::pread(f.fd, hdr + got, size_t(kHeaderBytes - got), got);
+    if (r < 0) throw Error{DK_EIO, std::string(path) + ": " + std::strerror(errno)};
+    if (r == 0) break;
+    got += r;
+  }
+  if (got != kHeaderBytes)
+    throw Error{DK_EFORMAT, std::string(path) + ": truncated header at byte " + std::to_string(got)};
+  static const unsigned char kMagic[8] = {'D', 'E', 'A', 'N', 'N', '1', 0, 0};
+  if (std::memcmp(hdr, kMagic, 8) != 0)
+    throw Error{DK_EFORMAT, std::string(path) + ": bad magic " + py_bytes_repr(hdr, 8) + " at byte 0"};
+  auto u32 = [&](int o) {
+    return uint32_t(hdr[o]) | (uint32_t(hdr[o + 1]) << 8) | (uint32_t(hdr[o + 2]) << 16) | (uint32_t(hdr[o + 3]) << 24);
+  };
+  FileHeader fh;
+  fh.n = int64_t(u32(8));
+  const uint32_t d = u32(12);
+  if (fh.n < 1 || d < 1)
+    throw Error{DK_EFORMAT, std::string(path) + ": invalid shape " + std::to_string(fh.n) + " x " +
+                                std::to_string(d) + " in header"};
+  struct stat st;
+  if (::fstat(f.fd, &st) != 0) throw Error{DK_EIO, std::string(path) + ": " + std::strerror(errno)};
+  // n * d * 4 < 2^66: exact in 128 bits (Python ints in the reference)
+  const unsigned __int128 expected = static_cast<unsigned __int128>(fh.n) * d * 4u;
+  const int64_t payload = int64_t(st.st_size) - kHeaderBytes;
+  if (payload < 0 || static_cast<unsigned __int128>(payload) != expected) {
+    std::string ex;
+    for (unsigned __int128 v = expected; ex.empty() || v; v /= 10) ex.insert(ex.begin(), char('0' + int(v % 10)));
+    throw Error{DK_EFORMAT, std::string(path) + ": expected " + ex + " data bytes after byte " +
+                                std::to_string(kHeaderBytes) + ", got " + std::to_string(payload)};
+  }
+  if (d > uint32_t(std::numeric_limits<int32_t>::max()))
+    throw Error{DK_EINVAL, std::string(path) + ": d = " + std::to_string(d) + " exceeds 2^31 - 1"};
+  fh.d = int32_t(d);
+  return fh;
+}
+
+// File bytes [offset, offset+bytes) -> device memory.  Groups of kSlots pinned
+// buffers are filled by parallel pread threads; each group's host->device copies
+// run on a stream while the next group is read (the pinned slot is reused only
+// after its copy's event has completed).  Rows are little-endian fp32 on disk and
+// in memory (x86/ARM hosts), so bytes move verbatim.
+void stream_file_rows(const char* path, int64_t offset, size_t bytes, float* dst) {
+  constexpr int kSlots = 4;
+  constexpr size_t kChunk = size_t(16) << 20;
+  Fd f;
+  f.fd = ::open(path, O_RDONLY | O_CLOEXEC);
+  if (f.fd < 0) throw Error{DK_EIO, std::string(path) + ": " + std::strerror(errno)};
+  ::posix_fadvise(f.fd, offset, off_t(bytes), POSIX_FADV_SEQUENTIAL);
+  struct Pinned {
+    void* p = nullptr;
+    cudaEvent_t ev = nullptr;
+    ~Pinned() {
+      if (ev) cudaEventDestroy(ev);
+      if (p) cudaFreeHost(p);
+    }
+  } slot[kSlots];
+  for (auto& sl : slot) {
+    DK_CUDA(cudaHostAlloc(&sl.p, kChunk, cudaHostAllocDefault));
+    DK_CUDA(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+  }
+  cudaStream_t s;
+  DK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } sg{s};
+  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  bool used[kSlots] = {false, false, false, false};
+  for (size_t c0 = 0; c0 < nchunks; c0 += kSlots) {
+    const int cnt = int(std::min<size_t>(kSlots, nchunks - c0));
+    std::string err[kSlots];
+    std::vector<std::thread> readers;
+    for (int i = 0; i < cnt; ++i) {
+      if (used[i]) DK_CUDA(cudaEventSynchronize(slot[i].ev));
+      const size_t c = c0 + size_t(i);
+      const size_t len = std::min(kChunk, bytes - c * kChunk);
+      const int64_t off = offset + int64_t(c * kChunk);
+      readers.emplace_back([&, i, len, off] {
+        size_t done = 0;
+        while (done < len) {
+          const ssize_t r = ::pread(f.fd, static_cast<char*>(slot[i].p) + done, len - done, off + int64_t(done));
+          if (r <= 0) {
+            err[i] = std::string(path) + ": read failed at byte " + std::to_string(off + int64_t(done)) +
+                     (r < 0 ? std::string(": ") + std::strerror(errno) : std::string(": unexpected end of file"));
+            return;
+          }
+          done += size_t(r);
+        }
+      });
+    }
+    for (auto& t : readers) t.join();
+    for (int i = 0; i < cnt; ++i)
+      if (!err[i].empty()) throw Error{DK_EIO, err[i]};
+    for (int i = 0; i < cnt; ++i) {
+      const size_t c = c0 + size_t(i);
+      const size_t len = std::min(kChunk, bytes - c * kChunk);
+      DK_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + c * kChunk, slot[i].p, len, cudaMemcpyHostToDevice, s));
+      DK_CUDA(cudaEventRecord(slot[i].ev, s));
+      used[i] = true;
+    }
+  }
+  DK_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace
 }  // namespace dk
 
@@ -435,45 +656,44 @@ dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts, 
     DK_REQUIRE(n >= 1 && d >= 1, "dataset must have n >= 1 and d >= 1, got " + std::to_string(n) + " x " +
                                      std::to_string(d));
     DK_REQUIRE(X != nullptr, "dataset pointer is NULL");
-    const int device = opts ? opts->device : 0;
-    int ndev = 0;
-    DK_CUDA(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) throw Error{DK_ENODEV, "no CUDA device " + std::to_string(device)};
-    cudaDeviceProp prop;
-    DK_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10)
-      throw Error{DK_ENODEV, std::string("device is not sm_100 (B200): ") + prop.name};
-    DeviceGuard g(device);
-    auto h = std::make_unique<dk_dataset>();
-    h->device = device;
-    h->num_sms = prop.multiProcessorCount;
-    h->n = n;
-    h->d = d;
-    h->n_pad = round_up(n, kBN);
-    h->global_offset = opts ? opts->global_offset : 0;
-    h->global_n = (opts && opts->global_n > 0) ? opts->global_n : n;
-    h->precision = opts ? opts->precision : DK_PREC_AUTO;
-    h->knn_stats = std::getenv("DK_KNN_STATS") != nullptr;
-    if (const char* pv = std::getenv("DK_PAIR")) set_pair_enabled(std::atoi(pv) != 0);
-    DK_REQUIRE(h->precision >= 0 && h->precision <= 2, "unknown precision mode");
-    DK_REQUIRE(h->global_offset >= 0 && h->global_offset + n <= h->global_n, "shard outside [0, global_n)");
-    cudaStream_t s = nullptr;
+    HandlePtr h = new_handle(n, d, opts);
+    DeviceGuard g(h->device);
     DK_CUDA(cudaMalloc(&h->X, size_t(n) * d * sizeof(float)));
     DK_CUDA(cudaMemcpy(h->X, X, size_t(n) * d * sizeof(float), cudaMemcpyDefault));
-    DK_CUDA(cudaMalloc(&h->xn64, size_t(n) * sizeof(double)));
-    uint32_t* flags_d = nullptr;
-    DK_CUDA(cudaMalloc(&flags_d, sizeof(uint32_t)));
-    DK_CUDA(cudaMemset(flags_d, 0, sizeof(uint32_t)));
-    launch_row_stats(h->X, n, d, h->xn64, flags_d, s);
-    uint32_t flags = 0;
-    DK_CUDA(cudaMemcpy(&flags, flags_d, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    cudaFree(flags_d);
-    DK_REQUIRE(!(flags & 1u), "dataset entries must be finite");
-    h->int_exact = (flags & 6u) == 0;
-    if (h->precision == DK_PREC_AUTO) ensure_encoding(h.get(), h->int_exact ? 0 : 1, s);
-    else if (h->precision == DK_PREC_SPLIT3) ensure_encoding(h.get(), 1, s);
-    else ensure_encoding(h.get(), 2, s);
-    DK_CUDA(cudaDeviceSynchronize());
+    finish_fit(h.get());
+    *out = h.release();
+  });
+}
+
+dk_status dk_file_info(const char* path, int64_t* n, int32_t* d) {
+  return guard([&] {
+    DK_REQUIRE(path != nullptr, "NULL path");
+    const FileHeader fh = read_header(path);
+    if (n) *n = fh.n;
+    if (d) *d = fh.d;
+  });
+}
+
+dk_status dk_fit_file(const char* path, int64_t row_begin, int64_t row_count, const dk_fit_opts* opts,
+                      dk_handle* out) {
+  return guard([&] {
+    DK_REQUIRE(path != nullptr && out != nullptr, "NULL argument");
+    *out = nullptr;
+    const FileHeader fh = read_header(path);
+    if (row_count < 0) row_count = fh.n - row_begin;
+    DK_REQUIRE(row_begin >= 0 && row_count >= 1 && row_begin + row_count <= fh.n,
+               "row range [" + std::to_string(row_begin) + ", " + std::to_string(row_begin + row_count) +
+                   ") outside the file's " + std::to_string(fh.n) + " rows");
+    dk_fit_opts o = opts ? *opts : dk_fit_opts{0, DK_PREC_AUTO, 0, 0};
+    if (o.global_n == 0 && row_count < fh.n) {  // a row shard of the file: global ids = file row ids
+      o.global_offset = row_begin;
+      o.global_n = fh.n;
+    }
+    HandlePtr h = new_handle(row_count, fh.d, &o);
+    DeviceGuard g(h->device);
+    DK_CUDA(cudaMalloc(&h->X, size_t(row_count) * fh.d * sizeof(float)));
+    stream_file_rows(path, kHeaderBytes + row_begin * int64_t(fh.d) * 4, size_t(row_count) * fh.d * 4, h->X);
+    finish_fit(h.get());
     *out = h.release();
   });
 }
@@ -931,7 +1151,7 @@ dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* byte
 dk_status dk_sweep_probe(dk_handle h, const double* Q, int64_t nq, int32_t mode, int32_t encoding, double* ms) {
   return guard([&] {
     DK_REQUIRE(h != nullptr && Q != nullptr && ms != nullptr && nq > 0, "bad probe arguments");
-    DK_REQUIRE(mode >= MODE_KDE_GAUSS && mode <= MODE_NULL && encoding >= 0 && encoding <= 2, "bad probe mode");
+    DK_REQUIRE(mode >= MODE_KDE_GAUSS && mode <= MODE_KDE_GAUSS_MUFU && encoding >= 0 && encoding <= 2, "bad probe mode");
     DeviceGuard g(h->device);
     cudaStream_t s = nullptr;
     const Encoding& e = ensure_encoding(h, encoding, s);

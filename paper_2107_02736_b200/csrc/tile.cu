@@ -161,7 +161,14 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const int grid = std::min(nunits, nslots) * (pr ? 2 : 1);
   const CUtensorMap& tb = pr ? e.tmap_half : e.tmap;
   switch (a.mode) {
-    case MODE_KDE_GAUSS: launch_any<MODE_KDE_GAUSS>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_KDE_GAUSS:
+      // MMA-heavy encodings (split3: >= 4 K-blocks per tile) leave no FMA-pipe slack for the
+      // exp2 polynomial and run power-capped: every exponential on MUFU is faster there
+      // (c3: 6.6 vs 7.0 ms); the single-pass encodings offload 2 of 16 pairs (c2: 2.83 vs 2.98 ms).
+      if (kblocks >= 4) launch_any<MODE_KDE_GAUSS_MUFU>(pr, q.tmap, tb, p, grid, pl.smem, s);
+      else launch_any<MODE_KDE_GAUSS>(pr, q.tmap, tb, p, grid, pl.smem, s);
+      break;
+    case MODE_KDE_GAUSS_MUFU: launch_any<MODE_KDE_GAUSS_MUFU>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_KDE_EXP: launch_any<MODE_KDE_EXP>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_TILEMIN: launch_any<MODE_TILEMIN>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_FILTER: launch_any<MODE_FILTER>(pr, q.tmap, tb, p, grid, pl.smem, s); break;

@@ -34,7 +34,17 @@
 
 namespace dk {
 
-enum TileMode : int { MODE_KDE_GAUSS = 0, MODE_KDE_EXP = 1, MODE_TILEMIN = 2, MODE_FILTER = 3, MODE_NULL = 4 };
+enum TileMode : int {
+  MODE_KDE_GAUSS = 0,
+  MODE_KDE_EXP = 1,
+  MODE_TILEMIN = 2,
+  MODE_FILTER = 3,
+  MODE_NULL = 4,
+  MODE_KDE_GAUSS_MUFU = 5  // gaussian with every exponential on MUFU (MMA-heavy encodings)
+};
+__host__ __device__ constexpr bool is_kde(int mode) {
+  return mode == MODE_KDE_GAUSS || mode == MODE_KDE_EXP || mode == MODE_KDE_GAUSS_MUFU;
+}
 
 constexpr int kBM = 128;           // query rows per tile (UMMA M)
 constexpr int kBN = 256;           // dataset columns per tile (UMMA N)
@@ -102,6 +112,16 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   return d;
 }
 
+// Gaussian epilogue: which of the 16 pairs of a 32-column chunk take the FMA-pipe
+// polynomial instead of MUFU.EX2 (bit i = pair i), trading XU-pipe cycles (8 per
+// warp MUFU) for FMA-pipe cycles (2 per packed FADD2/FFMA2).  Measured on c2 (B200,
+// power-capped at ~990 W): 0 pairs 2.98 ms, 1: 2.92, 2: 2.83, 3: 2.86, 4: 2.87, 6: 2.99,
+// 8: 3.19 ms — the sweet spot is small because the kernel also runs at the power cap.
+#ifndef DK_POLY_PAIRS
+#define DK_POLY_PAIRS 0x0808u
+#endif
+constexpr uint32_t kPolyPairs = DK_POLY_PAIRS;
+
 // 2^t for a pair, t <= 0, on the FMA pipe: t = j + f (j = round(t), |f| <= 1/2),
 // 2^f by a degree-5 polynomial (relative error < 2.4e-7 on |f| <= 1/2, i.e. at the
 // level of ex2.approx), exponent j added to the float bits.  t is clamped at -126
@@ -146,7 +166,9 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
                                           uint32_t* scnt, unsigned long long* sbuf, int lrow) {
   const float4* x4 = reinterpret_cast<const float4*>(xs_smem);
   if (full || MODE == MODE_TILEMIN || MODE == MODE_FILTER) {
-    if constexpr (MODE == MODE_KDE_GAUSS) {
+    if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU) {
+      constexpr uint32_t poly = MODE == MODE_KDE_GAUSS ? kPolyPairs : 0u;
+      // d2 = S * m2s + (qn + xn) in the cancellation-safe order, then t = d2 * negc
       const float2 q2 = make_float2(qn, qn), m2 = make_float2(m2s, m2s), c2 = make_float2(negc, negc);
 #pragma unroll
       for (int j4 = 0; j4 < 8; ++j4) {
@@ -156,9 +178,8 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
         const float2 da = fma2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), m2, ua);
         const float2 db = fma2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), m2, ub);
         const float2 ta = mul2(da, c2), tb = mul2(db, c2);
-        const float2 ea = make_float2(ex2_approx(ta.x), ex2_approx(ta.y));
-        // every other group of 4: one pair on the FMA pipe (25% of the exponentials)
-        const float2 eb = (j4 & 1) ? exp2_poly2(tb) : make_float2(ex2_approx(tb.x), ex2_approx(tb.y));
+        const float2 ea = (poly >> (2 * j4)) & 1 ? exp2_poly2(ta) : make_float2(ex2_approx(ta.x), ex2_approx(ta.y));
+        const float2 eb = (poly >> (2 * j4 + 1)) & 1 ? exp2_poly2(tb) : make_float2(ex2_approx(tb.x), ex2_approx(tb.y));
         acc0 = add2(acc0, ea);
         acc1 = add2(acc1, eb);
       }
@@ -221,7 +242,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
     for (int j = 0; j < 32; ++j) {
       if (j >= lim) continue;
       const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs_smem[j]);
-      if constexpr (MODE == MODE_KDE_GAUSS) {
+      if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU) {
         acc0.x += ex2_approx(d2 * negc);
       } else {
         acc0.x += ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
@@ -479,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         lrow);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
-        if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
+        if constexpr (is_kde(MODE)) {
           usum += double((a0.x + a0.y) + (a1.x + a1.y));
         } else if constexpr (MODE == MODE_TILEMIN) {
           if (p.seg_tiles == 0) {
@@ -488,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_EXP) {
+      if constexpr (is_kde(MODE)) {
         p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
       } else if constexpr (MODE == MODE_TILEMIN) {
         if (t1 > t0 && p.seg_tiles > 0)

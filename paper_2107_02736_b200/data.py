@@ -14,13 +14,20 @@ Any object with a ``.data`` float32 (n, d) array — e.g. the reference's own
 from __future__ import annotations
 
 import ctypes
+import os
+import struct
 import weakref
 
 import numpy as np
 
 from . import _lib
 
-__all__ = ["Dataset", "as_gpu_dataset", "PermutedDataset", "permute", "as_gpu_permuted"]
+__all__ = ["Dataset", "as_gpu_dataset", "PermutedDataset", "permute", "as_gpu_permuted", "DatasetFormatError",
+           "file_info", "load", "save"]
+
+DatasetFormatError = _lib.DatasetFormatError
+MAGIC = b"DEANN1\x00\x00"
+HEADER_BYTES = 16
 
 _PRECISION = {"auto": _lib.DK_PREC_AUTO, "split3": _lib.DK_PREC_SPLIT3, "fp16": _lib.DK_PREC_FP16}
 
@@ -176,3 +183,84 @@ def as_gpu_permuted(permuted) -> PermutedDataset:
                           np.asarray(permuted.inverse_permutation, dtype=np.int64))
     _PCACHE[permuted] = out
     return out
+
+
+# ---------------------------------------------------------------- files
+
+
+def file_info(path) -> tuple[int, int]:
+    """(n, d) of a DEANN1 file; header and payload size validated as data.py:151-167."""
+    with open(path, "rb"):  # FileNotFoundError / PermissionError exactly as the reference's open()
+        pass
+    n, d = ctypes.c_int64(), ctypes.c_int32()
+    _lib.check(_lib.load().dk_file_info(os.fsencode(path), ctypes.byref(n), ctypes.byref(d)))
+    return int(n.value), int(d.value)
+
+
+def load(path, fmt: str = "binary", *, device: int = 0, precision: str = "auto", rows=None) -> Dataset:
+    """Read a dataset file (reference data.load, data.py:142-148) straight onto the GPU.
+
+    binary: the header is validated by the C-ABI (same DatasetFormatError messages
+    as the reference), the rows stream from the file through pinned buffers into
+    device memory (dk_fit_file), and ``.data`` is a read-only memory map of the
+    file — no host copy is made.  ``rows=(begin, count)`` loads a row range as a
+    dataset shard whose global ids are the file's row ids.
+    csv: parsed on the host exactly like data.py:170-190, then uploaded.
+    """
+    if fmt == "binary":
+        return _load_binary(path, device, precision, rows)
+    if fmt == "csv":
+        if rows is not None:
+            raise ValueError("rows= is only supported for binary files")
+        return Dataset.from_array(_parse_csv(path), device=device, precision=precision)
+    raise ValueError(f"unknown format {fmt!r}")
+
+
+def _load_binary(path, device, precision, rows) -> Dataset:
+    if precision not in _PRECISION:
+        raise ValueError(f"precision must be one of {sorted(_PRECISION)}, got {precision!r}")
+    n, d = file_info(path)
+    begin, count = (0, n) if rows is None else (int(rows[0]), int(rows[1]))
+    if not (0 <= begin and 1 <= count and begin + count <= n):
+        raise ValueError(f"row range [{begin}, {begin + count}) outside the file's {n} rows")
+    data = np.memmap(path, dtype="<f4", mode="r", offset=HEADER_BYTES + begin * d * 4, shape=(count, d))
+    shard = count < n
+    opts = _lib.FitOpts(device, _PRECISION[precision], begin if shard else 0, n if shard else 0)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().dk_fit_file(os.fsencode(path), begin, count, ctypes.byref(opts), ctypes.byref(h)))
+    return Dataset(data, h, device=device, global_offset=begin if shard else 0, global_n=n, precision=precision)
+
+
+def _parse_csv(path) -> np.ndarray:
+    rows = []
+    width = None
+    with open(path, "r") as f:
+        for lineno, line in enumerate(f, start=1):
+            line = line.strip()
+            if not line:
+                continue
+            parts = line.split(",")
+            if width is None:
+                width = len(parts)
+            elif len(parts) != width:
+                raise DatasetFormatError(f"{path}: line {lineno} has {len(parts)} fields, expected {width}")
+            try:
+                rows.append([float(p) for p in parts])
+            except ValueError as exc:
+                raise DatasetFormatError(f"{path}: line {lineno}: {exc}") from exc
+    if not rows:
+        raise DatasetFormatError(f"{path}: no data rows")
+    return np.asarray(rows, dtype=np.float32)
+
+
+def save(dataset, path, fmt: str = "binary") -> None:
+    """Write a dataset (reference data.save, data.py:131-139); binary is bit-exact."""
+    data = np.asarray(getattr(dataset, "data", dataset))
+    if fmt == "binary":
+        with open(path, "wb") as f:
+            f.write(MAGIC + struct.pack("<II", data.shape[0], data.shape[1]))
+            f.write(np.ascontiguousarray(data, dtype="<f4").tobytes())
+    elif fmt == "csv":
+        np.savetxt(path, data, delimiter=",", fmt="%.9g")
+    else:
+        raise ValueError(f"unknown format {fmt!r}")

@@ -75,17 +75,29 @@ class LocalComm:
 class GpuShardEngine:
     """One shard on one GPU: fits rows [offset, offset+n) of a global dataset of N rows."""
 
-    def __init__(self, rows, *, global_offset: int, global_n: int, device: int = 0, precision: str = "auto"):
+    def __init__(self, rows, *, global_offset: int, global_n: int, device: int = 0, precision: str = "auto",
+                 dataset: Dataset | None = None):
         import torch
 
         self.torch = torch
         self.device = torch.device("cuda", device)
-        self.ds = Dataset.from_array(rows, device=device, precision=precision, global_offset=global_offset,
-                                     global_n=global_n)
+        self.ds = dataset if dataset is not None else Dataset.from_array(
+            rows, device=device, precision=precision, global_offset=global_offset, global_n=global_n)
         self.global_n = int(global_n)
         self.global_offset = int(global_offset)
         self.n_local = self.ds.n
         self.d = self.ds.d
+
+    @classmethod
+    def from_file(cls, path, world: int, rank: int, *, device: int = 0, precision: str = "auto"):
+        """This rank's contiguous row shard of a DEANN1 file, streamed file -> device (row f4)."""
+        from .data import file_info, load
+
+        n, _ = file_info(path)
+        lo, hi = shard_bounds(n, world, rank)
+        ds = load(path, device=device, precision=precision, rows=(lo, hi - lo)) if hi - lo < n else \
+            load(path, device=device, precision=precision)
+        return cls(None, global_offset=lo, global_n=n, device=device, dataset=ds)
 
     def _stream(self):
         return self.torch.cuda.current_stream(self.device).cuda_stream

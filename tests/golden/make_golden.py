@@ -23,10 +23,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, REPO)
 sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(REPO, "tests"))
 
 import deann  # noqa: E402  (the reference)
 
 from oracle.philox import IndexReplay  # noqa: E402
+from dk_testutil import malformed_files  # noqa: E402
 
 
 class _Fixed:
@@ -148,6 +150,30 @@ def main():
     out["dp_batch_cursor"] = np.array([shared.cursor])
     out["dp_indep"] = np.array([e.value for e in indep])
     out["rsp_perm80"] = deann.RspState.from_dataset(ds, 80).permuted.permutation.copy()
+
+    # --- DEANN1 files (row f4): reference save bytes, load norms, and its error messages
+    import tempfile
+
+    X = _random_dataset(37, 7, 90)
+    X[0, :3] = [-0.0, 1e-40, 3.0e38]  # signed zero, a denormal, a large finite value
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "ds.bin")
+        deann.save(deann.Dataset.from_array(X), p)
+        raw = open(p, "rb").read()
+        out["file_bytes"] = np.frombuffer(raw, np.uint8).copy()
+        out["file_sq_norms"] = deann.load(p).sq_norms.copy()
+        cases = malformed_files(raw)
+        msgs = []
+        for name, data in cases:
+            q = os.path.join(td, name)
+            open(q, "wb").write(data)
+            try:
+                deann.load(q)
+                msgs.append("")
+            except deann.DatasetFormatError as exc:
+                msgs.append(str(exc).replace(q, "<P>"))
+        out["file_bad_names"] = np.array([c[0] for c in cases])
+        out["file_bad_msgs"] = np.array(msgs)
 
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", os.path.join(HERE, "reference_golden.npz"), len(out), "arrays")
