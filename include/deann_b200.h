@@ -195,6 +195,38 @@ dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, 
                       int32_t independent, double* z_sum, int32_t* taken, int64_t* cursor_out,
                       void* stream);
 
+/* ---- inverted-file index --------------------------------
+ * ivf_build / ivf_query / IvfAnnIndex (ann.py:124-316) over a fitted dataset.
+ * The host keeps the reference's numpy PCG64 stream and drives k-means++ one
+ * centroid at a time (ann.py:152-169):
+ *   dk_kmeanspp_seed(c, row): centroid c = row; closest = D^2 to centroid 0
+ *     (c == 0) or min(closest, D^2 to c); *total = sum(closest)
+ *   dk_kmeanspp_pick(u, total): rng.choice(n, p=closest/total) given its one
+ *     uniform draw u: searchsorted(cumsum(p) / cumsum(p)[-1], u, 'right')
+ * dk_kmeans_lloyd runs the Lloyd loop of ivf_build (ann.py:184-198, fp64 norms
+ * identity, argmin ties -> lower centroid, sequential member means, empty
+ * clusters kept) plus the final assignment, and lays the rows out cluster-
+ * contiguously (IvfAnnIndex, ann.py:244-252).  dk_ivf_get copies centroids
+ * (C x d fp64), list rows (n, increasing id within a list) and offsets (C + 1);
+ * dk_ivf_set installs an existing index (a reference IvfIndex or a loaded one).
+ * dk_ivf_query: for each query the n_probe nearest centroids ((d2, id) order;
+ * formula 0 = sum (c - y)^2 as ivf_query, 1 = (C y) * -2 + |c|^2 as
+ * IvfAnnIndex) and the exact k smallest d2 = ((x.y) * -2 + |x|^2) + |y|^2
+ * (clamped at 0) over their members, (d2, row) order; cnt[j] = min(k, members
+ * probed), unused slots idx -1 / d2 +inf.  k <= 4096, n_clusters <= 8192. */
+typedef struct dk_ivf* dk_ivf_handle;
+dk_status dk_ivf_create(dk_handle h, int32_t n_clusters, dk_ivf_handle* out);
+dk_status dk_ivf_free(dk_ivf_handle ivf);
+dk_status dk_kmeanspp_seed(dk_ivf_handle ivf, int32_t c, int64_t row, double* total);
+dk_status dk_kmeanspp_pick(dk_ivf_handle ivf, double u, double total, int64_t* row);
+dk_status dk_kmeans_lloyd(dk_ivf_handle ivf, int32_t max_iter, double rel_tol, int32_t* iters);
+dk_status dk_ivf_get(dk_ivf_handle ivf, double* centroids, int64_t* rows, int64_t* offsets);
+dk_status dk_ivf_set(dk_ivf_handle ivf, const double* centroids, const int64_t* rows,
+                     const int64_t* offsets);
+dk_status dk_ivf_query(dk_ivf_handle ivf, const double* Q, int64_t nq, int32_t k, int32_t n_probe,
+                       int32_t formula, int64_t* idx_out, double* d2_out, int32_t* cnt_out,
+                       void* stream);
+
 /* Timing support for bench.py: average device duration (ms) of the LAST launch
  * of the dominant kernel of the last call on this handle (CUDA events on the
  * launching stream) and its algorithmic work. */

@@ -376,3 +376,86 @@ def deann_rsp(data: Data, family: str, h: float, neighbors, query, k: int, m: in
     z2, used, clamped = rsp_excluding(state, family, h, y, m, exclude if k_hat else None, k_hat)
     value = (k_hat / n) * z1 + ((n - k_hat) / n) * z2
     return value, k_hat + used, k_hat, used, False, clamped
+
+
+# ---------------------------------------------------------------- inverted file (row f3)
+
+KMEANS_MAX_ITER = 25   # ann.py:45
+KMEANS_REL_TOL = 1e-4  # ann.py:46
+
+
+def centroid_sqdists(x64: np.ndarray, sq_norms: np.ndarray, cent: np.ndarray) -> np.ndarray:
+    """ann.py:142-149: ((x.c) * -2 + |x|^2) + |c|^2, clamped at 0."""
+    cn = np.einsum("ij,ij->i", cent, cent)
+    out = (x64 @ cent.T) * -2.0
+    out += sq_norms[:, None]
+    out += cn[None, :]
+    return np.maximum(out, 0.0)
+
+
+def kmeans_pp(x64: np.ndarray, n_clusters: int, rng) -> np.ndarray:
+    """ann.py:152-169: D^2 seeding; one rng.choice(p=...) per further centroid."""
+    n, d = x64.shape
+    cent = np.zeros((n_clusters, d))
+    cent[0] = x64[int(rng.integers(n))]
+    diff = x64 - cent[0]
+    dmin = np.einsum("ij,ij->i", diff, diff)
+    for c in range(1, n_clusters):
+        mass = dmin.sum()
+        row = int(rng.integers(n)) if mass <= 0.0 else int(rng.choice(n, p=dmin / mass))
+        cent[c] = x64[row]
+        diff = x64 - cent[c]
+        dmin = np.minimum(dmin, np.einsum("ij,ij->i", diff, diff))
+    return cent
+
+
+def ivf_build(data: Data, n_clusters: int, seed: int):
+    """ann.py:172-199 -> (centroids (C, d), list of member arrays).
+
+    Note the convergence test uses prev = +inf on the first pass, so inf - wcss <=
+    tol * inf holds and the reference stops after one Lloyd update; restated as is.
+    """
+    n = data.n
+    if not 1 <= n_clusters <= n:
+        raise ValueError(f"n_clusters={n_clusters} out of range [1, {n}]")
+    rng = np.random.default_rng(seed)
+    cent = kmeans_pp(data.x64, n_clusters, rng)
+    prev = math.inf
+    for _ in range(KMEANS_MAX_ITER):
+        d2 = centroid_sqdists(data.x64, data.sq_norms, cent)
+        lab = np.argmin(d2, axis=1)
+        wcss = float(d2[np.arange(n), lab].sum())
+        for c in range(n_clusters):
+            sel = lab == c
+            if sel.any():
+                cent[c] = data.x64[sel].mean(axis=0)
+        if prev - wcss <= KMEANS_REL_TOL * max(prev, 1e-300):
+            break
+        prev = wcss
+    lab = np.argmin(centroid_sqdists(data.x64, data.sq_norms, cent), axis=1)
+    return cent, [np.flatnonzero(lab == c).astype(np.int64) for c in range(n_clusters)]
+
+
+def _probe(cent: np.ndarray, y: np.ndarray, n_probe: int, formula: int) -> np.ndarray:
+    """n_probe nearest centroids, ties to the lower id: formula 0 = sum (c - y)^2
+    (ivf_query, ann.py:212-214), 1 = (C y) * -2 + |c|^2 (IvfAnnIndex, ann.py:262-275)."""
+    if formula == 0:
+        diff = cent - y
+        cd = np.einsum("ij,ij->i", diff, diff)
+    else:
+        cd = (cent @ y) * -2.0 + np.einsum("ij,ij->i", cent, cent)
+    ids = np.arange(len(cent), dtype=np.int64)
+    return ids[np.lexsort((ids, cd))[:n_probe]]
+
+
+def ivf_query(data: Data, cent: np.ndarray, lists, query, k: int, n_probe: int, formula: int = 0):
+    """ann.py:202-229 -> (indices, sq_distances): exact k smallest among the probed lists."""
+    y = np.asarray(query, dtype=np.float64).ravel()
+    members = [lists[c] for c in _probe(cent, y, n_probe, formula) if len(lists[c])]
+    if not members:
+        return np.empty(0, np.int64), np.empty(0)
+    cand = np.concatenate(members)
+    d2 = (data.x64[cand] @ y) * -2.0
+    d2 += data.sq_norms[cand]
+    d2 += float(y @ y)
+    return smallest_k(np.maximum(d2, 0.0), cand, k)

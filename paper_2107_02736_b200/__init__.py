@@ -4,7 +4,9 @@ Drop-in for the estimator API of the reference package ``deann``
 (/root/reference/pkg/src/deann/__init__.py:8-43, hot-path subset):
 ``Dataset``, ``KernelFamily``/``KernelSpec``, ``naive_kde``, ``rs_kde``,
 ``deann``, ``deann_batch``, ``Estimate``/``BatchKde``, ``NeighborList``,
-``AnnIndex``/``BruteForceIndex`` (GPU brute force) and ``brute_force_knn``.
+``AnnIndex``/``BruteForceIndex`` (GPU brute force), ``brute_force_knn``, the
+inverted-file index (``ivf_build``, ``ivf_query``, ``IvfAnnIndex``), the
+permuted sampler (``RspState``, ``rsp_kde``) and DEANN1 files (``load``/``save``).
 All arithmetic runs in hand-written sm_100a kernels behind the C-ABI in
 ``include/deann_b200.h``; see DESIGN.md.
 """
@@ -25,6 +27,16 @@ from .estimators import (
     rs_kde,
     rsp_kde,
 )
+from .ivf import (
+    IvfAnnIndex,
+    IvfIndex,
+    ivf_build,
+    ivf_query,
+    ivf_query_batch,
+    load_ivf_index,
+    recall,
+    save_ivf_index,
+)
 from .kernels import KernelFamily, KernelSpec
 from .sampler import PhiloxSampler
 
@@ -36,5 +48,6 @@ __all__ = [
     "as_gpu_dataset", "file_info", "load", "save", "BatchKde",
     "Estimate", "RspState", "rsp_kde", "deann",
     "deann_arrays", "deann_batch", "kernel_from_distance", "naive_kde", "naive_kde_into", "rs_kde",
-    "KernelFamily", "KernelSpec", "PhiloxSampler",
+    "KernelFamily", "KernelSpec", "PhiloxSampler", "IvfIndex", "IvfAnnIndex", "ivf_build", "ivf_query",
+    "ivf_query_batch", "recall", "save_ivf_index", "load_ivf_index",
 ]

@@ -27,7 +27,8 @@ EXPORTED = (
     "dk_version", "dk_last_error", "dk_device_ok", "dk_fit", "dk_free", "dk_file_info", "dk_fit_file",
     "dk_info", "dk_sq_norms",
     "dk_naive", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
-    "dk_rsp_attach", "dk_rsp_walk", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
+    "dk_rsp_attach", "dk_rsp_walk", "dk_ivf_create", "dk_ivf_free", "dk_kmeanspp_seed", "dk_kmeanspp_pick",
+    "dk_kmeans_lloyd", "dk_ivf_get", "dk_ivf_set", "dk_ivf_query", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
 )
 
 
@@ -66,6 +67,14 @@ def _declare(lib):
         "dk_device_ok": (_i32, [_i32]),
         "dk_fit": (_i32, [_vp, _i64, _i32, ctypes.POINTER(FitOpts), ctypes.POINTER(_vp)]),
         "dk_free": (_i32, [_vp]),
+        "dk_ivf_create": (_i32, [_vp, _i32, ctypes.POINTER(_vp)]),
+        "dk_ivf_free": (_i32, [_vp]),
+        "dk_kmeanspp_seed": (_i32, [_vp, _i32, _i64, ctypes.POINTER(_f64)]),
+        "dk_kmeanspp_pick": (_i32, [_vp, _f64, _f64, ctypes.POINTER(_i64)]),
+        "dk_kmeans_lloyd": (_i32, [_vp, _i32, _f64, ctypes.POINTER(_i32)]),
+        "dk_ivf_get": (_i32, [_vp, _vp, _vp, _vp]),
+        "dk_ivf_set": (_i32, [_vp, _vp, _vp, _vp]),
+        "dk_ivf_query": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
         "dk_file_info": (_i32, [ctypes.c_char_p, ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
         "dk_fit_file": (_i32, [ctypes.c_char_p, _i64, _i64, ctypes.POINTER(FitOpts), ctypes.POINTER(_vp)]),
         "dk_info": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),

@@ -60,33 +60,7 @@ T* at(Workspace& ws, size_t o) {
   return reinterpret_cast<T*>(ws.base + o);
 }
 
-bool is_device_ptr(const void* p) {
-  if (!p) return false;
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
 
-template <class F>
-dk_status guard(F&& f) {
-  try {
-    f();
-    return DK_OK;
-  } catch (const Error& e) {
-    set_error(e.msg);
-    cudaGetLastError();  // do not leak a non-sticky error into the next call
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    set_error("host allocation failed");
-    return DK_ENOMEM;
-  } catch (const std::exception& e) {
-    set_error(e.what());
-    return DK_ECUDA;
-  }
-}
 
 constexpr int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 // query rows padded to whole 128-row blocks, and to an even block count beyond one block so the
@@ -99,14 +73,6 @@ void check_family_bw(int32_t family, double bw) {
   DK_REQUIRE(std::isfinite(bw) && bw > 0.0, "bandwidth must be positive and finite, got " + std::to_string(bw));
 }
 
-struct DeviceGuard {
-  int prev = 0;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) DK_CUDA(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() { cudaSetDevice(prev); }
-};
 
 // ------------------------------------------------------------------ encodings
 Encoding& enc_slot(dk_dataset* h, int mode) {

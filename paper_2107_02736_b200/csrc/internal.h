@@ -37,6 +37,44 @@ extern std::atomic<long long> g_launches;  // kernels launched by this library
     DK_CUDA(cudaGetLastError());                  \
   } while (0)
 
+inline bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// C-ABI entry wrapper: exceptions -> status + thread-local message
+template <class F>
+inline dk_status guard(F&& f) {
+  try {
+    f();
+    return DK_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    cudaGetLastError();  // do not leak a non-sticky error into the next call
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return DK_ENOMEM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return DK_ECUDA;
+  }
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) DK_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
 // Opt a kernel into `bytes` of dynamic shared memory (only ever raises the limit).
 template <class K>
 inline void set_dynamic_smem(K* kernel, size_t bytes) {

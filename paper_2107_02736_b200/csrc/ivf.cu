@@ -1,0 +1,651 @@
+// ivf.cu — GPU inverted-file index: k-means build and probed scans.
+//
+// Reference: ann.py:124-316 (IvfIndex, _centroid_sqdists, _kmeans_pp_init,
+// ivf_build, ivf_query, IvfAnnIndex).  The build keeps the reference's numpy
+// PCG64 stream on the host (ivf.py drives k-means++ one centroid at a time and
+// draws exactly what rng.integers / rng.choice draw); everything that touches
+// the n rows runs here:
+//   * k-means++ distances   closest_i = min(closest_i, sum_j (x_ij - c_j)^2)      fp64
+//   * rng.choice(n, p)      searchsorted(cumsum(p) / cumsum(p)[-1], u, 'right')   fp64 scan
+//   * Lloyd assignment      d2 = ((x.c) * -2 + |x|^2) + |c|^2, argmin (lower id on ties), fp64
+//                           register-tiled over (64 rows x 64 centroids) tiles
+//   * centroid update       members in increasing row order summed sequentially in fp64 /
+//                           count — numpy's axis-0 mean — empty clusters keep their centroid
+//   * inverted lists        stable radix sort of (label, row): rows cluster-contiguous in
+//                           increasing id order = np.flatnonzero(labels == c); the fp32 rows
+//                           are re-stored in that order so a probed list is one contiguous block
+// Query (batched): per query the n_probe nearest centroids ((d2, id) order), then an
+// exact fp64 scan of the probed lists with a shared-memory top-k ((d2, row) order,
+// threshold-filtered), d2 = ((x.y) * -2 + |x|^2) + |y|^2 clamped at 0 (ann.py:224-229).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "internal.h"
+
+struct dk_ivf {
+  dk_dataset* ds = nullptr;
+  int32_t C = 0, d = 0;
+  int64_t n = 0;
+  double* cent = nullptr;        // [C][d]
+  double* cnorm = nullptr;       // [C]
+  double* closest = nullptr;     // [n]  k-means++ D^2
+  double* cdf = nullptr;         // [n]
+  int32_t* labels = nullptr;     // [n]
+  int32_t* labels_s = nullptr;   // [n] sorted
+  int64_t* ids = nullptr;        // [n] 0..n-1
+  int64_t* rows = nullptr;       // [n] cluster-sorted row ids
+  int64_t* offsets = nullptr;    // [C + 1]
+  double* d2min = nullptr;       // [n]
+  float* xs = nullptr;           // [n][d] rows in list order
+  double* xns = nullptr;         // [n] |x|^2 in list order
+  double* scal = nullptr;        // device scalars
+  void* temp = nullptr;          // CUB scratch
+  size_t temp_bytes = 0;
+  bool lists = false;
+};
+
+namespace dk {
+namespace {
+
+struct K128 {
+  unsigned long long hi, lo;
+};
+__device__ __forceinline__ bool k_less(const K128& a, const K128& b) {
+  return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
+}
+__device__ void bitonic(K128* buf, int B) {
+  for (int k = 2; k <= B; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < B; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const K128 a = buf[i], b = buf[ixj];
+          if (k_less(b, a) == up) { buf[i] = b; buf[ixj] = a; }
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- build
+
+__global__ void set_row_kernel(const float* __restrict__ X, int64_t row, int32_t d, double* __restrict__ c) {
+  for (int j = threadIdx.x; j < d; j += blockDim.x) c[j] = double(X[row * d + j]);
+}
+
+// k-means++ D^2 update (ann.py:157-168): warp per row, direct difference in fp64
+__global__ void pp_dist_kernel(const float* __restrict__ X, int64_t n, int32_t d, const double* __restrict__ c,
+                               int init, double* __restrict__ closest) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float* x = X + row * d;
+  double s = 0.0;
+  for (int j = lane; j < d; j += 32) {
+    const double t = double(x[j]) - c[j];
+    s = fma(t, t, s);
+  }
+  s = warp_sum(s);
+  if (lane == 0) closest[row] = init ? s : fmin(closest[row], s);
+}
+
+__global__ void div_kernel(const double* __restrict__ a, int64_t n, double total, double* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] / total;
+}
+
+// first i with cdf[i] / cdf[n-1] > u (numpy searchsorted side='right' on the normalised cdf)
+__global__ void search_kernel(const double* __restrict__ cdf, int64_t n, double u, int64_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double last = cdf[n - 1];
+  const bool here = cdf[i] / last > u;
+  const bool before = i > 0 && cdf[i - 1] / last > u;
+  if (here && !before) *out = i;
+}
+
+__global__ void cnorm_kernel(const double* __restrict__ cent, int32_t C, int32_t d, double* __restrict__ cn) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
+  double s = 0.0;
+  for (int j = lane; j < d; j += 32) s = fma(cent[size_t(c) * d + j], cent[size_t(c) * d + j], s);
+  s = warp_sum(s);
+  if (lane == 0) cn[c] = s;
+}
+
+// Lloyd assignment (ann.py:142-149, 187-189): 64 rows x 64 centroids per tile, 4 x 4 fp64
+// accumulators per thread, K staged through shared memory in chunks of 16.
+constexpr int AM = 64, AN = 64, AK = 16;
+__global__ __launch_bounds__(256) void assign_kernel(const float* __restrict__ X, const double* __restrict__ xn,
+                                                     int64_t n, int32_t d, const double* __restrict__ cent,
+                                                     const double* __restrict__ cn, int32_t C,
+                                                     int32_t* __restrict__ labels, double* __restrict__ d2min) {
+  __shared__ double xsm[AK][AM + 2];
+  __shared__ __align__(16) double csm[AK][AN];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t row0 = int64_t(blockIdx.x) * AM;
+  double best[4];
+  int bidx[4];
+  double xnr[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    best[i] = __longlong_as_double(0x7ff0000000000000ll);
+    bidx[i] = 0;
+    const int64_t r = row0 + ty * 4 + i;
+    xnr[i] = r < n ? xn[r] : 0.0;
+  }
+  for (int c0 = 0; c0 < C; c0 += AN) {
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < d; k0 += AK) {
+      for (int e = threadIdx.x; e < AM * AK; e += 256) {
+        const int r = e / AK, kk = e % AK;
+        const int64_t row = row0 + r;
+        xsm[kk][r] = (row < n && k0 + kk < d) ? double(X[row * d + k0 + kk]) : 0.0;
+      }
+      for (int e = threadIdx.x; e < AN * AK; e += 256) {
+        const int cc = e / AK, kk = e % AK;
+        const int c = c0 + cc;
+        csm[kk][cc] = (c < C && k0 + kk < d) ? cent[size_t(c) * d + k0 + kk] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < AK; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = xsm[kk][ty * 4 + i];
+        const double2 b01 = *reinterpret_cast<const double2*>(&csm[kk][tx * 4]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&csm[kk][tx * 4 + 2]);
+        b[0] = b01.x; b[1] = b01.y; b[2] = b23.x; b[3] = b23.y;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + tx * 4 + j;
+      if (c < C) {
+        const double cnc = cn[c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double t = acc[i][j] * -2.0;
+          t += xnr[i];
+          t += cnc;
+          t = fmax(t, 0.0);
+          if (t < best[i]) { best[i] = t; bidx[i] = c; }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best[i], o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx[i], o);
+      if (ob < best[i] || (ob == best[i] && oi < bidx[i])) { best[i] = ob; bidx[i] = oi; }
+    }
+    const int64_t r = row0 + ty * 4 + i;
+    if (tx == 0 && r < n) {
+      labels[r] = bidx[i];
+      d2min[r] = best[i];
+    }
+  }
+}
+
+__global__ void iota_kernel(int64_t* __restrict__ a, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+// offsets[c] = first position of label c in the sorted labels (c = 0..C)
+__global__ void offsets_kernel(const int32_t* __restrict__ ls, int64_t n, int32_t C, int64_t* __restrict__ off) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > C) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ls[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  off[c] = lo;
+}
+
+// centroid c, dims j: sequential fp64 sum over members in increasing row order, / count
+// (numpy's x64[labels == c].mean(axis=0)); empty clusters keep their centroid (ann.py:191-193)
+__global__ void update_kernel(const float* __restrict__ X, int32_t d, const int64_t* __restrict__ rows,
+                              const int64_t* __restrict__ off, int32_t C, double* __restrict__ cent) {
+  const int c = blockIdx.x;
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= C || j >= d) return;
+  const int64_t b = off[c], e = off[c + 1];
+  if (e == b) return;
+  double acc = 0.0;
+  int64_t m = b;
+  for (; m + 4 <= e; m += 4) {
+    const int64_t r0 = rows[m], r1 = rows[m + 1], r2 = rows[m + 2], r3 = rows[m + 3];
+    const float v0 = X[r0 * d + j], v1 = X[r1 * d + j], v2 = X[r2 * d + j], v3 = X[r3 * d + j];
+    acc += double(v0);
+    acc += double(v1);
+    acc += double(v2);
+    acc += double(v3);
+  }
+  for (; m < e; ++m) acc += double(X[rows[m] * d + j]);
+  cent[size_t(c) * d + j] = acc / double(e - b);
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ X, const double* __restrict__ xn, int32_t d,
+                                   const int64_t* __restrict__ rows, int64_t n, float* __restrict__ xs,
+                                   double* __restrict__ xns) {
+  const int64_t p = blockIdx.x;
+  if (p >= n) return;
+  const int64_t r = rows[p];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) xs[p * d + j] = X[r * d + j];
+  if (threadIdx.x == 0) xns[p] = xn[r];
+}
+
+// ---------------------------------------------------------------- query
+
+// n_probe nearest centroids per query, (d2, id) order.  formula 0: sum (c - y)^2
+// (ivf_query, ann.py:212-214); formula 1: (C y) * -2 + |c|^2 (IvfAnnIndex._probe_clusters,
+// ann.py:262-275).  Block per query, bitonic over pow2(C) keys in shared memory.
+__global__ void probe_kernel(const double* __restrict__ Q, int32_t d, const double* __restrict__ cent,
+                             const double* __restrict__ cn, int32_t C, int32_t Bc, int32_t n_probe,
+                             int32_t formula, int32_t* __restrict__ probe) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K128* keys = reinterpret_cast<K128*>(smem_raw);
+  double* y = reinterpret_cast<double*>(keys + Bc);
+  const int64_t q = blockIdx.x;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) y[j] = Q[q * d + j];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < Bc; c += nw) {
+    K128 k{~0ull, ~0ull};
+    if (c < C) {
+      double s = 0.0;
+      const double* cc = cent + size_t(c) * d;
+      if (formula == 0) {
+        for (int j = lane; j < d; j += 32) {
+          const double t = cc[j] - y[j];
+          s = fma(t, t, s);
+        }
+        s = warp_sum(s);
+      } else {
+        for (int j = lane; j < d; j += 32) s = fma(cc[j], y[j], s);
+        s = warp_sum(s);
+        s = s * -2.0 + cn[c];
+      }
+      // order-preserving map of a signed double onto unsigned bits
+      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(s));
+      k.hi = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+      k.lo = static_cast<unsigned long long>(c);
+    }
+    if (lane == 0) keys[c] = k;
+  }
+  bitonic(keys, Bc);
+  for (int i = threadIdx.x; i < n_probe; i += blockDim.x) probe[q * n_probe + i] = int32_t(keys[i].lo);
+}
+
+// Exact scan of the probed lists with a (d2, row) top-k in shared memory.  Rounds of
+// R rows: warps compute fp64 distances (warp per row), rows beating the current k-th
+// key are staged, and a bitonic merge of [top | stage] keeps the k smallest.
+__global__ void scan_kernel(const float* __restrict__ xs, const double* __restrict__ xns,
+                            const int64_t* __restrict__ rows, const int64_t* __restrict__ off, int32_t d,
+                            const double* __restrict__ Q, const int32_t* __restrict__ probe, int32_t n_probe,
+                            int32_t k, int32_t Kp, int64_t* __restrict__ idx_out, double* __restrict__ d2_out,
+                            int32_t* __restrict__ cnt_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K128* top = reinterpret_cast<K128*>(smem_raw);  // [2 Kp]: sorted top Kp, then the stage
+  double* y = reinterpret_cast<double*>(top + 2 * Kp);
+  __shared__ int s_cnt;
+  __shared__ double s_yy;
+  const int64_t q = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) y[j] = Q[q * d + j];
+  for (int i = threadIdx.x; i < 2 * Kp; i += blockDim.x) top[i] = K128{~0ull, ~0ull};
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  if (warp == 0) {
+    double s = 0.0;
+    for (int j = lane; j < d; j += 32) s = fma(y[j], y[j], s);
+    s = warp_sum(s);
+    if (lane == 0) s_yy = s;
+  }
+  __syncthreads();
+  const double yy = s_yy;
+  int64_t total = 0;
+  const int R = min(Kp, 256);
+  for (int p = 0; p < n_probe; ++p) {
+    const int c = probe[q * n_probe + p];
+    const int64_t b = off[c], e = off[c + 1];
+    total += e - b;
+    for (int64_t r0 = b; r0 < e; r0 += R) {
+      const K128 tau = top[Kp - 1];
+      const int64_t r1 = min(e, r0 + R);
+      for (int64_t pos = r0 + warp; pos < r1; pos += nw) {
+        const float* x = xs + pos * d;
+        double s = 0.0;
+        for (int j = lane; j < d; j += 32) s = fma(double(x[j]), y[j], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+          double t = s * -2.0;
+          t += xns[pos];
+          t += yy;
+          t = fmax(t, 0.0);
+          const K128 key{static_cast<unsigned long long>(__double_as_longlong(t)),
+                         static_cast<unsigned long long>(rows[pos])};
+          if (k_less(key, tau)) top[Kp + atomicAdd(&s_cnt, 1)] = key;
+        }
+      }
+      __syncthreads();
+      if (s_cnt > 0) {
+        bitonic(top, 2 * Kp);
+        for (int i = Kp + threadIdx.x; i < 2 * Kp; i += blockDim.x) top[i] = K128{~0ull, ~0ull};
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+      }
+    }
+  }
+  const int cnt = int(total < int64_t(k) ? total : int64_t(k));
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const bool ok = i < cnt;
+    idx_out[q * k + i] = ok ? static_cast<int64_t>(top[i].lo) : -1;
+    d2_out[q * k + i] = ok ? __longlong_as_double(static_cast<long long>(top[i].hi))
+                           : __longlong_as_double(0x7ff0000000000000ll);
+  }
+  if (threadIdx.x == 0) cnt_out[q] = cnt;
+}
+
+size_t cub_bytes(int64_t n) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceReduce::Sum(nullptr, a, static_cast<const double*>(nullptr), static_cast<double*>(nullptr), n);
+  cub::DeviceScan::InclusiveSum(nullptr, b, static_cast<const double*>(nullptr), static_cast<double*>(nullptr), n);
+  cub::DeviceRadixSort::SortPairs(nullptr, c, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                  static_cast<const int64_t*>(nullptr), static_cast<int64_t*>(nullptr), n);
+  return std::max(a, std::max(b, c)) + 256;
+}
+
+void free_ivf(dk_ivf* v) {
+  if (!v) return;
+  for (void* p : {static_cast<void*>(v->cent), static_cast<void*>(v->cnorm), static_cast<void*>(v->closest),
+                  static_cast<void*>(v->cdf), static_cast<void*>(v->labels), static_cast<void*>(v->labels_s),
+                  static_cast<void*>(v->ids), static_cast<void*>(v->rows), static_cast<void*>(v->offsets),
+                  static_cast<void*>(v->d2min), static_cast<void*>(v->xs), static_cast<void*>(v->xns),
+                  static_cast<void*>(v->scal), v->temp})
+    if (p) cudaFree(p);
+  delete v;
+}
+
+struct IvfDeleter {
+  void operator()(dk_ivf* v) const { free_ivf(v); }
+};
+
+double read_scalar(const double* p) {
+  double v = 0;
+  DK_CUDA(cudaMemcpy(&v, p, sizeof(double), cudaMemcpyDeviceToHost));
+  return v;
+}
+
+void launch_cnorm(dk_ivf* v) {
+  cnorm_kernel<<<unsigned((int64_t(v->C) * 32 + 255) / 256), 256>>>(v->cent, v->C, v->d, v->cnorm);
+  DK_CHECK_LAUNCH();
+}
+
+// labels for the current centroids; returns wcss = sum of the clamped minimum d2
+double assign(dk_ivf* v) {
+  const dk_dataset* h = v->ds;
+  launch_cnorm(v);
+  assign_kernel<<<unsigned((v->n + AM - 1) / AM), 256>>>(h->X, h->xn64, v->n, v->d, v->cent, v->cnorm, v->C,
+                                                        v->labels, v->d2min);
+  DK_CHECK_LAUNCH();
+  size_t tb = v->temp_bytes;
+  DK_CUDA(cub::DeviceReduce::Sum(v->temp, tb, v->d2min, v->scal, v->n));
+  return read_scalar(v->scal);
+}
+
+// stable (label, row) sort -> cluster-contiguous rows in increasing id order + offsets
+void build_lists(dk_ivf* v) {
+  iota_kernel<<<unsigned((v->n + 255) / 256), 256>>>(v->ids, v->n);
+  DK_CHECK_LAUNCH();
+  int bits = 1;
+  while ((int64_t(1) << bits) < int64_t(v->C)) ++bits;
+  size_t tb = v->temp_bytes;
+  DK_CUDA(cub::DeviceRadixSort::SortPairs(v->temp, tb, v->labels, v->labels_s, v->ids, v->rows, v->n, 0, bits));
+  offsets_kernel<<<unsigned((v->C + 1 + 255) / 256), 256>>>(v->labels_s, v->n, v->C, v->offsets);
+  DK_CHECK_LAUNCH();
+}
+
+void update_centroids(dk_ivf* v) {
+  dim3 grid(unsigned(v->C), unsigned((v->d + 31) / 32));
+  update_kernel<<<grid, 32>>>(v->ds->X, v->d, v->rows, v->offsets, v->C, v->cent);
+  DK_CHECK_LAUNCH();
+}
+
+void restore_rows(dk_ivf* v) {
+  const dk_dataset* h = v->ds;
+  if (!v->xs) DK_CUDA(cudaMalloc(&v->xs, size_t(v->n) * v->d * sizeof(float)));
+  if (!v->xns) DK_CUDA(cudaMalloc(&v->xns, size_t(v->n) * sizeof(double)));
+  gather_rows_kernel<<<unsigned(v->n), 128>>>(h->X, h->xn64, v->d, v->rows, v->n, v->xs, v->xns);
+  DK_CHECK_LAUNCH();
+  v->lists = true;
+}
+
+}  // namespace
+}  // namespace dk
+
+using namespace dk;
+
+extern "C" {
+
+dk_status dk_ivf_create(dk_handle h, int32_t n_clusters, dk_ivf_handle* out) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr && out != nullptr, "NULL argument");
+    *out = nullptr;
+    DK_REQUIRE(n_clusters >= 1 && int64_t(n_clusters) <= h->n,
+               "n_clusters=" + std::to_string(n_clusters) + " out of range [1, " + std::to_string(h->n) + "]");
+    DeviceGuard g(h->device);
+    std::unique_ptr<dk_ivf, IvfDeleter> v(new dk_ivf());
+    v->ds = h;
+    v->C = n_clusters;
+    v->d = h->d;
+    v->n = h->n;
+    DK_CUDA(cudaMalloc(&v->cent, size_t(v->C) * v->d * sizeof(double)));
+    DK_CUDA(cudaMalloc(&v->cnorm, size_t(v->C) * sizeof(double)));
+    DK_CUDA(cudaMalloc(&v->closest, size_t(v->n) * sizeof(double)));
+    DK_CUDA(cudaMalloc(&v->cdf, size_t(v->n) * sizeof(double)));
+    DK_CUDA(cudaMalloc(&v->labels, size_t(v->n) * sizeof(int32_t)));
+    DK_CUDA(cudaMalloc(&v->labels_s, size_t(v->n) * sizeof(int32_t)));
+    DK_CUDA(cudaMalloc(&v->ids, size_t(v->n) * sizeof(int64_t)));
+    DK_CUDA(cudaMalloc(&v->rows, size_t(v->n) * sizeof(int64_t)));
+    DK_CUDA(cudaMalloc(&v->offsets, size_t(v->C + 1) * sizeof(int64_t)));
+    DK_CUDA(cudaMalloc(&v->d2min, size_t(v->n) * sizeof(double)));
+    DK_CUDA(cudaMalloc(&v->scal, 4 * sizeof(double)));
+    v->temp_bytes = cub_bytes(v->n);
+    DK_CUDA(cudaMalloc(&v->temp, v->temp_bytes));
+    *out = v.release();
+  });
+}
+
+dk_status dk_ivf_free(dk_ivf_handle v) {
+  return guard([&] {
+    if (!v) return;
+    DeviceGuard g(v->ds->device);
+    cudaDeviceSynchronize();
+    free_ivf(v);
+  });
+}
+
+dk_status dk_kmeanspp_seed(dk_ivf_handle v, int32_t c, int64_t row, double* total_out) {
+  return guard([&] {
+    DK_REQUIRE(v != nullptr && total_out != nullptr, "NULL argument");
+    DK_REQUIRE(c >= 0 && c < v->C && row >= 0 && row < v->n, "centroid or row out of range");
+    DeviceGuard g(v->ds->device);
+    double* cc = v->cent + size_t(c) * v->d;
+    set_row_kernel<<<1, 128>>>(v->ds->X, row, v->d, cc);
+    DK_CHECK_LAUNCH();
+    pp_dist_kernel<<<unsigned((v->n * 32 + 255) / 256), 256>>>(v->ds->X, v->n, v->d, cc, c == 0 ? 1 : 0,
+                                                               v->closest);
+    DK_CHECK_LAUNCH();
+    size_t tb = v->temp_bytes;
+    DK_CUDA(cub::DeviceReduce::Sum(v->temp, tb, v->closest, v->scal, v->n));
+    *total_out = read_scalar(v->scal);
+  });
+}
+
+dk_status dk_kmeanspp_pick(dk_ivf_handle v, double u, double total, int64_t* row_out) {
+  return guard([&] {
+    DK_REQUIRE(v != nullptr && row_out != nullptr, "NULL argument");
+    DK_REQUIRE(total > 0.0 && u >= 0.0 && u < 1.0, "pick needs total > 0 and u in [0, 1)");
+    DeviceGuard g(v->ds->device);
+    div_kernel<<<unsigned((v->n + 255) / 256), 256>>>(v->closest, v->n, total, v->cdf);
+    DK_CHECK_LAUNCH();
+    size_t tb = v->temp_bytes;
+    DK_CUDA(cub::DeviceScan::InclusiveSum(v->temp, tb, v->cdf, v->cdf, v->n));
+    int64_t* out = reinterpret_cast<int64_t*>(v->scal + 1);
+    const int64_t sentinel = v->n - 1;  // cdf[-1] / cdf[-1] == 1 > u always selects something
+    DK_CUDA(cudaMemcpy(out, &sentinel, sizeof(int64_t), cudaMemcpyHostToDevice));
+    search_kernel<<<unsigned((v->n + 255) / 256), 256>>>(v->cdf, v->n, u, out);
+    DK_CHECK_LAUNCH();
+    DK_CUDA(cudaMemcpy(row_out, out, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+dk_status dk_kmeans_lloyd(dk_ivf_handle v, int32_t max_iter, double rel_tol, int32_t* iters_out) {
+  return guard([&] {
+    DK_REQUIRE(v != nullptr, "NULL argument");
+    DK_REQUIRE(max_iter >= 0 && rel_tol >= 0.0, "bad k-means parameters");
+    DeviceGuard g(v->ds->device);
+    double prev = std::numeric_limits<double>::infinity();
+    int32_t it = 0;
+    for (; it < max_iter;) {  // ann.py:184-195
+      const double wcss = assign(v);
+      build_lists(v);
+      update_centroids(v);
+      ++it;
+      if (prev - wcss <= rel_tol * std::max(prev, 1e-300)) break;
+      prev = wcss;
+    }
+    assign(v);  // final assignment against the final centroids (ann.py:196-198)
+    build_lists(v);
+    launch_cnorm(v);
+    restore_rows(v);
+    DK_CUDA(cudaDeviceSynchronize());
+    if (iters_out) *iters_out = it;
+  });
+}
+
+dk_status dk_ivf_get(dk_ivf_handle v, double* centroids, int64_t* rows, int64_t* offsets) {
+  return guard([&] {
+    DK_REQUIRE(v != nullptr, "NULL argument");
+    DeviceGuard g(v->ds->device);
+    if (centroids)
+      DK_CUDA(cudaMemcpy(centroids, v->cent, size_t(v->C) * v->d * sizeof(double), cudaMemcpyDefault));
+    if (rows) DK_CUDA(cudaMemcpy(rows, v->rows, size_t(v->n) * sizeof(int64_t), cudaMemcpyDefault));
+    if (offsets) DK_CUDA(cudaMemcpy(offsets, v->offsets, size_t(v->C + 1) * sizeof(int64_t), cudaMemcpyDefault));
+  });
+}
+
+dk_status dk_ivf_set(dk_ivf_handle v, const double* centroids, const int64_t* rows, const int64_t* offsets) {
+  return guard([&] {
+    DK_REQUIRE(v != nullptr && centroids != nullptr && rows != nullptr && offsets != nullptr, "NULL argument");
+    std::vector<int64_t> off(static_cast<size_t>(v->C) + 1);
+    std::memcpy(off.data(), offsets, off.size() * sizeof(int64_t));
+    DK_REQUIRE(off[0] == 0, "offsets must start at 0");
+    for (int32_t c = 0; c < v->C; ++c) DK_REQUIRE(off[size_t(c) + 1] >= off[size_t(c)], "offsets must be nondecreasing");
+    DK_REQUIRE(off.back() == v->n, "the lists must hold every dataset row exactly once");
+    std::vector<char> seen(static_cast<size_t>(v->n), 0);
+    for (int64_t i = 0; i < v->n; ++i) {
+      DK_REQUIRE(rows[i] >= 0 && rows[i] < v->n && !seen[size_t(rows[i])],
+                 "the lists must hold every dataset row exactly once");
+      seen[size_t(rows[i])] = 1;
+    }
+    DeviceGuard g(v->ds->device);
+    DK_CUDA(cudaMemcpy(v->cent, centroids, size_t(v->C) * v->d * sizeof(double), cudaMemcpyHostToDevice));
+    DK_CUDA(cudaMemcpy(v->rows, rows, size_t(v->n) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    DK_CUDA(cudaMemcpy(v->offsets, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    launch_cnorm(v);
+    restore_rows(v);
+    DK_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, int32_t n_probe, int32_t formula,
+                       int64_t* idx_out, double* d2_out, int32_t* cnt_out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(v != nullptr, "NULL handle");
+    DK_REQUIRE(v->lists, "index lists are not built (dk_kmeans_lloyd or dk_ivf_set first)");
+    DK_REQUIRE(k >= 1, "k=" + std::to_string(k) + " must be >= 1");
+    DK_REQUIRE(n_probe >= 1 && n_probe <= v->C,
+               "n_probe=" + std::to_string(n_probe) + " out of range [1, " + std::to_string(v->C) + "]");
+    DK_REQUIRE(k <= 4096, "k > 4096 is not supported by the IVF scan");
+    DK_REQUIRE(formula == 0 || formula == 1, "unknown probe formula");
+    DK_REQUIRE(nq >= 0, "negative query count");
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && idx_out != nullptr && d2_out != nullptr && cnt_out != nullptr, "NULL argument");
+    dk_dataset* h = v->ds;
+    DeviceGuard g(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int Bc = 2;
+    while (Bc < v->C) Bc <<= 1;
+    const size_t probe_smem = size_t(Bc) * sizeof(K128) + size_t(v->d) * sizeof(double);
+    DK_REQUIRE(probe_smem <= 232448, "n_clusters too large for the GPU probe (max 8192 at d <= 4096)");
+    int Kp = 32;
+    while (Kp < k) Kp <<= 1;
+    const size_t scan_smem = size_t(2 * Kp) * sizeof(K128) + size_t(v->d) * sizeof(double);
+    DK_REQUIRE(scan_smem <= 232000, "k or d too large for the IVF scan");
+    // staging: queries, probe lists, outputs
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t a = (off + 255) & ~size_t(255);
+      off = a + bytes;
+      return a;
+    };
+    const size_t o_q = take(size_t(nq) * v->d * sizeof(double));
+    const size_t o_p = take(size_t(nq) * n_probe * sizeof(int32_t));
+    const size_t o_i = take(size_t(nq) * k * sizeof(int64_t));
+    const size_t o_d = take(size_t(nq) * k * sizeof(double));
+    const size_t o_c = take(size_t(nq) * sizeof(int32_t));
+    h->ws.reserve(off);
+    uint8_t* base = h->ws.base;
+    const double* Qd = Q;
+    if (!is_device_ptr(Q)) {
+      DK_CUDA(cudaMemcpyAsync(base + o_q, Q, size_t(nq) * v->d * sizeof(double), cudaMemcpyHostToDevice, s));
+      Qd = reinterpret_cast<const double*>(base + o_q);
+    }
+    int32_t* probe = reinterpret_cast<int32_t*>(base + o_p);
+    set_dynamic_smem(probe_kernel, probe_smem);
+    probe_kernel<<<unsigned(nq), 256, probe_smem, s>>>(Qd, v->d, v->cent, v->cnorm, v->C, Bc, n_probe, formula,
+                                                      probe);
+    DK_CHECK_LAUNCH();
+    const bool idev = is_device_ptr(idx_out), ddev = is_device_ptr(d2_out), cdev = is_device_ptr(cnt_out);
+    int64_t* io = idev ? idx_out : reinterpret_cast<int64_t*>(base + o_i);
+    double* dd = ddev ? d2_out : reinterpret_cast<double*>(base + o_d);
+    int32_t* co = cdev ? cnt_out : reinterpret_cast<int32_t*>(base + o_c);
+    set_dynamic_smem(scan_kernel, scan_smem);
+    scan_kernel<<<unsigned(nq), 256, scan_smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, Qd, probe, n_probe,
+                                                    k, Kp, io, dd, co);
+    DK_CHECK_LAUNCH();
+    if (!idev) DK_CUDA(cudaMemcpyAsync(idx_out, io, size_t(nq) * k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (!ddev) DK_CUDA(cudaMemcpyAsync(d2_out, dd, size_t(nq) * k * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (!cdev) DK_CUDA(cudaMemcpyAsync(cnt_out, co, size_t(nq) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (!idev || !ddev || !cdev) DK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+}  // extern "C"

@@ -308,7 +308,48 @@ def deann_batch(dataset, kernel, ann, queries, k: int, m: int, *, rng=None, rsp_
         values, _, _ = deann_arrays(ds, spec, q, k, m, seed=seed, query_base=base)
         return [Estimate(value=float(v), kernel_evals=k + m, neighbors_used=k, samples_used=m,
                          truncated=(m == 0 and k < n)) for v in values]
+    if _is_gpu_ivf(ann, ds):
+        return _deann_ivf_batch(ds, spec, ann, q, k, m, rng)
     return [deann(ds, spec, ann, q[j], k, m, rng=rng, rsp_state=rsp_state) for j in range(q.shape[0])]
+
+
+def _is_gpu_ivf(ann, ds: Dataset) -> bool:
+    from .ivf import IvfAnnIndex
+
+    return isinstance(ann, IvfAnnIndex) and ann._ds is ds
+
+
+def _deann_ivf_batch(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, rng) -> list[Estimate]:
+    """DEANN over a batch with the GPU IVF index: one probed scan for all queries, neighbour
+    lists of per-query length k_hat (ann.py:30-31: a short probe set is not an error), then one
+    Philox sampling pass excluding each query's list (estimators.py:338-372)."""
+    n = ds.n
+    nq = q.shape[0]
+    idx, d2, cnt = ann.query_batch(q, k)
+    cnt = np.ascontiguousarray(cnt, dtype=np.int32)
+    z1 = np.zeros(nq)
+    if spec.family is KernelFamily.LAPLACIAN:
+        sums = np.empty(nq, dtype=np.float64)
+        rows = np.ascontiguousarray(np.where(idx >= 0, idx, 0))
+        _lib.check(_lib.load().dk_eval_rows(ds.handle, q.ctypes.data, nq, _lib.DK_LAPLACIAN, spec.bandwidth,
+                                            rows.ctypes.data, cnt.ctypes.data, k, sums.ctypes.data, None))
+        z1 = np.where(cnt > 0, sums / np.maximum(cnt, 1), 0.0)
+    else:
+        dist = d2 if spec.family is KernelFamily.GAUSSIAN else np.sqrt(d2)
+        kv = np.where(idx >= 0, kernel_from_distance(spec, np.where(idx >= 0, dist, 0.0)), 0.0)
+        z1 = np.where(cnt > 0, kv.sum(axis=1) / np.maximum(cnt, 1), 0.0)
+    if m == 0:
+        return [Estimate(value=(int(c) / n) * float(z), kernel_evals=int(c), neighbors_used=int(c), samples_used=0,
+                         truncated=int(c) < n) for c, z in zip(cnt, z1)]
+    seed, base = resolve_sampler(rng).take(nq)
+    excl = np.ascontiguousarray(np.where(idx >= 0, idx, 0))
+    z, _ = _sample_sums(ds, spec, q, m, seed, base, excl=excl, excl_cnt=cnt, stride=k)
+    out = []
+    for j in range(nq):
+        kh = int(cnt[j])
+        value = (kh / n) * float(z1[j]) + ((n - kh) / n) * float(z[j] / m)
+        out.append(Estimate(value=value, kernel_evals=kh + m, neighbors_used=kh, samples_used=m))
+    return out
 
 
 def _deann_rsp(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, state, independent: bool) -> list[Estimate]:

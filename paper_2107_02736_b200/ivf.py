@@ -1,0 +1,253 @@
+"""Inverted-file k-means index on the GPU.
+
+Mirrors reference ann.py:124-352: ``IvfIndex``, ``ivf_build``, ``ivf_query``,
+``IvfAnnIndex``, ``recall``, ``save_ivf_index`` / ``load_ivf_index``.
+
+* ``ivf_build`` keeps the reference's numpy PCG64 stream on the host and draws
+  exactly what ``_kmeans_pp_init`` draws (``rng.integers(n)`` for the first
+  centroid; per further centroid one ``rng.random()`` — the single uniform
+  ``rng.choice(n, p=...)`` consumes — or ``rng.integers(n)`` when all mass sits
+  on existing centroids).  Every pass over the n rows runs on the device
+  (csrc/ivf.cu): the D^2 updates, the cumulative-probability search, the Lloyd
+  assignment (fp64, ties to the lower centroid), the sequential member means and
+  the final inverted lists.
+* ``ivf_query`` / ``IvfAnnIndex.query`` / ``query_batch`` probe the n_probe
+  nearest centroids ((d2, id) order) and return the exact k smallest
+  d2 = ((x.y) * -2 + |x|^2) + |y|^2 among their members, (d2, row) order.
+  ``IvfAnnIndex`` ranks candidates in fp64 where the reference ranks them in
+  fp32 before its fp64 re-evaluation (ann.py:294-316); the two agree except when
+  fp32 rounding reorders rows at the k-th boundary, where this one is exact.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .ann import AnnIndex, NeighborList
+from .data import as_gpu_dataset
+
+__all__ = ["IvfIndex", "IvfAnnIndex", "ivf_build", "ivf_query", "ivf_query_batch", "recall", "save_ivf_index",
+           "load_ivf_index", "KMEANS_MAX_ITER", "KMEANS_REL_TOL"]
+
+IVF_MAGIC = b"DEANNIVF"
+IVF_VERSION = 1
+KMEANS_MAX_ITER = 25      # ann.py:45
+KMEANS_REL_TOL = 1e-4     # ann.py:46
+
+
+class _DeviceIvf:
+    """A dk_ivf handle bound to one fitted dataset."""
+
+    def __init__(self, ds, n_clusters: int):
+        self.ds = ds
+        self.n_clusters = int(n_clusters)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().dk_ivf_create(ds.handle, self.n_clusters, ctypes.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, _free, h)
+
+    def export(self):
+        C, d, n = self.n_clusters, self.ds.d, self.ds.n
+        cent = np.empty((C, d), dtype=np.float64)
+        rows = np.empty(n, dtype=np.int64)
+        off = np.empty(C + 1, dtype=np.int64)
+        _lib.check(_lib.load().dk_ivf_get(self.handle, cent.ctypes.data, rows.ctypes.data, off.ctypes.data))
+        return cent, rows, off
+
+    def install(self, centroids, assignments):
+        cent = np.ascontiguousarray(centroids, dtype=np.float64)
+        sizes = np.array([len(a) for a in assignments], dtype=np.int64)
+        rows = np.ascontiguousarray(np.concatenate([np.asarray(a, dtype=np.int64) for a in assignments])
+                                    if len(assignments) else np.empty(0, np.int64))
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        _lib.check(_lib.load().dk_ivf_set(self.handle, cent.ctypes.data, rows.ctypes.data, off.ctypes.data))
+
+    def query(self, Q: np.ndarray, k: int, n_probe: int, formula: int):
+        nq = Q.shape[0]
+        idx = np.empty((nq, k), dtype=np.int64)
+        d2 = np.empty((nq, k), dtype=np.float64)
+        cnt = np.empty(nq, dtype=np.int32)
+        _lib.check(_lib.load().dk_ivf_query(self.handle, Q.ctypes.data, nq, k, n_probe, formula, idx.ctypes.data,
+                                            d2.ctypes.data, cnt.ctypes.data, None))
+        return idx, d2, cnt
+
+
+def _free(h):
+    try:
+        _lib.load().dk_ivf_free(h)
+    except Exception:  # interpreter shutdown
+        pass
+
+
+@dataclass
+class IvfIndex:
+    """k-means centroids plus per-cluster member lists (ann.py:124-139)."""
+
+    centroids: np.ndarray
+    assignments: list
+    seed: int
+    _device: dict = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def n_clusters(self) -> int:
+        return self.centroids.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self.centroids.shape[1]
+
+
+# device copies of indices we did not build (the reference's IvfIndex, loaded files)
+_FOREIGN: dict = {}
+
+
+def _device_index(index, ds) -> _DeviceIvf:
+    cache = getattr(index, "_device", None)
+    if not isinstance(cache, dict):
+        key = id(index)
+        cache = _FOREIGN.get(key)
+        if cache is None:
+            cache = _FOREIGN[key] = {}
+            weakref.finalize(index, _FOREIGN.pop, key, None)
+    dev = cache.get(id(ds))
+    if dev is None or dev.ds is not ds:
+        dev = _DeviceIvf(ds, len(index.assignments))
+        dev.install(index.centroids, index.assignments)
+        cache[id(ds)] = dev
+    return dev
+
+
+def ivf_build(dataset, n_clusters: int, seed: int) -> IvfIndex:
+    """Lloyd's k-means with k-means++ seeding on the GPU; deterministic given seed (ann.py:172-199)."""
+    ds = as_gpu_dataset(dataset)
+    n = ds.n
+    if not 1 <= n_clusters <= n:
+        raise ValueError(f"n_clusters={n_clusters} out of range [1, {n}]")
+    lib = _lib.load()
+    rng = np.random.default_rng(seed)
+    dev = _DeviceIvf(ds, n_clusters)
+    total = ctypes.c_double()
+    pick = ctypes.c_int64()
+    first = int(rng.integers(n))
+    _lib.check(lib.dk_kmeanspp_seed(dev.handle, 0, first, ctypes.byref(total)))
+    for c in range(1, n_clusters):  # ann.py:157-169
+        if total.value <= 0.0:
+            row = int(rng.integers(n))
+        else:
+            _lib.check(lib.dk_kmeanspp_pick(dev.handle, float(rng.random()), total.value, ctypes.byref(pick)))
+            row = int(pick.value)
+        _lib.check(lib.dk_kmeanspp_seed(dev.handle, c, row, ctypes.byref(total)))
+    iters = ctypes.c_int32()
+    _lib.check(lib.dk_kmeans_lloyd(dev.handle, KMEANS_MAX_ITER, KMEANS_REL_TOL, ctypes.byref(iters)))
+    cent, rows, off = dev.export()
+    assignments = [rows[off[c]:off[c + 1]].copy() for c in range(n_clusters)]
+    index = IvfIndex(centroids=cent, assignments=assignments, seed=seed)
+    index._device[id(ds)] = dev
+    return index
+
+
+def _check_query(index, k: int, n_probe: int, d: int):
+    if k < 1:
+        raise ValueError(f"k={k} must be >= 1")
+    if not 1 <= n_probe <= index.n_clusters:
+        raise ValueError(f"n_probe={n_probe} out of range [1, {index.n_clusters}]")
+    if d != index.d:
+        raise ValueError(f"dimension mismatch: query d={d}, index d={index.d}")
+
+
+def _as_list(idx, d2, cnt, j) -> NeighborList:
+    c = int(cnt[j])
+    return NeighborList(indices=idx[j, :c].copy(), sq_distances=d2[j, :c].copy())
+
+
+def ivf_query_batch(index, dataset, queries, k: int, n_probe: int, *, formula: int = 0):
+    """Batched ivf_query: (idx (nq, k), d2 (nq, k), count (nq,)); unused slots -1 / +inf."""
+    ds = as_gpu_dataset(dataset)
+    Q = np.ascontiguousarray(np.atleast_2d(np.asarray(queries, dtype=np.float64)))
+    _check_query(index, k, n_probe, Q.shape[1])
+    return _device_index(index, ds).query(Q, k, n_probe, formula)
+
+
+def ivf_query(index, dataset, query, k: int, n_probe: int) -> NeighborList:
+    """Exact k-NN restricted to the members of the n_probe nearest clusters (ann.py:202-229)."""
+    if k < 1:
+        raise ValueError(f"k={k} must be >= 1")
+    if not 1 <= n_probe <= index.n_clusters:
+        raise ValueError(f"n_probe={n_probe} out of range [1, {index.n_clusters}]")
+    y = np.asarray(query, dtype=np.float64).ravel()
+    idx, d2, cnt = ivf_query_batch(index, dataset, y.reshape(1, -1), k, n_probe, formula=0)
+    return _as_list(idx, d2, cnt, 0)
+
+
+class IvfAnnIndex(AnnIndex):
+    """An IvfIndex bound to its dataset and probe width (ann.py:232-316)."""
+
+    def __init__(self, dataset, index, n_probe: int):
+        if not 1 <= n_probe <= index.n_clusters:
+            raise ValueError(f"n_probe={n_probe} out of range [1, {index.n_clusters}]")
+        self.dataset = dataset
+        self.index = index
+        self.n_probe = n_probe
+        self._ds = as_gpu_dataset(dataset)
+        self._dev = _device_index(index, self._ds)
+
+    @classmethod
+    def build(cls, dataset, n_clusters: int, seed: int, n_probe: int) -> "IvfAnnIndex":
+        return cls(dataset, ivf_build(dataset, n_clusters, seed), n_probe)
+
+    def query_batch(self, queries, k: int):
+        Q = np.ascontiguousarray(np.atleast_2d(np.asarray(queries, dtype=np.float64)))
+        _check_query(self.index, k, self.n_probe, Q.shape[1])
+        return self._dev.query(Q, k, self.n_probe, 1)
+
+    def query(self, query, k: int) -> NeighborList:
+        if k < 1:
+            raise ValueError(f"k={k} must be >= 1")
+        y = np.asarray(query, dtype=np.float64).ravel()
+        if y.shape[0] != self.index.d:
+            raise ValueError(f"dimension mismatch: query d={y.shape[0]}, index d={self.index.d}")
+        idx, d2, cnt = self.query_batch(y.reshape(1, -1), k)
+        return _as_list(idx, d2, cnt, 0)
+
+
+def recall(approx, exact) -> float:
+    """|approx intersect exact| / |exact| (ann.py:319-324)."""
+    if len(exact.indices) == 0:
+        raise ValueError("exact neighbor list must be nonempty")
+    hits = np.intersect1d(approx.indices, exact.indices).size
+    return hits / len(exact.indices)
+
+
+def save_ivf_index(index, path) -> None:
+    """The reference's versioned binary container (ann.py:327-335), byte for byte."""
+    with open(path, "wb") as f:
+        f.write(IVF_MAGIC)
+        f.write(struct.pack("<IIIQ", IVF_VERSION, index.n_clusters, index.d, index.seed))
+        f.write(np.ascontiguousarray(index.centroids, dtype="<f8").tobytes())
+        for members in index.assignments:
+            f.write(struct.pack("<I", len(members)))
+            f.write(np.ascontiguousarray(members, dtype="<u4").tobytes())
+
+
+def load_ivf_index(path) -> IvfIndex:
+    """Read save_ivf_index output (ann.py:338-352); same errors."""
+    with open(path, "rb") as f:
+        magic = f.read(8)
+        if magic != IVF_MAGIC:
+            raise ValueError(f"{path}: bad index magic {magic!r}")
+        version, n_clusters, d, seed = struct.unpack("<IIIQ", f.read(20))
+        if version != IVF_VERSION:
+            raise ValueError(f"{path}: unsupported index version {version}")
+        centroids = np.frombuffer(f.read(n_clusters * d * 8), dtype="<f8").reshape(n_clusters, d)
+        assignments = []
+        for _ in range(n_clusters):
+            (count,) = struct.unpack("<I", f.read(4))
+            members = np.frombuffer(f.read(count * 4), dtype="<u4").astype(np.int64)
+            assignments.append(members)
+    return IvfIndex(centroids=centroids.copy(), assignments=assignments, seed=seed)

@@ -175,6 +175,35 @@ def main():
         out["file_bad_names"] = np.array([c[0] for c in cases])
         out["file_bad_msgs"] = np.array(msgs)
 
+    # --- inverted file (row f3): ivf_build / ivf_query / IvfAnnIndex / save_ivf_index
+    for tag, (n, d, C, seed) in {"ivf_a": (500, 6, 12, 3), "ivf_b": (20_000, 16, 64, 7)}.items():
+        X = np.random.default_rng(seed).normal(size=(n, d)).astype(np.float32)
+        Q = np.random.default_rng(seed + 1).normal(size=(8, d))
+        ds = deann.Dataset.from_array(X)
+        index = deann.ivf_build(ds, C, seed=seed)
+        out[f"{tag}_cent"] = index.centroids.copy()
+        out[f"{tag}_rows"] = np.concatenate(index.assignments).astype(np.int64)
+        out[f"{tag}_off"] = np.concatenate([[0], np.cumsum([len(a) for a in index.assignments])]).astype(np.int64)
+        probes = [1, 2, 5, C]
+        qi, qd, ai, ad = [], [], [], []
+        for p_ in probes:
+            ann = deann.IvfAnnIndex(ds, index, p_)
+            for q in Q:
+                nl = deann.ivf_query(index, ds, q, 10, p_)
+                qi.append(np.pad(nl.indices, (0, 10 - len(nl)), constant_values=-1))
+                qd.append(np.pad(nl.sq_distances, (0, 10 - len(nl)), constant_values=np.inf))
+                nl = ann.query(q, 10)
+                ai.append(np.pad(nl.indices, (0, 10 - len(nl)), constant_values=-1))
+                ad.append(np.pad(nl.sq_distances, (0, 10 - len(nl)), constant_values=np.inf))
+        out[f"{tag}_probes"] = np.array(probes)
+        out[f"{tag}_q_idx"], out[f"{tag}_q_d2"] = np.array(qi), np.array(qd)
+        out[f"{tag}_ann_idx"], out[f"{tag}_ann_d2"] = np.array(ai), np.array(ad)
+        if tag == "ivf_a":
+            with tempfile.TemporaryDirectory() as td:
+                p = os.path.join(td, "ivf.bin")
+                deann.save_ivf_index(index, p)
+                out["ivf_a_file"] = np.frombuffer(open(p, "rb").read(), np.uint8).copy()
+
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", os.path.join(HERE, "reference_golden.npz"), len(out), "arrays")
 

@@ -180,3 +180,31 @@ def test_deannp_batch_cursor_threading(golden):
         s2 = O.Permuted(d, 80, cursor=(j * d.n) // len(Q))
         indep.append(O.deann_rsp(d, "gaussian", 1.1, nb, q, 12, 50, s2)[0])
     np.testing.assert_allclose(indep, golden["dp_indep"], rtol=1e-12)
+
+
+# ------------------------------------------------------------------ inverted file (row f3)
+
+
+def _ivf_lists(golden, tag):
+    rows, off = golden[f"{tag}_rows"], golden[f"{tag}_off"]
+    return [rows[off[c]:off[c + 1]] for c in range(len(off) - 1)]
+
+
+@pytest.mark.parametrize("tag,n,d,C,seed", [("ivf_a", 500, 6, 12, 3), ("ivf_b", 20_000, 16, 64, 7)])
+def test_oracle_ivf_matches_reference_goldens(golden, tag, n, d, C, seed):
+    X = np.random.default_rng(seed).normal(size=(n, d)).astype(np.float32)
+    Q = np.random.default_rng(seed + 1).normal(size=(8, d))
+    data = O.Data(X)
+    cent, lists = O.ivf_build(data, C, seed)
+    np.testing.assert_array_equal(cent, golden[f"{tag}_cent"])
+    for a, b in zip(lists, _ivf_lists(golden, tag)):
+        np.testing.assert_array_equal(a, b)
+    i = 0
+    for p in golden[f"{tag}_probes"]:
+        for q in Q:
+            for formula, key in ((0, "q"), (1, "ann")):
+                idx, d2 = O.ivf_query(data, cent, lists, q, 10, int(p), formula)
+                gi, gd = golden[f"{tag}_{key}_idx"][i], golden[f"{tag}_{key}_d2"][i]
+                np.testing.assert_array_equal(idx, gi[gi >= 0])
+                np.testing.assert_allclose(d2, gd[gi >= 0], rtol=1e-12 if formula else 0)
+            i += 1
