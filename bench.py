@@ -58,7 +58,8 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []  # (sm_mhz, max_mhz, reasons_bitmask)
+        self.samples = []  # (t, sm_mhz, max_mhz, reasons_bitmask)
+        self.window = None  # (t0, t1) of the timed region
         self._stop = threading.Event()
         self._t = None
         self.nvml = None
@@ -77,11 +78,11 @@ class ClockSampler:
             p = self.nvml
             sm = p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM)
             reasons = p.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-            return float(sm), float(self.max_mhz), int(reasons)
+            return time.perf_counter(), float(sm), float(self.max_mhz), int(reasons)
         out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm",
                               "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
         sm, mx = (float(v) for v in out.strip().split(","))
-        return sm, mx, 0
+        return time.perf_counter(), sm, mx, 0
 
     def _run(self):
         while not self._stop.is_set():
@@ -89,7 +90,7 @@ class ClockSampler:
                 self.samples.append(self._poll())
             except Exception:
                 pass
-            self._stop.wait(0.005 if self.nvml is not None else 0.2)
+            self._stop.wait(0.002 if self.nvml is not None else 0.2)
 
     def __enter__(self):
         try:
@@ -105,19 +106,35 @@ class ClockSampler:
         if self._t:
             self._t.join(timeout=6)
 
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
     def summary(self):
+        """Samples taken inside the timed window (the sampler runs from the warm-up on, so a
+        short window is padded with the samples nearest to it until there are >= 5)."""
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
-        sm = [x[0] for x in self.samples]
+        sel = list(self.samples)
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [x for x in self.samples if t0 <= x[0] <= t1]
+            if len(inside) < 5:
+                mid = 0.5 * (t0 + t1)
+                inside = sorted(self.samples, key=lambda x: abs(x[0] - mid))[:5]
+            sel = inside
+        sm = [x[1] for x in sel]
         reasons = set()
         if self.nvml is not None:
             for name, const in self.REASONS:
                 bit = getattr(self.nvml, const, 0)
-                if any(x[2] & bit for x in self.samples):
+                if any(x[3] & bit for x in sel):
                     reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(x[1] for x in self.samples),
-                "reasons": sorted(reasons), "samples": len(self.samples),
-                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(x[2] for x in sel),
+               "reasons": sorted(reasons), "samples": len(sel),
+               "source": "nvml" if self.nvml is not None else "nvidia-smi"}
+        if self.window is not None:
+            out["window_ms"] = round(1e3 * (self.window[1] - self.window[0]), 3)
+        return out
 
 
 def _dist_env():
@@ -243,27 +260,30 @@ def run_ours(args):
             dist.all_reduce(out)
             out.mul_(1.0 / n)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    _lib.check(lib.dk_set_profiling(ds.handle, 1))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     import ctypes
 
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local) as clocks:  # running from the warm-up on: the timed region is short
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+        _lib.check(lib.dk_set_profiling(ds.handle, 1))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t_w0 = time.perf_counter()
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        t_w1 = time.perf_counter()
         if dist:
             dist.barrier()
+    clocks.mark(t_w0, t_w1)
     cnt = ctypes.c_int64()
     _lib.check(lib.dk_last_launch_count(ds.handle, ctypes.byref(cnt)))
     launches = int(cnt.value) * args.steps
@@ -432,7 +452,7 @@ def fit_manifest():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")

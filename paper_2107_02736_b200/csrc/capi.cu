@@ -733,7 +733,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
         ProfScope ps(h, s, 3.0 * double(h->d) * double(nq) * double(h->n), double(h->n) * h->d * 4);
         launch_l1_kde(h->X, h->n, h->d, Qd, nq, 1.0 / bandwidth, part, &nparts, nullptr, s);
       }
-      launch_reduce_partials(part, nparts, int32_t((nq + 63) / 64 * 64), nq, scale, od, s);
+      launch_reduce_partials(part, nparts, l1_nq_pad(nq), nq, scale, od, s);
       if (!out_dev) {
         copy_out(out, od, size_t(nq) * sizeof(double), s);
         DK_CUDA(cudaStreamSynchronize(s));

@@ -203,6 +203,7 @@ void set_pair_enabled(bool on);  // 2-CTA (cta_group::2) sweeps; off by default 
 
 // L1 / laplacian exact KDE on CUDA cores
 size_t l1_part_count(int64_t n, int32_t nq);
+int32_t l1_nq_pad(int64_t nq);  // row stride of the L1 partials
 void launch_l1_kde(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, double inv_h, double* part,
                    int32_t* nparts, float* q32, cudaStream_t s);
 

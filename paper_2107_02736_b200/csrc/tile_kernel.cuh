@@ -91,26 +91,6 @@ __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, i
   return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + stage + 512 /*barriers*/;
 }
 
-// ---------------------------------------------------------------- packed f32x2 helpers
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  float2 c;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(reinterpret_cast<uint64_t&>(c))
-      : "l"(reinterpret_cast<uint64_t&>(a)), "l"(reinterpret_cast<uint64_t&>(b)));
-  return c;
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-  float2 c;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(reinterpret_cast<uint64_t&>(c))
-      : "l"(reinterpret_cast<uint64_t&>(a)), "l"(reinterpret_cast<uint64_t&>(b)));
-  return c;
-}
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(reinterpret_cast<uint64_t&>(d))
-      : "l"(reinterpret_cast<uint64_t&>(a)), "l"(reinterpret_cast<uint64_t&>(b)),
-        "l"(reinterpret_cast<uint64_t&>(c)));
-  return d;
-}
 
 // Gaussian epilogue: which of the 16 pairs of a 32-column chunk take the FMA-pipe
 // polynomial instead of MUFU.EX2 (bit i = pair i), trading XU-pipe cycles (8 per

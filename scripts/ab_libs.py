@@ -27,8 +27,9 @@ def child(config, op, reps, out_path):
 
     man = json.load(open(os.path.join(ROOT, "tests", "golden", "bandwidths.json")))
     W = workloads.make(config)
-    fam = "exponential" if op == "naive-exp" else W.family
-    h = W.h if W.h is not None else man[config]["h"]
+    fam = {"naive-exp": "exponential", "naive-lap": "laplacian"}.get(op, W.family)
+    key = f"{config}-laplacian" if fam == "laplacian" else config
+    h = man[key]["h"] if fam == "laplacian" or W.h is None else W.h
     ds = g.Dataset.from_array(W.X)
     spec = g.KernelSpec(fam, h)
     Qd = torch.from_numpy(np.ascontiguousarray(W.Q)).cuda()
