@@ -183,22 +183,36 @@ __global__ void query_check_kernel(const double* __restrict__ Q, int64_t nq, int
   }
 }
 
-__global__ void reduce_partials_kernel(const double* __restrict__ part, int32_t nparts, int32_t nq_pad, int64_t nq,
-                                       double scale, double* __restrict__ out) {
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= nq) return;
-  // fixed summation order (deterministic); loads issued 8 ahead of the adds (latency-bound otherwise)
+// out[q] = scale * sum_j part[j][q].  Block = 32 queries x 8 warps: warp w sums parts
+// j = w, w+8, ... sequentially (coalesced over q), then the 8 warp sums are added in
+// warp order — a fixed summation tree, so the result is deterministic.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ part, int32_t nparts,
+                                                              int32_t nq_pad, int64_t nq, double scale,
+                                                              double* __restrict__ out) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = int64_t(blockIdx.x) * 32 + lane;
   double s = 0.0;
-  int j = 0;
-  for (; j + 8 <= nparts; j += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = part[size_t(j + u) * nq_pad + q];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s += v[u];
+  if (q < nq) {
+    int j = w;
+    for (; j + 24 < nparts; j += 32) {  // 4 loads in flight per thread
+      const double v0 = part[size_t(j) * nq_pad + q], v1 = part[size_t(j + 8) * nq_pad + q];
+      const double v2 = part[size_t(j + 16) * nq_pad + q], v3 = part[size_t(j + 24) * nq_pad + q];
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
+    }
+    for (; j < nparts; j += 8) s += part[size_t(j) * nq_pad + q];
   }
-  for (; j < nparts; ++j) s += part[size_t(j) * nq_pad + q];
-  out[q] = s * scale;
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && q < nq) {
+    double t = red[0][lane];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += red[i][lane];
+    out[q] = t * scale;
+  }
 }
 
 }  // namespace
@@ -257,7 +271,7 @@ void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t 
 
 void launch_reduce_partials(const double* part, int32_t nparts, int32_t nq_pad, int64_t nq, double scale, double* out,
                             cudaStream_t s) {
-  reduce_partials_kernel<<<unsigned((nq + 63) / 64), 64, 0, s>>>(part, nparts, nq_pad, nq, scale, out);
+  reduce_partials_kernel<<<unsigned((nq + 31) / 32), 256, 0, s>>>(part, nparts, nq_pad, nq, scale, out);
   DK_CHECK_LAUNCH();
 }
 

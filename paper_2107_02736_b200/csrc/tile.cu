@@ -178,3 +178,15 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
 }
 
 }  // namespace dk
+
+#ifdef DK_TIMING
+extern "C" int dk_debug_counters(unsigned long long* out, int reset) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return 2;
+  if (cudaMemcpyFromSymbol(out, dk::g_dbg, sizeof(unsigned long long) * 8) != cudaSuccess) return 2;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(dk::g_dbg, z, sizeof(z)) != cudaSuccess) return 2;
+  }
+  return 0;
+}
+#endif

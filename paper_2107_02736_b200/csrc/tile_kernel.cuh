@@ -34,6 +34,21 @@
 
 namespace dk {
 
+#ifdef DK_TIMING
+// debug-only wait accounting (scripts/epi_timing.py): [0] epilogue tfull wait cycles,
+// [1] epilogue xfull wait, [2] epilogue busy cycles, [3] MMA tempty wait, [4] MMA full wait,
+// [5] producer empty wait, [6] epilogue tile count
+__device__ unsigned long long g_dbg[8];
+#define DK_TWAIT(slot, call)               \
+  do {                                     \
+    const long long t0_ = clock64();       \
+    call;                                  \
+    dbgw[slot] += clock64() - t0_;         \
+  } while (0)
+#else
+#define DK_TWAIT(slot, call) call
+#endif
+
 enum TileMode : int {
   MODE_KDE_GAUSS = 0,
   MODE_KDE_EXP = 1,
@@ -307,6 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+#ifdef DK_TIMING
+  long long dbgw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
   if (warp == 0) {
     // ===================== TMA producer (each CTA) =====================
@@ -342,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_load(smemX + xs * kBN, p.xn + col0, kBN * 4, &xfull_bar[xs]);
           }
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            mbar_wait(&empty_bar[stage], phase ^ 1);
+            DK_TWAIT(5, mbar_wait(&empty_bar[stage], phase ^ 1));
             if constexpr (kPair) {
               const uint32_t bytes = 2u * (kBStage + (p.a_resident ? 0u : uint32_t(kABlockBytes)));
               if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
@@ -385,11 +403,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         for (int t = t0; t < t1; ++t) {
-          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          DK_TWAIT(3, mbar_wait(&tempty_bar[acc], acc_phase ^ 1));
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + uint32_t(acc * kBN);
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            mbar_wait(&full_bar[stage], phase);
+            DK_TWAIT(4, mbar_wait(&full_bar[stage], phase));
             tc_fence_after();
             const uint32_t abase = p.a_resident ? a0 + uint32_t(kb) * kABlockBytes : a0 + uint32_t(stage) * kABlockBytes;
             const uint32_t bbase = b0 + uint32_t(stage) * kBStage;
@@ -424,6 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t titer = 0;
     const float m2s = *p.m2s;
     const float negc = p.negc;
+#ifdef DK_TIMING
+    const long long tepi0 = clock64();
+#endif
     for (int u = first_unit; u < nunits; u += unit_step) {
       const int qb = (u % ngroups) * (kPair ? 2 : 1) + int(crank), cc = u / ngroups;
       const int t0 = cc * p.tiles_per_unit;
@@ -447,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mn = __int_as_float(0x7f800000);
           }
         }
-        mbar_wait(&tfull_bar[acc], acc_phase);
+        DK_TWAIT(0, mbar_wait(&tfull_bar[acc], acc_phase));
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN + cg * 64);
         uint32_t r0[32], r1[32];
@@ -461,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else mbar_arrive(&tempty_bar[acc]);
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
+        DK_TWAIT(1, mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1));
         if constexpr (MODE == MODE_NULL) {  // pipeline probe: consume the accumulator, no epilogue math
           uint32_t x = 0;
 #pragma unroll
@@ -509,7 +530,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi_bar();
       }
     }
+#ifdef DK_TIMING
+    dbgw[2] = clock64() - tepi0;
+    dbgw[6] = titer;
+#endif
   }
+#ifdef DK_TIMING
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (dbgw[i]) atomicAdd(&g_dbg[i], (unsigned long long)dbgw[i]);
+#endif
 
   __syncwarp();
   tc_fence_before();
