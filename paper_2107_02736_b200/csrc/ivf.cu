@@ -303,47 +303,66 @@ __global__ void probe_kernel(const double* __restrict__ Q, int32_t d, const doub
 }
 
 // Exact scan of the probed lists with a (d2, row) top-k in shared memory.  Rounds of
-// R rows: warps compute fp64 distances (warp per row), rows beating the current k-th
-// key are staged, and a bitonic merge of [top | stage] keeps the k smallest.
-__global__ void scan_kernel(const float* __restrict__ xs, const double* __restrict__ xns,
-                            const int64_t* __restrict__ rows, const int64_t* __restrict__ off, int32_t d,
-                            const double* __restrict__ Q, const int32_t* __restrict__ probe, int32_t n_probe,
-                            int32_t k, int32_t Kp, int64_t* __restrict__ idx_out, double* __restrict__ d2_out,
-                            int32_t* __restrict__ cnt_out) {
+// S rows: G lanes per row (float4 loads, fp64 FMA, G-lane shuffle reduction), rows
+// beating the current k-th key are staged, and a bitonic merge of [top | stage]
+// keeps the k smallest.  d2 = ((x.y) * -2 + |x|^2) + |y|^2 clamped at 0.
+template <int G>
+__global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs, const double* __restrict__ xns,
+                                                   const int64_t* __restrict__ rows, const int64_t* __restrict__ off,
+                                                   int32_t d, const double* __restrict__ Q,
+                                                   const int32_t* __restrict__ probe, int32_t n_probe, int32_t k,
+                                                   int32_t Kp, int32_t S, int32_t B, int64_t* __restrict__ idx_out,
+                                                   double* __restrict__ d2_out, int32_t* __restrict__ cnt_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K128* top = reinterpret_cast<K128*>(smem_raw);  // [2 Kp]: sorted top Kp, then the stage
-  double* y = reinterpret_cast<double*>(top + 2 * Kp);
+  K128* top = reinterpret_cast<K128*>(smem_raw);  // [B]: sorted top Kp, then the stage of S
+  double* y = reinterpret_cast<double*>(top + B);
   __shared__ int s_cnt;
   __shared__ double s_yy;
+  constexpr int RPW = 32 / G;  // rows per warp step
   const int64_t q = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int grp = lane / G, gl = lane % G;
   for (int j = threadIdx.x; j < d; j += blockDim.x) y[j] = Q[q * d + j];
-  for (int i = threadIdx.x; i < 2 * Kp; i += blockDim.x) top[i] = K128{~0ull, ~0ull};
+  for (int i = threadIdx.x; i < B; i += blockDim.x) top[i] = K128{~0ull, ~0ull};
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   if (warp == 0) {
-    double s = 0.0;
-    for (int j = lane; j < d; j += 32) s = fma(y[j], y[j], s);
-    s = warp_sum(s);
-    if (lane == 0) s_yy = s;
+    double sy = 0.0;
+    for (int j = lane; j < d; j += 32) sy = fma(y[j], y[j], sy);
+    sy = warp_sum(sy);
+    if (lane == 0) s_yy = sy;
   }
   __syncthreads();
   const double yy = s_yy;
+  const bool vec = (d & 3) == 0;
   int64_t total = 0;
-  const int R = min(Kp, 256);
   for (int p = 0; p < n_probe; ++p) {
     const int c = probe[q * n_probe + p];
     const int64_t b = off[c], e = off[c + 1];
     total += e - b;
-    for (int64_t r0 = b; r0 < e; r0 += R) {
+    for (int64_t r0 = b; r0 < e; r0 += S) {
       const K128 tau = top[Kp - 1];
-      const int64_t r1 = min(e, r0 + R);
-      for (int64_t pos = r0 + warp; pos < r1; pos += nw) {
-        const float* x = xs + pos * d;
+      const int64_t r1 = min(e, r0 + S);
+      for (int64_t base = r0 + int64_t(warp) * RPW; base < r1; base += int64_t(nw) * RPW) {
+        const int64_t pos = base + grp;
+        const bool ok = pos < r1;
+        const float* x = xs + (ok ? pos : b) * d;
         double s = 0.0;
-        for (int j = lane; j < d; j += 32) s = fma(double(x[j]), y[j], s);
-        s = warp_sum(s);
-        if (lane == 0) {
+        if (vec) {
+          const float4* x4 = reinterpret_cast<const float4*>(x);
+          for (int j4 = gl; j4 < (d >> 2); j4 += G) {
+            const float4 v = __ldg(x4 + j4);
+            s = fma(double(v.x), y[4 * j4 + 0], s);
+            s = fma(double(v.y), y[4 * j4 + 1], s);
+            s = fma(double(v.z), y[4 * j4 + 2], s);
+            s = fma(double(v.w), y[4 * j4 + 3], s);
+          }
+        } else {
+          for (int j = gl; j < d; j += G) s = fma(double(__ldg(x + j)), y[j], s);
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (ok && gl == 0) {
           double t = s * -2.0;
           t += xns[pos];
           t += yy;
@@ -355,8 +374,8 @@ __global__ void scan_kernel(const float* __restrict__ xs, const double* __restri
       }
       __syncthreads();
       if (s_cnt > 0) {
-        bitonic(top, 2 * Kp);
-        for (int i = Kp + threadIdx.x; i < 2 * Kp; i += blockDim.x) top[i] = K128{~0ull, ~0ull};
+        bitonic(top, B);
+        for (int i = Kp + threadIdx.x; i < B; i += blockDim.x) top[i] = K128{~0ull, ~0ull};
         if (threadIdx.x == 0) s_cnt = 0;
         __syncthreads();
       }
@@ -607,7 +626,10 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     DK_REQUIRE(probe_smem <= 232448, "n_clusters too large for the GPU probe (max 8192 at d <= 4096)");
     int Kp = 32;
     while (Kp < k) Kp <<= 1;
-    const size_t scan_smem = size_t(2 * Kp) * sizeof(K128) + size_t(v->d) * sizeof(double);
+    const int S = std::max(Kp, 256);  // rows per round (stage capacity)
+    int B = 2;
+    while (B < Kp + S) B <<= 1;
+    const size_t scan_smem = size_t(B) * sizeof(K128) + size_t(v->d) * sizeof(double);
     DK_REQUIRE(scan_smem <= 232000, "k or d too large for the IVF scan");
     // staging: queries, probe lists, outputs
     size_t off = 0;
@@ -637,9 +659,21 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     int64_t* io = idev ? idx_out : reinterpret_cast<int64_t*>(base + o_i);
     double* dd = ddev ? d2_out : reinterpret_cast<double*>(base + o_d);
     int32_t* co = cdev ? cnt_out : reinterpret_cast<int32_t*>(base + o_c);
-    set_dynamic_smem(scan_kernel, scan_smem);
-    scan_kernel<<<unsigned(nq), 256, scan_smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, Qd, probe, n_probe,
-                                                    k, Kp, io, dd, co);
+    // lanes per row: enough that one float4 sweep covers about half of a row's 16-byte chunks
+    const int chunks = (v->d + 3) / 4;
+#define DK_SCAN(G)                                                                                           \
+  do {                                                                                                       \
+    set_dynamic_smem(scan_kernel<G>, scan_smem);                                                             \
+    scan_kernel<G><<<unsigned(nq), 256, scan_smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, Qd, probe, \
+                                                       n_probe, k, Kp, S, B, io, dd, co);                    \
+  } while (0)
+    if (chunks >= 64) DK_SCAN(32);
+    else if (chunks >= 32) DK_SCAN(16);
+    else if (chunks >= 16) DK_SCAN(8);
+    else if (chunks >= 8) DK_SCAN(4);
+    else if (chunks >= 4) DK_SCAN(2);
+    else DK_SCAN(1);
+#undef DK_SCAN
     DK_CHECK_LAUNCH();
     if (!idev) DK_CUDA(cudaMemcpyAsync(idx_out, io, size_t(nq) * k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     if (!ddev) DK_CUDA(cudaMemcpyAsync(d2_out, dd, size_t(nq) * k * sizeof(double), cudaMemcpyDeviceToHost, s));

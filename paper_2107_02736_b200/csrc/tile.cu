@@ -1,6 +1,11 @@
 // tile.cu — host launcher for the tcgen05 tile sweep (tile_kernel.cuh).
+
 #include <algorithm>
+#include <limits>
+#include <map>
 #include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "internal.h"
 #include "tile_kernel.cuh"
@@ -34,6 +39,45 @@ struct Plan {
   size_t smem;
 };
 
+// Tiles per work unit.  Units (query block, column chunk) are dealt to the persistent CTAs
+// round-robin, so the sweep ends when the most loaded CTA does: pick, among 12-48 units
+// per CTA, the chunk length whose exact makespan (in tiles, the ragged last chunk
+// included) is smallest — e.g. c2 (3907 tiles x 79 query blocks on 148 SMs): 130 tiles
+// per unit gives 2210 tiles on the busiest CTA vs an average of 2085; the balanced
+// choice is within ~1%.  Ties go to the longer chunk (fewer partial sums).  Cached.
+int64_t balanced_tiles_per_unit(int ntiles, int ngroups, int nslots) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, int64_t> cache;
+  const auto key = std::make_tuple(ntiles, ngroups, nslots);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const int64_t total = int64_t(ntiles) * ngroups;
+  int64_t lo = std::max<int64_t>(1, total / (int64_t(nslots) * 48));
+  int64_t hi = std::max<int64_t>(1, total / (int64_t(nslots) * 12));
+  hi = std::min<int64_t>(hi, ntiles);
+  lo = std::min(lo, hi);
+  int64_t best = hi, best_span = std::numeric_limits<int64_t>::max();
+  std::vector<int64_t> load(static_cast<size_t>(nslots));
+  for (int64_t tpu = hi; tpu >= lo; --tpu) {
+    const int64_t ncc = (ntiles + tpu - 1) / tpu;
+    const int64_t last = ntiles - (ncc - 1) * tpu;
+    const int64_t units = int64_t(ngroups) * ncc;
+    std::fill(load.begin(), load.end(), 0);
+    for (int64_t u = 0; u < units; ++u) load[size_t(u % nslots)] += (u / ngroups == ncc - 1) ? last : tpu;
+    const int64_t span = *std::max_element(load.begin(), load.end());
+    if (span < best_span) {
+      best_span = span;
+      best = tpu;
+    }
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = best;
+  return best;
+}
+
 Plan make_plan(int kblocks, int ntiles, int ngroups, int nslots, int mode, bool pair) {
   Plan pl{};
   // keep the query block resident when it fits next to a >=3-stage ring
@@ -48,10 +92,7 @@ Plan make_plan(int kblocks, int ntiles, int ngroups, int nslots, int mode, bool 
     while (st < 6 && tile_smem_bytes(kblocks, 0, st + 1, mode, pair) <= kMaxSmem) ++st;
     pl.stages = st;
   }
-  // ~16+ units per CTA (pair) for balance; at least 1 tile per unit
-  const int64_t total_tiles = int64_t(ntiles) * ngroups;
-  int64_t tpu = total_tiles / (int64_t(nslots) * 16);
-  tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, ntiles));
+  const int64_t tpu = balanced_tiles_per_unit(ntiles, ngroups, nslots);
   pl.tiles_per_unit = int(tpu);
   pl.ncc = int((ntiles + tpu - 1) / tpu);
   pl.smem = tile_smem_bytes(kblocks, pl.a_resident, pl.stages, mode, pair);
