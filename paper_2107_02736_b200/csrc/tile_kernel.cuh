@@ -218,9 +218,19 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
         }
         mn = fminf(mn, fminf(fminf(m0, m1), fminf(m2_, m3)));
       } else {
-        uint32_t hits = 0;
+        // candidates are rare (~1e-4 of the pairs): a min tree (4 independent chains)
+        // rejects the whole chunk before any per-column mask is built
+        float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[2], m3 = d2v[3];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) hits |= (d2v[j] <= tau ? 1u : 0u) << j;
+        for (int j = 4; j < 32; j += 4) {
+          m0 = fminf(m0, d2v[j]); m1 = fminf(m1, d2v[j + 1]);
+          m2_ = fminf(m2_, d2v[j + 2]); m3 = fminf(m3, d2v[j + 3]);
+        }
+        uint32_t hits = 0;
+        if (fminf(fminf(m0, m1), fminf(m2_, m3)) <= tau) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) hits |= (d2v[j] <= tau ? 1u : 0u) << j;
+        }
         while (hits) {  // rare: appended candidates
           const int j = __ffs(hits) - 1;
           hits &= hits - 1;

@@ -34,18 +34,31 @@ def child(config, op, reps, out_path):
     spec = g.KernelSpec(fam, h)
     Qd = torch.from_numpy(np.ascontiguousarray(W.Q)).cuda()
     out = torch.empty(W.Q.shape[0], dtype=torch.float64, device="cuda")
+    if op == "knn":
+        from paper_2107_02736_b200 import _lib
+
+        k = 100
+        idx = torch.empty((len(W.Q), k), dtype=torch.int64, device="cuda")
+        d2 = torch.empty((len(W.Q), k), dtype=torch.float64, device="cuda")
+
+        def call():
+            _lib.check(_lib.load().dk_knn(ds.handle, Qd.data_ptr(), len(W.Q), k, idx.data_ptr(), d2.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream))
+    else:
+        def call():
+            g.naive_kde_into(ds, spec, Qd, out)
     for _ in range(3):
-        g.naive_kde_into(ds, spec, Qd, out)
+        call()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        g.naive_kde_into(ds, spec, Qd, out)
+        call()
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
-    np.save(out_path, out.cpu().numpy())
+    np.save(out_path, (d2 if op == "knn" else out).cpu().numpy().ravel())
     print(json.dumps({"ms": sorted(ts)[len(ts) // 2], "min": min(ts)}))
 
 
