@@ -27,14 +27,26 @@ def child(config, op, reps, out_path):
 
     man = json.load(open(os.path.join(ROOT, "tests", "golden", "bandwidths.json")))
     W = workloads.make(config)
-    fam = {"naive-exp": "exponential", "naive-lap": "laplacian"}.get(op, W.family)
+    fam = {"naive-exp": "exponential", "naive-lap": "laplacian", "deann-exp": "exponential",
+           "deann-lap": "laplacian"}.get(op, W.family)
     key = f"{config}-laplacian" if fam == "laplacian" else config
     h = man[key]["h"] if fam == "laplacian" or W.h is None else W.h
     ds = g.Dataset.from_array(W.X)
     spec = g.KernelSpec(fam, h)
     Qd = torch.from_numpy(np.ascontiguousarray(W.Q)).cuda()
     out = torch.empty(W.Q.shape[0], dtype=torch.float64, device="cuda")
-    if op == "knn":
+    if op.startswith("deann"):
+        k, m = (50, 500) if config == "c4" else (100, 1000)
+        vals = torch.empty(len(W.Q), dtype=torch.float64, device="cuda")
+        fam_code = _lib_family = {"gaussian": 0, "exponential": 1, "laplacian": 2}[fam]
+
+        def call():
+            from paper_2107_02736_b200 import _lib
+            _lib.check(_lib.load().dk_deann(ds.handle, Qd.data_ptr(), len(W.Q), fam_code, h, k, m, 12345, 0,
+                                            vals.data_ptr(), None, None, None,
+                                            torch.cuda.current_stream().cuda_stream))
+        out = vals
+    elif op == "knn":
         from paper_2107_02736_b200 import _lib
 
         k = 100
