@@ -114,7 +114,41 @@ __device__ __forceinline__ double group_row_kernel(const float* __restrict__ x, 
   return exp(-acc * c);
 }
 
-template <int G>
+// Kernel value of one row from float4s already in registers (IT per lane, same
+// accumulation order as group_row_kernel: lane gl takes chunks gl, gl+G, ...).
+template <int G, int IT>
+__device__ __forceinline__ double group_row_regs(const float4 (&xv)[IT], const double* __restrict__ q, int chunks,
+                                                 int family, double c, int gl) {
+  double acc = 0.0;
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int k4 = gl + it * G;
+    if (k4 < chunks) {
+      const float4 v = xv[it];
+      const double t0 = double(v.x) - q[4 * k4 + 0], t1 = double(v.y) - q[4 * k4 + 1];
+      const double t2 = double(v.z) - q[4 * k4 + 2], t3 = double(v.w) - q[4 * k4 + 3];
+      if (family == DK_LAPLACIAN) acc += (fabs(t0) + fabs(t1)) + (fabs(t2) + fabs(t3));
+      else { acc = fma(t0, t0, acc); acc = fma(t1, t1, acc); acc = fma(t2, t2, acc); acc = fma(t3, t3, acc); }
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (family == DK_EXPONENTIAL) acc = sqrt(acc);
+  return exp(-acc * c);
+}
+
+template <int G, int IT>
+__device__ __forceinline__ void load_row(const float* __restrict__ x, bool valid, int chunks, int gl,
+                                         float4 (&b)[IT]) {
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int k4 = gl + it * G;
+    b[it] = (valid && k4 < chunks) ? __ldg(x4 + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <int G, int IT>
 __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int64_t global_offset, int64_t N,
                               int32_t d, const double* __restrict__ Q, int64_t nq, int32_t family, double c,
                               int32_t m, uint64_t seed, int64_t query_base, const int64_t* __restrict__ excl,
@@ -153,13 +187,33 @@ __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int6
     const uint32_t took = __ballot_sync(0xffffffffu, take);
     const int ntook = __popc(took);
     __syncwarp();
-    for (int r0 = 0; r0 < ntook; r0 += R) {
-      const int r = r0 + grp;
-      const int64_t loc = r < ntook ? rows_s[r] - global_offset : -1;
-      const bool mine = loc >= 0 && loc < n_local;
-      // groups with no row still take part in the shuffles (G-lane reduction is warp-synchronous)
-      const double v = group_row_kernel<G>(X + size_t(mine ? loc : 0) * d, q, d, family, c, gl);
-      if (mine && gl == 0) zsum += v;
+    if constexpr (IT > 0) {
+      // software-pipelined: the next row's float4s are in flight while this one is reduced
+      const int chunks = d >> 2;
+      float4 cur[IT], nxt[IT];
+      int64_t loc = grp < ntook ? rows_s[grp] - global_offset : -1;
+      bool mine = loc >= 0 && loc < n_local;
+      load_row<G, IT>(X + size_t(mine ? loc : 0) * d, mine, chunks, gl, cur);
+      for (int r0 = 0; r0 < ntook; r0 += R) {
+        const int rn = r0 + R + grp;
+        const int64_t locn = rn < ntook ? rows_s[rn] - global_offset : -1;
+        const bool minen = locn >= 0 && locn < n_local;
+        if (r0 + R < ntook) load_row<G, IT>(X + size_t(minen ? locn : 0) * d, minen, chunks, gl, nxt);
+        const double v = group_row_regs<G, IT>(cur, q, chunks, family, c, gl);
+        if (mine && gl == 0) zsum += v;
+#pragma unroll
+        for (int it = 0; it < IT; ++it) cur[it] = nxt[it];
+        mine = minen;
+      }
+    } else {
+      for (int r0 = 0; r0 < ntook; r0 += R) {
+        const int r = r0 + grp;
+        const int64_t loc = r < ntook ? rows_s[r] - global_offset : -1;
+        const bool mine = loc >= 0 && loc < n_local;
+        // groups with no row still take part in the shuffles (G-lane reduction is warp-synchronous)
+        const double v = group_row_kernel<G>(X + size_t(mine ? loc : 0) * d, q, d, family, c, gl);
+        if (mine && gl == 0) zsum += v;
+      }
     }
     __syncwarp();
     if (took) last_t = int64_t(t_base) + 31 - __clz(took);
@@ -269,19 +323,30 @@ void launch_sample(const float* X, int64_t n_local, int64_t global_offset, int64
   const unsigned grid = unsigned((nq + wpb - 1) / wpb);
   // lanes per row: enough that one float4 sweep of the row covers >= ~1/2 of its 16 B chunks
   const int chunks = (d + 3) / 4;
-#define DK_SAMPLE_LAUNCH(G)                                                                                   \
+#define DK_SAMPLE_LAUNCH(G, IT)                                                                               \
   do {                                                                                                        \
-    set_dynamic_smem(sample_kernel<G>, smem);                                                                 \
-    sample_kernel<G><<<grid, wpb * 32, smem, s>>>(X, n_local, global_offset, global_n, d, Q, nq, family, c, m, \
-                                                  seed, query_base, excl_sorted, excl_cnt, excl_stride, z_sum,  \
-                                                  acc_idx, draws);                                            \
+    set_dynamic_smem(sample_kernel<G, IT>, smem);                                                             \
+    sample_kernel<G, IT><<<grid, wpb * 32, smem, s>>>(X, n_local, global_offset, global_n, d, Q, nq, family, c, \
+                                                      m, seed, query_base, excl_sorted, excl_cnt, excl_stride,  \
+                                                      z_sum, acc_idx, draws);                                   \
   } while (0)
-  if (chunks >= 64) DK_SAMPLE_LAUNCH(32);
-  else if (chunks >= 32) DK_SAMPLE_LAUNCH(16);
-  else if (chunks >= 16) DK_SAMPLE_LAUNCH(8);
-  else if (chunks >= 8) DK_SAMPLE_LAUNCH(4);
-  else if (chunks >= 4) DK_SAMPLE_LAUNCH(2);
-  else DK_SAMPLE_LAUNCH(1);
+  // pipelined row loads when rows are whole float4s and G < 32 (a row is at most 4 float4s
+  // per lane).  For wide rows (G = 32) the double buffer costs more occupancy than it hides
+  // latency (c4, d = 784: 8.5 -> 9.1 ms), so those keep the plain loop.
+  const bool vec = (d & 3) == 0;
+  if (chunks >= 64) {
+    DK_SAMPLE_LAUNCH(32, 0);
+  } else if (chunks >= 32) {
+    if (vec) DK_SAMPLE_LAUNCH(16, 4); else DK_SAMPLE_LAUNCH(16, 0);
+  } else if (chunks >= 16) {
+    if (vec) DK_SAMPLE_LAUNCH(8, 4); else DK_SAMPLE_LAUNCH(8, 0);
+  } else if (chunks >= 8) {
+    if (vec) DK_SAMPLE_LAUNCH(4, 4); else DK_SAMPLE_LAUNCH(4, 0);
+  } else if (chunks >= 4) {
+    if (vec) DK_SAMPLE_LAUNCH(2, 4); else DK_SAMPLE_LAUNCH(2, 0);
+  } else {
+    if (vec) DK_SAMPLE_LAUNCH(1, 4); else DK_SAMPLE_LAUNCH(1, 0);
+  }
 #undef DK_SAMPLE_LAUNCH
   DK_CHECK_LAUNCH();
 }
