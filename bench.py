@@ -35,6 +35,18 @@ sys.path.insert(0, HERE)
 METRIC = "KDE queries/sec (exact naive KDE, gaussian) at n=1M, d=128"
 UNIT = "queries/s"
 WORKLOAD = "c2: exact naive gaussian KDE, n=1,000,000 x d=128 integer rows, 10,000 queries, h by median-1e-3 rule"
+# --workload c5: the north star's scale-out config (BASELINE configs[4]), exact KDE part
+WORKLOADS = {
+    "c2": {"metric": METRIC, "desc": WORKLOAD, "dtype": "fp16-exact-int (fp32 accumulate, fp64 row sums)",
+           "l2": "inputs larger than L2 (256 MB fp16 operand + 512 MB fp32 rows > 126 MB)",
+           "traffic": "c2_kde_gauss"},
+    "c5": {"metric": "KDE queries/sec (exact naive KDE, gaussian) at n=8M, d=96",
+           "desc": "c5: exact naive gaussian KDE, n=8,000,000 x d=96 mixture rows (Dirichlet weights), "
+                   "100,000 queries, h by median-1e-3 rule",
+           "dtype": "fp16 split3 (fp32 accumulate, fp64 row sums)",
+           "l2": "inputs larger than L2 (5.1 GB split3 operand + 3.07 GB fp32 rows > 126 MB)",
+           "traffic": None},
+}
 
 
 def _peaks():
@@ -177,7 +189,8 @@ def run_reference(args):
     import workloads
     from oracle import deann_oracle as O
 
-    W = workloads.make("c2")
+    WL = WORKLOADS[args.workload]
+    W = workloads.make(args.workload)
     h = _bandwidth_cpu_free(W)
     data = O.Data(W.X)
     cores = len(os.sched_getaffinity(0))
@@ -198,12 +211,12 @@ def run_reference(args):
     total = sum(times)
     value = per_step * args.steps / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "impl": "reference", "metric": WL["metric"], "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "bandwidth": h, "sample_queries_per_step": per_step},
+        "config": {"workload": WL["desc"], "bandwidth": h, "sample_queries_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} random queries of the 10,000 per step, full n=1,000,000 rows, "
+                         "sample": f"{per_step} random queries of the {len(W.Q):,} per step, full n={W.X.shape[0]:,} rows, "
                                    "oracle/deann_oracle.naive_kde (NumPy/OpenBLAS fp64, all host threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -237,14 +250,15 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    W = workloads.make("c2")
+    WL = WORKLOADS[args.workload]
+    W = workloads.make(args.workload)
     n, d = W.X.shape
     nq = W.Q.shape[0]
     lo, hi = (rank * n) // ws, ((rank + 1) * n) // ws
     t_fit = time.perf_counter()
     ds = g.Dataset.from_array(W.X[lo:hi], device=local, global_offset=lo, global_n=n)
     t_fit = time.perf_counter() - t_fit
-    if ws == 1:
+    if ws == 1 and args.workload == "c2":
         h = g.fit_bandwidth(ds, W.pilot, "gaussian", 1e-3)
     else:
         h = _bandwidth_cpu_free(W)
@@ -340,14 +354,14 @@ def run_ours(args):
     tpath = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("c2_kde_gauss", {}).get("dram_bytes_per_launch")
+            traffic = json.load(f).get(WL["traffic"] or "", {}).get("dram_bytes_per_launch")
     line = {
-        "metric": METRIC, "value": nq / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": WL["metric"], "value": nq / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "fp16-exact-int (fp32 accumulate, fp64 row sums)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "bandwidth": h, "parallelism": f"dataset-sharded x{ws}" if ws > 1 else "1 GPU",
-                   "l2": "inputs larger than L2 (256 MB fp16 operand + 512 MB fp32 rows > 126 MB)",
-                   "fit_seconds": t_fit},
+        "vs_baseline": None, "dtype": WL["dtype"], "data": "synthetic",
+        "config": {"workload": WL["desc"], "bandwidth": h,
+                   "parallelism": f"dataset-sharded x{ws}" if ws > 1 else "1 GPU",
+                   "l2": WL["l2"], "fit_seconds": t_fit},
         "roofline": {
             "bound": "tensor", "achieved": flops / t_k / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": (flops / t_k) / tc_peak, "traffic": traffic, "peak_source": peaks["source"],
@@ -362,12 +376,12 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if ws == 1 and not args.no_secondary:
+    if ws == 1 and not args.no_secondary and args.workload == "c2":
         line["secondary"] = measure_deann_c3(args, local)
     if ws == 1 and not args.no_cpu_baseline:
         rate, cores, done, el, odata = cpu_oracle_rate(W.X, W.Q, h)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"first {done} of the 10,000 queries over all n=1,000,000 rows "
+                                "sample": f"first {done} of the {nq:,} queries over all n={n:,} rows "
                                           f"({el:.1f} s), oracle/deann_oracle.naive_kde, NumPy/OpenBLAS fp64"}
         # parity of the timed device output against the oracle on a query sample
         from oracle import deann_oracle as O
@@ -455,6 +469,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2",
+                    help="c2 (default; BASELINE configs[1], the metric's config) or c5 (scale-out config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the c3 DEANN secondary measurement")
     ap.add_argument("--fit-bandwidth", action="store_true", help="(re)write tests/golden/bandwidths.json")
