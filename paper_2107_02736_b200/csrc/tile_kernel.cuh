@@ -119,8 +119,10 @@ constexpr uint32_t kPolyPairs = DK_POLY_PAIRS;
 
 // 2^t for a pair, t <= 0, on the FMA pipe: t = j + f (j = round(t), |f| <= 1/2),
 // 2^f by a degree-5 polynomial (relative error < 2.4e-7 on |f| <= 1/2, i.e. at the
-// level of ex2.approx), exponent j added to the float bits.  t is clamped at -126
-// (ex2.approx.ftz flushes below 2^-126 as well).
+// level of ex2.approx), exponent j added to the float bits.  t is clamped at -126, so a
+// term below fp32's normal range contributes 2^-126 instead of ex2.approx.ftz's 0: at
+// most 2/16 x 2^-126 = 1.5e-39 on a mean, far below the parity floor (1e-16).  Selecting
+// 0 there costs 4 instructions per 32 columns, 3.5% of the c2 sweep (issue-bound).
 __device__ __forceinline__ float2 exp2_poly2(float2 t) {
   t.x = fmaxf(t.x, -126.f);
   t.y = fmaxf(t.y, -126.f);

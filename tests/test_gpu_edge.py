@@ -1,0 +1,139 @@
+"""Edge cases across the GPU paths: odd widths (rows not whole float4s), single rows,
+query-padding boundaries, underflowing and saturating bandwidths, far queries.
+
+Every value is checked against the oracle restatement of the reference
+(oracle/deann_oracle.py), with the same tolerances as the parity tests:
+exact KDE 1e-5 relative (gate 1e-4), k-NN identical, RS/DEANN 1e-12 relative
+given the same neighbour and sample indices.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2107_02736_b200 as g
+from dk_testutil import FAMILIES
+from oracle import deann_oracle as O
+from oracle.philox import IndexReplay, NeighborReplay
+
+pytestmark = pytest.mark.gpu
+
+KDE_RTOL = 1e-5
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+def _h(fam, d):
+    return 2 * d ** 0.75 if fam == "laplacian" else math.sqrt(d)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 7, 13, 33])
+def test_odd_widths_all_paths(d):
+    rng = np.random.default_rng(100 + d)
+    n = 3000
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    Q = rng.normal(size=(9, d))
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    for fam in FAMILIES:
+        h = _h(fam, d)
+        got = g.naive_kde(ds, g.KernelSpec(fam, h), Q).values
+        assert _rel(got, O.naive_kde(od, fam, h, Q)) < KDE_RTOL, (fam, d)
+    k, m, seed = 20, 150, 31
+    idx, d2 = g.knn_batch(ds, Q, k)
+    for fam in FAMILIES:
+        h = _h(fam, d)
+        vals, nbr, _ = g.deann_arrays(ds, g.KernelSpec(fam, h), Q, k, m, seed=seed, export_neighbors=True)
+        for j in range(len(Q)):
+            ri, rd = O.brute_force_knn(od, Q[j], k)
+            np.testing.assert_array_equal(nbr[j], ri)
+            ref = O.deann(od, fam, h, NeighborReplay(ri, rd), Q[j], k, m, rng=IndexReplay(seed, j, n))[0]
+            assert vals[j] == pytest.approx(ref, rel=1e-12), (fam, d, j)
+    # permuted sampler and IVF on the same odd width
+    st = g.RspState.from_dataset(ds, 3)
+    ost = O.Permuted(od, 3)
+    for j in range(3):
+        assert g.rsp_kde(st, g.KernelSpec("gaussian", _h("gaussian", d)), Q[j], 200).value == pytest.approx(
+            O.rsp_kde(ost, "gaussian", _h("gaussian", d), Q[j], 200), rel=1e-12)
+    index = g.ivf_build(ds, 8, seed=d)
+    cent, lists = O.ivf_build(od, 8, d)
+    for j in range(3):
+        ri, _ = O.ivf_query(od, cent, lists, Q[j], 10, 3)
+        np.testing.assert_array_equal(g.ivf_query(index, ds, Q[j], 10, 3).indices, ri)
+
+
+def test_single_row_dataset():
+    X = np.array([[0.5, -1.0, 2.0]], dtype=np.float32)
+    q = np.array([0.0, 0.0, 1.0])
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    for fam in FAMILIES:
+        assert g.naive_kde(ds, g.KernelSpec(fam, 1.3), q.reshape(1, -1)).values[0] == pytest.approx(
+            O.naive_kde(od, fam, 1.3, q.reshape(1, -1))[0], rel=KDE_RTOL)
+    nl = g.brute_force_knn(ds, q, 1)
+    assert nl.indices.tolist() == [0]
+    est = g.deann(ds, g.KernelSpec("gaussian", 1.3), g.BruteForceIndex(ds), q, 1, 0)
+    assert est.value == pytest.approx(O.naive_kde(od, "gaussian", 1.3, q.reshape(1, -1))[0], rel=1e-12)
+    assert est.kernel_evals == 1 and not est.truncated
+
+
+@pytest.mark.parametrize("nq", [1, 127, 128, 129, 255, 256, 257, 1023])
+def test_query_padding_boundaries(nq):
+    rng = np.random.default_rng(nq)
+    X = rng.normal(size=(2000, 24)).astype(np.float32)
+    Q = rng.normal(size=(nq, 24))
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", 4.0), Q).values
+    ref = O.naive_kde(od, "gaussian", 4.0, Q)
+    assert _rel(got, ref) < KDE_RTOL
+    idx, _ = g.knn_batch(ds, Q, 5)
+    for j in range(0, nq, max(1, nq // 7)):
+        np.testing.assert_array_equal(idx[j], O.brute_force_knn(od, Q[j], 5)[0])
+
+
+def test_underflow_and_saturation():
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(1500, 6)).astype(np.float32)
+    Q = rng.normal(size=(10, 6)) + 50.0     # far from every row
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    for fam in FAMILIES:
+        # tiny bandwidth, far queries: every kernel value underflows (exactly 0 in fp64); the
+        # fp32 epilogue is exact 0 on MUFU and <= 2^-126 per polynomial term (tile_kernel.cuh),
+        # both far below the parity floor of 1e-16
+        got = g.naive_kde(ds, g.KernelSpec(fam, 0.05), Q).values
+        ref = O.naive_kde(od, fam, 0.05, Q)
+        assert np.all(ref == 0.0) and np.all(got >= 0.0) and np.all(got < 1e-37), fam
+        # huge bandwidth: every kernel value ~1
+        got = g.naive_kde(ds, g.KernelSpec(fam, 1e6), Q - 50.0).values
+        ref = O.naive_kde(od, fam, 1e6, Q - 50.0)
+        assert _rel(got, ref) < KDE_RTOL, fam
+
+
+def test_large_magnitude_rows_split_encoding():
+    # offsets and spreads in the thousands: the split encoding's centring/scaling
+    rng = np.random.default_rng(6)
+    X = (rng.normal(size=(4000, 40)) * 30 + 5000).astype(np.float32)
+    Q = rng.normal(size=(16, 40)) * 30 + 5000
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    for fam in ("gaussian", "exponential"):
+        h = 150.0 if fam == "gaussian" else 80.0
+        got = g.naive_kde(ds, g.KernelSpec(fam, h), Q).values
+        assert _rel(got, O.naive_kde(od, fam, h, Q)) < KDE_RTOL, fam
+
+
+def test_integer_dataset_with_fractional_queries_and_duplicates():
+    rng = np.random.default_rng(7)
+    X = rng.integers(0, 4, size=(3000, 10)).astype(np.float32)   # exact-mode rows, many duplicates
+    Q = rng.integers(0, 4, size=(12, 10)).astype(np.float64)
+    Q[6:] += 0.25                                                  # fractional half: split encoding
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    assert ds.exact_mode
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", 1.5), Q).values
+    assert _rel(got, O.naive_kde(od, "gaussian", 1.5, Q)) < KDE_RTOL
+    idx, _ = g.knn_batch(ds, Q, 40)
+    for j in range(len(Q)):
+        np.testing.assert_array_equal(idx[j], O.brute_force_knn(od, Q[j], 40)[0])
