@@ -306,10 +306,11 @@ __global__ void probe_kernel(const double* __restrict__ Q, int32_t d, const doub
 // S rows: G lanes per row (float4 loads, fp64 FMA, G-lane shuffle reduction), rows
 // beating the current k-th key are staged, and a bitonic merge of [top | stage]
 // keeps the k smallest.  d2 = ((x.y) * -2 + |x|^2) + |y|^2 clamped at 0.
-template <int G>
+template <int G, int IT>
 __global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs, const double* __restrict__ xns,
                                                    const int64_t* __restrict__ rows, const int64_t* __restrict__ off,
-                                                   int32_t d, const double* __restrict__ Q,
+                                                   int32_t d, const int32_t* __restrict__ order,
+                                                   const double* __restrict__ Q,
                                                    const int32_t* __restrict__ probe, int32_t n_probe, int32_t k,
                                                    int32_t Kp, int32_t S, int32_t B, int64_t* __restrict__ idx_out,
                                                    double* __restrict__ d2_out, int32_t* __restrict__ cnt_out) {
@@ -319,7 +320,9 @@ __global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs,
   __shared__ int s_cnt;
   __shared__ double s_yy;
   constexpr int RPW = 32 / G;  // rows per warp step
-  const int64_t q = blockIdx.x;
+  // blocks take the queries grouped by their nearest list, so concurrently running blocks
+  // stream the same lists through L2
+  const int64_t q = order ? order[blockIdx.x] : blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int grp = lane / G, gl = lane % G;
   for (int j = threadIdx.x; j < d; j += blockDim.x) y[j] = Q[q * d + j];
@@ -335,6 +338,16 @@ __global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs,
   __syncthreads();
   const double yy = s_yy;
   const bool vec = (d & 3) == 0;
+  // IT > 0: this lane's slice of the query in registers (no per-row shared-memory reads)
+  double yv[IT > 0 ? IT : 1][4];
+  if constexpr (IT > 0) {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int j4 = gl + it * G;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) yv[it][i] = j4 < (d >> 2) ? y[4 * j4 + i] : 0.0;
+    }
+  }
   int64_t total = 0;
   for (int p = 0; p < n_probe; ++p) {
     const int c = probe[q * n_probe + p];
@@ -348,7 +361,20 @@ __global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs,
         const bool ok = pos < r1;
         const float* x = xs + (ok ? pos : b) * d;
         double s = 0.0;
-        if (vec) {
+        if constexpr (IT > 0) {
+          const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll
+          for (int it = 0; it < IT; ++it) {
+            const int j4 = gl + it * G;
+            if (j4 < (d >> 2)) {
+              const float4 v = __ldg(x4 + j4);
+              s = fma(double(v.x), yv[it][0], s);
+              s = fma(double(v.y), yv[it][1], s);
+              s = fma(double(v.z), yv[it][2], s);
+              s = fma(double(v.w), yv[it][3], s);
+            }
+          }
+        } else if (vec) {
           const float4* x4 = reinterpret_cast<const float4*>(x);
           for (int j4 = gl; j4 < (d >> 2); j4 += G) {
             const float4 v = __ldg(x4 + j4);
@@ -389,6 +415,14 @@ __global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs,
                            : __longlong_as_double(0x7ff0000000000000ll);
   }
   if (threadIdx.x == 0) cnt_out[q] = cnt;
+}
+
+__global__ void first_probe_kernel(const int32_t* __restrict__ probe, int64_t nq, int32_t n_probe,
+                                   int32_t* __restrict__ key, int32_t* __restrict__ val) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  key[q] = probe[q * n_probe];
+  val[q] = int32_t(q);
 }
 
 size_t cub_bytes(int64_t n) {
@@ -643,6 +677,13 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     const size_t o_i = take(size_t(nq) * k * sizeof(int64_t));
     const size_t o_d = take(size_t(nq) * k * sizeof(double));
     const size_t o_c = take(size_t(nq) * sizeof(int32_t));
+    DK_REQUIRE(nq < (int64_t(1) << 31), "too many queries in one IVF call");
+    size_t ord_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, ord_bytes, static_cast<const int32_t*>(nullptr),
+                                    static_cast<int32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+                                    static_cast<int32_t*>(nullptr), int(nq));
+    const size_t o_k0 = take(size_t(nq) * 4), o_k1 = take(size_t(nq) * 4), o_v0 = take(size_t(nq) * 4);
+    const size_t o_ord = take(size_t(nq) * 4), o_ot = take(ord_bytes + 256);
     h->ws.reserve(off);
     uint8_t* base = h->ws.base;
     const double* Qd = Q;
@@ -661,18 +702,33 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     int32_t* co = cdev ? cnt_out : reinterpret_cast<int32_t*>(base + o_c);
     // lanes per row: enough that one float4 sweep covers about half of a row's 16-byte chunks
     const int chunks = (v->d + 3) / 4;
-#define DK_SCAN(G)                                                                                           \
+    // query order: sorted by nearest probed list (L2 reuse across concurrently running blocks)
+    int32_t* order = reinterpret_cast<int32_t*>(base + o_ord);
+    {
+      auto* kin = reinterpret_cast<int32_t*>(base + o_k0);
+      auto* kout = reinterpret_cast<int32_t*>(base + o_k1);
+      auto* vin = reinterpret_cast<int32_t*>(base + o_v0);
+      first_probe_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(probe, nq, n_probe, kin, vin);
+      DK_CHECK_LAUNCH();
+      int bits = 1;
+      while ((int64_t(1) << bits) < int64_t(v->C)) ++bits;
+      size_t tb = ord_bytes;
+      DK_CUDA(cub::DeviceRadixSort::SortPairs(base + o_ot, tb, kin, kout, vin, order, int(nq), 0, bits, s));
+    }
+    const bool vec = (v->d & 3) == 0;
+#define DK_SCAN(G, IT)                                                                                       \
   do {                                                                                                       \
-    set_dynamic_smem(scan_kernel<G>, scan_smem);                                                             \
-    scan_kernel<G><<<unsigned(nq), 256, scan_smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, Qd, probe, \
-                                                       n_probe, k, Kp, S, B, io, dd, co);                    \
+    set_dynamic_smem(scan_kernel<G, IT>, scan_smem);                                                         \
+    scan_kernel<G, IT><<<unsigned(nq), 256, scan_smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, order, \
+                                                           Qd, probe, n_probe, k, Kp, S, B, io, dd, co);     \
   } while (0)
-    if (chunks >= 64) DK_SCAN(32);
-    else if (chunks >= 32) DK_SCAN(16);
-    else if (chunks >= 16) DK_SCAN(8);
-    else if (chunks >= 8) DK_SCAN(4);
-    else if (chunks >= 4) DK_SCAN(2);
-    else DK_SCAN(1);
+    // register-resident query slices where a row is at most 4 float4 steps per lane (G < 32)
+    if (chunks >= 64) DK_SCAN(32, 0);
+    else if (chunks >= 32) { if (vec) DK_SCAN(16, 4); else DK_SCAN(16, 0); }
+    else if (chunks >= 16) { if (vec) DK_SCAN(8, 4); else DK_SCAN(8, 0); }
+    else if (chunks >= 8) { if (vec) DK_SCAN(4, 4); else DK_SCAN(4, 0); }
+    else if (chunks >= 4) { if (vec) DK_SCAN(2, 4); else DK_SCAN(2, 0); }
+    else { if (vec) DK_SCAN(1, 4); else DK_SCAN(1, 0); }
 #undef DK_SCAN
     DK_CHECK_LAUNCH();
     if (!idev) DK_CUDA(cudaMemcpyAsync(idx_out, io, size_t(nq) * k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
