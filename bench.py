@@ -269,10 +269,11 @@ def run_ours(args):
     lib = _lib.load()
 
     def step():
-        g.naive_kde_into(ds, spec, Qd, out, sums=(ws > 1), stream=stream.cuda_stream)
+        # each shard writes its contribution to the global mean (sum / global n): the all-reduce
+        # (sum) of the shards is the KDE
+        g.naive_kde_into(ds, spec, Qd, out, stream=stream.cuda_stream)
         if ws > 1:
             dist.all_reduce(out)
-            out.mul_(1.0 / n)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
@@ -319,9 +320,9 @@ def run_ours(args):
         if ws == 1:
             return g.naive_kde(ds, spec, Qh).values
         tmp = torch.empty(nq, dtype=torch.float64, device=f"cuda:{local}")
-        g.naive_kde_into(ds, spec, Qh, tmp, sums=True, stream=stream.cuda_stream)
+        g.naive_kde_into(ds, spec, Qh, tmp, stream=stream.cuda_stream)
         dist.all_reduce(tmp)
-        return (tmp / n).cpu().numpy()
+        return tmp.cpu().numpy()
     for _ in range(max(1, args.warmup)):
         e2e_step()
     torch.cuda.synchronize()

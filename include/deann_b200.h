@@ -108,7 +108,9 @@ dk_status dk_sq_norms(dk_handle h, double* out, void* stream);
  * naive_kde (estimators.py:122-149): out[j] = (1/n) sum_i K_h(q_j, x_i), fp64.
  * Gaussian/exponential run the fused tcgen05 distance-tile + exp + row-sum;
  * laplacian runs the CUDA-core L1 kernel.  With DK_OUT_SUM the un-normalised
- * local sum is written (dataset-sharded partials). */
+ * local sum is written; without it the sum is divided by the GLOBAL row count
+ * (global_n of a shard handle, n otherwise), so the shards' outputs all-reduce
+ * (sum) straight to the KDE. */
 dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family,
                    double bandwidth, uint32_t flags, double* out, void* stream);
 

@@ -155,7 +155,7 @@ int choose_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cu
 }
 
 QueryOperand encode_queries(dk_dataset* h, const Encoding& e, const double* Qd, int64_t nq, int32_t nq_pad,
-                            __half* A, float* qn, float* scal, cudaStream_t s) {
+                            __half* A, float* qn, float* scal, cudaStream_t s, uint32_t* check_flags = nullptr) {
   QueryOperand q;
   q.nq = int32_t(nq);
   q.nq_pad = nq_pad;
@@ -163,7 +163,7 @@ QueryOperand encode_queries(dk_dataset* h, const Encoding& e, const double* Qd, 
   q.qn = qn;
   q.m2s = scal;
   launch_encode_queries(Qd, nq, nq_pad, h->d, e.mode, e.mu, e.Kp, e.sx, A, qn, scal,
-                        reinterpret_cast<uint32_t*>(scal + 1), s);
+                        reinterpret_cast<uint32_t*>(scal + 1), s, check_flags);
   q.tmap = make_tmap_2d_f16(A, uint64_t(nq_pad), uint64_t(e.Kp), uint32_t(kBM));
   return q;
 }
@@ -409,6 +409,11 @@ HandlePtr new_handle(int64_t n, int32_t d, const dk_fit_opts* opts) {
   if (const char* pv = std::getenv("DK_PAIR")) set_pair_enabled(std::atoi(pv) != 0);
   DK_REQUIRE(h->precision >= 0 && h->precision <= 2, "unknown precision mode");
   DK_REQUIRE(h->global_offset >= 0 && h->global_offset + n <= h->global_n, "shard outside [0, global_n)");
+  {
+    DeviceGuard g(device);
+    DK_CUDA(cudaHostAlloc(&h->flag_host, sizeof(uint32_t), cudaHostAllocDefault));
+    DK_CUDA(cudaEventCreateWithFlags(&h->flag_event, cudaEventDisableTiming));
+  }
   return h;
 }
 
@@ -676,6 +681,8 @@ dk_status dk_free(dk_handle h) {
     if (h->xn64) cudaFree(h->xn64);
     if (h->mu) cudaFree(h->mu);
     if (h->rsp_inverse) cudaFree(h->rsp_inverse);
+    if (h->flag_host) cudaFreeHost(h->flag_host);
+    if (h->flag_event) cudaEventDestroy(h->flag_event);
     for (auto& pr : h->prof_events) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
@@ -717,7 +724,9 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     LaunchCount lc(h);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool out_dev = is_device_ptr(out);
-    const double scale = (flags & DK_OUT_SUM) ? 1.0 : 1.0 / double(h->n);
+    // mean over the GLOBAL row count: a shard handle writes its contribution to the global mean,
+    // so an all-reduce (sum) of the shards gives the KDE directly
+    const double scale = (flags & DK_OUT_SUM) ? 1.0 : 1.0 / double(h->global_n);
     Plan pl;
     const size_t o_Q = pl.add<double>(size_t(nq) * h->d);
     const size_t o_out = pl.add<double>(size_t(nq));
@@ -748,32 +757,52 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     const size_t o_part = pl.add<double>(sweep_part_count(h->n_pad, nq_pad, h->num_sms));
     h->ws.reserve(pl.off);
     const double* Qd = stage_queries(h, Q, nq, o_Q, s);
-    const int mode = choose_mode(h, Qd, nq, at<uint32_t>(h->ws, o_flags), s);
-    const Encoding& e = ensure_encoding(h, mode, s);
-    QueryOperand q = encode_queries(h, e, Qd, nq, nq_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
-                                    at<float>(h->ws, o_scal), s);
-    SweepArgs a{};
-    a.mode = family == DK_GAUSSIAN ? MODE_KDE_GAUSS : MODE_KDE_EXP;
-    a.qop = &q;
-    a.enc = &e;
-    a.n = h->n;
-    a.n_pad = h->n_pad;
-    a.tile_stride = 1;
-    const double log2e = 1.4426950408889634;
-    a.negc = float(family == DK_GAUSSIAN ? -log2e / (2.0 * bandwidth * bandwidth) : -log2e / bandwidth);
-    a.part = at<double>(h->ws, o_part);
-    int32_t ncc = 0;
-    a.ncc_out = &ncc;
-    {
-      ProfScope ps(h, s, 2.0 * double(h->d) * double(nq) * double(h->n), double(h->n_pad) * e.Kp * 2);
-      launch_sweep(a, h->num_sms, s);
-    }
     double* od = out_dev ? out : at<double>(h->ws, o_out);
-    launch_reduce_partials(a.part, ncc * kColGroups, nq_pad, nq, scale, od, s);
-    if (!out_dev) {
-      copy_out(out, od, size_t(nq) * sizeof(double), s);
-      DK_CUDA(cudaStreamSynchronize(s));
+    auto run_sweep = [&](int mode, uint32_t* guard_flags) {
+      const Encoding& e = ensure_encoding(h, mode, s);
+      // speculative exact mode: the query encode also computes the exact-mode flags
+      QueryOperand q = encode_queries(h, e, Qd, nq, nq_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
+                                      at<float>(h->ws, o_scal), s, guard_flags);
+      if (guard_flags) {
+        DK_CUDA(cudaMemcpyAsync(h->flag_host, guard_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaEventRecord(h->flag_event, s));
+      }
+      SweepArgs a{};
+      a.mode = family == DK_GAUSSIAN ? MODE_KDE_GAUSS : MODE_KDE_EXP;
+      a.qop = &q;
+      a.enc = &e;
+      a.n = h->n;
+      a.n_pad = h->n_pad;
+      a.tile_stride = 1;
+      const double log2e = 1.4426950408889634;
+      a.negc = float(family == DK_GAUSSIAN ? -log2e / (2.0 * bandwidth * bandwidth) : -log2e / bandwidth);
+      a.part = at<double>(h->ws, o_part);
+      a.guard = guard_flags;
+      int32_t ncc = 0;
+      a.ncc_out = &ncc;
+      {
+        ProfScope ps(h, s, 2.0 * double(h->d) * double(nq) * double(h->n), double(h->n_pad) * e.Kp * 2);
+        launch_sweep(a, h->num_sms, s);
+      }
+      launch_reduce_partials(a.part, ncc * kColGroups, nq_pad, nq, scale, od, s);
+      if (!out_dev) copy_out(out, od, size_t(nq) * sizeof(double), s);
+    };
+    if (h->precision == DK_PREC_AUTO && h->int_exact) {
+      // Integer dataset: launch the exact-mode sweep without waiting for the query check.
+      // The sweep reads the check's flags and skips itself for fractional queries; the host
+      // waits only for the (early) check result — overlapped with the sweep — and redoes a
+      // fractional batch in split3.  No host round trip sits between consecutive calls.
+      uint32_t* flags = at<uint32_t>(h->ws, o_flags);
+      DK_CUDA(cudaMemsetAsync(flags, 0, sizeof(uint32_t), s));
+      run_sweep(0, flags);
+      DK_CUDA(cudaEventSynchronize(h->flag_event));
+      const uint32_t f = *h->flag_host;
+      DK_REQUIRE(!(f & 1u), "queries must be finite");
+      if (f & 6u) run_sweep(1, nullptr);
+    } else {
+      run_sweep(choose_mode(h, Qd, nq, at<uint32_t>(h->ws, o_flags), s), nullptr);
     }
+    if (!out_dev) DK_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -142,6 +142,8 @@ struct dk_dataset {
   dk::Workspace ws;
   double* mu = nullptr;     // [d] column means (split/fp16 centring)
   int64_t* rsp_inverse = nullptr;  // [n] original id -> permuted position (dk_rsp_attach)
+  uint32_t* flag_host = nullptr;   // pinned word: query-check flags of the last speculative sweep
+  cudaEvent_t flag_event = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   bool profiling = false;
@@ -174,9 +176,10 @@ void launch_encode_rows(const float* X, int64_t n, int64_t n_pad, int32_t d, int
                         int32_t Kp, __half* B, float* xn, float* scale, uint32_t* maxabs_bits, cudaStream_t s);
 // queries
 void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags, cudaStream_t s);
+// check_flags (mode 0 only, nullable): also OR query_check's exact-mode flags into *check_flags
 void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
                            int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
-                           cudaStream_t s);
+                           cudaStream_t s, uint32_t* check_flags = nullptr);
 void launch_reduce_partials(const double* part, int32_t nparts, int32_t nq_pad, int64_t nq, double scale,
                             double* out, cudaStream_t s);
 
@@ -196,6 +199,7 @@ struct SweepArgs {
   unsigned long long* cand;
   int32_t cap;
   int32_t seg_tiles;          // TILEMIN: tiles per segment
+  const uint32_t* guard;      // optional device flags: skip the sweep if (*guard & 6) (see TileParams)
 };
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms);  // doubles needed for KDE partials
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);

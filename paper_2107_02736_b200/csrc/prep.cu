@@ -113,7 +113,7 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
                               const double* __restrict__ mu, int32_t Kp, const uint32_t* __restrict__ maxabs_bits,
                               const float* __restrict__ other_scale, __half* __restrict__ out,
                               float* __restrict__ norms, float* __restrict__ scale_out,
-                              float* __restrict__ m2s_out) {
+                              float* __restrict__ m2s_out, uint32_t* __restrict__ check_flags) {
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const float s = (mode == 0) ? 1.f : pow2_scale(*maxabs_bits);
@@ -130,6 +130,7 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
   }
   const T* v = V + row * d;
   double nrm = 0.0;
+  uint32_t f = 0;  // exact-mode eligibility of this row (query_check_kernel's flags), mode 0 only
   for (int k = lane; k < Kp; k += 32) {
     if (mode == 1) {
       // K-concatenation A=[Qh|Ql|Qh], B=[Xl|Xh|Xh]: the two small cross terms are accumulated
@@ -153,6 +154,7 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
     } else {
       if (k >= d) { o[k] = __float2half_rn(0.f); continue; }
       double x = double(v[k]);
+      if (check_flags) f |= value_flags(x);
       if (mu) x -= mu[k];
       nrm = fma(x, x, nrm);
       o[k] = __float2half_rn(float(x * double(s)));
@@ -160,6 +162,13 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
   }
   nrm = warp_sum_d(nrm);
   if (lane == 0) norms[row] = float(nrm);
+  if (check_flags) {
+    f = warp_or(f);
+    if (lane == 0) {
+      if (!(nrm < 8388608.0)) f |= FLAG_BIGNORM;
+      if (f) atomicOr(check_flags, f);
+    }
+  }
 }
 
 // queries: finiteness / integrality (exact-mode eligibility)
@@ -243,7 +252,7 @@ void launch_encode_rows(const float* X, int64_t n, int64_t n_pad, int32_t d, int
   }
   const int64_t threads = n_pad * 32;
   encode_kernel<float><<<unsigned((threads + 255) / 256), 256, 0, s>>>(X, n, n_pad, d, mode, mu, Kp, maxabs_bits,
-                                                                      nullptr, B, xn, scale, nullptr);
+                                                                      nullptr, B, xn, scale, nullptr, nullptr);
   DK_CHECK_LAUNCH();
 }
 
@@ -255,17 +264,17 @@ void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags,
 
 void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
                            int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
-                           cudaStream_t s) {
-  DK_CUDA(cudaMemsetAsync(maxabs_bits, 0, sizeof(uint32_t), s));
+                           cudaStream_t s, uint32_t* check_flags) {
   if (mode != 0) {
+    DK_CUDA(cudaMemsetAsync(maxabs_bits, 0, sizeof(uint32_t), s));
     const int64_t total = nq * d;
     const unsigned blocks = unsigned(std::min<int64_t>(1184, (total + 255) / 256 + 1));
     maxabs_kernel<double><<<blocks, 256, 0, s>>>(Q, nq, d, mu, maxabs_bits);
     DK_CHECK_LAUNCH();
   }
   const int64_t threads = int64_t(nq_pad) * 32;
-  encode_kernel<double><<<unsigned((threads + 255) / 256), 256, 0, s>>>(Q, nq, nq_pad, d, mode, mu, Kp, maxabs_bits,
-                                                                       sx, A, qn, nullptr, m2s);
+  encode_kernel<double><<<unsigned((threads + 255) / 256), 256, 0, s>>>(
+      Q, nq, nq_pad, d, mode, mu, Kp, maxabs_bits, sx, A, qn, nullptr, m2s, mode == 0 ? check_flags : nullptr);
   DK_CHECK_LAUNCH();
 }
 

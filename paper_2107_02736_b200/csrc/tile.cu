@@ -196,6 +196,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.cand = a.cand;
   p.cap = a.cap;
   p.seg_tiles = a.seg_tiles;
+  p.guard = a.guard;
   if (a.ncc_out) *a.ncc_out = pl.ncc;
 
   const int nunits = ngroups * pl.ncc;

@@ -97,6 +97,7 @@ struct TileParams {
   uint32_t* cand_cnt;      // FILTER: [nq_pad]
   unsigned long long* cand;  // FILTER: [nq_pad][cap] keys (f32 bits << 32 | col)
   int32_t cap;
+  const uint32_t* guard;     // optional: the sweep is skipped when (*guard & 6) != 0 (queries not exact-mode)
 };
 
 __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode, bool pair) {
@@ -271,6 +272,9 @@ template <int MODE, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
                 const TileParams p) {
+  // speculative exact-mode launch (capi.cu dk_naive): the host has not waited for the query
+  // check, so a batch that turned out fractional skips this sweep and is redone in split3
+  if (p.guard != nullptr && (*p.guard & 6u) != 0u) return;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the shared pointer itself, so the
   // compiler keeps the shared address space (LDS/ATOMS instead of generic LD/ATOM)
