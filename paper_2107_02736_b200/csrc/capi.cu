@@ -287,6 +287,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
   const size_t o_cand = pl.add<unsigned long long>(size_t(kp.cap) * bpad);
   const size_t o_status = pl.add<int32_t>(bpad);
   const size_t o_list = pl.add<int32_t>(bpad);
+  const size_t o_max = pl.add<uint32_t>(1);
   if (pl.off > h->ws.cap) throw Error{DK_ECUDA, "internal: k-NN workspace under-reserved"};
   const float inf = std::numeric_limits<float>::infinity();
   for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
@@ -343,8 +344,9 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       h->knn_queries += bn;
     }
     int32_t* status = at<int32_t>(h->ws, o_status);
+    const uint32_t cmax = max_count(cnt, bn, at<uint32_t>(h->ws, o_max), s);
     launch_select_rerank(h->X, h->global_offset, h->d, Qb, bn, k, cand, cnt, kp.cap, q.qn, e.xn_max, e.eps_rel,
-                         idx_d + b0 * k, d2_d + b0 * k, status, s);
+                         idx_d + b0 * k, d2_d + b0 * k, status, s, int32_t(std::min<uint32_t>(cmax, 1u << 30)));
     std::vector<int32_t> st(static_cast<size_t>(bn));
     DK_CUDA(cudaMemcpyAsync(st.data(), status, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     DK_CUDA(cudaStreamSynchronize(s));
@@ -377,6 +379,7 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
   pl.add<unsigned long long>(size_t(kp.cap) * kp.batch);
   pl.add<int32_t>(kp.batch);
   pl.add<int32_t>(kp.batch);
+  pl.add<uint32_t>(1);
   return pl.off + 4096;
 }
 

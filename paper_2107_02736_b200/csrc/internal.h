@@ -229,7 +229,8 @@ void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s);
 void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
                           const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
                           float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* status,
-                          cudaStream_t s);
+                          cudaStream_t s, int32_t max_cnt = 0);
+uint32_t max_count(const uint32_t* v, int64_t n, uint32_t* scratch, cudaStream_t s);  // synchronises
 void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
                                const int32_t* qlist, int32_t nlist, int32_t k, int64_t* idx_out, double* d2_out,
                                cudaStream_t s);
