@@ -168,7 +168,6 @@ struct QueryOperand {
 CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint32_t box_rows);
 
 // dataset prep
-void launch_check_finite_rows(const float* X, int64_t count, uint32_t* flags, cudaStream_t s);
 void launch_row_stats(const float* X, int64_t n, int32_t d, double* xn64, uint32_t* flags, cudaStream_t s);
 void launch_column_mean(const float* X, int64_t n, int32_t d, double* partial, int32_t row_blocks, double* mu,
                         cudaStream_t s);

@@ -232,7 +232,6 @@ void launch_row_stats(const float* X, int64_t n, int32_t d, double* xn64, uint32
   DK_CHECK_LAUNCH();
 }
 
-void launch_check_finite_rows(const float*, int64_t, uint32_t*, cudaStream_t) {}
 
 void launch_column_mean(const float* X, int64_t n, int32_t d, double* partial, int32_t row_blocks, double* mu,
                         cudaStream_t s) {
