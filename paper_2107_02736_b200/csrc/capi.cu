@@ -414,7 +414,7 @@ HandlePtr new_handle(int64_t n, int32_t d, const dk_fit_opts* opts) {
   DK_REQUIRE(h->global_offset >= 0 && h->global_offset + n <= h->global_n, "shard outside [0, global_n)");
   {
     DeviceGuard g(device);
-    DK_CUDA(cudaHostAlloc(&h->flag_host, sizeof(uint32_t), cudaHostAllocDefault));
+    DK_CUDA(cudaHostAlloc(&h->flag_host, 2 * sizeof(uint32_t), cudaHostAllocDefault));
     DK_CUDA(cudaEventCreateWithFlags(&h->flag_event, cudaEventDisableTiming));
   }
   return h;
@@ -686,6 +686,9 @@ dk_status dk_free(dk_handle h) {
     if (h->rsp_inverse) cudaFree(h->rsp_inverse);
     if (h->flag_host) cudaFreeHost(h->flag_host);
     if (h->flag_event) cudaEventDestroy(h->flag_event);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->copy_ready) cudaEventDestroy(h->copy_ready);
+    if (h->copy_done) cudaEventDestroy(h->copy_done);
     for (auto& pr : h->prof_events) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
@@ -752,22 +755,57 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       }
       return;
     }
-    const int32_t nq_pad = int32_t(query_pad(nq));
+    // Host queries of a large batch run as two chunks: the copy of the second (3/4 of the
+    // batch) overlaps the sweep of the first on a side stream, hiding most of the H2D time.
+    const bool host_q = !is_device_ptr(Q);
+    const int64_t split = (host_q && nq >= 4096) ? round_up(nq / 4, 256) : nq;
+    const int64_t c_beg[2] = {0, split};
+    const int64_t c_cnt[2] = {split, nq - split};
+    const int nchunks = c_cnt[1] > 0 ? 2 : 1;
     const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
-    const size_t o_A = pl.add<__half>(size_t(nq_pad) * Kp_max);
-    const size_t o_qn = pl.add<float>(nq_pad);
-    const size_t o_scal = pl.add<float>(4);
-    const size_t o_part = pl.add<double>(sweep_part_count(h->n_pad, nq_pad, h->num_sms));
+    size_t o_A[2], o_qn[2], o_scal[2], o_part[2], o_fl[2];
+    for (int c = 0; c < nchunks; ++c) {
+      const int32_t pad = int32_t(query_pad(c_cnt[c]));
+      o_A[c] = pl.add<__half>(size_t(pad) * Kp_max);
+      o_qn[c] = pl.add<float>(pad);
+      o_scal[c] = pl.add<float>(4);
+      o_part[c] = pl.add<double>(sweep_part_count(h->n_pad, pad, h->num_sms));
+      o_fl[c] = pl.add<uint32_t>(4);
+    }
     h->ws.reserve(pl.off);
-    const double* Qd = stage_queries(h, Q, nq, o_Q, s);
     double* od = out_dev ? out : at<double>(h->ws, o_out);
-    auto run_sweep = [&](int mode, uint32_t* guard_flags) {
+    const double* Qd = Q;
+    if (host_q) {
+      double* dst = at<double>(h->ws, o_Q);
+      DK_CUDA(cudaMemcpyAsync(dst, Q, size_t(c_cnt[0]) * h->d * sizeof(double), cudaMemcpyHostToDevice, s));
+      if (nchunks == 2) {
+        if (!h->copy_stream) {
+          DK_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+          DK_CUDA(cudaEventCreateWithFlags(&h->copy_ready, cudaEventDisableTiming));
+          DK_CUDA(cudaEventCreateWithFlags(&h->copy_done, cudaEventDisableTiming));
+        }
+        // the side copy may only overwrite the staging area once earlier work on s is done
+        DK_CUDA(cudaEventRecord(h->copy_ready, s));
+        DK_CUDA(cudaStreamWaitEvent(h->copy_stream, h->copy_ready, 0));
+        DK_CUDA(cudaMemcpyAsync(dst + size_t(c_beg[1]) * h->d, Q + size_t(c_beg[1]) * h->d,
+                                size_t(c_cnt[1]) * h->d * sizeof(double), cudaMemcpyHostToDevice,
+                                h->copy_stream));
+        DK_CUDA(cudaEventRecord(h->copy_done, h->copy_stream));
+      }
+      Qd = dst;
+    }
+    const double log2e = 1.4426950408889634;
+    const float negc = float(family == DK_GAUSSIAN ? -log2e / (2.0 * bandwidth * bandwidth) : -log2e / bandwidth);
+    auto run_sweep = [&](int c, int mode, uint32_t* guard_flags) {
+      const int64_t q0 = c_beg[c], cn = c_cnt[c];
+      const int32_t pad = int32_t(query_pad(cn));
+      const double* Qc = Qd + size_t(q0) * h->d;
       const Encoding& e = ensure_encoding(h, mode, s);
       // speculative exact mode: the query encode also computes the exact-mode flags
-      QueryOperand q = encode_queries(h, e, Qd, nq, nq_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
-                                      at<float>(h->ws, o_scal), s, guard_flags);
+      QueryOperand q = encode_queries(h, e, Qc, cn, pad, at<__half>(h->ws, o_A[c]), at<float>(h->ws, o_qn[c]),
+                                      at<float>(h->ws, o_scal[c]), s, guard_flags);
       if (guard_flags) {
-        DK_CUDA(cudaMemcpyAsync(h->flag_host, guard_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaMemcpyAsync(h->flag_host + c, guard_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         DK_CUDA(cudaEventRecord(h->flag_event, s));
       }
       SweepArgs a{};
@@ -777,33 +815,36 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       a.n = h->n;
       a.n_pad = h->n_pad;
       a.tile_stride = 1;
-      const double log2e = 1.4426950408889634;
-      a.negc = float(family == DK_GAUSSIAN ? -log2e / (2.0 * bandwidth * bandwidth) : -log2e / bandwidth);
-      a.part = at<double>(h->ws, o_part);
+      a.negc = negc;
+      a.part = at<double>(h->ws, o_part[c]);
       a.guard = guard_flags;
       int32_t ncc = 0;
       a.ncc_out = &ncc;
       {
-        ProfScope ps(h, s, 2.0 * double(h->d) * double(nq) * double(h->n), double(h->n_pad) * e.Kp * 2);
+        ProfScope ps(h, s, 2.0 * double(h->d) * double(cn) * double(h->n), double(h->n_pad) * e.Kp * 2);
         launch_sweep(a, h->num_sms, s);
       }
-      launch_reduce_partials(a.part, ncc * kColGroups, nq_pad, nq, scale, od, s);
-      if (!out_dev) copy_out(out, od, size_t(nq) * sizeof(double), s);
+      launch_reduce_partials(a.part, ncc * kColGroups, pad, cn, scale, od + q0, s);
+      if (!out_dev) copy_out(out + q0, od + q0, size_t(cn) * sizeof(double), s);
     };
-    if (h->precision == DK_PREC_AUTO && h->int_exact) {
-      // Integer dataset: launch the exact-mode sweep without waiting for the query check.
-      // The sweep reads the check's flags and skips itself for fractional queries; the host
-      // waits only for the (early) check result — overlapped with the sweep — and redoes a
-      // fractional batch in split3.  No host round trip sits between consecutive calls.
-      uint32_t* flags = at<uint32_t>(h->ws, o_flags);
-      DK_CUDA(cudaMemsetAsync(flags, 0, sizeof(uint32_t), s));
-      run_sweep(0, flags);
-      DK_CUDA(cudaEventSynchronize(h->flag_event));
-      const uint32_t f = *h->flag_host;
-      DK_REQUIRE(!(f & 1u), "queries must be finite");
-      if (f & 6u) run_sweep(1, nullptr);
-    } else {
-      run_sweep(choose_mode(h, Qd, nq, at<uint32_t>(h->ws, o_flags), s), nullptr);
+    for (int c = 0; c < nchunks; ++c) {
+      if (c == 1) DK_CUDA(cudaStreamWaitEvent(s, h->copy_done, 0));
+      if (h->precision == DK_PREC_AUTO && h->int_exact) {
+        // Integer dataset: launch the exact-mode sweep without waiting for the query check.
+        // The sweep reads the check's flags and skips itself for fractional queries; the host
+        // waits only for the (early) check result — overlapped with the sweep — and redoes a
+        // fractional chunk in split3.  No host round trip sits between consecutive calls.
+        uint32_t* flags = at<uint32_t>(h->ws, o_fl[c]);
+        DK_CUDA(cudaMemsetAsync(flags, 0, sizeof(uint32_t), s));
+        run_sweep(c, 0, flags);
+        DK_CUDA(cudaEventSynchronize(h->flag_event));
+        const uint32_t f = h->flag_host[c];
+        DK_REQUIRE(!(f & 1u), "queries must be finite");
+        if (f & 6u) run_sweep(c, 1, nullptr);
+      } else {
+        run_sweep(c, choose_mode(h, Qd + size_t(c_beg[c]) * h->d, c_cnt[c], at<uint32_t>(h->ws, o_fl[c]), s),
+                  nullptr);
+      }
     }
     if (!out_dev) DK_CUDA(cudaStreamSynchronize(s));
   });

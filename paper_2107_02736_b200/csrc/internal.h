@@ -142,8 +142,10 @@ struct dk_dataset {
   dk::Workspace ws;
   double* mu = nullptr;     // [d] column means (split/fp16 centring)
   int64_t* rsp_inverse = nullptr;  // [n] original id -> permuted position (dk_rsp_attach)
-  uint32_t* flag_host = nullptr;   // pinned word: query-check flags of the last speculative sweep
+  uint32_t* flag_host = nullptr;   // pinned words: query-check flags of the speculative sweeps (2 chunks)
   cudaEvent_t flag_event = nullptr;
+  cudaStream_t copy_stream = nullptr;  // side stream for the overlapped host->device query copy
+  cudaEvent_t copy_ready = nullptr, copy_done = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   bool profiling = false;
