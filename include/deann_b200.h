@@ -114,6 +114,17 @@ dk_status dk_sq_norms(dk_handle h, double* out, void* stream);
 dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family,
                    double bandwidth, uint32_t flags, double* out, void* stream);
 
+/* ---- materialised distances ---------------------------------------------
+ * batch_sqdist / window_sqdist (distance.py:58-123): out[j][i] (nq x row_count,
+ * fp64) = max(0, ((q_j . x_i) * -2 + |q_j|^2) + |x_i|^2) for rows i in
+ * [row_begin, row_begin + row_count), the reference's norms identity in fp64.
+ * x_norms (nullable, n fp64) overrides the handle's norms (a caller's cached
+ * sq_norms).  *worst = the most negative entry before clamping, for the
+ * NormConsistencyError check of _clamp (distance.py:54-64). */
+dk_status dk_sqdist(dk_handle h, const double* Q, int64_t nq, const double* x_norms,
+                    int64_t row_begin, int64_t row_count, double* out, double* worst,
+                    void* stream);
+
 /* ---- exact k-NN -----------------------------------------------------------
  * brute_force_knn (ann.py:105-111) / BruteForceIndex.query (ann.py:120-121)
  * for a batch: idx_out (nq x k, int64, GLOBAL row ids), d2_out (nq x k, fp64

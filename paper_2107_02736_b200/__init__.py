@@ -14,6 +14,7 @@ All arithmetic runs in hand-written sm_100a kernels behind the C-ABI in
 from .ann import AnnIndex, BruteForceIndex, GpuBruteForceIndex, NeighborList, brute_force_knn, knn_batch
 from .bandwidth import fit_bandwidth, NoBandwidthError
 from .data import Dataset, DatasetFormatError, PermutedDataset, as_gpu_dataset, file_info, load, permute, save
+from .distance import DistanceMatrix, NormConsistencyError, batch_sqdist, sqdist, window_sqdist
 from .estimators import (
     BatchKde,
     Estimate,
@@ -50,4 +51,5 @@ __all__ = [
     "deann_arrays", "deann_batch", "kernel_from_distance", "naive_kde", "naive_kde_into", "rs_kde",
     "KernelFamily", "KernelSpec", "PhiloxSampler", "IvfIndex", "IvfAnnIndex", "ivf_build", "ivf_query",
     "ivf_query_batch", "recall", "save_ivf_index", "load_ivf_index",
+    "DistanceMatrix", "NormConsistencyError", "batch_sqdist", "sqdist", "window_sqdist",
 ]

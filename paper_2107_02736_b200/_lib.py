@@ -26,7 +26,7 @@ DK_OUT_SUM = 1
 EXPORTED = (
     "dk_version", "dk_last_error", "dk_device_ok", "dk_fit", "dk_free", "dk_file_info", "dk_fit_file",
     "dk_info", "dk_sq_norms",
-    "dk_naive", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
+    "dk_naive", "dk_sqdist", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
     "dk_rsp_attach", "dk_rsp_walk", "dk_ivf_create", "dk_ivf_free", "dk_kmeanspp_seed", "dk_kmeanspp_pick",
     "dk_kmeans_lloyd", "dk_ivf_get", "dk_ivf_set", "dk_ivf_query", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
 )
@@ -67,6 +67,7 @@ def _declare(lib):
         "dk_device_ok": (_i32, [_i32]),
         "dk_fit": (_i32, [_vp, _i64, _i32, ctypes.POINTER(FitOpts), ctypes.POINTER(_vp)]),
         "dk_free": (_i32, [_vp]),
+        "dk_sqdist": (_i32, [_vp, _vp, _i64, _vp, _i64, _i64, _vp, ctypes.POINTER(_f64), _vp]),
         "dk_ivf_create": (_i32, [_vp, _i32, ctypes.POINTER(_vp)]),
         "dk_ivf_free": (_i32, [_vp]),
         "dk_kmeanspp_seed": (_i32, [_vp, _i32, _i64, ctypes.POINTER(_f64)]),
