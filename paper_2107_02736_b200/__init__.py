@@ -13,7 +13,18 @@ All arithmetic runs in hand-written sm_100a kernels behind the C-ABI in
 
 from .ann import AnnIndex, BruteForceIndex, GpuBruteForceIndex, NeighborList, brute_force_knn, knn_batch
 from .bandwidth import fit_bandwidth, NoBandwidthError
-from .data import Dataset, DatasetFormatError, PermutedDataset, as_gpu_dataset, file_info, load, permute, save
+from .data import (
+    Dataset,
+    DatasetFormatError,
+    PermutedDataset,
+    Splits,
+    as_gpu_dataset,
+    file_info,
+    load,
+    permute,
+    save,
+    split,
+)
 from .distance import DistanceMatrix, NormConsistencyError, batch_sqdist, sqdist, window_sqdist
 from .estimators import (
     BatchKde,
@@ -21,8 +32,11 @@ from .estimators import (
     RspState,
     deann,
     deann_arrays,
+    dataset_sha256,
     deann_batch,
+    ground_truth,
     kernel_from_distance,
+    kernel_pair,
     naive_kde,
     naive_kde_into,
     rs_kde,
@@ -52,4 +66,5 @@ __all__ = [
     "KernelFamily", "KernelSpec", "PhiloxSampler", "IvfIndex", "IvfAnnIndex", "ivf_build", "ivf_query",
     "ivf_query_batch", "recall", "save_ivf_index", "load_ivf_index",
     "DistanceMatrix", "NormConsistencyError", "batch_sqdist", "sqdist", "window_sqdist",
+    "Splits", "split", "kernel_pair", "ground_truth", "dataset_sha256",
 ]

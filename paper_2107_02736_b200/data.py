@@ -17,13 +17,14 @@ import ctypes
 import os
 import struct
 import weakref
+from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
 
 __all__ = ["Dataset", "as_gpu_dataset", "PermutedDataset", "permute", "as_gpu_permuted", "DatasetFormatError",
-           "file_info", "load", "save"]
+           "file_info", "load", "save", "Splits", "split"]
 
 DatasetFormatError = _lib.DatasetFormatError
 MAGIC = b"DEANN1\x00\x00"
@@ -101,6 +102,11 @@ class Dataset:
 
     def free(self) -> None:
         self._finalizer()
+
+    def take(self, indices) -> "Dataset":
+        """New fitted dataset from a row subset (data.py:85-87; norms recomputed on the device)."""
+        return Dataset.from_array(self.data[np.asarray(indices, dtype=np.intp)], device=self.device,
+                                  precision=self.precision)
 
 
 def _free_handle(h):
@@ -264,3 +270,36 @@ def save(dataset, path, fmt: str = "binary") -> None:
         np.savetxt(path, data, delimiter=",", fmt="%.9g")
     else:
         raise ValueError(f"unknown format {fmt!r}")
+
+
+# ---------------------------------------------------------------- splits (data.py:90-101, 192-211)
+
+
+@dataclass
+class Splits:
+    """Disjoint train/validation/test parts whose union is the input."""
+
+    train: Dataset
+    validation: Dataset
+    test: Dataset
+    seed: int
+    train_indices: np.ndarray
+    validation_indices: np.ndarray
+    test_indices: np.ndarray
+
+
+def split(dataset, seed: int) -> Splits:
+    """Seeded disjoint split with numpy's PCG64, identical to the reference's (data.py:192-211):
+    up to 500 validation and 500 test rows, the rest training (at least one row)."""
+    ds = as_gpu_dataset(dataset)
+    n = ds.n
+    if n <= 2:
+        raise ValueError(f"cannot split a dataset with n={n}; need n > 2")
+    n_val = min(500, n - 2)
+    n_test = min(500, n - n_val - 1)
+    order = np.random.default_rng(seed).permutation(n)
+    val_idx = np.sort(order[:n_val])
+    test_idx = np.sort(order[n_val:n_val + n_test])
+    train_idx = np.sort(order[n_val + n_test:])
+    return Splits(train=ds.take(train_idx), validation=ds.take(val_idx), test=ds.take(test_idx), seed=seed,
+                  train_indices=train_idx, validation_indices=val_idx, test_indices=test_idx)

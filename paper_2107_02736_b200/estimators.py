@@ -23,9 +23,10 @@ The permuted sampler is deterministic and matches the reference exactly
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-
 import ctypes
+import hashlib
+import math
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -114,6 +115,44 @@ def kernel_from_distance(kernel, dist):
     if scalar:
         return float(out[0])
     return out.reshape(np.shape(dist))
+
+
+def kernel_pair(kernel, x, y) -> float:
+    """Kernel value between two points with the family's own metric (kernels.py:86-106)."""
+    spec = as_spec(kernel)
+    xv = np.asarray(x, dtype=np.float64).ravel()
+    yv = np.asarray(y, dtype=np.float64).ravel()
+    if xv.shape != yv.shape:
+        raise ValueError(f"dimension mismatch: {xv.shape[0]} vs {yv.shape[0]}")
+    if xv.size == 0:
+        raise ValueError("vectors must have dimension >= 1")
+    diff = xv - yv
+    if spec.family is KernelFamily.GAUSSIAN:
+        dist = float(diff @ diff)
+    elif spec.family is KernelFamily.EXPONENTIAL:
+        dist = math.sqrt(float(diff @ diff))
+    else:
+        dist = float(np.abs(diff).sum())
+    return kernel_from_distance(spec, dist)
+
+
+def dataset_sha256(dataset) -> str:
+    """SHA-256 of the rows as little-endian fp32 (harness.py:183-184)."""
+    data = getattr(dataset, "data", dataset)
+    return hashlib.sha256(np.ascontiguousarray(data, dtype="<f4").tobytes()).hexdigest()
+
+
+def ground_truth(dataset, queries, kernel) -> dict:
+    """Exact KDE values plus a manifest tying them to their inputs (harness.py:187-196), on the GPU."""
+    spec = as_spec(kernel)
+    values = naive_kde(dataset, spec, queries).values
+    return {
+        "kernel": spec.family.value,
+        "bandwidth": spec.bandwidth,
+        "dataset_sha256": dataset_sha256(dataset),
+        "n_queries": int(len(values)),
+        "values": [float(v) for v in values],
+    }
 
 
 # ---------------------------------------------------------------- sampling

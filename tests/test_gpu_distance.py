@@ -98,3 +98,23 @@ def test_window_sqdist_wraps_and_matches_permuted_rows():
         g.window_sqdist(pds, 50, 3, y)
     with pytest.raises(ValueError):
         g.window_sqdist(pds, 0, 51, y)
+
+
+def test_kernel_pair_ground_truth_and_split():
+    x, y = [0.0, 0.0, 0.0], [1.0, 2.0, 2.0]
+    assert g.kernel_pair(g.KernelSpec("gaussian", 1.5), x, y) == pytest.approx(np.exp(-9.0 / 4.5), rel=1e-15)
+    assert g.kernel_pair(g.KernelSpec("exponential", 1.5), x, y) == pytest.approx(np.exp(-2.0), rel=1e-15)
+    assert g.kernel_pair(g.KernelSpec("laplacian", 2.5), x, y) == pytest.approx(np.exp(-2.0), rel=1e-15)
+    with pytest.raises(ValueError):
+        g.kernel_pair(g.KernelSpec("gaussian", 1.0), [1.0], [1.0, 2.0])
+    X = np.random.default_rng(4).normal(size=(1200, 5)).astype(np.float32)
+    sp = g.split(g.Dataset.from_array(X), 9)
+    ref_order = np.random.default_rng(9).permutation(1200)   # data.py:200-206
+    np.testing.assert_array_equal(sp.validation_indices, np.sort(ref_order[:500]))
+    np.testing.assert_array_equal(sp.test_indices, np.sort(ref_order[500:1000]))
+    assert sp.train.n == 200 and sp.validation.n == 500 and sp.test.n == 500
+    np.testing.assert_array_equal(sp.train.data, X[sp.train_indices])
+    gt = g.ground_truth(sp.train, X[:4].astype(np.float64), g.KernelSpec("gaussian", 1.0))
+    ref = O.naive_kde(O.Data(X[sp.train_indices]), "gaussian", 1.0, X[:4].astype(np.float64))
+    np.testing.assert_allclose(gt["values"], ref, rtol=1e-5)
+    assert gt["n_queries"] == 4 and gt["kernel"] == "gaussian" and len(gt["dataset_sha256"]) == 64
