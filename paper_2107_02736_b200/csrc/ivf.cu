@@ -20,6 +20,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "internal.h"
 
@@ -425,6 +426,139 @@ __global__ void first_probe_kernel(const int32_t* __restrict__ probe, int64_t nq
   val[q] = int32_t(q);
 }
 
+// ---- large k (> 4096, beyond the shared-memory top-k): every probed candidate's exact
+// (d2, row) pair, then a stable two-pass segmented radix sort (row id, then d2) per query
+__global__ void probe_total_kernel(const int32_t* __restrict__ probe, const int64_t* __restrict__ off, int64_t nq,
+                                   int32_t n_probe, int64_t* __restrict__ tot) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int64_t t = 0;
+  for (int p = 0; p < n_probe; ++p) {
+    const int c = probe[q * n_probe + p];
+    t += off[c + 1] - off[c];
+  }
+  tot[q] = t;
+}
+
+__global__ void gather_cands_kernel(const float* __restrict__ xs, const double* __restrict__ xns,
+                                    const int64_t* __restrict__ rows, const int64_t* __restrict__ off, int32_t d,
+                                    const double* __restrict__ Q, const int32_t* __restrict__ probe, int32_t n_probe,
+                                    int64_t q0, const int64_t* __restrict__ seg, unsigned long long* __restrict__ key,
+                                    unsigned long long* __restrict__ val) {
+  extern __shared__ double y[];
+  __shared__ double s_yy;
+  const int64_t q = q0 + blockIdx.x;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) y[j] = Q[q * d + j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int j = 0; j < d; ++j) t = fma(y[j], y[j], t);
+    s_yy = t;
+  }
+  __syncthreads();
+  const double yy = s_yy;
+  int64_t o = seg[blockIdx.x];
+  for (int p = 0; p < n_probe; ++p) {
+    const int c = probe[q * n_probe + p];
+    const int64_t b = off[c], e = off[c + 1];
+    for (int64_t pos = b + threadIdx.x; pos < e; pos += blockDim.x) {
+      const float* x = xs + pos * d;
+      double dot = 0.0;
+      for (int j = 0; j < d; ++j) dot = fma(double(x[j]), y[j], dot);
+      double t = dot * -2.0;
+      t += xns[pos];
+      t += yy;
+      t = fmax(t, 0.0);
+      key[o + (pos - b)] = static_cast<unsigned long long>(rows[pos]);
+      val[o + (pos - b)] = static_cast<unsigned long long>(__double_as_longlong(t));
+    }
+    o += e - b;
+  }
+}
+
+__global__ void take_cands_kernel(const unsigned long long* __restrict__ d2bits,
+                                  const unsigned long long* __restrict__ ids, const int64_t* __restrict__ seg,
+                                  int64_t q0, int64_t nqc, int32_t k, int64_t* __restrict__ idx_out,
+                                  double* __restrict__ d2_out, int32_t* __restrict__ cnt_out) {
+  const int64_t qi = blockIdx.x;
+  if (qi >= nqc) return;
+  const int64_t b = seg[qi], e = seg[qi + 1];
+  const int64_t cnt = min(int64_t(k), e - b);
+  const int64_t q = q0 + qi;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const bool ok = i < cnt;
+    idx_out[q * k + i] = ok ? static_cast<int64_t>(ids[b + i]) : -1;
+    d2_out[q * k + i] = ok ? __longlong_as_double(static_cast<long long>(d2bits[b + i]))
+                           : __longlong_as_double(0x7ff0000000000000ll);
+  }
+  if (threadIdx.x == 0) cnt_out[q] = int32_t(cnt);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) { DK_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as(size_t byte_off = 0) const {
+    return reinterpret_cast<T*>(static_cast<uint8_t*>(p) + byte_off);
+  }
+};
+
+// Queries in chunks of <= 2^26 candidates (the reference accepts any k >= 1, ann.py:208-209).
+void ivf_query_bigk(dk_ivf* v, const double* Qd, int64_t nq, int32_t k, int32_t n_probe, const int32_t* probe,
+                    int64_t* io, double* dd, int32_t* co, cudaStream_t s) {
+  DevBuf totb(size_t(nq) * 8);
+  probe_total_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(probe, v->offsets, nq, n_probe,
+                                                                totb.as<int64_t>());
+  DK_CHECK_LAUNCH();
+  std::vector<int64_t> tot(static_cast<size_t>(nq));
+  DK_CUDA(cudaMemcpyAsync(tot.data(), totb.p, size_t(nq) * 8, cudaMemcpyDeviceToHost, s));
+  DK_CUDA(cudaStreamSynchronize(s));
+  const int64_t cap = int64_t(1) << 26;
+  const size_t smem = size_t(v->d) * sizeof(double);
+  set_dynamic_smem(gather_cands_kernel, smem);
+  int64_t q0 = 0;
+  while (q0 < nq) {
+    int64_t q1 = q0, T = 0;
+    while (q1 < nq && (q1 == q0 || T + tot[size_t(q1)] <= cap)) T += tot[size_t(q1++)];
+    DK_REQUIRE(T < (int64_t(1) << 31), "too many IVF candidates for one query");
+    const int64_t nqc = q1 - q0;
+    std::vector<int64_t> seg(static_cast<size_t>(nqc) + 1, 0);
+    for (int64_t i = 0; i < nqc; ++i) seg[size_t(i) + 1] = seg[size_t(i)] + tot[size_t(q0 + i)];
+    size_t sort_bytes = 0;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, sort_bytes, static_cast<const unsigned long long*>(nullptr),
+                                             static_cast<unsigned long long*>(nullptr),
+                                             static_cast<const unsigned long long*>(nullptr),
+                                             static_cast<unsigned long long*>(nullptr), int(T), int(nqc),
+                                             static_cast<const int64_t*>(nullptr),
+                                             static_cast<const int64_t*>(nullptr));
+    const size_t eT = size_t(std::max<int64_t>(T, 1)) * 8;
+    DevBuf buf(4 * eT + size_t(nqc + 1) * 8 + sort_bytes + 256);
+    auto* k0 = buf.as<unsigned long long>(0);
+    auto* v0 = buf.as<unsigned long long>(eT);
+    auto* k1 = buf.as<unsigned long long>(2 * eT);
+    auto* v1 = buf.as<unsigned long long>(3 * eT);
+    auto* segd = buf.as<int64_t>(4 * eT);
+    void* tmp = buf.as<uint8_t>((4 * eT + size_t(nqc + 1) * 8 + 255) & ~size_t(255));
+    DK_CUDA(cudaMemcpyAsync(segd, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s));
+    gather_cands_kernel<<<unsigned(nqc), 128, smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, Qd, probe,
+                                                         n_probe, q0, segd, k0, v0);
+    DK_CHECK_LAUNCH();
+    size_t tb = sort_bytes;  // pass 1: by row id (keys k0 = ids), pass 2 (stable): by d2
+    DK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, int(T), int(nqc), segd, segd + 1,
+                                                     0, 64, s));
+    tb = sort_bytes;
+    DK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tb, v1, v0, k1, k0, int(T), int(nqc), segd, segd + 1,
+                                                     0, 64, s));
+    take_cands_kernel<<<unsigned(nqc), 128, 0, s>>>(v0, k0, segd, q0, nqc, k, io, dd, co);
+    DK_CHECK_LAUNCH();
+    DK_CUDA(cudaStreamSynchronize(s));  // buffers are freed at the end of the chunk
+    q0 = q1;
+  }
+}
+
 size_t cub_bytes(int64_t n) {
   size_t a = 0, b = 0, c = 0;
   cub::DeviceReduce::Sum(nullptr, a, static_cast<const double*>(nullptr), static_cast<double*>(nullptr), n);
@@ -646,7 +780,6 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     DK_REQUIRE(k >= 1, "k=" + std::to_string(k) + " must be >= 1");
     DK_REQUIRE(n_probe >= 1 && n_probe <= v->C,
                "n_probe=" + std::to_string(n_probe) + " out of range [1, " + std::to_string(v->C) + "]");
-    DK_REQUIRE(k <= 4096, "k > 4096 is not supported by the IVF scan");
     DK_REQUIRE(formula == 0 || formula == 1, "unknown probe formula");
     DK_REQUIRE(nq >= 0, "negative query count");
     if (nq == 0) return;
@@ -664,7 +797,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     int B = 2;
     while (B < Kp + S) B <<= 1;
     const size_t scan_smem = size_t(B) * sizeof(K128) + size_t(v->d) * sizeof(double);
-    DK_REQUIRE(scan_smem <= 232000, "k or d too large for the IVF scan");
+    const bool bigk = k > 4096 || scan_smem > 232000;  // beyond the shared-memory top-k
     // staging: queries, probe lists, outputs
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -674,7 +807,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     };
     const size_t o_q = take(size_t(nq) * v->d * sizeof(double));
     const size_t o_p = take(size_t(nq) * n_probe * sizeof(int32_t));
-    const size_t o_i = take(size_t(nq) * k * sizeof(int64_t));
+    const size_t o_i = take(size_t(nq) * k * sizeof(int64_t));  // (host outputs only)
     const size_t o_d = take(size_t(nq) * k * sizeof(double));
     const size_t o_c = take(size_t(nq) * sizeof(int32_t));
     DK_REQUIRE(nq < (int64_t(1) << 31), "too many queries in one IVF call");
@@ -700,6 +833,9 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     int64_t* io = idev ? idx_out : reinterpret_cast<int64_t*>(base + o_i);
     double* dd = ddev ? d2_out : reinterpret_cast<double*>(base + o_d);
     int32_t* co = cdev ? cnt_out : reinterpret_cast<int32_t*>(base + o_c);
+    if (bigk) {
+      ivf_query_bigk(v, Qd, nq, k, n_probe, probe, io, dd, co, s);
+    } else {
     // lanes per row: enough that one float4 sweep covers about half of a row's 16-byte chunks
     const int chunks = (v->d + 3) / 4;
     // query order: sorted by nearest probed list (L2 reuse across concurrently running blocks)
@@ -731,6 +867,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     else { if (vec) DK_SCAN(1, 4); else DK_SCAN(1, 0); }
 #undef DK_SCAN
     DK_CHECK_LAUNCH();
+    }
     if (!idev) DK_CUDA(cudaMemcpyAsync(idx_out, io, size_t(nq) * k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     if (!ddev) DK_CUDA(cudaMemcpyAsync(d2_out, dd, size_t(nq) * k * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (!cdev) DK_CUDA(cudaMemcpyAsync(cnt_out, co, size_t(nq) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));

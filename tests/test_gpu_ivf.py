@@ -186,3 +186,20 @@ def test_large_build_and_batch_scan_vs_oracle():
         ri, rd = O.ivf_query(od, cent, lists, Q[j], 100, 8)
         np.testing.assert_array_equal(idx[j, :cnt[j]], ri)
         np.testing.assert_allclose(d2[j, :cnt[j]], rd, rtol=1e-12)
+
+
+def test_large_k_beyond_the_shared_memory_top_k():
+    # k > 4096: every probed candidate is sorted by (d2, row) on the device
+    n, d = 30_000, 6
+    X = np.random.default_rng(41).normal(size=(n, d)).astype(np.float32)
+    X[:2000] = X[0]                                   # a block of exact ties
+    Q = np.random.default_rng(42).normal(size=(3, d))
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    index = g.ivf_build(ds, 16, seed=5)
+    cent, lists = O.ivf_build(od, 16, 5)
+    for q in np.vstack([Q, X[:1].astype(np.float64)]):
+        for k, p in ((5000, 4), (30_000, 16)):
+            nl = g.ivf_query(index, ds, q, k, p)
+            ri, rd = O.ivf_query(od, cent, lists, q, k, p)
+            np.testing.assert_array_equal(nl.indices, ri)
+            np.testing.assert_allclose(nl.sq_distances, rd, rtol=1e-12, atol=1e-12)
