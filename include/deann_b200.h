@@ -227,7 +227,7 @@ dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, 
  * IvfAnnIndex) and the exact k smallest d2 = ((x.y) * -2 + |x|^2) + |y|^2
  * (clamped at 0) over their members, (d2, row) order; cnt[j] = min(k, members
  * probed), unused slots idx -1 / d2 +inf; any k >= 1 (k > 4096 sorts every
- * probed candidate).  n_clusters <= 8192. */
+ * probed candidate); any n_clusters (beyond 8192 the probe is a segmented sort). */
 typedef struct dk_ivf* dk_ivf_handle;
 dk_status dk_ivf_create(dk_handle h, int32_t n_clusters, dk_ivf_handle* out);
 dk_status dk_ivf_free(dk_ivf_handle ivf);

@@ -559,6 +559,50 @@ void ivf_query_bigk(dk_ivf* v, const double* Qd, int64_t nq, int32_t k, int32_t 
   }
 }
 
+// ---- n_clusters beyond the shared-memory probe sort (> 8192): all centroid distances of a
+// query chunk, one stable segmented radix sort by the order-preserving key (ties keep the
+// lower centroid id), first n_probe taken
+__global__ void centroid_keys_kernel(const double* __restrict__ Q, int32_t d, const double* __restrict__ cent,
+                                     const double* __restrict__ cn, int32_t C, int64_t q0, int32_t formula,
+                                     unsigned long long* __restrict__ key, int32_t* __restrict__ val) {
+  const int64_t qi = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= C) return;
+  const double* y = Q + (q0 + qi) * d;
+  const double* cc = cent + size_t(c) * d;
+  double sacc = 0.0;
+  if (formula == 0) {
+    for (int j = lane; j < d; j += 32) {
+      const double t = cc[j] - y[j];
+      sacc = fma(t, t, sacc);
+    }
+    sacc = warp_sum(sacc);
+  } else {
+    for (int j = lane; j < d; j += 32) sacc = fma(cc[j], y[j], sacc);
+    sacc = warp_sum(sacc);
+    sacc = sacc * -2.0 + cn[c];
+  }
+  if (lane == 0) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(sacc));
+    key[qi * C + c] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    val[qi * C + c] = c;
+  }
+}
+
+__global__ void take_probe_kernel(const int32_t* __restrict__ sval, int32_t C, int64_t q0, int64_t nqc,
+                                  int32_t n_probe, int32_t* __restrict__ probe) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nqc * n_probe) return;
+  const int64_t qi = i / n_probe, p = i % n_probe;
+  probe[(q0 + qi) * n_probe + p] = sval[qi * C + p];
+}
+
+__global__ void seg_starts_kernel(int64_t nqc, int32_t C, int64_t* __restrict__ seg) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i <= nqc) seg[i] = i * C;
+}
+
 size_t cub_bytes(int64_t n) {
   size_t a = 0, b = 0, c = 0;
   cub::DeviceReduce::Sum(nullptr, a, static_cast<const double*>(nullptr), static_cast<double*>(nullptr), n);
@@ -790,7 +834,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     int Bc = 2;
     while (Bc < v->C) Bc <<= 1;
     const size_t probe_smem = size_t(Bc) * sizeof(K128) + size_t(v->d) * sizeof(double);
-    DK_REQUIRE(probe_smem <= 232448, "n_clusters too large for the GPU probe (max 8192 at d <= 4096)");
+    const bool bigc = probe_smem > 232448;  // probe by a segmented radix sort instead
     int Kp = 32;
     while (Kp < k) Kp <<= 1;
     const int S = std::max(Kp, 256);  // rows per round (stage capacity)
@@ -825,10 +869,42 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       Qd = reinterpret_cast<const double*>(base + o_q);
     }
     int32_t* probe = reinterpret_cast<int32_t*>(base + o_p);
-    set_dynamic_smem(probe_kernel, probe_smem);
-    probe_kernel<<<unsigned(nq), 256, probe_smem, s>>>(Qd, v->d, v->cent, v->cnorm, v->C, Bc, n_probe, formula,
-                                                      probe);
-    DK_CHECK_LAUNCH();
+    if (!bigc) {
+      set_dynamic_smem(probe_kernel, probe_smem);
+      probe_kernel<<<unsigned(nq), 256, probe_smem, s>>>(Qd, v->d, v->cent, v->cnorm, v->C, Bc, n_probe, formula,
+                                                        probe);
+      DK_CHECK_LAUNCH();
+    } else {
+      const int64_t chunk = std::max<int64_t>(1, (int64_t(1) << 26) / v->C);
+      for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+        const int64_t nqc = std::min(chunk, nq - q0);
+        const int64_t T = nqc * v->C;
+        size_t sb = 0;
+        cub::DeviceSegmentedRadixSort::SortPairs(nullptr, sb, static_cast<const unsigned long long*>(nullptr),
+                                                 static_cast<unsigned long long*>(nullptr),
+                                                 static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                                 int(T), int(nqc), static_cast<const int64_t*>(nullptr),
+                                                 static_cast<const int64_t*>(nullptr));
+        DevBuf buf(size_t(T) * (8 + 8 + 4 + 4) + size_t(nqc + 1) * 8 + sb + 512);
+        auto* k0 = buf.as<unsigned long long>(0);
+        auto* k1 = buf.as<unsigned long long>(size_t(T) * 8);
+        auto* v0 = buf.as<int32_t>(size_t(T) * 16);
+        auto* v1 = buf.as<int32_t>(size_t(T) * 20);
+        auto* seg = buf.as<int64_t>((size_t(T) * 24 + 7) & ~size_t(7));
+        void* tmp = buf.as<uint8_t>((size_t(T) * 24 + size_t(nqc + 1) * 8 + 255 + 8) & ~size_t(255));
+        seg_starts_kernel<<<unsigned((nqc + 1 + 255) / 256), 256, 0, s>>>(nqc, v->C, seg);
+        DK_CHECK_LAUNCH();
+        dim3 grid(unsigned((v->C + 7) / 8), unsigned(nqc));
+        centroid_keys_kernel<<<grid, 256, 0, s>>>(Qd, v->d, v->cent, v->cnorm, v->C, q0, formula, k0, v0);
+        DK_CHECK_LAUNCH();
+        size_t tb = sb;
+        DK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, int(T), int(nqc), seg, seg + 1,
+                                                         0, 64, s));
+        take_probe_kernel<<<unsigned((nqc * n_probe + 255) / 256), 256, 0, s>>>(v1, v->C, q0, nqc, n_probe, probe);
+        DK_CHECK_LAUNCH();
+        DK_CUDA(cudaStreamSynchronize(s));
+      }
+    }
     const bool idev = is_device_ptr(idx_out), ddev = is_device_ptr(d2_out), cdev = is_device_ptr(cnt_out);
     int64_t* io = idev ? idx_out : reinterpret_cast<int64_t*>(base + o_i);
     double* dd = ddev ? d2_out : reinterpret_cast<double*>(base + o_d);

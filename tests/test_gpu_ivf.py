@@ -203,3 +203,28 @@ def test_large_k_beyond_the_shared_memory_top_k():
             ri, rd = O.ivf_query(od, cent, lists, q, k, p)
             np.testing.assert_array_equal(nl.indices, ri)
             np.testing.assert_allclose(nl.sq_distances, rd, rtol=1e-12, atol=1e-12)
+
+
+def test_many_clusters_probe_by_segmented_sort():
+    # n_clusters > 8192: the probe switches from the shared-memory sort to a radix sort
+    rng = np.random.default_rng(43)
+    n, d, C = 20_000, 4, 9000
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    cent = X[rng.choice(n, C, replace=False)].astype(np.float64)
+    cent[1] = cent[0]                                  # tied centroids: lower id first
+    lab = np.empty(n, dtype=np.int64)
+    for s in range(0, n, 2000):
+        d2 = O.centroid_sqdists(X[s:s + 2000].astype(np.float64), O.Data(X[s:s + 2000]).sq_norms, cent)
+        lab[s:s + 2000] = np.argmin(d2, axis=1)
+    lists = [np.flatnonzero(lab == c).astype(np.int64) for c in range(C)]
+    index = g.IvfIndex(centroids=cent, assignments=lists, seed=0)
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    Q = rng.normal(size=(5, d))
+    for q in np.vstack([Q, cent[:1]]):
+        for p in (1, 7, 40):
+            nl = g.ivf_query(index, ds, q, 10, p)
+            ri, rd = O.ivf_query(od, cent, lists, q, 10, p)
+            np.testing.assert_array_equal(nl.indices, ri)
+        ann = g.IvfAnnIndex(ds, index, 7)
+        ri, _ = O.ivf_query(od, cent, lists, q, 10, 7, formula=1)
+        np.testing.assert_array_equal(ann.query(q, 10).indices, ri)
