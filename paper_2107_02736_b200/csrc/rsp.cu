@@ -205,9 +205,9 @@ void launch_rsp_starts(const int64_t* pos, int32_t cnt, int64_t nq, int64_t n, i
 void launch_rsp_eval(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, int32_t family,
                      double bandwidth, const int64_t* pos, int32_t cnt, const int64_t* start, const int64_t* len,
                      double* z_sum, cudaStream_t s) {
-  const int wpb = 8;
+  const int wpb = int(std::max<int64_t>(1, std::min<int64_t>(8, 232448 / (int64_t(d) * 8))));
   const size_t smem = size_t(wpb) * d * sizeof(double);
-  if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the permuted sampler"};
+  if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the permuted sampler (d > 29000)"};
   const double c = family == DK_GAUSSIAN ? 1.0 / (2.0 * bandwidth * bandwidth) : 1.0 / bandwidth;
   const unsigned grid = unsigned((nq + wpb - 1) / wpb);
   const int chunks = (d + 3) / 4;

@@ -316,9 +316,10 @@ void launch_sample(const float* X, int64_t n_local, int64_t global_offset, int64
                    const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t m, uint64_t seed,
                    int64_t query_base, const int64_t* excl_sorted, const int32_t* excl_cnt, int32_t excl_stride,
                    double* z_sum, int64_t* acc_idx, int64_t* draws, cudaStream_t s) {
-  const int wpb = 8;
+  // 8 warps (queries) per block; fewer for very wide rows so the fp64 query copies fit
+  const int wpb = int(std::max<int64_t>(1, std::min<int64_t>(8, 232448 / (int64_t(d) * 8 + 256))));
   const size_t smem = size_t(wpb) * d * sizeof(double) + size_t(wpb) * 32 * sizeof(int64_t);
-  if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the sampling kernel"};
+  if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the sampling kernel (d > 29000)"};
   const double c = family_c(family, bandwidth);
   const unsigned grid = unsigned((nq + wpb - 1) / wpb);
   // lanes per row: enough that one float4 sweep of the row covers >= ~1/2 of its 16 B chunks
@@ -365,8 +366,9 @@ void launch_sort_excl(const int64_t* excl, const int32_t* excl_cnt, int32_t stri
 void launch_eval_rows(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q, int64_t nq,
                       int32_t family, double bandwidth, const int64_t* rows, const int32_t* cnt, int32_t stride,
                       double* out, cudaStream_t s) {
-  const int wpb = 8;
+  const int wpb = int(std::max<int64_t>(1, std::min<int64_t>(8, 232448 / (int64_t(d) * 8))));
   const size_t smem = size_t(wpb) * d * sizeof(double);
+  if (smem > 232448) throw Error{DK_EINVAL, "dimension too large for the row evaluation (d > 29000)"};
   set_dynamic_smem(eval_rows_kernel, smem);
   eval_rows_kernel<<<unsigned((nq + wpb - 1) / wpb), wpb * 32, smem, s>>>(
       X, n_local, global_offset, d, Q, nq, family, family_c(family, bandwidth), rows, cnt, stride, out);

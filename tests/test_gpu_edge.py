@@ -137,3 +137,24 @@ def test_integer_dataset_with_fractional_queries_and_duplicates():
     idx, _ = g.knn_batch(ds, Q, 40)
     for j in range(len(Q)):
         np.testing.assert_array_equal(idx[j], O.brute_force_knn(od, Q[j], 40)[0])
+
+
+def test_very_wide_rows():
+    # d = 4100: the split3 tile streams its A operand, the gather kernels run fewer queries per block
+    rng = np.random.default_rng(9)
+    n, d = 1500, 4100
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    Q = X[:4].astype(np.float64) + rng.normal(scale=0.5, size=(4, d))
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    for fam, h in (("gaussian", 40.0), ("exponential", 30.0), ("laplacian", 2000.0)):
+        got = g.naive_kde(ds, g.KernelSpec(fam, h), Q).values
+        assert _rel(got, O.naive_kde(od, fam, h, Q)) < KDE_RTOL, fam
+        vals, nbr, _ = g.deann_arrays(ds, g.KernelSpec(fam, h), Q, 10, 100, seed=3, export_neighbors=True)
+        for j in range(len(Q)):
+            ri, rd = O.brute_force_knn(od, Q[j], 10)
+            np.testing.assert_array_equal(nbr[j], ri)
+            ref = O.deann(od, fam, h, NeighborReplay(ri, rd), Q[j], 10, 100, rng=IndexReplay(3, j, n))[0]
+            assert vals[j] == pytest.approx(ref, rel=1e-12)
+    st, ost = g.RspState.from_dataset(ds, 2), O.Permuted(od, 2)
+    assert g.rsp_kde(st, g.KernelSpec("gaussian", 40.0), Q[0], 300).value == pytest.approx(
+        O.rsp_kde(ost, "gaussian", 40.0, Q[0], 300), rel=1e-12)
