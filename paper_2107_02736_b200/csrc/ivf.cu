@@ -17,6 +17,7 @@
 // Query (batched): per query the n_probe nearest centroids ((d2, id) order), then an
 // exact fp64 scan of the probed lists with a shared-memory top-k ((d2, row) order,
 // threshold-filtered), d2 = ((x.y) * -2 + |x|^2) + |y|^2 clamped at 0 (ann.py:224-229).
+#include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -43,6 +44,8 @@ struct dk_ivf {
   double* scal = nullptr;        // device scalars
   void* temp = nullptr;          // CUB scratch
   size_t temp_bytes = 0;
+  void* keys1 = nullptr;         // query scratch: phase-1 (d2, row) keys, grow-only
+  size_t keys1_bytes = 0;
   bool lists = false;
 };
 
@@ -312,7 +315,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs,
                                                    const int64_t* __restrict__ rows, const int64_t* __restrict__ off,
                                                    int32_t d, const int32_t* __restrict__ order,
                                                    const double* __restrict__ Q,
-                                                   const int32_t* __restrict__ probe, int32_t n_probe, int32_t k,
+                                                   const int32_t* __restrict__ probe, int32_t n_probe,
+                                                   const int32_t* __restrict__ np_q, int32_t k,
                                                    int32_t Kp, int32_t S, int32_t B, int64_t* __restrict__ idx_out,
                                                    double* __restrict__ d2_out, int32_t* __restrict__ cnt_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -350,7 +354,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const float* __restrict__ xs,
     }
   }
   int64_t total = 0;
-  for (int p = 0; p < n_probe; ++p) {
+  const int np = np_q ? np_q[q] : n_probe;  // np_q: scan only the leading probed lists
+  for (int p = 0; p < np; ++p) {
     const int c = probe[q * n_probe + p];
     const int64_t b = off[c], e = off[c + 1];
     total += e - b;
@@ -603,6 +608,295 @@ __global__ void seg_starts_kernel(int64_t nqc, int32_t C, int64_t* __restrict__ 
   if (i <= nqc) seg[i] = i * C;
 }
 
+// ---- two-phase probed k-NN (the default path):
+//  (1) per query, its nearest probed lists until they hold >= k rows: every (d2, row) key of
+//      those rows (list-major, pair_tile_kernel<0>), then their exact top-k (seg_topk_kernel)
+//      -> tau_q = that k-th key, an upper bound on the query's true k-th key over all its
+//      probed lists;
+//  (2) the remaining (list, query) pairs, list-major: keys < tau_q are appended to the
+//      query's candidate buffer (pair_tile_kernel<1>);
+//  (3) per query: top-k of (phase-1 top-k + appended keys) by (d2, row) (seg_topk_kernel).
+// Queries whose candidate buffer overflows are redone exactly, one block per (query, list).
+__global__ void prefix_probes_kernel(const int32_t* __restrict__ probe, const int64_t* __restrict__ off,
+                                     int64_t nq, int32_t n_probe, int32_t k, int32_t* __restrict__ np_q,
+                                     int32_t* __restrict__ cnt_all, int64_t* __restrict__ rows1) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int64_t all = 0, r1 = 0;
+  int p1 = n_probe;
+  for (int p = 0; p < n_probe; ++p) {
+    const int c = probe[q * n_probe + p];
+    all += off[c + 1] - off[c];
+    if (p1 == n_probe && all >= k) {
+      p1 = p + 1;
+      r1 = all;
+    }
+  }
+  if (p1 == n_probe) r1 = all;
+  np_q[q] = p1;
+  cnt_all[q] = int32_t(all < k ? all : k);
+  rows1[q] = r1;
+  if (q == nq - 1) rows1[nq] = 0;
+}
+
+__global__ void list_pairs_kernel(const int32_t* __restrict__ skey, int64_t npairs, int32_t C,
+                                  int64_t* __restrict__ pstart) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > C) return;
+  int64_t lo = 0, hi = npairs;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (skey[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  pstart[c] = lo;
+}
+
+__global__ void list_items_kernel(const int64_t* __restrict__ pstart, int32_t C, int32_t per,
+                                  int64_t* __restrict__ nitems) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > C) return;
+  nitems[c] = c < C ? (pstart[c + 1] - pstart[c] + per - 1) / per : 0;
+}
+
+// ---- tiled list-major pass (both phases): a work item is one list and up to PQ = 32 of the
+// (query, list) pairs that probe it.  4 warps x 8 queries; lane = 4 rows of a 128-row chunk.
+// Rows (as fp64) and query slices are staged DJ = 16 dimensions at a time, so every staged x
+// value feeds 8 fp64 FMAs and every broadcast query value 4, and the dot product of each
+// (query, row) is the same sequential fma chain over j = 0..d-1 as gather_cands_kernel.
+//   MODE 0 (phase 1): every key of the pair is written to the query's key segment.
+//   MODE 1 (phase 2): keys < tau_q are appended to the query's candidate buffer.
+constexpr int PQ = 32, PW = 8, PR = 4, PRC = 32 * PR, PDJ = 16;
+
+__global__ void query_norms_kernel(const double* __restrict__ Q, int64_t nq, int32_t d, double* __restrict__ yy) {
+  const int64_t q = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  double sy = 0.0;  // the order of scan_kernel
+  for (int j = lane; j < d; j += 32) sy = fma(Q[q * d + j], Q[q * d + j], sy);
+  sy = warp_sum(sy);
+  if (lane == 0) yy[q] = sy;
+}
+
+// bucket b < nb: (list b, phase 1); bucket nb + 1 + c: (list c, phase 2); pairs sorted by bucket
+__global__ void bucket_pairs_kernel(const int32_t* __restrict__ probe, const int32_t* __restrict__ np_q, int64_t nq,
+                                    int32_t n_probe, int32_t C, int32_t* __restrict__ key,
+                                    int32_t* __restrict__ val) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nq * n_probe) return;
+  const int64_t q = i / n_probe;
+  const int slot = int(i % n_probe);
+  key[i] = slot < np_q[q] ? probe[i] : C + 1 + probe[i];
+  val[i] = int32_t(i);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) pair_tile_kernel(
+    const float* __restrict__ xs, const double* __restrict__ xns, const int64_t* __restrict__ rows,
+    const int64_t* __restrict__ off, int32_t d, int32_t C, const double* __restrict__ Q,
+    const double* __restrict__ yyq, const int32_t* __restrict__ probe, int32_t n_probe,
+    const int32_t* __restrict__ sval, const int64_t* __restrict__ pstart, const int64_t* __restrict__ istart,
+    int32_t blo, int32_t bhi, const int64_t* __restrict__ qoff, K128* __restrict__ keys,
+    const K128* __restrict__ tau, int32_t cap, K128* __restrict__ cand, int32_t* __restrict__ ccnt) {
+  __shared__ double xr[PRC * (PDJ + 1)];
+  __shared__ double ys[PQ * PDJ];
+  __shared__ int64_t s_q[PQ], s_pos[PQ];
+  __shared__ double s_yy[PQ];
+  __shared__ K128 s_tau[PQ];
+  const int64_t i0 = istart[blo], item = i0 + blockIdx.x;
+  if (item >= istart[bhi]) return;
+  int lo = blo, hi = bhi - 1;  // bucket: istart[b] <= item < istart[b + 1]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (istart[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  const int bkt = lo;
+  const int c = MODE == 0 ? bkt : bkt - C - 1;
+  const int64_t p0 = pstart[bkt] + (item - istart[bkt]) * PQ;
+  const int np = int(min(pstart[bkt + 1] - p0, int64_t(PQ)));
+  const int64_t b = off[c], e = off[c + 1];
+  if (threadIdx.x < PQ) {
+    const int t = threadIdx.x;
+    int64_t q = -1, pos = 0;
+    if (t < np) {
+      const int64_t pr = sval[p0 + t];
+      q = pr / n_probe;
+      if (MODE == 0) {  // segment offset: the rows of the query's earlier leading lists
+        pos = qoff[q];
+        for (int64_t p = q * n_probe; p < pr; ++p) pos += off[probe[p] + 1] - off[probe[p]];
+      } else {
+        s_tau[t] = tau[q];
+      }
+      s_yy[t] = yyq[q];
+    }
+    s_q[t] = q;
+    s_pos[t] = pos;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r0 = b; r0 < e; r0 += PRC) {
+    const int rn = int(min(e - r0, int64_t(PRC)));
+    double acc[PW][PR];
+#pragma unroll
+    for (int t = 0; t < PW; ++t)
+#pragma unroll
+      for (int i = 0; i < PR; ++i) acc[t][i] = 0.0;
+    for (int j0 = 0; j0 < d; j0 += PDJ) {
+      const int dj = min(PDJ, d - j0);
+      __syncthreads();  // previous slice consumed (and s_q visible)
+      float xv[PRC * PDJ / 128];  // all loads of the slice in flight before the stores
+#pragma unroll
+      for (int u = 0; u < PRC * PDJ / 128; ++u) {
+        const int t = threadIdx.x + 128 * u, r = t / PDJ, jj = t % PDJ;
+        xv[u] = (r < rn && jj < dj) ? __ldg(xs + (r0 + r) * d + j0 + jj) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < PQ * PDJ / 128; ++u) {
+        const int t = threadIdx.x + 128 * u, qq = t / PDJ, jj = t % PDJ;
+        ys[t] = (qq < np && jj < dj) ? Q[s_q[qq] * d + j0 + jj] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PRC * PDJ / 128; ++u) {
+        const int t = threadIdx.x + 128 * u, r = t / PDJ, jj = t % PDJ;
+        xr[r * (PDJ + 1) + jj] = double(xv[u]);
+      }
+      __syncthreads();
+      for (int jj = 0; jj < dj; ++jj) {
+        double y[PW], x[PR];
+#pragma unroll
+        for (int t = 0; t < PW; ++t) y[t] = ys[(warp * PW + t) * PDJ + jj];
+#pragma unroll
+        for (int i = 0; i < PR; ++i) x[i] = xr[(lane + 32 * i) * (PDJ + 1) + jj];
+#pragma unroll
+        for (int t = 0; t < PW; ++t)
+#pragma unroll
+          for (int i = 0; i < PR; ++i) acc[t][i] = fma(x[i], y[t], acc[t][i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PR; ++i) {
+      const int r = lane + 32 * i;
+      if (r >= rn) continue;
+      const double xn = xns[r0 + r];
+      const unsigned long long id = static_cast<unsigned long long>(rows[r0 + r]);
+#pragma unroll
+      for (int t = 0; t < PW; ++t) {
+        const int qq = warp * PW + t;
+        if (qq >= np) continue;
+        double v = acc[t][i] * -2.0;
+        v += xn;
+        v += s_yy[qq];
+        v = fmax(v, 0.0);
+        const K128 key{static_cast<unsigned long long>(__double_as_longlong(v)), id};
+        if (MODE == 0) {
+          keys[s_pos[qq] + (r0 - b) + r] = key;
+        } else if (k_less(key, s_tau[qq])) {
+          const int64_t q = s_q[qq];
+          const int slot = atomicAdd(&ccnt[q], 1);
+          if (slot < cap) cand[q * cap + slot] = key;
+        }
+      }
+    }
+  }
+}
+
+// per query: top-k by (d2, row) of an optional sorted head (idx/d2, c1 entries) and a key
+// segment, through a shared-memory buffer of NB keys (chunks of the segment when it is larger)
+__global__ void seg_topk_kernel(const int64_t* __restrict__ hidx, const double* __restrict__ hd2,
+                                const int32_t* __restrict__ hcnt, const K128* __restrict__ seg,
+                                const int64_t* __restrict__ seg_off, int64_t seg_stride,
+                                const int32_t* __restrict__ seg_cnt, int32_t seg_cap, int32_t NB, int32_t k,
+                                const int32_t* __restrict__ cnt_valid, int64_t* __restrict__ idx_out,
+                                double* __restrict__ d2_out, int32_t* __restrict__ cnt_out,
+                                K128* __restrict__ tau_out, int32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K128* buf = reinterpret_cast<K128*>(smem_raw);
+  const int64_t q = blockIdx.x;
+  const int64_t n = seg_off ? seg_off[q + 1] - seg_off[q] : int64_t(seg_cnt[q]);
+  const K128* src = seg + (seg_off ? seg_off[q] : q * seg_stride);
+  if (overflow) {
+    if (n > seg_cap) {  // redone separately
+      if (threadIdx.x == 0) overflow[q] = 1;
+      return;
+    }
+    if (threadIdx.x == 0) overflow[q] = 0;
+  }
+  int filled = hcnt ? hcnt[q] : 0;
+  for (int i = threadIdx.x; i < filled; i += blockDim.x)
+    buf[i] = K128{static_cast<unsigned long long>(__double_as_longlong(hd2[q * k + i])),
+                  static_cast<unsigned long long>(hidx[q * k + i])};
+  int64_t pos = 0;
+  do {
+    const int take = int(min(n - pos, int64_t(NB - filled)));
+    const int tot = filled + take;
+    int B = 2;
+    while (B < tot) B <<= 1;
+    for (int i = threadIdx.x; i < B - filled; i += blockDim.x)
+      buf[filled + i] = i < take ? src[pos + i] : K128{~0ull, ~0ull};
+    bitonic(buf, B);
+    pos += take;
+    filled = min(tot, k);
+  } while (pos < n);
+  const int cnt = cnt_valid ? cnt_valid[q] : filled;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const bool ok = i < cnt;
+    idx_out[q * k + i] = ok ? static_cast<int64_t>(buf[i].lo) : -1;
+    d2_out[q * k + i] = ok ? __longlong_as_double(static_cast<long long>(buf[i].hi))
+                           : __longlong_as_double(0x7ff0000000000000ll);
+  }
+  if (threadIdx.x == 0) {
+    cnt_out[q] = cnt;
+    if (tau_out) tau_out[q] = cnt == k ? buf[k - 1] : K128{~0ull, ~0ull};
+  }
+}
+
+// overflowed queries: one virtual query per (query, probed list) -- the query row copied, a
+// single-list probe -- scanned block-parallel, then the per-list top-k merged per query
+__global__ void redo_split_kernel(const int32_t* __restrict__ redo, int64_t nr, const double* __restrict__ Q,
+                                  int32_t d, const int32_t* __restrict__ probe, int32_t n_probe,
+                                  double* __restrict__ Qv, int32_t* __restrict__ pv) {
+  const int64_t v = blockIdx.x;  // virtual query = redo slot * n_probe + list slot
+  if (v >= nr * n_probe) return;
+  const int64_t q = redo[v / n_probe];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) Qv[v * d + j] = Q[q * d + j];
+  if (threadIdx.x == 0) pv[v] = probe[q * n_probe + v % n_probe];
+}
+
+__global__ void redo_merge_kernel(const int32_t* __restrict__ redo, int32_t n_probe, int32_t k,
+                                  const int64_t* __restrict__ iv, const double* __restrict__ dv,
+                                  const int32_t* __restrict__ cv, const int32_t* __restrict__ cnt_all,
+                                  int64_t* __restrict__ idx_out, double* __restrict__ d2_out,
+                                  int32_t* __restrict__ cnt_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K128* buf = reinterpret_cast<K128*>(smem_raw);
+  __shared__ int s_off;
+  const int64_t r = blockIdx.x;
+  const int64_t q = redo[r];
+  if (threadIdx.x == 0) s_off = 0;
+  __syncthreads();
+  int B = 2;
+  while (B < n_probe * k) B <<= 1;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) buf[i] = K128{~0ull, ~0ull};
+  __syncthreads();
+  for (int p = 0; p < n_probe; ++p) {  // concatenate the per-list top-k
+    const int64_t v = r * n_probe + p;
+    const int c = cv[v], o = s_off;
+    for (int i = threadIdx.x; i < c; i += blockDim.x)
+      buf[o + i] = K128{static_cast<unsigned long long>(__double_as_longlong(dv[v * k + i])),
+                        static_cast<unsigned long long>(iv[v * k + i])};
+    __syncthreads();
+    if (threadIdx.x == 0) s_off = o + c;
+    __syncthreads();
+  }
+  bitonic(buf, B);
+  const int cnt = cnt_all[q];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const bool ok = i < cnt;
+    idx_out[q * k + i] = ok ? static_cast<int64_t>(buf[i].lo) : -1;
+    d2_out[q * k + i] = ok ? __longlong_as_double(static_cast<long long>(buf[i].hi))
+                           : __longlong_as_double(0x7ff0000000000000ll);
+  }
+  if (threadIdx.x == 0) cnt_out[q] = cnt;
+}
+
 size_t cub_bytes(int64_t n) {
   size_t a = 0, b = 0, c = 0;
   cub::DeviceReduce::Sum(nullptr, a, static_cast<const double*>(nullptr), static_cast<double*>(nullptr), n);
@@ -618,7 +912,7 @@ void free_ivf(dk_ivf* v) {
                   static_cast<void*>(v->cdf), static_cast<void*>(v->labels), static_cast<void*>(v->labels_s),
                   static_cast<void*>(v->ids), static_cast<void*>(v->rows), static_cast<void*>(v->offsets),
                   static_cast<void*>(v->d2min), static_cast<void*>(v->xs), static_cast<void*>(v->xns),
-                  static_cast<void*>(v->scal), v->temp})
+                  static_cast<void*>(v->scal), v->temp, v->keys1})
     if (p) cudaFree(p);
   delete v;
 }
@@ -861,6 +1155,59 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
                                     static_cast<int32_t*>(nullptr), int(nq));
     const size_t o_k0 = take(size_t(nq) * 4), o_k1 = take(size_t(nq) * 4), o_v0 = take(size_t(nq) * 4);
     const size_t o_ord = take(size_t(nq) * 4), o_ot = take(ord_bytes + 256);
+    // two-phase plan (see pair_tile_kernel)
+    static const bool one_phase = std::getenv("DK_IVF_ONE_PHASE") != nullptr;  // A/B switch
+    const int64_t npairs = nq * int64_t(n_probe);
+    const int32_t NBK = 2 * v->C + 2;  // pair buckets: phase-1 lists, a gap, phase-2 lists
+    const bool two_phase = !bigk && !one_phase && n_probe > 1 && npairs < (int64_t(1) << 31);
+    int64_t cap_rows = std::max<int64_t>(2048, 16 * int64_t(k));
+    if (const char* e = std::getenv("DK_IVF_CAP")) cap_rows = std::max<int64_t>(1, std::atoll(e));  // tests
+    const int32_t cap = int32_t(std::min<int64_t>(int64_t(1) << 20, cap_rows));
+    int NB = 2048;  // seg_topk_kernel buffer: at least twice the top-k
+    while (NB < 2 * Kp) NB <<= 1;
+    size_t cub2 = 0;
+    size_t o_i1 = 0, o_d1 = 0, o_c1 = 0, o_np = 0, o_ca = 0, o_tau = 0, o_kin = 0, o_kout = 0, o_vin = 0,
+           o_vout = 0, o_ps = 0, o_ni = 0, o_is = 0, o_t2 = 0, o_cc = 0, o_cand = 0, o_ov = 0, o_rq = 0, o_rQ = 0,
+           o_ri = 0, o_rd = 0, o_rp = 0, o_rc = 0, o_yy = 0, o_r1 = 0, o_qo = 0;
+    int64_t redo_R = 0;
+    if (two_phase) {
+      size_t a = 0, b2 = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const int32_t*>(nullptr),
+                                      static_cast<int32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+                                      static_cast<int32_t*>(nullptr), int(npairs));
+      cub::DeviceScan::ExclusiveSum(nullptr, b2, static_cast<const int64_t*>(nullptr),
+                                    static_cast<int64_t*>(nullptr), std::max<int64_t>(NBK + 1, nq + 1));
+      cub2 = std::max(a, b2) + 256;
+      o_i1 = take(size_t(nq) * k * 8);
+      o_d1 = take(size_t(nq) * k * 8);
+      o_c1 = take(size_t(nq) * 4);
+      o_np = take(size_t(nq) * 4);
+      o_ca = take(size_t(nq) * 4);
+      o_tau = take(size_t(nq) * sizeof(K128));
+      o_yy = take(size_t(nq) * 8);
+      o_r1 = take(size_t(nq + 1) * 8);
+      o_qo = take(size_t(nq + 1) * 8);
+      o_kin = take(size_t(npairs) * 4);
+      o_kout = take(size_t(npairs) * 4);
+      o_vin = take(size_t(npairs) * 4);
+      o_vout = take(size_t(npairs) * 4);
+      o_ps = take(size_t(NBK + 1) * 8);
+      o_ni = take(size_t(NBK + 1) * 8);
+      o_is = take(size_t(NBK + 1) * 8);
+      o_t2 = take(cub2);
+      o_cc = take(size_t(nq) * 4);
+      o_cand = take(size_t(nq) * cap * sizeof(K128));
+      o_ov = take(size_t(nq) * 4);
+      // overflow redo in chunks of R queries (see redo_merge_kernel)
+      const size_t per = size_t(n_probe) * (size_t(v->d) * 8 + size_t(k) * 16 + 8) + 4;
+      redo_R = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nq, 1024), int64_t((64u << 20) / per)));
+      o_rq = take(size_t(redo_R) * 4);
+      o_rQ = take(size_t(redo_R) * n_probe * v->d * 8);
+      o_ri = take(size_t(redo_R) * n_probe * k * 8);
+      o_rd = take(size_t(redo_R) * n_probe * k * 8);
+      o_rp = take(size_t(redo_R) * n_probe * 4);
+      o_rc = take(size_t(redo_R) * n_probe * 4);
+    }
     h->ws.reserve(off);
     uint8_t* base = h->ws.base;
     const double* Qd = Q;
@@ -928,21 +1275,145 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       DK_CUDA(cub::DeviceRadixSort::SortPairs(base + o_ot, tb, kin, kout, vin, order, int(nq), 0, bits, s));
     }
     const bool vec = (v->d & 3) == 0;
+    // per-query scan over all probed lists (np_q == nullptr) or a per-query prefix of them, of the
+    // queries Qs with probe lists ps (npr per query), taken in the order ord (nullptr: 0..count-1)
+    auto scan_with = [&](const double* Qs, const int32_t* ps, int32_t npr, const int32_t* ord, int64_t count,
+                         int64_t* oi, double* od2, int32_t* oc, const int32_t* np_q = nullptr) {
 #define DK_SCAN(G, IT)                                                                                       \
   do {                                                                                                       \
     set_dynamic_smem(scan_kernel<G, IT>, scan_smem);                                                         \
-    scan_kernel<G, IT><<<unsigned(nq), 256, scan_smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, order, \
-                                                           Qd, probe, n_probe, k, Kp, S, B, io, dd, co);     \
+    scan_kernel<G, IT><<<unsigned(count), 256, scan_smem, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, ord, \
+                                                              Qs, ps, npr, np_q, k, Kp, S, B, oi, od2, oc); \
   } while (0)
-    // register-resident query slices where a row is at most 4 float4 steps per lane (G < 32)
-    if (chunks >= 64) DK_SCAN(32, 0);
-    else if (chunks >= 32) { if (vec) DK_SCAN(16, 4); else DK_SCAN(16, 0); }
-    else if (chunks >= 16) { if (vec) DK_SCAN(8, 4); else DK_SCAN(8, 0); }
-    else if (chunks >= 8) { if (vec) DK_SCAN(4, 4); else DK_SCAN(4, 0); }
-    else if (chunks >= 4) { if (vec) DK_SCAN(2, 4); else DK_SCAN(2, 0); }
-    else { if (vec) DK_SCAN(1, 4); else DK_SCAN(1, 0); }
+      // register-resident query slices where a row is at most 4 float4 steps per lane (G < 32)
+      if (chunks >= 64) DK_SCAN(32, 0);
+      else if (chunks >= 32) { if (vec) DK_SCAN(16, 4); else DK_SCAN(16, 0); }
+      else if (chunks >= 16) { if (vec) DK_SCAN(8, 4); else DK_SCAN(8, 0); }
+      else if (chunks >= 8) { if (vec) DK_SCAN(4, 4); else DK_SCAN(4, 0); }
+      else if (chunks >= 4) { if (vec) DK_SCAN(2, 4); else DK_SCAN(2, 0); }
+      else { if (vec) DK_SCAN(1, 4); else DK_SCAN(1, 0); }
 #undef DK_SCAN
-    DK_CHECK_LAUNCH();
+      DK_CHECK_LAUNCH();
+    };
+    auto run_scan = [&](const int32_t* ord, int64_t count, const int32_t* np_q, int64_t* oi, double* od2,
+                        int32_t* oc) { scan_with(Qd, probe, n_probe, ord, count, oi, od2, oc, np_q); };
+    if (!two_phase) {
+      run_scan(order, nq, nullptr, io, dd, co);
+    } else {
+      auto* idx1 = reinterpret_cast<int64_t*>(base + o_i1);
+      auto* d21 = reinterpret_cast<double*>(base + o_d1);
+      auto* cnt1 = reinterpret_cast<int32_t*>(base + o_c1);
+      auto* npq = reinterpret_cast<int32_t*>(base + o_np);
+      auto* call = reinterpret_cast<int32_t*>(base + o_ca);
+      auto* tau = reinterpret_cast<K128*>(base + o_tau);
+      auto* kin = reinterpret_cast<int32_t*>(base + o_kin);
+      auto* kout = reinterpret_cast<int32_t*>(base + o_kout);
+      auto* vin = reinterpret_cast<int32_t*>(base + o_vin);
+      auto* vout = reinterpret_cast<int32_t*>(base + o_vout);
+      auto* ps = reinterpret_cast<int64_t*>(base + o_ps);
+      auto* ni = reinterpret_cast<int64_t*>(base + o_ni);
+      auto* is = reinterpret_cast<int64_t*>(base + o_is);
+      auto* ccnt = reinterpret_cast<int32_t*>(base + o_cc);
+      auto* cand = reinterpret_cast<K128*>(base + o_cand);
+      auto* ovf = reinterpret_cast<int32_t*>(base + o_ov);
+      auto* yyq = reinterpret_cast<double*>(base + o_yy);
+      auto* rows1 = reinterpret_cast<int64_t*>(base + o_r1);
+      auto* qoff = reinterpret_cast<int64_t*>(base + o_qo);
+      // (1) per query: the leading probed lists holding >= k rows, their row count
+      prefix_probes_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(probe, v->offsets, nq, n_probe, k, npq, call,
+                                                                       rows1);
+      DK_CHECK_LAUNCH();
+      query_norms_kernel<<<unsigned((nq + 7) / 8), 256, 0, s>>>(Qd, nq, v->d, yyq);
+      DK_CHECK_LAUNCH();
+      size_t tb = cub2;
+      DK_CUDA(cub::DeviceScan::ExclusiveSum(base + o_t2, tb, rows1, qoff, nq + 1, s));
+      // (list, query) pairs bucketed by phase and list
+      bucket_pairs_kernel<<<unsigned((npairs + 255) / 256), 256, 0, s>>>(probe, npq, nq, n_probe, v->C, kin, vin);
+      DK_CHECK_LAUNCH();
+      int bits = 1;
+      while ((int64_t(1) << bits) < int64_t(NBK)) ++bits;
+      tb = cub2;
+      DK_CUDA(cub::DeviceRadixSort::SortPairs(base + o_t2, tb, kin, kout, vin, vout, int(npairs), 0, bits, s));
+      list_pairs_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(kout, npairs, NBK, ps);
+      DK_CHECK_LAUNCH();
+      list_items_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(ps, NBK, PQ, ni);
+      DK_CHECK_LAUNCH();
+      tb = cub2;
+      DK_CUDA(cub::DeviceScan::ExclusiveSum(base + o_t2, tb, ni, is, NBK + 1, s));
+      int64_t tot1 = 0;
+      DK_CUDA(cudaMemcpyAsync(&tot1, qoff + nq, 8, cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaStreamSynchronize(s));
+      const size_t kbytes = size_t(std::max<int64_t>(tot1, 1)) * sizeof(K128);
+      if (kbytes > v->keys1_bytes) {
+        if (v->keys1) DK_CUDA(cudaFree(v->keys1));
+        v->keys1 = nullptr;
+        v->keys1_bytes = 0;
+        DK_CUDA(cudaMalloc(&v->keys1, kbytes));
+        v->keys1_bytes = kbytes;
+      }
+      auto* keys1 = static_cast<K128*>(v->keys1);
+      const unsigned grid = unsigned(npairs / PQ + v->C + 1);  // upper bound on the items of a phase
+      // (2) every key of the leading lists, then the exact top-k of each query -> tau_q
+      pair_tile_kernel<0><<<grid, 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe, n_probe,
+                                               vout, ps, is, 0, v->C, qoff, keys1, nullptr, 0, nullptr, nullptr);
+      DK_CHECK_LAUNCH();
+      const size_t tsm = size_t(NB) * sizeof(K128);
+      set_dynamic_smem(seg_topk_kernel, tsm);
+      seg_topk_kernel<<<unsigned(nq), 256, tsm, s>>>(nullptr, nullptr, nullptr, keys1, qoff, 0, nullptr, 0, NB, k,
+                                                     nullptr, idx1, d21, cnt1, tau, nullptr);
+      DK_CHECK_LAUNCH();
+      // (3) the remaining pairs: keys below tau_q into the query's candidate buffer
+      DK_CUDA(cudaMemsetAsync(ccnt, 0, size_t(nq) * 4, s));
+      pair_tile_kernel<1><<<grid, 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe, n_probe,
+                                               vout, ps, is, v->C + 1, NBK - 1, nullptr, nullptr, tau, cap, cand,
+                                               ccnt);
+      DK_CHECK_LAUNCH();
+      // (4) top-k of the phase-1 top-k and the candidates
+      seg_topk_kernel<<<unsigned(nq), 256, tsm, s>>>(idx1, d21, cnt1, cand, nullptr, cap, ccnt, cap, NB, k, call, io,
+                                                     dd, co, nullptr, ovf);
+      DK_CHECK_LAUNCH();
+      std::vector<int32_t> ov(static_cast<size_t>(nq));
+      DK_CUDA(cudaMemcpyAsync(ov.data(), ovf, size_t(nq) * 4, cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaStreamSynchronize(s));
+      std::vector<int32_t> redo;
+      for (int64_t q = 0; q < nq; ++q)
+        if (ov[size_t(q)]) redo.push_back(int32_t(q));
+      if (std::getenv("DK_IVF_DEBUG")) {
+        std::vector<int32_t> cc(static_cast<size_t>(nq));
+        DK_CUDA(cudaMemcpy(cc.data(), ccnt, size_t(nq) * 4, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> srt(cc);
+        std::sort(srt.begin(), srt.end());
+        fprintf(stderr, "ivf two-phase: redo %zu, cand p50 %d p90 %d p99 %d max %d\n", redo.size(),
+                srt[srt.size() / 2], srt[srt.size() * 9 / 10], srt[srt.size() * 99 / 100], srt.back());
+      }
+      // candidate buffer overflowed (queries far from every list, whose tau_q passes most rows):
+      // each (query, probed list) pair as its own block-parallel scan, then a per-query merge
+      const bool split = int64_t(n_probe) * k <= 8192;
+      for (size_t r0 = 0; r0 < redo.size(); r0 += size_t(split ? redo_R : int64_t(redo.size()))) {
+        const int64_t nr = int64_t(std::min(redo.size() - r0, size_t(split ? redo_R : int64_t(redo.size()))));
+        auto* rq = reinterpret_cast<int32_t*>(split ? base + o_rq : base + o_ord);
+        DK_CUDA(cudaMemcpyAsync(rq, redo.data() + r0, size_t(nr) * 4, cudaMemcpyHostToDevice, s));
+        if (!split) {  // n_probe * k beyond the merge buffer: one block per query
+          run_scan(rq, nr, nullptr, io, dd, co);
+          continue;
+        }
+        auto* Qv = reinterpret_cast<double*>(base + o_rQ);
+        auto* pv = reinterpret_cast<int32_t*>(base + o_rp);
+        auto* iv = reinterpret_cast<int64_t*>(base + o_ri);
+        auto* dv = reinterpret_cast<double*>(base + o_rd);
+        auto* cv = reinterpret_cast<int32_t*>(base + o_rc);
+        const int64_t nv = nr * n_probe;
+        redo_split_kernel<<<unsigned(nv), 128, 0, s>>>(rq, nr, Qd, v->d, probe, n_probe, Qv, pv);
+        DK_CHECK_LAUNCH();
+        scan_with(Qv, pv, 1, nullptr, nv, iv, dv, cv);
+        int Bv = 2;
+        while (Bv < n_probe * k) Bv <<= 1;
+        set_dynamic_smem(redo_merge_kernel, size_t(Bv) * sizeof(K128));
+        redo_merge_kernel<<<unsigned(nr), 256, size_t(Bv) * sizeof(K128), s>>>(rq, n_probe, k, iv, dv, cv, call, io,
+                                                                               dd, co);
+        DK_CHECK_LAUNCH();
+      }
+    }
     }
     if (!idev) DK_CUDA(cudaMemcpyAsync(idx_out, io, size_t(nq) * k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     if (!ddev) DK_CUDA(cudaMemcpyAsync(d2_out, dd, size_t(nq) * k * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -228,3 +228,25 @@ def test_many_clusters_probe_by_segmented_sort():
         ann = g.IvfAnnIndex(ds, index, 7)
         ri, _ = O.ivf_query(od, cent, lists, q, 10, 7, formula=1)
         np.testing.assert_array_equal(ann.query(q, 10).indices, ri)
+
+
+@pytest.mark.parametrize("cap", [None, "1", "40"])
+def test_two_phase_overflow_redo_for_far_queries(cap, monkeypatch):
+    # queries far from every list pass many rows of the other probed lists under their phase-1
+    # threshold; a candidate buffer that overflows (forced small with DK_IVF_CAP) sends the
+    # query to the exact redo path
+    if cap is not None:
+        monkeypatch.setenv("DK_IVF_CAP", cap)
+    rng = np.random.default_rng(47)
+    n, d, C = 40_000, 12, 8
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    Q = np.vstack([rng.normal(size=(6, d)), 60.0 * rng.normal(size=(6, d))])
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    index = g.ivf_build(ds, C, seed=3)
+    cent, lists = O.ivf_build(od, C, 3)
+    for k, p in ((10, 6), (100, 8)):
+        idx, d2, cnt = g.ivf_query_batch(index, ds, Q, k, p)
+        for j in range(len(Q)):
+            ri, rd = O.ivf_query(od, cent, lists, Q[j], k, p)
+            np.testing.assert_array_equal(idx[j, :cnt[j]], ri)
+            np.testing.assert_allclose(d2[j, :cnt[j]], rd, rtol=1e-12)
