@@ -18,6 +18,7 @@
 // exact fp64 scan of the probed lists with a shared-memory top-k ((d2, row) order,
 // threshold-filtered), d2 = ((x.y) * -2 + |x|^2) + |y|^2 clamped at 0 (ann.py:224-229).
 #include <algorithm>
+#include <climits>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -46,6 +47,8 @@ struct dk_ivf {
   size_t temp_bytes = 0;
   void* keys1 = nullptr;         // query scratch: phase-1 (d2, row) keys, grow-only
   size_t keys1_bytes = 0;
+  void* ckeys = nullptr;         // query scratch: centroid distance keys [queries][C], grow-only
+  size_t ckeys_bytes = 0;
   bool lists = false;
 };
 
@@ -265,46 +268,6 @@ __global__ void gather_rows_kernel(const float* __restrict__ X, const double* __
 }
 
 // ---------------------------------------------------------------- query
-
-// n_probe nearest centroids per query, (d2, id) order.  formula 0: sum (c - y)^2
-// (ivf_query, ann.py:212-214); formula 1: (C y) * -2 + |c|^2 (IvfAnnIndex._probe_clusters,
-// ann.py:262-275).  Block per query, bitonic over pow2(C) keys in shared memory.
-__global__ void probe_kernel(const double* __restrict__ Q, int32_t d, const double* __restrict__ cent,
-                             const double* __restrict__ cn, int32_t C, int32_t Bc, int32_t n_probe,
-                             int32_t formula, int32_t* __restrict__ probe) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  K128* keys = reinterpret_cast<K128*>(smem_raw);
-  double* y = reinterpret_cast<double*>(keys + Bc);
-  const int64_t q = blockIdx.x;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) y[j] = Q[q * d + j];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int c = warp; c < Bc; c += nw) {
-    K128 k{~0ull, ~0ull};
-    if (c < C) {
-      double s = 0.0;
-      const double* cc = cent + size_t(c) * d;
-      if (formula == 0) {
-        for (int j = lane; j < d; j += 32) {
-          const double t = cc[j] - y[j];
-          s = fma(t, t, s);
-        }
-        s = warp_sum(s);
-      } else {
-        for (int j = lane; j < d; j += 32) s = fma(cc[j], y[j], s);
-        s = warp_sum(s);
-        s = s * -2.0 + cn[c];
-      }
-      // order-preserving map of a signed double onto unsigned bits
-      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(s));
-      k.hi = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-      k.lo = static_cast<unsigned long long>(c);
-    }
-    if (lane == 0) keys[c] = k;
-  }
-  bitonic(keys, Bc);
-  for (int i = threadIdx.x; i < n_probe; i += blockDim.x) probe[q * n_probe + i] = int32_t(keys[i].lo);
-}
 
 // Exact scan of the probed lists with a (d2, row) top-k in shared memory.  Rounds of
 // S rows: G lanes per row (float4 loads, fp64 FMA, G-lane shuffle reduction), rows
@@ -603,6 +566,128 @@ __global__ void take_probe_kernel(const int32_t* __restrict__ sval, int32_t C, i
   probe[(q0 + qi) * n_probe + p] = sval[qi * C + p];
 }
 
+// Probe: the n_probe nearest centroids per query in (distance, id) order.  formula 0:
+// sum (c - y)^2 (ivf_query, ann.py:212-214); formula 1: (C y) * -2 + |c|^2
+// (IvfAnnIndex._probe_clusters, ann.py:262-275).
+// Tiled: every (query, centroid) distance of a query chunk as an order-preserving key
+// (32 queries x 128 centroids per block, staged 16 dimensions at a time, each distance the
+// sequential fma chain over j), then the n_probe smallest (key, centroid id) per query.
+constexpr int CQ = 32, CW = 8, CR = 4, CRC = 32 * CR, CDJ = 16;
+
+__device__ __forceinline__ unsigned long long order_key(double v) {  // signed double -> ordered bits
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <int FORMULA>
+__global__ void __launch_bounds__(128) centroid_tile_kernel(const double* __restrict__ Q, int64_t q0, int64_t nqc,
+                                                            int32_t d, const double* __restrict__ cent,
+                                                            const double* __restrict__ cn, int32_t C,
+                                                            unsigned long long* __restrict__ keys) {
+  __shared__ double cr[CRC * (CDJ + 1)];
+  __shared__ double ys[CQ * CDJ];
+  const int c0 = blockIdx.x * CRC;
+  const int64_t qb = int64_t(blockIdx.y) * CQ;  // within the chunk
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[CW][CR];
+#pragma unroll
+  for (int t = 0; t < CW; ++t)
+#pragma unroll
+    for (int i = 0; i < CR; ++i) acc[t][i] = 0.0;
+  for (int j0 = 0; j0 < d; j0 += CDJ) {
+    const int dj = min(CDJ, d - j0);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < CRC * CDJ / 128; ++u) {
+      const int t = threadIdx.x + 128 * u, r = t / CDJ, jj = t % CDJ;
+      cr[r * (CDJ + 1) + jj] = (c0 + r < C && jj < dj) ? cent[int64_t(c0 + r) * d + j0 + jj] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CQ * CDJ / 128; ++u) {
+      const int t = threadIdx.x + 128 * u, qq = t / CDJ, jj = t % CDJ;
+      ys[t] = (qb + qq < nqc && jj < dj) ? Q[(q0 + qb + qq) * d + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+    for (int jj = 0; jj < dj; ++jj) {
+      double y[CW], x[CR];
+#pragma unroll
+      for (int t = 0; t < CW; ++t) y[t] = ys[(warp * CW + t) * CDJ + jj];
+#pragma unroll
+      for (int i = 0; i < CR; ++i) x[i] = cr[(lane + 32 * i) * (CDJ + 1) + jj];
+#pragma unroll
+      for (int t = 0; t < CW; ++t)
+#pragma unroll
+        for (int i = 0; i < CR; ++i) {
+          if (FORMULA == 0) {
+            const double df = x[i] - y[t];
+            acc[t][i] = fma(df, df, acc[t][i]);
+          } else {
+            acc[t][i] = fma(x[i], y[t], acc[t][i]);
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < CW; ++t) {
+    const int64_t qq = qb + warp * CW + t;
+    if (qq >= nqc) continue;
+#pragma unroll
+    for (int i = 0; i < CR; ++i) {
+      const int c = c0 + lane + 32 * i;
+      if (c >= C) continue;
+      const double v = FORMULA == 0 ? acc[t][i] : acc[t][i] * -2.0 + cn[c];
+      keys[qq * C + c] = order_key(v);
+    }
+  }
+}
+
+// n_probe <= 64: warp per query, n_probe rounds of "smallest (key, id) above the previous one"
+__global__ void probe_select_kernel(const unsigned long long* __restrict__ keys, int64_t q0, int64_t nqc,
+                                    int32_t C, int32_t n_probe, int32_t* __restrict__ probe) {
+  const int64_t qq = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (qq >= nqc) return;
+  const unsigned long long* kq = keys + qq * C;
+  unsigned long long pk = 0ull;
+  int pc = -1;
+  for (int r = 0; r < n_probe; ++r) {
+    unsigned long long bk = ~0ull;
+    int bc = INT_MAX;
+    for (int c = lane; c < C; c += 32) {
+      const unsigned long long kv = kq[c];
+      const bool above = kv > pk || (kv == pk && c > pc);
+      if (above && (kv < bk || (kv == bk && c < bc))) {
+        bk = kv;
+        bc = c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ok < bk || (ok == bk && oc < bc)) {
+        bk = ok;
+        bc = oc;
+      }
+    }
+    if (lane == 0) probe[(q0 + qq) * n_probe + r] = bc;
+    pk = bk;
+    pc = bc;
+  }
+}
+
+// n_probe > 64: block per query, bitonic over pow2(C) (key, id) pairs
+__global__ void probe_sort_kernel(const unsigned long long* __restrict__ keys, int64_t q0, int32_t C, int32_t Bc,
+                                  int32_t n_probe, int32_t* __restrict__ probe) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K128* buf = reinterpret_cast<K128*>(smem_raw);
+  const int64_t qq = blockIdx.x;
+  for (int c = threadIdx.x; c < Bc; c += blockDim.x)
+    buf[c] = c < C ? K128{keys[qq * C + c], static_cast<unsigned long long>(c)} : K128{~0ull, ~0ull};
+  bitonic(buf, Bc);
+  for (int i = threadIdx.x; i < n_probe; i += blockDim.x) probe[(q0 + qq) * n_probe + i] = int32_t(buf[i].lo);
+}
+
 __global__ void seg_starts_kernel(int64_t nqc, int32_t C, int64_t* __restrict__ seg) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i <= nqc) seg[i] = i * C;
@@ -819,11 +904,84 @@ __global__ void seg_topk_kernel(const int64_t* __restrict__ hidx, const double* 
     }
     if (threadIdx.x == 0) overflow[q] = 0;
   }
-  int filled = hcnt ? hcnt[q] : 0;
-  for (int i = threadIdx.x; i < filled; i += blockDim.x)
-    buf[i] = K128{static_cast<unsigned long long>(__double_as_longlong(hd2[q * k + i])),
-                  static_cast<unsigned long long>(hidx[q * k + i])};
+  const int c1 = hcnt ? hcnt[q] : 0;
+  auto head = [&](int i) {
+    return K128{static_cast<unsigned long long>(__double_as_longlong(hd2[q * k + i])),
+                static_cast<unsigned long long>(hidx[q * k + i])};
+  };
+  int filled = c1;
   int64_t pos = 0;
+  if (c1 + n > 1024 && c1 + n >= k) {
+    // selection: a 2048-bin histogram of the d2 bits (monotone for d2 >= 0) between the
+    // smallest and largest key; every key in the bins up to the k-th key's bin is kept
+    __shared__ unsigned long long s_mn, s_mx;
+    __shared__ int s_hist[2048], s_m, s_bin;
+    if (threadIdx.x == 0) {
+      s_mn = ~0ull;
+      s_mx = 0ull;
+      s_m = 0;
+    }
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (int i = threadIdx.x; i < c1; i += blockDim.x) {
+      const unsigned long long h = head(i).hi;
+      mn = h < mn ? h : mn;
+      mx = h > mx ? h : mx;
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long h = src[i].hi;
+      mn = h < mn ? h : mn;
+      mx = h > mx ? h : mx;
+    }
+    atomicMin(&s_mn, mn);
+    atomicMax(&s_mx, mx);
+    __syncthreads();
+    mn = s_mn;
+    const unsigned long long span = s_mx - mn;
+    const int shift = span == 0 ? 0 : max(0, 64 - __clzll(static_cast<long long>(span)) - 11);
+    for (int i = threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&s_hist[(head(i).hi - mn) >> shift], 1);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&s_hist[(src[i].hi - mn) >> shift], 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // bin of the k-th key: warp scan over 64 bins per lane
+      const int l = threadIdx.x;
+      int sum = 0;
+      for (int i = 0; i < 64; ++i) sum += s_hist[l * 64 + i];
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += t;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= k);
+      const int L = __ffs(hit) - 1;
+      if (l == L) {
+        int cum = incl - sum, b = l * 64;
+        while (cum + s_hist[b] < k) cum += s_hist[b++];
+        s_bin = b;
+        s_m = cum + s_hist[b];
+      }
+    }
+    __syncthreads();
+    if (s_m <= NB) {
+      const unsigned long long lim = static_cast<unsigned long long>(s_bin);
+      if (threadIdx.x == 0) s_m = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < c1; i += blockDim.x) {
+        const K128 v = head(i);
+        if (((v.hi - mn) >> shift) <= lim) buf[atomicAdd(&s_m, 1)] = v;
+      }
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const K128 v = src[i];
+        if (((v.hi - mn) >> shift) <= lim) buf[atomicAdd(&s_m, 1)] = v;
+      }
+      __syncthreads();
+      filled = s_m;
+      pos = n;  // every candidate is in buf: one sort below
+    }
+  }
+  if (pos == 0)
+    for (int i = threadIdx.x; i < c1; i += blockDim.x) buf[i] = head(i);
   do {
     const int take = int(min(n - pos, int64_t(NB - filled)));
     const int tot = filled + take;
@@ -912,7 +1070,7 @@ void free_ivf(dk_ivf* v) {
                   static_cast<void*>(v->cdf), static_cast<void*>(v->labels), static_cast<void*>(v->labels_s),
                   static_cast<void*>(v->ids), static_cast<void*>(v->rows), static_cast<void*>(v->offsets),
                   static_cast<void*>(v->d2min), static_cast<void*>(v->xs), static_cast<void*>(v->xns),
-                  static_cast<void*>(v->scal), v->temp, v->keys1})
+                  static_cast<void*>(v->scal), v->temp, v->keys1, v->ckeys})
     if (p) cudaFree(p);
   delete v;
 }
@@ -1217,10 +1375,33 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     }
     int32_t* probe = reinterpret_cast<int32_t*>(base + o_p);
     if (!bigc) {
-      set_dynamic_smem(probe_kernel, probe_smem);
-      probe_kernel<<<unsigned(nq), 256, probe_smem, s>>>(Qd, v->d, v->cent, v->cnorm, v->C, Bc, n_probe, formula,
-                                                        probe);
-      DK_CHECK_LAUNCH();
+      const int64_t chunk = std::max<int64_t>(CQ, std::min<int64_t>(nq, (int64_t(1) << 24) / v->C));
+      const size_t cbytes = size_t(chunk) * v->C * 8;
+      if (cbytes > v->ckeys_bytes) {
+        if (v->ckeys) DK_CUDA(cudaFree(v->ckeys));
+        v->ckeys = nullptr;
+        v->ckeys_bytes = 0;
+        DK_CUDA(cudaMalloc(&v->ckeys, cbytes));
+        v->ckeys_bytes = cbytes;
+      }
+      auto* ck = static_cast<unsigned long long*>(v->ckeys);
+      for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+        const int64_t nqc = std::min(chunk, nq - q0);
+        const dim3 grid(unsigned((v->C + CRC - 1) / CRC), unsigned((nqc + CQ - 1) / CQ));
+        if (formula == 0)
+          centroid_tile_kernel<0><<<grid, 128, 0, s>>>(Qd, q0, nqc, v->d, v->cent, v->cnorm, v->C, ck);
+        else
+          centroid_tile_kernel<1><<<grid, 128, 0, s>>>(Qd, q0, nqc, v->d, v->cent, v->cnorm, v->C, ck);
+        DK_CHECK_LAUNCH();
+        if (n_probe <= 64) {
+          probe_select_kernel<<<unsigned((nqc + 7) / 8), 256, 0, s>>>(ck, q0, nqc, v->C, n_probe, probe);
+        } else {
+          const size_t psm = size_t(Bc) * sizeof(K128);
+          set_dynamic_smem(probe_sort_kernel, psm);
+          probe_sort_kernel<<<unsigned(nqc), 256, psm, s>>>(ck, q0, v->C, Bc, n_probe, probe);
+        }
+        DK_CHECK_LAUNCH();
+      }
     } else {
       const int64_t chunk = std::max<int64_t>(1, (int64_t(1) << 26) / v->C);
       for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
