@@ -25,6 +25,7 @@
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 struct dk_ivf {
   dk_dataset* ds = nullptr;
@@ -736,11 +737,21 @@ __global__ void list_pairs_kernel(const int32_t* __restrict__ skey, int64_t npai
   pstart[c] = lo;
 }
 
-__global__ void list_items_kernel(const int64_t* __restrict__ pstart, int32_t C, int32_t per,
-                                  int64_t* __restrict__ nitems) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > C) return;
-  nitems[c] = c < C ? (pstart[c + 1] - pstart[c] + per - 1) / per : 0;
+// rows per work item of the list-major passes (long lists are split so no item trails)
+constexpr int64_t kSpan = 1024;
+
+// items of bucket b (list b for b < C, list b - C - 1 for b > C): query groups x row spans
+__global__ void list_items_kernel(const int64_t* __restrict__ pstart, const int64_t* __restrict__ off, int32_t C,
+                                  int32_t nb, int32_t per, int64_t* __restrict__ nitems) {
+  const int bk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bk > nb) return;
+  const int c = bk < C ? bk : bk - C - 1;
+  if (bk == nb || bk == C || c >= C) {
+    nitems[bk] = 0;
+    return;
+  }
+  const int64_t span = (off[c + 1] - off[c] + kSpan - 1) / kSpan;
+  nitems[bk] = (pstart[bk + 1] - pstart[bk] + per - 1) / per * span;
 }
 
 // ---- tiled list-major pass (both phases): a work item is one list and up to PQ = 32 of the
@@ -796,9 +807,12 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
   }
   const int bkt = lo;
   const int c = MODE == 0 ? bkt : bkt - C - 1;
-  const int64_t p0 = pstart[bkt] + (item - istart[bkt]) * PQ;
+  // item = (query group, row span) of the bucket, spans of kSpan rows
+  const int64_t lb = off[c], le = off[c + 1];
+  const int64_t nspan = (le - lb + kSpan - 1) / kSpan, local = item - istart[bkt];
+  const int64_t p0 = pstart[bkt] + (local / nspan) * PQ;
   const int np = int(min(pstart[bkt + 1] - p0, int64_t(PQ)));
-  const int64_t b = off[c], e = off[c + 1];
+  const int64_t b = lb + (local % nspan) * kSpan, e = min(le, b + kSpan);
   if (threadIdx.x < PQ) {
     const int t = threadIdx.x;
     int64_t q = -1, pos = 0;
@@ -844,6 +858,7 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
         xr[r * (PDJ + 1) + jj] = double(xv[u]);
       }
       __syncthreads();
+      if (warp * PW >= np) continue;  // no query on this warp (it still stages)
       for (int jj = 0; jj < dj; ++jj) {
         double y[PW], x[PR];
 #pragma unroll
@@ -872,7 +887,7 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
         v = fmax(v, 0.0);
         const K128 key{static_cast<unsigned long long>(__double_as_longlong(v)), id};
         if (MODE == 0) {
-          keys[s_pos[qq] + (r0 - b) + r] = key;
+          keys[s_pos[qq] + (r0 - lb) + r] = key;
         } else if (k_less(key, s_tau[qq])) {
           const int64_t q = s_q[qq];
           const int slot = atomicAdd(&ccnt[q], 1);
@@ -880,6 +895,167 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
         }
       }
     }
+  }
+}
+
+// Phase 2 on packed fp32 FMAs (FFMA2) with an exact fp64 re-check.  The fp32 dot
+// dot_f = sum x_j * fl32(y_j) (sequential chain) satisfies |dot_f - x.y| <= (d + 1) u |x||y|
+// (u = 2^-24: the rounding of y plus the chain), so with d2_f = |x|^2 + |y|^2 - 2 dot_f
+// (fp32, each operand rounding <= u times |x|^2 + |y|^2 + 2|x.y| <= 2(|x|^2 + |y|^2))
+//   d2 <= tau  =>  d2_f <= tau + 2.05 (d + 1) u |x||y| + 10 u (|x|^2 + |y|^2 + tau);
+// rows passing that test are re-evaluated exactly (the fp64 chain of pair_tile_kernel) and
+// appended when their (d2, row) key is below tau_q.  32 queries x 256 rows per step, lane =
+// 8 rows x 8 queries, x staged row-major (stride 33, conflict-free), y staged as {y, y}.
+constexpr int FQ = 32, FW = 8, FR = 8, FRC = 32 * FR, FDJ = 16;
+constexpr size_t kFilterSmem = size_t(FRC) * (FDJ + 1) * 4 + size_t(4) * FW * FRC * 2;
+static_assert(FQ == PQ, "phase-2 items are built with PQ queries each");
+
+__global__ void __launch_bounds__(128, 4) pair_filter_f32_kernel(
+    const float* __restrict__ xs, const double* __restrict__ xns, const int64_t* __restrict__ rows,
+    const int64_t* __restrict__ off, int32_t d, int32_t C, const double* __restrict__ Q,
+    const double* __restrict__ yyq, int32_t n_probe, const int32_t* __restrict__ sval,
+    const int64_t* __restrict__ pstart, const int64_t* __restrict__ istart, int32_t blo, int32_t bhi,
+    const K128* __restrict__ tau, int32_t cap, K128* __restrict__ cand, int32_t* __restrict__ ccnt) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* xr = reinterpret_cast<float*>(smem_raw);                                    // [FRC][FDJ + 1]
+  uint16_t* s_queue = reinterpret_cast<uint16_t*>(xr + FRC * (FDJ + 1));             // [4][FW * FRC]
+  __shared__ __align__(16) float2 ys[FDJ * FQ];  // [jj][query] = {y, y}
+  __shared__ int64_t s_q[FQ];
+  __shared__ double s_yy[FQ];
+  __shared__ K128 s_tau[FQ];
+  __shared__ float s_A[FQ], s_P[FQ];
+  const int64_t i0 = istart[blo], item = i0 + blockIdx.x;
+  if (item >= istart[bhi]) return;
+  int lo = blo, hi = bhi - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (istart[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  const int bkt = lo, c = bkt - C - 1;
+  // item = (query group, row span) of the bucket, spans of kSpan rows
+  const int64_t lb = off[c], le = off[c + 1];
+  const int64_t nspan = (le - lb + kSpan - 1) / kSpan, local = item - istart[bkt];
+  const int64_t p0 = pstart[bkt] + (local / nspan) * FQ;
+  const int np = int(min(pstart[bkt + 1] - p0, int64_t(FQ)));
+  const int64_t b = lb + (local % nspan) * kSpan, e = min(le, b + kSpan);
+  constexpr float u = 5.9604645e-8f;  // 2^-24
+  if (threadIdx.x < FQ) {
+    const int t = threadIdx.x;
+    int64_t q = -1;
+    float A = 0.f, P = -INFINITY;  // inactive slots pass nothing
+    if (t < np) {
+      q = int64_t(sval[p0 + t]) / n_probe;
+      const K128 tq = tau[q];
+      const double yy = yyq[q];
+      s_tau[t] = tq;
+      s_yy[t] = yy;
+      if (tq.hi == ~0ull) {  // no threshold: every row passes
+        A = 0.f;
+        P = INFINITY;
+      } else {
+        const float tf = __double2float_ru(__longlong_as_double(static_cast<long long>(tq.hi)));
+        const float yf = __double2float_rn(yy);
+        A = 2.05f * float(d + 1) * u * sqrtf(yf) * 1.0001f;
+        P = tf + 10.f * u * (yf + tf) - yf;  // test: -2 dot_f <= A |x| + P + 10 u |x|^2 - |x|^2
+      }
+    }
+    s_q[t] = q;
+    s_A[t] = A;
+    s_P[t] = P;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint16_t* queue = s_queue + warp * FW * FRC;
+  for (int64_t r0 = b; r0 < e; r0 += FRC) {
+    const int rn = int(min(e - r0, int64_t(FRC)));
+    float2 acc[FW][FR / 2];
+#pragma unroll
+    for (int t = 0; t < FW; ++t)
+#pragma unroll
+      for (int i = 0; i < FR / 2; ++i) acc[t][i] = make_float2(0.f, 0.f);
+    for (int j0 = 0; j0 < d; j0 += FDJ) {
+      const int dj = min(FDJ, d - j0);
+      __syncthreads();
+#pragma unroll 4
+      for (int u4 = 0; u4 < FRC * FDJ / 128; u4 += 16) {
+        float xv[16];
+#pragma unroll
+        for (int w = 0; w < 16; ++w) {
+          const int t = threadIdx.x + 128 * (u4 + w), r = t / FDJ, jj = t % FDJ;
+          xv[w] = (r < rn && jj < dj) ? __ldg(xs + (r0 + r) * d + j0 + jj) : 0.f;
+        }
+#pragma unroll
+        for (int w = 0; w < 16; ++w) {
+          const int t = threadIdx.x + 128 * (u4 + w), r = t / FDJ, jj = t % FDJ;
+          xr[r * (FDJ + 1) + jj] = xv[w];
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < FQ * FDJ / 128; ++w) {
+        const int t = threadIdx.x + 128 * w, jj = t / FQ, qq = t % FQ;
+        const float y = (qq < np && jj < dj) ? __double2float_rn(Q[s_q[qq] * d + j0 + jj]) : 0.f;
+        ys[t] = make_float2(y, y);
+      }
+      __syncthreads();
+      if (warp * FW >= np) continue;  // no query on this warp (it still stages)
+      for (int jj = 0; jj < dj; ++jj) {
+        const float4* y4 = reinterpret_cast<const float4*>(ys + jj * FQ + warp * FW);
+        float2 y[FW];
+#pragma unroll
+        for (int t = 0; t < FW / 2; ++t) {
+          const float4 v = y4[t];
+          y[2 * t] = make_float2(v.x, v.y);
+          y[2 * t + 1] = make_float2(v.z, v.w);
+        }
+        float2 x[FR / 2];
+#pragma unroll
+        for (int i = 0; i < FR / 2; ++i)
+          x[i] = make_float2(xr[(lane + 64 * i) * (FDJ + 1) + jj], xr[(lane + 64 * i + 32) * (FDJ + 1) + jj]);
+#pragma unroll
+        for (int t = 0; t < FW; ++t)
+#pragma unroll
+          for (int i = 0; i < FR / 2; ++i) acc[t][i] = fma2(x[i], y[t], acc[t][i]);
+      }
+    }
+    // approximate test, survivors queued per warp as (query slot, row)
+    int qn = 0;
+#pragma unroll
+    for (int i = 0; i < FR; ++i) {
+      const int r = lane + 64 * (i >> 1) + 32 * (i & 1);
+      const bool rv = r < rn;
+      const double xn = rv ? xns[r0 + r] : 0.0;
+      const float xf = float(xn), xnorm = sqrtf(xf);
+      const float R = 10.f * u * xf - xf;
+#pragma unroll
+      for (int t = 0; t < FW; ++t) {
+        const int qq = warp * FW + t;
+        const float dot = (i & 1) ? acc[t][i >> 1].y : acc[t][i >> 1].x;
+        const bool pass = rv && (-2.f * dot <= fmaf(s_A[qq], xnorm, s_P[qq] + R));
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (pass) queue[qn + __popc(m & ((1u << lane) - 1u))] = uint16_t((t << 8) | r);
+        qn += __popc(m);
+      }
+    }
+    __syncwarp();
+    // exact re-check, one queued pair per lane
+    for (int k2 = lane; k2 < qn; k2 += 32) {
+      const int ent = queue[k2], t = ent >> 8, r = ent & 255, qq = warp * FW + t;
+      const int64_t q = s_q[qq], pos = r0 + r;
+      const float* x = xs + pos * d;
+      const double* y = Q + q * d;
+      double dot = 0.0;
+      for (int j = 0; j < d; ++j) dot = fma(double(__ldg(x + j)), y[j], dot);
+      double v = dot * -2.0;
+      v += xns[pos];
+      v += s_yy[qq];
+      v = fmax(v, 0.0);
+      const K128 key{static_cast<unsigned long long>(__double_as_longlong(v)),
+                     static_cast<unsigned long long>(rows[pos])};
+      if (k_less(key, s_tau[qq])) {
+        const int slot = atomicAdd(&ccnt[q], 1);
+        if (slot < cap) cand[q * cap + slot] = key;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -1517,13 +1693,16 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       DK_CUDA(cub::DeviceRadixSort::SortPairs(base + o_t2, tb, kin, kout, vin, vout, int(npairs), 0, bits, s));
       list_pairs_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(kout, npairs, NBK, ps);
       DK_CHECK_LAUNCH();
-      list_items_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(ps, NBK, PQ, ni);
+      list_items_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(ps, v->offsets, v->C, NBK, PQ, ni);
       DK_CHECK_LAUNCH();
       tb = cub2;
       DK_CUDA(cub::DeviceScan::ExclusiveSum(base + o_t2, tb, ni, is, NBK + 1, s));
-      int64_t tot1 = 0;
+      int64_t tot1 = 0, items1 = 0, items2 = 0;  // phase-1 keys, items of either phase
       DK_CUDA(cudaMemcpyAsync(&tot1, qoff + nq, 8, cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaMemcpyAsync(&items1, is + v->C, 8, cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaMemcpyAsync(&items2, is + (NBK - 1), 8, cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaStreamSynchronize(s));
+      items2 -= items1;
       const size_t kbytes = size_t(std::max<int64_t>(tot1, 1)) * sizeof(K128);
       if (kbytes > v->keys1_bytes) {
         if (v->keys1) DK_CUDA(cudaFree(v->keys1));
@@ -1533,9 +1712,9 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
         v->keys1_bytes = kbytes;
       }
       auto* keys1 = static_cast<K128*>(v->keys1);
-      const unsigned grid = unsigned(npairs / PQ + v->C + 1);  // upper bound on the items of a phase
       // (2) every key of the leading lists, then the exact top-k of each query -> tau_q
-      pair_tile_kernel<0><<<grid, 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe, n_probe,
+      if (items1 > 0)
+        pair_tile_kernel<0><<<unsigned(items1), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe, n_probe,
                                                vout, ps, is, 0, v->C, qoff, keys1, nullptr, 0, nullptr, nullptr);
       DK_CHECK_LAUNCH();
       const size_t tsm = size_t(NB) * sizeof(K128);
@@ -1545,9 +1724,19 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       DK_CHECK_LAUNCH();
       // (3) the remaining pairs: keys below tau_q into the query's candidate buffer
       DK_CUDA(cudaMemsetAsync(ccnt, 0, size_t(nq) * 4, s));
-      pair_tile_kernel<1><<<grid, 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe, n_probe,
-                                               vout, ps, is, v->C + 1, NBK - 1, nullptr, nullptr, tau, cap, cand,
-                                               ccnt);
+      static const bool f64_filter = std::getenv("DK_IVF_F64_FILTER") != nullptr;  // A/B switch
+      if (f64_filter) {
+        if (items2 > 0)
+          pair_tile_kernel<1><<<unsigned(items2), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe,
+                                                 n_probe, vout, ps, is, v->C + 1, NBK - 1, nullptr, nullptr, tau, cap,
+                                                 cand, ccnt);
+      } else {
+        set_dynamic_smem(pair_filter_f32_kernel, kFilterSmem);
+        if (items2 > 0)
+          pair_filter_f32_kernel<<<unsigned(items2), 128, kFilterSmem, s>>>(
+            v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, n_probe, vout, ps, is, v->C + 1, NBK - 1, tau,
+            cap, cand, ccnt);
+      }
       DK_CHECK_LAUNCH();
       // (4) top-k of the phase-1 top-k and the candidates
       seg_topk_kernel<<<unsigned(nq), 256, tsm, s>>>(idx1, d21, cnt1, cand, nullptr, cap, ccnt, cap, NB, k, call, io,
