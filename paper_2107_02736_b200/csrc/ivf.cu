@@ -737,12 +737,10 @@ __global__ void list_pairs_kernel(const int32_t* __restrict__ skey, int64_t npai
   pstart[c] = lo;
 }
 
-// rows per work item of the list-major passes (long lists are split so no item trails)
-constexpr int64_t kSpan = 1024;
-
 // items of bucket b (list b for b < C, list b - C - 1 for b > C): query groups x row spans
+// of `span` rows (long lists are split so no item trails)
 __global__ void list_items_kernel(const int64_t* __restrict__ pstart, const int64_t* __restrict__ off, int32_t C,
-                                  int32_t nb, int32_t per, int64_t* __restrict__ nitems) {
+                                  int32_t nb, int32_t per, int32_t span, int64_t* __restrict__ nitems) {
   const int bk = blockIdx.x * blockDim.x + threadIdx.x;
   if (bk > nb) return;
   const int c = bk < C ? bk : bk - C - 1;
@@ -750,8 +748,8 @@ __global__ void list_items_kernel(const int64_t* __restrict__ pstart, const int6
     nitems[bk] = 0;
     return;
   }
-  const int64_t span = (off[c + 1] - off[c] + kSpan - 1) / kSpan;
-  nitems[bk] = (pstart[bk + 1] - pstart[bk] + per - 1) / per * span;
+  const int64_t ns = (off[c + 1] - off[c] + span - 1) / span;
+  nitems[bk] = (pstart[bk + 1] - pstart[bk] + per - 1) / per * ns;
 }
 
 // ---- tiled list-major pass (both phases): a work item is one list and up to PQ = 32 of the
@@ -791,7 +789,7 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
     const int64_t* __restrict__ off, int32_t d, int32_t C, const double* __restrict__ Q,
     const double* __restrict__ yyq, const int32_t* __restrict__ probe, int32_t n_probe,
     const int32_t* __restrict__ sval, const int64_t* __restrict__ pstart, const int64_t* __restrict__ istart,
-    int32_t blo, int32_t bhi, const int64_t* __restrict__ qoff, K128* __restrict__ keys,
+    int32_t blo, int32_t bhi, int32_t span, const int64_t* __restrict__ qoff, K128* __restrict__ keys,
     const K128* __restrict__ tau, int32_t cap, K128* __restrict__ cand, int32_t* __restrict__ ccnt) {
   __shared__ double xr[PRC * (PDJ + 1)];
   __shared__ double ys[PQ * PDJ];
@@ -807,12 +805,12 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
   }
   const int bkt = lo;
   const int c = MODE == 0 ? bkt : bkt - C - 1;
-  // item = (query group, row span) of the bucket, spans of kSpan rows
+  // item = (query group, row span) of the bucket, spans of `span` rows
   const int64_t lb = off[c], le = off[c + 1];
-  const int64_t nspan = (le - lb + kSpan - 1) / kSpan, local = item - istart[bkt];
+  const int64_t nspan = (le - lb + span - 1) / span, local = item - istart[bkt];
   const int64_t p0 = pstart[bkt] + (local / nspan) * PQ;
   const int np = int(min(pstart[bkt + 1] - p0, int64_t(PQ)));
-  const int64_t b = lb + (local % nspan) * kSpan, e = min(le, b + kSpan);
+  const int64_t b = lb + (local % nspan) * span, e = min(le, b + span);
   if (threadIdx.x < PQ) {
     const int t = threadIdx.x;
     int64_t q = -1, pos = 0;
@@ -914,7 +912,7 @@ __global__ void __launch_bounds__(128, 4) pair_filter_f32_kernel(
     const float* __restrict__ xs, const double* __restrict__ xns, const int64_t* __restrict__ rows,
     const int64_t* __restrict__ off, int32_t d, int32_t C, const double* __restrict__ Q,
     const double* __restrict__ yyq, int32_t n_probe, const int32_t* __restrict__ sval,
-    const int64_t* __restrict__ pstart, const int64_t* __restrict__ istart, int32_t blo, int32_t bhi,
+    const int64_t* __restrict__ pstart, const int64_t* __restrict__ istart, int32_t blo, int32_t bhi, int32_t span,
     const K128* __restrict__ tau, int32_t cap, K128* __restrict__ cand, int32_t* __restrict__ ccnt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* xr = reinterpret_cast<float*>(smem_raw);                                    // [FRC][FDJ + 1]
@@ -932,12 +930,12 @@ __global__ void __launch_bounds__(128, 4) pair_filter_f32_kernel(
     if (istart[mid] <= item) lo = mid; else hi = mid - 1;
   }
   const int bkt = lo, c = bkt - C - 1;
-  // item = (query group, row span) of the bucket, spans of kSpan rows
+  // item = (query group, row span) of the bucket, spans of `span` rows
   const int64_t lb = off[c], le = off[c + 1];
-  const int64_t nspan = (le - lb + kSpan - 1) / kSpan, local = item - istart[bkt];
+  const int64_t nspan = (le - lb + span - 1) / span, local = item - istart[bkt];
   const int64_t p0 = pstart[bkt] + (local / nspan) * FQ;
   const int np = int(min(pstart[bkt + 1] - p0, int64_t(FQ)));
-  const int64_t b = lb + (local % nspan) * kSpan, e = min(le, b + kSpan);
+  const int64_t b = lb + (local % nspan) * span, e = min(le, b + span);
   constexpr float u = 5.9604645e-8f;  // 2^-24
   if (threadIdx.x < FQ) {
     const int t = threadIdx.x;
@@ -1182,53 +1180,30 @@ __global__ void seg_topk_kernel(const int64_t* __restrict__ hidx, const double* 
   }
 }
 
-// overflowed queries: one virtual query per (query, probed list) -- the query row copied, a
-// single-list probe -- scanned block-parallel, then the per-list top-k merged per query
-__global__ void redo_split_kernel(const int32_t* __restrict__ redo, int64_t nr, const double* __restrict__ Q,
-                                  int32_t d, const int32_t* __restrict__ probe, int32_t n_probe,
-                                  double* __restrict__ Qv, int32_t* __restrict__ pv) {
-  const int64_t v = blockIdx.x;  // virtual query = redo slot * n_probe + list slot
-  if (v >= nr * n_probe) return;
-  const int64_t q = redo[v / n_probe];
-  for (int j = threadIdx.x; j < d; j += blockDim.x) Qv[v * d + j] = Q[q * d + j];
-  if (threadIdx.x == 0) pv[v] = probe[q * n_probe + v % n_probe];
+// overflowed queries: compacted (query row, probe list), every probed key through the
+// list-major pass, the per-query top-k, and the answers scattered back
+__global__ void redo_compact_kernel(const int32_t* __restrict__ redo, int64_t nr, const double* __restrict__ Q,
+                                    int32_t d, const int32_t* __restrict__ probe, int32_t n_probe,
+                                    double* __restrict__ Qr, int32_t* __restrict__ pr) {
+  const int64_t i = blockIdx.x;
+  if (i >= nr) return;
+  const int64_t q = redo[i];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) Qr[i * d + j] = Q[q * d + j];
+  for (int p = threadIdx.x; p < n_probe; p += blockDim.x) pr[i * n_probe + p] = probe[q * n_probe + p];
 }
 
-__global__ void redo_merge_kernel(const int32_t* __restrict__ redo, int32_t n_probe, int32_t k,
-                                  const int64_t* __restrict__ iv, const double* __restrict__ dv,
-                                  const int32_t* __restrict__ cv, const int32_t* __restrict__ cnt_all,
-                                  int64_t* __restrict__ idx_out, double* __restrict__ d2_out,
-                                  int32_t* __restrict__ cnt_out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  K128* buf = reinterpret_cast<K128*>(smem_raw);
-  __shared__ int s_off;
-  const int64_t r = blockIdx.x;
-  const int64_t q = redo[r];
-  if (threadIdx.x == 0) s_off = 0;
-  __syncthreads();
-  int B = 2;
-  while (B < n_probe * k) B <<= 1;
-  for (int i = threadIdx.x; i < B; i += blockDim.x) buf[i] = K128{~0ull, ~0ull};
-  __syncthreads();
-  for (int p = 0; p < n_probe; ++p) {  // concatenate the per-list top-k
-    const int64_t v = r * n_probe + p;
-    const int c = cv[v], o = s_off;
-    for (int i = threadIdx.x; i < c; i += blockDim.x)
-      buf[o + i] = K128{static_cast<unsigned long long>(__double_as_longlong(dv[v * k + i])),
-                        static_cast<unsigned long long>(iv[v * k + i])};
-    __syncthreads();
-    if (threadIdx.x == 0) s_off = o + c;
-    __syncthreads();
+__global__ void redo_scatter_kernel(const int32_t* __restrict__ redo, int64_t nr, int32_t k,
+                                    const int64_t* __restrict__ ir, const double* __restrict__ dr,
+                                    const int32_t* __restrict__ cr, int64_t* __restrict__ io,
+                                    double* __restrict__ dd, int32_t* __restrict__ co) {
+  const int64_t i = blockIdx.x;
+  if (i >= nr) return;
+  const int64_t q = redo[i];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    io[q * k + j] = ir[i * k + j];
+    dd[q * k + j] = dr[i * k + j];
   }
-  bitonic(buf, B);
-  const int cnt = cnt_all[q];
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    const bool ok = i < cnt;
-    idx_out[q * k + i] = ok ? static_cast<int64_t>(buf[i].lo) : -1;
-    d2_out[q * k + i] = ok ? __longlong_as_double(static_cast<long long>(buf[i].hi))
-                           : __longlong_as_double(0x7ff0000000000000ll);
-  }
-  if (threadIdx.x == 0) cnt_out[q] = cnt;
+  if (threadIdx.x == 0) co[q] = cr[i];
 }
 
 size_t cub_bytes(int64_t n) {
@@ -1502,7 +1477,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     size_t cub2 = 0;
     size_t o_i1 = 0, o_d1 = 0, o_c1 = 0, o_np = 0, o_ca = 0, o_tau = 0, o_kin = 0, o_kout = 0, o_vin = 0,
            o_vout = 0, o_ps = 0, o_ni = 0, o_is = 0, o_t2 = 0, o_cc = 0, o_cand = 0, o_ov = 0, o_rq = 0, o_rQ = 0,
-           o_ri = 0, o_rd = 0, o_rp = 0, o_rc = 0, o_yy = 0, o_r1 = 0, o_qo = 0;
+           o_rp = 0, o_yy = 0, o_r1 = 0, o_qo = 0;
     int64_t redo_R = 0;
     if (two_phase) {
       size_t a = 0, b2 = 0;
@@ -1532,15 +1507,11 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       o_cc = take(size_t(nq) * 4);
       o_cand = take(size_t(nq) * cap * sizeof(K128));
       o_ov = take(size_t(nq) * 4);
-      // overflow redo in chunks of R queries (see redo_merge_kernel)
-      const size_t per = size_t(n_probe) * (size_t(v->d) * 8 + size_t(k) * 16 + 8) + 4;
-      redo_R = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nq, 1024), int64_t((64u << 20) / per)));
+      // overflow redo in chunks of R queries (compacted query rows and probe lists)
+      redo_R = std::min<int64_t>(nq, 1024);
       o_rq = take(size_t(redo_R) * 4);
-      o_rQ = take(size_t(redo_R) * n_probe * v->d * 8);
-      o_ri = take(size_t(redo_R) * n_probe * k * 8);
-      o_rd = take(size_t(redo_R) * n_probe * k * 8);
+      o_rQ = take(size_t(redo_R) * v->d * 8);
       o_rp = take(size_t(redo_R) * n_probe * 4);
-      o_rc = take(size_t(redo_R) * n_probe * 4);
     }
     h->ws.reserve(off);
     uint8_t* base = h->ws.base;
@@ -1684,6 +1655,10 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       DK_CHECK_LAUNCH();
       size_t tb = cub2;
       DK_CUDA(cub::DeviceScan::ExclusiveSum(base + o_t2, tb, rows1, qoff, nq + 1, s));
+      static const int span = [] {  // rows per list-major work item
+        const char* e = std::getenv("DK_IVF_SPAN");
+        return e ? std::max(128, std::atoi(e)) : 512;
+      }();
       // (list, query) pairs bucketed by phase and list
       bucket_pairs_kernel<<<unsigned((npairs + 255) / 256), 256, 0, s>>>(probe, npq, nq, n_probe, v->C, kin, vin);
       DK_CHECK_LAUNCH();
@@ -1693,7 +1668,8 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       DK_CUDA(cub::DeviceRadixSort::SortPairs(base + o_t2, tb, kin, kout, vin, vout, int(npairs), 0, bits, s));
       list_pairs_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(kout, npairs, NBK, ps);
       DK_CHECK_LAUNCH();
-      list_items_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(ps, v->offsets, v->C, NBK, PQ, ni);
+      list_items_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(ps, v->offsets, v->C, NBK, PQ, span,
+                                                                         ni);
       DK_CHECK_LAUNCH();
       tb = cub2;
       DK_CUDA(cub::DeviceScan::ExclusiveSum(base + o_t2, tb, ni, is, NBK + 1, s));
@@ -1715,7 +1691,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       // (2) every key of the leading lists, then the exact top-k of each query -> tau_q
       if (items1 > 0)
         pair_tile_kernel<0><<<unsigned(items1), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe, n_probe,
-                                               vout, ps, is, 0, v->C, qoff, keys1, nullptr, 0, nullptr, nullptr);
+                                               vout, ps, is, 0, v->C, span, qoff, keys1, nullptr, 0, nullptr, nullptr);
       DK_CHECK_LAUNCH();
       const size_t tsm = size_t(NB) * sizeof(K128);
       set_dynamic_smem(seg_topk_kernel, tsm);
@@ -1728,13 +1704,13 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       if (f64_filter) {
         if (items2 > 0)
           pair_tile_kernel<1><<<unsigned(items2), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe,
-                                                 n_probe, vout, ps, is, v->C + 1, NBK - 1, nullptr, nullptr, tau, cap,
+                                                 n_probe, vout, ps, is, v->C + 1, NBK - 1, span, nullptr, nullptr, tau, cap,
                                                  cand, ccnt);
       } else {
         set_dynamic_smem(pair_filter_f32_kernel, kFilterSmem);
         if (items2 > 0)
           pair_filter_f32_kernel<<<unsigned(items2), 128, kFilterSmem, s>>>(
-            v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, n_probe, vout, ps, is, v->C + 1, NBK - 1, tau,
+            v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, n_probe, vout, ps, is, v->C + 1, NBK - 1, span, tau,
             cap, cand, ccnt);
       }
       DK_CHECK_LAUNCH();
@@ -1757,30 +1733,56 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
                 srt[srt.size() / 2], srt[srt.size() * 9 / 10], srt[srt.size() * 99 / 100], srt.back());
       }
       // candidate buffer overflowed (queries far from every list, whose tau_q passes most rows):
-      // each (query, probed list) pair as its own block-parallel scan, then a per-query merge
-      const bool split = int64_t(n_probe) * k <= 8192;
-      for (size_t r0 = 0; r0 < redo.size(); r0 += size_t(split ? redo_R : int64_t(redo.size()))) {
-        const int64_t nr = int64_t(std::min(redo.size() - r0, size_t(split ? redo_R : int64_t(redo.size()))));
-        auto* rq = reinterpret_cast<int32_t*>(split ? base + o_rq : base + o_ord);
+      // every probed key of those queries through the list-major pass, then the top-k
+      for (size_t r0 = 0; r0 < redo.size(); r0 += size_t(redo_R)) {
+        const int64_t nr = int64_t(std::min(redo.size() - r0, size_t(redo_R)));
+        auto* rq = reinterpret_cast<int32_t*>(base + o_rq);
+        auto* Qr = reinterpret_cast<double*>(base + o_rQ);
+        auto* pr = reinterpret_cast<int32_t*>(base + o_rp);
         DK_CUDA(cudaMemcpyAsync(rq, redo.data() + r0, size_t(nr) * 4, cudaMemcpyHostToDevice, s));
-        if (!split) {  // n_probe * k beyond the merge buffer: one block per query
-          run_scan(rq, nr, nullptr, io, dd, co);
-          continue;
-        }
-        auto* Qv = reinterpret_cast<double*>(base + o_rQ);
-        auto* pv = reinterpret_cast<int32_t*>(base + o_rp);
-        auto* iv = reinterpret_cast<int64_t*>(base + o_ri);
-        auto* dv = reinterpret_cast<double*>(base + o_rd);
-        auto* cv = reinterpret_cast<int32_t*>(base + o_rc);
-        const int64_t nv = nr * n_probe;
-        redo_split_kernel<<<unsigned(nv), 128, 0, s>>>(rq, nr, Qd, v->d, probe, n_probe, Qv, pv);
+        redo_compact_kernel<<<unsigned(nr), 128, 0, s>>>(rq, nr, Qd, v->d, probe, n_probe, Qr, pr);
         DK_CHECK_LAUNCH();
-        scan_with(Qv, pv, 1, nullptr, nv, iv, dv, cv);
-        int Bv = 2;
-        while (Bv < n_probe * k) Bv <<= 1;
-        set_dynamic_smem(redo_merge_kernel, size_t(Bv) * sizeof(K128));
-        redo_merge_kernel<<<unsigned(nr), 256, size_t(Bv) * sizeof(K128), s>>>(rq, n_probe, k, iv, dv, cv, call, io,
-                                                                               dd, co);
+        const int64_t rpairs = nr * n_probe;
+        prefix_probes_kernel<<<unsigned((nr + 255) / 256), 256, 0, s>>>(pr, v->offsets, nr, n_probe, INT_MAX, npq,
+                                                                         call, rows1);
+        DK_CHECK_LAUNCH();
+        query_norms_kernel<<<unsigned((nr + 7) / 8), 256, 0, s>>>(Qr, nr, v->d, yyq);
+        DK_CHECK_LAUNCH();
+        size_t tb2 = cub2;
+        DK_CUDA(cub::DeviceScan::ExclusiveSum(base + o_t2, tb2, rows1, qoff, nr + 1, s));
+        bucket_pairs_kernel<<<unsigned((rpairs + 255) / 256), 256, 0, s>>>(pr, npq, nr, n_probe, v->C, kin, vin);
+        DK_CHECK_LAUNCH();
+        tb2 = cub2;
+        DK_CUDA(cub::DeviceRadixSort::SortPairs(base + o_t2, tb2, kin, kout, vin, vout, int(rpairs), 0, bits, s));
+        list_pairs_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(kout, rpairs, NBK, ps);
+        DK_CHECK_LAUNCH();
+        list_items_kernel<<<unsigned((NBK + 1 + 255) / 256), 256, 0, s>>>(ps, v->offsets, v->C, NBK, PQ, 256,
+                                                                           ni);
+        DK_CHECK_LAUNCH();
+        tb2 = cub2;
+        DK_CUDA(cub::DeviceScan::ExclusiveSum(base + o_t2, tb2, ni, is, NBK + 1, s));
+        int64_t totr = 0, itemsr = 0;
+        DK_CUDA(cudaMemcpyAsync(&totr, qoff + nr, 8, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaMemcpyAsync(&itemsr, is + v->C, 8, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+        const size_t rbytes = size_t(std::max<int64_t>(totr, 1)) * sizeof(K128);
+        if (rbytes > v->keys1_bytes) {
+          DK_CUDA(cudaFree(v->keys1));
+          v->keys1 = nullptr;
+          v->keys1_bytes = 0;
+          DK_CUDA(cudaMalloc(&v->keys1, rbytes));
+          v->keys1_bytes = rbytes;
+        }
+        auto* keysr = static_cast<K128*>(v->keys1);
+        if (itemsr > 0)
+          pair_tile_kernel<0><<<unsigned(itemsr), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qr,
+                                                               yyq, pr, n_probe, vout, ps, is, 0, v->C, 256, qoff, keysr,
+                                                               nullptr, 0, nullptr, nullptr);
+        DK_CHECK_LAUNCH();
+        seg_topk_kernel<<<unsigned(nr), 256, tsm, s>>>(nullptr, nullptr, nullptr, keysr, qoff, 0, nullptr, 0, NB, k,
+                                                       nullptr, idx1, d21, cnt1, nullptr, nullptr);
+        DK_CHECK_LAUNCH();
+        redo_scatter_kernel<<<unsigned(nr), 128, 0, s>>>(rq, nr, k, idx1, d21, cnt1, io, dd, co);
         DK_CHECK_LAUNCH();
       }
     }
