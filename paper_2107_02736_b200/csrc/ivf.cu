@@ -897,27 +897,38 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
 }
 
 // Phase 2 on packed fp32 FMAs (FFMA2) with an exact fp64 re-check.  The fp32 dot
-// dot_f = sum x_j * fl32(y_j) (sequential chain) satisfies |dot_f - x.y| <= (d + 1) u |x||y|
-// (u = 2^-24: the rounding of y plus the chain), so with d2_f = |x|^2 + |y|^2 - 2 dot_f
-// (fp32, each operand rounding <= u times |x|^2 + |y|^2 + 2|x.y| <= 2(|x|^2 + |y|^2))
+// dot_f = sum x_j * fl32(y_j) (two interleaved chains, even and odd j, added at the end)
+// satisfies |dot_f - x.y| <= (d + 1) u |x||y| (u = 2^-24: the rounding of y plus the chains),
+// so with d2_f = |x|^2 + |y|^2 - 2 dot_f (fp32, each operand rounding <= u times
+// |x|^2 + |y|^2 + 2|x.y| <= 2(|x|^2 + |y|^2))
 //   d2 <= tau  =>  d2_f <= tau + 2.05 (d + 1) u |x||y| + 10 u (|x|^2 + |y|^2 + tau);
 // rows passing that test are re-evaluated exactly (the fp64 chain of pair_tile_kernel) and
-// appended when their (d2, row) key is below tau_q.  32 queries x 256 rows per step, lane =
-// 8 rows x 8 queries, x staged row-major (stride 33, conflict-free), y staged as {y, y}.
-constexpr int FQ = 32, FW = 8, FR = 8, FRC = 32 * FR, FDJ = 16;
-constexpr size_t kFilterSmem = size_t(FRC) * (FDJ + 1) * 4 + size_t(4) * FW * FRC * 2;
+// appended when their (d2, row) key is below tau_q.
+// Work item: 32 queries x up to `span` rows; per step 128 rows x 16 dimensions of x and the
+// 32 query slices (fp32) arrive by cp.async into one of two buffers while the other is
+// consumed; lane = 4 rows x 8 queries, 16-byte shared loads (x rows at a stride of 5
+// 16-byte units: conflict-free), accumulators as {even j, odd j} pairs.
+constexpr int FQ = 32, FW = 8, FR = 4, FRC = 32 * FR, FDJ = 16, FXS = FDJ + 4;
+constexpr size_t kFilterSmem = size_t(2) * FRC * FXS * 4 + size_t(2) * FQ * FDJ * 4 + size_t(4) * FW * FRC * 2;
 static_assert(FQ == PQ, "phase-2 items are built with PQ queries each");
 
+__global__ void to_f32_kernel(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = __double2float_rn(a[i]);
+}
+
+template <bool VEC>
 __global__ void __launch_bounds__(128, 4) pair_filter_f32_kernel(
     const float* __restrict__ xs, const double* __restrict__ xns, const int64_t* __restrict__ rows,
     const int64_t* __restrict__ off, int32_t d, int32_t C, const double* __restrict__ Q,
-    const double* __restrict__ yyq, int32_t n_probe, const int32_t* __restrict__ sval,
-    const int64_t* __restrict__ pstart, const int64_t* __restrict__ istart, int32_t blo, int32_t bhi, int32_t span,
-    const K128* __restrict__ tau, int32_t cap, K128* __restrict__ cand, int32_t* __restrict__ ccnt) {
+    const float* __restrict__ Qf, const double* __restrict__ yyq, int32_t n_probe,
+    const int32_t* __restrict__ sval, const int64_t* __restrict__ pstart, const int64_t* __restrict__ istart,
+    int32_t blo, int32_t bhi, int32_t span, const K128* __restrict__ tau, int32_t cap, K128* __restrict__ cand,
+    int32_t* __restrict__ ccnt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* xr = reinterpret_cast<float*>(smem_raw);                                    // [FRC][FDJ + 1]
-  uint16_t* s_queue = reinterpret_cast<uint16_t*>(xr + FRC * (FDJ + 1));             // [4][FW * FRC]
-  __shared__ __align__(16) float2 ys[FDJ * FQ];  // [jj][query] = {y, y}
+  float* xb = reinterpret_cast<float*>(smem_raw);                     // [2][FRC][FXS]
+  float* yb = xb + 2 * FRC * FXS;                                      // [2][FQ][FDJ]
+  uint16_t* s_queue = reinterpret_cast<uint16_t*>(yb + 2 * FQ * FDJ);  // [4][FW * FRC]
   __shared__ int64_t s_q[FQ];
   __shared__ double s_yy[FQ];
   __shared__ K128 s_tau[FQ];
@@ -948,7 +959,6 @@ __global__ void __launch_bounds__(128, 4) pair_filter_f32_kernel(
       s_tau[t] = tq;
       s_yy[t] = yy;
       if (tq.hi == ~0ull) {  // no threshold: every row passes
-        A = 0.f;
         P = INFINITY;
       } else {
         const float tf = __double2float_ru(__longlong_as_double(static_cast<long long>(tq.hi)));
@@ -961,99 +971,123 @@ __global__ void __launch_bounds__(128, 4) pair_filter_f32_kernel(
     s_A[t] = A;
     s_P[t] = P;
   }
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint16_t* queue = s_queue + warp * FW * FRC;
-  for (int64_t r0 = b; r0 < e; r0 += FRC) {
-    const int rn = int(min(e - r0, int64_t(FRC)));
-    float2 acc[FW][FR / 2];
+  const int nstage = (d + FDJ - 1) / FDJ;
+  const int nst = int((e - b + FRC - 1) / FRC) * nstage;
+  auto issue = [&](int st) {
+    const int64_t r0 = b + int64_t(st / nstage) * FRC;
+    const int j0 = (st % nstage) * FDJ;
+    const int rn = int(min(e - r0, int64_t(FRC))), dj = min(FDJ, d - j0);
+    float* xd = xb + (st & 1) * FRC * FXS;
+    float* yd = yb + (st & 1) * FQ * FDJ;
+    if constexpr (VEC) {
 #pragma unroll
-    for (int t = 0; t < FW; ++t)
-#pragma unroll
-      for (int i = 0; i < FR / 2; ++i) acc[t][i] = make_float2(0.f, 0.f);
-    for (int j0 = 0; j0 < d; j0 += FDJ) {
-      const int dj = min(FDJ, d - j0);
-      __syncthreads();
+      for (int w = 0; w < FRC * FDJ / 4 / 128; ++w) {
+        const int t = threadIdx.x + 128 * w, r = t >> 2, c4 = t & 3;
+        const int nb = r < rn ? min(max(dj - 4 * c4, 0), 4) * 4 : 0;
+        cp_async16(xd + r * FXS + 4 * c4, nb ? xs + (r0 + r) * d + j0 + 4 * c4 : xs, uint32_t(nb));
+      }
+      {
+        const int t = threadIdx.x, qq = t >> 2, c4 = t & 3;
+        const int nb = qq < np ? min(max(dj - 4 * c4, 0), 4) * 4 : 0;
+        cp_async16(yd + qq * FDJ + 4 * c4, nb ? Qf + s_q[qq] * d + j0 + 4 * c4 : Qf, uint32_t(nb));
+      }
+    } else {
 #pragma unroll 4
-      for (int u4 = 0; u4 < FRC * FDJ / 128; u4 += 16) {
-        float xv[16];
-#pragma unroll
-        for (int w = 0; w < 16; ++w) {
-          const int t = threadIdx.x + 128 * (u4 + w), r = t / FDJ, jj = t % FDJ;
-          xv[w] = (r < rn && jj < dj) ? __ldg(xs + (r0 + r) * d + j0 + jj) : 0.f;
-        }
-#pragma unroll
-        for (int w = 0; w < 16; ++w) {
-          const int t = threadIdx.x + 128 * (u4 + w), r = t / FDJ, jj = t % FDJ;
-          xr[r * (FDJ + 1) + jj] = xv[w];
-        }
+      for (int w = 0; w < FRC * FDJ / 128; ++w) {
+        const int t = threadIdx.x + 128 * w, r = t / FDJ, jj = t % FDJ;
+        const bool ok = r < rn && jj < dj;
+        cp_async4(xd + r * FXS + jj, ok ? xs + (r0 + r) * d + j0 + jj : xs, ok ? 4u : 0u);
       }
 #pragma unroll
       for (int w = 0; w < FQ * FDJ / 128; ++w) {
-        const int t = threadIdx.x + 128 * w, jj = t / FQ, qq = t % FQ;
-        const float y = (qq < np && jj < dj) ? __double2float_rn(Q[s_q[qq] * d + j0 + jj]) : 0.f;
-        ys[t] = make_float2(y, y);
+        const int t = threadIdx.x + 128 * w, qq = t / FDJ, jj = t % FDJ;
+        const bool ok = qq < np && jj < dj;
+        cp_async4(yd + qq * FDJ + jj, ok ? Qf + s_q[qq] * d + j0 + jj : Qf, ok ? 4u : 0u);
       }
-      __syncthreads();
-      if (warp * FW >= np) continue;  // no query on this warp (it still stages)
-      for (int jj = 0; jj < dj; ++jj) {
-        const float4* y4 = reinterpret_cast<const float4*>(ys + jj * FQ + warp * FW);
-        float2 y[FW];
+    }
+    cp_async_commit();
+  };
+  float2 acc[FW][FR];
 #pragma unroll
-        for (int t = 0; t < FW / 2; ++t) {
-          const float4 v = y4[t];
-          y[2 * t] = make_float2(v.x, v.y);
-          y[2 * t + 1] = make_float2(v.z, v.w);
+  for (int t = 0; t < FW; ++t)
+#pragma unroll
+    for (int i = 0; i < FR; ++i) acc[t][i] = make_float2(0.f, 0.f);
+  if (nst > 0) issue(0);
+  for (int st = 0; st < nst; ++st) {
+    if (st + 1 < nst) {
+      issue(st + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int js = st % nstage, dj = min(FDJ, d - js * FDJ);
+    const float* xc = xb + (st & 1) * FRC * FXS;
+    const float* yc = yb + (st & 1) * FQ * FDJ;
+    if (warp * FW < np) {  // (a warp without queries only stages)
+      for (int jj = 0; jj < dj; jj += 4) {
+        float4 x[FR];
+#pragma unroll
+        for (int i = 0; i < FR; ++i) x[i] = *reinterpret_cast<const float4*>(xc + (lane + 32 * i) * FXS + jj);
+#pragma unroll
+        for (int t = 0; t < FW; ++t) {
+          const float4 y = *reinterpret_cast<const float4*>(yc + (warp * FW + t) * FDJ + jj);
+#pragma unroll
+          for (int i = 0; i < FR; ++i) {
+            acc[t][i] = fma2(make_float2(x[i].x, x[i].y), make_float2(y.x, y.y), acc[t][i]);
+            acc[t][i] = fma2(make_float2(x[i].z, x[i].w), make_float2(y.z, y.w), acc[t][i]);
+          }
         }
-        float2 x[FR / 2];
-#pragma unroll
-        for (int i = 0; i < FR / 2; ++i)
-          x[i] = make_float2(xr[(lane + 64 * i) * (FDJ + 1) + jj], xr[(lane + 64 * i + 32) * (FDJ + 1) + jj]);
-#pragma unroll
-        for (int t = 0; t < FW; ++t)
-#pragma unroll
-          for (int i = 0; i < FR / 2; ++i) acc[t][i] = fma2(x[i], y[t], acc[t][i]);
       }
     }
-    // approximate test, survivors queued per warp as (query slot, row)
-    int qn = 0;
+    if (js == nstage - 1 && warp * FW < np) {
+      // chunk done: approximate test, survivors queued per warp as (query slot, row)
+      const int64_t r0 = b + int64_t(st / nstage) * FRC;
+      const int rn = int(min(e - r0, int64_t(FRC)));
+      int qn = 0;
 #pragma unroll
-    for (int i = 0; i < FR; ++i) {
-      const int r = lane + 64 * (i >> 1) + 32 * (i & 1);
-      const bool rv = r < rn;
-      const double xn = rv ? xns[r0 + r] : 0.0;
-      const float xf = float(xn), xnorm = sqrtf(xf);
-      const float R = 10.f * u * xf - xf;
+      for (int i = 0; i < FR; ++i) {
+        const int r = lane + 32 * i;
+        const bool rv = r < rn;
+        const float xf = rv ? float(xns[r0 + r]) : 0.f, xnorm = sqrtf(xf);
+        const float R = 10.f * u * xf - xf;
 #pragma unroll
-      for (int t = 0; t < FW; ++t) {
-        const int qq = warp * FW + t;
-        const float dot = (i & 1) ? acc[t][i >> 1].y : acc[t][i >> 1].x;
-        const bool pass = rv && (-2.f * dot <= fmaf(s_A[qq], xnorm, s_P[qq] + R));
-        const unsigned m = __ballot_sync(0xffffffffu, pass);
-        if (pass) queue[qn + __popc(m & ((1u << lane) - 1u))] = uint16_t((t << 8) | r);
-        qn += __popc(m);
+        for (int t = 0; t < FW; ++t) {
+          const int qq = warp * FW + t;
+          const float dot = acc[t][i].x + acc[t][i].y;
+          const bool pass = rv && (-2.f * dot <= fmaf(s_A[qq], xnorm, s_P[qq] + R));
+          const unsigned m = __ballot_sync(0xffffffffu, pass);
+          if (pass) queue[qn + __popc(m & ((1u << lane) - 1u))] = uint16_t((t << 8) | r);
+          qn += __popc(m);
+          acc[t][i] = make_float2(0.f, 0.f);
+        }
       }
-    }
-    __syncwarp();
-    // exact re-check, one queued pair per lane
-    for (int k2 = lane; k2 < qn; k2 += 32) {
-      const int ent = queue[k2], t = ent >> 8, r = ent & 255, qq = warp * FW + t;
-      const int64_t q = s_q[qq], pos = r0 + r;
-      const float* x = xs + pos * d;
-      const double* y = Q + q * d;
-      double dot = 0.0;
-      for (int j = 0; j < d; ++j) dot = fma(double(__ldg(x + j)), y[j], dot);
-      double v = dot * -2.0;
-      v += xns[pos];
-      v += s_yy[qq];
-      v = fmax(v, 0.0);
-      const K128 key{static_cast<unsigned long long>(__double_as_longlong(v)),
-                     static_cast<unsigned long long>(rows[pos])};
-      if (k_less(key, s_tau[qq])) {
-        const int slot = atomicAdd(&ccnt[q], 1);
-        if (slot < cap) cand[q * cap + slot] = key;
+      __syncwarp();
+      // exact re-check, one queued pair per lane
+      for (int k2 = lane; k2 < qn; k2 += 32) {
+        const int ent = queue[k2], t = ent >> 8, r = ent & 255, qq = warp * FW + t;
+        const int64_t q = s_q[qq], pos = r0 + r;
+        const float* x = xs + pos * d;
+        const double* y = Q + q * d;
+        double dot = 0.0;
+        for (int j = 0; j < d; ++j) dot = fma(double(__ldg(x + j)), y[j], dot);
+        double v = dot * -2.0;
+        v += xns[pos];
+        v += s_yy[qq];
+        v = fmax(v, 0.0);
+        const K128 key{static_cast<unsigned long long>(__double_as_longlong(v)),
+                       static_cast<unsigned long long>(rows[pos])};
+        if (k_less(key, s_tau[qq])) {
+          const int slot = atomicAdd(&ccnt[q], 1);
+          if (slot < cap) cand[q * cap + slot] = key;
+        }
       }
+      __syncwarp();
     }
-    __syncwarp();
+    __syncthreads();  // buffer (st & 1) is refilled by the next iteration's issue
   }
 }
 
@@ -1477,7 +1511,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     size_t cub2 = 0;
     size_t o_i1 = 0, o_d1 = 0, o_c1 = 0, o_np = 0, o_ca = 0, o_tau = 0, o_kin = 0, o_kout = 0, o_vin = 0,
            o_vout = 0, o_ps = 0, o_ni = 0, o_is = 0, o_t2 = 0, o_cc = 0, o_cand = 0, o_ov = 0, o_rq = 0, o_rQ = 0,
-           o_rp = 0, o_yy = 0, o_r1 = 0, o_qo = 0;
+           o_rp = 0, o_yy = 0, o_r1 = 0, o_qo = 0, o_qf = 0;
     int64_t redo_R = 0;
     if (two_phase) {
       size_t a = 0, b2 = 0;
@@ -1494,6 +1528,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       o_ca = take(size_t(nq) * 4);
       o_tau = take(size_t(nq) * sizeof(K128));
       o_yy = take(size_t(nq) * 8);
+      o_qf = take(size_t(nq) * v->d * 4);
       o_r1 = take(size_t(nq + 1) * 8);
       o_qo = take(size_t(nq + 1) * 8);
       o_kin = take(size_t(npairs) * 4);
@@ -1707,11 +1742,22 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
                                                  n_probe, vout, ps, is, v->C + 1, NBK - 1, span, nullptr, nullptr, tau, cap,
                                                  cand, ccnt);
       } else {
-        set_dynamic_smem(pair_filter_f32_kernel, kFilterSmem);
-        if (items2 > 0)
-          pair_filter_f32_kernel<<<unsigned(items2), 128, kFilterSmem, s>>>(
-            v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, n_probe, vout, ps, is, v->C + 1, NBK - 1, span, tau,
-            cap, cand, ccnt);
+        auto* Qf = reinterpret_cast<float*>(base + o_qf);
+        to_f32_kernel<<<unsigned((nq * v->d + 255) / 256), 256, 0, s>>>(Qd, nq * v->d, Qf);
+        DK_CHECK_LAUNCH();
+        if (items2 > 0) {
+          if ((v->d & 3) == 0) {
+            set_dynamic_smem(pair_filter_f32_kernel<true>, kFilterSmem);
+            pair_filter_f32_kernel<true><<<unsigned(items2), 128, kFilterSmem, s>>>(
+                v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, Qf, yyq, n_probe, vout, ps, is, v->C + 1,
+                NBK - 1, span, tau, cap, cand, ccnt);
+          } else {
+            set_dynamic_smem(pair_filter_f32_kernel<false>, kFilterSmem);
+            pair_filter_f32_kernel<false><<<unsigned(items2), 128, kFilterSmem, s>>>(
+                v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, Qf, yyq, n_probe, vout, ps, is, v->C + 1,
+                NBK - 1, span, tau, cap, cand, ccnt);
+          }
+        }
       }
       DK_CHECK_LAUNCH();
       // (4) top-k of the phase-1 top-k and the candidates

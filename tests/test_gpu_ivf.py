@@ -250,3 +250,22 @@ def test_two_phase_overflow_redo_for_far_queries(cap, monkeypatch):
             ri, rd = O.ivf_query(od, cent, lists, Q[j], k, p)
             np.testing.assert_array_equal(idx[j, :cnt[j]], ri)
             np.testing.assert_allclose(d2[j, :cnt[j]], rd, rtol=1e-12)
+
+
+@pytest.mark.parametrize("d", [13, 36])
+def test_two_phase_odd_and_wide_rows(d):
+    # row widths off the 16-byte copy path (13) and over several 16-dimension stages (36)
+    rng = np.random.default_rng(53 + d)
+    n, C = 30_000, 24
+    centers = rng.normal(scale=3.0, size=(12, d))
+    X = (centers[rng.integers(0, 12, n)] + rng.normal(size=(n, d))).astype(np.float32)
+    Q = np.vstack([centers[rng.integers(0, 12, 20)] + rng.normal(size=(20, d)), 25.0 * rng.normal(size=(4, d))])
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    index = g.ivf_build(ds, C, seed=9)
+    cent, lists = O.ivf_build(od, C, 9)
+    for k, p in ((1, 3), (64, 7)):
+        idx, d2, cnt = g.ivf_query_batch(index, ds, Q, k, p)
+        for j in range(len(Q)):
+            ri, rd = O.ivf_query(od, cent, lists, Q[j], k, p)
+            np.testing.assert_array_equal(idx[j, :cnt[j]], ri)
+            np.testing.assert_allclose(d2[j, :cnt[j]], rd, rtol=1e-12)
