@@ -94,13 +94,27 @@ __device__ __forceinline__ double group_row_kernel(const float* __restrict__ x, 
                                                    int family, double c, int gl) {
   double acc = 0.0;
   if ((d & 3) == 0) {
+    // batches of 4 float4 per lane, all loads issued before the fp64 work (memory-level
+    // parallelism for wide rows); the accumulation order stays k4 = gl, gl + G, ...
     const float4* x4 = reinterpret_cast<const float4*>(x);
-    for (int k4 = gl; k4 < (d >> 2); k4 += G) {
-      const float4 v = __ldg(x4 + k4);
-      const double t0 = double(v.x) - q[4 * k4 + 0], t1 = double(v.y) - q[4 * k4 + 1];
-      const double t2 = double(v.z) - q[4 * k4 + 2], t3 = double(v.w) - q[4 * k4 + 3];
-      if (family == DK_LAPLACIAN) acc += (fabs(t0) + fabs(t1)) + (fabs(t2) + fabs(t3));
-      else { acc = fma(t0, t0, acc); acc = fma(t1, t1, acc); acc = fma(t2, t2, acc); acc = fma(t3, t3, acc); }
+    const int chunks = d >> 2;
+    for (int b0 = gl; b0 < chunks; b0 += 4 * G) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k4 = b0 + u * G;
+        v[u] = k4 < chunks ? __ldg(x4 + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k4 = b0 + u * G;
+        if (k4 < chunks) {
+          const double t0 = double(v[u].x) - q[4 * k4 + 0], t1 = double(v[u].y) - q[4 * k4 + 1];
+          const double t2 = double(v[u].z) - q[4 * k4 + 2], t3 = double(v[u].w) - q[4 * k4 + 3];
+          if (family == DK_LAPLACIAN) acc += (fabs(t0) + fabs(t1)) + (fabs(t2) + fabs(t3));
+          else { acc = fma(t0, t0, acc); acc = fma(t1, t1, acc); acc = fma(t2, t2, acc); acc = fma(t3, t3, acc); }
+        }
+      }
     }
   } else {
     for (int k = gl; k < d; k += G) {
