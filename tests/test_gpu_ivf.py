@@ -269,3 +269,29 @@ def test_two_phase_odd_and_wide_rows(d):
             ri, rd = O.ivf_query(od, cent, lists, Q[j], k, p)
             np.testing.assert_array_equal(idx[j, :cnt[j]], ri)
             np.testing.assert_allclose(d2[j, :cnt[j]], rd, rtol=1e-12)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_arbitrary_lists_empty_lists_ties_and_short_probes(seed):
+    # hand-made inverted lists (empty lists, lists shorter than k, duplicated rows across the
+    # two phases), n_probe from 2 to C, k from 1 to beyond the probed rows; batch vs oracle
+    rng = np.random.default_rng(300 + seed)
+    n, d, C = int(rng.integers(40, 400)), int(rng.integers(1, 40)), int(rng.integers(3, 12))
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    X[: n // 5] = X[0]                                   # a block of identical rows
+    cent = rng.normal(size=(C, d))
+    cent[1] = cent[0]                                     # tied centroids
+    lab = rng.integers(0, C, n)
+    lab[lab == C - 1] = 0                                 # list C-1 empty
+    lists = [np.flatnonzero(lab == c).astype(np.int64) for c in range(C)]
+    index = g.IvfIndex(centroids=cent, assignments=lists, seed=0)
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    Q = np.vstack([rng.normal(size=(7, d)), X[:2].astype(np.float64), 30.0 * rng.normal(size=(2, d))])
+    for k, p in ((1, 2), (3, C), (int(rng.integers(5, 60)), max(2, C // 2)), (n, C)):
+        idx, d2, cnt = g.ivf_query_batch(index, ds, Q, k, p)
+        for j in range(len(Q)):
+            ri, rd = O.ivf_query(od, cent, lists, Q[j], k, p)
+            assert cnt[j] == len(ri)
+            np.testing.assert_array_equal(idx[j, :cnt[j]], ri)
+            np.testing.assert_allclose(d2[j, :cnt[j]], rd, rtol=1e-12, atol=1e-12)
+            assert (idx[j, cnt[j]:] == -1).all()
