@@ -449,7 +449,7 @@ def _probe(cent: np.ndarray, y: np.ndarray, n_probe: int, formula: int) -> np.nd
 
 
 def ivf_query(data: Data, cent: np.ndarray, lists, query, k: int, n_probe: int, formula: int = 0):
-    """ann.py:202-229 -> (indices, sq_distances): exact k smallest among the probed lists."""
+    """ann.py:204-230 -> (indices, sq_distances): exact k smallest among the probed lists."""
     y = np.asarray(query, dtype=np.float64).ravel()
     members = [lists[c] for c in _probe(cent, y, n_probe, formula) if len(lists[c])]
     if not members:

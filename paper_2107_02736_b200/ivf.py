@@ -175,7 +175,7 @@ def ivf_query_batch(index, dataset, queries, k: int, n_probe: int, *, formula: i
 
 
 def ivf_query(index, dataset, query, k: int, n_probe: int) -> NeighborList:
-    """Exact k-NN restricted to the members of the n_probe nearest clusters (ann.py:202-229)."""
+    """Exact k-NN restricted to the members of the n_probe nearest clusters (ann.py:204-230)."""
     if k < 1:
         raise ValueError(f"k={k} must be >= 1")
     if not 1 <= n_probe <= index.n_clusters:
