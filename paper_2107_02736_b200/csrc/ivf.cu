@@ -1502,7 +1502,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     static const bool one_phase = std::getenv("DK_IVF_ONE_PHASE") != nullptr;  // A/B switch
     const int64_t npairs = nq * int64_t(n_probe);
     const int32_t NBK = 2 * v->C + 2;  // pair buckets: phase-1 lists, a gap, phase-2 lists
-    const bool two_phase = !bigk && !one_phase && n_probe > 1 && npairs < (int64_t(1) << 31);
+    const bool two_phase = !bigk && !one_phase && npairs < (int64_t(1) << 31);
     int64_t cap_rows = std::max<int64_t>(2048, 16 * int64_t(k));
     if (const char* e = std::getenv("DK_IVF_CAP")) cap_rows = std::max<int64_t>(1, std::atoll(e));  // tests
     const int32_t cap = int32_t(std::min<int64_t>(int64_t(1) << 20, cap_rows));
