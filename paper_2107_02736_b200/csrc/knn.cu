@@ -115,6 +115,34 @@ __device__ __forceinline__ double exact_d2_warp(const float* __restrict__ x, con
   return s;
 }
 
+// exact fp64 direct-difference d2 by a group of G lanes (float4 row loads when rows are
+// whole float4s), reduced within the group
+template <int G>
+__device__ __forceinline__ double exact_d2_group(const float* __restrict__ x, const double* __restrict__ q, int d,
+                                                 int gl) {
+  double s = 0.0;
+  if ((d & 3) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int k4 = gl; k4 < (d >> 2); k4 += G) {
+      const float4 v = __ldg(x4 + k4);
+      const double t0 = double(v.x) - q[4 * k4 + 0], t1 = double(v.y) - q[4 * k4 + 1];
+      const double t2 = double(v.z) - q[4 * k4 + 2], t3 = double(v.w) - q[4 * k4 + 3];
+      s = fma(t0, t0, s);
+      s = fma(t1, t1, s);
+      s = fma(t2, t2, s);
+      s = fma(t3, t3, s);
+    }
+  } else {
+    for (int k = gl; k < d; k += G) {
+      const double t = double(__ldg(x + k)) - q[k];
+      s = fma(t, t, s);
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 // exact re-rank of the candidates in increasing approx order with early termination
 __global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global_offset, int32_t d,
                                      const double* __restrict__ Q, int64_t nq, int32_t k,
@@ -142,20 +170,23 @@ __global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global
   Key128* top = reinterpret_cast<Key128*>(sbuf + B);  // [Kp + W]
   for (int i = threadIdx.x; i < Kp + W; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
   __syncthreads();
-  const double* qv = Q + size_t(q) * d;
+  double* qv = reinterpret_cast<double*>(top + Kp + W);  // the query in shared memory
+  for (int j = threadIdx.x; j < d; j += blockDim.x) qv[j] = Q[size_t(q) * d + j];
+  __syncthreads();
   const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  constexpr int G = 8;  // lanes per candidate: 4 candidates per warp step
+  const int grp = lane / G, gl = lane % G;
   __shared__ int s_stop;
   for (int pos = 0; pos < c; pos += W) {
-    for (int i = warp; i < W; i += nwarps) {
-      Key128 key{~0ull, ~0ull};
-      if (pos + i < c) {
-        const unsigned long long col = sbuf[pos + i] & 0xffffffffull;
-        const double dd = exact_d2_warp(X + size_t(col) * d, qv, d, lane);
-        key.hi = static_cast<unsigned long long>(__double_as_longlong(dd));
-        key.lo = col;
-      }
-      if (lane == 0) top[Kp + i] = key;
+    for (int i0 = warp * (32 / G); i0 < W; i0 += nwarps * (32 / G)) {
+      const int i = i0 + grp;
+      const bool ok = i < W && pos + i < c;
+      const unsigned long long col = ok ? (sbuf[pos + i] & 0xffffffffull) : 0ull;
+      const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
+      if (gl == 0 && i < W)
+        top[Kp + i] = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)), col}
+                         : Key128{~0ull, ~0ull};
     }
     bitonic_k128(top, Kp + W);
     if (threadIdx.x == 0) {
@@ -287,7 +318,7 @@ void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, cons
   // candidates per query against a cap of 8192); counts above the cap overflow as before
   const int B = std::max(2, pow2_ceil(max_cnt > 0 ? std::min(max_cnt, cap) : cap));
   const int Kp = std::max(32, pow2_ceil(k));
-  const size_t smem = size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128);
+  const size_t smem = size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double);
   set_dynamic_smem(select_rerank_kernel, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
   select_rerank_kernel<<<unsigned(nq), 256, smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,
