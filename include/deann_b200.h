@@ -259,6 +259,14 @@ dk_status dk_sweep_probe(dk_handle h, const double* Q, int64_t nq, int32_t mode,
 /* Number of this library's kernels launched by the last API call. */
 dk_status dk_last_launch_count(dk_handle h, int64_t* count);
 
+/* Page-locked host buffers for results (no reference counterpart: host plumbing of the
+ * Python layer).  dk_host_alloc returns a buffer of >= bytes from a size-class cache of
+ * cudaHostAlloc blocks (a new block only when the cache has none); dk_host_free returns
+ * it to the cache (blocks beyond 1 GiB of cached memory are released).  Device->host
+ * copies of results into such buffers run at full DMA speed. */
+dk_status dk_host_alloc(int64_t bytes, void** out);
+dk_status dk_host_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

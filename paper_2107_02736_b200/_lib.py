@@ -29,6 +29,7 @@ EXPORTED = (
     "dk_naive", "dk_sqdist", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
     "dk_rsp_attach", "dk_rsp_walk", "dk_ivf_create", "dk_ivf_free", "dk_kmeanspp_seed", "dk_kmeanspp_pick",
     "dk_kmeans_lloyd", "dk_ivf_get", "dk_ivf_set", "dk_ivf_query", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
+    "dk_host_alloc", "dk_host_free",
 )
 
 
@@ -97,6 +98,8 @@ def _declare(lib):
         "dk_sweep_probe": (_i32, [_vp, _vp, _i64, _i32, _i32, ctypes.POINTER(_f64)]),
         "dk_knn_stats": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                 ctypes.POINTER(_i64)]),
+        "dk_host_alloc": (_i32, [_i64, ctypes.POINTER(_vp)]),
+        "dk_host_free": (_i32, [_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -155,6 +158,43 @@ def current_stream():
     if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
         return torch.cuda.current_stream().cuda_stream
     return None
+
+
+class _PinnedBlock:
+    """One dk_host_alloc buffer, returned to the library's cache when collected."""
+
+    __slots__ = ("ptr",)
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        check(load().dk_host_alloc(nbytes, ctypes.byref(p)))
+        self.ptr = p.value
+
+    def __del__(self):
+        try:
+            load().dk_host_free(ctypes.c_void_p(self.ptr))
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """Uninitialised host output array; large ones (1 MiB .. 512 MiB) live in page-locked memory
+    from the library's cache (dk_host_alloc), so device->host copies of results run at
+    full DMA speed instead of through a pageable bounce buffer.  The array (and any view
+    of it) keeps the buffer alive."""
+    dt = np.dtype(dtype)
+    shape = tuple(int(x) for x in np.atleast_1d(shape))
+    count = int(np.prod(shape, dtype=np.int64))
+    nbytes = count * dt.itemsize
+    if nbytes < (1 << 20) or nbytes > (1 << 29):  # small, or too big to pin by power-of-two classes
+        return np.empty(shape, dtype=dt)
+    try:
+        block = _PinnedBlock(nbytes)
+    except (MemoryError, DeannGpuError):
+        return np.empty(shape, dtype=dt)
+    buf = (ctypes.c_char * nbytes).from_address(block.ptr)
+    buf._dk_block = block
+    return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
 
 
 def family_code(family) -> int:

@@ -63,8 +63,8 @@ def knn_batch(dataset, queries, k: int) -> tuple[np.ndarray, np.ndarray]:
     if not 1 <= k <= ds.n:
         raise ValueError(f"k={k} out of range [1, {ds.n}]")
     q = _queries64(queries, ds.d)
-    idx = np.empty((q.shape[0], k), dtype=np.int64)
-    d2 = np.empty((q.shape[0], k), dtype=np.float64)
+    idx = _lib.host_empty((q.shape[0], k), np.int64)
+    d2 = _lib.host_empty((q.shape[0], k), np.float64)
     _lib.check(_lib.load().dk_knn(ds.handle, q.ctypes.data, q.shape[0], k, idx.ctypes.data, d2.ctypes.data,
                                   _lib.current_stream()))
     return idx, d2

@@ -18,6 +18,9 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <map>
+#include <mutex>
+
 #include "internal.h"
 #include "tile_kernel.cuh"
 
@@ -1255,6 +1258,66 @@ dk_status dk_last_launch_count(dk_handle h, int64_t* count) {
   return guard([&] {
     DK_REQUIRE(h != nullptr && count != nullptr, "NULL argument");
     *count = h->launches;
+  });
+}
+
+// ---- page-locked host result buffers: power-of-two size classes, cached
+namespace {
+struct HostCache {
+  std::mutex mu;
+  std::map<void*, size_t> live;                  // pointer -> class bytes
+  std::multimap<size_t, void*> free_blocks;      // class bytes -> pointer
+  size_t cached = 0;
+};
+HostCache& host_cache() {
+  static HostCache* c = new HostCache;  // never destroyed: blocks may be freed at exit
+  return *c;
+}
+}  // namespace
+
+dk_status dk_host_alloc(int64_t bytes, void** out) {
+  return guard([&] {
+    DK_REQUIRE(out != nullptr && bytes >= 0, "bad argument");
+    size_t cls = 4096;
+    while (cls < size_t(bytes)) cls <<= 1;
+    HostCache& c = host_cache();
+    {
+      std::lock_guard<std::mutex> lk(c.mu);
+      auto it = c.free_blocks.find(cls);
+      if (it != c.free_blocks.end()) {
+        *out = it->second;
+        c.free_blocks.erase(it);
+        c.cached -= cls;
+        c.live[*out] = cls;
+        return;
+      }
+    }
+    void* p = nullptr;
+    DK_CUDA(cudaHostAlloc(&p, cls, cudaHostAllocPortable));
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.live[p] = cls;
+    *out = p;
+  });
+}
+
+dk_status dk_host_free(void* p) {
+  return guard([&] {
+    if (p == nullptr) return;
+    HostCache& c = host_cache();
+    size_t cls = 0;
+    {
+      std::lock_guard<std::mutex> lk(c.mu);
+      auto it = c.live.find(p);
+      DK_REQUIRE(it != c.live.end(), "dk_host_free: not a dk_host_alloc buffer");
+      cls = it->second;
+      c.live.erase(it);
+      if (c.cached + cls <= (size_t(1) << 30)) {
+        c.free_blocks.emplace(cls, p);
+        c.cached += cls;
+        return;
+      }
+    }
+    DK_CUDA(cudaFreeHost(p));
   });
 }
 

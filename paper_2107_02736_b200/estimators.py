@@ -162,7 +162,7 @@ def _sample_sums(ds: Dataset, spec, q: np.ndarray, m: int, seed: int, base: int,
                  stride: int = 0, export: bool = False):
     nq = q.shape[0]
     z = np.empty(nq, dtype=np.float64)
-    acc = np.empty((nq, m), dtype=np.int64) if export else None
+    acc = _lib.host_empty((nq, m), np.int64) if export else None
     _lib.check(_lib.load().dk_sample(ds.handle, q.ctypes.data, nq, _lib.family_code(spec.family), spec.bandwidth,
                                      m, seed, base, _lib.ptr(excl), _lib.ptr(excl_cnt), stride, z.ctypes.data,
                                      _lib.ptr(acc), None, None))
@@ -284,8 +284,8 @@ def deann_arrays(dataset, kernel, queries, k: int, m: int, *, seed: int, query_b
     q = _queries64(queries, ds.d)
     nq = q.shape[0]
     values = np.empty(nq, dtype=np.float64)
-    nbr = np.empty((nq, k), dtype=np.int64) if (export_neighbors and k > 0) else None
-    smp = np.empty((nq, m), dtype=np.int64) if (export_samples and m > 0) else None
+    nbr = _lib.host_empty((nq, k), np.int64) if (export_neighbors and k > 0) else None
+    smp = _lib.host_empty((nq, m), np.int64) if (export_samples and m > 0) else None
     _lib.check(_lib.load().dk_deann(ds.handle, q.ctypes.data, nq, _lib.family_code(spec.family), spec.bandwidth,
                                     k, m, int(seed), int(query_base), values.ctypes.data, _lib.ptr(nbr), None,
                                     _lib.ptr(smp), _lib.current_stream()))

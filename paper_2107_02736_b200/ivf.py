@@ -70,8 +70,8 @@ class _DeviceIvf:
 
     def query(self, Q: np.ndarray, k: int, n_probe: int, formula: int):
         nq = Q.shape[0]
-        idx = np.empty((nq, k), dtype=np.int64)
-        d2 = np.empty((nq, k), dtype=np.float64)
+        idx = _lib.host_empty((nq, k), np.int64)
+        d2 = _lib.host_empty((nq, k), np.float64)
         cnt = np.empty(nq, dtype=np.int32)
         _lib.check(_lib.load().dk_ivf_query(self.handle, Q.ctypes.data, nq, k, n_probe, formula, idx.ctypes.data,
                                             d2.ctypes.data, cnt.ctypes.data, None))

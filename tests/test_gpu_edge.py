@@ -158,3 +158,33 @@ def test_very_wide_rows():
     st, ost = g.RspState.from_dataset(ds, 2), O.Permuted(od, 2)
     assert g.rsp_kde(st, g.KernelSpec("gaussian", 40.0), Q[0], 300).value == pytest.approx(
         O.rsp_kde(ost, "gaussian", 40.0, Q[0], 300), rel=1e-12)
+
+
+def test_pinned_result_buffers_lifecycle():
+    # results >= 1 MiB come back in page-locked buffers from the library's cache; an array
+    # (or a view of it) keeps its buffer alive, and freed buffers are reused
+    import gc
+
+    from paper_2107_02736_b200 import _lib
+
+    a = _lib.host_empty((512, 300), np.float64)
+    assert a.shape == (512, 300) and a.dtype == np.float64
+    a[:] = 3.0
+    v = a[10:20, 5]
+    del a
+    gc.collect()
+    assert (v == 3.0).all()
+    del v
+    gc.collect()
+    b = _lib.host_empty((300, 512), np.int64)
+    b[:] = 7
+    assert int(b.sum()) == 7 * 300 * 512
+    assert _lib.host_empty((4, 4), np.float64).flags.owndata  # small: plain numpy
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(5000, 24)).astype(np.float32)
+    Q = rng.normal(size=(1500, 24))
+    ds = g.Dataset.from_array(X)
+    idx, d2 = g.knn_batch(ds, Q, 100)          # 1.2 MB outputs: pinned path
+    idx2, d22 = g.knn_batch(ds, Q[:7], 100)    # small: numpy path
+    np.testing.assert_array_equal(idx[:7], idx2)
+    np.testing.assert_array_equal(d2[:7], d22)
