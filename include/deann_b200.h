@@ -240,6 +240,15 @@ dk_status dk_ivf_set(dk_ivf_handle ivf, const double* centroids, const int64_t* 
 dk_status dk_ivf_query(dk_ivf_handle ivf, const double* Q, int64_t nq, int32_t k, int32_t n_probe,
                        int32_t formula, int64_t* idx_out, double* d2_out, int32_t* cnt_out,
                        void* stream);
+/* DEANN over a query batch with the IVF index as the ANN (estimators.py:306-379 with an
+ * IvfAnnIndex, ann.py:276-316): per query the k^ <= k probed neighbours of dk_ivf_query
+ * (formula 1), Z1 = mean kernel over them (L2 families from their d2; laplacian re-evaluated
+ * in L1, estimators.py:346-351), Z2 = mean kernel over the first m Philox draws outside
+ * them (dk_sample's stream), value = (k^/n) Z1 + ((n-k^)/n) Z2.  value_out[nq] and
+ * khat_out[nq] (optional) may be host or device memory. */
+dk_status dk_deann_ivf(dk_ivf_handle ivf, const double* Q, int64_t nq, int32_t family, double bandwidth,
+                       int32_t k, int32_t m, int32_t n_probe, uint64_t seed, int64_t query_base,
+                       double* value_out, int32_t* khat_out, void* stream);
 
 /* Timing support for bench.py: average device duration (ms) of the LAST launch
  * of the dominant kernel of the last call on this handle (CUDA events on the

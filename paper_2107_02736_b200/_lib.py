@@ -29,7 +29,7 @@ EXPORTED = (
     "dk_naive", "dk_sqdist", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
     "dk_rsp_attach", "dk_rsp_walk", "dk_ivf_create", "dk_ivf_free", "dk_kmeanspp_seed", "dk_kmeanspp_pick",
     "dk_kmeans_lloyd", "dk_ivf_get", "dk_ivf_set", "dk_ivf_query", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
-    "dk_host_alloc", "dk_host_free",
+    "dk_host_alloc", "dk_host_free", "dk_deann_ivf",
 )
 
 
@@ -77,6 +77,7 @@ def _declare(lib):
         "dk_ivf_get": (_i32, [_vp, _vp, _vp, _vp]),
         "dk_ivf_set": (_i32, [_vp, _vp, _vp, _vp]),
         "dk_ivf_query": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+        "dk_deann_ivf": (_i32, [_vp, _vp, _i64, _i32, _f64, _i32, _i32, _i32, _u64, _i64, _vp, _vp, _vp]),
         "dk_file_info": (_i32, [ctypes.c_char_p, ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
         "dk_fit_file": (_i32, [ctypes.c_char_p, _i64, _i64, ctypes.POINTER(FitOpts), ctypes.POINTER(_vp)]),
         "dk_info": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),

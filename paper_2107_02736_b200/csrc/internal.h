@@ -259,6 +259,6 @@ void launch_rsp_eval(const float* X, int64_t n, int32_t d, const double* Q, int6
                      double* z_sum, cudaStream_t s);
 void launch_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m, int64_t n_total,
                           const double* nbr_d2, const double* z1_l1_sum, const double* z2_sum, double* value,
-                          cudaStream_t s);
+                          cudaStream_t s, const int32_t* khat = nullptr);
 
 }  // namespace dk

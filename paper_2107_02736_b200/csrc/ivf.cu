@@ -18,6 +18,7 @@
 // exact fp64 scan of the probed lists with a shared-memory top-k ((d2, row) order,
 // threshold-filtered), d2 = ((x.y) * -2 + |x|^2) + |y|^2 clamped at 0 (ann.py:224-229).
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -50,6 +51,8 @@ struct dk_ivf {
   size_t keys1_bytes = 0;
   void* ckeys = nullptr;         // query scratch: centroid distance keys [queries][C], grow-only
   size_t ckeys_bytes = 0;
+  void* dws = nullptr;           // dk_deann_ivf scratch, grow-only
+  size_t dws_bytes = 0;
   bool lists = false;
 };
 
@@ -1255,7 +1258,7 @@ void free_ivf(dk_ivf* v) {
                   static_cast<void*>(v->cdf), static_cast<void*>(v->labels), static_cast<void*>(v->labels_s),
                   static_cast<void*>(v->ids), static_cast<void*>(v->rows), static_cast<void*>(v->offsets),
                   static_cast<void*>(v->d2min), static_cast<void*>(v->xs), static_cast<void*>(v->xns),
-                  static_cast<void*>(v->scal), v->temp, v->keys1, v->ckeys})
+                  static_cast<void*>(v->scal), v->temp, v->keys1, v->ckeys, v->dws})
     if (p) cudaFree(p);
   delete v;
 }
@@ -1837,6 +1840,82 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     if (!ddev) DK_CUDA(cudaMemcpyAsync(d2_out, dd, size_t(nq) * k * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (!cdev) DK_CUDA(cudaMemcpyAsync(cnt_out, co, size_t(nq) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     if (!idev || !ddev || !cdev) DK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+dk_status dk_deann_ivf(dk_ivf_handle v, const double* Q, int64_t nq, int32_t family, double bandwidth,
+                       int32_t k, int32_t m, int32_t n_probe, uint64_t seed, int64_t query_base,
+                       double* value_out, int32_t* khat_out, void* stream) {
+  return guard([&] {
+    DK_REQUIRE(v != nullptr, "NULL handle");
+    DK_REQUIRE(family == DK_GAUSSIAN || family == DK_EXPONENTIAL || family == DK_LAPLACIAN,
+               "unknown kernel family " + std::to_string(family));
+    DK_REQUIRE(std::isfinite(bandwidth) && bandwidth > 0.0,
+               "bandwidth must be positive and finite, got " + std::to_string(bandwidth));
+    dk_dataset* h = v->ds;
+    const int64_t n = h->n;
+    DK_REQUIRE(h->global_offset == 0 && h->global_n == n, "dk_deann_ivf runs on an unsharded handle");
+    DK_REQUIRE(k >= 1 && int64_t(k) <= n, "k=" + std::to_string(k) + " out of range [1, " + std::to_string(n) + "]");
+    DK_REQUIRE(m >= 0, "m=" + std::to_string(m) + " must be >= 0");
+    DK_REQUIRE(!(m > 0 && int64_t(k) >= n), "m > 0 requires k + 1 <= n so the remainder is nonempty");
+    DK_REQUIRE(nq >= 0, "negative query count");
+    if (nq == 0) return;
+    DK_REQUIRE(Q != nullptr && value_out != nullptr, "NULL argument");
+    DeviceGuard g(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool long_excl = m > 0 && k > kSmemSortMax;
+    const size_t seg_bytes = long_excl ? seg_sort_temp_bytes(k, nq) : 0;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t a = (off + 255) & ~size_t(255);
+      off = a + bytes;
+      return a;
+    };
+    const size_t o_q = take(size_t(nq) * h->d * 8), o_i = take(size_t(nq) * k * 8), o_d = take(size_t(nq) * k * 8);
+    const size_t o_c = take(size_t(nq) * 4), o_s = take(m > 0 ? size_t(nq) * k * 8 : 8);
+    const size_t o_z1 = take(size_t(nq) * 8), o_z2 = take(size_t(nq) * 8), o_v = take(size_t(nq) * 8);
+    const size_t o_g = take(seg_bytes);
+    if (off > v->dws_bytes) {
+      if (v->dws) DK_CUDA(cudaFree(v->dws));
+      v->dws = nullptr;
+      v->dws_bytes = 0;
+      DK_CUDA(cudaMalloc(&v->dws, off));
+      v->dws_bytes = off;
+    }
+    uint8_t* base = static_cast<uint8_t*>(v->dws);
+    const double* Qd = Q;
+    if (!is_device_ptr(Q)) {
+      DK_CUDA(cudaMemcpyAsync(base + o_q, Q, size_t(nq) * h->d * 8, cudaMemcpyHostToDevice, s));
+      Qd = reinterpret_cast<const double*>(base + o_q);
+    }
+    auto* idx = reinterpret_cast<int64_t*>(base + o_i);
+    auto* d2 = reinterpret_cast<double*>(base + o_d);
+    auto* cnt = reinterpret_cast<int32_t*>(base + o_c);
+    auto* z1 = reinterpret_cast<double*>(base + o_z1);
+    auto* z2 = reinterpret_cast<double*>(base + o_z2);
+    const dk_status st = dk_ivf_query(v, Qd, nq, k, n_probe, 1, idx, d2, cnt, stream);
+    if (st != DK_OK) throw Error{st, dk_last_error()};
+    if (family == DK_LAPLACIAN) launch_eval_rows(h->X, n, 0, h->d, Qd, nq, family, bandwidth, idx, cnt, k, z1, s);
+    if (m > 0) {
+      auto* srt = reinterpret_cast<int64_t*>(base + o_s);
+      if (long_excl) launch_seg_sort_i64(idx, srt, cnt, k, nq, base + o_g, seg_bytes, s);
+      else launch_sort_excl(idx, cnt, k, nq, srt, s);
+      launch_sample(h->X, n, 0, n, h->d, Qd, nq, family, bandwidth, m, seed, query_base, srt, cnt, k, z2, nullptr,
+                    nullptr, s);
+    }
+    const bool v_dev = is_device_ptr(value_out);
+    double* vd = v_dev ? value_out : reinterpret_cast<double*>(base + o_v);
+    launch_deann_combine(nq, family, bandwidth, k, m, n, d2, z1, z2, vd, s, cnt);
+    bool sync = false;
+    if (!v_dev) {
+      DK_CUDA(cudaMemcpyAsync(value_out, vd, size_t(nq) * 8, cudaMemcpyDeviceToHost, s));
+      sync = true;
+    }
+    if (khat_out) {
+      DK_CUDA(cudaMemcpyAsync(khat_out, cnt, size_t(nq) * 4, cudaMemcpyDefault, s));
+      sync = sync || !is_device_ptr(khat_out);
+    }
+    if (sync) DK_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -287,28 +287,31 @@ __global__ void eval_rows_kernel(const float* __restrict__ X, int64_t n_local, i
   if (lane == 0) out[j] = s;
 }
 
-// value = (k/n) Z1 + ((n-k)/n) Z2   (estimators.py:344-372), one thread per query
+// value = (k^/n) Z1 + ((n-k^)/n) Z2   (estimators.py:344-372), one thread per query;
+// k^ = khat[j] neighbours (an index may return fewer than k, ann.py:30-31) or k
 __global__ void deann_combine_kernel(int64_t nq, int32_t family, double c, int32_t k, int32_t m, int64_t n,
-                                     const double* __restrict__ nbr_d2, const double* __restrict__ z1_l1_sum,
-                                     const double* __restrict__ z2_sum, double* __restrict__ value) {
+                                     const int32_t* __restrict__ khat, const double* __restrict__ nbr_d2,
+                                     const double* __restrict__ z1_l1_sum, const double* __restrict__ z2_sum,
+                                     double* __restrict__ value) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= nq) return;
+  const int kh = khat ? khat[j] : k;
   double z1 = 0.0;
-  if (k > 0) {
+  if (kh > 0) {
     if (family == DK_LAPLACIAN) {
-      z1 = z1_l1_sum[j] / double(k);
+      z1 = z1_l1_sum[j] / double(kh);
     } else {
       double s = 0.0;
-      for (int i = 0; i < k; ++i) {
+      for (int i = 0; i < kh; ++i) {
         double dd = nbr_d2[size_t(j) * k + i];
         if (family == DK_EXPONENTIAL) dd = sqrt(dd);
         s += exp(-dd * c);
       }
-      z1 = s / double(k);
+      z1 = s / double(kh);
     }
   }
-  double v = (double(k) / double(n)) * z1;
-  if (m > 0) v += (double(n - k) / double(n)) * (z2_sum[j] / double(m));
+  double v = (double(kh) / double(n)) * z1;
+  if (m > 0) v += (double(n - kh) / double(n)) * (z2_sum[j] / double(m));
   value[j] = v;
 }
 
@@ -397,9 +400,9 @@ void launch_kernel_values(int32_t family, double h, const double* dist, int64_t 
 
 void launch_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m, int64_t n_total,
                           const double* nbr_d2, const double* z1_l1_sum, const double* z2_sum, double* value,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int32_t* khat) {
   deann_combine_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(nq, family, family_c(family, bandwidth), k, m,
-                                                                  n_total, nbr_d2, z1_l1_sum, z2_sum, value);
+                                                                  n_total, khat, nbr_d2, z1_l1_sum, z2_sum, value);
   DK_CHECK_LAUNCH();
 }
 

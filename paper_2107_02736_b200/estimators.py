@@ -359,36 +359,23 @@ def _is_gpu_ivf(ann, ds: Dataset) -> bool:
 
 
 def _deann_ivf_batch(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, rng) -> list[Estimate]:
-    """DEANN over a batch with the GPU IVF index: one probed scan for all queries, neighbour
-    lists of per-query length k_hat (ann.py:30-31: a short probe set is not an error), then one
-    Philox sampling pass excluding each query's list (estimators.py:338-372)."""
+    """DEANN over a batch with the GPU IVF index, in one device call (dk_deann_ivf): one
+    probed query pass for all queries, neighbour lists of per-query length k_hat (ann.py:30-31:
+    a short probe set is not an error), Z1 from their distances, then one Philox sampling
+    pass excluding each query's list (estimators.py:338-372)."""
     n = ds.n
     nq = q.shape[0]
-    idx, d2, cnt = ann.query_batch(q, k)
-    cnt = np.ascontiguousarray(cnt, dtype=np.int32)
-    z1 = np.zeros(nq)
-    if spec.family is KernelFamily.LAPLACIAN:
-        sums = np.empty(nq, dtype=np.float64)
-        rows = np.ascontiguousarray(np.where(idx >= 0, idx, 0))
-        _lib.check(_lib.load().dk_eval_rows(ds.handle, q.ctypes.data, nq, _lib.DK_LAPLACIAN, spec.bandwidth,
-                                            rows.ctypes.data, cnt.ctypes.data, k, sums.ctypes.data, None))
-        z1 = np.where(cnt > 0, sums / np.maximum(cnt, 1), 0.0)
-    else:
-        dist = d2 if spec.family is KernelFamily.GAUSSIAN else np.sqrt(d2)
-        kv = np.where(idx >= 0, kernel_from_distance(spec, np.where(idx >= 0, dist, 0.0)), 0.0)
-        z1 = np.where(cnt > 0, kv.sum(axis=1) / np.maximum(cnt, 1), 0.0)
+    values = np.empty(nq, dtype=np.float64)
+    khat = np.empty(nq, dtype=np.int32)
+    seed, base = resolve_sampler(rng).take(nq) if m > 0 else (0, 0)
+    _lib.check(_lib.load().dk_deann_ivf(ann._dev.handle, q.ctypes.data, nq, _lib.family_code(spec.family),
+                                        spec.bandwidth, k, m, ann.n_probe, seed, base, values.ctypes.data,
+                                        khat.ctypes.data, _lib.current_stream()))
     if m == 0:
-        return [Estimate(value=(int(c) / n) * float(z), kernel_evals=int(c), neighbors_used=int(c), samples_used=0,
-                         truncated=int(c) < n) for c, z in zip(cnt, z1)]
-    seed, base = resolve_sampler(rng).take(nq)
-    excl = np.ascontiguousarray(np.where(idx >= 0, idx, 0))
-    z, _ = _sample_sums(ds, spec, q, m, seed, base, excl=excl, excl_cnt=cnt, stride=k)
-    out = []
-    for j in range(nq):
-        kh = int(cnt[j])
-        value = (kh / n) * float(z1[j]) + ((n - kh) / n) * float(z[j] / m)
-        out.append(Estimate(value=value, kernel_evals=kh + m, neighbors_used=kh, samples_used=m))
-    return out
+        return [Estimate(value=float(v), kernel_evals=int(c), neighbors_used=int(c), samples_used=0,
+                         truncated=int(c) < n) for c, v in zip(khat, values)]
+    return [Estimate(value=float(v), kernel_evals=int(c) + m, neighbors_used=int(c), samples_used=m)
+            for c, v in zip(khat, values)]
 
 
 def _deann_rsp(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, state, independent: bool) -> list[Estimate]:

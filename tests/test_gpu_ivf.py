@@ -295,3 +295,24 @@ def test_arbitrary_lists_empty_lists_ties_and_short_probes(seed):
             np.testing.assert_array_equal(idx[j, :cnt[j]], ri)
             np.testing.assert_allclose(d2[j, :cnt[j]], rd, rtol=1e-12, atol=1e-12)
             assert (idx[j, cnt[j]:] == -1).all()
+
+
+@pytest.mark.parametrize("family,h,m", [("gaussian", 1.2, 0), ("laplacian", 3.0, 40), ("exponential", 1.0, 40)])
+def test_deann_with_short_ivf_lists(family, h, m):
+    # the probed lists hold fewer than k rows: k_hat < k neighbours, Z1 and the weights use k_hat
+    n, d = 300, 6
+    X = np.random.default_rng(61).normal(size=(n, d)).astype(np.float32)
+    Q = np.random.default_rng(62).normal(size=(9, d))
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    ann = g.IvfAnnIndex.build(ds, 32, seed=2, n_probe=1)
+    k, seed = 50, 5
+    batch = g.deann_batch(ds, g.KernelSpec(family, h), ann, Q, k, m, rng=g.PhiloxSampler(seed))
+    cent, lists = O.ivf_build(od, 32, 2)
+    for j, q in enumerate(Q):
+        ri, rd = O.ivf_query(od, cent, lists, q, k, 1, formula=1)
+        assert len(ri) < k
+        ref = O.deann(od, family, h, NeighborReplay(ri, rd), q, k, m,
+                      rng=IndexReplay(seed, j, n) if m else None)
+        assert batch[j].neighbors_used == len(ri)
+        assert batch[j].samples_used == m
+        assert batch[j].value == pytest.approx(ref[0], rel=1e-12)
