@@ -211,8 +211,24 @@ constexpr int32_t kKnnCap = 8192;  // candidates per query before the exact-scan
 
 struct KnnPlan {
   int32_t seg_tiles = 1, nseg = 0, cap = 0, batch = 0;
+  int32_t stride = 1;  // TILEMIN visits every stride-th dataset tile
   bool tau_inf = false;
 };
+
+// The threshold sweep only needs SOME k disjoint point sets whose minima bound the
+// k-th distance: the k-th smallest segment minimum over any subset of the rows is
+// >= the k-th smallest distance over all rows.  Sweeping every stride-th tile cuts
+// that pass to 1/stride of the tensor work; the looser tau admits ~stride x more
+// candidates to the FILTER pass, whose cost barely depends on the count.
+int32_t knn_stride(int64_t ntiles, int64_t target) {
+  static const int env = [] {
+    const char* v = std::getenv("DK_KNN_STRIDE");  // A/B switch
+    return v ? std::max(1, std::atoi(v)) : 0;
+  }();
+  const int64_t auto_s = std::clamp<int64_t>(ntiles / (2 * target), 1, 4);
+  const int64_t s = env ? env : auto_s;
+  return int32_t(std::max<int64_t>(1, std::min<int64_t>(s, ntiles / target)));
+}
 
 KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
   KnnPlan p;
@@ -222,8 +238,10 @@ KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
     p.tau_inf = true;  // every row is a candidate
     p.cap = int32_t(h->n);
   } else if (ntiles >= target) {
-    p.seg_tiles = int32_t((ntiles + target - 1) / target);
-    p.nseg = int32_t((ntiles + p.seg_tiles - 1) / p.seg_tiles);
+    p.stride = knn_stride(ntiles, target);
+    const int64_t nvis = (ntiles + p.stride - 1) / p.stride;
+    p.seg_tiles = int32_t((nvis + target - 1) / target);
+    p.nseg = int32_t((nvis + p.seg_tiles - 1) / p.seg_tiles);
     p.cap = kKnnCap;
   } else {  // one segment per 64-column group of every tile
     p.seg_tiles = 0;
@@ -313,7 +331,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       a.enc = &e;
       a.n = h->n;
       a.n_pad = h->n_pad;
-      a.tile_stride = 1;
+      a.tile_stride = kp.stride;
       a.seg_tiles = kp.seg_tiles;
       a.tmin = tmin;
       launch_sweep(a, h->num_sms, s);
