@@ -118,6 +118,22 @@ __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, i
 #endif
 constexpr uint32_t kPolyPairs = DK_POLY_PAIRS;
 
+// Ping-pong epilogue for the KDE sweeps (single-CTA): the two accumulator buffers are
+// consumed by two different groups of 8 epilogue warps (group = accumulator), each warp
+// taking 128 columns of every other tile, so on every SM sub-partition one group's
+// TMEM loads and barrier waits overlap the other group's exponentials instead of all
+// four warps stalling together at every tile boundary.  c2: 2.704 -> 2.633 ms (A/B,
+// interleaved runs); split3 / exponential sweeps are MMA-bound and unchanged.  Issuing
+// the second 32-column TMEM load only after the first chunk's wait (to overlap it with
+// that chunk's math) measured slower (2.76 ms), as did 1 or 3 polynomial pairs (2.64).
+#ifndef DK_PINGPONG
+#define DK_PINGPONG 1
+#endif
+template <int MODE, bool kPair>
+__host__ __device__ constexpr bool use_pingpong() {
+  return DK_PINGPONG != 0 && !kPair && (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU || MODE == MODE_KDE_EXP);
+}
+
 // 2^t for a pair, t <= 0, on the FMA pipe: t = j + f (j = round(t), |f| <= 1/2),
 // 2^f by a degree-5 polynomial (relative error < 2.4e-7 on |f| <= 1/2, i.e. at the
 // level of ex2.approx), exponent j added to the float bits.  t is clamped at -126, so a
@@ -275,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // speculative exact-mode launch (capi.cu dk_naive): the host has not waited for the query
   // check, so a batch that turned out fractional skips this sweep and is redone in split3
   if (p.guard != nullptr && (*p.guard & 6u) != 0u) return;
+  constexpr bool kPP = use_pingpong<MODE, kPair>();
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the shared pointer itself, so the
   // compiler keeps the shared address space (LDS/ATOMS instead of generic LD/ATOM)
@@ -316,13 +333,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], kPair ? 2 * kNumEpiWarps : kNumEpiWarps);
+      mbar_init(&tempty_bar[a], kPair ? 2 * kNumEpiWarps : (kPP ? kNumEpiWarps / 2 : kNumEpiWarps));
     }
     mbar_init(afull_bar, 1);
     mbar_init(aempty_bar, 1);
     for (int x = 0; x < kXnSlots; ++x) {
       mbar_init(&xfull_bar[x], 1);
-      mbar_init(&xempty_bar[x], kNumEpiWarps);
+      mbar_init(&xempty_bar[x], kPP ? kNumEpiWarps / 2 : kNumEpiWarps);
     }
     fence_mbar_init();
   }
@@ -446,6 +463,63 @@ __global__ void __launch_bounds__(kThreads, 1)
           else mma_commit(aempty_bar);
         }
       }
+    }
+  } else if (kPP && warp >= kEpiWarp0) {
+    // ===================== ping-pong KDE epilogue =====================
+    // warp (quarter, cg): group = cg >> 1 owns accumulator `group` (tiles with titer % 2 ==
+    // group), half = cg & 1 its columns [128 half, 128 half + 128), in two 64-column steps
+    const int ew = int(warp) - kEpiWarp0;
+    const int quarter = int(warp & 3);
+    const int cg = ew >> 2;
+    const uint32_t group = uint32_t(cg >> 1);
+    const int half = cg & 1;
+    const int lrow = quarter * 32 + int(lane);
+    uint32_t ph = 0;  // phase of this group's accumulator barriers
+    uint32_t titer = 0;
+    const float m2s = *p.m2s;
+    const float negc = p.negc;
+    float mn_unused = 0.f;
+    for (int u = first_unit; u < nunits; u += unit_step) {
+      const int qb = u % ngroups, cc = u / ngroups;
+      const int t0 = cc * p.tiles_per_unit;
+      const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
+      const int row = qb * kBM + lrow;
+      const float qn = p.qn[row];
+      double usum = 0.0;
+      for (int t = t0; t < t1; ++t, ++titer) {
+        if ((titer & 1u) != group) continue;
+        const uint32_t xs = titer % kXnSlots;
+        DK_TWAIT(0, mbar_wait(&tfull_bar[group], ph));
+        tc_fence_after();
+        DK_TWAIT(1, mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1));
+        const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(group * kBN + half * 128);
+        const int64_t tbase = int64_t(t) * p.tile_stride * kBN + half * 128;
+        const float* xsm = smemX + xs * kBN + half * 128;
+        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll 1
+        for (int sub = 0; sub < 2; ++sub) {
+          uint32_t r0[32], r1[32];
+          const int64_t cbase = tbase + sub * 64;
+          const bool full = cbase + 64 <= p.n;
+          tmem_ld32(taddr + uint32_t(sub * 64), r0);
+          tmem_ld32(taddr + uint32_t(sub * 64 + 32), r1);
+          tmem_ld_wait();
+          if (sub == 1) {  // the whole 128-column slice is in registers: release the accumulator
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[group]);
+          }
+          epi_chunk<MODE>(r0, xsm + sub * 64, qn, m2s, negc, 0.f, full, cbase, p.n, a0, a1, mn_unused, p, row,
+                          nullptr, nullptr, lrow);
+          epi_chunk<MODE>(r1, xsm + sub * 64 + 32, qn, m2s, negc, 0.f, full, cbase + 32, p.n, a0, a1, mn_unused,
+                          p, row, nullptr, nullptr, lrow);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty_bar[xs]);
+        ph ^= 1u;
+        usum += double((a0.x + a0.y) + (a1.x + a1.y));
+      }
+      p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
     }
   } else if (warp >= kEpiWarp0) {
     // ===================== epilogue (each CTA, its own 128 rows) =====================
