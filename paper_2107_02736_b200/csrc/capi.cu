@@ -271,7 +271,7 @@ bool use_bigk(const dk_dataset* h, int32_t k, int64_t nq) {
   int B = 2, Kp = 32;
   while (B < kp.cap) B <<= 1;
   while (Kp < k) Kp <<= 1;
-  return size_t(B) * 8 + size_t(2 * Kp) * 16 + size_t(h->d) * 8 > 232448;  // launch_select_rerank's buffer
+  return size_t(B) * 8 + size_t(2 * Kp) * 16 + size_t(h->d) * 8 + 4096 > 232448;  // launch_select_rerank's buffer
 }
 
 // encoding for the k-NN sweeps: exact integers when possible, else single-pass

@@ -27,6 +27,8 @@ namespace dk {
 
 namespace {
 
+constexpr int kSelHist = 1024;  // histogram bins of the k-NN selection (4 per thread of a 256-thread block)
+
 struct Key128 {
   unsigned long long hi;  // fp64 bits of d2 (>= 0, so bit order == numeric order)
   unsigned long long lo;  // row index
@@ -161,22 +163,123 @@ __global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global
   const int c = int(craw);
   const int Kp = max(32, pow2_ceil(k));
   const int W = Kp;  // candidates re-ranked per round; Kp + W is a power of two for the bitonic merge
-  int Bc = 1;
-  while (Bc < c) Bc <<= 1;
-  Bc = max(Bc, 2);
   const unsigned long long* keys = cand + size_t(q) * cap;
-  for (int i = threadIdx.x; i < Bc; i += blockDim.x) sbuf[i] = i < c ? keys[i] : ~0ull;
-  bitonic_u64(sbuf, Bc);
   Key128* top = reinterpret_cast<Key128*>(sbuf + B);  // [Kp + W]
-  for (int i = threadIdx.x; i < Kp + W; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
-  __syncthreads();
   double* qv = reinterpret_cast<double*>(top + Kp + W);  // the query in shared memory
+  uint32_t* hist = reinterpret_cast<uint32_t*>(qv + d);   // [kSelHist]
   for (int j = threadIdx.x; j < d; j += blockDim.x) qv[j] = Q[size_t(q) * d + j];
-  __syncthreads();
   const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   constexpr int G = 8;  // lanes per candidate: 4 candidates per warp step
   const int grp = lane / G, gl = lane % G;
+
+  // ---- fast path: no sort of the whole candidate list.  T' = the largest approx key in the
+  // histogram bins up to the one holding the k-th smallest approx key (T' >= that key).  The
+  // k candidates with approx d2 <= T' have exact d2 <= T' + eps, so every member of the exact
+  // top k (ties included) has approx d2 <= T' + 2 eps: exactly those are evaluated and sorted.
+  if (c >= k) {
+    __shared__ uint32_t s_lo, s_hi, s_bstar, s_tmax, s_ns;
+    __shared__ uint32_t s_wsum[32];
+    if (threadIdx.x == 0) { s_lo = 0xffffffffu; s_hi = 0u; s_bstar = kSelHist - 1; s_tmax = 0u; s_ns = 0u; }
+    for (int i = threadIdx.x; i < kSelHist; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int i = threadIdx.x; i < c; i += blockDim.x) {
+      const unsigned long long v = keys[i];
+      sbuf[i] = v;
+      const uint32_t b = uint32_t(v >> 32);  // bits of an approx d2 >= 0: uint order == float order
+      lo = min(lo, b);
+      hi = max(hi, b);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
+    __syncthreads();
+    const float flo = __uint_as_float(s_lo), fhi = __uint_as_float(s_hi);
+    const float scale = fhi > flo ? float(kSelHist) / (fhi - flo) : 0.f;
+    // monotone bin of a key (NaN from 0 * inf lands in bin 0, i.e. still monotone)
+    auto bin_of = [&](uint32_t b) {
+      return min(max(__float2int_rz((__uint_as_float(b) - flo) * scale), 0), kSelHist - 1);
+    };
+    for (int i = threadIdx.x; i < c; i += blockDim.x) atomicAdd(&hist[bin_of(uint32_t(sbuf[i] >> 32))], 1u);
+    __syncthreads();
+    {  // block scan: thread t owns bins [4t, 4t + 4) (kSelHist = 4 * blockDim)
+      const int t = threadIdx.x;
+      const uint32_t h0 = hist[4 * t], h1 = hist[4 * t + 1], h2 = hist[4 * t + 2], h3 = hist[4 * t + 3];
+      const uint32_t own = h0 + h1 + h2 + h3;
+      uint32_t incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      uint32_t cum = incl - own;
+      for (int w = 0; w < warp; ++w) cum += s_wsum[w];
+      const uint32_t hh[4] = {h0, h1, h2, h3};
+      const uint32_t kk = uint32_t(k);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (cum < kk && cum + hh[j] >= kk) s_bstar = uint32_t(4 * t + j);
+        cum += hh[j];
+      }
+    }
+    __syncthreads();
+    const int bstar = int(s_bstar);
+    uint32_t tm = 0u;
+    for (int i = threadIdx.x; i < c; i += blockDim.x) {
+      const uint32_t b = uint32_t(sbuf[i] >> 32);
+      if (bin_of(b) <= bstar) tm = max(tm, b);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tm = max(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+    if (lane == 0) atomicMax(&s_tmax, tm);
+    __syncthreads();
+    const double thr = double(__uint_as_float(s_tmax)) + 2.0 * eps;
+    const int scap = Kp + W;
+    for (int i = threadIdx.x; i < c; i += blockDim.x) {
+      const unsigned long long v = sbuf[i];
+      if (double(__uint_as_float(uint32_t(v >> 32))) <= thr) {
+        const uint32_t pos = atomicAdd(&s_ns, 1u);
+        if (pos < uint32_t(scap)) top[pos].lo = v & 0xffffffffull;
+      }
+    }
+    __syncthreads();
+    const int ns = int(s_ns);
+    if (ns <= scap) {
+      int P = 2;
+      while (P < ns) P <<= 1;
+      for (int i0 = warp * (32 / G); i0 < ns; i0 += nwarps * (32 / G)) {
+        const int i = i0 + grp;
+        const bool ok = i < ns;
+        const unsigned long long col = ok ? top[i].lo : 0ull;
+        const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
+        if (gl == 0 && ok) top[i].hi = static_cast<unsigned long long>(__double_as_longlong(dd));
+      }
+      for (int i = ns + threadIdx.x; i < P; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
+      bitonic_k128(top, P);
+      if (threadIdx.x == 0) status[q] = 0;
+      for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const Key128 key = top[i];
+        idx_out[size_t(q) * k + i] = int64_t(key.lo) + global_offset;
+        d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(key.hi));
+      }
+      return;
+    }
+    __syncthreads();  // too many keys within 2 eps of the k-th: the sorted-rounds path below
+  }
+
+  int Bc = 1;
+  while (Bc < c) Bc <<= 1;
+  Bc = max(Bc, 2);
+  for (int i = threadIdx.x; i < Bc; i += blockDim.x) sbuf[i] = i < c ? keys[i] : ~0ull;
+  bitonic_u64(sbuf, Bc);
+  for (int i = threadIdx.x; i < Kp + W; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
+  __syncthreads();
   __shared__ int s_stop;
   for (int pos = 0; pos < c; pos += W) {
     for (int i0 = warp * (32 / G); i0 < W; i0 += nwarps * (32 / G)) {
@@ -318,7 +421,8 @@ void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, cons
   // candidates per query against a cap of 8192); counts above the cap overflow as before
   const int B = std::max(2, pow2_ceil(max_cnt > 0 ? std::min(max_cnt, cap) : cap));
   const int Kp = std::max(32, pow2_ceil(k));
-  const size_t smem = size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double);
+  const size_t smem =
+      size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double) + kSelHist * sizeof(uint32_t);
   set_dynamic_smem(select_rerank_kernel, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
   select_rerank_kernel<<<unsigned(nq), 256, smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,

@@ -223,10 +223,11 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
                                add2(q2, make_float2(xv.z, xv.w)));
         d2v[4 * j4] = da.x; d2v[4 * j4 + 1] = da.y; d2v[4 * j4 + 2] = db.x; d2v[4 * j4 + 3] = db.y;
       }
-      if (!full) {  // columns past n: +inf never wins a min and never passes the threshold
+      if (!full) {  // columns past n: +inf never wins a min; NaN never passes a threshold (not even +inf)
         const int lim = int(min(int64_t(32), n - cbase));
+        const float pad = MODE == MODE_FILTER ? __int_as_float(0x7fc00000) : __int_as_float(0x7f800000);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) d2v[j] = j < lim ? d2v[j] : __int_as_float(0x7f800000);
+        for (int j = 0; j < 32; ++j) d2v[j] = j < lim ? d2v[j] : pad;
       }
       if constexpr (MODE == MODE_TILEMIN) {
         float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[2], m3 = d2v[3];
