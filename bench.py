@@ -430,10 +430,30 @@ def measure_deann_c3(args, local):
     ms = e0.elapsed_time(e1) / steps
     cnt = ctypes.c_int64()
     _lib.check(lib.dk_last_launch_count(ds.handle, ctypes.byref(cnt)))
+    # per-kernel rooflines of the two dominant kernels (library CUDA events on the launch
+    # stream, separate untimed steps): the k-NN FILTER distance sweep against the tensor peak
+    # (algorithmic 2 d flops per pair, fp16 operands) and the Philox gather against HBM
+    # (algorithmic m accepted fp32 rows of d floats per query)
+    peaks = _peaks()
+    kroof = {}
+    for mode, name in ((1, "knn_filter_sweep"), (2, "sampling_gather")):
+        _lib.check(lib.dk_set_profiling(ds.handle, mode))
+        step(200 + mode)
+        kms, kfl, kby = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        _lib.check(lib.dk_last_kernel_ms(ds.handle, ctypes.byref(kms), ctypes.byref(kfl), ctypes.byref(kby)))
+        _lib.check(lib.dk_set_profiling(ds.handle, 0))
+        if mode == 1:
+            ach = kfl.value / (kms.value / 1e3) / 1e12
+            kroof[name] = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                           "frac": ach / peaks["bf16_tflops"], "kernel_ms": kms.value}
+        else:
+            ach = kby.value / (kms.value / 1e3) / 1e9
+            kroof[name] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                           "frac": ach / peaks["hbm_gbs"], "kernel_ms": kms.value}
     ds.free()
     return {"metric": "DEANN queries/sec (exact k=100 NN + m=1000 samples, gaussian) at n=1.2M, d=100",
             "value": W.Q.shape[0] / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
-            "gpu_launches_per_step": int(cnt.value),
+            "gpu_launches_per_step": int(cnt.value), "kernel_rooflines": kroof,
             "config": {"workload": "c3: 1,200,000 x 100 L2-normalised rows, 10,000 queries, h by median-1e-3 rule",
                        "bandwidth": h, "k": W.k, "m": W.m}}
 

@@ -254,6 +254,8 @@ dk_status dk_deann_ivf(dk_ivf_handle ivf, const double* Q, int64_t nq, int32_t f
  * of the dominant kernel of the last call on this handle (CUDA events on the
  * launching stream) and its algorithmic work. */
 dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* bytes);
+/* on: 0 = off, 1 = time the tile sweeps (KDE / k-NN distance tiles), 2 = time the
+ * sampling gathers (RS / DEANN residual estimators). */
 dk_status dk_set_profiling(dk_handle h, int32_t on);
 /* k-NN diagnostics accumulated on this handle (counted when DK_KNN_STATS is set
  * in the environment at fit time; fallbacks always): queries, total and max

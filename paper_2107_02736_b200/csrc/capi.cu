@@ -98,6 +98,7 @@ const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
   if (e.mode == mode) return e;
   const int32_t d = h->d;
   e.Kp = int32_t(round_up(mode == 1 ? 3 * int64_t(d) : d, kBK));
+  e.d = d;
   if (mode != 0) ensure_mu(h, s);
   e.mu = mode == 0 ? nullptr : h->mu;
   DK_CUDA(cudaMalloc(&e.B, size_t(h->n_pad) * e.Kp * sizeof(__half)));
@@ -180,8 +181,10 @@ struct ProfScope {
   dk_dataset* h;
   cudaStream_t s;
   cudaEvent_t e1 = nullptr;
-  ProfScope(dk_dataset* hh, cudaStream_t ss, double flops, double bytes) : h(hh), s(ss) {
-    if (!h->profiling) return;
+  // kind: 1 = tile sweep (the KDE / k-NN distance tiles), 2 = sampling gather; dk_set_profiling
+  // picks which kind is timed
+  ProfScope(dk_dataset* hh, cudaStream_t ss, double flops, double bytes, int kind) : h(hh), s(ss) {
+    if (h->profiling != kind) return;
     if (h->prof_used == h->prof_events.size()) {
       cudaEvent_t a, b;
       DK_CUDA(cudaEventCreate(&a));
@@ -351,7 +354,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       a.cand_cnt = cnt;
       a.cand = cand;
       a.cap = kp.cap;
-      ProfScope ps(h, s, 2.0 * double(h->d) * double(bn) * double(h->n), double(h->n_pad) * e.Kp * 2);
+      ProfScope ps(h, s, 2.0 * double(h->d) * double(bn) * double(h->n), double(h->n_pad) * e.Kp * 2, 1);
       launch_sweep(a, h->num_sms, s);
     }
     if (h->knn_stats) {
@@ -766,7 +769,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       double* part = at<double>(h->ws, o_part);
       double* od = out_dev ? out : at<double>(h->ws, o_out);
       {
-        ProfScope ps(h, s, 3.0 * double(h->d) * double(nq) * double(h->n), double(h->n) * h->d * 4);
+        ProfScope ps(h, s, 3.0 * double(h->d) * double(nq) * double(h->n), double(h->n) * h->d * 4, 1);
         launch_l1_kde(h->X, h->n, h->d, Qd, nq, 1.0 / bandwidth, part, &nparts, nullptr, s);
       }
       launch_reduce_partials(part, nparts, l1_nq_pad(nq), nq, scale, od, s);
@@ -842,7 +845,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       int32_t ncc = 0;
       a.ncc_out = &ncc;
       {
-        ProfScope ps(h, s, 2.0 * double(h->d) * double(cn) * double(h->n), double(h->n_pad) * e.Kp * 2);
+        ProfScope ps(h, s, 2.0 * double(h->d) * double(cn) * double(h->n), double(h->n_pad) * e.Kp * 2, 1);
         launch_sweep(a, h->num_sms, s);
       }
       launch_reduce_partials(a.part, ncc * kColGroups, pad, cn, scale, od + q0, s);
@@ -962,7 +965,7 @@ dk_status dk_sample(dk_handle h, const double* Q, int64_t nq, int32_t family, do
     const bool dr_dev = draws_out && is_device_ptr(draws_out);
     int64_t* drd = draws_out ? (dr_dev ? draws_out : at<int64_t>(h->ws, o_dr)) : nullptr;
     {
-      ProfScope ps(h, s, 0.0, double(nq) * m * h->d * 4.0);
+      ProfScope ps(h, s, 0.0, double(nq) * m * h->d * 4.0, 2);
       launch_sample(h->X, h->n, h->global_offset, h->global_n, h->d, Qd, nq, family, bandwidth, m, seed, query_base,
                     ex_sorted, cnt_d, excl ? excl_stride : 0, zd, accd, drd, s);
     }
@@ -1096,7 +1099,7 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
         else launch_sort_excl(idx, nullptr, k, nq, srt, s);
         ex = srt;
       }
-      ProfScope ps(h, s, 0.0, double(nq) * (m + k) * h->d * 4.0);
+      ProfScope ps(h, s, 0.0, double(nq) * m * h->d * 4.0, 2);  // accepted rows read
       launch_sample(h->X, h->n, 0, n, h->d, Qd, nq, family, bandwidth, m, seed, query_base, ex, nullptr,
                     k > 0 ? k : 0, z2, accd, nullptr, s);
     }
@@ -1173,7 +1176,7 @@ dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, 
     const bool z_dev = is_device_ptr(z_sum);
     double* zd = z_dev ? z_sum : at<double>(h->ws, o_z);
     {
-      ProfScope ps(h, s, 0.0, double(nq) * m * h->d * 4.0);
+      ProfScope ps(h, s, 0.0, double(nq) * m * h->d * 4.0, 2);
       launch_rsp_eval(h->X, h->n, h->d, Qd, nq, family, bandwidth, pos, cnt, start, len, zd, s);
     }
     if (!z_dev) copy_out(z_sum, zd, size_t(nq) * sizeof(double), s);
@@ -1186,7 +1189,8 @@ dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, 
 dk_status dk_set_profiling(dk_handle h, int32_t on) {
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");
-    h->profiling = on != 0;
+    DK_REQUIRE(on >= 0 && on <= 2, "profiling mode must be 0 (off), 1 (tile sweep) or 2 (sampling gather)");
+    h->profiling = on;
     h->prof_used = 0;
   });
 }

@@ -96,6 +96,7 @@ inline void set_dynamic_smem(K* kernel, size_t bytes) {
 struct Encoding {
   int mode = -1;            // 0 exact fp16, 1 split3, 2 fp16 single (lossy)
   int32_t Kp = 0;           // padded K (multiple of 64)
+  int32_t d = 0;            // data columns per part (K used = d, or 3d for split3)
   __half* B = nullptr;      // [n_pad][Kp]
   float* xn = nullptr;      // [n_pad] |x - mu|^2 in fp32
   double* mu = nullptr;     // [d] centring (nullptr = none)
@@ -148,7 +149,7 @@ struct dk_dataset {
   cudaEvent_t copy_ready = nullptr, copy_done = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
-  bool profiling = false;
+  int profiling = 0;  // 0 off, 1 tile sweeps, 2 sampling gathers (ProfScope kinds)
   double last_flops = 0, last_bytes = 0;
   int64_t launches = 0;
   // k-NN diagnostics (DK_KNN_STATS=1 in the environment): candidates per query, fallbacks

@@ -183,6 +183,14 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.tiles_per_unit = pl.tiles_per_unit;
   p.ncc = pl.ncc;
   p.kblocks = kblocks;
+#ifndef DK_KSKIP
+#define DK_KSKIP 1
+#endif
+  {
+    const int kused = e.mode == 1 ? 3 * e.d : e.d;  // columns holding data (the rest is zero padding)
+    const int rem = kused - (kblocks - 1) * kBK;
+    p.klast = DK_KSKIP && e.d > 0 && rem > 0 && rem <= kBK ? (rem + 15) / 16 : kBK / 16;
+  }
   p.a_resident = pl.a_resident;
   p.stages = pl.stages;
   p.xn = e.xn;

@@ -84,6 +84,7 @@ struct TileParams {
   int32_t tiles_per_unit;
   int32_t ncc;             // column chunks = ceil(ntiles / tiles_per_unit)
   int32_t kblocks;         // Kp / 64
+  int32_t klast;           // 16-wide MMA k-steps of the last K-block that touch real columns (1..4)
   int32_t a_resident;      // 1: query block loaded once per unit
   int32_t stages;          // B ring depth
   int32_t seg_tiles;       // TILEMIN: tiles per segment (0: one segment per 64-column group)
@@ -446,10 +447,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t abase = p.a_resident ? a0 + uint32_t(kb) * kABlockBytes : a0 + uint32_t(stage) * kABlockBytes;
             const uint32_t bbase = b0 + uint32_t(stage) * kBStage;
             const uint64_t ad = sw128_kmajor_desc(abase), bd = sw128_kmajor_desc(bbase);
+            // k-steps over the K padding only multiply zeros: skipped (c3 fp16 sweeps: 7 of 8)
+            const int ksteps = kb == p.kblocks - 1 ? p.klast : kBK / 16;
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
-              if constexpr (kPair) mma_f16_ss_pair(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
-              else mma_f16_ss(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+              if (k < ksteps) {
+                if constexpr (kPair) mma_f16_ss_pair(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+                else mma_f16_ss(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+              }
             }
             if constexpr (kPair) mma_commit_pair_mc(&empty_bar[stage], uint16_t(0x3));
             else mma_commit(&empty_bar[stage]);

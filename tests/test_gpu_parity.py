@@ -203,6 +203,28 @@ def test_knn_many_duplicates_fallback_path():
     assert (d2 == 0).all()
 
 
+def test_knn_small_dataset_selects_without_exact_fallback(monkeypatch):
+    # n <= 8192: every row is a candidate (tau = inf); the rows past n in the last tile
+    # must not be appended, or every query overflows into the exact-scan fallback
+    import ctypes
+
+    from paper_2107_02736_b200 import _lib
+
+    monkeypatch.setenv("DK_KNN_STATS", "1")
+    X = np.random.default_rng(8).normal(size=(3001, 24)).astype(np.float32)
+    ds = g.Dataset.from_array(X)
+    Q = np.random.default_rng(9).normal(size=(40, 24))
+    idx, _ = g.knn_batch(ds, Q, 17)
+    od = O.Data(X)
+    for j in range(len(Q)):
+        np.testing.assert_array_equal(idx[j], O.brute_force_knn(od, Q[j], 17)[0])
+    v = [ctypes.c_int64() for _ in range(4)]
+    _lib.check(_lib.load().dk_knn_stats(ds.handle, *[ctypes.byref(x) for x in v]))
+    queries, cand_sum, _, fallbacks = (x.value for x in v)
+    assert queries == len(Q) and fallbacks == 0
+    assert cand_sum == len(Q) * X.shape[0]
+
+
 def test_knn_out_of_range():
     ds = g.Dataset.from_array(np.random.default_rng(0).normal(size=(5, 2)).astype(np.float32))
     for bad in (0, 6):
