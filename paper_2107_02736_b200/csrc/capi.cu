@@ -286,6 +286,57 @@ int knn_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cudaS
   return m == 0 ? 0 : 2;
 }
 
+// Pruned FILTER pass (internal.h KnnClusters): for datasets of >= 512 tiles the rows are
+// grouped once by k-means into balls; each block of 128 queries (sorted by their nearest
+// ball) then sweeps only the tiles whose balls can hold a row inside some member's tau_q.
+// Exact: a tile is skipped only when (|q - c| - r)^2 > tau_q + eps_q for all its balls
+// and all queries of the block.  DK_KNN_PRUNE=0 turns it off.
+constexpr int64_t kPruneMinTiles = 512;
+bool knn_prune_enabled(const dk_dataset* h, const KnnPlan& kp) {
+  static const bool off = [] {
+    const char* v = std::getenv("DK_KNN_PRUNE");
+    return v != nullptr && std::atoi(v) == 0;
+  }();
+  if (off || kp.tau_inf || h->n_pad / kBN < kPruneMinTiles) return false;
+  return h->kc == nullptr || !h->kc->useless;
+}
+int32_t knn_cluster_count(const dk_dataset* h) {
+  static const int div = [] {
+    const char* v = std::getenv("DK_KNN_TILES_PER_BALL");  // A/B switch
+    return v ? std::max(1, std::atoi(v)) : 16;
+  }();
+  return int32_t(std::clamp<int64_t>(h->n_pad / kBN / div, 16, 4096));
+}
+
+void ensure_knn_clusters(dk_dataset* h, const Encoding& e, cudaStream_t s) {
+  if (h->kc != nullptr && h->kc->enc.mode == e.mode) return;
+  if (h->kc != nullptr) {  // encoding changed (precision pinned differently): rebuild
+    free_knn_clusters(*h->kc);
+    delete h->kc;
+    h->kc = nullptr;
+  }
+  std::unique_ptr<KnnClusters> kc(new KnnClusters());
+  build_knn_clusters(h, knn_cluster_count(h), 3, *kc, s);
+  Encoding& se = kc->enc;
+  se.Kp = e.Kp;
+  se.d = e.d;
+  se.mu = e.mu;
+  DK_CUDA(cudaMalloc(&se.B, size_t(h->n_pad) * se.Kp * sizeof(__half)));
+  DK_CUDA(cudaMalloc(&se.xn, size_t(h->n_pad) * sizeof(float)));
+  DK_CUDA(cudaMalloc(&se.sx, 2 * sizeof(float)));
+  // same rows, same centring: the power-of-two scale (from the max |value|) equals the k-NN
+  // encoding's, so the encoded queries serve both operands
+  launch_encode_rows(kc->xs, h->n, h->n_pad, h->d, e.mode, e.mu, se.Kp, se.B, se.xn, se.sx,
+                     reinterpret_cast<uint32_t*>(se.sx + 1), s);
+  se.xn_max = e.xn_max;
+  se.eps_rel = e.eps_rel;
+  se.tmap = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN));
+  se.tmap_half = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN / 2));
+  se.mode = e.mode;
+  DK_CUDA(cudaStreamSynchronize(s));
+  h->kc = kc.release();
+}
+
 // k-NN for nq queries already on the device; idx/d2 outputs on the device.
 void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t* idx_d, double* d2_d,
                 cudaStream_t s, size_t ws_off_base) {
@@ -312,12 +363,51 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
   const size_t o_status = pl.add<int32_t>(bpad);
   const size_t o_list = pl.add<int32_t>(bpad);
   const size_t o_max = pl.add<uint32_t>(1);
+  const bool prune = knn_prune_enabled(h, kp);
+  const int32_t ntiles = int32_t(h->n_pad / kBN);
+  const int32_t nqb_max = bpad / kBM;
+  const int32_t Cn = knn_cluster_count(h);
+  size_t o_dq = 0, o_near = 0, o_qperm = 0, o_qp = 0, o_tidx = 0, o_td2 = 0, o_tlist = 0, o_tcnt = 0, o_ul = 0;
+  if (prune) {
+    o_dq = pl.add<double>(size_t(bpad) * Cn);
+    o_near = pl.add<int32_t>(bpad);
+    o_qperm = pl.add<int32_t>(bpad);
+    o_qp = pl.add<double>(size_t(bpad) * h->d);
+    o_tidx = pl.add<int64_t>(size_t(bpad) * k);
+    o_td2 = pl.add<double>(size_t(bpad) * k);
+    o_tlist = pl.add<int32_t>(size_t(nqb_max) * ntiles);
+    o_tcnt = pl.add<int32_t>(nqb_max);
+    o_ul = pl.add<int32_t>(size_t(3) * nqb_max * (ntiles / 8 + 2));
+  }
   if (pl.off > h->ws.cap) throw Error{DK_ECUDA, "internal: k-NN workspace under-reserved"};
+  if (prune) ensure_knn_clusters(h, e, s);
   const float inf = std::numeric_limits<float>::infinity();
   for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
     const int64_t bn = std::min<int64_t>(bpad, nq - b0);
     const int32_t bn_pad = int32_t(query_pad(bn));
     const double* Qb = Qd + b0 * h->d;
+    int64_t* idx_b = idx_d + b0 * k;
+    double* d2_b = d2_d + b0 * k;
+    int32_t* qperm = nullptr;
+    std::vector<int32_t> perm_h;
+    if (prune) {  // order the batch by nearest ball so each block of 128 queries is local
+      double* dq = at<double>(h->ws, o_dq);
+      int32_t* near = at<int32_t>(h->ws, o_near);
+      launch_query_cluster_dist(Qb, bn, h->d, h->kc->cent, h->kc->C, dq, near, s);
+      std::vector<int32_t> nh(static_cast<size_t>(bn));
+      DK_CUDA(cudaMemcpyAsync(nh.data(), near, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaStreamSynchronize(s));
+      perm_h.resize(static_cast<size_t>(bn));
+      for (int64_t i = 0; i < bn; ++i) perm_h[size_t(i)] = int32_t(i);
+      std::stable_sort(perm_h.begin(), perm_h.end(), [&](int32_t a, int32_t b) { return nh[size_t(a)] < nh[size_t(b)]; });
+      qperm = at<int32_t>(h->ws, o_qperm);
+      DK_CUDA(cudaMemcpyAsync(qperm, perm_h.data(), size_t(bn) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      double* Qp = at<double>(h->ws, o_qp);
+      launch_gather_rows_f64(Qb, qperm, bn, h->d, Qp, s);
+      Qb = Qp;
+      idx_b = at<int64_t>(h->ws, o_tidx);
+      d2_b = at<double>(h->ws, o_td2);
+    }
     QueryOperand q = encode_queries(h, e, Qb, bn, bn_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
                                     at<float>(h->ws, o_scal), s);
     float* tau = at<float>(h->ws, o_tau);
@@ -342,11 +432,42 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     }
     launch_fill_float(tau + bn, bn_pad - bn, -inf, s);
     DK_CUDA(cudaMemsetAsync(cnt, 0, size_t(bn_pad) * sizeof(uint32_t), s));
+    std::vector<int32_t> ul;
+    if (prune) {
+      const int32_t nqb = bn_pad / kBM;
+      int32_t* tlist = at<int32_t>(h->ws, o_tlist);
+      int32_t* tcnt = at<int32_t>(h->ws, o_tcnt);
+      launch_block_tile_lists(at<double>(h->ws, o_dq), h->kc->C, qperm, bn, nqb, tau, q.qn, e.xn_max, e.eps_rel,
+                              h->kc->rad, h->kc->tclo, h->kc->tchi, ntiles, tlist, tcnt, s);
+      std::vector<int32_t> tc(static_cast<size_t>(nqb));
+      DK_CUDA(cudaMemcpyAsync(tc.data(), tcnt, size_t(nqb) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaStreamSynchronize(s));
+      int64_t active = 0;
+      for (int32_t v : tc) active += v;
+      // units of ~equal length so the 148 persistent CTAs finish together
+      const int64_t U = std::max<int64_t>(8, (active + 4 * h->num_sms - 1) / (4 * h->num_sms));
+      for (int32_t b = 0; b < nqb; ++b)
+        for (int64_t i = 0; i < tc[size_t(b)]; i += U) {
+          ul.push_back(b);
+          ul.push_back(int32_t(int64_t(b) * ntiles + i));
+          ul.push_back(int32_t(int64_t(b) * ntiles + std::min<int64_t>(tc[size_t(b)], i + U)));
+        }
+      if (ul.size() > size_t(3) * nqb_max * (ntiles / 8 + 2)) throw Error{DK_ECUDA, "internal: unit list overflow"};
+      if (!ul.empty())
+        DK_CUDA(cudaMemcpyAsync(at<int32_t>(h->ws, o_ul), ul.data(), ul.size() * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+      // nearly every tile survives (unclustered data): stop paying for the ordering
+      if (active > int64_t(0.6 * double(nqb) * double(ntiles))) h->kc->useless = true;
+      if (h->knn_stats)
+        std::fprintf(stderr, "[dk] pruned k-NN: %lld of %lld (block, tile) pairs swept (%.1f%%), %d balls\n",
+                     (long long)active, (long long)nqb * ntiles, 100.0 * double(active) / (double(nqb) * ntiles),
+                     int(h->kc->C));
+    }
     {
       SweepArgs a{};
       a.mode = MODE_FILTER;
       a.qop = &q;
-      a.enc = &e;
+      a.enc = prune ? &h->kc->enc : &e;
       a.n = h->n;
       a.n_pad = h->n_pad;
       a.tile_stride = 1;
@@ -354,6 +475,11 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       a.cand_cnt = cnt;
       a.cand = cand;
       a.cap = kp.cap;
+      if (prune) {
+        a.ulist = at<int32_t>(h->ws, o_ul);
+        a.tlist = at<int32_t>(h->ws, o_tlist);
+        a.nunits_list = int32_t(ul.size() / 3);
+      }
       ProfScope ps(h, s, 2.0 * double(h->d) * double(bn) * double(h->n), double(h->n_pad) * e.Kp * 2, 1);
       launch_sweep(a, h->num_sms, s);
     }
@@ -369,8 +495,10 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     }
     int32_t* status = at<int32_t>(h->ws, o_status);
     const uint32_t cmax = max_count(cnt, bn, at<uint32_t>(h->ws, o_max), s);
-    launch_select_rerank(h->X, h->global_offset, h->d, Qb, bn, k, cand, cnt, kp.cap, q.qn, e.xn_max, e.eps_rel,
-                         idx_d + b0 * k, d2_d + b0 * k, status, s, int32_t(std::min<uint32_t>(cmax, 1u << 30)));
+    // pruned: candidates are positions in the cluster-sorted rows (read from there, reported as row ids)
+    launch_select_rerank(prune ? h->kc->xs : h->X, h->global_offset, h->d, Qb, bn, k, cand, cnt, kp.cap, q.qn,
+                         e.xn_max, e.eps_rel, idx_b, d2_b, status, s, int32_t(std::min<uint32_t>(cmax, 1u << 30)),
+                         prune ? h->kc->perm : nullptr);
     std::vector<int32_t> st(static_cast<size_t>(bn));
     DK_CUDA(cudaMemcpyAsync(st.data(), status, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     DK_CUDA(cudaStreamSynchronize(s));
@@ -380,11 +508,12 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     if (!fail.empty()) {
       int32_t* list = at<int32_t>(h->ws, o_list);
       DK_CUDA(cudaMemcpyAsync(list, fail.data(), fail.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, list, int32_t(fail.size()), k,
-                                idx_d + b0 * k, d2_d + b0 * k, s);
+      launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, list, int32_t(fail.size()), k, idx_b,
+                                d2_b, s);
       DK_CUDA(cudaStreamSynchronize(s));
     }
     h->knn_fallbacks += int64_t(fail.size());
+    if (prune) launch_scatter_knn(idx_b, d2_b, qperm, bn, k, idx_d + b0 * k, d2_d + b0 * k, s);
   }
 }
 
@@ -404,6 +533,18 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
   pl.add<int32_t>(kp.batch);
   pl.add<int32_t>(kp.batch);
   pl.add<uint32_t>(1);
+  if (knn_prune_enabled(h, kp)) {  // the pruned FILTER's buffers (knn_device)
+    const int32_t ntiles = int32_t(h->n_pad / kBN), nqb = kp.batch / kBM;
+    pl.add<double>(size_t(kp.batch) * knn_cluster_count(h));
+    pl.add<int32_t>(kp.batch);
+    pl.add<int32_t>(kp.batch);
+    pl.add<double>(size_t(kp.batch) * h->d);
+    pl.add<int64_t>(size_t(kp.batch) * k);
+    pl.add<double>(size_t(kp.batch) * k);
+    pl.add<int32_t>(size_t(nqb) * ntiles);
+    pl.add<int32_t>(nqb);
+    pl.add<int32_t>(size_t(3) * nqb * (ntiles / 8 + 2));
+  }
   return pl.off + 4096;
 }
 
@@ -704,6 +845,10 @@ dk_status dk_free(dk_handle h) {
     free_encoding(h->enc_exact);
     free_encoding(h->enc_split);
     free_encoding(h->enc_fp16);
+    if (h->kc) {
+      free_knn_clusters(*h->kc);
+      delete h->kc;
+    }
     if (h->X) cudaFree(h->X);
     if (h->xn64) cudaFree(h->xn64);
     if (h->mu) cudaFree(h->mu);

@@ -107,6 +107,23 @@ struct Encoding {
   CUtensorMap tmap_half;    // B boxes of 128 rows (2-CTA pair sweep: each CTA loads half)
 };
 
+// Cluster-sorted copy of the rows for the pruned k-NN FILTER pass (ivf.cu build,
+// capi.cu knn_device): rows grouped by a few Lloyd iterations of k-means, the sweep
+// operand re-encoded in that order (same scale and centring as the k-NN encoding, so
+// the query operand is shared), and per-cluster balls (centroid, radius) that bound
+// the distance from a query to every row of a tile from below.
+struct KnnClusters {
+  int32_t C = 0;
+  double* cent = nullptr;    // [C][d] centroids (fp64)
+  double* rad = nullptr;     // [C] max |x - cent| over the members, inflated by 1e-12 relative
+  int64_t* perm = nullptr;   // [n] sorted position -> dataset row
+  float* xs = nullptr;       // [n][d] rows in sorted order
+  int32_t* tclo = nullptr;   // [ntiles] first / last cluster of each 256-row tile of the sorted rows
+  int32_t* tchi = nullptr;
+  Encoding enc;              // sweep operand of xs (mode of the k-NN encoding)
+  bool useless = false;      // measured: pruning keeps most tiles -> not used
+};
+
 // Growable device scratch, carved per call.
 struct Workspace {
   uint8_t* base = nullptr;
@@ -153,6 +170,7 @@ struct dk_dataset {
   double last_flops = 0, last_bytes = 0;
   int64_t launches = 0;
   // k-NN diagnostics (DK_KNN_STATS=1 in the environment): candidates per query, fallbacks
+  dk::KnnClusters* kc = nullptr;  // pruned k-NN (built on the first large k-NN call)
   bool knn_stats = false;
   int64_t knn_queries = 0, knn_cand_sum = 0, knn_cand_max = 0, knn_fallbacks = 0;
 };
@@ -202,6 +220,11 @@ struct SweepArgs {
   int32_t cap;
   int32_t seg_tiles;          // TILEMIN: tiles per segment
   const uint32_t* guard;      // optional device flags: skip the sweep if (*guard & 6) (see TileParams)
+  // tile-list mode (FILTER over pruned lists): unit u = (query block ulist[3u], list positions
+  // [ulist[3u+1], ulist[3u+2])) of the flat tile list tlist
+  const int32_t* ulist;
+  const int32_t* tlist;
+  int32_t nunits_list;
 };
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms);  // doubles needed for KDE partials
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
@@ -224,6 +247,21 @@ void launch_eval_rows(const float* X, int64_t n_local, int64_t global_offset, in
                       int32_t family, double bandwidth, const int64_t* rows, const int32_t* cnt, int32_t stride,
                       double* out, cudaStream_t s);
 
+// pruned k-NN (ivf.cu / knn.cu)
+void build_knn_clusters(dk_dataset* h, int32_t C, int32_t iters, KnnClusters& kc, cudaStream_t s);
+void free_knn_clusters(KnnClusters& kc);
+// dq[j][c] = |q_j - cent_c| (fp64 direct difference), nearest[j] = argmin_c dq[j][c]
+void launch_query_cluster_dist(const double* Q, int64_t nq, int32_t d, const double* cent, int32_t C, double* dq,
+                               int32_t* nearest, cudaStream_t s);
+// per block of 128 permuted queries: the tiles whose clusters can hold a row with approx d2 <= tau_q
+void launch_block_tile_lists(const double* dq, int32_t C, const int32_t* qperm, int64_t bn, int32_t nqb,
+                             const float* tau, const float* qn, float xn_max, float eps_rel, const double* rad,
+                             const int32_t* tclo, const int32_t* tchi, int32_t ntiles, int32_t* tlist,
+                             int32_t* tcount, cudaStream_t s);
+void launch_gather_rows_f64(const double* Q, const int32_t* perm, int64_t nq, int32_t d, double* out, cudaStream_t s);
+void launch_scatter_knn(const int64_t* idx_p, const double* d2_p, const int32_t* perm, int64_t nq, int32_t k,
+                        int64_t* idx_out, double* d2_out, cudaStream_t s);
+
 // k-NN selection
 void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
                           float xn_max, float eps_rel, float* tau, cudaStream_t s);
@@ -231,7 +269,7 @@ void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s);
 void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
                           const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
                           float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* status,
-                          cudaStream_t s, int32_t max_cnt = 0);
+                          cudaStream_t s, int32_t max_cnt = 0, const int64_t* perm = nullptr);
 uint32_t max_count(const uint32_t* v, int64_t n, uint32_t* scratch, cudaStream_t s);  // synchronises
 void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
                                const int32_t* qlist, int32_t nlist, int32_t k, int64_t* idx_out, double* d2_out,

@@ -1317,7 +1317,99 @@ void restore_rows(dk_ivf* v) {
   v->lists = true;
 }
 
+// per cluster: max fp64 distance of its members (list order) to the centroid, inflated
+__global__ void cluster_radius_kernel(const float* __restrict__ xs, const int64_t* __restrict__ off, int32_t d,
+                                      const double* __restrict__ cent, double* __restrict__ rad) {
+  const int c = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double smax[32];
+  double mx = 0.0;
+  for (int64_t r = off[c] + w; r < off[c + 1]; r += nw) {
+    double acc = 0.0;
+    for (int j = lane; j < d; j += 32) {
+      const double t = double(xs[r * d + j]) - cent[size_t(c) * d + j];
+      acc = fma(t, t, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    mx = fmax(mx, acc);
+  }
+  if (lane == 0) smax[w] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < nw; ++i) m = fmax(m, smax[i]);
+    rad[c] = sqrt(m) * (1.0 + 1e-12) + 1e-300;
+  }
+}
+
+__global__ void tile_range_kernel(const int32_t* __restrict__ ls, int64_t n, int32_t ntiles, int32_t* __restrict__ lo,
+                                  int32_t* __restrict__ hi) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int64_t a = int64_t(t) * 256;
+  if (a >= n) { lo[t] = 1; hi[t] = 0; return; }  // padding tile: empty range
+  lo[t] = ls[a];
+  hi[t] = ls[min(n, a + 256) - 1];
+}
+
 }  // namespace
+
+// Cluster-sorted rows for the pruned k-NN (internal.h KnnClusters): C centroids seeded
+// with evenly spaced rows, `iters` Lloyd rounds (fp64 assignment, member means), then the
+// rows in cluster order, per-cluster radii and per-tile cluster ranges.
+void build_knn_clusters(dk_dataset* h, int32_t C, int32_t iters, KnnClusters& kc, cudaStream_t s) {
+  DK_CUDA(cudaStreamSynchronize(s));
+  std::unique_ptr<dk_ivf, IvfDeleter> v(new dk_ivf());
+  v->ds = h;
+  v->C = C;
+  v->d = h->d;
+  v->n = h->n;
+  DK_CUDA(cudaMalloc(&v->cent, size_t(C) * v->d * sizeof(double)));
+  DK_CUDA(cudaMalloc(&v->cnorm, size_t(C) * sizeof(double)));
+  DK_CUDA(cudaMalloc(&v->labels, size_t(v->n) * sizeof(int32_t)));
+  DK_CUDA(cudaMalloc(&v->labels_s, size_t(v->n) * sizeof(int32_t)));
+  DK_CUDA(cudaMalloc(&v->ids, size_t(v->n) * sizeof(int64_t)));
+  DK_CUDA(cudaMalloc(&v->rows, size_t(v->n) * sizeof(int64_t)));
+  DK_CUDA(cudaMalloc(&v->offsets, size_t(C + 1) * sizeof(int64_t)));
+  DK_CUDA(cudaMalloc(&v->d2min, size_t(v->n) * sizeof(double)));
+  DK_CUDA(cudaMalloc(&v->scal, 4 * sizeof(double)));
+  v->temp_bytes = cub_bytes(v->n);
+  DK_CUDA(cudaMalloc(&v->temp, v->temp_bytes));
+  for (int c = 0; c < C; ++c) {
+    set_row_kernel<<<1, 128>>>(h->X, (int64_t(c) * v->n) / C, v->d, v->cent + size_t(c) * v->d);
+    DK_CHECK_LAUNCH();
+  }
+  for (int it = 0; it < iters; ++it) {
+    assign(v.get());
+    build_lists(v.get());
+    update_centroids(v.get());
+  }
+  restore_rows(v.get());
+  const int32_t ntiles = int32_t(h->n_pad / 256);
+  kc.C = C;
+  DK_CUDA(cudaMalloc(&kc.rad, size_t(C) * sizeof(double)));
+  DK_CUDA(cudaMalloc(&kc.tclo, size_t(ntiles) * sizeof(int32_t)));
+  DK_CUDA(cudaMalloc(&kc.tchi, size_t(ntiles) * sizeof(int32_t)));
+  cluster_radius_kernel<<<unsigned(C), 256>>>(v->xs, v->offsets, v->d, v->cent, kc.rad);
+  DK_CHECK_LAUNCH();
+  tile_range_kernel<<<unsigned((ntiles + 255) / 256), 256>>>(v->labels_s, v->n, ntiles, kc.tclo, kc.tchi);
+  DK_CHECK_LAUNCH();
+  DK_CUDA(cudaDeviceSynchronize());
+  kc.cent = v->cent; v->cent = nullptr;   // ownership moves to kc
+  kc.perm = v->rows; v->rows = nullptr;
+  kc.xs = v->xs; v->xs = nullptr;
+}
+
+void free_knn_clusters(KnnClusters& kc) {
+  for (void* p : {static_cast<void*>(kc.cent), static_cast<void*>(kc.rad), static_cast<void*>(kc.perm),
+                  static_cast<void*>(kc.xs), static_cast<void*>(kc.tclo), static_cast<void*>(kc.tchi)})
+    if (p) cudaFree(p);
+  for (void* p : {static_cast<void*>(kc.enc.B), static_cast<void*>(kc.enc.xn), static_cast<void*>(kc.enc.sx)})
+    if (p) cudaFree(p);
+  kc = KnnClusters{};
+}
+
 }  // namespace dk
 
 using namespace dk;

@@ -151,7 +151,9 @@ __global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global
                                      const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt,
                                      int32_t cap, const float* __restrict__ qn, float xn_max, float eps_rel,
                                      int32_t B, int64_t* __restrict__ idx_out, double* __restrict__ d2_out,
-                                     int32_t* __restrict__ status) {
+                                     int32_t* __restrict__ status, const int64_t* __restrict__ perm) {
+  // candidates are row positions of X; perm (optional) maps a position to the reported row id,
+  // which is also the tie-break key (pruned k-NN: X holds the cluster-sorted rows)
   extern __shared__ unsigned long long sbuf[];
   const int64_t q = blockIdx.x;
   if (q >= nq) return;
@@ -258,7 +260,10 @@ __global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global
         const bool ok = i < ns;
         const unsigned long long col = ok ? top[i].lo : 0ull;
         const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
-        if (gl == 0 && ok) top[i].hi = static_cast<unsigned long long>(__double_as_longlong(dd));
+        if (gl == 0 && ok) {
+          top[i].hi = static_cast<unsigned long long>(__double_as_longlong(dd));
+          if (perm != nullptr) top[i].lo = static_cast<unsigned long long>(perm[col]);
+        }
       }
       for (int i = ns + threadIdx.x; i < P; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
       bitonic_k128(top, P);
@@ -288,7 +293,8 @@ __global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global
       const unsigned long long col = ok ? (sbuf[pos + i] & 0xffffffffull) : 0ull;
       const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
       if (gl == 0 && i < W)
-        top[Kp + i] = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)), col}
+        top[Kp + i] = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)),
+                                  perm != nullptr ? static_cast<unsigned long long>(perm[col]) : col}
                          : Key128{~0ull, ~0ull};
     }
     bitonic_k128(top, Kp + W);
@@ -385,7 +391,180 @@ __global__ void fill_float_kernel(float* p, int64_t count, float v) {
   if (i < count) p[i] = v;
 }
 
+// ---------------------------------------------------------------- pruned k-NN helpers
+
+// dq[j][c] = |q_j - cent_c| in fp64 (direct difference).  Block: 32 queries x 64 clusters,
+// d in chunks of 32 through shared memory, 2 queries x 4 clusters per thread.
+__global__ void __launch_bounds__(256) query_cluster_dist_kernel(const double* __restrict__ Q, int64_t nq, int32_t d,
+                                                                 const double* __restrict__ cent, int32_t C,
+                                                                 double* __restrict__ dq) {
+  __shared__ double qs[32][33];
+  __shared__ double cs[64][33];
+  const int64_t q0 = int64_t(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 64;
+  const int tq = threadIdx.x >> 4, tc = threadIdx.x & 15;  // queries tq, tq+16; clusters tc + 16 i
+  double acc[2][4] = {};
+  for (int k0 = 0; k0 < d; k0 += 32) {
+    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+      const int r = i >> 5, k = i & 31;
+      qs[r][k] = (q0 + r < nq && k0 + k < d) ? Q[(q0 + r) * d + k0 + k] : 0.0;
+    }
+    for (int i = threadIdx.x; i < 64 * 32; i += 256) {
+      const int r = i >> 5, k = i & 31;
+      cs[r][k] = (c0 + r < C && k0 + k < d) ? cent[size_t(c0 + r) * d + k0 + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const double a0 = qs[tq][k], a1 = qs[tq + 16][k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double b = cs[tc + 16 * i][k];
+        const double t0 = a0 - b, t1 = a1 - b;
+        acc[0][i] = fma(t0, t0, acc[0][i]);
+        acc[1][i] = fma(t1, t1, acc[1][i]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int64_t q = q0 + tq + 16 * a;
+    if (q >= nq) continue;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = c0 + tc + 16 * i;
+      if (c < C) dq[q * C + c] = sqrt(acc[a][i]);
+    }
+  }
+}
+
+__global__ void nearest_cluster_kernel(const double* __restrict__ dq, int64_t nq, int32_t C,
+                                       int32_t* __restrict__ nearest) {
+  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  double best = INFINITY;
+  int bi = 0;
+  for (int c = lane; c < C; c += 32) {
+    const double v = dq[q * C + c];
+    if (v < best) { best = v; bi = c; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if (lane == 0) nearest[q] = bi;
+}
+
+// Tile list of one block of 128 (permuted) queries: cluster c is needed when some query
+// of the block can see a row of its ball with approx d2 <= tau_q, i.e. (|q - cent_c| -
+// rad_c)^2 <= tau_q + eps_q (approx d2 >= exact d2 - eps_q); a tile is needed when any
+// cluster of its range is.  fp64 slack: dq shrunk by 1e-12 relative (rad is inflated at
+// build), the threshold grown by 1e-6 relative.
+__global__ void __launch_bounds__(256) block_tile_lists_kernel(
+    const double* __restrict__ dq, int32_t C, const int32_t* __restrict__ qperm, int64_t bn,
+    const float* __restrict__ tau, const float* __restrict__ qn, float xn_max, float eps_rel,
+    const double* __restrict__ rad, const int32_t* __restrict__ tclo, const int32_t* __restrict__ tchi,
+    int32_t ntiles, int32_t* __restrict__ tlist, int32_t* __restrict__ tcount) {
+  extern __shared__ uint8_t need[];
+  __shared__ int s_wcnt[8];
+  __shared__ int s_base;
+  const int qb = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = int64_t(qb) * 128;
+  const int rows = int(bn - r0 < 128 ? bn - r0 : 128);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    bool nd = false;
+    const double rc = rad[c];
+    for (int i = 0; i < rows && !nd; ++i) {
+      const int64_t row = r0 + i;
+      const double thr = (double(tau[row]) + double(eps_rel) * (double(qn[row]) + double(xn_max))) * (1.0 + 1e-6);
+      const double lb = fmax(dq[int64_t(qperm[row]) * C + c] * (1.0 - 1e-12) - rc, 0.0);
+      nd = lb * lb <= thr;
+    }
+    need[c] = nd ? 1 : 0;
+  }
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int t0 = 0; t0 < ntiles; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    bool on = false;
+    if (t < ntiles)
+      for (int c = tclo[t]; c <= tchi[t] && !on; ++c) on = need[c] != 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) s_wcnt[warp] = __popc(b);
+    __syncthreads();
+    int off = s_base;
+    for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+    if (on) tlist[int64_t(qb) * ntiles + off + __popc(b & ((1u << lane) - 1u))] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < 8; ++w) tot += s_wcnt[w];
+      s_base += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tcount[qb] = s_base;
+}
+
+__global__ void gather_rows_f64_kernel(const double* __restrict__ Q, const int32_t* __restrict__ perm, int64_t nq,
+                                       int32_t d, double* __restrict__ out) {
+  const int64_t i = blockIdx.x;
+  if (i >= nq) return;
+  const int64_t src = perm[i];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) out[i * d + j] = Q[src * d + j];
+}
+
+__global__ void scatter_knn_kernel(const int64_t* __restrict__ idx_p, const double* __restrict__ d2_p,
+                                   const int32_t* __restrict__ perm, int64_t nq, int32_t k,
+                                   int64_t* __restrict__ idx_out, double* __restrict__ d2_out) {
+  const int64_t i = blockIdx.x;
+  if (i >= nq) return;
+  const int64_t dst = perm[i];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    idx_out[dst * k + j] = idx_p[i * k + j];
+    d2_out[dst * k + j] = d2_p[i * k + j];
+  }
+}
+
 }  // namespace
+
+void launch_query_cluster_dist(const double* Q, int64_t nq, int32_t d, const double* cent, int32_t C, double* dq,
+                               int32_t* nearest, cudaStream_t s) {
+  if (nq <= 0) return;
+  dim3 grid(unsigned((nq + 31) / 32), unsigned((C + 63) / 64));
+  query_cluster_dist_kernel<<<grid, 256, 0, s>>>(Q, nq, d, cent, C, dq);
+  DK_CHECK_LAUNCH();
+  nearest_cluster_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(dq, nq, C, nearest);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_block_tile_lists(const double* dq, int32_t C, const int32_t* qperm, int64_t bn, int32_t nqb,
+                             const float* tau, const float* qn, float xn_max, float eps_rel, const double* rad,
+                             const int32_t* tclo, const int32_t* tchi, int32_t ntiles, int32_t* tlist,
+                             int32_t* tcount, cudaStream_t s) {
+  set_dynamic_smem(block_tile_lists_kernel, size_t(C));
+  block_tile_lists_kernel<<<unsigned(nqb), 256, size_t(C), s>>>(dq, C, qperm, bn, tau, qn, xn_max, eps_rel, rad,
+                                                                 tclo, tchi, ntiles, tlist, tcount);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_gather_rows_f64(const double* Q, const int32_t* perm, int64_t nq, int32_t d, double* out, cudaStream_t s) {
+  if (nq <= 0) return;
+  gather_rows_f64_kernel<<<unsigned(nq), 128, 0, s>>>(Q, perm, nq, d, out);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_scatter_knn(const int64_t* idx_p, const double* d2_p, const int32_t* perm, int64_t nq, int32_t k,
+                        int64_t* idx_out, double* d2_out, cudaStream_t s) {
+  if (nq <= 0) return;
+  scatter_knn_kernel<<<unsigned(nq), 128, 0, s>>>(idx_p, d2_p, perm, nq, k, idx_out, d2_out);
+  DK_CHECK_LAUNCH();
+}
 
 uint32_t max_count(const uint32_t* v, int64_t n, uint32_t* scratch, cudaStream_t s) {
   DK_CUDA(cudaMemsetAsync(scratch, 0, sizeof(uint32_t), s));
@@ -416,7 +595,7 @@ void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64
 void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
                           const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
                           float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* status,
-                          cudaStream_t s, int32_t max_cnt) {
+                          cudaStream_t s, int32_t max_cnt, const int64_t* perm) {
   // candidate buffer sized by the largest count actually seen (occupancy: c3 averages ~200
   // candidates per query against a cap of 8192); counts above the cap overflow as before
   const int B = std::max(2, pow2_ceil(max_cnt > 0 ? std::min(max_cnt, cap) : cap));
@@ -426,7 +605,7 @@ void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, cons
   set_dynamic_smem(select_rerank_kernel, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
   select_rerank_kernel<<<unsigned(nq), 256, smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,
-                                                       xn_max, eps_rel, B, idx_out, d2_out, status);
+                                                       xn_max, eps_rel, B, idx_out, d2_out, status, perm);
   DK_CHECK_LAUNCH();
 }
 

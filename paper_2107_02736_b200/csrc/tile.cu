@@ -168,7 +168,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const int ntiles_all = int(a.n_pad / kBN);
   const int ntiles = (ntiles_all + a.tile_stride - 1) / a.tile_stride;
   const int nqb = q.nq_pad / kBM;
-  const bool pr = use_pair(nqb);
+  const bool pr = a.ulist == nullptr && use_pair(nqb);
   const int ngroups = pr ? nqb / 2 : nqb;
   const int nslots = pr ? num_sms / 2 : num_sms;  // CTAs (or CTA pairs) resident at once
   const Plan pl = make_plan(kblocks, ntiles, ngroups, nslots, a.mode, pr);
@@ -204,10 +204,15 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.cand = a.cand;
   p.cap = a.cap;
   p.seg_tiles = a.seg_tiles;
+  p.ulist = a.ulist;
+  p.tlist = a.tlist;
+  p.nunits_list = a.nunits_list;
   p.guard = a.guard;
   if (a.ncc_out) *a.ncc_out = pl.ncc;
 
-  const int nunits = ngroups * pl.ncc;
+  const int nunits = a.ulist != nullptr ? a.nunits_list : ngroups * pl.ncc;
+  if (nunits <= 0) return;
+  if (a.ulist != nullptr && (pr || a.mode != MODE_FILTER)) throw Error{DK_EINVAL, "internal: tile lists are FILTER-only"};
   const int grid = std::min(nunits, nslots) * (pr ? 2 : 1);
   const CUtensorMap& tb = pr ? e.tmap_half : e.tmap;
   switch (a.mode) {

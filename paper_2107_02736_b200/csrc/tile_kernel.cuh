@@ -88,6 +88,11 @@ struct TileParams {
   int32_t a_resident;      // 1: query block loaded once per unit
   int32_t stages;          // B ring depth
   int32_t seg_tiles;       // TILEMIN: tiles per segment (0: one segment per 64-column group)
+  // tile-list mode (FILTER over pruned per-block lists, capi.cu knn_device): unit u covers query
+  // block ulist[3u] and positions [ulist[3u+1], ulist[3u+2]) of tlist (tile ids of the sweep operand)
+  const int32_t* ulist;
+  const int32_t* tlist;
+  int32_t nunits_list;
   const float* xn;         // [n_pad] |x|^2 (encoding-consistent)
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
@@ -158,19 +163,6 @@ __device__ __forceinline__ float2 exp2_poly2(float2 t) {
   r.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(tr.x) << 23));
   r.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(tr.y) << 23));
   return r;
-}
-
-__device__ __forceinline__ void candidate(float d2, int64_t col, int row, const TileParams& p, uint32_t* scnt,
-                                          unsigned long long* sbuf, int lrow) {
-  const unsigned long long key =
-      (static_cast<unsigned long long>(__float_as_uint(fmaxf(d2, 0.f))) << 32) | static_cast<unsigned long long>(col);
-  const uint32_t pos = atomicAdd(&scnt[lrow], 1u);
-  if (pos < uint32_t(kStageCap)) {
-    sbuf[lrow * kStageCap + pos] = key;
-  } else {  // dense region: spill straight to the global list
-    const uint32_t g = atomicAdd(&p.cand_cnt[row], 1u);
-    if (g < uint32_t(p.cap)) p.cand[size_t(row) * p.cap + g] = key;
-  }
 }
 
 // One 32-column chunk of the epilogue.  `full` = all 32 columns valid (warp-uniform).
@@ -252,13 +244,29 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
 #pragma unroll
           for (int j = 0; j < 32; ++j) hits |= (d2v[j] <= tau ? 1u : 0u) << j;
         }
-        while (hits) {  // rare: appended candidates
-          const int j = __ffs(hits) - 1;
-          hits &= hits - 1;
-          float dj = d2v[0];
+        if (hits) {  // appended candidates: one shared (and at most one global) atomic per chunk
+          const uint32_t nh = uint32_t(__popc(hits));
+          const uint32_t pos = atomicAdd(&scnt[lrow], nh);
+          const uint32_t first_spill = max(pos, uint32_t(kStageCap));
+          const uint32_t nspill = pos + nh > first_spill ? pos + nh - first_spill : 0u;
+          const uint32_t g = nspill ? atomicAdd(&p.cand_cnt[row], nspill) : 0u;
+          uint32_t slot = pos;
+          while (hits) {
+            const int j = __ffs(hits) - 1;
+            hits &= hits - 1;
+            float dj = d2v[0];
 #pragma unroll
-          for (int i = 1; i < 32; ++i) dj = (i == j) ? d2v[i] : dj;
-          candidate(dj, cbase + j, row, p, scnt, sbuf, lrow);
+            for (int i = 1; i < 32; ++i) dj = (i == j) ? d2v[i] : dj;
+            const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(fmaxf(dj, 0.f))) << 32) |
+                                           static_cast<unsigned long long>(cbase + j);
+            if (slot < uint32_t(kStageCap)) {
+              sbuf[lrow * kStageCap + slot] = key;
+            } else {  // dense region: straight to the global list
+              const uint32_t gi = g + (slot - first_spill);
+              if (gi < uint32_t(p.cap)) p.cand[size_t(row) * p.cap + gi] = key;
+            }
+            ++slot;
+          }
         }
       }
     }
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool leader = crank == 0;
   // work units: (query-block group, column chunk); a pair owns 2 query blocks
   const int ngroups = kPair ? p.nqb / 2 : p.nqb;
-  const int nunits = ngroups * p.ncc;
+  const int nunits = p.ulist != nullptr ? p.nunits_list : ngroups * p.ncc;
   const int first_unit = kPair ? int(blockIdx.x) / 2 : int(blockIdx.x);
   const int unit_step = kPair ? int(gridDim.x) / 2 : int(gridDim.x);
 
@@ -371,9 +379,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int uiter = 0;
       uint32_t titer = 0;
       for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
-        const int qb = (u % ngroups) * (kPair ? 2 : 1) + int(crank), cc = u / ngroups;
-        const int t0 = cc * p.tiles_per_unit;
-        const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
+        int qb = (u % ngroups) * (kPair ? 2 : 1) + int(crank), cc = u / ngroups;
+        int t0 = cc * p.tiles_per_unit;
+        int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
+        if (p.ulist != nullptr) { qb = p.ulist[3 * u]; t0 = p.ulist[3 * u + 1]; t1 = p.ulist[3 * u + 2]; }
         if (p.a_resident) {
           mbar_wait(aempty_bar, (uiter & 1) ^ 1);
           if constexpr (kPair) {
@@ -387,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         for (int t = t0; t < t1; ++t, ++titer) {
-          const int col0 = t * p.tile_stride * kBN;
+          const int col0 = (p.tlist != nullptr ? p.tlist[t] : t * p.tile_stride) * kBN;
           {  // column norms of this tile -> own smem ring slot
             const uint32_t xs = titer % kXnSlots;
             mbar_wait(&xempty_bar[xs], ((titer / kXnSlots) & 1) ^ 1);
@@ -431,8 +440,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t a0 = smem_u32(smemA), b0 = smem_u32(smemB);
       for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
         const int cc = u / ngroups;
-        const int t0 = cc * p.tiles_per_unit;
-        const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
+        int t0 = cc * p.tiles_per_unit;
+        int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
+        if (p.ulist != nullptr) { t0 = p.ulist[3 * u + 1]; t1 = p.ulist[3 * u + 2]; }
         if (p.a_resident) {
           mbar_wait(afull_bar, uiter & 1);
           tc_fence_after();
@@ -542,9 +552,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long tepi0 = clock64();
 #endif
     for (int u = first_unit; u < nunits; u += unit_step) {
-      const int qb = (u % ngroups) * (kPair ? 2 : 1) + int(crank), cc = u / ngroups;
-      const int t0 = cc * p.tiles_per_unit;
-      const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
+      int qb = (u % ngroups) * (kPair ? 2 : 1) + int(crank), cc = u / ngroups;
+      int t0 = cc * p.tiles_per_unit;
+      int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
+      if (p.ulist != nullptr) { qb = p.ulist[3 * u]; t0 = p.ulist[3 * u + 1]; t1 = p.ulist[3 * u + 2]; }
       const int row = qb * kBM + lrow;
       const float qn = p.qn[row];
       float tau = 0.f;
@@ -588,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&xempty_bar[xs]);
           continue;
         }
-        const int64_t cbase = int64_t(t) * p.tile_stride * kBN + cg * 64;
+        const int64_t cbase = int64_t(p.tlist != nullptr ? p.tlist[t] : t * p.tile_stride) * kBN + cg * 64;
         const float* xsm = smemX + xs * kBN + cg * 64;
         const bool full = cbase + 64 <= p.n;
         float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
