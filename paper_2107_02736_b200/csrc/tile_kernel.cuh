@@ -395,8 +395,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_2d(smemA + size_t(kb) * kABlockBytes, &tmapA, afull_bar, kb * kBK, qb * kBM, pol_a);
           }
         }
+        // tile-list mode: the next tile id is loaded one tile ahead (off the issue path)
+        int tnext = (p.tlist != nullptr && t0 < t1) ? __ldg(p.tlist + t0) : 0;
         for (int t = t0; t < t1; ++t, ++titer) {
-          const int col0 = (p.tlist != nullptr ? p.tlist[t] : t * p.tile_stride) * kBN;
+          int col0;
+          if (p.tlist != nullptr) {
+            col0 = tnext * kBN;
+            if (t + 1 < t1) tnext = __ldg(p.tlist + t + 1);
+          } else {
+            col0 = t * p.tile_stride * kBN;
+          }
           {  // column norms of this tile -> own smem ring slot
             const uint32_t xs = titer % kXnSlots;
             mbar_wait(&xempty_bar[xs], ((titer / kXnSlots) & 1) ^ 1);

@@ -225,6 +225,30 @@ def test_knn_small_dataset_selects_without_exact_fallback(monkeypatch):
     assert cand_sum == len(Q) * X.shape[0]
 
 
+def test_knn_pruned_path_clustered_ties_and_far_queries():
+    # >= 512 tiles: the FILTER pass runs over k-means balls (capi.cu knn_device, pruned);
+    # duplicated rows (ties across balls), queries on data points, between clusters and far
+    # outside every ball must all give the brute-force answer (ann.py:82-102 tie rule)
+    rng = np.random.default_rng(21)
+    cent = rng.normal(0.0, 4.0, size=(40, 24))
+    lab = rng.integers(0, 40, size=300_000)
+    X = (cent[lab] + rng.normal(0.0, 1.0, size=(300_000, 24))).astype(np.float32)
+    X[250_000:250_500] = X[1000:1500]  # exact duplicates far apart in row order
+    ds = g.Dataset.from_array(X)
+    Q = np.concatenate([
+        X[[1000, 1001, 77, 299_999]].astype(np.float64),                 # on data points (ties)
+        0.5 * (cent[:6] + cent[6:12]),                                   # between clusters
+        rng.normal(0.0, 40.0, size=(4, 24)),                             # far outside every ball
+        cent[lab[:6]] + rng.normal(0.0, 1.0, size=(6, 24)),             # ordinary
+    ])
+    idx, d2 = g.knn_batch(ds, Q, 30)
+    od = O.Data(X)
+    for j in range(len(Q)):
+        ri, rd = O.brute_force_knn(od, Q[j], 30)
+        np.testing.assert_array_equal(idx[j], ri)
+        np.testing.assert_allclose(d2[j], rd, rtol=1e-9, atol=1e-12)
+
+
 def test_knn_out_of_range():
     ds = g.Dataset.from_array(np.random.default_rng(0).normal(size=(5, 2)).astype(np.float32))
     for bad in (0, 6):
