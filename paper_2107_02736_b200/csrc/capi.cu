@@ -433,6 +433,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     launch_fill_float(tau + bn, bn_pad - bn, -inf, s);
     DK_CUDA(cudaMemsetAsync(cnt, 0, size_t(bn_pad) * sizeof(uint32_t), s));
     std::vector<int32_t> ul;
+    int64_t active = 0;  // (block, tile) pairs the pruned FILTER sweeps
     if (prune) {
       const int32_t nqb = bn_pad / kBM;
       int32_t* tlist = at<int32_t>(h->ws, o_tlist);
@@ -442,7 +443,6 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       std::vector<int32_t> tc(static_cast<size_t>(nqb));
       DK_CUDA(cudaMemcpyAsync(tc.data(), tcnt, size_t(nqb) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaStreamSynchronize(s));
-      int64_t active = 0;
       for (int32_t v : tc) active += v;
       // units of ~equal length so the 148 persistent CTAs finish together
       const int64_t U = std::max<int64_t>(8, (active + 4 * h->num_sms - 1) / (4 * h->num_sms));
@@ -480,7 +480,9 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
         a.tlist = at<int32_t>(h->ws, o_tlist);
         a.nunits_list = int32_t(ul.size() / 3);
       }
-      ProfScope ps(h, s, 2.0 * double(h->d) * double(bn) * double(h->n), double(h->n_pad) * e.Kp * 2, 1);
+      // work of the tiles actually swept (all of them unless pruned)
+      const double pairs = prune ? double(active) * kBM * kBN : double(bn) * double(h->n);
+      ProfScope ps(h, s, 2.0 * double(h->d) * pairs, double(h->n_pad) * e.Kp * 2, 1);
       launch_sweep(a, h->num_sms, s);
     }
     if (h->knn_stats) {
