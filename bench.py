@@ -432,7 +432,8 @@ def measure_deann_c3(args, local):
     _lib.check(lib.dk_last_launch_count(ds.handle, ctypes.byref(cnt)))
     # per-kernel rooflines of the two dominant kernels (library CUDA events on the launch
     # stream, separate untimed steps): the k-NN FILTER distance sweep against the tensor peak
-    # (algorithmic 2 d flops per pair, fp16 operands) and the Philox gather against HBM
+    # (2 d flops per (query, row) pair of the tiles it visits — the ball-pruned lists — fp16
+    # operands) and the Philox gather against HBM
     # (algorithmic m accepted fp32 rows of d floats per query)
     peaks = _peaks()
     kroof = {}
