@@ -124,11 +124,17 @@ __device__ __forceinline__ double group_row_kernel(const float* __restrict__ x, 
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;  // the family's distance sum (squared L2 or L1); kernel value by kernel_of_sum
+}
+
+// kernel value from a distance sum: exp(-d2 c) gaussian, exp(-sqrt(d2) c) exponential,
+// exp(-L1 c) laplacian (c = 1/(2h^2) or 1/h)
+__device__ __forceinline__ double kernel_of_sum(double acc, int family, double c) {
   if (family == DK_EXPONENTIAL) acc = sqrt(acc);
   return exp(-acc * c);
 }
 
-// Kernel value of one row from float4s already in registers (IT per lane, same
+// Distance sum of one row from float4s already in registers (IT per lane, same
 // accumulation order as group_row_kernel: lane gl takes chunks gl, gl+G, ...).
 template <int G, int IT>
 __device__ __forceinline__ double group_row_regs(const float4 (&xv)[IT], const double* __restrict__ q, int chunks,
@@ -147,8 +153,7 @@ __device__ __forceinline__ double group_row_regs(const float4 (&xv)[IT], const d
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (family == DK_EXPONENTIAL) acc = sqrt(acc);
-  return exp(-acc * c);
+  return acc;
 }
 
 template <int G, int IT>
@@ -201,6 +206,14 @@ __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int6
     const uint32_t took = __ballot_sync(0xffffffffu, take);
     const int ntook = __popc(took);
     __syncwarp();
+    // each group reduces its row's distance sum; batch row r's sum is handed to lane r, which
+    // evaluates the fp64 exponential once for the batch (not once per lane of every group)
+    double lane_sum = 0.0;
+    auto hand_over = [&](int r0, double acc) {
+      const int src = ((lane - r0) & (R - 1)) * G;  // group (lane - r0) holds row lane's sum
+      const double a = __shfl_sync(0xffffffffu, acc, src);
+      if (lane >= r0 && lane < r0 + R) lane_sum = a;
+    };
     if constexpr (IT > 0) {
       // software-pipelined: the next row's float4s are in flight while this one is reduced
       const int chunks = d >> 2;
@@ -213,8 +226,7 @@ __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int6
         const int64_t locn = rn < ntook ? rows_s[rn] - global_offset : -1;
         const bool minen = locn >= 0 && locn < n_local;
         if (r0 + R < ntook) load_row<G, IT>(X + size_t(minen ? locn : 0) * d, minen, chunks, gl, nxt);
-        const double v = group_row_regs<G, IT>(cur, q, chunks, family, c, gl);
-        if (mine && gl == 0) zsum += v;
+        hand_over(r0, group_row_regs<G, IT>(cur, q, chunks, family, c, gl));
 #pragma unroll
         for (int it = 0; it < IT; ++it) cur[it] = nxt[it];
         mine = minen;
@@ -225,9 +237,12 @@ __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int6
         const int64_t loc = r < ntook ? rows_s[r] - global_offset : -1;
         const bool mine = loc >= 0 && loc < n_local;
         // groups with no row still take part in the shuffles (G-lane reduction is warp-synchronous)
-        const double v = group_row_kernel<G>(X + size_t(mine ? loc : 0) * d, q, d, family, c, gl);
-        if (mine && gl == 0) zsum += v;
+        hand_over(r0, group_row_kernel<G>(X + size_t(mine ? loc : 0) * d, q, d, family, c, gl));
       }
+    }
+    if (lane < ntook) {
+      const int64_t loc = rows_s[lane] - global_offset;
+      if (loc >= 0 && loc < n_local) zsum += kernel_of_sum(lane_sum, family, c);
     }
     __syncwarp();
     if (took) last_t = int64_t(t_base) + 31 - __clz(took);
