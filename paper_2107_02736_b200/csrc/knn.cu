@@ -20,6 +20,7 @@
 //      exceeds the current exact k-th distance; output sorted by (d2, idx).
 //   4. queries whose candidate list overflowed take an exact fp64 full scan.
 #include <cfloat>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -101,6 +102,65 @@ __global__ void tau_from_tmin_kernel(const float* __restrict__ tmin, int32_t nse
       t = v + 2.f * eps;
       t = __fmul_ru(t, 1.0f + 2.4e-7f);  // absorb the rounding of the addition itself
     }
+    tau[q] = t;
+  }
+}
+
+// Same tau by a 4-pass 8-bit radix select of the k-th smallest segment minimum (the
+// minima are >= 0, so their float bits order like the values): no sort of all segments.
+__global__ void __launch_bounds__(256) tau_radix_kernel(const float* __restrict__ tmin, int32_t nseg, int32_t nq_pad,
+                                                        int64_t nq, int32_t k, const float* __restrict__ qn,
+                                                        float xn_max, float eps_rel, float* __restrict__ tau) {
+  extern __shared__ uint32_t vals[];
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_digit, s_below;
+  const int64_t q = blockIdx.x;
+  if (q >= nq) return;
+  if (nseg < k) {
+    if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
+    return;
+  }
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) vals[i] = __float_as_uint(fmaxf(tmin[size_t(i) * nq_pad + q], 0.f));
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0u, mask = 0u, krem = uint32_t(k);
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    hist[threadIdx.x] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+      const uint32_t v = vals[i];
+      if ((v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // lane l owns bins [8l, 8l + 8)
+      uint32_t own = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) own += hist[8 * lane + j];
+      uint32_t incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      uint32_t cum = incl - own;
+      if (cum < krem && incl >= krem) {
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t h = hist[8 * lane + j];
+          if (cum + h >= krem) { s_digit = uint32_t(8 * lane + j); s_below = cum; break; }
+          cum += h;
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= s_digit << shift;
+    mask |= 255u << shift;
+    krem -= s_below;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const float v = __uint_as_float(prefix);  // the k-th smallest segment minimum
+    const float eps = eps_rel * (qn[q] + xn_max);
+    float t = v + 2.f * eps;
+    t = __fmul_ru(t, 1.0f + 2.4e-7f);  // as tau_from_tmin_kernel
     tau[q] = t;
   }
 }
@@ -584,6 +644,15 @@ void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s) {
 
 void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
                           float xn_max, float eps_rel, float* tau, cudaStream_t s) {
+  static const bool sort_path = std::getenv("DK_TAU_SORT") != nullptr;  // A/B switch
+  if (!sort_path) {
+    const size_t smem = size_t(std::max(nseg, 1)) * 4;
+    if (smem > 232448) throw Error{DK_EINVAL, "too many k-NN segments"};
+    set_dynamic_smem(tau_radix_kernel, smem);
+    tau_radix_kernel<<<unsigned(nq), 256, smem, s>>>(tmin, nseg, nq_pad, nq, k, qn, xn_max, eps_rel, tau);
+    DK_CHECK_LAUNCH();
+    return;
+  }
   const int B = std::max(2, pow2_ceil(nseg));
   const size_t smem = size_t(B) * 8;
   if (smem > 232448) throw Error{DK_EINVAL, "too many k-NN segments"};
