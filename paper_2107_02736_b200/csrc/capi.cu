@@ -397,9 +397,12 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       std::vector<int32_t> nh(static_cast<size_t>(bn));
       DK_CUDA(cudaMemcpyAsync(nh.data(), near, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaStreamSynchronize(s));
+      // stable counting sort by nearest ball (keys < C): O(bn + C) on the host
       perm_h.resize(static_cast<size_t>(bn));
-      for (int64_t i = 0; i < bn; ++i) perm_h[size_t(i)] = int32_t(i);
-      std::stable_sort(perm_h.begin(), perm_h.end(), [&](int32_t a, int32_t b) { return nh[size_t(a)] < nh[size_t(b)]; });
+      std::vector<int32_t> start(size_t(h->kc->C) + 1, 0);
+      for (int64_t i = 0; i < bn; ++i) ++start[size_t(nh[size_t(i)]) + 1];
+      for (int32_t c = 0; c < h->kc->C; ++c) start[size_t(c) + 1] += start[size_t(c)];
+      for (int64_t i = 0; i < bn; ++i) perm_h[size_t(start[size_t(nh[size_t(i)])]++)] = int32_t(i);
       qperm = at<int32_t>(h->ws, o_qperm);
       DK_CUDA(cudaMemcpyAsync(qperm, perm_h.data(), size_t(bn) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
       double* Qp = at<double>(h->ws, o_qp);
