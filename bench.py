@@ -445,8 +445,12 @@ def measure_deann_c3(args, local):
         _lib.check(lib.dk_set_profiling(ds.handle, 0))
         if mode == 1:
             ach = kfl.value / (kms.value / 1e3) / 1e12
+            # the FILTER sweep skips the tiles no neighbour can be in (ball-pruned lists):
+            # dense_equivalent = the work of an unpruned sweep over the kernel's time
+            dense = 2.0 * W.X.shape[1] * W.Q.shape[0] * W.X.shape[0] / (kms.value / 1e3) / 1e12
             kroof[name] = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                           "frac": ach / peaks["bf16_tflops"], "kernel_ms": kms.value}
+                           "frac": ach / peaks["bf16_tflops"], "kernel_ms": kms.value,
+                           "dense_equivalent_tflops": dense}
         else:
             ach = kby.value / (kms.value / 1e3) / 1e9
             kroof[name] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
