@@ -259,13 +259,15 @@ KnnPlan plan_knn(const dk_dataset* h, int32_t k, int64_t nq) {
   }
   const int64_t budget = int64_t(1) << 30;  // bytes of candidate storage per batch
   int64_t b = budget / (int64_t(p.cap) * 8 + int64_t(p.nseg) * 4 + 64);
-  b = std::max<int64_t>(2 * kBM, std::min<int64_t>(16384, b)) / (2 * kBM) * (2 * kBM);
+  int64_t bmax = 16384;
+  if (const char* v = std::getenv("DK_KNN_MAX_BATCH")) bmax = std::max<int64_t>(2 * kBM, std::atoll(v));  // tests
+  b = std::max<int64_t>(2 * kBM, std::min<int64_t>(bmax, b)) / (2 * kBM) * (2 * kBM);
   p.batch = int32_t(std::min<int64_t>(b, query_pad(nq)));
   return p;
 }
 
 // The tile path's selection keeps the candidate list and 2*pow2(k) keys in one
-// CTA's shared memory (knn.cu launch_select_rerank); plans that do not fit —
+// CTA's shared memory (knn.cu select_slow_kernel); plans that do not fit —
 // k > 4096, or every row a candidate because fewer segment minima than k exist
 // to bound tau — take the exact fp64 + radix-sort path instead (bigk.cu).
 bool use_bigk(const dk_dataset* h, int32_t k, int64_t nq) {
@@ -274,7 +276,7 @@ bool use_bigk(const dk_dataset* h, int32_t k, int64_t nq) {
   int B = 2, Kp = 32;
   while (B < kp.cap) B <<= 1;
   while (Kp < k) Kp <<= 1;
-  return size_t(B) * 8 + size_t(2 * Kp) * 16 + size_t(h->d) * 8 + 4096 > 232448;  // launch_select_rerank's buffer
+  return size_t(B) * 8 + size_t(2 * Kp) * 16 + size_t(h->d) * 8 + 4096 > 232448;  // select_slow_kernel's buffer
 }
 
 // encoding for the k-NN sweeps: exact integers when possible, else single-pass
@@ -292,13 +294,12 @@ int knn_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cudaS
 // Exact: a tile is skipped only when (|q - c| - r)^2 > tau_q + eps_q for all its balls
 // and all queries of the block.  DK_KNN_PRUNE=0 turns it off.
 constexpr int64_t kPruneMinTiles = 512;
-bool knn_prune_enabled(const dk_dataset* h, const KnnPlan& kp) {
+bool knn_prunable(const dk_dataset* h, const KnnPlan& kp) {
   static const bool off = [] {
     const char* v = std::getenv("DK_KNN_PRUNE");
     return v != nullptr && std::atoi(v) == 0;
   }();
-  if (off || kp.tau_inf || h->n_pad / kBN < kPruneMinTiles) return false;
-  return h->kc == nullptr || !h->kc->useless;
+  return !(off || kp.tau_inf || h->kc_failed || h->n_pad / kBN < kPruneMinTiles);
 }
 int32_t knn_cluster_count(const dk_dataset* h) {
   static const int div = [] {
@@ -308,36 +309,140 @@ int32_t knn_cluster_count(const dk_dataset* h) {
   return int32_t(std::clamp<int64_t>(h->n_pad / kBN / div, 16, 4096));
 }
 
-void ensure_knn_clusters(dk_dataset* h, const Encoding& e, cudaStream_t s) {
-  if (h->kc != nullptr && h->kc->enc.mode == e.mode) return;
+// Whether this call prunes (internal.h KnnClusters: the swept fraction of earlier calls,
+// read without waiting; unclustered data turns pruning off, re-tested every 32nd call).
+bool knn_prune_decide(dk_dataset* h) {
+  KnnClusters* kc = h->kc;
+  if (kc == nullptr) return true;
+  if (kc->stat_pending) {
+    const cudaError_t q = cudaEventQuery(kc->stat_ev);
+    if (q == cudaSuccess) {
+      kc->stat_pending = false;
+      const bool wide = double(kc->stat_host[0]) > 0.6 * kc->stat_total;
+      kc->over = wide ? kc->over + 1 : 0;
+      if (kc->over >= 3) kc->useless = true;
+    } else if (q == cudaErrorNotReady) {
+      (void)cudaGetLastError();
+    } else {
+      DK_CUDA(q);
+    }
+  }
+  if (kc->useless) {
+    if (++kc->off_calls < 32) return false;
+    kc->useless = false;
+    kc->over = 0;
+    kc->off_calls = 0;
+  }
+  return true;
+}
+
+// Builds the cluster-sorted copy on the first pruned call.  Returns false (and disables
+// pruning for the handle) when it does not fit in device memory: the unpruned sweep is exact.
+bool ensure_knn_clusters(dk_dataset* h, const Encoding& e, cudaStream_t s) {
+  if (h->kc != nullptr && h->kc->enc.mode == e.mode) return true;
   if (h->kc != nullptr) {  // encoding changed (precision pinned differently): rebuild
     free_knn_clusters(*h->kc);
     delete h->kc;
     h->kc = nullptr;
   }
+  {  // rows copy + operand + k-means scratch (labels, ids, d2, CUB temp): ~(4d + 2 Kp + 48) B per row
+    size_t free_b = 0, total_b = 0;
+    DK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double need = double(h->n_pad) * (4.0 * h->d + 2.0 * e.Kp + 64.0) * 1.1 + double(64 << 20);
+    if (double(free_b) < need) {
+      h->kc_failed = true;
+      return false;
+    }
+  }
   std::unique_ptr<KnnClusters> kc(new KnnClusters());
-  build_knn_clusters(h, knn_cluster_count(h), 3, *kc, s);
-  Encoding& se = kc->enc;
-  se.Kp = e.Kp;
-  se.d = e.d;
-  se.mu = e.mu;
-  DK_CUDA(cudaMalloc(&se.B, size_t(h->n_pad) * se.Kp * sizeof(__half)));
-  DK_CUDA(cudaMalloc(&se.xn, size_t(h->n_pad) * sizeof(float)));
-  DK_CUDA(cudaMalloc(&se.sx, 2 * sizeof(float)));
-  // same rows, same centring: the power-of-two scale (from the max |value|) equals the k-NN
-  // encoding's, so the encoded queries serve both operands
-  launch_encode_rows(kc->xs, h->n, h->n_pad, h->d, e.mode, e.mu, se.Kp, se.B, se.xn, se.sx,
-                     reinterpret_cast<uint32_t*>(se.sx + 1), s);
-  se.xn_max = e.xn_max;
-  se.eps_rel = e.eps_rel;
-  se.tmap = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN));
-  se.tmap_half = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN / 2));
-  se.mode = e.mode;
-  DK_CUDA(cudaStreamSynchronize(s));
+  try {
+    build_knn_clusters(h, knn_cluster_count(h), 3, *kc, s);
+    Encoding& se = kc->enc;
+    se.Kp = e.Kp;
+    se.d = e.d;
+    se.mu = e.mu;
+    DK_CUDA(cudaMalloc(&se.B, size_t(h->n_pad) * se.Kp * sizeof(__half)));
+    DK_CUDA(cudaMalloc(&se.xn, size_t(h->n_pad) * sizeof(float)));
+    DK_CUDA(cudaMalloc(&se.sx, 2 * sizeof(float)));
+    // same rows, same centring: the power-of-two scale (from the max |value|) equals the k-NN
+    // encoding's, so the encoded queries serve both operands
+    launch_encode_rows(kc->xs, h->n, h->n_pad, h->d, e.mode, e.mu, se.Kp, se.B, se.xn, se.sx,
+                       reinterpret_cast<uint32_t*>(se.sx + 1), s);
+    se.xn_max = e.xn_max;
+    se.eps_rel = e.eps_rel;
+    se.tmap = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN));
+    se.tmap_half = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN / 2));
+    se.mode = e.mode;
+    DK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&kc->stat_host), 4 * sizeof(int32_t), cudaHostAllocDefault));
+    DK_CUDA(cudaEventCreateWithFlags(&kc->stat_ev, cudaEventDisableTiming));
+    DK_CUDA(cudaStreamSynchronize(s));
+  } catch (const Error& err) {
+    free_knn_clusters(*kc);
+    cudaGetLastError();
+    if (err.code != DK_ENOMEM) throw;
+    h->kc_failed = true;  // out of memory: exact unpruned sweeps from now on
+    return false;
+  }
   h->kc = kc.release();
+  return true;
 }
 
-// k-NN for nq queries already on the device; idx/d2 outputs on the device.
+// Device workspace of one k-NN batch (knn_device / knn_ws_bytes share this layout).
+struct KnnLayout {
+  size_t flags, A, qn, scal, tmin, tau, cnt, cand, lists, ctr;
+  // pruned path
+  size_t dq, near, near_s, iota, qperm, sort_tmp, qp, tidx, td2, tlist, tcnt, bits, tcnt_t, tstart, ustart, blist,
+      ulist;
+  size_t sort_tmp_bytes = 0, ulist_ints = 0;
+  size_t end = 0;
+};
+
+KnnLayout knn_layout(const dk_dataset* h, const KnnPlan& kp, int32_t k, int32_t Kp, bool prune, size_t base) {
+  KnnLayout L{};
+  Plan pl;
+  pl.off = base;
+  const int32_t bpad = kp.batch;
+  L.flags = pl.add<uint32_t>(4);
+  L.A = pl.add<__half>(size_t(bpad) * Kp);
+  L.qn = pl.add<float>(bpad);
+  L.scal = pl.add<float>(4);
+  L.tmin = pl.add<float>(size_t(std::max(kp.nseg, 1)) * bpad);
+  L.tau = pl.add<float>(bpad);
+  L.cnt = pl.add<uint32_t>(bpad);
+  L.cand = pl.add<unsigned long long>(size_t(kp.cap) * bpad);
+  L.lists = pl.add<int32_t>(size_t(2) * bpad);
+  L.ctr = pl.add<int32_t>(16);  // [0] slow, [1] overflow, [4..6] unit plan (count, pairs, U)
+  if (prune) {
+    const int32_t ntiles = int32_t(h->n_pad / kBN), nqb = bpad / kBM, nwords = (ntiles + 31) / 32;
+    const int32_t Cn = knn_cluster_count(h);
+    L.dq = pl.add<double>(size_t(bpad) * Cn);
+    L.near = pl.add<int32_t>(bpad);
+    L.near_s = pl.add<int32_t>(bpad);
+    L.iota = pl.add<int32_t>(bpad);
+    L.qperm = pl.add<int32_t>(bpad);
+    L.sort_tmp_bytes = ball_sort_temp_bytes(bpad);
+    L.sort_tmp = pl.add<uint8_t>(L.sort_tmp_bytes);
+    L.qp = pl.add<double>(size_t(bpad) * h->d);
+    L.tidx = pl.add<int64_t>(size_t(bpad) * k);
+    L.td2 = pl.add<double>(size_t(bpad) * k);
+    L.tlist = pl.add<int32_t>(size_t(nqb) * ntiles);  // block-major lists, or the tile-major blist
+    L.tcnt = pl.add<int32_t>(nqb);
+    L.bits = pl.add<uint32_t>(size_t(nqb) * nwords);
+    L.tcnt_t = pl.add<int32_t>(ntiles);
+    L.tstart = pl.add<int32_t>(std::max(ntiles, nqb));
+    L.ustart = pl.add<int32_t>(std::max(ntiles, nqb));
+    L.blist = L.tlist;
+    // units: tile-major <= ntiles + pairs / 4, block-major <= nqb + pairs / 8
+    L.ulist_ints = size_t(3) * (size_t(std::max(ntiles, nqb)) + size_t(nqb) * ntiles / 4 + 1);
+    L.ulist = pl.add<int32_t>(L.ulist_ints);
+  }
+  L.end = pl.off;
+  return L;
+}
+
+// k-NN for nq queries already on the device; idx/d2 outputs on the device.  No host
+// synchronisation on the pruned or unpruned tile path (integer datasets wait once for the
+// query integrality check): work lists, unit plans and fallbacks live in device memory.
 void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t* idx_d, double* d2_d,
                 cudaStream_t s, size_t ws_off_base) {
   if (use_bigk(h, k, nq)) {  // exact fp64 distances + stable radix sort (bigk.cu)
@@ -347,79 +452,49 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     return;
   }
   const KnnPlan kp = plan_knn(h, k, nq);
-  Plan pl;
-  pl.off = ws_off_base;
-  const size_t o_flags = pl.add<uint32_t>(4);
-  const int mode = knn_mode(h, Qd, nq, at<uint32_t>(h->ws, o_flags), s);
+  const bool prunable = knn_prunable(h, kp);
+  const KnnLayout L0 = knn_layout(h, kp, k, int32_t(round_up(3 * int64_t(h->d), kBK)), prunable, ws_off_base);
+  if (L0.end > h->ws.cap) throw Error{DK_ECUDA, "internal: k-NN workspace under-reserved"};
+  const int mode = knn_mode(h, Qd, nq, at<uint32_t>(h->ws, L0.flags), s);
   const Encoding& e = ensure_encoding(h, mode, s);
+  bool prune = prunable && knn_prune_decide(h);
+  if (prune) prune = ensure_knn_clusters(h, e, s);
+  const KnnLayout L = knn_layout(h, kp, k, e.Kp, prunable, ws_off_base);
   const int32_t bpad = kp.batch;
-  const size_t o_A = pl.add<__half>(size_t(bpad) * e.Kp);
-  const size_t o_qn = pl.add<float>(bpad);
-  const size_t o_scal = pl.add<float>(4);
-  const size_t o_tmin = pl.add<float>(size_t(std::max(kp.nseg, 1)) * bpad);
-  const size_t o_tau = pl.add<float>(bpad);
-  const size_t o_cnt = pl.add<uint32_t>(bpad);
-  const size_t o_cand = pl.add<unsigned long long>(size_t(kp.cap) * bpad);
-  const size_t o_status = pl.add<int32_t>(bpad);
-  const size_t o_list = pl.add<int32_t>(bpad);
-  const size_t o_max = pl.add<uint32_t>(1);
-  const bool prune = knn_prune_enabled(h, kp);
   const int32_t ntiles = int32_t(h->n_pad / kBN);
-  const int32_t nqb_max = bpad / kBM;
-  const int32_t Cn = knn_cluster_count(h);
-  size_t o_dq = 0, o_near = 0, o_qperm = 0, o_qp = 0, o_tidx = 0, o_td2 = 0, o_tlist = 0, o_tcnt = 0, o_ul = 0;
-  if (prune) {
-    o_dq = pl.add<double>(size_t(bpad) * Cn);
-    o_near = pl.add<int32_t>(bpad);
-    o_qperm = pl.add<int32_t>(bpad);
-    o_qp = pl.add<double>(size_t(bpad) * h->d);
-    o_tidx = pl.add<int64_t>(size_t(bpad) * k);
-    o_td2 = pl.add<double>(size_t(bpad) * k);
-    o_tlist = pl.add<int32_t>(size_t(nqb_max) * ntiles);
-    o_tcnt = pl.add<int32_t>(nqb_max);
-    o_ul = pl.add<int32_t>(size_t(3) * nqb_max * (ntiles / 8 + 2));
-  }
-  if (pl.off > h->ws.cap) throw Error{DK_ECUDA, "internal: k-NN workspace under-reserved"};
-  if (prune) ensure_knn_clusters(h, e, s);
+  const bool tmajor = prune && tile_major_fits(e.Kp);
   const float inf = std::numeric_limits<float>::infinity();
+  int32_t* ctr = at<int32_t>(h->ws, L.ctr);
   for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
     const int64_t bn = std::min<int64_t>(bpad, nq - b0);
     const int32_t bn_pad = int32_t(query_pad(bn));
+    const int32_t nqb = bn_pad / kBM;
     const double* Qb = Qd + b0 * h->d;
     int64_t* idx_b = idx_d + b0 * k;
     double* d2_b = d2_d + b0 * k;
     int32_t* qperm = nullptr;
-    std::vector<int32_t> perm_h;
-    if (prune) {  // order the batch by nearest ball so each block of 128 queries is local
-      double* dq = at<double>(h->ws, o_dq);
-      int32_t* near = at<int32_t>(h->ws, o_near);
-      launch_query_cluster_dist(Qb, bn, h->d, h->kc->cent, h->kc->C, dq, near, s);
-      std::vector<int32_t> nh(static_cast<size_t>(bn));
-      DK_CUDA(cudaMemcpyAsync(nh.data(), near, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      DK_CUDA(cudaStreamSynchronize(s));
-      // stable counting sort by nearest ball (keys < C): O(bn + C) on the host
-      perm_h.resize(static_cast<size_t>(bn));
-      std::vector<int32_t> start(size_t(h->kc->C) + 1, 0);
-      for (int64_t i = 0; i < bn; ++i) ++start[size_t(nh[size_t(i)]) + 1];
-      for (int32_t c = 0; c < h->kc->C; ++c) start[size_t(c) + 1] += start[size_t(c)];
-      for (int64_t i = 0; i < bn; ++i) perm_h[size_t(start[size_t(nh[size_t(i)])]++)] = int32_t(i);
-      qperm = at<int32_t>(h->ws, o_qperm);
-      DK_CUDA(cudaMemcpyAsync(qperm, perm_h.data(), size_t(bn) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      double* Qp = at<double>(h->ws, o_qp);
+    DK_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), s));
+    if (prune) {  // order the batch by nearest ball (stable) so each block of 128 queries is local
+      int32_t* near = at<int32_t>(h->ws, L.near);
+      launch_query_cluster_dist(Qb, bn, h->d, h->kc->cent, h->kc->C, at<double>(h->ws, L.dq), near, s);
+      qperm = at<int32_t>(h->ws, L.qperm);
+      launch_sort_queries_by_ball(near, bn, h->kc->C, at<int32_t>(h->ws, L.near_s), at<int32_t>(h->ws, L.iota), qperm,
+                                  h->ws.base + L.sort_tmp, L.sort_tmp_bytes, s);
+      double* Qp = at<double>(h->ws, L.qp);
       launch_gather_rows_f64(Qb, qperm, bn, h->d, Qp, s);
       Qb = Qp;
-      idx_b = at<int64_t>(h->ws, o_tidx);
-      d2_b = at<double>(h->ws, o_td2);
+      idx_b = at<int64_t>(h->ws, L.tidx);
+      d2_b = at<double>(h->ws, L.td2);
     }
-    QueryOperand q = encode_queries(h, e, Qb, bn, bn_pad, at<__half>(h->ws, o_A), at<float>(h->ws, o_qn),
-                                    at<float>(h->ws, o_scal), s);
-    float* tau = at<float>(h->ws, o_tau);
-    uint32_t* cnt = at<uint32_t>(h->ws, o_cnt);
-    unsigned long long* cand = at<unsigned long long>(h->ws, o_cand);
+    QueryOperand q = encode_queries(h, e, Qb, bn, bn_pad, at<__half>(h->ws, L.A), at<float>(h->ws, L.qn),
+                                    at<float>(h->ws, L.scal), s);
+    float* tau = at<float>(h->ws, L.tau);
+    uint32_t* cnt = at<uint32_t>(h->ws, L.cnt);
+    unsigned long long* cand = at<unsigned long long>(h->ws, L.cand);
     if (kp.tau_inf) {
       launch_fill_float(tau, bn, inf, s);
     } else {
-      float* tmin = at<float>(h->ws, o_tmin);
+      float* tmin = at<float>(h->ws, L.tmin);
       launch_fill_float(tmin, int64_t(kp.nseg) * bn_pad, inf, s);
       SweepArgs a{};
       a.mode = MODE_TILEMIN;
@@ -435,36 +510,21 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     }
     launch_fill_float(tau + bn, bn_pad - bn, -inf, s);
     DK_CUDA(cudaMemsetAsync(cnt, 0, size_t(bn_pad) * sizeof(uint32_t), s));
-    std::vector<int32_t> ul;
-    int64_t active = 0;  // (block, tile) pairs the pruned FILTER sweeps
+    int32_t* uplan = ctr + 4;  // [0] units, [1] swept (block, tile) pairs, [2] U
     if (prune) {
-      const int32_t nqb = bn_pad / kBM;
-      int32_t* tlist = at<int32_t>(h->ws, o_tlist);
-      int32_t* tcnt = at<int32_t>(h->ws, o_tcnt);
-      launch_block_tile_lists(at<double>(h->ws, o_dq), h->kc->C, qperm, bn, nqb, tau, q.qn, e.xn_max, e.eps_rel,
-                              h->kc->rad, h->kc->tclo, h->kc->tchi, ntiles, tlist, tcnt, s);
-      std::vector<int32_t> tc(static_cast<size_t>(nqb));
-      DK_CUDA(cudaMemcpyAsync(tc.data(), tcnt, size_t(nqb) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      DK_CUDA(cudaStreamSynchronize(s));
-      for (int32_t v : tc) active += v;
-      // units of ~equal length so the 148 persistent CTAs finish together
-      const int64_t U = std::max<int64_t>(8, (active + 4 * h->num_sms - 1) / (4 * h->num_sms));
-      for (int32_t b = 0; b < nqb; ++b)
-        for (int64_t i = 0; i < tc[size_t(b)]; i += U) {
-          ul.push_back(b);
-          ul.push_back(int32_t(int64_t(b) * ntiles + i));
-          ul.push_back(int32_t(int64_t(b) * ntiles + std::min<int64_t>(tc[size_t(b)], i + U)));
-        }
-      if (ul.size() > size_t(3) * nqb_max * (ntiles / 8 + 2)) throw Error{DK_ECUDA, "internal: unit list overflow"};
-      if (!ul.empty())
-        DK_CUDA(cudaMemcpyAsync(at<int32_t>(h->ws, o_ul), ul.data(), ul.size() * sizeof(int32_t),
-                                cudaMemcpyHostToDevice, s));
-      // nearly every tile survives (unclustered data): stop paying for the ordering
-      if (active > int64_t(0.6 * double(nqb) * double(ntiles))) h->kc->useless = true;
-      if (h->knn_stats)
-        std::fprintf(stderr, "[dk] pruned k-NN: %lld of %lld (block, tile) pairs swept (%.1f%%), %d balls\n",
-                     (long long)active, (long long)nqb * ntiles, 100.0 * double(active) / (double(nqb) * ntiles),
-                     int(h->kc->C));
+      int32_t* tlist = at<int32_t>(h->ws, L.tlist);
+      int32_t* tcnt = at<int32_t>(h->ws, L.tcnt);
+      uint32_t* bits = at<uint32_t>(h->ws, L.bits);
+      launch_block_tile_lists(at<double>(h->ws, L.dq), h->kc->C, qperm, bn, nqb, tau, q.qn, e.xn_max, e.eps_rel,
+                              h->kc->rad, h->kc->tclo, h->kc->tchi, ntiles, tmajor ? nullptr : tlist, tcnt,
+                              tmajor ? bits : nullptr, s);
+      if (tmajor)
+        launch_tile_units(bits, nqb, ntiles, h->num_sms, at<int32_t>(h->ws, L.tcnt_t), at<int32_t>(h->ws, L.tstart),
+                          at<int32_t>(h->ws, L.ustart), uplan, at<int32_t>(h->ws, L.blist),
+                          at<int32_t>(h->ws, L.ulist), s);
+      else
+        launch_block_units(tcnt, nqb, ntiles, h->num_sms, at<int32_t>(h->ws, L.tstart), at<int32_t>(h->ws, L.ustart),
+                           uplan, at<int32_t>(h->ws, L.ulist), s);
     }
     {
       SweepArgs a{};
@@ -479,45 +539,53 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       a.cand = cand;
       a.cap = kp.cap;
       if (prune) {
-        a.ulist = at<int32_t>(h->ws, o_ul);
-        a.tlist = at<int32_t>(h->ws, o_tlist);
-        a.nunits_list = int32_t(ul.size() / 3);
+        a.ulist = at<int32_t>(h->ws, L.ulist);
+        a.tlist = tmajor ? nullptr : at<int32_t>(h->ws, L.tlist);
+        a.nunits_dev = uplan;
+        a.tmajor = tmajor ? 1 : 0;
+        a.blist = tmajor ? at<int32_t>(h->ws, L.blist) : nullptr;
       }
-      // work of the tiles actually swept (all of them unless pruned)
-      const double pairs = prune ? double(active) * kBM * kBN : double(bn) * double(h->n);
+      // work of the tiles actually swept (all of them unless pruned; the pruned count is read
+      // back below only when profiling)
+      const double pairs = double(bn) * double(h->n);
       ProfScope ps(h, s, 2.0 * double(h->d) * pairs, double(h->n_pad) * e.Kp * 2, 1);
       launch_sweep(a, h->num_sms, s);
     }
+    if (prune && (h->profiling == 1 || h->knn_stats)) {  // diagnostics only: wait for the plan
+      int32_t act = 0;
+      DK_CUDA(cudaMemcpyAsync(&act, uplan + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaStreamSynchronize(s));
+      if (h->profiling == 1) h->last_flops = 2.0 * double(h->d) * double(act) * kBM * kBN;
+      if (h->knn_stats)
+        std::fprintf(stderr, "[dk] pruned k-NN (%s): %d of %lld (block, tile) pairs swept (%.1f%%), %d balls\n",
+                     tmajor ? "tile-major" : "block-major", act, (long long)nqb * ntiles,
+                     100.0 * double(act) / (double(nqb) * ntiles), int(h->kc->C));
+    }
+    if (prune && b0 + bpad >= nq) {  // the swept fraction of the call's last batch, read next call
+      DK_CUDA(cudaMemcpyAsync(h->kc->stat_host, uplan + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaEventRecord(h->kc->stat_ev, s));
+      h->kc->stat_total = double(nqb) * double(ntiles);
+      h->kc->stat_pending = true;
+    }
+    int32_t* lists = at<int32_t>(h->ws, L.lists);
+    // pruned: candidates are positions in the cluster-sorted rows (read from there, reported as row ids)
+    launch_select(prune ? h->kc->xs : h->X, h->global_offset, h->d, Qb, bn, k, cand, cnt, kp.cap, q.qn, e.xn_max,
+                  e.eps_rel, idx_b, d2_b, lists, ctr, h->num_sms, s, prune ? h->kc->perm : nullptr);
+    launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, lists + bn, ctr + 1, k, idx_b, d2_b,
+                              h->num_sms, s);
     if (h->knn_stats) {
       std::vector<uint32_t> c(static_cast<size_t>(bn));
+      int32_t nf = 0;
       DK_CUDA(cudaMemcpyAsync(c.data(), cnt, size_t(bn) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaMemcpyAsync(&nf, ctr + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaStreamSynchronize(s));
       for (uint32_t v : c) {
         h->knn_cand_sum += v;
         h->knn_cand_max = std::max<int64_t>(h->knn_cand_max, v);
       }
       h->knn_queries += bn;
+      h->knn_fallbacks += nf;
     }
-    int32_t* status = at<int32_t>(h->ws, o_status);
-    const uint32_t cmax = max_count(cnt, bn, at<uint32_t>(h->ws, o_max), s);
-    // pruned: candidates are positions in the cluster-sorted rows (read from there, reported as row ids)
-    launch_select_rerank(prune ? h->kc->xs : h->X, h->global_offset, h->d, Qb, bn, k, cand, cnt, kp.cap, q.qn,
-                         e.xn_max, e.eps_rel, idx_b, d2_b, status, s, int32_t(std::min<uint32_t>(cmax, 1u << 30)),
-                         prune ? h->kc->perm : nullptr);
-    std::vector<int32_t> st(static_cast<size_t>(bn));
-    DK_CUDA(cudaMemcpyAsync(st.data(), status, size_t(bn) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    DK_CUDA(cudaStreamSynchronize(s));
-    std::vector<int32_t> fail;
-    for (int64_t i = 0; i < bn; ++i)
-      if (st[size_t(i)]) fail.push_back(int32_t(i));
-    if (!fail.empty()) {
-      int32_t* list = at<int32_t>(h->ws, o_list);
-      DK_CUDA(cudaMemcpyAsync(list, fail.data(), fail.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, list, int32_t(fail.size()), k, idx_b,
-                                d2_b, s);
-      DK_CUDA(cudaStreamSynchronize(s));
-    }
-    h->knn_fallbacks += int64_t(fail.size());
     if (prune) launch_scatter_knn(idx_b, d2_b, qperm, bn, k, idx_d + b0 * k, d2_d + b0 * k, s);
   }
 }
@@ -526,31 +594,7 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
   if (use_bigk(h, k, nq)) return bigk_temp_bytes(h->n) + 4096;
   const KnnPlan kp = plan_knn(h, k, nq);
   const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
-  Plan pl;
-  pl.add<uint32_t>(4);
-  pl.add<__half>(size_t(kp.batch) * Kp_max);
-  pl.add<float>(kp.batch);
-  pl.add<float>(4);
-  pl.add<float>(size_t(std::max(kp.nseg, 1)) * kp.batch);
-  pl.add<float>(kp.batch);
-  pl.add<uint32_t>(kp.batch);
-  pl.add<unsigned long long>(size_t(kp.cap) * kp.batch);
-  pl.add<int32_t>(kp.batch);
-  pl.add<int32_t>(kp.batch);
-  pl.add<uint32_t>(1);
-  if (knn_prune_enabled(h, kp)) {  // the pruned FILTER's buffers (knn_device)
-    const int32_t ntiles = int32_t(h->n_pad / kBN), nqb = kp.batch / kBM;
-    pl.add<double>(size_t(kp.batch) * knn_cluster_count(h));
-    pl.add<int32_t>(kp.batch);
-    pl.add<int32_t>(kp.batch);
-    pl.add<double>(size_t(kp.batch) * h->d);
-    pl.add<int64_t>(size_t(kp.batch) * k);
-    pl.add<double>(size_t(kp.batch) * k);
-    pl.add<int32_t>(size_t(nqb) * ntiles);
-    pl.add<int32_t>(nqb);
-    pl.add<int32_t>(size_t(3) * nqb * (ntiles / 8 + 2));
-  }
-  return pl.off + 4096;
+  return knn_layout(h, kp, k, Kp_max, knn_prunable(h, kp), 0).end + 4096;
 }
 
 
@@ -1176,21 +1220,40 @@ dk_status dk_kernel_values(int32_t family, double bandwidth, const double* dist,
     DK_REQUIRE(dist != nullptr && out != nullptr, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool din = is_device_ptr(dist), dout = is_device_ptr(out);
-    double *dd = nullptr, *od = nullptr;
-    uint32_t* bad = nullptr;
-    DK_CUDA(cudaMalloc(&bad, 2 * sizeof(uint32_t) + 2 * size_t(count) * sizeof(double)));
-    dd = reinterpret_cast<double*>(bad + 2);
-    od = dd + count;
+    // per-device scratch, grown on demand and reused (no allocation per call); the call
+    // synchronises its stream before returning, so holding the lock makes reuse safe
+    static std::mutex mu;
+    static std::map<int, std::pair<uint8_t*, size_t>> scratch;
+    std::lock_guard<std::mutex> lk(mu);
+    int dev = 0;
+    DK_CUDA(cudaGetDevice(&dev));
+    const size_t need = 256 + (din ? 0 : size_t(count)) * sizeof(double) + (dout ? 0 : size_t(count)) * sizeof(double);
+    auto& sc = scratch[dev];
+    if (sc.second < need) {
+      if (sc.first) {
+        DK_CUDA(cudaDeviceSynchronize());
+        DK_CUDA(cudaFree(sc.first));
+        sc = {nullptr, 0};
+      }
+      const size_t want = std::max(need + need / 4, size_t(1) << 20);
+      DK_CUDA(cudaMalloc(&sc.first, want));
+      sc.second = want;
+    }
+    uint32_t* bad = reinterpret_cast<uint32_t*>(sc.first);
+    double* cur = reinterpret_cast<double*>(sc.first + 256);
+    const double* dd = dist;
+    if (!din) {
+      DK_CUDA(cudaMemcpyAsync(cur, dist, size_t(count) * sizeof(double), cudaMemcpyHostToDevice, s));
+      dd = cur;
+      cur += count;
+    }
+    double* od = dout ? out : cur;
     DK_CUDA(cudaMemsetAsync(bad, 0, sizeof(uint32_t), s));
-    DK_CUDA(cudaMemcpyAsync(dd, dist, size_t(count) * sizeof(double), cudaMemcpyDefault, s));
     launch_kernel_values(family, bandwidth, dd, count, od, bad, s);
     uint32_t b = 0;
     DK_CUDA(cudaMemcpyAsync(&b, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    DK_CUDA(cudaMemcpyAsync(out, od, size_t(count) * sizeof(double), cudaMemcpyDefault, s));
+    if (!dout) DK_CUDA(cudaMemcpyAsync(out, od, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost, s));
     DK_CUDA(cudaStreamSynchronize(s));
-    cudaFree(bad);
-    (void)din;
-    (void)dout;
     DK_REQUIRE(!(b & 1u), "distance must be finite");
     DK_REQUIRE(!(b & 2u), "distance must be nonnegative");
   });

@@ -121,7 +121,15 @@ struct KnnClusters {
   int32_t* tclo = nullptr;   // [ntiles] first / last cluster of each 256-row tile of the sorted rows
   int32_t* tchi = nullptr;
   Encoding enc;              // sweep operand of xs (mode of the k-NN encoding)
-  bool useless = false;      // measured: pruning keeps most tiles -> not used
+  // pruning pays only when it skips tiles: the swept fraction of each call's last batch is
+  // copied back asynchronously (stat_host, stat_ev) and read at the next call; 3 calls in a
+  // row sweeping > 60% of the pairs turn pruning off, and every 32nd call re-tests it
+  bool useless = false;
+  int over = 0, off_calls = 0;
+  int32_t* stat_host = nullptr;  // pinned: [0] swept (block, tile) pairs of the last batch
+  double stat_total = 0;         // (block, tile) pairs of that batch
+  bool stat_pending = false;
+  cudaEvent_t stat_ev = nullptr;
 };
 
 // Growable device scratch, carved per call.
@@ -171,6 +179,7 @@ struct dk_dataset {
   int64_t launches = 0;
   // k-NN diagnostics (DK_KNN_STATS=1 in the environment): candidates per query, fallbacks
   dk::KnnClusters* kc = nullptr;  // pruned k-NN (built on the first large k-NN call)
+  bool kc_failed = false;          // the cluster build did not fit in device memory: unpruned sweeps
   bool knn_stats = false;
   int64_t knn_queries = 0, knn_cand_sum = 0, knn_cand_max = 0, knn_fallbacks = 0;
 };
@@ -225,7 +234,13 @@ struct SweepArgs {
   const int32_t* ulist;
   const int32_t* tlist;
   int32_t nunits_list;
+  const int32_t* nunits_dev;  // unit count in device memory (built on the device); overrides nunits_list
+  // tile-major FILTER: unit u = (dataset tile ulist[3u], query blocks blist[ulist[3u+1] .. ulist[3u+2]))
+  int32_t tmajor;
+  const int32_t* blist;
 };
+// tile-major FILTER fits when the resident dataset tile (kblocks x 32 KB) leaves a >= 3-stage ring
+bool tile_major_fits(int32_t Kp);
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms);  // doubles needed for KDE partials
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
 void set_pair_enabled(bool on);  // 2-CTA (cta_group::2) sweeps; off by default (DK_PAIR=1)
@@ -257,7 +272,18 @@ void launch_query_cluster_dist(const double* Q, int64_t nq, int32_t d, const dou
 void launch_block_tile_lists(const double* dq, int32_t C, const int32_t* qperm, int64_t bn, int32_t nqb,
                              const float* tau, const float* qn, float xn_max, float eps_rel, const double* rad,
                              const int32_t* tclo, const int32_t* tchi, int32_t ntiles, int32_t* tlist,
-                             int32_t* tcount, cudaStream_t s);
+                             int32_t* tcount, uint32_t* bits, cudaStream_t s);
+// stable sort of the batch by nearest ball (CUB radix sort): qperm[i] = batch position of the
+// i-th query in ball order
+size_t ball_sort_temp_bytes(int64_t nq);
+void launch_sort_queries_by_ball(const int32_t* nearest, int64_t nq, int32_t C, int32_t* nearest_sorted,
+                                 int32_t* iota, int32_t* qperm, void* temp, size_t temp_bytes, cudaStream_t s);
+// FILTER work units built on the device (scal[0] = unit count, [1] = swept (block, tile) pairs)
+void launch_tile_units(const uint32_t* bits, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* tcnt,
+                       int32_t* tstart, int32_t* ustart, int32_t* scal, int32_t* blist, int32_t* ulist,
+                       cudaStream_t s);
+void launch_block_units(const int32_t* tcount, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* bstart,
+                        int32_t* ustart, int32_t* scal, int32_t* ulist, cudaStream_t s);
 void launch_gather_rows_f64(const double* Q, const int32_t* perm, int64_t nq, int32_t d, double* out, cudaStream_t s);
 void launch_scatter_knn(const int64_t* idx_p, const double* d2_p, const int32_t* perm, int64_t nq, int32_t k,
                         int64_t* idx_out, double* d2_out, cudaStream_t s);
@@ -266,14 +292,16 @@ void launch_scatter_knn(const int64_t* idx_p, const double* d2_p, const int32_t*
 void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
                           float xn_max, float eps_rel, float* tau, cudaStream_t s);
 void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s);
-void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
-                          const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
-                          float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* status,
-                          cudaStream_t s, int32_t max_cnt = 0, const int64_t* perm = nullptr);
-uint32_t max_count(const uint32_t* v, int64_t n, uint32_t* scratch, cudaStream_t s);  // synchronises
+// selection: fast path for every query, sorted-rounds kernel over the device list of queries
+// the fast path could not finish; queries with overflowing or too-short candidate lists are
+// appended to the overflow list (lists + nq, counts[1]) for launch_exact_knn_fallback
+void launch_select(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
+                   const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
+                   float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* lists, int32_t* counts,
+                   int num_sms, cudaStream_t s, const int64_t* perm = nullptr);
 void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
-                               const int32_t* qlist, int32_t nlist, int32_t k, int64_t* idx_out, double* d2_out,
-                               cudaStream_t s);
+                               const int32_t* qlist, const int32_t* qcount, int32_t k, int64_t* idx_out,
+                               double* d2_out, int num_sms, cudaStream_t s);
 void launch_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_in, const double* d2_in,
                        int64_t* idx_out, double* d2_out, cudaStream_t s);
 void launch_kernel_values(int32_t family, double h, const double* dist, int64_t count, double* out, uint32_t* bad,

@@ -1407,6 +1407,8 @@ void free_knn_clusters(KnnClusters& kc) {
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(kc.enc.B), static_cast<void*>(kc.enc.xn), static_cast<void*>(kc.enc.sx)})
     if (p) cudaFree(p);
+  if (kc.stat_host) cudaFreeHost(kc.stat_host);
+  if (kc.stat_ev) cudaEventDestroy(kc.stat_ev);
   kc = KnnClusters{};
 }
 

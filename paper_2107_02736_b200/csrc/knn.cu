@@ -15,12 +15,18 @@
 //   2. FILTER sweep: keep every (approx d2, col) with approx d2 <= tau_q.  The
 //      candidate set provably contains all points at or inside the exact k-th
 //      distance, including every tie there.
-//   3. select_rerank: candidates sorted by approx d2, re-ranked exactly (fp64
-//      direct difference) in that order until the next approx d2 - eps_q
-//      exceeds the current exact k-th distance; output sorted by (d2, idx).
-//   4. queries whose candidate list overflowed take an exact fp64 full scan.
+//   3. select_fast: a histogram of the approx keys locates the k-th; the few
+//      candidates within 2 eps_q of it are re-ranked exactly (fp64 direct
+//      difference) and sorted by (d2, idx).  Queries with too many near-ties
+//      go to select_slow (sorted rounds with early termination) through a
+//      device-side list.
+//   4. queries whose candidate list overflowed take an exact fp64 full scan
+//      (device-side list again: the host never waits on the selection).
 #include <cfloat>
+#include <climits>
 #include <cstdlib>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "internal.h"
 
@@ -205,245 +211,297 @@ __device__ __forceinline__ double exact_d2_group(const float* __restrict__ x, co
   return s;
 }
 
-// exact re-rank of the candidates in increasing approx order with early termination
-__global__ void select_rerank_kernel(const float* __restrict__ X, int64_t global_offset, int32_t d,
-                                     const double* __restrict__ Q, int64_t nq, int32_t k,
-                                     const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt,
-                                     int32_t cap, const float* __restrict__ qn, float xn_max, float eps_rel,
-                                     int32_t B, int64_t* __restrict__ idx_out, double* __restrict__ d2_out,
-                                     int32_t* __restrict__ status, const int64_t* __restrict__ perm) {
+// Selection, fast path (one CTA per query, small shared memory): no sort of the whole
+// candidate list.  T' = the largest approx key in the histogram bins up to the one holding
+// the k-th smallest approx key (T' >= that key).  The k candidates with approx d2 <= T' have
+// exact d2 <= T' + eps, so every member of the exact top k (ties included) has approx
+// d2 <= T' + 2 eps: exactly those are evaluated (fp64 direct difference) and sorted by
+// (d2, id).  The candidate keys stay in global memory (L2) and are read in four passes.
+// Queries this path cannot finish are appended to device lists, so the host never waits:
+//   slow list: more than 2 pow2(k) keys within 2 eps of T' -> select_slow_kernel;
+//   ovf list : candidate list overflowed (> cap) or shorter than k -> exact fp64 scan.
+__global__ void __launch_bounds__(256) select_fast_kernel(
+    const float* __restrict__ X, int64_t global_offset, int32_t d, const double* __restrict__ Q, int64_t nq,
+    int32_t k, const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt, int32_t cap,
+    const float* __restrict__ qn, float xn_max, float eps_rel, int64_t* __restrict__ idx_out,
+    double* __restrict__ d2_out, int32_t* __restrict__ slow_list, int32_t* __restrict__ slow_cnt,
+    int32_t* __restrict__ ovf_list, int32_t* __restrict__ ovf_cnt, const int64_t* __restrict__ perm) {
   // candidates are row positions of X; perm (optional) maps a position to the reported row id,
   // which is also the tie-break key (pruned k-NN: X holds the cluster-sorted rows)
-  extern __shared__ unsigned long long sbuf[];
+  extern __shared__ unsigned long long sraw[];
   const int64_t q = blockIdx.x;
   if (q >= nq) return;
   const uint32_t craw = cnt[q];
-  if (craw > uint32_t(cap)) {  // overflow -> exact scan on the host's request
-    if (threadIdx.x == 0) status[q] = 1;
+  if (craw > uint32_t(cap) || craw < uint32_t(k)) {
+    if (threadIdx.x == 0) ovf_list[atomicAdd(ovf_cnt, 1)] = int32_t(q);
     return;
   }
   const int c = int(craw);
   const int Kp = max(32, pow2_ceil(k));
-  const int W = Kp;  // candidates re-ranked per round; Kp + W is a power of two for the bitonic merge
+  const int W = Kp;
   const unsigned long long* keys = cand + size_t(q) * cap;
-  Key128* top = reinterpret_cast<Key128*>(sbuf + B);  // [Kp + W]
+  Key128* top = reinterpret_cast<Key128*>(sraw);         // [Kp + W]
   double* qv = reinterpret_cast<double*>(top + Kp + W);  // the query in shared memory
-  uint32_t* hist = reinterpret_cast<uint32_t*>(qv + d);   // [kSelHist]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(qv + d);  // [kSelHist]
   for (int j = threadIdx.x; j < d; j += blockDim.x) qv[j] = Q[size_t(q) * d + j];
   const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   constexpr int G = 8;  // lanes per candidate: 4 candidates per warp step
   const int grp = lane / G, gl = lane % G;
-
-  // ---- fast path: no sort of the whole candidate list.  T' = the largest approx key in the
-  // histogram bins up to the one holding the k-th smallest approx key (T' >= that key).  The
-  // k candidates with approx d2 <= T' have exact d2 <= T' + eps, so every member of the exact
-  // top k (ties included) has approx d2 <= T' + 2 eps: exactly those are evaluated and sorted.
-  if (c >= k) {
-    __shared__ uint32_t s_lo, s_hi, s_bstar, s_tmax, s_ns;
-    __shared__ uint32_t s_wsum[32];
-    if (threadIdx.x == 0) { s_lo = 0xffffffffu; s_hi = 0u; s_bstar = kSelHist - 1; s_tmax = 0u; s_ns = 0u; }
-    for (int i = threadIdx.x; i < kSelHist; i += blockDim.x) hist[i] = 0u;
-    __syncthreads();
-    uint32_t lo = 0xffffffffu, hi = 0u;
-    for (int i = threadIdx.x; i < c; i += blockDim.x) {
-      const unsigned long long v = keys[i];
-      sbuf[i] = v;
-      const uint32_t b = uint32_t(v >> 32);  // bits of an approx d2 >= 0: uint order == float order
-      lo = min(lo, b);
-      hi = max(hi, b);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (lane == 0) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
-    __syncthreads();
-    const float flo = __uint_as_float(s_lo), fhi = __uint_as_float(s_hi);
-    const float scale = fhi > flo ? float(kSelHist) / (fhi - flo) : 0.f;
-    // monotone bin of a key (NaN from 0 * inf lands in bin 0, i.e. still monotone)
-    auto bin_of = [&](uint32_t b) {
-      return min(max(__float2int_rz((__uint_as_float(b) - flo) * scale), 0), kSelHist - 1);
-    };
-    for (int i = threadIdx.x; i < c; i += blockDim.x) atomicAdd(&hist[bin_of(uint32_t(sbuf[i] >> 32))], 1u);
-    __syncthreads();
-    {  // block scan: thread t owns bins [4t, 4t + 4) (kSelHist = 4 * blockDim)
-      const int t = threadIdx.x;
-      const uint32_t h0 = hist[4 * t], h1 = hist[4 * t + 1], h2 = hist[4 * t + 2], h3 = hist[4 * t + 3];
-      const uint32_t own = h0 + h1 + h2 + h3;
-      uint32_t incl = own;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      if (lane == 31) s_wsum[warp] = incl;
-      __syncthreads();
-      uint32_t cum = incl - own;
-      for (int w = 0; w < warp; ++w) cum += s_wsum[w];
-      const uint32_t hh[4] = {h0, h1, h2, h3};
-      const uint32_t kk = uint32_t(k);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (cum < kk && cum + hh[j] >= kk) s_bstar = uint32_t(4 * t + j);
-        cum += hh[j];
-      }
-    }
-    __syncthreads();
-    const int bstar = int(s_bstar);
-    uint32_t tm = 0u;
-    for (int i = threadIdx.x; i < c; i += blockDim.x) {
-      const uint32_t b = uint32_t(sbuf[i] >> 32);
-      if (bin_of(b) <= bstar) tm = max(tm, b);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tm = max(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-    if (lane == 0) atomicMax(&s_tmax, tm);
-    __syncthreads();
-    const double thr = double(__uint_as_float(s_tmax)) + 2.0 * eps;
-    const int scap = Kp + W;
-    for (int i = threadIdx.x; i < c; i += blockDim.x) {
-      const unsigned long long v = sbuf[i];
-      if (double(__uint_as_float(uint32_t(v >> 32))) <= thr) {
-        const uint32_t pos = atomicAdd(&s_ns, 1u);
-        if (pos < uint32_t(scap)) top[pos].lo = v & 0xffffffffull;
-      }
-    }
-    __syncthreads();
-    const int ns = int(s_ns);
-    if (ns <= scap) {
-      int P = 2;
-      while (P < ns) P <<= 1;
-      for (int i0 = warp * (32 / G); i0 < ns; i0 += nwarps * (32 / G)) {
-        const int i = i0 + grp;
-        const bool ok = i < ns;
-        const unsigned long long col = ok ? top[i].lo : 0ull;
-        const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
-        if (gl == 0 && ok) {
-          top[i].hi = static_cast<unsigned long long>(__double_as_longlong(dd));
-          if (perm != nullptr) top[i].lo = static_cast<unsigned long long>(perm[col]);
-        }
-      }
-      for (int i = ns + threadIdx.x; i < P; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
-      bitonic_k128(top, P);
-      if (threadIdx.x == 0) status[q] = 0;
-      for (int i = threadIdx.x; i < k; i += blockDim.x) {
-        const Key128 key = top[i];
-        idx_out[size_t(q) * k + i] = int64_t(key.lo) + global_offset;
-        d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(key.hi));
-      }
-      return;
-    }
-    __syncthreads();  // too many keys within 2 eps of the k-th: the sorted-rounds path below
-  }
-
-  int Bc = 1;
-  while (Bc < c) Bc <<= 1;
-  Bc = max(Bc, 2);
-  for (int i = threadIdx.x; i < Bc; i += blockDim.x) sbuf[i] = i < c ? keys[i] : ~0ull;
-  bitonic_u64(sbuf, Bc);
-  for (int i = threadIdx.x; i < Kp + W; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
+  __shared__ uint32_t s_lo, s_hi, s_bstar, s_tmax, s_ns;
+  __shared__ uint32_t s_wsum[32];
+  if (threadIdx.x == 0) { s_lo = 0xffffffffu; s_hi = 0u; s_bstar = kSelHist - 1; s_tmax = 0u; s_ns = 0u; }
+  for (int i = threadIdx.x; i < kSelHist; i += blockDim.x) hist[i] = 0u;
   __syncthreads();
-  __shared__ int s_stop;
-  for (int pos = 0; pos < c; pos += W) {
-    for (int i0 = warp * (32 / G); i0 < W; i0 += nwarps * (32 / G)) {
-      const int i = i0 + grp;
-      const bool ok = i < W && pos + i < c;
-      const unsigned long long col = ok ? (sbuf[pos + i] & 0xffffffffull) : 0ull;
-      const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
-      if (gl == 0 && i < W)
-        top[Kp + i] = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)),
-                                  perm != nullptr ? static_cast<unsigned long long>(perm[col]) : col}
-                         : Key128{~0ull, ~0ull};
-    }
-    bitonic_k128(top, Kp + W);
-    if (threadIdx.x == 0) {
-      int stop = 0;
-      if (pos + W < c && top[k - 1].hi != ~0ull) {
-        const double Dk = __longlong_as_double(static_cast<long long>(top[k - 1].hi));
-        const double next = double(__uint_as_float(uint32_t(sbuf[pos + W] >> 32)));
-        stop = (next - eps > Dk) ? 1 : 0;
-      }
-      s_stop = stop;
-    }
-    __syncthreads();
-    if (s_stop) break;
-    __syncthreads();
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    const uint32_t b = uint32_t(__ldg(keys + i) >> 32);  // bits of an approx d2 >= 0: uint order == float order
+    lo = min(lo, b);
+    hi = max(hi, b);
   }
-  if (threadIdx.x == 0) status[q] = (c < k) ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
+  __syncthreads();
+  const float flo = __uint_as_float(s_lo), fhi = __uint_as_float(s_hi);
+  const float scale = fhi > flo ? float(kSelHist) / (fhi - flo) : 0.f;
+  // monotone bin of a key (NaN from 0 * inf lands in bin 0, i.e. still monotone)
+  auto bin_of = [&](uint32_t b) {
+    return min(max(__float2int_rz((__uint_as_float(b) - flo) * scale), 0), kSelHist - 1);
+  };
+  for (int i = threadIdx.x; i < c; i += blockDim.x) atomicAdd(&hist[bin_of(uint32_t(__ldg(keys + i) >> 32))], 1u);
+  __syncthreads();
+  {  // block scan: thread t owns bins [4t, 4t + 4) (kSelHist = 4 * blockDim)
+    const int t = threadIdx.x;
+    const uint32_t h0 = hist[4 * t], h1 = hist[4 * t + 1], h2 = hist[4 * t + 2], h3 = hist[4 * t + 3];
+    const uint32_t own = h0 + h1 + h2 + h3;
+    uint32_t incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t cum = incl - own;
+    for (int w = 0; w < warp; ++w) cum += s_wsum[w];
+    const uint32_t hh[4] = {h0, h1, h2, h3};
+    const uint32_t kk = uint32_t(k);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (cum < kk && cum + hh[j] >= kk) s_bstar = uint32_t(4 * t + j);
+      cum += hh[j];
+    }
+  }
+  __syncthreads();
+  const int bstar = int(s_bstar);
+  uint32_t tm = 0u;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    const uint32_t b = uint32_t(__ldg(keys + i) >> 32);
+    if (bin_of(b) <= bstar) tm = max(tm, b);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tm = max(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+  if (lane == 0) atomicMax(&s_tmax, tm);
+  __syncthreads();
+  const double thr = double(__uint_as_float(s_tmax)) + 2.0 * eps;
+  const int scap = Kp + W;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    const unsigned long long v = __ldg(keys + i);
+    if (double(__uint_as_float(uint32_t(v >> 32))) <= thr) {
+      const uint32_t pos = atomicAdd(&s_ns, 1u);
+      if (pos < uint32_t(scap)) top[pos].lo = v & 0xffffffffull;
+    }
+  }
+  __syncthreads();
+  const int ns = int(s_ns);
+  if (ns > scap) {  // too many keys within 2 eps of the k-th: the sorted-rounds kernel
+    if (threadIdx.x == 0) slow_list[atomicAdd(slow_cnt, 1)] = int32_t(q);
+    return;
+  }
+  int P = 2;
+  while (P < ns) P <<= 1;
+  for (int i0 = warp * (32 / G); i0 < ns; i0 += nwarps * (32 / G)) {
+    const int i = i0 + grp;
+    const bool ok = i < ns;
+    const unsigned long long col = ok ? top[i].lo : 0ull;
+    const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
+    if (gl == 0 && ok) {
+      top[i].hi = static_cast<unsigned long long>(__double_as_longlong(dd));
+      if (perm != nullptr) top[i].lo = static_cast<unsigned long long>(perm[col]);
+    }
+  }
+  for (int i = ns + threadIdx.x; i < P; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
+  bitonic_k128(top, P);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     const Key128 key = top[i];
-    idx_out[size_t(q) * k + i] = key.lo == ~0ull ? -1 : int64_t(key.lo) + global_offset;
+    idx_out[size_t(q) * k + i] = int64_t(key.lo) + global_offset;
     d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(key.hi));
   }
 }
 
-// exact fp64 full scan for queries whose certificate failed (rare / degenerate inputs)
+// Selection, sorted-rounds path for the queries select_fast_kernel listed (persistent grid
+// over the device list): all candidates bitonic-sorted by approx key in shared memory, then
+// re-ranked exactly W at a time in that order until the next approx key - eps exceeds the
+// current exact k-th distance.
+__global__ void __launch_bounds__(256) select_slow_kernel(
+    const float* __restrict__ X, int64_t global_offset, int32_t d, const double* __restrict__ Q, int32_t k,
+    const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt, int32_t cap,
+    const float* __restrict__ qn, float xn_max, float eps_rel, int32_t B, int64_t* __restrict__ idx_out,
+    double* __restrict__ d2_out, const int32_t* __restrict__ slow_list, const int32_t* __restrict__ slow_cnt,
+    const int64_t* __restrict__ perm) {
+  extern __shared__ unsigned long long sbuf[];
+  const int nlist = *slow_cnt;
+  const int Kp = max(32, pow2_ceil(k));
+  const int W = Kp;
+  Key128* top = reinterpret_cast<Key128*>(sbuf + B);
+  double* qv = reinterpret_cast<double*>(top + Kp + W);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  constexpr int G = 8;
+  const int grp = lane / G, gl = lane % G;
+  __shared__ int s_stop;
+  for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
+    const int64_t q = slow_list[li];
+    const int c = int(cnt[q]);
+    const unsigned long long* keys = cand + size_t(q) * cap;
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x) qv[j] = Q[size_t(q) * d + j];
+    const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
+    int Bc = 2;
+    while (Bc < c) Bc <<= 1;
+    for (int i = threadIdx.x; i < Bc; i += blockDim.x) sbuf[i] = i < c ? keys[i] : ~0ull;
+    bitonic_u64(sbuf, Bc);
+    for (int i = threadIdx.x; i < Kp + W; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
+    __syncthreads();
+    for (int pos = 0; pos < c; pos += W) {
+      for (int i0 = warp * (32 / G); i0 < W; i0 += nwarps * (32 / G)) {
+        const int i = i0 + grp;
+        const bool ok = i < W && pos + i < c;
+        const unsigned long long col = ok ? (sbuf[pos + i] & 0xffffffffull) : 0ull;
+        const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
+        if (gl == 0 && i < W)
+          top[Kp + i] = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)),
+                                    perm != nullptr ? static_cast<unsigned long long>(perm[col]) : col}
+                           : Key128{~0ull, ~0ull};
+      }
+      bitonic_k128(top, Kp + W);
+      if (threadIdx.x == 0) {
+        int stop = 0;
+        if (pos + W < c && top[k - 1].hi != ~0ull) {
+          const double Dk = __longlong_as_double(static_cast<long long>(top[k - 1].hi));
+          const double next = double(__uint_as_float(uint32_t(sbuf[pos + W] >> 32)));
+          stop = (next - eps > Dk) ? 1 : 0;
+        }
+        s_stop = stop;
+      }
+      __syncthreads();
+      if (s_stop) break;
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      const Key128 key = top[i];
+      idx_out[size_t(q) * k + i] = int64_t(key.lo) + global_offset;
+      d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(key.hi));
+    }
+  }
+}
+
+// exact fp64 full scan for the queries on the overflow list (rare / degenerate inputs);
+// persistent grid over the device list
 __global__ void exact_knn_kernel(const float* __restrict__ X, int64_t n, int64_t global_offset, int32_t d,
-                                 const double* __restrict__ Q, const int32_t* __restrict__ qlist, int32_t k,
-                                 int32_t B, int64_t* __restrict__ idx_out, double* __restrict__ d2_out) {
+                                 const double* __restrict__ Q, const int32_t* __restrict__ qlist,
+                                 const int32_t* __restrict__ qcount, int32_t k, int32_t B,
+                                 int64_t* __restrict__ idx_out, double* __restrict__ d2_out) {
   extern __shared__ unsigned long long sbuf[];
   Key128* buf = reinterpret_cast<Key128*>(sbuf);
-  const int q = qlist[blockIdx.x];
+  const int nlist = *qcount;
   const int Kp = pow2_ceil(k);
-  const double* qv = Q + size_t(q) * d;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < Kp; i += blockDim.x) buf[i] = Key128{~0ull, ~0ull};
   const int chunk = B - Kp;
-  for (int64_t pos = 0; pos < n; pos += chunk) {
-    for (int i = warp; i < chunk; i += nwarps) {
-      Key128 key{~0ull, ~0ull};
-      const int64_t col = pos + i;
-      if (col < n) {
-        const double dd = exact_d2_warp(X + size_t(col) * d, qv, d, lane);
-        key.hi = static_cast<unsigned long long>(__double_as_longlong(dd));
-        key.lo = static_cast<unsigned long long>(col);
+  for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
+    const int q = qlist[li];
+    const double* qv = Q + size_t(q) * d;
+    __syncthreads();
+    for (int i = threadIdx.x; i < Kp; i += blockDim.x) buf[i] = Key128{~0ull, ~0ull};
+    for (int64_t pos = 0; pos < n; pos += chunk) {
+      for (int i = warp; i < chunk; i += nwarps) {
+        Key128 key{~0ull, ~0ull};
+        const int64_t col = pos + i;
+        if (col < n) {
+          const double dd = exact_d2_warp(X + size_t(col) * d, qv, d, lane);
+          key.hi = static_cast<unsigned long long>(__double_as_longlong(dd));
+          key.lo = static_cast<unsigned long long>(col);
+        }
+        if (lane == 0) buf[Kp + i] = key;
       }
-      if (lane == 0) buf[Kp + i] = key;
+      bitonic_k128(buf, B);
     }
-    bitonic_k128(buf, B);
-  }
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    idx_out[size_t(q) * k + i] = int64_t(buf[i].lo) + global_offset;
-    d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(buf[i].hi));
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      idx_out[size_t(q) * k + i] = int64_t(buf[i].lo) + global_offset;
+      d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(buf[i].hi));
+    }
   }
 }
 
-// merge `parts` sorted (d2, idx) lists per query -> global top k (dataset-sharded mode)
-__global__ void merge_topk_kernel(int32_t parts, int64_t nq, int32_t k, const int64_t* __restrict__ idx_in,
-                                  const double* __restrict__ d2_in, int64_t* __restrict__ idx_out,
-                                  double* __restrict__ d2_out) {
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// merge `parts` sorted (d2, idx) lists per query -> global top k (dataset-sharded mode).
+// One warp per query: lane p holds the head of part p (and p + 32), the warp picks the
+// smallest (d2, idx) head by shuffles, its owner advances; no per-thread arrays.
+__global__ void __launch_bounds__(256) merge_topk_kernel(int32_t parts, int64_t nq, int32_t k,
+                                                         const int64_t* __restrict__ idx_in,
+                                                         const double* __restrict__ d2_in,
+                                                         int64_t* __restrict__ idx_out, double* __restrict__ d2_out) {
+  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (q >= nq) return;
-  int head[64];
-  for (int p = 0; p < parts; ++p) head[p] = 0;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  // two heads per lane (parts lane and lane + 32) in scalar registers
+  int h0 = 0, h1 = 0;
+  double d0 = kInf, d1 = kInf;
+  long long i0 = LLONG_MAX, i1 = LLONG_MAX;
+  auto load_i = [&](int p, int head) -> long long {
+    if (p >= parts || head >= k) return LLONG_MAX;
+    const long long v = idx_in[(size_t(p) * nq + q) * k + head];
+    return v >= 0 ? v : LLONG_MAX;
+  };
+  auto load_d = [&](int p, int head, long long ii) -> double {
+    return ii == LLONG_MAX ? kInf : d2_in[(size_t(p) * nq + q) * k + head];
+  };
+  i0 = load_i(lane, h0);
+  d0 = load_d(lane, h0, i0);
+  i1 = load_i(lane + 32, h1);
+  d1 = load_d(lane + 32, h1, i1);
   for (int i = 0; i < k; ++i) {
-    int best = -1;
-    double bd = 0;
-    int64_t bi = 0;
-    for (int p = 0; p < parts; ++p) {
-      if (head[p] >= k) continue;
-      const size_t off = (size_t(p) * nq + q) * k + head[p];
-      const double dd = d2_in[off];
-      const int64_t ii = idx_in[off];
-      if (ii < 0) continue;
-      if (best < 0 || dd < bd || (dd == bd && ii < bi)) { best = p; bd = dd; bi = ii; }
-    }
-    if (best < 0) { idx_out[q * k + i] = -1; d2_out[q * k + i] = __longlong_as_double(0x7ff0000000000000ll); continue; }
-    ++head[best];
-    idx_out[q * k + i] = bi;
-    d2_out[q * k + i] = bd;
-  }
-}
-
-__global__ void max_u32_kernel(const uint32_t* __restrict__ v, int64_t n, uint32_t* __restrict__ out) {
-  uint32_t m = 0;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    m = max(m, v[i]);
+    // this lane's best of its two heads, then the warp minimum of (d2, idx)
+    const bool second = d1 < d0 || (d1 == d0 && i1 < i0);
+    double bd = second ? d1 : d0;
+    long long bi = second ? i1 : i0;
+    int bl = lane;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (od < bd || (od == bd && (oi < bi || (oi == bi && ol < bl)))) { bd = od; bi = oi; bl = ol; }
+    }
+    if (lane == 0) {
+      idx_out[q * k + i] = bi == LLONG_MAX ? -1 : bi;
+      d2_out[q * k + i] = bi == LLONG_MAX ? kInf : bd;
+    }
+    if (lane == bl && bi != LLONG_MAX) {
+      if (second) {
+        ++h1;
+        i1 = load_i(lane + 32, h1);
+        d1 = load_d(lane + 32, h1, i1);
+      } else {
+        ++h0;
+        i0 = load_i(lane, h0);
+        d0 = load_d(lane, h0, i0);
+      }
+    }
+  }
 }
 
 __global__ void fill_float_kernel(float* p, int64_t count, float v) {
@@ -528,7 +586,7 @@ __global__ void __launch_bounds__(256) block_tile_lists_kernel(
     const double* __restrict__ dq, int32_t C, const int32_t* __restrict__ qperm, int64_t bn,
     const float* __restrict__ tau, const float* __restrict__ qn, float xn_max, float eps_rel,
     const double* __restrict__ rad, const int32_t* __restrict__ tclo, const int32_t* __restrict__ tchi,
-    int32_t ntiles, int32_t* __restrict__ tlist, int32_t* __restrict__ tcount) {
+    int32_t ntiles, int32_t* __restrict__ tlist, int32_t* __restrict__ tcount, uint32_t* __restrict__ bits) {
   extern __shared__ uint8_t need[];
   __shared__ int s_wcnt[8];
   __shared__ int s_base;
@@ -556,10 +614,13 @@ __global__ void __launch_bounds__(256) block_tile_lists_kernel(
       for (int c = tclo[t]; c <= tchi[t] && !on; ++c) on = need[c] != 0;
     const uint32_t b = __ballot_sync(0xffffffffu, on);
     if (lane == 0) s_wcnt[warp] = __popc(b);
+    // tile-major schedule: bit t of row qb (32 tiles per word)
+    const int nwords = (ntiles + 31) >> 5;
+    if (bits != nullptr && lane == 0 && (t0 >> 5) + warp < nwords) bits[int64_t(qb) * nwords + (t0 >> 5) + warp] = b;
     __syncthreads();
     int off = s_base;
     for (int w = 0; w < warp; ++w) off += s_wcnt[w];
-    if (on) tlist[int64_t(qb) * ntiles + off + __popc(b & ((1u << lane) - 1u))] = t;
+    if (on && tlist != nullptr) tlist[int64_t(qb) * ntiles + off + __popc(b & ((1u << lane) - 1u))] = t;
     __syncthreads();
     if (threadIdx.x == 0) {
       int tot = 0;
@@ -569,6 +630,122 @@ __global__ void __launch_bounds__(256) block_tile_lists_kernel(
     __syncthreads();
   }
   if (threadIdx.x == 0) tcount[qb] = s_base;
+}
+
+// number of query blocks that sweep each tile (tile-major schedule)
+__global__ void tile_count_kernel(const uint32_t* __restrict__ bits, int32_t nqb, int32_t ntiles,
+                                  int32_t* __restrict__ cnt) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int nwords = (ntiles + 31) >> 5;
+  int c = 0;
+  for (int b = 0; b < nqb; ++b) c += (bits[int64_t(b) * nwords + (t >> 5)] >> (t & 31)) & 1u;
+  cnt[t] = c;
+}
+
+// Work-unit plan over m groups holding cnt[g] list entries (one CTA, 1024 threads):
+// total = sum cnt, U = max(umin, ceil(total / (per_slot * slots))) entries per unit,
+// start[g] = exclusive scan of cnt, ustart[g] = exclusive scan of ceil(cnt / U).
+// scal[0] = number of units, scal[1] = total, scal[2] = U.
+__global__ void __launch_bounds__(1024) unit_plan_kernel(const int32_t* __restrict__ cnt, int32_t m, int32_t slots,
+                                                         int32_t per_slot, int32_t umin,
+                                                         int32_t* __restrict__ start, int32_t* __restrict__ ustart,
+                                                         int32_t* __restrict__ scal) {
+  __shared__ long long s_w[32];
+  __shared__ int s_u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (m + 1023) / 1024;
+  const int g0 = min(m, tid * per), g1 = min(m, g0 + per);
+  auto block_excl_scan = [&](long long own) -> long long {  // exclusive prefix over threads, s_w[31] = total
+    long long incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    __syncthreads();
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      long long v = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      s_w[lane] = v;
+    }
+    __syncthreads();
+    return incl - own + (warp ? s_w[warp - 1] : 0ll);
+  };
+  long long own = 0;
+  for (int g = g0; g < g1; ++g) own += cnt[g];
+  long long pre = block_excl_scan(own);
+  const long long total = s_w[31];
+  if (tid == 0) {
+    const long long want = (total + int64_t(per_slot) * slots - 1) / (int64_t(per_slot) * slots);
+    s_u = int(want > (long long)umin ? want : (long long)umin);
+  }
+  for (int g = g0; g < g1; ++g) {
+    start[g] = int32_t(pre);
+    pre += cnt[g];
+  }
+  __syncthreads();
+  const int U = s_u;
+  long long uown = 0;
+  for (int g = g0; g < g1; ++g) uown += (cnt[g] + U - 1) / U;
+  long long upre = block_excl_scan(uown);
+  for (int g = g0; g < g1; ++g) {
+    ustart[g] = int32_t(upre);
+    upre += (cnt[g] + U - 1) / U;
+  }
+  if (tid == 0) {
+    scal[0] = int32_t(s_w[31]);
+    scal[1] = int32_t(total);
+    scal[2] = U;
+  }
+}
+
+// tile-major units: unit = (tile t, query blocks blist[i0..i1)); the blocks of a tile in
+// increasing order
+__global__ void tile_units_fill_kernel(const uint32_t* __restrict__ bits, int32_t nqb, int32_t ntiles,
+                                       const int32_t* __restrict__ cnt, const int32_t* __restrict__ start,
+                                       const int32_t* __restrict__ ustart, const int32_t* __restrict__ scal,
+                                       int32_t* __restrict__ blist, int32_t* __restrict__ ulist) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int nwords = (ntiles + 31) >> 5;
+  int pos = start[t];
+  for (int b = 0; b < nqb; ++b)
+    if ((bits[int64_t(b) * nwords + (t >> 5)] >> (t & 31)) & 1u) blist[pos++] = b;
+  const int U = scal[2], c = cnt[t], s0 = start[t];
+  int u = ustart[t];
+  for (int i = 0; i < c; i += U, ++u) {
+    ulist[3 * u] = t;
+    ulist[3 * u + 1] = s0 + i;
+    ulist[3 * u + 2] = s0 + min(c, i + U);
+  }
+}
+
+// block-major units (FILTER operand too wide to keep a tile resident): unit = (query block b,
+// positions [i0, i1) of its tile list tlist[b][...], flat index b * ntiles + i)
+__global__ void block_units_fill_kernel(int32_t nqb, int32_t ntiles, const int32_t* __restrict__ cnt,
+                                        const int32_t* __restrict__ ustart, const int32_t* __restrict__ scal,
+                                        int32_t* __restrict__ ulist) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nqb) return;
+  const int U = scal[2], c = cnt[b];
+  int u = ustart[b];
+  for (int i = 0; i < c; i += U, ++u) {
+    ulist[3 * u] = b;
+    ulist[3 * u + 1] = int32_t(int64_t(b) * ntiles + i);
+    ulist[3 * u + 2] = int32_t(int64_t(b) * ntiles + min(c, i + U));
+  }
+}
+
+__global__ void iota_i32_kernel(int32_t* __restrict__ a, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = int32_t(i);
 }
 
 __global__ void gather_rows_f64_kernel(const double* __restrict__ Q, const int32_t* __restrict__ perm, int64_t nq,
@@ -606,10 +783,52 @@ void launch_query_cluster_dist(const double* Q, int64_t nq, int32_t d, const dou
 void launch_block_tile_lists(const double* dq, int32_t C, const int32_t* qperm, int64_t bn, int32_t nqb,
                              const float* tau, const float* qn, float xn_max, float eps_rel, const double* rad,
                              const int32_t* tclo, const int32_t* tchi, int32_t ntiles, int32_t* tlist,
-                             int32_t* tcount, cudaStream_t s) {
+                             int32_t* tcount, uint32_t* bits, cudaStream_t s) {
   set_dynamic_smem(block_tile_lists_kernel, size_t(C));
   block_tile_lists_kernel<<<unsigned(nqb), 256, size_t(C), s>>>(dq, C, qperm, bn, tau, qn, xn_max, eps_rel, rad,
-                                                                 tclo, tchi, ntiles, tlist, tcount);
+                                                                 tclo, tchi, ntiles, tlist, tcount, bits);
+  DK_CHECK_LAUNCH();
+}
+
+size_t ball_sort_temp_bytes(int64_t nq) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                  static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), int(nq));
+  return bytes + 256;
+}
+
+void launch_sort_queries_by_ball(const int32_t* nearest, int64_t nq, int32_t C, int32_t* nearest_sorted,
+                                 int32_t* iota, int32_t* qperm, void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (nq <= 0) return;
+  iota_i32_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(iota, nq);
+  DK_CHECK_LAUNCH();
+  int bits = 1;
+  while ((int64_t(1) << bits) < int64_t(C)) ++bits;
+  // stable LSD radix sort: queries of a ball keep their batch order (== a counting sort)
+  DK_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, nearest, nearest_sorted, iota, qperm, int(nq), 0, bits,
+                                          s));
+  g_launches.fetch_add(1);
+}
+
+void launch_tile_units(const uint32_t* bits, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* tcnt,
+                       int32_t* tstart, int32_t* ustart, int32_t* scal, int32_t* blist, int32_t* ulist,
+                       cudaStream_t s) {
+  tile_count_kernel<<<unsigned((ntiles + 255) / 256), 256, 0, s>>>(bits, nqb, ntiles, tcnt);
+  DK_CHECK_LAUNCH();
+  // >= 4 units per CTA; a unit keeps its tile resident while its query blocks stream past
+  unit_plan_kernel<<<1, 1024, 0, s>>>(tcnt, ntiles, slots, 4, 4, tstart, ustart, scal);
+  DK_CHECK_LAUNCH();
+  tile_units_fill_kernel<<<unsigned((ntiles + 255) / 256), 256, 0, s>>>(bits, nqb, ntiles, tcnt, tstart, ustart, scal,
+                                                                        blist, ulist);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_block_units(const int32_t* tcount, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* bstart,
+                        int32_t* ustart, int32_t* scal, int32_t* ulist, cudaStream_t s) {
+  // units of ~equal length (>= 8 tiles) so the persistent CTAs finish together
+  unit_plan_kernel<<<1, 1024, 0, s>>>(tcount, nqb, slots, 4, 8, bstart, ustart, scal);
+  DK_CHECK_LAUNCH();
+  block_units_fill_kernel<<<unsigned((nqb + 127) / 128), 128, 0, s>>>(nqb, ntiles, tcount, ustart, scal, ulist);
   DK_CHECK_LAUNCH();
 }
 
@@ -626,16 +845,6 @@ void launch_scatter_knn(const int64_t* idx_p, const double* d2_p, const int32_t*
   DK_CHECK_LAUNCH();
 }
 
-uint32_t max_count(const uint32_t* v, int64_t n, uint32_t* scratch, cudaStream_t s) {
-  DK_CUDA(cudaMemsetAsync(scratch, 0, sizeof(uint32_t), s));
-  max_u32_kernel<<<unsigned(std::min<int64_t>(148, (n + 255) / 256)), 256, 0, s>>>(v, n, scratch);
-  DK_CHECK_LAUNCH();
-  uint32_t m = 0;
-  DK_CUDA(cudaMemcpyAsync(&m, scratch, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  DK_CUDA(cudaStreamSynchronize(s));
-  return m;
-}
-
 void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s) {
   if (count <= 0) return;
   fill_float_kernel<<<unsigned((count + 255) / 256), 256, 0, s>>>(p, count, v);
@@ -644,7 +853,7 @@ void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s) {
 
 void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
                           float xn_max, float eps_rel, float* tau, cudaStream_t s) {
-  static const bool sort_path = std::getenv("DK_TAU_SORT") != nullptr;  // A/B switch
+  const bool sort_path = std::getenv("DK_TAU_SORT") != nullptr;  // A/B switch (read per call: tests)
   if (!sort_path) {
     const size_t smem = size_t(std::max(nseg, 1)) * 4;
     if (smem > 232448) throw Error{DK_EINVAL, "too many k-NN segments"};
@@ -661,40 +870,49 @@ void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64
   DK_CHECK_LAUNCH();
 }
 
-void launch_select_rerank(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
-                          const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
-                          float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* status,
-                          cudaStream_t s, int32_t max_cnt, const int64_t* perm) {
-  // candidate buffer sized by the largest count actually seen (occupancy: c3 averages ~200
-  // candidates per query against a cap of 8192); counts above the cap overflow as before
-  const int B = std::max(2, pow2_ceil(max_cnt > 0 ? std::min(max_cnt, cap) : cap));
+void launch_select(const float* X, int64_t global_offset, int32_t d, const double* Q, int64_t nq, int32_t k,
+                   const unsigned long long* cand, const uint32_t* cand_cnt, int32_t cap, const float* qn,
+                   float xn_max, float eps_rel, int64_t* idx_out, double* d2_out, int32_t* lists, int32_t* counts,
+                   int num_sms, cudaStream_t s, const int64_t* perm) {
+  // lists: [2][nq] (slow, overflow), counts: [2] device counters, zeroed by the caller
+  if (nq <= 0) return;
+  int32_t* slow_list = lists;
+  int32_t* ovf_list = lists + nq;
   const int Kp = std::max(32, pow2_ceil(k));
-  const size_t smem =
-      size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double) + kSelHist * sizeof(uint32_t);
-  set_dynamic_smem(select_rerank_kernel, smem);
-  if (smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
-  select_rerank_kernel<<<unsigned(nq), 256, smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,
-                                                       xn_max, eps_rel, B, idx_out, d2_out, status, perm);
+  const size_t fast_smem = size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double) + kSelHist * sizeof(uint32_t);
+  set_dynamic_smem(select_fast_kernel, fast_smem);
+  if (fast_smem > 232448) throw Error{DK_EINVAL, "k too large for the k-NN selection buffer"};
+  select_fast_kernel<<<unsigned(nq), 256, fast_smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,
+                                                          xn_max, eps_rel, idx_out, d2_out, slow_list, counts,
+                                                          ovf_list, counts + 1, perm);
+  DK_CHECK_LAUNCH();
+  const int B = std::max(2, pow2_ceil(cap));
+  const size_t slow_smem = size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double);
+  if (slow_smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
+  set_dynamic_smem(select_slow_kernel, slow_smem);
+  select_slow_kernel<<<unsigned(std::max(1, num_sms)), 256, slow_smem, s>>>(
+      X, global_offset, d, Q, k, cand, cand_cnt, cap, qn, xn_max, eps_rel, B, idx_out, d2_out, slow_list, counts, perm);
   DK_CHECK_LAUNCH();
 }
 
 void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
-                               const int32_t* qlist, int32_t nlist, int32_t k, int64_t* idx_out, double* d2_out,
-                               cudaStream_t s) {
-  if (nlist <= 0) return;
+                               const int32_t* qlist, const int32_t* qcount, int32_t k, int64_t* idx_out,
+                               double* d2_out, int num_sms, cudaStream_t s) {
   const int Kp = pow2_ceil(k);
   const int B = std::max(1024, 2 * Kp);
   const size_t smem = size_t(B) * sizeof(Key128);
   set_dynamic_smem(exact_knn_kernel, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "k too large for the exact k-NN fallback"};
-  exact_knn_kernel<<<unsigned(nlist), 256, smem, s>>>(X, n_local, global_offset, d, Q, qlist, k, B, idx_out, d2_out);
+  exact_knn_kernel<<<unsigned(std::max(1, num_sms)), 256, smem, s>>>(X, n_local, global_offset, d, Q, qlist, qcount,
+                                                                     k, B, idx_out, d2_out);
   DK_CHECK_LAUNCH();
 }
 
 void launch_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_in, const double* d2_in,
                        int64_t* idx_out, double* d2_out, cudaStream_t s) {
   if (parts > 64) throw Error{DK_EINVAL, "dk_merge_topk supports at most 64 parts"};
-  merge_topk_kernel<<<unsigned((nq + 127) / 128), 128, 0, s>>>(parts, nq, k, idx_in, d2_in, idx_out, d2_out);
+  if (nq <= 0) return;
+  merge_topk_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(parts, nq, k, idx_in, d2_in, idx_out, d2_out);
   DK_CHECK_LAUNCH();
 }
 

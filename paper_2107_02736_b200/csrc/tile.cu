@@ -78,8 +78,18 @@ int64_t balanced_tiles_per_unit(int ntiles, int ngroups, int nslots) {
   return best;
 }
 
-Plan make_plan(int kblocks, int ntiles, int ngroups, int nslots, int mode, bool pair) {
+Plan make_plan(int kblocks, int ntiles, int ngroups, int nslots, int mode, bool pair, bool tmajor = false) {
   Plan pl{};
+  if (tmajor) {
+    pl.a_resident = 0;
+    int st = 3;
+    while (st < 8 && tile_smem_bytes(kblocks, 0, st + 1, mode, false, true) <= kMaxSmem) ++st;
+    pl.stages = st;
+    pl.tiles_per_unit = 1;
+    pl.ncc = 1;
+    pl.smem = tile_smem_bytes(kblocks, 0, st, mode, false, true);
+    return pl;
+  }
   // keep the query block resident when it fits next to a >=3-stage ring
   if (tile_smem_bytes(kblocks, 1, 3, mode, pair) <= kMaxSmem) {
     pl.a_resident = 1;
@@ -149,6 +159,10 @@ CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint3
   return m;
 }
 
+bool tile_major_fits(int32_t Kp) {
+  return tile_smem_bytes(Kp / kBK, 0, 3, MODE_FILTER, false, true) <= kMaxSmem;
+}
+
 static bool use_pair(int nqb) { return g_pair_enabled && nqb >= 2 && nqb % 2 == 0; }
 
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms) {
@@ -171,7 +185,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const bool pr = a.ulist == nullptr && use_pair(nqb);
   const int ngroups = pr ? nqb / 2 : nqb;
   const int nslots = pr ? num_sms / 2 : num_sms;  // CTAs (or CTA pairs) resident at once
-  const Plan pl = make_plan(kblocks, ntiles, ngroups, nslots, a.mode, pr);
+  const bool tmajor = a.tmajor != 0;
+  if (tmajor && (a.mode != MODE_FILTER || a.ulist == nullptr || a.blist == nullptr))
+    throw Error{DK_EINVAL, "internal: tile-major sweeps are FILTER tile lists"};
+  const Plan pl = make_plan(kblocks, ntiles, ngroups, nslots, a.mode, pr, tmajor);
 
   TileParams p{};
   p.nq = q.nq;
@@ -207,10 +224,14 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.ulist = a.ulist;
   p.tlist = a.tlist;
   p.nunits_list = a.nunits_list;
+  p.nunits_dev = a.nunits_dev;
+  p.tmajor = tmajor ? 1 : 0;
+  p.blist = a.blist;
   p.guard = a.guard;
   if (a.ncc_out) *a.ncc_out = pl.ncc;
 
-  const int nunits = a.ulist != nullptr ? a.nunits_list : ngroups * pl.ncc;
+  // a device-side unit count is unknown here: one CTA per SM, surplus CTAs find no unit
+  const int nunits = a.ulist != nullptr ? (a.nunits_dev != nullptr ? nslots : a.nunits_list) : ngroups * pl.ncc;
   if (nunits <= 0) return;
   if (a.ulist != nullptr && (pr || a.mode != MODE_FILTER)) throw Error{DK_EINVAL, "internal: tile lists are FILTER-only"};
   const int grid = std::min(nunits, nslots) * (pr ? 2 : 1);

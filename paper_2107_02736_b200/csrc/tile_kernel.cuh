@@ -93,6 +93,12 @@ struct TileParams {
   const int32_t* ulist;
   const int32_t* tlist;
   int32_t nunits_list;
+  // tile-major FILTER (tmajor = 1): unit u = dataset tile ulist[3u] (resident in shared memory)
+  // x query blocks blist[ulist[3u+1] .. ulist[3u+2]) streamed through the ring; the unit count
+  // is read from device memory (built on the device, capi.cu knn_device)
+  int32_t tmajor;
+  const int32_t* blist;
+  const int32_t* nunits_dev;
   const float* xn;         // [n_pad] |x|^2 (encoding-consistent)
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
@@ -106,9 +112,14 @@ struct TileParams {
   const uint32_t* guard;     // optional: the sweep is skipped when (*guard & 6) != 0 (queries not exact-mode)
 };
 
-__host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode, bool pair) {
+__host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode, bool pair,
+                                                  bool tmajor = false) {
   size_t a = a_resident ? size_t(kblocks) * kABlockBytes : size_t(stages) * kABlockBytes;
   size_t b = size_t(stages) * (pair ? kBBlockBytes / 2 : kBBlockBytes);
+  if (tmajor) {  // resident dataset tile + ring of query K-blocks
+    a = size_t(stages) * kABlockBytes;
+    b = size_t(kblocks) * kBBlockBytes;
+  }
   size_t stage = mode == MODE_FILTER ? size_t(kBM) * kStageCap * 8 + kBM * 4 : 0;
   return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + stage + 512 /*barriers*/;
 }
@@ -244,7 +255,21 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
 #pragma unroll
           for (int j = 0; j < 32; ++j) hits |= (d2v[j] <= tau ? 1u : 0u) << j;
         }
-        if (hits) {  // appended candidates: one shared (and at most one global) atomic per chunk
+        if (hits && scnt == nullptr) {  // tile-major sweep: straight to the global list
+          const uint32_t g = atomicAdd(&p.cand_cnt[row], uint32_t(__popc(hits)));
+          uint32_t slot = g;
+          while (hits) {
+            const int j = __ffs(hits) - 1;
+            hits &= hits - 1;
+            float dj = d2v[0];
+#pragma unroll
+            for (int i = 1; i < 32; ++i) dj = (i == j) ? d2v[i] : dj;
+            const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(fmaxf(dj, 0.f))) << 32) |
+                                           static_cast<unsigned long long>(cbase + j);
+            if (slot < uint32_t(p.cap)) p.cand[size_t(row) * p.cap + slot] = key;
+            ++slot;
+          }
+        } else if (hits) {  // appended candidates: one shared (and at most one global) atomic per chunk
           const uint32_t nh = uint32_t(__popc(hits));
           const uint32_t pos = atomicAdd(&scnt[lrow], nh);
           const uint32_t first_spill = max(pos, uint32_t(kStageCap));
@@ -308,9 +333,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
   constexpr int kBStage = kPair ? kBBlockBytes / 2 : kBBlockBytes;  // B bytes per CTA per stage
+  const bool tmajor = MODE == MODE_FILTER && !kPair && p.tmajor != 0;
   uint8_t* smemA = smem;
   uint8_t* smemB = smem + (p.a_resident ? size_t(p.kblocks) * kABlockBytes : size_t(stages) * kABlockBytes);
   float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBStage);  // [kXnSlots][256]
+  if (tmajor) {  // [resident tile: kblocks x 32 KB][ring: stages x 16 KB query K-blocks][norms]
+    smemB = smem;
+    smemA = smem + size_t(p.kblocks) * kBBlockBytes;
+    smemX = reinterpret_cast<float*>(smemA + size_t(stages) * kABlockBytes);
+  }
   unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smemX + kXnSlots * kBN);  // FILTER staging
   uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (MODE == MODE_FILTER ? kBM * kStageCap : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(scnt + (MODE == MODE_FILTER ? kBM : 0));
@@ -330,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool leader = crank == 0;
   // work units: (query-block group, column chunk); a pair owns 2 query blocks
   const int ngroups = kPair ? p.nqb / 2 : p.nqb;
-  const int nunits = p.ulist != nullptr ? p.nunits_list : ngroups * p.ncc;
+  const int nunits = p.ulist != nullptr ? (p.nunits_dev != nullptr ? *p.nunits_dev : p.nunits_list) : ngroups * p.ncc;
   const int first_unit = kPair ? int(blockIdx.x) / 2 : int(blockIdx.x);
   const int unit_step = kPair ? int(gridDim.x) / 2 : int(gridDim.x);
 
@@ -371,7 +402,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ===================== TMA producer (each CTA) =====================
-    if (lane == 0) {
+    if (lane == 0 && tmajor) {
+      // tile-major FILTER: the unit's dataset tile once into the resident buffer, then the
+      // query blocks that list it through the ring (they stay in L2: a batch's whole query
+      // operand is a few MB; the tile is read from DRAM about once per batch)
+      const uint64_t pol_b = policy_evict_first();
+      const uint64_t pol_a = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int uiter = 0;
+      uint32_t titer = 0;
+      for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
+        const int col0 = __ldg(p.ulist + 3 * u) * kBN;
+        const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
+        mbar_wait(aempty_bar, (uiter & 1) ^ 1);
+        mbar_arrive_expect_tx(afull_bar, uint32_t(p.kblocks) * kBBlockBytes);
+        for (int kb = 0; kb < p.kblocks; ++kb)
+          tma_load_2d(smemB + size_t(kb) * kBBlockBytes, &tmapB, afull_bar, kb * kBK, col0, pol_b);
+        for (int i = i0; i < i1; ++i, ++titer) {
+          const int qb = __ldg(p.blist + i);
+          const uint32_t xs = titer % kXnSlots;
+          mbar_wait(&xempty_bar[xs], ((titer / kXnSlots) & 1) ^ 1);
+          mbar_arrive_expect_tx(&xfull_bar[xs], kBN * 4);
+          bulk_load(smemX + xs * kBN, p.xn + col0, kBN * 4, &xfull_bar[xs]);
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full_bar[stage], kABlockBytes);
+            tma_load_2d(smemA + size_t(stage) * kABlockBytes, &tmapA, &full_bar[stage], kb * kBK, qb * kBM, pol_a);
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    } else if (lane == 0) {
       const uint64_t pol_b = policy_evict_last();   // dataset tiles are re-read by other query blocks
       const uint64_t pol_a = policy_evict_last();
       int stage = 0;
@@ -438,7 +500,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
-    if (lane == 0 && leader) {
+    if (lane == 0 && tmajor) {
+      constexpr uint32_t idesc = idesc_f16_f32(kBM, kBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int uiter = 0;
+      const uint32_t a0 = smem_u32(smemA), b0 = smem_u32(smemB);
+      for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
+        const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
+        mbar_wait(afull_bar, uiter & 1);
+        tc_fence_after();
+        for (int i = i0; i < i1; ++i) {
+          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + uint32_t(acc * kBN);
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint64_t ad = sw128_kmajor_desc(a0 + uint32_t(stage) * kABlockBytes);
+            const uint64_t bd = sw128_kmajor_desc(b0 + uint32_t(kb) * kBBlockBytes);
+            const int ksteps = kb == p.kblocks - 1 ? p.klast : kBK / 16;
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              if (k < ksteps) mma_f16_ss(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+            mma_commit(&empty_bar[stage]);
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+          }
+          mma_commit(&tfull_bar[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        mma_commit(aempty_bar);  // the resident tile may be replaced
+      }
+    } else if (lane == 0 && leader) {
       constexpr uint32_t idesc = idesc_f16_f32(kPair ? 2 * kBM : kBM, kBN);
       int stage = 0;
       uint32_t phase = 0;
@@ -544,6 +639,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         usum += double((a0.x + a0.y) + (a1.x + a1.y));
       }
       p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
+    }
+  } else if (tmajor && warp >= kEpiWarp0) {
+    // ===================== tile-major FILTER epilogue =====================
+    // the query block changes every iteration: its |q|^2 and thresholds are read per tile
+    // pass, candidates go straight to the global lists (one atomic per 32-column chunk with hits)
+    if constexpr (MODE == MODE_FILTER) {
+      const int ew = int(warp) - kEpiWarp0;
+      const int quarter = int(warp & 3);
+      const int cg = ew >> 2;
+      const int lrow = quarter * 32 + int(lane);
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      uint32_t titer = 0;
+      const float m2s = *p.m2s;
+      float mn_unused = 0.f;
+      for (int u = first_unit; u < nunits; u += unit_step) {
+        const int64_t cbase = int64_t(__ldg(p.ulist + 3 * u)) * kBN + cg * 64;
+        const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
+        const bool full = cbase + 64 <= p.n;
+        for (int i = i0; i < i1; ++i, ++titer) {
+          const int row = __ldg(p.blist + i) * kBM + lrow;
+          const float qn = __ldg(p.qn + row);
+          const float tau = __ldg(p.tau + row);
+          const uint32_t xs = titer % kXnSlots;
+          mbar_wait(&tfull_bar[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kBN + cg * 64);
+          uint32_t r0[32], r1[32];
+          tmem_ld32(taddr, r0);
+          tmem_ld32(taddr + 32u, r1);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
+          const float* xsm = smemX + xs * kBN + cg * 64;
+          float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+          epi_chunk<MODE>(r0, xsm, qn, m2s, 0.f, tau, full, cbase, p.n, a0, a1, mn_unused, p, row, nullptr,
+                          nullptr, lrow);
+          epi_chunk<MODE>(r1, xsm + 32, qn, m2s, 0.f, tau, full, cbase + 32, p.n, a0, a1, mn_unused, p, row,
+                          nullptr, nullptr, lrow);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xempty_bar[xs]);
+        }
+      }
     }
   } else if (warp >= kEpiWarp0) {
     // ===================== epilogue (each CTA, its own 128 rows) =====================

@@ -45,6 +45,7 @@ class Dataset:
         self.global_n = global_n
         self.precision = precision
         self._sq_norms = None
+        self._data64 = None
         self._finalizer = weakref.finalize(self, _free_handle, handle)
 
     @classmethod
@@ -99,6 +100,17 @@ class Dataset:
             out.flags.writeable = False
             self._sq_norms = out
         return self._sq_norms
+
+    def data64(self) -> np.ndarray:
+        """Read-only fp64 copy of the host rows, cached after first use (data.py:77-83).
+
+        Not used by any estimator here (the device holds the rows); provided for the
+        reference's own callers (harness.py:247, analysis.py:215-283, cli.py:148-200)."""
+        if self._data64 is None:
+            d64 = np.asarray(self.data).astype(np.float64)
+            d64.flags.writeable = False
+            self._data64 = d64
+        return self._data64
 
     def free(self) -> None:
         self._finalizer()

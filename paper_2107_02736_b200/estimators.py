@@ -38,11 +38,11 @@ from .sampler import resolve_sampler
 
 __all__ = [
     "Estimate", "BatchKde", "RspState", "naive_kde", "rs_kde", "rsp_kde", "deann", "deann_batch",
-    "naive_kde_into", "deann_arrays", "kernel_from_distance",
+    "naive_kde_into", "deann_arrays", "kernel_from_distance", "EstimateList",
 ]
 
 
-@dataclass
+@dataclass(slots=True)
 class Estimate:
     """A single KDE estimate plus its cost counters (estimators.py:57-72)."""
 
@@ -60,6 +60,70 @@ class BatchKde:
 
     values: np.ndarray
     kernel_evals: int
+
+
+class EstimateList(list):
+    """``list[Estimate]`` of a batch, built from the batch's result arrays on first use.
+
+    ``deann_batch`` returns one ``Estimate`` per query (estimators.py:382-410).  Creating
+    10,000 Python objects costs about as much host time as the whole device batch, so the
+    list keeps the value / counter arrays and materialises the ``Estimate`` objects the first
+    time it is read (indexing, iteration, len, comparison, copy, mutation, pickling...).
+    After that it is an ordinary list.  ``values`` / ``kernel_evals`` / ... give the arrays
+    without materialising.
+    """
+
+    __slots__ = ("values", "kernel_evals", "neighbors_used", "samples_used", "truncated", "clamped", "_lazy")
+
+    def __init__(self, values, kernel_evals, neighbors_used, samples_used, truncated=False, clamped=False):
+        super().__init__()
+        n = len(values)
+        self.values = np.asarray(values, dtype=np.float64)
+        self.kernel_evals = np.broadcast_to(np.asarray(kernel_evals, dtype=np.int64), (n,))
+        self.neighbors_used = np.broadcast_to(np.asarray(neighbors_used, dtype=np.int64), (n,))
+        self.samples_used = np.broadcast_to(np.asarray(samples_used, dtype=np.int64), (n,))
+        self.truncated = np.broadcast_to(np.asarray(truncated, dtype=bool), (n,))
+        self.clamped = np.broadcast_to(np.asarray(clamped, dtype=bool), (n,))
+        self._lazy = True
+
+    def _m(self):
+        if self._lazy:
+            self._lazy = False
+            list.extend(self, map(Estimate, self.values.tolist(), self.kernel_evals.tolist(),
+                                  self.neighbors_used.tolist(), self.samples_used.tolist(), self.truncated.tolist(),
+                                  self.clamped.tolist()))
+        return self
+
+    def __len__(self):
+        return len(self.values) if self._lazy else list.__len__(self)
+
+    def __bool__(self):
+        return len(self) > 0
+
+    def __array__(self, dtype=None, copy=None):
+        return np.asarray(list(self._m()), dtype=dtype if dtype is not None else object)
+
+    def __reduce_ex__(self, protocol):
+        return (list, (list(self._m()),))
+
+
+def _lazy_method(name):
+    base = getattr(list, name)
+
+    def method(self, *args, **kwargs):
+        return base(self._m(), *args, **kwargs)
+
+    method.__name__ = name
+    return method
+
+
+for _name in ("__getitem__", "__iter__", "__contains__", "__reversed__", "__repr__", "__eq__", "__ne__", "__lt__",
+              "__le__", "__gt__", "__ge__", "__add__", "__mul__", "__rmul__", "__iadd__", "__imul__", "__setitem__",
+              "__delitem__", "__sizeof__", "append", "extend", "insert", "pop", "remove", "clear", "index", "count",
+              "copy", "sort", "reverse"):
+    setattr(EstimateList, _name, _lazy_method(_name))
+EstimateList.__radd__ = lambda self, other: list(other) + list(self._m())  # noqa: E731
+EstimateList.__hash__ = None
 
 
 def _queries64(queries, d: int) -> np.ndarray:
@@ -99,9 +163,9 @@ def naive_kde(dataset, kernel, queries) -> BatchKde:
     return BatchKde(values=values, kernel_evals=q.shape[0] * ds.n)
 
 
-def kernel_from_distance(kernel, dist):
+def kernel_from_distance(spec, dist):
     """Kernel values from precomputed family distances (kernels.py:65-83), on the GPU."""
-    spec = as_spec(kernel)
+    spec = as_spec(spec)
     scalar = np.isscalar(dist) or np.ndim(dist) == 0
     d = np.ascontiguousarray(np.asarray(dist, dtype=np.float64).ravel())
     if not np.all(np.isfinite(d)):
@@ -117,9 +181,9 @@ def kernel_from_distance(kernel, dist):
     return out.reshape(np.shape(dist))
 
 
-def kernel_pair(kernel, x, y) -> float:
+def kernel_pair(spec, x, y) -> float:
     """Kernel value between two points with the family's own metric (kernels.py:86-106)."""
-    spec = as_spec(kernel)
+    spec = as_spec(spec)
     xv = np.asarray(x, dtype=np.float64).ravel()
     yv = np.asarray(y, dtype=np.float64).ravel()
     if xv.shape != yv.shape:
@@ -345,11 +409,14 @@ def deann_batch(dataset, kernel, ann, queries, k: int, m: int, *, rng=None, rsp_
     if k == 0 or _is_gpu_bruteforce(ann, ds):
         seed, base = resolve_sampler(rng).take(q.shape[0]) if m > 0 else (0, 0)
         values, _, _ = deann_arrays(ds, spec, q, k, m, seed=seed, query_base=base)
-        return [Estimate(value=float(v), kernel_evals=k + m, neighbors_used=k, samples_used=m,
-                         truncated=(m == 0 and k < n)) for v in values]
+        return EstimateList(values, k + m, k, m, truncated=(m == 0 and k < n))
     if _is_gpu_ivf(ann, ds):
         return _deann_ivf_batch(ds, spec, ann, q, k, m, rng)
-    return [deann(ds, spec, ann, q[j], k, m, rng=rng, rsp_state=rsp_state) for j in range(q.shape[0])]
+    # black-box index: one call per query in query order (estimators.py:405-409) over ONE
+    # sampler, so query j draws from stream position base + j exactly as the fused batch does
+    # (an int seed must not restart the stream at every query)
+    sampler = resolve_sampler(rng) if m > 0 else None
+    return [deann(ds, spec, ann, q[j], k, m, rng=sampler) for j in range(q.shape[0])]
 
 
 def _is_gpu_ivf(ann, ds: Dataset) -> bool:
@@ -372,10 +439,8 @@ def _deann_ivf_batch(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, rng)
                                         spec.bandwidth, k, m, ann.n_probe, seed, base, values.ctypes.data,
                                         khat.ctypes.data, _lib.current_stream()))
     if m == 0:
-        return [Estimate(value=float(v), kernel_evals=int(c), neighbors_used=int(c), samples_used=0,
-                         truncated=int(c) < n) for c, v in zip(khat, values)]
-    return [Estimate(value=float(v), kernel_evals=int(c) + m, neighbors_used=int(c), samples_used=m)
-            for c, v in zip(khat, values)]
+        return EstimateList(values, khat, khat, 0, truncated=khat < n)
+    return EstimateList(values, khat.astype(np.int64) + m, khat, m)
 
 
 def _deann_rsp(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, state, independent: bool) -> list[Estimate]:
@@ -403,13 +468,11 @@ def _deann_rsp(ds: Dataset, spec, ann, q: np.ndarray, k: int, m: int, state, ind
     else:
         idx, z1, k_hat = None, np.zeros(nq), np.zeros(nq, dtype=np.int64)
     z, taken = _rsp_walk(state, spec, q, m, idx, independent)
-    out = []
-    for j in range(nq):
-        kh, t = int(k_hat[j]), int(taken[j])
-        z2 = z[j] / t if t else 0.0
-        value = (kh / n) * float(z1[j]) + ((n - kh) / n) * z2
-        out.append(Estimate(value=value, kernel_evals=kh + t, neighbors_used=kh, samples_used=t, clamped=t < m))
-    return out
+    kh = np.asarray(k_hat, dtype=np.int64)
+    t = taken.astype(np.int64)
+    z2 = np.divide(z, t, out=np.zeros_like(z), where=t > 0)
+    value = (kh / n) * np.asarray(z1, dtype=np.float64) + ((n - kh) / n) * z2
+    return EstimateList(value, kh + t, kh, t, clamped=t < m)
 
 
 def _deann_rsp_indep(ds, spec, ann, q, j, k, m, state):

@@ -201,6 +201,32 @@ class IvfAnnIndex(AnnIndex):
     def build(cls, dataset, n_clusters: int, seed: int, n_probe: int) -> "IvfAnnIndex":
         return cls(dataset, ivf_build(dataset, n_clusters, seed), n_probe)
 
+    # The reference's host-side list layout (ann.py:248-255).  Queries never read these
+    # (the device holds the list-contiguous rows); they exist for the reference's own
+    # callers, e.g. harness._Runner.warm touching ann._vectors32 (harness.py:249).
+    @property
+    def _row_ids(self) -> np.ndarray:
+        if getattr(self, "_row_ids_", None) is None:
+            a = self.index.assignments
+            order = np.concatenate(list(a)) if len(a) else np.empty(0, np.int64)
+            self._row_ids_ = np.ascontiguousarray(order, dtype=np.int64)
+        return self._row_ids_
+
+    @property
+    def _vectors32(self) -> np.ndarray:
+        if getattr(self, "_vectors32_", None) is None:
+            self._vectors32_ = np.ascontiguousarray(np.asarray(self._ds.data)[self._row_ids])
+        return self._vectors32_
+
+    @property
+    def _norms32(self) -> np.ndarray:
+        return self._ds.sq_norms[self._row_ids].astype(np.float32)
+
+    @property
+    def _offsets(self) -> np.ndarray:
+        sizes = np.array([len(a) for a in self.index.assignments], dtype=np.int64)
+        return np.concatenate([[0], np.cumsum(sizes)])
+
     def query_batch(self, queries, k: int):
         Q = np.ascontiguousarray(np.atleast_2d(np.asarray(queries, dtype=np.float64)))
         _check_query(self.index, k, self.n_probe, Q.shape[1])

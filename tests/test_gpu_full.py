@@ -144,15 +144,14 @@ def test_c5_scale_out_properties():
         lo, hi = (r * n) // 4, ((r + 1) * n) // 4
         acc += g.naive_kde(g.Dataset.from_array(W.X[lo:hi]), kern, W.Q).values * (hi - lo)
     assert _rel(acc / n, full) < 1e-5
-    # oracle on two queries over a 1M-row prefix (fp64 copy of all 8M rows is 6 GB)
-    pre = W.X[:1_000_000]
-    got = g.naive_kde(g.Dataset.from_array(pre), kern, W.Q[:2]).values
-    assert _rel(got, O.naive_kde(O.Data(pre), "gaussian", h, W.Q[:2])) < KDE_RTOL
+    # exact KDE over ALL 8M rows against the fp64 oracle on 16 seeded queries of the batch
+    # (the oracle's fp64 copy of the rows is 6 GB of host memory; ~1 s per query)
+    od = O.Data(W.X)
+    sel16 = np.random.default_rng(5).choice(len(W.Q), 16, replace=False)
+    assert _rel(full[sel16], O.naive_kde(od, "gaussian", h, W.Q[sel16])) < KDE_RTOL
     # DEANN at the config's own k = 100, m = 2000 over all 8M rows: neighbour sets equal the
     # oracle's brute force, estimates equal the reference algorithm replaying the GPU's
-    # Philox stream (the fp64 oracle copy of 8M x 96 rows is 6 GB of host memory)
-    del pre
-    od = O.Data(W.X)
+    # Philox stream
     sel = [0, 1, 2049]
     vals, nbr, _ = g.deann_arrays(ds, kern, W.Q[sel], 100, 2000, seed=5, export_neighbors=True)
     for j, qj in enumerate(sel):
@@ -161,3 +160,40 @@ def test_c5_scale_out_properties():
         ref = O.deann(od, "gaussian", h, NeighborReplay(ri, rd), W.Q[qj], 100, 2000,
                       rng=IndexReplay(5, j, od.n))[0]
         assert vals[j] == pytest.approx(ref, rel=1e-11)
+
+
+def test_c4_exponential_deann_config_size():
+    """c4 DEANN with the exponential kernel at the config's k = 50, m = 500 (tensor-core k-NN on
+    784-wide rows + Philox residual), replayed through the reference algorithm."""
+    W = workloads.make("c4")
+    ds, od = g.Dataset.from_array(W.X), O.Data(W.X)
+    h = MAN["c4"]["h"]
+    sel = np.random.default_rng(12).choice(10_000, 6, replace=False)
+    Q = W.Q[sel]
+    vals, nbr, smp = g.deann_arrays(ds, g.KernelSpec("exponential", h), Q, 50, 500, seed=13, query_base=100,
+                                    export_neighbors=True, export_samples=True)
+    for j in range(len(Q)):
+        ri, rd = O.brute_force_knn(od, Q[j], 50)
+        np.testing.assert_array_equal(nbr[j], ri)
+        assert not np.isin(smp[j], ri).any()  # residual samples exclude the neighbours
+        ref = O.deann(od, "exponential", h, NeighborReplay(ri, rd), Q[j], 50, 500,
+                      rng=IndexReplay(13, 100 + j, od.n))[0]
+        assert vals[j] == pytest.approx(ref, rel=1e-11)
+
+
+def test_c1_rs_config_m500():
+    """c1 RS with m = 500 over the whole 1,000-query batch: the GPU's values equal the reference's
+    rs_kde fed the same Philox stream (estimators.py:152-164), through both the batch path and
+    the per-query drop-in rs_kde."""
+    W = workloads.make("c1")
+    ds, od = g.Dataset.from_array(W.X), O.Data(W.X)
+    kern = g.KernelSpec("gaussian", 2.0)
+    vals, _, smp = g.deann_arrays(ds, kern, W.Q, 0, 500, seed=21, export_samples=True)
+    for j in range(0, 1000, 37):
+        ref = O.rs_kde(od, "gaussian", 2.0, W.Q[j], 500, IndexReplay(21, j, od.n))
+        assert vals[j] == pytest.approx(ref, rel=1e-12)
+        np.testing.assert_array_equal(smp[j], IndexReplay(21, j, od.n).integers(0, od.n, size=500))
+    sampler = g.PhiloxSampler(21)
+    for j in range(5):
+        e = g.rs_kde(ds, kern, W.Q[j], 500, sampler)
+        assert e.value == pytest.approx(vals[j], rel=1e-14) and e.kernel_evals == 500 and e.samples_used == 500

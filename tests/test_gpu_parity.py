@@ -436,3 +436,99 @@ def test_fit_bandwidth_hits_target_median():
     vals = O.naive_kde(O.Data(X), "gaussian", h, P)
     med = float(np.sort(vals)[(len(vals) - 1) // 2])
     assert abs(med - 1e-2) <= 0.0101 * 1e-2
+
+
+class _BlackBoxExact(g.AnnIndex):
+    """A user index that is NOT recognised as the GPU brute force (black-box path)."""
+
+    def __init__(self, ds):
+        self.ds = ds
+
+    def query(self, query, k):
+        return g.brute_force_knn(self.ds, query, k)
+
+
+@pytest.mark.parametrize("rng", [11, "philox"])
+def test_deann_batch_black_box_index_uses_one_stream(rng):
+    """a black-box index with an int seed must not restart the Philox stream per
+    query; the per-query loop equals the fused brute-force batch value for value."""
+    X = np.random.default_rng(41).normal(size=(300, 5)).astype(np.float32)
+    Q = np.random.default_rng(42).normal(size=(6, 5))
+    ds = g.Dataset.from_array(X)
+    spec = g.KernelSpec("gaussian", 1.3)
+    mk = (lambda: 11) if rng == 11 else (lambda: g.PhiloxSampler(11))
+    fused = g.deann_batch(ds, spec, g.BruteForceIndex(ds), Q, 7, 40, rng=mk())
+    loop = g.deann_batch(ds, spec, _BlackBoxExact(ds), Q, 7, 40, rng=mk())
+    a = np.array([e.value for e in fused])
+    b = np.array([e.value for e in loop])
+    assert np.allclose(a, b, rtol=1e-12, atol=0)
+    assert len(set(np.round(b, 12))) == len(b)  # distinct queries, distinct streams
+
+
+def _oracle_knn_block(od, Q, k, step=200):
+    """O.brute_force_knn for many queries (the reference's batch_sqdist + _smallest_k per row)."""
+    out_i = np.empty((len(Q), k), dtype=np.int64)
+    ids = np.arange(od.n, dtype=np.int64)
+    for lo in range(0, len(Q), step):
+        D = O.batch_sqdist(Q[lo:lo + step], od.x64, od.sq_norms)
+        for r in range(D.shape[0]):
+            out_i[lo + r] = O.smallest_k(D[r], ids, k)[0]
+    return out_i
+
+
+@pytest.fixture(scope="module")
+def clustered_150k():
+    rng = np.random.default_rng(77)
+    centers = rng.normal(scale=6.0, size=(300, 32))
+    lab = rng.integers(0, 300, size=150_000)
+    X = (centers[lab] + rng.normal(size=(150_000, 32))).astype(np.float32)
+    qlab = rng.integers(0, 300, size=2000)
+    Q = centers[qlab] + rng.normal(size=(2000, 32))
+    Q[:20] = X[rng.integers(0, len(X), 20)]            # on-point queries (distance-0 neighbour)
+    Q[20:40] = rng.normal(scale=40.0, size=(20, 32))    # far from every cluster
+    return X, Q, g.Dataset.from_array(X), O.Data(X)
+
+
+def test_pruned_knn_many_queries_exact(clustered_150k, monkeypatch):
+    """the pruned FILTER path (>= 512 tiles) on 2,000 queries spread over many balls,
+    compared query by query with the reference's brute force; then again split into 4 batches
+    (DK_KNN_MAX_BATCH test hook: multi-batch qperm scatter and per-batch unit plans) and with
+    the bitonic tau path (DK_TAU_SORT) — all identical, indices and distances."""
+    X, Q, ds, od = clustered_150k
+    k = 50
+    idx, d2 = g.knn_batch(ds, Q, k)
+    want = _oracle_knn_block(od, Q, k)
+    np.testing.assert_array_equal(idx, want)
+    monkeypatch.setenv("DK_KNN_MAX_BATCH", "512")
+    idx2, d22 = g.knn_batch(ds, Q, k)
+    monkeypatch.delenv("DK_KNN_MAX_BATCH")
+    monkeypatch.setenv("DK_TAU_SORT", "1")
+    idx3, d23 = g.knn_batch(ds, Q, k)
+    monkeypatch.delenv("DK_TAU_SORT")
+    for a, b in ((idx2, d22), (idx3, d23)):
+        np.testing.assert_array_equal(a, idx)
+        np.testing.assert_array_equal(b, d2)
+
+
+def test_merge_topk_matches_single_shard(clustered_150k):
+    """dk_merge_topk (warp per query) of 3 row shards' exact top-k equals the whole dataset's."""
+    import torch
+
+    X, Q, ds, od = clustered_150k
+    k = 40
+    Qs = Q[:300]
+    full_i, full_d = g.knn_batch(ds, Qs, k)
+    cuts = [0, 41_000, 97_777, len(X)]
+    parts_i, parts_d = [], []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sh = g.Dataset.from_array(X[a:b], global_offset=a, global_n=len(X))
+        i, d = g.knn_batch(sh, Qs, k)
+        parts_i.append(i)
+        parts_d.append(d)
+    from paper_2107_02736_b200.sharded import GpuShardEngine
+
+    eng = GpuShardEngine(None, global_offset=0, global_n=len(X), dataset=ds)
+    mi, md = eng.merge_topk(torch.as_tensor(np.stack(parts_i), device="cuda"),
+                            torch.as_tensor(np.stack(parts_d), device="cuda"), k)
+    np.testing.assert_array_equal(mi.cpu().numpy(), full_i)
+    np.testing.assert_array_equal(md.cpu().numpy(), full_d)
