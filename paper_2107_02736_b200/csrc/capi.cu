@@ -357,6 +357,18 @@ bool ensure_knn_clusters(dk_dataset* h, const Encoding& e, cudaStream_t s) {
   std::unique_ptr<KnnClusters> kc(new KnnClusters());
   try {
     build_knn_clusters(h, knn_cluster_count(h), 3, *kc, s);
+    {  // nearest neighbour balls of each ball (the threshold sweep's lists)
+      double* dcc = nullptr;
+      int32_t* tmp = nullptr;
+      DK_CUDA(cudaMalloc(&dcc, size_t(kc->C) * kc->C * sizeof(double)));
+      DK_CUDA(cudaMalloc(&tmp, size_t(kc->C) * sizeof(int32_t)));
+      DK_CUDA(cudaMalloc(&kc->nbr, size_t(kc->C) * kBallNbrs * sizeof(int32_t)));
+      launch_query_cluster_dist(kc->cent, kc->C, h->d, kc->cent, kc->C, dcc, tmp, s);
+      launch_ball_neighbors(dcc, kc->C, kc->nbr, s);
+      DK_CUDA(cudaStreamSynchronize(s));
+      cudaFree(dcc);
+      cudaFree(tmp);
+    }
     Encoding& se = kc->enc;
     se.Kp = e.Kp;
     se.d = e.d;
@@ -387,12 +399,17 @@ bool ensure_knn_clusters(dk_dataset* h, const Encoding& e, cudaStream_t s) {
   return true;
 }
 
+constexpr int32_t kHomeTiles = 768;  // threshold sweep: at most this many tiles of the block's nearest balls
+constexpr int32_t kListSegs = 8;     // listed threshold sweep: 32-column segments per tile
+
 // Device workspace of one k-NN batch (knn_device / knn_ws_bytes share this layout).
 struct KnnLayout {
   size_t flags, A, qn, scal, tmin, tau, cnt, cand, lists, ctr;
   // pruned path
   size_t dq, near, near_s, iota, qperm, sort_tmp, qp, tidx, td2, tlist, tcnt, bits, tcnt_t, tstart, ustart, blist,
-      ulist;
+      ulist, hlist, hcnt;
+  int32_t hS = 1, hlmax = 0;  // threshold sweep: stride of the strided tiles, list length per block
+  int32_t hneed = 0, hmax = 0;  // near tiles wanted / allowed per block
   size_t sort_tmp_bytes = 0, ulist_ints = 0;
   size_t end = 0;
 };
@@ -406,7 +423,14 @@ KnnLayout knn_layout(const dk_dataset* h, const KnnPlan& kp, int32_t k, int32_t 
   L.A = pl.add<__half>(size_t(bpad) * Kp);
   L.qn = pl.add<float>(bpad);
   L.scal = pl.add<float>(4);
-  L.tmin = pl.add<float>(size_t(std::max(kp.nseg, 1)) * bpad);
+  if (prune) {  // threshold sweep over per-block lists: every hS-th tile + the nearest balls' tiles
+    const int32_t ntiles = int32_t(h->n_pad / kBN);
+    L.hS = std::max<int32_t>(1, ntiles / ((k + kListSegs - 1) / kListSegs + 16));  // >= k strided segments
+    L.hneed = std::max<int32_t>(16, 2 * ((k + kListSegs - 1) / kListSegs));  // rows around a ball: >= 2k segments
+    L.hmax = std::max(kHomeTiles, L.hneed);
+    L.hlmax = (ntiles + L.hS - 1) / L.hS + L.hmax;
+  }
+  L.tmin = pl.add<float>(size_t(std::max({kp.nseg, 1, L.hlmax * kListSegs})) * bpad);
   L.tau = pl.add<float>(bpad);
   L.cnt = pl.add<uint32_t>(bpad);
   L.cand = pl.add<unsigned long long>(size_t(kp.cap) * bpad);
@@ -432,9 +456,11 @@ KnnLayout knn_layout(const dk_dataset* h, const KnnPlan& kp, int32_t k, int32_t 
     L.tstart = pl.add<int32_t>(std::max(ntiles, nqb));
     L.ustart = pl.add<int32_t>(std::max(ntiles, nqb));
     L.blist = L.tlist;
-    // units: tile-major <= ntiles + pairs / 4, block-major <= nqb + pairs / 8
-    L.ulist_ints = size_t(3) * (size_t(std::max(ntiles, nqb)) + size_t(nqb) * ntiles / 4 + 1);
+    // units: tile-major <= ntiles + pairs / 4, block-major <= nqb + pairs / 8 (FILTER and threshold lists)
+    L.ulist_ints = size_t(3) * (size_t(std::max(ntiles, nqb)) + size_t(nqb) * std::max(ntiles, L.hlmax) / 4 + 1);
     L.ulist = pl.add<int32_t>(L.ulist_ints);
+    L.hlist = pl.add<int32_t>(size_t(nqb) * L.hlmax);
+    L.hcnt = pl.add<int32_t>(nqb);
   }
   L.end = pl.off;
   return L;
@@ -462,9 +488,18 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
   const KnnLayout L = knn_layout(h, kp, k, e.Kp, prunable, ws_off_base);
   const int32_t bpad = kp.batch;
   const int32_t ntiles = int32_t(h->n_pad / kBN);
-  const bool tmajor = prune && tile_major_fits(e.Kp);
+  static const bool tmajor_off = [] {  // A/B switch: block-major pruned FILTER
+    const char* v = std::getenv("DK_KNN_TMAJOR");
+    return v != nullptr && std::atoi(v) == 0;
+  }();
+  const bool tmajor = prune && !tmajor_off && tile_major_fits(e.Kp);
   const float inf = std::numeric_limits<float>::infinity();
   int32_t* ctr = at<int32_t>(h->ws, L.ctr);
+  // threshold sweep over per-block lists of near tiles (DK_KNN_HOME=1) instead of every
+  // stride-th tile: tighter on low-dimensional balls (c3), looser in high dimension (c5,
+  // where 32-row segment minima of a sub-ball sit far above the k-th distance) — off by default
+  const char* home_env = std::getenv("DK_KNN_HOME");  // read per call (tests toggle it)
+  const bool home_tau = home_env != nullptr && std::atoi(home_env) != 0;
   for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
     const int64_t bn = std::min<int64_t>(bpad, nq - b0);
     const int32_t bn_pad = int32_t(query_pad(bn));
@@ -493,6 +528,35 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     unsigned long long* cand = at<unsigned long long>(h->ws, L.cand);
     if (kp.tau_inf) {
       launch_fill_float(tau, bn, inf, s);
+    } else if (prune && home_tau) {
+      // threshold from the block's own neighbourhood: 32-column segment minima over every hS-th
+      // tile and the tiles of the balls nearest to the block's queries (tens to hundreds of tiles
+      // per block instead of a quarter of the dataset); tau_q = k-th smallest + 2 eps_q as before
+      int32_t* hl = at<int32_t>(h->ws, L.hlist);
+      int32_t* hc = at<int32_t>(h->ws, L.hcnt);
+      int32_t* hplan = ctr + 8;  // [0] units, [1] listed (block, tile) pairs, [2] U
+      launch_home_tile_lists(at<int32_t>(h->ws, L.near_s), h->kc->nbr, bn, nqb, h->kc->off, ntiles, L.hS,
+                             int64_t(L.hneed) * kBN, L.hmax, L.hlmax, hl, hc, s);
+      launch_block_units(hc, nqb, L.hlmax, h->num_sms, at<int32_t>(h->ws, L.tstart), at<int32_t>(h->ws, L.ustart),
+                         hplan, at<int32_t>(h->ws, L.ulist), s);
+      float* tmin = at<float>(h->ws, L.tmin);
+      const int32_t nseg = L.hlmax * kListSegs;
+      launch_fill_float(tmin, int64_t(nseg) * bn_pad, inf, s);
+      SweepArgs a{};
+      a.mode = MODE_TILEMIN;
+      a.qop = &q;
+      a.enc = &h->kc->enc;
+      a.n = h->n;
+      a.n_pad = h->n_pad;
+      a.tile_stride = 1;
+      a.seg_tiles = 0;
+      a.tmin = tmin;
+      a.ulist = at<int32_t>(h->ws, L.ulist);
+      a.tlist = hl;
+      a.nunits_dev = hplan;
+      a.list_stride = L.hlmax;
+      launch_sweep(a, h->num_sms, s);
+      launch_tau_from_tmin(tmin, nseg, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau, s);
     } else {
       float* tmin = at<float>(h->ws, L.tmin);
       launch_fill_float(tmin, int64_t(kp.nseg) * bn_pad, inf, s);

@@ -112,12 +112,15 @@ struct Encoding {
 // operand re-encoded in that order (same scale and centring as the k-NN encoding, so
 // the query operand is shared), and per-cluster balls (centroid, radius) that bound
 // the distance from a query to every row of a tile from below.
+constexpr int32_t kBallNbrs = 16;
 struct KnnClusters {
   int32_t C = 0;
   double* cent = nullptr;    // [C][d] centroids (fp64)
   double* rad = nullptr;     // [C] max |x - cent| over the members, inflated by 1e-12 relative
   int64_t* perm = nullptr;   // [n] sorted position -> dataset row
   float* xs = nullptr;       // [n][d] rows in sorted order
+  int64_t* off = nullptr;    // [C + 1] first sorted position of each ball
+  int32_t* nbr = nullptr;    // [C][kBallNbrs] nearest other balls by centroid distance (threshold-sweep lists)
   int32_t* tclo = nullptr;   // [ntiles] first / last cluster of each 256-row tile of the sorted rows
   int32_t* tchi = nullptr;
   Encoding enc;              // sweep operand of xs (mode of the k-NN encoding)
@@ -235,6 +238,7 @@ struct SweepArgs {
   const int32_t* tlist;
   int32_t nunits_list;
   const int32_t* nunits_dev;  // unit count in device memory (built on the device); overrides nunits_list
+  int32_t list_stride;        // TILEMIN over tile lists: entries per query block in tlist (segment = list position)
   // tile-major FILTER: unit u = (dataset tile ulist[3u], query blocks blist[ulist[3u+1] .. ulist[3u+2]))
   int32_t tmajor;
   const int32_t* blist;
@@ -282,8 +286,17 @@ void launch_sort_queries_by_ball(const int32_t* nearest, int64_t nq, int32_t C, 
 void launch_tile_units(const uint32_t* bits, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* tcnt,
                        int32_t* tstart, int32_t* ustart, int32_t* scal, int32_t* blist, int32_t* ulist,
                        cudaStream_t s);
-void launch_block_units(const int32_t* tcount, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* bstart,
+void launch_block_units(const int32_t* tcount, int32_t nqb, int32_t list_stride, int32_t slots, int32_t* bstart,
                         int32_t* ustart, int32_t* scal, int32_t* ulist, cudaStream_t s);
+// per block of 128 ball-sorted queries: the threshold sweep's tiles — every S-th tile of the
+// sorted rows (>= k/4 disjoint 64-column segments for every block) plus up to hmax tiles of
+// the balls nearest to the block's queries, each extended by its nearest neighbour balls until
+// rows_need rows surround it (tight bound); lists [nqb][lmax], lcnt [nqb]
+void launch_home_tile_lists(const int32_t* near_sorted, const int32_t* ball_nbr, int64_t bn, int32_t nqb,
+                            const int64_t* ball_off, int32_t ntiles, int32_t S, int64_t rows_need, int32_t hmax,
+                            int32_t lmax, int32_t* lists, int32_t* lcnt, cudaStream_t s);
+// nbr[c][0..kBallNbrs) = the nearest other balls of ball c ((distance, id) order) from dq [C][C]
+void launch_ball_neighbors(const double* dq, int32_t C, int32_t* nbr, cudaStream_t s);
 void launch_gather_rows_f64(const double* Q, const int32_t* perm, int64_t nq, int32_t d, double* out, cudaStream_t s);
 void launch_scatter_knn(const int64_t* idx_p, const double* d2_p, const int32_t* perm, int64_t nq, int32_t k,
                         int64_t* idx_out, double* d2_out, cudaStream_t s);

@@ -1399,11 +1399,13 @@ void build_knn_clusters(dk_dataset* h, int32_t C, int32_t iters, KnnClusters& kc
   kc.cent = v->cent; v->cent = nullptr;   // ownership moves to kc
   kc.perm = v->rows; v->rows = nullptr;
   kc.xs = v->xs; v->xs = nullptr;
+  kc.off = v->offsets; v->offsets = nullptr;
 }
 
 void free_knn_clusters(KnnClusters& kc) {
   for (void* p : {static_cast<void*>(kc.cent), static_cast<void*>(kc.rad), static_cast<void*>(kc.perm),
-                  static_cast<void*>(kc.xs), static_cast<void*>(kc.tclo), static_cast<void*>(kc.tchi)})
+                  static_cast<void*>(kc.xs), static_cast<void*>(kc.tclo), static_cast<void*>(kc.tchi),
+                  static_cast<void*>(kc.off), static_cast<void*>(kc.nbr)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(kc.enc.B), static_cast<void*>(kc.enc.xn), static_cast<void*>(kc.enc.sx)})
     if (p) cudaFree(p);

@@ -171,18 +171,6 @@ __global__ void __launch_bounds__(256) tau_radix_kernel(const float* __restrict_
   }
 }
 
-__device__ __forceinline__ double exact_d2_warp(const float* __restrict__ x, const double* __restrict__ q, int d,
-                                                int lane) {
-  double s = 0.0;
-  for (int k = lane; k < d; k += 32) {
-    const double t = double(x[k]) - q[k];
-    s = fma(t, t, s);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  return s;
-}
-
 // exact fp64 direct-difference d2 by a group of G lanes (float4 row loads when rows are
 // whole float4s), reduced within the group
 template <int G>
@@ -225,7 +213,7 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
     int32_t k, const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt, int32_t cap,
     const float* __restrict__ qn, float xn_max, float eps_rel, int64_t* __restrict__ idx_out,
     double* __restrict__ d2_out, int32_t* __restrict__ slow_list, int32_t* __restrict__ slow_cnt,
-    int32_t* __restrict__ ovf_list, int32_t* __restrict__ ovf_cnt, const int64_t* __restrict__ perm) {
+    int32_t* __restrict__ ovf_list, int32_t* __restrict__ ovf_cnt, const int64_t* __restrict__ perm, int32_t scap) {
   // candidates are row positions of X; perm (optional) maps a position to the reported row id,
   // which is also the tie-break key (pruned k-NN: X holds the cluster-sorted rows)
   extern __shared__ unsigned long long sraw[];
@@ -237,11 +225,9 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
     return;
   }
   const int c = int(craw);
-  const int Kp = max(32, pow2_ceil(k));
-  const int W = Kp;
   const unsigned long long* keys = cand + size_t(q) * cap;
-  Key128* top = reinterpret_cast<Key128*>(sraw);         // [Kp + W]
-  double* qv = reinterpret_cast<double*>(top + Kp + W);  // the query in shared memory
+  Key128* top = reinterpret_cast<Key128*>(sraw);         // [scap]
+  double* qv = reinterpret_cast<double*>(top + scap);    // the query in shared memory
   uint32_t* hist = reinterpret_cast<uint32_t*>(qv + d);  // [kSelHist]
   for (int j = threadIdx.x; j < d; j += blockDim.x) qv[j] = Q[size_t(q) * d + j];
   const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
@@ -308,7 +294,6 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
   if (lane == 0) atomicMax(&s_tmax, tm);
   __syncthreads();
   const double thr = double(__uint_as_float(s_tmax)) + 2.0 * eps;
-  const int scap = Kp + W;
   for (int i = threadIdx.x; i < c; i += blockDim.x) {
     const unsigned long long v = __ldg(keys + i);
     if (double(__uint_as_float(uint32_t(v >> 32))) <= thr) {
@@ -427,15 +412,19 @@ __global__ void exact_knn_kernel(const float* __restrict__ X, int64_t n, int64_t
     __syncthreads();
     for (int i = threadIdx.x; i < Kp; i += blockDim.x) buf[i] = Key128{~0ull, ~0ull};
     for (int64_t pos = 0; pos < n; pos += chunk) {
-      for (int i = warp; i < chunk; i += nwarps) {
-        Key128 key{~0ull, ~0ull};
+      // 8 lanes per row with the selection's summation order (exact_d2_group<8>), so a query
+      // gets bit-identical distances whichever path served it
+      constexpr int G = 8;
+      const int grp = lane / G, gl = lane % G;
+      for (int i0 = warp * (32 / G); i0 < chunk; i0 += nwarps * (32 / G)) {
+        const int i = i0 + grp;
         const int64_t col = pos + i;
-        if (col < n) {
-          const double dd = exact_d2_warp(X + size_t(col) * d, qv, d, lane);
-          key.hi = static_cast<unsigned long long>(__double_as_longlong(dd));
-          key.lo = static_cast<unsigned long long>(col);
-        }
-        if (lane == 0) buf[Kp + i] = key;
+        const bool ok = i < chunk && col < n;
+        const double dd = exact_d2_group<G>(X + size_t(ok ? col : 0) * d, qv, d, gl);
+        if (gl == 0 && i < chunk)
+          buf[Kp + i] = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)),
+                                    static_cast<unsigned long long>(col)}
+                           : Key128{~0ull, ~0ull};
       }
       bitonic_k128(buf, B);
     }
@@ -727,8 +716,9 @@ __global__ void tile_units_fill_kernel(const uint32_t* __restrict__ bits, int32_
   }
 }
 
-// block-major units (FILTER operand too wide to keep a tile resident): unit = (query block b,
-// positions [i0, i1) of its tile list tlist[b][...], flat index b * ntiles + i)
+// block-major units (per-block tile lists: the threshold sweep, and the FILTER when its operand is
+// too wide to keep a tile resident): unit = (query block b, positions [i0, i1) of its list,
+// flat index b * ntiles + i, ntiles = the list stride)
 __global__ void block_units_fill_kernel(int32_t nqb, int32_t ntiles, const int32_t* __restrict__ cnt,
                                         const int32_t* __restrict__ ustart, const int32_t* __restrict__ scal,
                                         int32_t* __restrict__ ulist) {
@@ -740,6 +730,82 @@ __global__ void block_units_fill_kernel(int32_t nqb, int32_t ntiles, const int32
     ulist[3 * u] = b;
     ulist[3 * u + 1] = int32_t(int64_t(b) * ntiles + i);
     ulist[3 * u + 2] = int32_t(int64_t(b) * ntiles + min(c, i + U));
+  }
+}
+
+// Threshold-sweep tile list of one block of 128 ball-sorted queries (thread 0 builds it; a
+// shared bitmap dedupes tiles): every S-th tile, then for each distinct nearest ball of the
+// block's queries (in sorted order) its tiles and those of its nearest neighbour balls until
+// rows_need rows surround it, up to hmax such tiles.  Any set of disjoint segments bounds the
+// k-th distance (the strided tiles alone give >= k of them); the near ones make it tight.
+__global__ void __launch_bounds__(128) home_tile_lists_kernel(
+    const int32_t* __restrict__ near_s, const int32_t* __restrict__ nbr, int64_t bn, const int64_t* __restrict__ off,
+    int32_t ntiles, int32_t S, int64_t rows_need, int32_t hmax, int32_t lmax, int32_t* __restrict__ lists,
+    int32_t* __restrict__ lcnt) {
+  extern __shared__ uint32_t mark[];
+  const int qb = blockIdx.x;
+  const int nwords = (ntiles + 31) >> 5;
+  for (int w = threadIdx.x; w < nwords; w += blockDim.x) mark[w] = 0u;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int32_t* L = lists + int64_t(qb) * lmax;
+  int c = 0, home = 0;
+  for (int t = 0; t < ntiles && c < lmax; t += S) {
+    L[c++] = t;
+    mark[t >> 5] |= 1u << (t & 31);
+  }
+  auto add_ball = [&](int b) -> int64_t {
+    const int64_t lo = off[b], hi = off[b + 1];
+    if (hi <= lo) return 0;
+    for (int t = int(lo / 256); t <= int((hi - 1) / 256) && home < hmax && c < lmax; ++t) {
+      if ((mark[t >> 5] >> (t & 31)) & 1u) continue;
+      mark[t >> 5] |= 1u << (t & 31);
+      L[c++] = t;
+      ++home;
+    }
+    return hi - lo;
+  };
+  int prev = -1;
+  const int64_t r0 = int64_t(qb) * 128, r1 = min(bn, r0 + 128);
+  for (int64_t r = r0; r < r1 && home < hmax; ++r) {
+    const int b = near_s[r];
+    if (b == prev) continue;
+    prev = b;
+    int64_t got = add_ball(b);
+    for (int j = 0; j < kBallNbrs && got < rows_need && home < hmax; ++j) {
+      const int nb = nbr[b * kBallNbrs + j];
+      if (nb >= 0) got += add_ball(nb);
+    }
+  }
+  lcnt[qb] = c;
+}
+
+// nearest other balls of each ball: one warp per ball, rounds of "smallest (d, id) above the last"
+__global__ void ball_neighbors_kernel(const double* __restrict__ dq, int32_t C, int32_t* __restrict__ nbr) {
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= C) return;
+  const double* row = dq + int64_t(b) * C;
+  double last_d = -1.0;
+  int last_i = -1;
+  for (int j = 0; j < kBallNbrs; ++j) {
+    double bd = INFINITY;
+    int bi = -1;
+    for (int c = lane; c < C; c += 32) {
+      if (c == b) continue;
+      const double v = row[c];
+      const bool above = v > last_d || (v == last_d && c > last_i);
+      if (above && (bi < 0 || v < bd || (v == bd && c < bi))) { bd = v; bi = c; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi >= 0 && (bi < 0 || od < bd || (od == bd && oi < bi))) { bd = od; bi = oi; }
+    }
+    if (lane == 0) nbr[b * kBallNbrs + j] = bi;
+    last_d = bd;
+    last_i = bi;
   }
 }
 
@@ -823,6 +889,21 @@ void launch_tile_units(const uint32_t* bits, int32_t nqb, int32_t ntiles, int32_
   DK_CHECK_LAUNCH();
 }
 
+void launch_home_tile_lists(const int32_t* near_sorted, const int32_t* ball_nbr, int64_t bn, int32_t nqb,
+                            const int64_t* ball_off, int32_t ntiles, int32_t S, int64_t rows_need, int32_t hmax,
+                            int32_t lmax, int32_t* lists, int32_t* lcnt, cudaStream_t s) {
+  const size_t smem = size_t((ntiles + 31) / 32) * 4;
+  set_dynamic_smem(home_tile_lists_kernel, smem);
+  home_tile_lists_kernel<<<unsigned(nqb), 128, smem, s>>>(near_sorted, ball_nbr, bn, ball_off, ntiles, S, rows_need,
+                                                          hmax, lmax, lists, lcnt);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_ball_neighbors(const double* dq, int32_t C, int32_t* nbr, cudaStream_t s) {
+  ball_neighbors_kernel<<<unsigned((int64_t(C) * 32 + 255) / 256), 256, 0, s>>>(dq, C, nbr);
+  DK_CHECK_LAUNCH();
+}
+
 void launch_block_units(const int32_t* tcount, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* bstart,
                         int32_t* ustart, int32_t* scal, int32_t* ulist, cudaStream_t s) {
   // units of ~equal length (>= 8 tiles) so the persistent CTAs finish together
@@ -879,18 +960,22 @@ void launch_select(const float* X, int64_t global_offset, int32_t d, const doubl
   int32_t* slow_list = lists;
   int32_t* ovf_list = lists + nq;
   const int Kp = std::max(32, pow2_ceil(k));
-  const size_t fast_smem = size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double) + kSelHist * sizeof(uint32_t);
+  // keys re-ranked by the fast path: every key within 2 eps of the k-th approx key, up to
+  // max(2 pow2(k), 2048) (single-pass fp16 sweeps at c5 put ~1,000 keys in that window; 32 KB
+  // of shared memory keeps 6 CTAs per SM)
+  const int scap = std::max(2 * Kp, 2048);
+  const size_t fast_smem = size_t(scap) * sizeof(Key128) + size_t(d) * sizeof(double) + kSelHist * sizeof(uint32_t);
   set_dynamic_smem(select_fast_kernel, fast_smem);
   if (fast_smem > 232448) throw Error{DK_EINVAL, "k too large for the k-NN selection buffer"};
   select_fast_kernel<<<unsigned(nq), 256, fast_smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,
                                                           xn_max, eps_rel, idx_out, d2_out, slow_list, counts,
-                                                          ovf_list, counts + 1, perm);
+                                                          ovf_list, counts + 1, perm, scap);
   DK_CHECK_LAUNCH();
   const int B = std::max(2, pow2_ceil(cap));
   const size_t slow_smem = size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double);
   if (slow_smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
   set_dynamic_smem(select_slow_kernel, slow_smem);
-  select_slow_kernel<<<unsigned(std::max(1, num_sms)), 256, slow_smem, s>>>(
+  select_slow_kernel<<<unsigned(std::max(1, 2 * num_sms)), 256, slow_smem, s>>>(
       X, global_offset, d, Q, k, cand, cand_cnt, cap, qn, xn_max, eps_rel, B, idx_out, d2_out, slow_list, counts, perm);
   DK_CHECK_LAUNCH();
 }

@@ -225,6 +225,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.tlist = a.tlist;
   p.nunits_list = a.nunits_list;
   p.nunits_dev = a.nunits_dev;
+  p.list_stride = a.list_stride;
   p.tmajor = tmajor ? 1 : 0;
   p.blist = a.blist;
   p.guard = a.guard;
@@ -233,7 +234,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   // a device-side unit count is unknown here: one CTA per SM, surplus CTAs find no unit
   const int nunits = a.ulist != nullptr ? (a.nunits_dev != nullptr ? nslots : a.nunits_list) : ngroups * pl.ncc;
   if (nunits <= 0) return;
-  if (a.ulist != nullptr && (pr || a.mode != MODE_FILTER)) throw Error{DK_EINVAL, "internal: tile lists are FILTER-only"};
+  if (a.ulist != nullptr && (pr || (a.mode != MODE_FILTER && a.mode != MODE_TILEMIN)))
+    throw Error{DK_EINVAL, "internal: tile lists are k-NN sweeps only"};
+  if (a.ulist != nullptr && a.mode == MODE_TILEMIN && a.seg_tiles != 0)
+    throw Error{DK_EINVAL, "internal: listed TILEMIN sweeps use one segment per 64-column group"};
   const int grid = std::min(nunits, nslots) * (pr ? 2 : 1);
   const CUtensorMap& tb = pr ? e.tmap_half : e.tmap;
   switch (a.mode) {

@@ -99,6 +99,7 @@ struct TileParams {
   int32_t tmajor;
   const int32_t* blist;
   const int32_t* nunits_dev;
+  int32_t list_stride;     // TILEMIN over per-block tile lists: segment = (list position) x 64-column group
   const float* xn;         // [n_pad] |x|^2 (encoding-consistent)
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
@@ -234,13 +235,15 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
         for (int j = 0; j < 32; ++j) d2v[j] = j < lim ? d2v[j] : pad;
       }
       if constexpr (MODE == MODE_TILEMIN) {
-        float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[2], m3 = d2v[3];
+        // minima of the two 16-column halves (listed sweeps keep them as separate segments)
+        float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[16], m3 = d2v[17];
 #pragma unroll
-        for (int j = 4; j < 32; j += 4) {
+        for (int j = 2; j < 16; j += 2) {
           m0 = fminf(m0, d2v[j]); m1 = fminf(m1, d2v[j + 1]);
-          m2_ = fminf(m2_, d2v[j + 2]); m3 = fminf(m3, d2v[j + 3]);
+          m2_ = fminf(m2_, d2v[16 + j]); m3 = fminf(m3, d2v[17 + j]);
         }
-        mn = fminf(mn, fminf(fminf(m0, m1), fminf(m2_, m3)));
+        acc0 = make_float2(fminf(m0, m1), fminf(m2_, m3));
+        mn = fminf(mn, fminf(acc0.x, acc0.y));
       } else {
         // candidates are rare (~1e-4 of the pairs): a min tree (4 independent chains)
         // rejects the whole chunk before any per-column mask is built
@@ -751,16 +754,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t cbase = int64_t(p.tlist != nullptr ? p.tlist[t] : t * p.tile_stride) * kBN + cg * 64;
         const float* xsm = smemX + xs * kBN + cg * 64;
         const bool full = cbase + 64 <= p.n;
-        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f), b0 = a0;
         epi_chunk<MODE>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf, lrow);
-        epi_chunk<MODE>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n, a0, a1, mn, p, row, scnt, sbuf,
-                        lrow);
+        // TILEMIN returns the chunk's two 16-column minima in its first accumulator
+        epi_chunk<MODE>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n, MODE == MODE_TILEMIN ? b0 : a0, a1,
+                        mn, p, row, scnt, sbuf, lrow);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         if constexpr (is_kde(MODE)) {
           usum += double((a0.x + a0.y) + (a1.x + a1.y));
         } else if constexpr (MODE == MODE_TILEMIN) {
-          if (p.seg_tiles == 0) {
+          if (p.tlist != nullptr) {
+            // listed threshold sweep: 8 segments of 32 columns per tile (segment = list position x 8 + 32-column
+            // group), fine enough that the tiles near a query hold k segments
+            float* tm = p.tmin + (size_t(t - qb * p.list_stride) * 8 + cg * 2) * p.nq_pad + row;
+            tm[0] = fmaxf(fminf(a0.x, a0.y), 0.f);
+            tm[size_t(p.nq_pad)] = fmaxf(fminf(b0.x, b0.y), 0.f);
+            mn = __int_as_float(0x7f800000);
+          } else if (p.seg_tiles == 0) {
             p.tmin[(size_t(t) * kColGroups + cg) * p.nq_pad + row] = fmaxf(mn, 0.f);
             mn = __int_as_float(0x7f800000);
           }

@@ -492,8 +492,9 @@ def clustered_150k():
 def test_pruned_knn_many_queries_exact(clustered_150k, monkeypatch):
     """the pruned FILTER path (>= 512 tiles) on 2,000 queries spread over many balls,
     compared query by query with the reference's brute force; then again split into 4 batches
-    (DK_KNN_MAX_BATCH test hook: multi-batch qperm scatter and per-batch unit plans) and with
-    the bitonic tau path (DK_TAU_SORT) — all identical, indices and distances."""
+    (DK_KNN_MAX_BATCH test hook: multi-batch qperm scatter and per-batch unit plans), with the
+    bitonic tau path (DK_TAU_SORT) and with the near-tile threshold lists (DK_KNN_HOME) — all
+    identical, indices and distances."""
     X, Q, ds, od = clustered_150k
     k = 50
     idx, d2 = g.knn_batch(ds, Q, k)
@@ -505,7 +506,10 @@ def test_pruned_knn_many_queries_exact(clustered_150k, monkeypatch):
     monkeypatch.setenv("DK_TAU_SORT", "1")
     idx3, d23 = g.knn_batch(ds, Q, k)
     monkeypatch.delenv("DK_TAU_SORT")
-    for a, b in ((idx2, d22), (idx3, d23)):
+    monkeypatch.setenv("DK_KNN_HOME", "1")  # threshold from per-block near-tile lists
+    idx4, d24 = g.knn_batch(ds, Q, k)
+    monkeypatch.delenv("DK_KNN_HOME")
+    for a, b in ((idx2, d22), (idx3, d23), (idx4, d24)):
         np.testing.assert_array_equal(a, idx)
         np.testing.assert_array_equal(b, d2)
 
