@@ -1,20 +1,26 @@
-"""Benchmark: exact KDE queries/s on config 2 (BASELINE.json configs[1]).
+"""Benchmark: KDE queries/s — exact (headline, config 2) and DEANN (configs 3 and 5).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one exact naive-KDE pass (gaussian, h by the median-1e-3 rule) of
-all 10,000 queries over the n = 1,000,000 x 128 integer dataset — the
+Headline step = one exact naive-KDE pass (gaussian, h by the median-1e-3 rule) of all
+10,000 queries over the n = 1,000,000 x 128 integer dataset of config 2 — the
 "single-GPU fused distance-GEMM + exp + row-sum" workload BASELINE.json names.
-N > 1 (torchrun): dataset-sharded mode — each rank fits n/N rows, computes
-per-query partial sums, NCCL all-reduce (fp64 sum) -> strong scaling.
+N > 1 (torchrun, or `--gpus N` which re-launches itself under torchrun): the same
+workload dataset-sharded — each rank fits n/N rows, per-query partial sums, NCCL
+all-reduce (fp64 sum) -> strong scaling.
 
-Rank 0 prints ONE JSON line (contract in the task statement): `value` is
-device-timed with inputs resident in HBM; `e2e` goes through the public
-`naive_kde` API with pinned host queries (H2D + D2H inside the timed region);
-`roofline` reports the fused tile kernel against the tensor-core peak and the
-SFU (ex2) peak; `cpu_baseline` times the NumPy oracle (oracle/) on a bounded
-query sample on this host.  `--impl reference` times the oracle port (the
-reference's own CPU algorithm, all host threads) on the same config.
+Rank 0 prints ONE JSON line.  Besides the contract keys (`value` device-timed with
+inputs in HBM, `e2e` through the public `naive_kde` API with pinned host queries,
+`roofline`, `cpu_baseline`, `clocks`, `gpu_launches`) it carries two first-class
+objects for the rest of BASELINE's metric ("exact & DEANN at n = 1M-8M"):
+  deann  config 3 DEANN (exact k = 100 NN + m = 1,000 Philox samples): device value,
+         e2e through `deann_batch` (pinned host queries, list of Estimates), per-kernel
+         rooflines, clocks, oracle parity of the timed output, CPU baseline.
+  c5     config 5 (n = 8M, 100,000 queries): exact KDE and DEANN (k = 100, m = 2,000);
+         dataset-sharded over the ranks when N > 1 (all-reduce of partial sums,
+         all-gather + merge of per-shard top-k, shared Philox stream).
+`--impl reference` times the oracle port (the reference's own CPU algorithm, all host
+threads) on the headline config.
 """
 
 from __future__ import annotations
@@ -156,29 +162,63 @@ def _dist_env():
     return ws, rank, local
 
 
-def cpu_oracle_rate(X, Q, h, budget_s=12.0, max_q=1024, threads=None):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _timed_cpu(fn, items, budget_s, threads, min_items=1):
+    """Run fn(item) over items until the budget is spent (>= min_items); (rate, done, seconds)."""
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(threads):
+        fn(items[0])  # warm (page-in, BLAS threads)
+        done, t0 = 0, time.perf_counter()
+        for it in items:
+            fn(it)
+            done += 1
+            if done >= min_items and time.perf_counter() - t0 >= budget_s:
+                break
+        el = time.perf_counter() - t0
+    return done / el, done, el
+
+
+def cpu_baseline(name, fn, items, unit_per_item, budget_s, sample_desc):
+    """The oracle port (the reference's algorithm, NumPy/OpenBLAS fp64) on the host cores, all
+    threads and threadpool_limits(1) (the reference harness's timing contract, harness.py:309)."""
+    cores = len(os.sched_getaffinity(0))
+    r_all, n_all, el_all = _timed_cpu(fn, items, budget_s, cores)
+    r_one, n_one, el_one = _timed_cpu(fn, items, budget_s / 2, 1)
+    return {"value": r_all * unit_per_item, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{sample_desc}: {n_all} in {el_all:.1f} s on {cores} threads; {n_one} in {el_one:.1f} s "
+                      f"single-threaded ({name})",
+            "single_thread": {"value": r_one * unit_per_item, "unit": UNIT, "cores": 1},
+            "cpu_model": cpu_model()}
+
+
+def cpu_oracle_rate(X, Q, h, budget_s=12.0, max_q=1024, threads=None, data=None):
     """NumPy oracle (the reference's algorithm) on a bounded query sample: queries/s."""
     from oracle import deann_oracle as O
+    from threadpoolctl import threadpool_limits
 
-    try:
-        from threadpoolctl import threadpool_limits
-    except ImportError:  # pragma: no cover
-        threadpool_limits = None
-    data = O.Data(X)
+    data = data if data is not None else O.Data(X)
     cores = threads or len(os.sched_getaffinity(0))
-    ctx = threadpool_limits(cores) if threadpool_limits else None
-    done, t0 = 0, time.perf_counter()
-    O.naive_kde(data, "gaussian", h, Q[:2])  # warm
-    t0 = time.perf_counter()
-    while done < max_q and (time.perf_counter() - t0) < budget_s:
-        blk = Q[done: done + 16]
-        if len(blk) == 0:
-            break
-        O.naive_kde(data, "gaussian", h, blk)
-        done += len(blk)
-    el = time.perf_counter() - t0
-    if ctx is not None and hasattr(ctx, "unregister"):
-        ctx.unregister()
+    with threadpool_limits(cores):
+        O.naive_kde(data, "gaussian", h, Q[:2])  # warm
+        done, t0 = 0, time.perf_counter()
+        while done < max_q and (time.perf_counter() - t0) < budget_s:
+            blk = Q[done: done + 16]
+            if len(blk) == 0:
+                break
+            O.naive_kde(data, "gaussian", h, blk)
+            done += len(blk)
+        el = time.perf_counter() - t0
     return done / el, cores, done, el, data
 
 
@@ -215,7 +255,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WL["desc"], "bandwidth": h, "sample_queries_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{per_step} random queries of the {len(W.Q):,} per step, full n={W.X.shape[0]:,} rows, "
                                    "oracle/deann_oracle.naive_kde (NumPy/OpenBLAS fp64, all host threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -236,6 +276,79 @@ def _bandwidth_cpu_free(W):
     raise RuntimeError(f"no bandwidth for {W.name} in {_H_CACHE}; run bench.py --fit-bandwidth on a GPU first")
 
 
+class Timer:
+    """CUDA events on the launch stream around K steps, a barrier + synchronize on both sides,
+    max over ranks; clocks sampled during the window."""
+
+    def __init__(self, torch, dist, local):
+        self.torch, self.dist, self.local = torch, dist, local
+
+    def run(self, step, steps, warmup, clocks=None):
+        torch = self.torch
+        for i in range(warmup):
+            step(i)
+        torch.cuda.synchronize()
+        if self.dist:
+            self.dist.barrier()
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for i in range(steps):
+            step(warmup + i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if clocks is not None:
+            clocks.mark(t0, t1)
+        ms = e0.elapsed_time(e1) / steps
+        return self.max_over_ranks(ms)
+
+    def wall(self, step, steps, warmup):
+        """Host wall clock per step (e2e: host buffers, copies inside), max over ranks."""
+        for i in range(warmup):
+            step(i)
+        self.torch.cuda.synchronize()
+        if self.dist:
+            self.dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(steps):
+            step(warmup + i)
+        self.torch.cuda.synchronize()
+        return self.max_over_ranks(1e3 * (time.perf_counter() - t0) / steps)
+
+    def max_over_ranks(self, v):
+        if not self.dist:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t[0])
+
+
+def _kernel_ms(lib, ds):
+    import ctypes
+
+    from paper_2107_02736_b200 import _lib
+
+    kms, kfl, kby = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _lib.check(lib.dk_last_kernel_ms(ds.handle, ctypes.byref(kms), ctypes.byref(kfl), ctypes.byref(kby)))
+    return kms.value, kfl.value, kby.value
+
+
+def _launches(lib, ds):
+    import ctypes
+
+    from paper_2107_02736_b200 import _lib
+
+    cnt = ctypes.c_int64()
+    _lib.check(lib.dk_last_launch_count(ds.handle, ctypes.byref(cnt)))
+    return int(cnt.value)
+
+
+def _sfu_peak(peaks):
+    return 148 * 16 * peaks["sm_max_mhz"] * 1e6
+
+
 def run_ours(args):
     import torch
 
@@ -244,12 +357,15 @@ def run_ours(args):
     from paper_2107_02736_b200 import _lib
 
     ws, rank, local = _dist_env()
+    if args.gpus > 1 and ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    timer = Timer(torch, dist, local)
     WL = WORKLOADS[args.workload]
     W = workloads.make(args.workload)
     n, d = W.X.shape
@@ -268,89 +384,41 @@ def run_ours(args):
     out = torch.empty(nq, dtype=torch.float64, device=f"cuda:{local}")
     lib = _lib.load()
 
-    def step():
+    def step(_i):
         # each shard writes its contribution to the global mean (sum / global n): the all-reduce
         # (sum) of the shards is the KDE
         g.naive_kde_into(ds, spec, Qd, out, stream=stream.cuda_stream)
         if ws > 1:
             dist.all_reduce(out)
 
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
-    import ctypes
-
     with ClockSampler(local) as clocks:  # running from the warm-up on: the timed region is short
-        for _ in range(args.warmup):
-            step()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
+        for i in range(args.warmup):
+            step(i)
         _lib.check(lib.dk_set_profiling(ds.handle, 1))
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        t_w0 = time.perf_counter()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        t_w1 = time.perf_counter()
-        if dist:
-            dist.barrier()
-    clocks.mark(t_w0, t_w1)
-    cnt = ctypes.c_int64()
-    _lib.check(lib.dk_last_launch_count(ds.handle, ctypes.byref(cnt)))
-    launches = int(cnt.value) * args.steps
-    ms = ev0.elapsed_time(ev1) / args.steps
-    kms, kflops, kbytes = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-    _lib.check(lib.dk_last_kernel_ms(ds.handle, ctypes.byref(kms), ctypes.byref(kflops), ctypes.byref(kbytes)))
+        ms = timer.run(step, args.steps, 0, clocks)
+    launches = _launches(lib, ds) * args.steps
+    kmsv = timer.max_over_ranks(_kernel_ms(lib, ds)[0])
     _lib.check(lib.dk_set_profiling(ds.handle, 0))
-    if dist:
-        t = torch.tensor([ms, kms.value], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kmsv = float(t[0]), float(t[1])
-    else:
-        kmsv = kms.value
-    # parity spot-check of the timed output against a small oracle sample (rank 0, N=1)
     # ---- e2e through the public API with pinned host buffers
-    Qpin = torch.from_numpy(W.Q).pin_memory()
-    Qh = Qpin.numpy()
-    def e2e_step():
+    Qh = torch.from_numpy(W.Q).pin_memory().numpy()
+
+    def e2e_step(_i):
         if ws == 1:
             return g.naive_kde(ds, spec, Qh).values
         tmp = torch.empty(nq, dtype=torch.float64, device=f"cuda:{local}")
         g.naive_kde_into(ds, spec, Qh, tmp, stream=stream.cuda_stream)
         dist.all_reduce(tmp)
         return tmp.cpu().numpy()
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        vals = e2e_step()
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
-        return
+
+    e2e_ms = timer.wall(e2e_step, args.steps, max(1, args.warmup))
     peaks = _peaks()
     n_local = hi - lo
     flops = 2.0 * d * nq * n_local
     ex2 = float(nq) * n_local
-    sm_mhz_max = peaks["sm_max_mhz"]
     tc_peak = peaks["bf16_tflops"] * 1e12
-    sfu_peak = 148 * 16 * sm_mhz_max * 1e6
+    sfu_peak = _sfu_peak(peaks)
     t_k = kmsv / 1e3
     t_bound = max(flops / tc_peak, ex2 / sfu_peak)
-    clk = clocks.summary()
     traffic = None
     tpath = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -368,99 +436,259 @@ def run_ours(args):
             "frac": (flops / t_k) / tc_peak, "traffic": traffic, "peak_source": peaks["source"],
             "kernel_ms": kmsv,
             "sfu": {"achieved": ex2 / t_k / 1e12, "peak": sfu_peak / 1e12, "unit": "Tex2/s",
-                    "frac": (ex2 / t_k) / sfu_peak, "peak_note": "148 SMs x 16 ex2/clk x clocks.max.sm (nominal)"},
+                    "frac": (ex2 / t_k) / sfu_peak,
+                    "peak_note": "148 SMs x 16 ex2/clk x clocks.max.sm (nominal; scripts/mufu_probe.py measures it)"},
             "binding": "sfu" if ex2 / sfu_peak >= flops / tc_peak else "tensor",
             "frac_of_binding": t_bound / t_k,
         },
-        "e2e": {"value": nq / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
-                "d2h_bytes_per_step": int(nq * 8)},
+        "e2e": {"value": nq / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
+                "d2h_bytes_per_step": int(nq * 8), "api": "naive_kde(ds, KernelSpec, pinned host queries)"},
         "gpu_launches": launches,
-        "clocks": clk,
+        "clocks": clocks.summary(),
     }
-    if ws == 1 and not args.no_secondary and args.workload == "c2":
-        line["secondary"] = measure_deann_c3(args, local)
     if ws == 1 and not args.no_cpu_baseline:
-        rate, cores, done, el, odata = cpu_oracle_rate(W.X, W.Q, h)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"first {done} of the {nq:,} queries over all n={n:,} rows "
-                                          f"({el:.1f} s), oracle/deann_oracle.naive_kde, NumPy/OpenBLAS fp64"}
-        # parity of the timed device output against the oracle on a query sample
         from oracle import deann_oracle as O
 
+        odata = O.Data(W.X)
+        line["cpu_baseline"] = cpu_baseline(
+            "oracle/deann_oracle.naive_kde", lambda blk: O.naive_kde(odata, "gaussian", h, blk),
+            [W.Q[i:i + 8] for i in range(0, 1024, 8)], 8, 10.0,
+            f"blocks of 8 of the first 1,024 of the {nq:,} queries over all n={n:,} rows")
+        # parity of the timed device output against the oracle on a query sample
         ref = O.naive_kde(odata, "gaussian", h, W.Q[:16])
         got = out[:16].cpu().numpy()
         line["parity_max_rel"] = float(np.max(np.abs(got - ref) / ref))
-    print(json.dumps(line), flush=True)
+        del odata
+    ds.free()
+    del W
+    if ws == 1 and not args.no_secondary:
+        line["deann"] = measure_deann_c3(args, local, timer)
+    if not args.no_c5:
+        c5 = measure_c5(args, ws, rank, local, dist, timer)
+        if rank == 0:
+            line["c5"] = c5
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
-def measure_deann_c3(args, local):
-    """Secondary line: DEANN (exact k=100 NN + m=1000 Philox samples) on config 3, device-resident."""
-    import ctypes
+def _deann_oracle_fn(od, family, h, k, m):
+    """The reference's DEANN with its BruteForceIndex (estimators.py:306-379, ann.py:105-121) and
+    a numpy PCG64 Generator, per query."""
+    from oracle import deann_oracle as O
 
+    def fn(item):
+        j, q = item
+        O.deann(od, family, h, lambda y, kk: O.brute_force_knn(od, y, kk), q, k, m, rng=np.random.default_rng(j))
+
+    return fn
+
+
+def _deann_parity(od, family, h, k, m, Q, vals, seed, base, sel):
+    """max relative error of GPU DEANN values against the oracle replaying the GPU's neighbours
+    and Philox stream; plus whether the neighbour sets matched the brute force."""
+    from oracle import deann_oracle as O
+    from oracle.philox import IndexReplay, NeighborReplay
+
+    err = 0.0
+    for j in sel:
+        ri, rd = O.brute_force_knn(od, Q[j], k)
+        ref = O.deann(od, family, h, NeighborReplay(ri, rd), Q[j], k, m, rng=IndexReplay(seed, base + j, od.n))[0]
+        err = max(err, abs(vals[j] - ref) / ref)
+    return err
+
+
+def measure_deann_c3(args, local, timer):
+    """DEANN on config 3 (exact k=100 NN + m=1000 Philox samples): device value, e2e through
+    deann_batch, per-kernel rooflines, clocks, parity, CPU baseline."""
+    import torch
+
+    import paper_2107_02736_b200 as g
+    import workloads
+    from oracle import deann_oracle as O
+    from paper_2107_02736_b200 import _lib
+
+    W = workloads.make("c3")
+    h = _bandwidth_cpu_free(W)
+    n, d = W.X.shape
+    nq = W.Q.shape[0]
+    ds = g.Dataset.from_array(W.X, device=local)
+    spec = g.KernelSpec("gaussian", h)
+    Qd = torch.from_numpy(W.Q).to(f"cuda:{local}")
+    out = torch.empty(nq, dtype=torch.float64, device=f"cuda:{local}")
+    lib = _lib.load()
+    stream = torch.cuda.current_stream()
+    seed0 = 1234
+
+    def step(i):
+        _lib.check(lib.dk_deann(ds.handle, Qd.data_ptr(), nq, _lib.DK_GAUSSIAN, h, W.k, W.m, seed0 + i, 0,
+                                out.data_ptr(), None, None, None, stream.cuda_stream))
+
+    steps, warm = max(3, min(args.steps, 20)), max(3, args.warmup)
+    with ClockSampler(local) as clocks:
+        ms = timer.run(step, steps, warm, clocks)
+    launches = _launches(lib, ds)
+    last_seed = seed0 + warm + steps - 1
+    vals = out.cpu().numpy()  # the timed output (last step), before the profiling steps overwrite it
+    # per-kernel rooflines (library CUDA events on the launch stream, separate untimed steps):
+    # the k-NN FILTER sweep against the tensor peak (2 d flops per (query, row) pair of the tiles
+    # it visits — the ball-pruned lists) and the Philox gather against HBM (m accepted fp32 rows
+    # of d floats per query)
+    peaks = _peaks()
+    kroof = {}
+    for mode, name in ((1, "knn_filter_sweep"), (2, "sampling_gather")):
+        _lib.check(lib.dk_set_profiling(ds.handle, mode))
+        step(10_000 + mode)
+        kms, kfl, kby = _kernel_ms(lib, ds)
+        _lib.check(lib.dk_set_profiling(ds.handle, 0))
+        if mode == 1:
+            ach = kfl / (kms / 1e3) / 1e12
+            dense = 2.0 * d * nq * n / (kms / 1e3) / 1e12
+            kroof[name] = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                           "frac": ach / peaks["bf16_tflops"], "kernel_ms": kms, "dense_equivalent_tflops": dense}
+        else:
+            ach = kby / (kms / 1e3) / 1e9
+            kroof[name] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                           "frac": ach / peaks["hbm_gbs"], "kernel_ms": kms}
+    # e2e: the public deann_batch with the GPU brute-force index, pinned host queries in, a
+    # list of Estimates out (the values come back to the host inside every step)
+    Qh = torch.from_numpy(W.Q).pin_memory().numpy()
+    bf = g.BruteForceIndex(ds)
+
+    def e2e_step(i):
+        est = g.deann_batch(ds, spec, bf, Qh, W.k, W.m, rng=g.PhiloxSampler(seed0 + i))
+        return est.values
+
+    e2e_ms = timer.wall(e2e_step, steps, 2)
+    res = {"metric": "DEANN queries/sec (exact k=100 NN + m=1000 Philox samples, gaussian) at n=1.2M, d=100",
+           "value": nq / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
+           "higher_is_better": True, "gpu_launches": launches * steps,
+           "e2e": {"value": nq / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
+                   "d2h_bytes_per_step": int(nq * 8),
+                   "api": "deann_batch(ds, KernelSpec, BruteForceIndex(ds), pinned host queries, 100, 1000, "
+                          "rng=PhiloxSampler) -> list[Estimate]"},
+           "kernel_rooflines": kroof, "clocks": clocks.summary(),
+           "config": {"workload": "c3: 1,200,000 x 100 L2-normalised rows, 10,000 queries, h by median-1e-3 rule",
+                      "bandwidth": h, "k": W.k, "m": W.m, "l2": "inputs larger than L2 (480 MB rows)"}}
+    ds.free()
+    if not args.no_cpu_baseline:
+        od = O.Data(W.X)
+        sel = list(np.random.default_rng(3).choice(nq, 16, replace=False))
+        res["parity_max_rel"] = _deann_parity(od, "gaussian", h, W.k, W.m, W.Q, vals, last_seed, 0, sel)
+        res["parity_note"] = ("timed output (last step, seed %d) vs the oracle deann replaying the GPU's neighbours "
+                              "and Philox stream, 16 seeded queries; gate 1e-5" % last_seed)
+        res["cpu_baseline"] = cpu_baseline(
+            "oracle deann + brute_force_knn, numpy PCG64", _deann_oracle_fn(od, "gaussian", h, W.k, W.m),
+            [(j, W.Q[j]) for j in range(256)], 1, 10.0, f"the first 256 of the {nq:,} queries")
+    return res
+
+
+def measure_c5(args, ws, rank, local, dist, timer):
+    """Config 5 (n = 8M, d = 96, 100,000 queries): exact KDE and DEANN (k = 100, m = 2,000).
+    N = 1: the fused single-GPU calls; N > 1: dataset-sharded (ShardedKDE over NCCL)."""
     import torch
 
     import paper_2107_02736_b200 as g
     import workloads
     from paper_2107_02736_b200 import _lib
+    from paper_2107_02736_b200.sharded import GpuShardEngine, ShardedKDE, TorchComm, shard_bounds
 
-    W = workloads.make("c3")
+    W = workloads.make("c5")
     h = _bandwidth_cpu_free(W)
-    ds = g.Dataset.from_array(W.X, device=local)
-    Qd = torch.from_numpy(W.Q).to(f"cuda:{local}")
-    out = torch.empty(W.Q.shape[0], dtype=torch.float64, device=f"cuda:{local}")
+    n, d = W.X.shape
+    nq = W.Q.shape[0]
+    lo, hi = shard_bounds(n, ws, rank)
+    t0 = time.perf_counter()
+    ds = g.Dataset.from_array(W.X[lo:hi], device=local, global_offset=lo, global_n=n)
+    fit_s = time.perf_counter() - t0
+    spec = g.KernelSpec("gaussian", h)
     lib = _lib.load()
     stream = torch.cuda.current_stream()
+    Qd = torch.from_numpy(W.Q).to(f"cuda:{local}")
+    out = torch.empty(nq, dtype=torch.float64, device=f"cuda:{local}")
+    sk = ShardedKDE(GpuShardEngine(None, global_offset=lo, global_n=n, device=local, dataset=ds), TorchComm()) \
+        if ws > 1 else None
+    seed0 = 777
+    steps, warm = max(2, min(args.steps, 5)), max(3, min(args.warmup, 3))
 
-    def step(i):
-        _lib.check(lib.dk_deann(ds.handle, Qd.data_ptr(), Qd.shape[0], _lib.DK_GAUSSIAN, h, W.k, W.m, 1234 + i, 0,
-                                out.data_ptr(), None, None, None, stream.cuda_stream))
+    def exact_step(_i):
+        g.naive_kde_into(ds, spec, Qd, out, stream=stream.cuda_stream)
+        if ws > 1:
+            dist.all_reduce(out)
 
-    for i in range(max(2, args.warmup)):
-        step(i)
-    torch.cuda.synchronize()
-    steps = max(3, min(args.steps, 10))
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(steps):
-        step(100 + i)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    cnt = ctypes.c_int64()
-    _lib.check(lib.dk_last_launch_count(ds.handle, ctypes.byref(cnt)))
-    # per-kernel rooflines of the two dominant kernels (library CUDA events on the launch
-    # stream, separate untimed steps): the k-NN FILTER distance sweep against the tensor peak
-    # (2 d flops per (query, row) pair of the tiles it visits — the ball-pruned lists — fp16
-    # operands) and the Philox gather against HBM
-    # (algorithmic m accepted fp32 rows of d floats per query)
-    peaks = _peaks()
-    kroof = {}
-    for mode, name in ((1, "knn_filter_sweep"), (2, "sampling_gather")):
-        _lib.check(lib.dk_set_profiling(ds.handle, mode))
-        step(200 + mode)
-        kms, kfl, kby = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-        _lib.check(lib.dk_last_kernel_ms(ds.handle, ctypes.byref(kms), ctypes.byref(kfl), ctypes.byref(kby)))
-        _lib.check(lib.dk_set_profiling(ds.handle, 0))
-        if mode == 1:
-            ach = kfl.value / (kms.value / 1e3) / 1e12
-            # the FILTER sweep skips the tiles no neighbour can be in (ball-pruned lists):
-            # dense_equivalent = the work of an unpruned sweep over the kernel's time
-            dense = 2.0 * W.X.shape[1] * W.Q.shape[0] * W.X.shape[0] / (kms.value / 1e3) / 1e12
-            kroof[name] = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                           "frac": ach / peaks["bf16_tflops"], "kernel_ms": kms.value,
-                           "dense_equivalent_tflops": dense}
+    def deann_step(i):
+        if ws == 1:
+            _lib.check(lib.dk_deann(ds.handle, Qd.data_ptr(), nq, _lib.DK_GAUSSIAN, h, W.k, W.m, seed0 + i, 0,
+                                    out.data_ptr(), None, None, None, stream.cuda_stream))
         else:
-            ach = kby.value / (kms.value / 1e3) / 1e9
-            kroof[name] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                           "frac": ach / peaks["hbm_gbs"], "kernel_ms": kms.value}
-    ds.free()
-    return {"metric": "DEANN queries/sec (exact k=100 NN + m=1000 samples, gaussian) at n=1.2M, d=100",
-            "value": W.Q.shape[0] / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
-            "gpu_launches_per_step": int(cnt.value), "kernel_rooflines": kroof,
-            "config": {"workload": "c3: 1,200,000 x 100 L2-normalised rows, 10,000 queries, h by median-1e-3 rule",
-                       "bandwidth": h, "k": W.k, "m": W.m}}
+            out.copy_(sk.deann(None, spec, W.k, W.m, seed=seed0 + i, Qd=Qd))
+
+    peaks = _peaks()
+    with ClockSampler(local) as clk_exact:
+        for i in range(warm):
+            exact_step(i)
+        _lib.check(lib.dk_set_profiling(ds.handle, 1))
+        ms_exact = timer.run(exact_step, steps, 0, clk_exact)
+    kms = timer.max_over_ranks(_kernel_ms(lib, ds)[0])
+    _lib.check(lib.dk_set_profiling(ds.handle, 0))
+    n_local = hi - lo
+    flops, ex2 = 2.0 * d * nq * n_local, float(nq) * n_local
+    t_bound = max(flops / (peaks["bf16_tflops"] * 1e12), ex2 / _sfu_peak(peaks))
+    with ClockSampler(local) as clk_deann:
+        ms_deann = timer.run(deann_step, steps, warm, clk_deann)
+    res = {
+        "config": {"workload": "c5: 8,000,000 x 96 mixture rows (Dirichlet weights), 100,000 queries, "
+                               "h by median-1e-3 rule", "bandwidth": h, "k": W.k, "m": W.m,
+                   "parallelism": f"dataset-sharded x{ws}" if ws > 1 else "1 GPU", "fit_seconds": fit_s,
+                   "l2": "inputs larger than L2 (3.07 GB rows)"},
+        "exact": {"metric": "KDE queries/sec (exact naive KDE, gaussian) at n=8M, d=96",
+                  "value": nq / (ms_exact / 1e3), "unit": UNIT, "ms_per_step": ms_exact, "steps": steps,
+                  "dtype": "fp16 split3 (fp32 accumulate, fp64 row sums)", "clocks": clk_exact.summary(),
+                  "roofline": {"bound": "tensor x3 (split3) / sfu", "kernel_ms": kms,
+                               "frac_of_1x_binding": t_bound / (kms / 1e3),
+                               "achieved_tflops_algorithmic": flops / (kms / 1e3) / 1e12,
+                               "achieved_tflops_issued_split3": 3 * flops / (kms / 1e3) / 1e12,
+                               "peak_tflops": peaks["bf16_tflops"]}},
+        "deann": {"metric": "DEANN queries/sec (exact k=100 NN + m=2000 Philox samples, gaussian) at n=8M, d=96",
+                  "value": nq / (ms_deann / 1e3), "unit": UNIT, "ms_per_step": ms_deann, "steps": steps,
+                  "clocks": clk_deann.summary()},
+    }
+    if ws == 1:
+        Qh = torch.from_numpy(W.Q).pin_memory().numpy()
+        e_ms = timer.wall(lambda i: g.naive_kde(ds, spec, Qh).values, 2, 1)
+        res["exact"]["e2e"] = {"value": nq / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
+                               "d2h_bytes_per_step": int(nq * 8)}
+        bf = g.BruteForceIndex(ds)
+        d_ms = timer.wall(lambda i: g.deann_batch(ds, spec, bf, Qh, W.k, W.m, rng=g.PhiloxSampler(i)).values, 2, 1)
+        res["deann"]["e2e"] = {"value": nq / (d_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
+                               "d2h_bytes_per_step": int(nq * 8)}
+        deann_vals = out.cpu().numpy()
+        last_seed = seed0 + warm + steps - 1
+        ds.free()
+        if not args.no_cpu_baseline:
+            from oracle import deann_oracle as O
+
+            naive_out = None
+            od = O.Data(W.X)
+            # parity: DEANN timed output (replay) and exact KDE on 4 queries over all 8M rows
+            res["deann"]["parity_max_rel"] = _deann_parity(od, "gaussian", h, W.k, W.m, W.Q, deann_vals, last_seed,
+                                                           0, [0, 50_000])
+            ds2 = g.Dataset.from_array(W.X, device=local)
+            naive_out = g.naive_kde(ds2, spec, W.Q[:4]).values
+            ds2.free()
+            ref = O.naive_kde(od, "gaussian", h, W.Q[:4])
+            res["exact"]["parity_max_rel"] = float(np.max(np.abs(naive_out - ref) / ref))
+            res["exact"]["cpu_baseline"] = cpu_baseline(
+                "oracle/deann_oracle.naive_kde", lambda q: O.naive_kde(od, "gaussian", h, q.reshape(1, -1)),
+                list(W.Q[:64]), 1, 8.0, "single queries of the first 64 over all 8M rows")
+            res["deann"]["cpu_baseline"] = cpu_baseline(
+                "oracle deann + brute_force_knn, numpy PCG64", _deann_oracle_fn(od, "gaussian", h, W.k, W.m),
+                [(j, W.Q[j]) for j in range(64)], 1, 8.0, "the first 64 queries over all 8M rows")
+            del od
+    else:
+        ds.free()
+    return res
 
 
 def fit_manifest():
@@ -489,6 +717,23 @@ def fit_manifest():
         json.dump(man, f, indent=1, sort_keys=True)
 
 
+def _self_launch(args):
+    """`python bench.py --gpus N` without torchrun: re-exec under torch.distributed.run with N
+    ranks on this node (127.0.0.1 rendezvous); NCCL's init lines go to stderr."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execve(sys.executable, cmd, env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -498,13 +743,20 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2",
                     help="c2 (default; BASELINE configs[1], the metric's config) or c5 (scale-out config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-secondary", action="store_true", help="skip the c3 DEANN secondary measurement")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the c3 DEANN object")
+    ap.add_argument("--no-c5", action="store_true", help="skip the c5 (n = 8M) object")
     ap.add_argument("--fit-bandwidth", action="store_true", help="(re)write tests/golden/bandwidths.json")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.fit_bandwidth:
         fit_manifest()
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _self_launch(args)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # NCCL's init lines (comm size) to stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         run_reference(args)
     else:

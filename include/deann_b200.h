@@ -188,6 +188,19 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family,
                    int64_t query_base, double* value_out, int64_t* nbr_idx_out,
                    double* nbr_d2_out, int64_t* sample_idx_out, void* stream);
 
+/* The DEANN combination step alone (estimators.py:344-372), for callers that
+ * assemble the parts themselves — dataset-sharded mode after its collectives
+ * (sharded.py): per query j, Z1 = mean over the k neighbours of kernel(nbr_d2)
+ * (L2 families, estimators.py:349-351) or z1_l1_sum[j] / k (laplacian,
+ * :346-348), Z2 = z2_sum[j] / m, value = (k/n_total) Z1 + ((n_total-k)/n_total) Z2.
+ * All arrays are DEVICE memory (nbr_d2 nq x k, the others nq); nullable when
+ * unused (z1_l1_sum unless laplacian, z2_sum when m == 0).  Same arithmetic as
+ * dk_deann's final step. */
+dk_status dk_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k,
+                           int32_t m, int64_t n_total, const double* nbr_d2,
+                           const double* z1_l1_sum, const double* z2_sum,
+                           double* value_out, void* stream);
+
 /* ---- permuted sampler (RSP / DEANNP) -----------------------
  * RspState (estimators.py:83-96) on the device: `h` is a dataset fitted on the
  * PERMUTED rows (row i = original row permutation[i], permute data.py:214-233);

@@ -1392,6 +1392,21 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
   });
 }
 
+dk_status dk_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m, int64_t n_total,
+                           const double* nbr_d2, const double* z1_l1_sum, const double* z2_sum, double* value_out,
+                           void* stream) {
+  return guard([&] {
+    check_family_bw(family, bandwidth);
+    DK_REQUIRE(nq >= 0 && k >= 0 && m >= 0 && int64_t(k) <= n_total, "bad k / m / n");
+    if (nq == 0) return;
+    DK_REQUIRE(value_out != nullptr && is_device_ptr(value_out), "value_out must be device memory");
+    DK_REQUIRE(k == 0 || (family == DK_LAPLACIAN ? z1_l1_sum != nullptr : nbr_d2 != nullptr), "NULL Z1 input");
+    DK_REQUIRE(m == 0 || z2_sum != nullptr, "NULL z2_sum");
+    launch_deann_combine(nq, family, bandwidth, k, m, n_total, nbr_d2, z1_l1_sum, z2_sum, value_out,
+                         static_cast<cudaStream_t>(stream));
+  });
+}
+
 dk_status dk_rsp_attach(dk_handle h, const int64_t* inverse_permutation) {
   return guard([&] {
     DK_REQUIRE(h != nullptr && inverse_permutation != nullptr, "NULL argument");

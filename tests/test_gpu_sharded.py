@@ -65,12 +65,9 @@ def test_shard_deann_composes_to_single_gpu_and_oracle(problem, family, h):
     i0, d0 = e0.knn(Qd, k)
     i1, d1 = e1.knn(Qd, k)
     idx, d2 = e0.merge_topk(torch.stack([i0, i1]), torch.stack([d0, d1]), k)
-    z2 = (e0.sample_sums(Qd, spec, m, seed, 0, idx) + e1.sample_sums(Qd, spec, m, seed, 0, idx)) / m
-    if family == "laplacian":
-        z1 = (e0.row_sums(Qd, spec, idx) + e1.row_sums(Qd, spec, idx)) / k
-    else:
-        z1 = e0.kernel_of_sq(d2, spec).mean(dim=1)
-    val = ((k / N) * z1 + ((N - k) / N) * z2).cpu().numpy()
+    z2s = e0.sample_sums(Qd, spec, m, seed, 0, idx) + e1.sample_sums(Qd, spec, m, seed, 0, idx)
+    z1s = (e0.row_sums(Qd, spec, idx) + e1.row_sums(Qd, spec, idx)) if family == "laplacian" else None
+    val = e0.combine(spec, k, m, d2, z1s, z2s).cpu().numpy()
     single, _, _ = g.deann_arrays(g.Dataset.from_array(X), spec, Q, k, m, seed=seed)
     np.testing.assert_allclose(val, single, rtol=1e-12)
     od = O.Data(X)
@@ -91,3 +88,38 @@ def test_sharded_kde_object_single_rank(problem):
     v = sk.deann(Q, spec, 10, 100, seed=5).cpu().numpy()
     single, _, _ = g.deann_arrays(g.Dataset.from_array(X), spec, Q, 10, 100, seed=5)
     np.testing.assert_allclose(v, single, rtol=1e-12)
+
+
+def test_query_sharded_equals_dataset_sharded_gpu(problem):
+    """Query-sharded (2 replicas, each a slice of the batch at its global query positions) and
+    dataset-sharded (2 row shards, merged k-NN, global Philox stream) give identical k-NN sets,
+    identical accepted sample ids and values equal to fp64 summation order."""
+    from paper_2107_02736_b200.sharded import GpuReplicaEngine
+
+    X, Q, (e0, e1) = problem
+    spec = g.KernelSpec("gaussian", 1.5)
+    k, m, seed, base = 20, 200, 31, 5
+    Qd = e0.queries(Q)
+    nq = Q.shape[0]
+    # dataset-sharded
+    i0, d0 = e0.knn(Qd, k)
+    i1, d1 = e1.knn(Qd, k)
+    idx, d2 = e0.merge_topk(torch.stack([i0, i1]), torch.stack([d0, d1]), k)
+    acc_ds = torch.empty((nq, m), dtype=torch.int64, device="cuda")
+    acc_ds1 = torch.empty((nq, m), dtype=torch.int64, device="cuda")
+    z2s = e0.sample_sums(Qd, spec, m, seed, base, idx, export=acc_ds) + \
+        e1.sample_sums(Qd, spec, m, seed, base, idx, export=acc_ds1)
+    val_ds = e0.combine(spec, k, m, d2, None, z2s)
+    assert torch.equal(acc_ds, acc_ds1)  # every rank walks the same global stream
+    # query-sharded: two replicas, each its slice
+    rep = GpuReplicaEngine(X, device=0)
+    vals, accs, idxs = [], [], []
+    for r in range(2):
+        lo, hi = shard_bounds(nq, 2, r)
+        a = torch.empty((hi - lo, m), dtype=torch.int64, device="cuda")
+        vals.append(rep.deann(Qd[lo:hi], spec, k, m, seed, base + lo, export_samples=a))
+        accs.append(a)
+        idxs.append(rep.knn(Qd[lo:hi], k)[0])
+    np.testing.assert_array_equal(torch.cat(idxs).cpu().numpy(), idx.cpu().numpy())
+    np.testing.assert_array_equal(torch.cat(accs).cpu().numpy(), acc_ds.cpu().numpy())
+    np.testing.assert_allclose(torch.cat(vals).cpu().numpy(), val_ds.cpu().numpy(), rtol=1e-12)

@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 from oracle import deann_oracle as O
 from oracle.philox import IndexReplay, NeighborReplay, draws
 from paper_2107_02736_b200.kernels import KernelSpec
-from paper_2107_02736_b200.sharded import LocalComm, ShardedKDE, TorchComm, shard_bounds
+from paper_2107_02736_b200.sharded import LocalComm, QueryShardedKDE, ShardedKDE, TorchComm, shard_bounds
 
 
 def _fh(kernel):
@@ -66,7 +66,7 @@ class OracleShardEngine:
             idx[j], d2[j] = ii[order], dd[order]
         return torch.as_tensor(idx), torch.as_tensor(d2)
 
-    def sample_sums(self, Qd, kernel, m, seed, query_base, excl):
+    def sample_sums(self, Qd, kernel, m, seed, query_base, excl, export=None):
         fam, h = _fh(kernel)
         out = np.zeros(Qd.shape[0])
         for j, q in enumerate(Qd.numpy()):
@@ -74,6 +74,8 @@ class OracleShardEngine:
             if excl is not None:
                 stream = stream[~np.isin(stream, excl[j].numpy())]
             acc = stream[:m]
+            if export is not None:
+                export[j] = torch.as_tensor(acc)
             loc = acc - self.global_offset
             loc = loc[(loc >= 0) & (loc < self.n_local)]
             out[j] = O.kernel_rows(self.data.x64, self.data.sq_norms, fam, h, loc, q).sum()
@@ -88,9 +90,53 @@ class OracleShardEngine:
             out[j] = O.kernel_rows(self.data.x64, self.data.sq_norms, fam, h, loc, q).sum()
         return torch.as_tensor(out)
 
-    def kernel_of_sq(self, d2, kernel):
+    def combine(self, kernel, k, m, nbr_d2, z1_l1_sum, z2_sum):
+        """estimators.py:344-372: Z1 from the neighbour distances (L2) or the L1 sums, Z2 = sum / m."""
         fam, h = _fh(kernel)
-        return torch.as_tensor(O.kernel_from_sql2(fam, h, d2.numpy().copy()))
+        N = self.global_n
+        t = nbr_d2 if nbr_d2 is not None else (z2_sum if z2_sum is not None else z1_l1_sum)
+        val = np.zeros(t.shape[0])
+        if k > 0:
+            z1 = z1_l1_sum.numpy() / k if fam == "laplacian" else \
+                O.kernel_from_sql2(fam, h, nbr_d2.numpy().copy()).mean(axis=1)
+            val += (k / N) * z1
+        if m > 0:
+            val += ((N - k) / N) * (z2_sum.numpy() / m)
+        return torch.as_tensor(val)
+
+
+class OracleReplicaEngine:
+    """CPU stand-in for GpuReplicaEngine (query-sharded mode): the whole dataset, oracle arithmetic."""
+
+    def __init__(self, rows):
+        self.data = O.Data(rows)
+        self.n = self.data.n
+        self.d = self.data.d
+
+    def queries(self, Q):
+        return torch.as_tensor(np.ascontiguousarray(Q, dtype=np.float64))
+
+    def naive(self, Qd, kernel):
+        fam, h = _fh(kernel)
+        return torch.as_tensor(O.naive_kde(self.data, fam, h, Qd.numpy()) if Qd.shape[0] else np.zeros(0))
+
+    def knn(self, Qd, k):
+        out = [O.brute_force_knn(self.data, q, k) for q in Qd.numpy()]
+        idx = np.array([o[0] for o in out], dtype=np.int64).reshape(-1, k)
+        d2 = np.array([o[1] for o in out]).reshape(-1, k)
+        return torch.as_tensor(idx), torch.as_tensor(d2)
+
+    def deann(self, Qd, kernel, k, m, seed, query_base, export_samples=None):
+        fam, h = _fh(kernel)
+        vals = np.zeros(Qd.shape[0])
+        for j, q in enumerate(Qd.numpy()):
+            i, dd = O.brute_force_knn(self.data, q, k) if k else (np.empty(0, np.int64), np.empty(0))
+            vals[j] = O.deann(self.data, fam, h, NeighborReplay(i, dd), q, k, m,
+                              rng=IndexReplay(seed, query_base + j, self.n))[0]
+            if export_samples is not None:
+                stream = draws(seed, query_base + j, 0, 20 * m + 1000, self.n)
+                export_samples[j] = torch.as_tensor(stream[~np.isin(stream, i)][:m])
+        return torch.as_tensor(vals)
 
 
 def _problem():
@@ -113,6 +159,17 @@ def _worker(rank, world, port, results):
             out[f"deann_{fam}"] = sk.deann(Q, KernelSpec(fam, h), 12, 40, seed=99, query_base=3).numpy()
         idx, d2 = sk.knn(Q, 12)
         out["knn_idx"], out["knn_d2"] = idx.numpy(), d2.numpy()
+        acc = torch.zeros((Q.shape[0], 40), dtype=torch.int64)
+        out["ds_deann"] = sk.deann(Q, KernelSpec("gaussian", 1.2), 12, 40, seed=7, query_base=11,
+                                   export_samples=acc).numpy()
+        out["ds_acc"] = acc.numpy()
+        # query-sharded mode: every rank holds all rows, evaluates its slice of the queries
+        qs = QueryShardedKDE(OracleReplicaEngine(X), TorchComm(), rank, world)
+        out["qs_naive"] = qs.naive_kde(Q, KernelSpec("gaussian", 1.2)).numpy()
+        qi, qd = qs.knn(Q, 12)
+        out["qs_knn_idx"], out["qs_knn_d2"] = qi.numpy(), qd.numpy()
+        v, a = qs.deann(Q, KernelSpec("gaussian", 1.2), 12, 40, seed=7, query_base=11, export_samples=True)
+        out["qs_deann"], out["qs_acc"] = v.numpy(), a.numpy()
         if rank == 0:
             results.update(out)
     finally:
@@ -157,6 +214,17 @@ def test_sharded_deann_equals_whole_with_replay(sharded_results):
             i, dd = O.brute_force_knn(d, q, 12)
             ref = O.deann(d, fam, h, NeighborReplay(i, dd), q, 12, 40, rng=IndexReplay(99, 3 + j, d.n))[0]
             assert sharded_results[f"deann_{fam}"][j] == pytest.approx(ref, rel=1e-12)
+
+
+def test_query_sharded_equals_dataset_sharded(sharded_results):
+    """SURVEY §7 test plan: both modes on the same seeds give identical k-NN sets and identical
+    accepted sample ids; the values agree (here both are fp64 oracle arithmetic)."""
+    r = sharded_results
+    np.testing.assert_array_equal(r["qs_knn_idx"], r["knn_idx"])
+    np.testing.assert_allclose(r["qs_knn_d2"], r["knn_d2"], rtol=1e-12)
+    np.testing.assert_array_equal(r["qs_acc"], r["ds_acc"])
+    np.testing.assert_allclose(r["qs_deann"], r["ds_deann"], rtol=1e-12)
+    np.testing.assert_allclose(r["qs_naive"], r["naive_gaussian"], rtol=1e-12)
 
 
 def test_local_comm_single_shard_matches():
