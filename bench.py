@@ -345,8 +345,26 @@ def _launches(lib, ds):
     return int(cnt.value)
 
 
+_SFU_MEASURED = {}
+
+
 def _sfu_peak(peaks):
-    return 148 * 16 * peaks["sm_max_mhz"] * 1e6
+    """ex2/s of the SFU: measured on this GPU by dk_mufu_probe when available (the
+    nominal 148 SMs x 16 / clk x max clock otherwise)."""
+    return _SFU_MEASURED.get("value", 148 * 16 * peaks["sm_max_mhz"] * 1e6)
+
+
+def _measure_sfu(local):
+    import ctypes
+
+    from paper_2107_02736_b200 import _lib
+
+    v = ctypes.c_double()
+    best = 0.0
+    for _ in range(3):
+        _lib.check(_lib.load().dk_mufu_probe(local, ctypes.byref(v)))
+        best = max(best, v.value)
+    _SFU_MEASURED["value"] = best
 
 
 def run_ours(args):
@@ -366,6 +384,7 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     timer = Timer(torch, dist, local)
+    _measure_sfu(local)
     WL = WORKLOADS[args.workload]
     W = workloads.make(args.workload)
     n, d = W.X.shape
@@ -437,7 +456,9 @@ def run_ours(args):
             "kernel_ms": kmsv,
             "sfu": {"achieved": ex2 / t_k / 1e12, "peak": sfu_peak / 1e12, "unit": "Tex2/s",
                     "frac": (ex2 / t_k) / sfu_peak,
-                    "peak_note": "148 SMs x 16 ex2/clk x clocks.max.sm (nominal; scripts/mufu_probe.py measures it)"},
+                    "peak_nominal": 148 * 16 * peaks["sm_max_mhz"] * 1e6 / 1e12,
+                    "peak_note": "measured: dk_mufu_probe (ex2.approx.ftz.f32, 8 independent chains per thread, "
+                                 "64 warps per SM, best of 3) on this GPU; nominal = 148 SMs x 16/clk x max clock"},
             "binding": "sfu" if ex2 / sfu_peak >= flops / tc_peak else "tensor",
             "frac_of_binding": t_bound / t_k,
         },

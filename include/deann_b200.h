@@ -280,6 +280,10 @@ dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t
  * given operand encoding (0 exact, 1 split3, 2 fp16) — a pipeline probe. */
 dk_status dk_sweep_probe(dk_handle h, const double* Q, int64_t nq, int32_t mode, int32_t encoding,
                          double* ms);
+/* Measured SFU exp2 throughput of `device` (ex2.approx.ftz.f32 per second, all SMs):
+ * the MUFU denominator of the exact-KDE roofline (no reference counterpart). */
+dk_status dk_mufu_probe(int32_t device, double* ex2_per_second);
+
 /* Number of this library's kernels launched by the last API call. */
 dk_status dk_last_launch_count(dk_handle h, int64_t* count);
 

@@ -29,7 +29,7 @@ EXPORTED = (
     "dk_naive", "dk_sqdist", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
     "dk_rsp_attach", "dk_rsp_walk", "dk_ivf_create", "dk_ivf_free", "dk_kmeanspp_seed", "dk_kmeanspp_pick",
     "dk_kmeans_lloyd", "dk_ivf_get", "dk_ivf_set", "dk_ivf_query", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_sweep_probe",
-    "dk_host_alloc", "dk_host_free", "dk_deann_ivf", "dk_deann_combine",
+    "dk_host_alloc", "dk_host_free", "dk_deann_ivf", "dk_deann_combine", "dk_mufu_probe",
 )
 
 
@@ -90,6 +90,7 @@ def _declare(lib):
         "dk_eval_rows": (_i32, [_vp, _vp, _i64, _i32, _f64, _vp, _vp, _i32, _vp, _vp]),
         "dk_kernel_values": (_i32, [_i32, _f64, _vp, _i64, _vp, _vp]),
         "dk_deann": (_i32, [_vp, _vp, _i64, _i32, _f64, _i32, _i32, _u64, _i64, _vp, _vp, _vp, _vp, _vp]),
+        "dk_mufu_probe": (_i32, [_i32, ctypes.POINTER(_f64)]),
         "dk_deann_combine": (_i32, [_i64, _i32, _f64, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),
         "dk_rsp_attach": (_i32, [_vp, _vp]),
         "dk_rsp_walk": (_i32, [_vp, _vp, _i64, _i32, _f64, _i32, _vp, _i32, _i64, _i32, _vp, _vp,

@@ -538,7 +538,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       launch_home_tile_lists(at<int32_t>(h->ws, L.near_s), h->kc->nbr, bn, nqb, h->kc->off, ntiles, L.hS,
                              int64_t(L.hneed) * kBN, L.hmax, L.hlmax, hl, hc, s);
       launch_block_units(hc, nqb, L.hlmax, h->num_sms, at<int32_t>(h->ws, L.tstart), at<int32_t>(h->ws, L.ustart),
-                         hplan, at<int32_t>(h->ws, L.ulist), s);
+                         hplan, at<int32_t>(h->ws, L.ulist), int64_t(L.ulist_ints / 3), s);
       float* tmin = at<float>(h->ws, L.tmin);
       const int32_t nseg = L.hlmax * kListSegs;
       launch_fill_float(tmin, int64_t(nseg) * bn_pad, inf, s);
@@ -585,10 +585,10 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       if (tmajor)
         launch_tile_units(bits, nqb, ntiles, h->num_sms, at<int32_t>(h->ws, L.tcnt_t), at<int32_t>(h->ws, L.tstart),
                           at<int32_t>(h->ws, L.ustart), uplan, at<int32_t>(h->ws, L.blist),
-                          at<int32_t>(h->ws, L.ulist), s);
+                          at<int32_t>(h->ws, L.ulist), int64_t(L.ulist_ints / 3), s);
       else
         launch_block_units(tcnt, nqb, ntiles, h->num_sms, at<int32_t>(h->ws, L.tstart), at<int32_t>(h->ws, L.ustart),
-                           uplan, at<int32_t>(h->ws, L.ulist), s);
+                           uplan, at<int32_t>(h->ws, L.ulist), int64_t(L.ulist_ints / 3), s);
     }
     {
       SweepArgs a{};
@@ -902,6 +902,7 @@ int32_t dk_device_ok(int32_t device) {
 }
 
 dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts, dk_handle* out) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(out != nullptr, "out handle pointer is NULL");
     *out = nullptr;
@@ -918,6 +919,7 @@ dk_status dk_fit(const float* X, int64_t n, int32_t d, const dk_fit_opts* opts, 
 }
 
 dk_status dk_file_info(const char* path, int64_t* n, int32_t* d) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(path != nullptr, "NULL path");
     const FileHeader fh = read_header(path);
@@ -928,6 +930,7 @@ dk_status dk_file_info(const char* path, int64_t* n, int32_t* d) {
 
 dk_status dk_fit_file(const char* path, int64_t row_begin, int64_t row_count, const dk_fit_opts* opts,
                       dk_handle* out) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(path != nullptr && out != nullptr, "NULL argument");
     *out = nullptr;
@@ -951,6 +954,7 @@ dk_status dk_fit_file(const char* path, int64_t row_begin, int64_t row_count, co
 }
 
 dk_status dk_free(dk_handle h) {
+  DK_NVTX();
   return guard([&] {
     if (!h) return;
     DeviceGuard g(h->device);
@@ -991,6 +995,7 @@ dk_status dk_info(dk_handle h, int64_t* n, int32_t* d, int64_t* go, int64_t* gn,
 }
 
 dk_status dk_sq_norms(dk_handle h, double* out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr && out != nullptr, "NULL argument");
     DeviceGuard g(h->device);
@@ -1002,6 +1007,7 @@ dk_status dk_sq_norms(dk_handle h, double* out, void* stream) {
 
 dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth, uint32_t flags,
                    double* out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");
     check_family_bw(family, bandwidth);
@@ -1134,6 +1140,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
 
 dk_status dk_knn(dk_handle h, const double* Q, int64_t nq, int32_t k, int64_t* idx_out, double* d2_out,
                  void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");
     DK_REQUIRE(k >= 1 && int64_t(k) <= h->n,
@@ -1163,6 +1170,7 @@ dk_status dk_knn(dk_handle h, const double* Q, int64_t nq, int32_t k, int64_t* i
 
 dk_status dk_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_in, const double* d2_in,
                         int64_t* idx_out, double* d2_out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(parts >= 1 && parts <= 64 && k >= 1 && nq >= 0, "bad merge arguments");
     if (nq == 0) return;
@@ -1177,6 +1185,7 @@ dk_status dk_sample(dk_handle h, const double* Q, int64_t nq, int32_t family, do
                     uint64_t seed, int64_t query_base, const int64_t* excl, const int32_t* excl_cnt,
                     int32_t excl_stride, double* z_sum, int64_t* accepted_idx_out, int64_t* draws_out,
                     void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");
     check_family_bw(family, bandwidth);
@@ -1237,6 +1246,7 @@ dk_status dk_sample(dk_handle h, const double* Q, int64_t nq, int32_t family, do
 
 dk_status dk_eval_rows(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth,
                        const int64_t* rows, const int32_t* cnt, int32_t stride, double* out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");
     check_family_bw(family, bandwidth);
@@ -1277,6 +1287,7 @@ dk_status dk_eval_rows(dk_handle h, const double* Q, int64_t nq, int32_t family,
 
 dk_status dk_kernel_values(int32_t family, double bandwidth, const double* dist, int64_t count, double* out,
                            void* stream) {
+  DK_NVTX();
   return guard([&] {
     check_family_bw(family, bandwidth);
     DK_REQUIRE(count >= 0, "negative count");
@@ -1326,6 +1337,7 @@ dk_status dk_kernel_values(int32_t family, double bandwidth, const double* dist,
 dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m,
                    uint64_t seed, int64_t query_base, double* value_out, int64_t* nbr_idx_out, double* nbr_d2_out,
                    int64_t* sample_idx_out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");
     check_family_bw(family, bandwidth);
@@ -1395,6 +1407,7 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
 dk_status dk_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t k, int32_t m, int64_t n_total,
                            const double* nbr_d2, const double* z1_l1_sum, const double* z2_sum, double* value_out,
                            void* stream) {
+  DK_NVTX();
   return guard([&] {
     check_family_bw(family, bandwidth);
     DK_REQUIRE(nq >= 0 && k >= 0 && m >= 0 && int64_t(k) <= n_total, "bad k / m / n");
@@ -1408,6 +1421,7 @@ dk_status dk_deann_combine(int64_t nq, int32_t family, double bandwidth, int32_t
 }
 
 dk_status dk_rsp_attach(dk_handle h, const int64_t* inverse_permutation) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr && inverse_permutation != nullptr, "NULL argument");
     DeviceGuard g(h->device);
@@ -1419,6 +1433,7 @@ dk_status dk_rsp_attach(dk_handle h, const int64_t* inverse_permutation) {
 dk_status dk_rsp_walk(dk_handle h, const double* Q, int64_t nq, int32_t family, double bandwidth, int32_t m,
                       const int64_t* excl, int32_t excl_stride, int64_t cursor_in, int32_t independent,
                       double* z_sum, int32_t* taken, int64_t* cursor_out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr, "NULL handle");
     check_family_bw(family, bandwidth);
@@ -1505,6 +1520,7 @@ dk_status dk_last_kernel_ms(dk_handle h, double* ms, double* flops, double* byte
 }
 
 dk_status dk_sweep_probe(dk_handle h, const double* Q, int64_t nq, int32_t mode, int32_t encoding, double* ms) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr && Q != nullptr && ms != nullptr && nq > 0, "bad probe arguments");
     DK_REQUIRE(mode >= MODE_KDE_GAUSS && mode <= MODE_KDE_GAUSS_MUFU && encoding >= 0 && encoding <= 2, "bad probe mode");
@@ -1590,6 +1606,7 @@ HostCache& host_cache() {
 }  // namespace
 
 dk_status dk_host_alloc(int64_t bytes, void** out) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(out != nullptr && bytes >= 0, "bad argument");
     size_t cls = 4096;

@@ -10,10 +10,23 @@
 #include <vector>
 
 #include "../../include/deann_b200.h"
+#include <nvtx3/nvToolsExt.h>
+
+#include "checks.cuh"
 
 namespace dk {
 
 void set_error(const std::string& msg);
+
+// NVTX range around every C-ABI entry point (header-only NVTX v3: a no-op unless a profiler
+// such as Nsight Systems / Compute is attached), named after the function.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define DK_NVTX() ::dk::NvtxRange dk_nvtx_range_(__func__)
 
 struct Error {
   dk_status code;
@@ -285,9 +298,9 @@ void launch_sort_queries_by_ball(const int32_t* nearest, int64_t nq, int32_t C, 
 // FILTER work units built on the device (scal[0] = unit count, [1] = swept (block, tile) pairs)
 void launch_tile_units(const uint32_t* bits, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* tcnt,
                        int32_t* tstart, int32_t* ustart, int32_t* scal, int32_t* blist, int32_t* ulist,
-                       cudaStream_t s);
+                       int64_t ucap, cudaStream_t s);
 void launch_block_units(const int32_t* tcount, int32_t nqb, int32_t list_stride, int32_t slots, int32_t* bstart,
-                        int32_t* ustart, int32_t* scal, int32_t* ulist, cudaStream_t s);
+                        int32_t* ustart, int32_t* scal, int32_t* ulist, int64_t ucap, cudaStream_t s);
 // per block of 128 ball-sorted queries: the threshold sweep's tiles — every S-th tile of the
 // sorted rows (>= k/4 disjoint 64-column segments for every block) plus up to hmax tiles of
 // the balls nearest to the block's queries, each extended by its nearest neighbour balls until

@@ -1421,6 +1421,7 @@ using namespace dk;
 extern "C" {
 
 dk_status dk_ivf_create(dk_handle h, int32_t n_clusters, dk_ivf_handle* out) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(h != nullptr && out != nullptr, "NULL argument");
     *out = nullptr;
@@ -1450,6 +1451,7 @@ dk_status dk_ivf_create(dk_handle h, int32_t n_clusters, dk_ivf_handle* out) {
 }
 
 dk_status dk_ivf_free(dk_ivf_handle v) {
+  DK_NVTX();
   return guard([&] {
     if (!v) return;
     DeviceGuard g(v->ds->device);
@@ -1459,6 +1461,7 @@ dk_status dk_ivf_free(dk_ivf_handle v) {
 }
 
 dk_status dk_kmeanspp_seed(dk_ivf_handle v, int32_t c, int64_t row, double* total_out) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(v != nullptr && total_out != nullptr, "NULL argument");
     DK_REQUIRE(c >= 0 && c < v->C && row >= 0 && row < v->n, "centroid or row out of range");
@@ -1476,6 +1479,7 @@ dk_status dk_kmeanspp_seed(dk_ivf_handle v, int32_t c, int64_t row, double* tota
 }
 
 dk_status dk_kmeanspp_pick(dk_ivf_handle v, double u, double total, int64_t* row_out) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(v != nullptr && row_out != nullptr, "NULL argument");
     DK_REQUIRE(total > 0.0 && u >= 0.0 && u < 1.0, "pick needs total > 0 and u in [0, 1)");
@@ -1494,6 +1498,7 @@ dk_status dk_kmeanspp_pick(dk_ivf_handle v, double u, double total, int64_t* row
 }
 
 dk_status dk_kmeans_lloyd(dk_ivf_handle v, int32_t max_iter, double rel_tol, int32_t* iters_out) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(v != nullptr, "NULL argument");
     DK_REQUIRE(max_iter >= 0 && rel_tol >= 0.0, "bad k-means parameters");
@@ -1518,6 +1523,7 @@ dk_status dk_kmeans_lloyd(dk_ivf_handle v, int32_t max_iter, double rel_tol, int
 }
 
 dk_status dk_ivf_get(dk_ivf_handle v, double* centroids, int64_t* rows, int64_t* offsets) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(v != nullptr, "NULL argument");
     DeviceGuard g(v->ds->device);
@@ -1529,6 +1535,7 @@ dk_status dk_ivf_get(dk_ivf_handle v, double* centroids, int64_t* rows, int64_t*
 }
 
 dk_status dk_ivf_set(dk_ivf_handle v, const double* centroids, const int64_t* rows, const int64_t* offsets) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(v != nullptr && centroids != nullptr && rows != nullptr && offsets != nullptr, "NULL argument");
     std::vector<int64_t> off(static_cast<size_t>(v->C) + 1);
@@ -1554,6 +1561,7 @@ dk_status dk_ivf_set(dk_ivf_handle v, const double* centroids, const int64_t* ro
 
 dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, int32_t n_probe, int32_t formula,
                        int64_t* idx_out, double* d2_out, int32_t* cnt_out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(v != nullptr, "NULL handle");
     DK_REQUIRE(v->lists, "index lists are not built (dk_kmeans_lloyd or dk_ivf_set first)");
@@ -1942,6 +1950,7 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
 dk_status dk_deann_ivf(dk_ivf_handle v, const double* Q, int64_t nq, int32_t family, double bandwidth,
                        int32_t k, int32_t m, int32_t n_probe, uint64_t seed, int64_t query_base,
                        double* value_out, int32_t* khat_out, void* stream) {
+  DK_NVTX();
   return guard([&] {
     DK_REQUIRE(v != nullptr, "NULL handle");
     DK_REQUIRE(family == DK_GAUSSIAN || family == DK_EXPONENTIAL || family == DK_LAPLACIAN,

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
     const int i = i0 + grp;
     const bool ok = i < ns;
     const unsigned long long col = ok ? top[i].lo : 0ull;
+    DK_DCHECK(col < (1ull << 40));
     const double dd = exact_d2_group<G>(X + size_t(col) * d, qv, d, gl);
     if (gl == 0 && ok) {
       top[i].hi = static_cast<unsigned long long>(__double_as_longlong(dd));
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(256) select_slow_kernel(
   __shared__ int s_stop;
   for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
     const int64_t q = slow_list[li];
+    DK_DCHECK(q >= 0 && int(cnt[q]) >= k);
     const int c = int(cnt[q]);
     const unsigned long long* keys = cand + size_t(q) * cap;
     __syncthreads();
@@ -700,7 +702,7 @@ __global__ void __launch_bounds__(1024) unit_plan_kernel(const int32_t* __restri
 __global__ void tile_units_fill_kernel(const uint32_t* __restrict__ bits, int32_t nqb, int32_t ntiles,
                                        const int32_t* __restrict__ cnt, const int32_t* __restrict__ start,
                                        const int32_t* __restrict__ ustart, const int32_t* __restrict__ scal,
-                                       int32_t* __restrict__ blist, int32_t* __restrict__ ulist) {
+                                       int32_t* __restrict__ blist, int32_t* __restrict__ ulist, int64_t ucap) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
   const int nwords = (ntiles + 31) >> 5;
@@ -710,6 +712,7 @@ __global__ void tile_units_fill_kernel(const uint32_t* __restrict__ bits, int32_
   const int U = scal[2], c = cnt[t], s0 = start[t];
   int u = ustart[t];
   for (int i = 0; i < c; i += U, ++u) {
+    if (u >= ucap) __trap();  // unit-list capacity (capi.cu KnnLayout) exceeded: an internal sizing bug
     ulist[3 * u] = t;
     ulist[3 * u + 1] = s0 + i;
     ulist[3 * u + 2] = s0 + min(c, i + U);
@@ -721,12 +724,13 @@ __global__ void tile_units_fill_kernel(const uint32_t* __restrict__ bits, int32_
 // flat index b * ntiles + i, ntiles = the list stride)
 __global__ void block_units_fill_kernel(int32_t nqb, int32_t ntiles, const int32_t* __restrict__ cnt,
                                         const int32_t* __restrict__ ustart, const int32_t* __restrict__ scal,
-                                        int32_t* __restrict__ ulist) {
+                                        int32_t* __restrict__ ulist, int64_t ucap) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nqb) return;
   const int U = scal[2], c = cnt[b];
   int u = ustart[b];
   for (int i = 0; i < c; i += U, ++u) {
+    if (u >= ucap) __trap();  // unit-list capacity exceeded: an internal sizing bug
     ulist[3 * u] = b;
     ulist[3 * u + 1] = int32_t(int64_t(b) * ntiles + i);
     ulist[3 * u + 2] = int32_t(int64_t(b) * ntiles + min(c, i + U));
@@ -777,6 +781,7 @@ __global__ void __launch_bounds__(128) home_tile_lists_kernel(
       if (nb >= 0) got += add_ball(nb);
     }
   }
+  DK_DCHECK(c <= lmax);
   lcnt[qb] = c;
 }
 
@@ -878,14 +883,14 @@ void launch_sort_queries_by_ball(const int32_t* nearest, int64_t nq, int32_t C, 
 
 void launch_tile_units(const uint32_t* bits, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* tcnt,
                        int32_t* tstart, int32_t* ustart, int32_t* scal, int32_t* blist, int32_t* ulist,
-                       cudaStream_t s) {
+                       int64_t ucap, cudaStream_t s) {
   tile_count_kernel<<<unsigned((ntiles + 255) / 256), 256, 0, s>>>(bits, nqb, ntiles, tcnt);
   DK_CHECK_LAUNCH();
   // >= 4 units per CTA; a unit keeps its tile resident while its query blocks stream past
   unit_plan_kernel<<<1, 1024, 0, s>>>(tcnt, ntiles, slots, 4, 4, tstart, ustart, scal);
   DK_CHECK_LAUNCH();
   tile_units_fill_kernel<<<unsigned((ntiles + 255) / 256), 256, 0, s>>>(bits, nqb, ntiles, tcnt, tstart, ustart, scal,
-                                                                        blist, ulist);
+                                                                        blist, ulist, ucap);
   DK_CHECK_LAUNCH();
 }
 
@@ -905,11 +910,12 @@ void launch_ball_neighbors(const double* dq, int32_t C, int32_t* nbr, cudaStream
 }
 
 void launch_block_units(const int32_t* tcount, int32_t nqb, int32_t ntiles, int32_t slots, int32_t* bstart,
-                        int32_t* ustart, int32_t* scal, int32_t* ulist, cudaStream_t s) {
+                        int32_t* ustart, int32_t* scal, int32_t* ulist, int64_t ucap, cudaStream_t s) {
   // units of ~equal length (>= 8 tiles) so the persistent CTAs finish together
   unit_plan_kernel<<<1, 1024, 0, s>>>(tcount, nqb, slots, 4, 8, bstart, ustart, scal);
   DK_CHECK_LAUNCH();
-  block_units_fill_kernel<<<unsigned((nqb + 127) / 128), 128, 0, s>>>(nqb, ntiles, tcount, ustart, scal, ulist);
+  block_units_fill_kernel<<<unsigned((nqb + 127) / 128), 128, 0, s>>>(nqb, ntiles, tcount, ustart, scal, ulist,
+                                                                       ucap);
   DK_CHECK_LAUNCH();
 }
 

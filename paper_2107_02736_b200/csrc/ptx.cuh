@@ -2,6 +2,7 @@
 // Written against the PTX ISA (tcgen05.*, cp.async.bulk.tensor.*) for
 // `-gencode arch=compute_100a,code=sm_100a`.
 #pragma once
+#include "checks.cuh"
 #include <cstdint>
 #include <cuda.h>
 

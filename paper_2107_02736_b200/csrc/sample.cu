@@ -195,6 +195,7 @@ __global__ void sample_kernel(const float* __restrict__ X, int64_t n_local, int6
   while (accepted < m) {
     const uint64_t t = t_base + lane;
     const int64_t row = draw_row(seed, t, jg, uint64_t(N));
+    DK_DCHECK(row >= 0 && row < N);
     const bool ok = ecnt == 0 || !in_sorted(ex, ecnt, row);
     const uint32_t ballot = __ballot_sync(0xffffffffu, ok);
     const int rank = __popc(ballot & lt_mask);

@@ -418,12 +418,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
         const int col0 = __ldg(p.ulist + 3 * u) * kBN;
         const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
+        DK_DCHECK(col0 >= 0 && col0 < p.n && i0 <= i1);
         mbar_wait(aempty_bar, (uiter & 1) ^ 1);
         mbar_arrive_expect_tx(afull_bar, uint32_t(p.kblocks) * kBBlockBytes);
         for (int kb = 0; kb < p.kblocks; ++kb)
           tma_load_2d(smemB + size_t(kb) * kBBlockBytes, &tmapB, afull_bar, kb * kBK, col0, pol_b);
         for (int i = i0; i < i1; ++i, ++titer) {
           const int qb = __ldg(p.blist + i);
+          DK_DCHECK(qb >= 0 && qb < p.nqb);
           const uint32_t xs = titer % kXnSlots;
           mbar_wait(&xempty_bar[xs], ((titer / kXnSlots) & 1) ^ 1);
           mbar_arrive_expect_tx(&xfull_bar[xs], kBN * 4);
@@ -466,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           int col0;
           if (p.tlist != nullptr) {
             col0 = tnext * kBN;
+            DK_DCHECK(tnext >= 0 && col0 < p.n && qb >= 0 && qb < p.nqb);
             if (t + 1 < t1) tnext = __ldg(p.tlist + t + 1);
           } else {
             col0 = t * p.tile_stride * kBN;
@@ -767,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.tlist != nullptr) {
             // listed threshold sweep: 8 segments of 32 columns per tile (segment = list position x 8 + 32-column
             // group), fine enough that the tiles near a query hold k segments
+            DK_DCHECK(t - qb * p.list_stride >= 0 && t - qb * p.list_stride < p.list_stride);
             float* tm = p.tmin + (size_t(t - qb * p.list_stride) * 8 + cg * 2) * p.nq_pad + row;
             tm[0] = fmaxf(fminf(a0.x, a0.y), 0.f);
             tm[size_t(p.nq_pad)] = fmaxf(fminf(b0.x, b0.y), 0.f);
