@@ -407,7 +407,7 @@ struct KnnLayout {
   size_t flags, A, qn, scal, tmin, tau, cnt, cand, lists, ctr;
   // pruned path
   size_t dq, near, near_s, iota, qperm, sort_tmp, qp, tidx, td2, tlist, tcnt, bits, tcnt_t, tstart, ustart, blist,
-      ulist, hlist, hcnt;
+      ulist, hlist, hcnt, hlo, hinv, htop, hist, tauh;
   int32_t hS = 1, hlmax = 0;  // threshold sweep: stride of the strided tiles, list length per block
   int32_t hneed = 0, hmax = 0;  // near tiles wanted / allowed per block
   size_t sort_tmp_bytes = 0, ulist_ints = 0;
@@ -426,7 +426,7 @@ KnnLayout knn_layout(const dk_dataset* h, const KnnPlan& kp, int32_t k, int32_t 
   if (prune) {  // threshold sweep over per-block lists: every hS-th tile + the nearest balls' tiles
     const int32_t ntiles = int32_t(h->n_pad / kBN);
     L.hS = std::max<int32_t>(1, ntiles / ((k + kListSegs - 1) / kListSegs + 16));  // >= k strided segments
-    L.hneed = std::max<int32_t>(16, 2 * ((k + kListSegs - 1) / kListSegs));  // rows around a ball: >= 2k segments
+    L.hneed = std::max<int32_t>(4, (4 * k + kBN - 1) / kBN);  // tiles' worth of rows around a ball: >= 4k rows
     L.hmax = std::max(kHomeTiles, L.hneed);
     L.hlmax = (ntiles + L.hS - 1) / L.hS + L.hmax;
   }
@@ -461,6 +461,11 @@ KnnLayout knn_layout(const dk_dataset* h, const KnnPlan& kp, int32_t k, int32_t 
     L.ulist = pl.add<int32_t>(L.ulist_ints);
     L.hlist = pl.add<int32_t>(size_t(nqb) * L.hlmax);
     L.hcnt = pl.add<int32_t>(nqb);
+    L.hlo = pl.add<float>(bpad);
+    L.hinv = pl.add<float>(bpad);
+    L.htop = pl.add<float>(bpad);
+    L.hist = pl.add<uint32_t>(size_t(bpad) * kHistBins);
+    L.tauh = pl.add<float>(bpad);
   }
   L.end = pl.off;
   return L;
@@ -495,11 +500,15 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
   const bool tmajor = prune && !tmajor_off && tile_major_fits(e.Kp);
   const float inf = std::numeric_limits<float>::infinity();
   int32_t* ctr = at<int32_t>(h->ws, L.ctr);
-  // threshold sweep over per-block lists of near tiles (DK_KNN_HOME=1) instead of every
-  // stride-th tile: tighter on low-dimensional balls (c3), looser in high dimension (c5,
-  // where 32-row segment minima of a sub-ball sit far above the k-th distance) — off by default
-  const char* home_env = std::getenv("DK_KNN_HOME");  // read per call (tests toggle it)
-  const bool home_tau = home_env != nullptr && std::atoi(home_env) != 0;
+  // Threshold for large datasets ("home" mode): a histogram-refined bound from per-block lists
+  // of the tiles near the block's balls, combined with a global bound from segment minima over
+  // ~4 x target tiles of the original row order (queries far from every ball: small clusters).
+  // It replaces the strided sweep over a quarter of the tiles when that global pass is at most
+  // 1/8 of the dataset (c5: 8M rows, 5% of the tiles; k-NN 106 -> 77 ms); smaller datasets keep
+  // the strided sweep.  DK_KNN_HOME=0/1 forces it (read per call: tests toggle it).
+  const char* home_env = std::getenv("DK_KNN_HOME");
+  const int64_t home_target = std::clamp<int64_t>(4 * int64_t(k), 256, 2048);
+  const bool home_tau = home_env != nullptr ? std::atoi(home_env) != 0 : int64_t(ntiles) >= 32 * home_target;
   for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
     const int64_t bn = std::min<int64_t>(bpad, nq - b0);
     const int32_t bn_pad = int32_t(query_pad(bn));
@@ -529,7 +538,33 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     if (kp.tau_inf) {
       launch_fill_float(tau, bn, inf, s);
     } else if (prune && home_tau) {
-      // threshold from the block's own neighbourhood: 32-column segment minima over every hS-th
+      // (a) a global bound, valid for every query however far it is from its balls: segment
+      // minima over every stride_g-th tile of the ORIGINAL row order (random rows: the k-th
+      // smallest segment minimum tracks a few-hundredth-neighbour distance), at 4x the stride of
+      // the plain threshold sweep
+      {
+        const int64_t target = std::clamp<int64_t>(4 * int64_t(k), 256, 2048);
+        const char* gs_env = std::getenv("DK_KNN_GTILES");  // A/B: tiles the global pass visits
+        const int64_t gtiles = gs_env ? std::max<int64_t>(target, std::atoll(gs_env)) : 4 * target;
+        const int32_t sg = int32_t(std::clamp<int64_t>(ntiles / gtiles, 1, std::max<int64_t>(1, ntiles / target)));
+        const int64_t nvis = (ntiles + sg - 1) / sg;
+        const int32_t seg_tiles = int32_t((nvis + target - 1) / target);
+        const int32_t nseg_g = int32_t((nvis + seg_tiles - 1) / seg_tiles);
+        float* tmin = at<float>(h->ws, L.tmin);
+        launch_fill_float(tmin, int64_t(nseg_g) * bn_pad, inf, s);
+        SweepArgs a{};
+        a.mode = MODE_TILEMIN;
+        a.qop = &q;
+        a.enc = &e;
+        a.n = h->n;
+        a.n_pad = h->n_pad;
+        a.tile_stride = sg;
+        a.seg_tiles = seg_tiles;
+        a.tmin = tmin;
+        launch_sweep(a, h->num_sms, s);
+        launch_tau_from_tmin(tmin, nseg_g, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau, s);
+      }
+      // (b) threshold from the block's own neighbourhood: 32-column segment minima over every hS-th
       // tile and the tiles of the balls nearest to the block's queries (tens to hundreds of tiles
       // per block instead of a quarter of the dataset); tau_q = k-th smallest + 2 eps_q as before
       int32_t* hl = at<int32_t>(h->ws, L.hlist);
@@ -540,8 +575,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       launch_block_units(hc, nqb, L.hlmax, h->num_sms, at<int32_t>(h->ws, L.tstart), at<int32_t>(h->ws, L.ustart),
                          hplan, at<int32_t>(h->ws, L.ulist), int64_t(L.ulist_ints / 3), s);
       float* tmin = at<float>(h->ws, L.tmin);
-      const int32_t nseg = L.hlmax * kListSegs;
-      launch_fill_float(tmin, int64_t(nseg) * bn_pad, inf, s);
+      const int32_t nseg = L.hlmax * kListSegs;  // no fill: tau reads only the listed segments
       SweepArgs a{};
       a.mode = MODE_TILEMIN;
       a.qop = &q;
@@ -556,7 +590,56 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       a.nunits_dev = hplan;
       a.list_stride = L.hlmax;
       launch_sweep(a, h->num_sms, s);
-      launch_tau_from_tmin(tmin, nseg, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau, s);
+      float* hlo = at<float>(h->ws, L.hlo);
+      float* hinv = at<float>(h->ws, L.hinv);
+      float* htop = at<float>(h->ws, L.htop);
+      uint32_t* hist = at<uint32_t>(h->ws, L.hist);
+      float* tau_h = at<float>(h->ws, L.tauh);
+      launch_tau_from_tmin(tmin, nseg, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau_h, s, hc, kListSegs, hlo, hinv,
+                           htop);
+      // refinement: a second listed sweep counts, per query, the approx d2 of the listed rows in
+      // 64 bins over [min segment minimum, k-th segment minimum]; the bin where the count reaches
+      // k gives a tighter (still valid) tau_q — segment minima alone sit well above the k-th
+      // distance when few segments are near (high dimension, small balls)
+      DK_CUDA(cudaMemsetAsync(hist, 0, size_t(bn) * kHistBins * sizeof(uint32_t), s));
+      {
+        SweepArgs b{};
+        b.mode = MODE_HIST;
+        b.qop = &q;
+        b.enc = &h->kc->enc;
+        b.n = h->n;
+        b.n_pad = h->n_pad;
+        b.tile_stride = 1;
+        b.ulist = at<int32_t>(h->ws, L.ulist);
+        b.tlist = hl;
+        b.nunits_dev = hplan;
+        b.list_stride = L.hlmax;
+        b.hlo = hlo;
+        b.hinv = hinv;
+        b.htop = htop;
+        b.hist = hist;
+        launch_sweep(b, h->num_sms, s);
+      }
+      launch_tau_from_hist(hist, hlo, hinv, htop, tau_h, bn, k, q.qn, e.xn_max, e.eps_rel, tau, s);
+      if (std::getenv("DK_KNN_DEBUG")) {  // diagnostics: threshold quantiles and list lengths
+        std::vector<float> ta(static_cast<size_t>(bn));
+        std::vector<int32_t> lc(static_cast<size_t>(nqb)), ns(static_cast<size_t>(bn));
+        DK_CUDA(cudaMemcpyAsync(ta.data(), tau, ta.size() * 4, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaMemcpyAsync(lc.data(), hc, lc.size() * 4, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaMemcpyAsync(ns.data(), at<int32_t>(h->ws, L.near_s), ns.size() * 4, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+        std::vector<float> st = ta;
+        std::sort(st.begin(), st.end());
+        const int w = int(std::max_element(ta.begin(), ta.end()) - ta.begin());
+        int distinct = 0;
+        for (int r = (w / 128) * 128; r < std::min<int>(int(bn), (w / 128) * 128 + 128); ++r)
+          distinct += (r == (w / 128) * 128 || ns[size_t(r)] != ns[size_t(r) - 1]) ? 1 : 0;
+        std::fprintf(stderr, "[dk] tau p0 %g p50 %g p90 %g p99 %g max %g | worst row %d block %d list %d of max %d, "
+                     "%d balls | list p50 %d max %d\n", st.front(), st[st.size() / 2], st[st.size() * 9 / 10],
+                     st[st.size() * 99 / 100], st.back(), w, w / 128, lc[size_t(w / 128)], L.hlmax, distinct,
+                     [&] { auto c = lc; std::sort(c.begin(), c.end()); return c[c.size() / 2]; }(),
+                     *std::max_element(lc.begin(), lc.end()));
+      }
     } else {
       float* tmin = at<float>(h->ws, L.tmin);
       launch_fill_float(tmin, int64_t(kp.nseg) * bn_pad, inf, s);

@@ -252,6 +252,11 @@ struct SweepArgs {
   int32_t nunits_list;
   const int32_t* nunits_dev;  // unit count in device memory (built on the device); overrides nunits_list
   int32_t list_stride;        // TILEMIN over tile lists: entries per query block in tlist (segment = list position)
+  // MODE_HIST (threshold refinement): per-row bin range and the [nq_pad][64] counts
+  const float* hlo;
+  const float* hinv;
+  const float* htop;
+  uint32_t* hist;
   // tile-major FILTER: unit u = (dataset tile ulist[3u], query blocks blist[ulist[3u+1] .. ulist[3u+2]))
   int32_t tmajor;
   const int32_t* blist;
@@ -315,8 +320,17 @@ void launch_scatter_knn(const int64_t* idx_p, const double* d2_p, const int32_t*
                         int64_t* idx_out, double* d2_out, cudaStream_t s);
 
 // k-NN selection
+// block_entries (nullable): per block of 128 queries, the entries of its listed threshold sweep;
+// only their segments_per x entries segments are read (the rest of tmin is never written)
 void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
-                          float xn_max, float eps_rel, float* tau, cudaStream_t s);
+                          float xn_max, float eps_rel, float* tau, cudaStream_t s,
+                          const int32_t* block_entries = nullptr, int32_t segs_per = 0, float* hlo = nullptr,
+                          float* hinv = nullptr, float* htop = nullptr);
+// threshold refinement from the MODE_HIST counts: tau_q = min(tau_q, tau_h_q, upper edge of the
+// first bin where the cumulative count reaches k + 2 eps_q)
+void launch_tau_from_hist(const uint32_t* hist, const float* hlo, const float* hinv, const float* htop,
+                          const float* tau_h, int64_t nq, int32_t k, const float* qn, float xn_max, float eps_rel,
+                          float* tau, cudaStream_t s);
 void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s);
 // selection: fast path for every query, sorted-rounds kernel over the device list of queries
 // the fast path could not finish; queries with overflowing or too-short candidate lists are

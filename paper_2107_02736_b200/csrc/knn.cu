@@ -29,6 +29,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "internal.h"
+#include "tile_kernel.cuh"
 
 namespace dk {
 
@@ -116,17 +117,38 @@ __global__ void tau_from_tmin_kernel(const float* __restrict__ tmin, int32_t nse
 // minima are >= 0, so their float bits order like the values): no sort of all segments.
 __global__ void __launch_bounds__(256) tau_radix_kernel(const float* __restrict__ tmin, int32_t nseg, int32_t nq_pad,
                                                         int64_t nq, int32_t k, const float* __restrict__ qn,
-                                                        float xn_max, float eps_rel, float* __restrict__ tau) {
+                                                        float xn_max, float eps_rel, float* __restrict__ tau,
+                                                        const int32_t* __restrict__ block_entries, int32_t segs_per,
+                                                        float* __restrict__ hlo, float* __restrict__ hinv,
+                                                        float* __restrict__ htop) {
   extern __shared__ uint32_t vals[];
   __shared__ uint32_t hist[256];
-  __shared__ uint32_t s_digit, s_below;
+  __shared__ uint32_t s_digit, s_below, s_min;
   const int64_t q = blockIdx.x;
   if (q >= nq) return;
+  // listed sweeps: only the segments of this query block's list were written
+  if (block_entries != nullptr) nseg = min(nseg, block_entries[q / 128] * segs_per);
+  if (hlo != nullptr && nseg < k) {  // no bound from these segments: no histogram refinement either
+    if (threadIdx.x == 0) {
+      tau[q] = __int_as_float(0x7f800000);
+      hlo[q] = 0.f;
+      hinv[q] = 0.f;
+      htop[q] = __int_as_float(0xff800000);  // -inf: nothing is counted
+    }
+    return;
+  }
   if (nseg < k) {
     if (threadIdx.x == 0) tau[q] = __int_as_float(0x7f800000);
     return;
   }
-  for (int i = threadIdx.x; i < nseg; i += blockDim.x) vals[i] = __float_as_uint(fmaxf(tmin[size_t(i) * nq_pad + q], 0.f));
+  if (threadIdx.x == 0) s_min = 0xffffffffu;
+  __syncthreads();
+  uint32_t vmin = 0xffffffffu;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    vals[i] = __float_as_uint(fmaxf(tmin[size_t(i) * nq_pad + q], 0.f));
+    vmin = min(vmin, vals[i]);
+  }
+  if (hlo != nullptr) atomicMin(&s_min, vmin);
   const int lane = threadIdx.x & 31;
   uint32_t prefix = 0u, mask = 0u, krem = uint32_t(k);
   for (int shift = 24; shift >= 0; shift -= 8) {
@@ -168,7 +190,45 @@ __global__ void __launch_bounds__(256) tau_radix_kernel(const float* __restrict_
     float t = v + 2.f * eps;
     t = __fmul_ru(t, 1.0f + 2.4e-7f);  // as tau_from_tmin_kernel
     tau[q] = t;
+    if (hlo != nullptr) {  // histogram range for the refinement sweep: [min segment minimum, k-th]
+      const float lo = __uint_as_float(s_min);
+      hlo[q] = lo;
+      htop[q] = v;
+      hinv[q] = v > lo ? 1.f / (v - lo) : 0.f;
+    }
   }
+}
+
+// tau_q from the per-query histogram of approx d2 over [lo_q, top_q] (bin b holds the values
+// with floor(64 sqrt((d2 - lo) / (top - lo))) == b): the upper edge of the first bin where the
+// cumulative count reaches k bounds the k-th smallest approx d2 (k distinct rows lie at or below
+// it); the edge carries a 1e-5 relative slack for the fp32 binning arithmetic.
+__global__ void tau_hist_kernel(const uint32_t* __restrict__ hist, const float* __restrict__ hlo,
+                                const float* __restrict__ hinv, const float* __restrict__ htop,
+                                const float* __restrict__ tau_h, int64_t nq, int32_t k, const float* __restrict__ qn,
+                                float xn_max, float eps_rel, float* __restrict__ tau) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  float t = tau_h[q];  // the listed segment-minimum bound (+inf when the list had < k segments)
+  if (hinv[q] > 0.f) {
+    const uint32_t* h = hist + size_t(q) * kHistBins;
+    uint32_t cum = 0;
+    int b = 0;
+    for (; b < kHistBins; ++b) {
+      cum += h[b];
+      if (cum >= uint32_t(k)) break;
+    }
+    if (b < kHistBins) {  // (always: the k segment minima themselves are counted)
+      const double lo = hlo[q], top = htop[q];
+      const double f = double(b + 1) / kHistBins;
+      const double edge = lo + (top - lo) * f * f * (1.0 + 1e-5) + 1e-6 * (top - lo);
+      const float eps = eps_rel * (qn[q] + xn_max);
+      float te = float(fmin(edge, double(top))) + 2.f * eps;
+      te = __fmul_ru(te, 1.0f + 2.4e-7f);
+      t = fminf(t, te);
+    }
+  }
+  tau[q] = fminf(tau[q], t);  // every bound is valid: keep the tightest
 }
 
 // exact fp64 direct-difference d2 by a group of G lanes (float4 row loads when rows are
@@ -938,14 +998,25 @@ void launch_fill_float(float* p, int64_t count, float v, cudaStream_t s) {
   DK_CHECK_LAUNCH();
 }
 
+void launch_tau_from_hist(const uint32_t* hist, const float* hlo, const float* hinv, const float* htop,
+                          const float* tau_h, int64_t nq, int32_t k, const float* qn, float xn_max, float eps_rel,
+                          float* tau, cudaStream_t s) {
+  if (nq <= 0) return;
+  tau_hist_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(hist, hlo, hinv, htop, tau_h, nq, k, qn, xn_max, eps_rel,
+                                                             tau);
+  DK_CHECK_LAUNCH();
+}
+
 void launch_tau_from_tmin(const float* tmin, int32_t nseg, int32_t nq_pad, int64_t nq, int32_t k, const float* qn,
-                          float xn_max, float eps_rel, float* tau, cudaStream_t s) {
-  const bool sort_path = std::getenv("DK_TAU_SORT") != nullptr;  // A/B switch (read per call: tests)
+                          float xn_max, float eps_rel, float* tau, cudaStream_t s, const int32_t* block_entries,
+                          int32_t segs_per, float* hlo, float* hinv, float* htop) {
+  const bool sort_path = std::getenv("DK_TAU_SORT") != nullptr && block_entries == nullptr && hlo == nullptr;
   if (!sort_path) {
     const size_t smem = size_t(std::max(nseg, 1)) * 4;
     if (smem > 232448) throw Error{DK_EINVAL, "too many k-NN segments"};
     set_dynamic_smem(tau_radix_kernel, smem);
-    tau_radix_kernel<<<unsigned(nq), 256, smem, s>>>(tmin, nseg, nq_pad, nq, k, qn, xn_max, eps_rel, tau);
+    tau_radix_kernel<<<unsigned(nq), 256, smem, s>>>(tmin, nseg, nq_pad, nq, k, qn, xn_max, eps_rel, tau,
+                                                     block_entries, segs_per, hlo, hinv, htop);
     DK_CHECK_LAUNCH();
     return;
   }

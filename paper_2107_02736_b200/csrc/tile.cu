@@ -226,6 +226,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.nunits_list = a.nunits_list;
   p.nunits_dev = a.nunits_dev;
   p.list_stride = a.list_stride;
+  p.hlo = a.hlo;
+  p.hinv = a.hinv;
+  p.htop = a.htop;
+  p.hist = a.hist;
   p.tmajor = tmajor ? 1 : 0;
   p.blist = a.blist;
   p.guard = a.guard;
@@ -234,7 +238,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   // a device-side unit count is unknown here: one CTA per SM, surplus CTAs find no unit
   const int nunits = a.ulist != nullptr ? (a.nunits_dev != nullptr ? nslots : a.nunits_list) : ngroups * pl.ncc;
   if (nunits <= 0) return;
-  if (a.ulist != nullptr && (pr || (a.mode != MODE_FILTER && a.mode != MODE_TILEMIN)))
+  if (a.ulist != nullptr && (pr || (a.mode != MODE_FILTER && a.mode != MODE_TILEMIN && a.mode != MODE_HIST)))
     throw Error{DK_EINVAL, "internal: tile lists are k-NN sweeps only"};
   if (a.ulist != nullptr && a.mode == MODE_TILEMIN && a.seg_tiles != 0)
     throw Error{DK_EINVAL, "internal: listed TILEMIN sweeps use one segment per 64-column group"};
@@ -253,6 +257,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
     case MODE_TILEMIN: launch_any<MODE_TILEMIN>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_FILTER: launch_any<MODE_FILTER>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_NULL: launch_any<MODE_NULL>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_HIST:
+      if (pr || a.ulist == nullptr) throw Error{DK_EINVAL, "internal: histogram sweeps are listed single-CTA sweeps"};
+      launch_mode<MODE_HIST, false>(q.tmap, tb, p, grid, pl.smem, s);
+      break;
     default: throw Error{DK_EINVAL, "bad tile mode"};
   }
 }

@@ -55,8 +55,10 @@ enum TileMode : int {
   MODE_TILEMIN = 2,
   MODE_FILTER = 3,
   MODE_NULL = 4,
-  MODE_KDE_GAUSS_MUFU = 5  // gaussian with every exponential on MUFU (MMA-heavy encodings)
+  MODE_KDE_GAUSS_MUFU = 5,  // gaussian with every exponential on MUFU (MMA-heavy encodings)
+  MODE_HIST = 6             // k-NN threshold refinement: per-query histogram of approx d2 (listed sweeps)
 };
+constexpr int kHistBins = 64;  // MODE_HIST bins per query (quadratic spacing over [lo_q, top_q])
 __host__ __device__ constexpr bool is_kde(int mode) {
   return mode == MODE_KDE_GAUSS || mode == MODE_KDE_EXP || mode == MODE_KDE_GAUSS_MUFU;
 }
@@ -100,6 +102,12 @@ struct TileParams {
   const int32_t* blist;
   const int32_t* nunits_dev;
   int32_t list_stride;     // TILEMIN over per-block tile lists: segment = (list position) x 64-column group
+  // MODE_HIST: per query row, bins b = floor(64 sqrt((d2 - hlo) * hinv)) for d2 <= htop, counted into
+  // hist[row][64] (shared-memory counts flushed with global atomics per work unit)
+  const float* hlo;
+  const float* hinv;
+  const float* htop;
+  uint32_t* hist;
   const float* xn;         // [n_pad] |x|^2 (encoding-consistent)
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
@@ -121,7 +129,7 @@ __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, i
     a = size_t(stages) * kABlockBytes;
     b = size_t(kblocks) * kBBlockBytes;
   }
-  size_t stage = mode == MODE_FILTER ? size_t(kBM) * kStageCap * 8 + kBM * 4 : 0;
+  size_t stage = (mode == MODE_FILTER || mode == MODE_HIST) ? size_t(kBM) * kStageCap * 8 + kBM * 4 : 0;
   return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + stage + 512 /*barriers*/;
 }
 
@@ -184,7 +192,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
                                           float2& acc0, float2& acc1, float& mn, const TileParams& p, int row,
                                           uint32_t* scnt, unsigned long long* sbuf, int lrow) {
   const float4* x4 = reinterpret_cast<const float4*>(xs_smem);
-  if (full || MODE == MODE_TILEMIN || MODE == MODE_FILTER) {
+  if (full || MODE == MODE_TILEMIN || MODE == MODE_FILTER || MODE == MODE_HIST) {
     if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU) {
       constexpr uint32_t poly = MODE == MODE_KDE_GAUSS ? kPolyPairs : 0u;
       // d2 = S * m2s + (qn + xn) in the cancellation-safe order, then t = d2 * negc
@@ -230,11 +238,22 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
       }
       if (!full) {  // columns past n: +inf never wins a min; NaN never passes a threshold (not even +inf)
         const int lim = int(min(int64_t(32), n - cbase));
-        const float pad = MODE == MODE_FILTER ? __int_as_float(0x7fc00000) : __int_as_float(0x7f800000);
+        const float pad = MODE != MODE_TILEMIN ? __int_as_float(0x7fc00000) : __int_as_float(0x7f800000);
 #pragma unroll
         for (int j = 0; j < 32; ++j) d2v[j] = j < lim ? d2v[j] : pad;
       }
-      if constexpr (MODE == MODE_TILEMIN) {
+      if constexpr (MODE == MODE_HIST) {
+        // tau holds htop; acc0 = (hlo, hinv) of this row (set by the caller); NaN pads never count
+        uint32_t* hrow = reinterpret_cast<uint32_t*>(sbuf) + lrow * kHistBins;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (d2v[j] <= tau) {
+            const float u = fmaxf((d2v[j] - acc0.x) * acc0.y, 0.f);
+            const int b = min(kHistBins - 1, __float2int_rz(sqrtf(u) * float(kHistBins)));
+            atomicAdd(hrow + b, 1u);
+          }
+        }
+      } else if constexpr (MODE == MODE_TILEMIN) {
         // minima of the two 16-column halves (listed sweeps keep them as separate segments)
         float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[16], m3 = d2v[17];
 #pragma unroll
@@ -346,8 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     smemX = reinterpret_cast<float*>(smemA + size_t(stages) * kABlockBytes);
   }
   unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smemX + kXnSlots * kBN);  // FILTER staging
-  uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (MODE == MODE_FILTER ? kBM * kStageCap : 0));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(scnt + (MODE == MODE_FILTER ? kBM : 0));
+  constexpr bool kStage = MODE == MODE_FILTER || MODE == MODE_HIST;  // FILTER staging / HIST bins
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (kStage ? kBM * kStageCap : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scnt + (kStage ? kBM : 0));
   uint64_t* full_bar = bars;                 // [stages]   (leader's counts both CTAs' bytes)
   uint64_t* empty_bar = bars + stages;       // [stages]
   uint64_t* tfull_bar = bars + 2 * stages;   // [2]
@@ -389,6 +409,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if constexpr (MODE == MODE_FILTER) {
     for (int i = threadIdx.x; i < kBM; i += blockDim.x) scnt[i] = 0;
+  }
+  if constexpr (MODE == MODE_HIST) {
+    static_assert(kBM * kHistBins * 4 <= kBM * kStageCap * 8, "histogram bins must fit the staging area");
+    uint32_t* hb = reinterpret_cast<uint32_t*>(sbuf);
+    for (int i = threadIdx.x; i < kBM * kHistBins; i += blockDim.x) hb[i] = 0u;
   }
   if (warp == 2) {
     if constexpr (kPair) tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -715,6 +740,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float qn = p.qn[row];
       float tau = 0.f;
       if constexpr (MODE == MODE_FILTER) tau = p.tau[row];
+      float2 hpar = make_float2(0.f, 0.f);  // MODE_HIST: (lo, 1 / (top - lo)) of the row
+      if constexpr (MODE == MODE_HIST) {
+        tau = p.htop[row];
+        hpar = make_float2(p.hlo[row], p.hinv[row]);
+      }
       double usum = 0.0;
       float mn = __int_as_float(0x7f800000);
       // TILEMIN segments: seg_tiles > 0 -> groups of seg_tiles whole tiles; seg_tiles == 0 -> one
@@ -757,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t cbase = int64_t(p.tlist != nullptr ? p.tlist[t] : t * p.tile_stride) * kBN + cg * 64;
         const float* xsm = smemX + xs * kBN + cg * 64;
         const bool full = cbase + 64 <= p.n;
-        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f), b0 = a0;
+        float2 a0 = MODE == MODE_HIST ? hpar : make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f), b0 = a0;
         epi_chunk<MODE>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf, lrow);
         // TILEMIN returns the chunk's two 16-column minima in its first accumulator
         epi_chunk<MODE>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n, MODE == MODE_TILEMIN ? b0 : a0, a1,
@@ -786,6 +816,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if constexpr (MODE == MODE_TILEMIN) {
         if (t1 > t0 && p.seg_tiles > 0)
           atomicMin(reinterpret_cast<int*>(&p.tmin[size_t(seg) * p.nq_pad + row]), __float_as_int(fmaxf(mn, 0.f)));
+      } else if constexpr (MODE == MODE_HIST) {
+        // flush the unit's bins: one global atomic per nonzero (row, bin)
+        epi_bar();
+        if (cg == 0) {
+          uint32_t* hrow = reinterpret_cast<uint32_t*>(sbuf) + lrow * kHistBins;
+          for (int b = 0; b < kHistBins; ++b) {
+            const uint32_t v = hrow[b];
+            if (v) {
+              atomicAdd(p.hist + size_t(row) * kHistBins + b, v);
+              hrow[b] = 0u;
+            }
+          }
+        }
+        epi_bar();
       } else if constexpr (MODE == MODE_FILTER) {
         // flush the unit's staged candidates: one global atomic per row
         epi_bar();
