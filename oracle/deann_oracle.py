@@ -459,3 +459,45 @@ def ivf_query(data: Data, cent: np.ndarray, lists, query, k: int, n_probe: int, 
     d2 += data.sq_norms[cand]
     d2 += float(y @ y)
     return smallest_k(np.maximum(d2, 0.0), cand, k)
+
+
+def ivf_ann_query(data: Data, cent: np.ndarray, lists, query, k: int, n_probe: int):
+    """IvfAnnIndex.query (ann.py:243-316) restated with the reference's own arithmetic: probe by
+    (C y) * -2 + |c|^2 with (distance, id) order; candidate ranking in SINGLE precision over the
+    list-contiguous fp32 rows (vectors32 @ y32, then norms32 - 2 * dot, numpy fp32 — the BLAS
+    sgemv of the reference), argpartition boundary widening and a stable argsort, i.e. the k
+    smallest by (fp32 key, position in the probe concatenation); then the selected rows are
+    re-evaluated in fp64 and ordered by _smallest_k."""
+    if k < 1:
+        raise ValueError(f"k={k} must be >= 1")
+    y = np.asarray(query, dtype=np.float64).ravel()
+    sizes = np.array([len(a) for a in lists], dtype=np.int64)
+    row_ids = np.concatenate(list(lists)).astype(np.int64) if len(lists) else np.empty(0, np.int64)
+    vectors32 = np.ascontiguousarray(data.x32[row_ids])
+    norms32 = data.sq_norms[row_ids].astype(np.float32)
+    offsets = np.concatenate([[0], np.cumsum(sizes)])
+    probe = _probe(cent, y, n_probe, 1)
+    blocks = [(offsets[c], offsets[c + 1]) for c in probe]
+    blocks = [(lo, hi) for lo, hi in blocks if hi > lo]
+    if not blocks:
+        return np.empty(0, np.int64), np.empty(0, np.float64)
+    y32 = y.astype(np.float32)
+    d2 = np.concatenate([vectors32[lo:hi] @ y32 for lo, hi in blocks])
+    norms = np.concatenate([norms32[lo:hi] for lo, hi in blocks])
+    ids = np.concatenate([row_ids[lo:hi] for lo, hi in blocks])
+    d2 = norms - np.float32(2.0) * d2
+    k_sel = min(k, len(d2))
+    if k_sel < len(d2):
+        part = np.argpartition(d2, k_sel - 1)[:k_sel]
+        boundary = d2[part].max()
+        cand = np.flatnonzero(d2 <= boundary)
+        order = np.argsort(d2[cand], kind="stable")[:k_sel]
+        sel_ids = ids[cand[order]]
+    else:
+        sel_ids = ids
+    ex = data.x64[sel_ids] @ y
+    ex *= -2.0
+    ex += data.sq_norms[sel_ids]
+    ex += float(y @ y)
+    np.maximum(ex, 0.0, out=ex)
+    return smallest_k(ex, sel_ids, len(sel_ids))

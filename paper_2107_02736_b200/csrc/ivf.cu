@@ -25,6 +25,8 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
 
+#include <type_traits>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -796,7 +798,7 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
     const K128* __restrict__ tau, int32_t cap, K128* __restrict__ cand, int32_t* __restrict__ ccnt) {
   __shared__ double xr[PRC * (PDJ + 1)];
   __shared__ double ys[PQ * PDJ];
-  __shared__ int64_t s_q[PQ], s_pos[PQ];
+  __shared__ int64_t s_q[PQ], s_pos[PQ], s_base[PQ];
   __shared__ double s_yy[PQ];
   __shared__ K128 s_tau[PQ];
   const int64_t i0 = istart[blo], item = i0 + blockIdx.x;
@@ -807,7 +809,11 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
     if (istart[mid] <= item) lo = mid; else hi = mid - 1;
   }
   const int bkt = lo;
-  const int c = MODE == 0 ? bkt : bkt - C - 1;
+  // MODE 0 / 2: phase-1 buckets (every key written); MODE 1 / 3: phase-2 buckets (keys below tau_q
+  // appended).  MODE 2 / 3 rank like IvfAnnIndex (fp32 keys), MODE 0 / 1 exactly (fp64)
+  constexpr bool kF32 = MODE >= 2;
+  constexpr bool kFilter = MODE == 1 || MODE == 3;
+  const int c = kFilter ? bkt - C - 1 : bkt;
   // item = (query group, row span) of the bucket, spans of `span` rows
   const int64_t lb = off[c], le = off[c + 1];
   const int64_t nspan = (le - lb + span - 1) / span, local = item - istart[bkt];
@@ -820,21 +826,25 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
     if (t < np) {
       const int64_t pr = sval[p0 + t];
       q = pr / n_probe;
-      if (MODE == 0) {  // segment offset: the rows of the query's earlier leading lists
-        pos = qoff[q];
+      if (!kFilter || kF32) {  // position: the rows of the query's earlier probed lists
+        const int64_t qb = qoff != nullptr ? qoff[q] : 0;
+        pos = qb;
         for (int64_t p = q * n_probe; p < pr; ++p) pos += off[probe[p] + 1] - off[probe[p]];
-      } else {
-        s_tau[t] = tau[q];
+        s_base[t] = qb;
       }
+      if (kFilter) s_tau[t] = tau[q];
       s_yy[t] = yyq[q];
     }
     s_q[t] = q;
     s_pos[t] = pos;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // MODE 2 (IvfAnnIndex ranking, ann.py:294-312): fp32 dot of the fp32 row and fl32(y), one
+  // sequential FMA chain over the dimensions; every other mode accumulates in fp64
+  using Acc = typename std::conditional<kF32, float, double>::type;
   for (int64_t r0 = b; r0 < e; r0 += PRC) {
     const int rn = int(min(e - r0, int64_t(PRC)));
-    double acc[PW][PR];
+    Acc acc[PW][PR];
 #pragma unroll
     for (int t = 0; t < PW; ++t)
 #pragma unroll
@@ -861,11 +871,11 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
       __syncthreads();
       if (warp * PW >= np) continue;  // no query on this warp (it still stages)
       for (int jj = 0; jj < dj; ++jj) {
-        double y[PW], x[PR];
+        Acc y[PW], x[PR];
 #pragma unroll
-        for (int t = 0; t < PW; ++t) y[t] = ys[(warp * PW + t) * PDJ + jj];
+        for (int t = 0; t < PW; ++t) y[t] = Acc(ys[(warp * PW + t) * PDJ + jj]);
 #pragma unroll
-        for (int i = 0; i < PR; ++i) x[i] = xr[(lane + 32 * i) * (PDJ + 1) + jj];
+        for (int i = 0; i < PR; ++i) x[i] = Acc(xr[(lane + 32 * i) * (PDJ + 1) + jj]);
 #pragma unroll
         for (int t = 0; t < PW; ++t)
 #pragma unroll
@@ -882,7 +892,25 @@ __global__ void __launch_bounds__(128) pair_tile_kernel(
       for (int t = 0; t < PW; ++t) {
         const int qq = warp * PW + t;
         if (qq >= np) continue;
-        double v = acc[t][i] * -2.0;
+        if constexpr (kF32) {
+          // key32 = norms32 - 2 dot32 (one fp32 rounding), ranked with the row's position in the
+          // query's probe concatenation: (order-preserving key bits << 32 | position), row id
+          const float key32 = __fsub_rn(float(xn), 2.0f * float(acc[t][i]));
+          uint32_t u = __float_as_uint(key32);
+          u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+          const int64_t p = s_pos[qq] - s_base[qq] + (r0 - lb) + r;
+          const K128 key{(static_cast<unsigned long long>(u) << 32) | static_cast<unsigned long long>(uint32_t(p)),
+                         id};
+          if constexpr (!kFilter) {
+            keys[s_pos[qq] + (r0 - lb) + r] = key;
+          } else if (k_less(key, s_tau[qq])) {
+            const int64_t q = s_q[qq];
+            const int slot = atomicAdd(&ccnt[q], 1);
+            if (slot < cap) cand[q * cap + slot] = key;
+          }
+          continue;
+        }
+        double v = double(acc[t][i]) * -2.0;
         v += xn;
         v += s_yy[qq];
         v = fmax(v, 0.0);
@@ -1241,6 +1269,62 @@ __global__ void redo_scatter_kernel(const int32_t* __restrict__ redo, int64_t nr
     dd[q * k + j] = dr[i * k + j];
   }
   if (threadIdx.x == 0) co[q] = cr[i];
+}
+
+// IvfAnnIndex (ann.py:313-316): the fp32-ranked selection (row ids in `sel`, `cnt` per query)
+// re-evaluated in fp64 — (x64 . y) * -2 + |x|^2 + |y|^2 clamped at 0, the sequential fma chain of
+// pair_tile_kernel — and ordered by (d2, row) like _smallest_k.  One block per query.
+__global__ void __launch_bounds__(128) ref32_finish_kernel(const float* __restrict__ X,
+                                                           const double* __restrict__ xn64, int32_t d,
+                                                           const double* __restrict__ Q,
+                                                           const double* __restrict__ yyq, int32_t k, int32_t P,
+                                                           const int64_t* __restrict__ sel,
+                                                           const int32_t* __restrict__ cnt,
+                                                           int64_t* __restrict__ io, double* __restrict__ dd,
+                                                           int32_t* __restrict__ co) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K128* buf = reinterpret_cast<K128*>(smem_raw);
+  const int64_t q = blockIdx.x;
+  const int c = cnt[q];
+  const double* y = Q + size_t(q) * d;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    K128 key{~0ull, ~0ull};
+    if (i < c) {
+      const int64_t row = sel[size_t(q) * k + i];
+      const float* x = X + size_t(row) * d;
+      double dot = 0.0;
+      for (int j = 0; j < d; ++j) dot = fma(double(x[j]), y[j], dot);
+      double v = dot * -2.0;
+      v += xn64[row];
+      v += yyq[q];
+      v = fmax(v, 0.0);
+      key = K128{static_cast<unsigned long long>(__double_as_longlong(v)), static_cast<unsigned long long>(row)};
+    }
+    buf[i] = key;
+  }
+  for (int kk = 2; kk <= P; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & kk) == 0;
+          const K128 a = buf[i], b = buf[ixj];
+          if (k_less(b, a) == up) {
+            buf[i] = b;
+            buf[ixj] = a;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const bool ok = i < c;
+    io[size_t(q) * k + i] = ok ? int64_t(buf[i].lo) : -1;
+    dd[size_t(q) * k + i] = ok ? __longlong_as_double(static_cast<long long>(buf[i].hi)) : __longlong_as_double(0x7ff0000000000000ll);
+  }
+  if (threadIdx.x == 0) co[q] = c;
 }
 
 size_t cub_bytes(int64_t n) {
@@ -1610,6 +1694,12 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
     const int64_t npairs = nq * int64_t(n_probe);
     const int32_t NBK = 2 * v->C + 2;  // pair buckets: phase-1 lists, a gap, phase-2 lists
     const bool two_phase = !bigk && !one_phase && npairs < (int64_t(1) << 31);
+    // IvfAnnIndex (formula 1) ranks the probed rows in fp32 like the reference (ann.py:294-312):
+    // the two-phase pass over (fp32 key, probe position) keys — the k smallest per query — then
+    // the fp64 re-evaluation of those (ref32_finish_kernel).  DK_IVF_EXACT_RANK=1: exact fp64
+    // ranking instead (differs only at fp32 near-ties).
+    static const bool exact_rank = std::getenv("DK_IVF_EXACT_RANK") != nullptr;
+    const bool ref32 = formula == 1 && two_phase && !exact_rank;
     int64_t cap_rows = std::max<int64_t>(2048, 16 * int64_t(k));
     if (const char* e = std::getenv("DK_IVF_CAP")) cap_rows = std::max<int64_t>(1, std::atoll(e));  // tests
     const int32_t cap = int32_t(std::min<int64_t>(int64_t(1) << 20, cap_rows));
@@ -1831,9 +1921,16 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       }
       auto* keys1 = static_cast<K128*>(v->keys1);
       // (2) every key of the leading lists, then the exact top-k of each query -> tau_q
-      if (items1 > 0)
-        pair_tile_kernel<0><<<unsigned(items1), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe, n_probe,
-                                               vout, ps, is, 0, v->C, span, qoff, keys1, nullptr, 0, nullptr, nullptr);
+      if (items1 > 0) {
+        if (ref32)
+          pair_tile_kernel<2><<<unsigned(items1), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd,
+                                                               yyq, probe, n_probe, vout, ps, is, 0, v->C, span, qoff,
+                                                               keys1, nullptr, 0, nullptr, nullptr);
+        else
+          pair_tile_kernel<0><<<unsigned(items1), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd,
+                                                               yyq, probe, n_probe, vout, ps, is, 0, v->C, span, qoff,
+                                                               keys1, nullptr, 0, nullptr, nullptr);
+      }
       DK_CHECK_LAUNCH();
       const size_t tsm = size_t(NB) * sizeof(K128);
       set_dynamic_smem(seg_topk_kernel, tsm);
@@ -1843,7 +1940,12 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
       // (3) the remaining pairs: keys below tau_q into the query's candidate buffer
       DK_CUDA(cudaMemsetAsync(ccnt, 0, size_t(nq) * 4, s));
       static const bool f64_filter = std::getenv("DK_IVF_F64_FILTER") != nullptr;  // A/B switch
-      if (f64_filter) {
+      if (ref32) {
+        if (items2 > 0)
+          pair_tile_kernel<3><<<unsigned(items2), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd,
+                                                               yyq, probe, n_probe, vout, ps, is, v->C + 1, NBK - 1,
+                                                               span, nullptr, nullptr, tau, cap, cand, ccnt);
+      } else if (f64_filter) {
         if (items2 > 0)
           pair_tile_kernel<1><<<unsigned(items2), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qd, yyq, probe,
                                                  n_probe, vout, ps, is, v->C + 1, NBK - 1, span, nullptr, nullptr, tau, cap,
@@ -1927,10 +2029,16 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
           v->keys1_bytes = rbytes;
         }
         auto* keysr = static_cast<K128*>(v->keys1);
-        if (itemsr > 0)
-          pair_tile_kernel<0><<<unsigned(itemsr), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qr,
-                                                               yyq, pr, n_probe, vout, ps, is, 0, v->C, 256, qoff, keysr,
-                                                               nullptr, 0, nullptr, nullptr);
+        if (itemsr > 0) {
+          if (ref32)
+            pair_tile_kernel<2><<<unsigned(itemsr), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qr,
+                                                                 yyq, pr, n_probe, vout, ps, is, 0, v->C, 256, qoff,
+                                                                 keysr, nullptr, 0, nullptr, nullptr);
+          else
+            pair_tile_kernel<0><<<unsigned(itemsr), 128, 0, s>>>(v->xs, v->xns, v->rows, v->offsets, v->d, v->C, Qr,
+                                                                 yyq, pr, n_probe, vout, ps, is, 0, v->C, 256, qoff,
+                                                                 keysr, nullptr, 0, nullptr, nullptr);
+        }
         DK_CHECK_LAUNCH();
         seg_topk_kernel<<<unsigned(nr), 256, tsm, s>>>(nullptr, nullptr, nullptr, keysr, qoff, 0, nullptr, 0, NB, k,
                                                        nullptr, idx1, d21, cnt1, nullptr, nullptr);
@@ -1939,6 +2047,16 @@ dk_status dk_ivf_query(dk_ivf_handle v, const double* Q, int64_t nq, int32_t k, 
         DK_CHECK_LAUNCH();
       }
     }
+    }
+    if (ref32) {  // the fp32-ranked selection re-evaluated in fp64 and ordered by (d2, row)
+      int P = 2;
+      while (P < k) P <<= 1;
+      const size_t fsm = size_t(P) * sizeof(K128);
+      set_dynamic_smem(ref32_finish_kernel, fsm);
+      ref32_finish_kernel<<<unsigned(nq), 128, fsm, s>>>(h->X, h->xn64, v->d, Qd,
+                                                         reinterpret_cast<double*>(base + o_yy), k, P, io, co, io, dd,
+                                                         co);
+      DK_CHECK_LAUNCH();
     }
     if (!idev) DK_CUDA(cudaMemcpyAsync(idx_out, io, size_t(nq) * k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     if (!ddev) DK_CUDA(cudaMemcpyAsync(d2_out, dd, size_t(nq) * k * sizeof(double), cudaMemcpyDeviceToHost, s));

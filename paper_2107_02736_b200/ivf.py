@@ -11,12 +11,15 @@ Mirrors reference ann.py:124-352: ``IvfIndex``, ``ivf_build``, ``ivf_query``,
   (csrc/ivf.cu): the D^2 updates, the cumulative-probability search, the Lloyd
   assignment (fp64, ties to the lower centroid), the sequential member means and
   the final inverted lists.
-* ``ivf_query`` / ``IvfAnnIndex.query`` / ``query_batch`` probe the n_probe
-  nearest centroids ((d2, id) order) and return the exact k smallest
-  d2 = ((x.y) * -2 + |x|^2) + |y|^2 among their members, (d2, row) order.
-  ``IvfAnnIndex`` ranks candidates in fp64 where the reference ranks them in
-  fp32 before its fp64 re-evaluation (ann.py:294-316); the two agree except when
-  fp32 rounding reorders rows at the k-th boundary, where this one is exact.
+* ``ivf_query`` probes the n_probe nearest centroids ((d2, id) order) and returns
+  the exact k smallest d2 = ((x.y) * -2 + |x|^2) + |y|^2 among their members,
+  (d2, row) order (ann.py:204-230).
+* ``IvfAnnIndex.query`` / ``query_batch`` keep the reference's two-step semantics
+  (ann.py:276-316): the probed rows are ranked in SINGLE precision — key
+  norms32 - 2 (x32 . fl32(y)), ties in the order of the probe concatenation (the
+  reference's stable argsort) — and the k selected rows are re-evaluated in fp64 and
+  ordered by (d2, row).  Pinned by reference goldens with engineered fp32 near-ties
+  (tests/test_gpu_ivf.py); ``DK_IVF_EXACT_RANK=1`` selects exact fp64 ranking instead.
 """
 
 from __future__ import annotations

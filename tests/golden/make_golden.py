@@ -204,6 +204,33 @@ def main():
                 deann.save_ivf_index(index, p)
                 out["ivf_a_file"] = np.frombuffer(open(p, "rb").read(), np.uint8).copy()
 
+    # --- IvfAnnIndex fp32-ranking semantics (ann.py:276-316) on engineered near-ties: integer rows
+    # with |x|^2 > 2^24, so the fp32 keys norms32 - 2 dot collide for rows whose exact (fp64)
+    # distances differ by 1 (norms32 rounds to even) while every fp32 / fp64 operation stays exact
+    # in any summation order; the reference then selects by list position among equal fp32 keys
+    # where exact ranking would select by distance.  Inputs and the reference's answers.
+    for tag, (n, d, C, seed) in {"ivf_t1": (600, 4, 8, 11), "ivf_t2": (3000, 6, 24, 12)}.items():
+        rng = np.random.default_rng(seed)
+        X = rng.integers(0, 6, size=(n, d)).astype(np.float32)
+        X[:, 0] = rng.integers(5000, 5040, size=n)
+        Q = rng.integers(0, 4, size=(12, d)).astype(np.float64)
+        ds = deann.Dataset.from_array(X)
+        index = deann.ivf_build(ds, C, seed=seed)
+        out[f"{tag}_X"], out[f"{tag}_Q"] = X, Q
+        out[f"{tag}_cent"] = index.centroids.copy()
+        out[f"{tag}_rows"] = np.concatenate(index.assignments).astype(np.int64)
+        out[f"{tag}_off"] = np.concatenate([[0], np.cumsum([len(a) for a in index.assignments])]).astype(np.int64)
+        probes = [1, 3, C]
+        ai, ad = [], []
+        for p_ in probes:
+            ann = deann.IvfAnnIndex(ds, index, p_)
+            for q in Q:
+                nl = ann.query(q, 10)
+                ai.append(np.pad(nl.indices, (0, 10 - len(nl)), constant_values=-1))
+                ad.append(np.pad(nl.sq_distances, (0, 10 - len(nl)), constant_values=np.inf))
+        out[f"{tag}_probes"] = np.array(probes)
+        out[f"{tag}_ann_idx"], out[f"{tag}_ann_d2"] = np.array(ai), np.array(ad)
+
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", os.path.join(HERE, "reference_golden.npz"), len(out), "arrays")
 

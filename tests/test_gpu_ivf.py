@@ -316,3 +316,28 @@ def test_deann_with_short_ivf_lists(family, h, m):
         assert batch[j].neighbors_used == len(ri)
         assert batch[j].samples_used == m
         assert batch[j].value == pytest.approx(ref[0], rel=1e-12)
+
+
+@pytest.mark.parametrize("tag", ["ivf_t1", "ivf_t2"])
+def test_ivf_ann_index_fp32_ranking_near_ties(golden, tag):
+    """IvfAnnIndex ranks the probed rows in fp32 by (key, probe position) before its fp64
+    re-evaluation (ann.py:294-316).  On the engineered fp32 near-ties of the goldens (integer rows
+    with |x|^2 > 2^24: fp32 keys collide for rows whose exact distances differ) the GPU equals the
+    reference's own answers — batch and per-query calls — where exact ranking would not."""
+    X, Q = golden[f"{tag}_X"], golden[f"{tag}_Q"]
+    ds = g.Dataset.from_array(X)
+    index = g.ivf_build(ds, len(golden[f"{tag}_cent"]), int(tag[-1]) + 10)
+    rows, off = golden[f"{tag}_rows"], golden[f"{tag}_off"]
+    for c in range(len(index.assignments)):
+        np.testing.assert_array_equal(index.assignments[c], rows[off[c]:off[c + 1]])
+    i = 0
+    for p in golden[f"{tag}_probes"]:
+        ann = g.IvfAnnIndex(ds, index, int(p))
+        bi, bd, bc = ann.query_batch(Q, 10)
+        for j, q in enumerate(Q):
+            gi, gd = golden[f"{tag}_ann_idx"][i], golden[f"{tag}_ann_d2"][i]
+            np.testing.assert_array_equal(bi[j, :bc[j]], gi[gi >= 0])
+            np.testing.assert_array_equal(bd[j, :bc[j]], gd[gi >= 0])
+            nl = ann.query(q, 10)
+            np.testing.assert_array_equal(nl.indices, gi[gi >= 0])
+            i += 1

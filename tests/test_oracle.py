@@ -208,3 +208,25 @@ def test_oracle_ivf_matches_reference_goldens(golden, tag, n, d, C, seed):
                 np.testing.assert_array_equal(idx, gi[gi >= 0])
                 np.testing.assert_allclose(d2, gd[gi >= 0], rtol=1e-12 if formula else 0)
             i += 1
+
+
+def test_ivf_ann_index_fp32_ranking_pinned(golden):
+    """The oracle's IvfAnnIndex restatement (fp32 ranking by (key, probe position), fp64
+    re-evaluation; ann.py:276-316) equals the reference on engineered fp32 near-ties, where an
+    exact (fp64) ranking of the same probed rows picks different neighbours."""
+    differs = 0
+    for tag in ("ivf_t1", "ivf_t2"):
+        X, Q = golden[f"{tag}_X"], golden[f"{tag}_Q"]
+        od = O.Data(X)
+        cent, rows, off = golden[f"{tag}_cent"], golden[f"{tag}_rows"], golden[f"{tag}_off"]
+        lists = [rows[off[c]:off[c + 1]] for c in range(len(cent))]
+        i = 0
+        for p in golden[f"{tag}_probes"]:
+            for q in Q:
+                ri, rd = O.ivf_ann_query(od, cent, lists, q, 10, int(p))
+                np.testing.assert_array_equal(ri, golden[f"{tag}_ann_idx"][i][:len(ri)])
+                np.testing.assert_array_equal(rd, golden[f"{tag}_ann_d2"][i][:len(rd)])
+                fi, _ = O.ivf_query(od, cent, lists, q, 10, int(p), formula=1)
+                differs += not np.array_equal(fi, ri)
+                i += 1
+    assert differs > 0  # the cases do exercise the fp32 tie order
