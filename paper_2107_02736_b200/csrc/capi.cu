@@ -694,6 +694,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
         a.nunits_dev = uplan;
         a.tmajor = tmajor ? 1 : 0;
         a.blist = tmajor ? at<int32_t>(h->ws, L.blist) : nullptr;
+        a.unit_counter = tmajor ? ctr + 12 : nullptr;  // zeroed with ctr at the batch start
       }
       // work of the tiles actually swept (all of them unless pruned; the pruned count is read
       // back below only when profiling)

@@ -260,6 +260,7 @@ struct SweepArgs {
   // tile-major FILTER: unit u = (dataset tile ulist[3u], query blocks blist[ulist[3u+1] .. ulist[3u+2]))
   int32_t tmajor;
   const int32_t* blist;
+  int32_t* unit_counter;  // tile-major: dynamic unit claims (zeroed by the caller)
 };
 // tile-major FILTER fits when the resident dataset tile (kblocks x 32 KB) leaves a >= 3-stage ring
 bool tile_major_fits(int32_t Kp);

@@ -232,6 +232,8 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.hist = a.hist;
   p.tmajor = tmajor ? 1 : 0;
   p.blist = a.blist;
+  p.unit_counter = a.unit_counter;
+  if (tmajor && a.unit_counter == nullptr) throw Error{DK_EINVAL, "internal: tile-major sweeps need a unit counter"};
   p.guard = a.guard;
   if (a.ncc_out) *a.ncc_out = pl.ncc;
 

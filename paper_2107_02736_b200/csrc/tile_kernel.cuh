@@ -75,6 +75,7 @@ constexpr int kColGroups = 4;      // 64-column groups per tile (one per epilogu
 constexpr int kXnSlots = 4;        // column-norm staging ring (1 KB per tile)
 constexpr uint32_t kTmemCols = 512;  // 2 accumulator buffers x 256 fp32 columns
 constexpr int kStageCap = 32;      // FILTER: per-row smem candidate staging (entries)
+constexpr int kUnitSlots = 4;      // tile-major: ring of claimed unit ids (producer -> MMA / epilogue)
 
 struct TileParams {
   int32_t nq;              // valid query rows
@@ -101,6 +102,7 @@ struct TileParams {
   int32_t tmajor;
   const int32_t* blist;
   const int32_t* nunits_dev;
+  int32_t* unit_counter;   // tile-major: units are claimed dynamically (atomicAdd), zeroed per launch
   int32_t list_stride;     // TILEMIN over per-block tile lists: segment = (list position) x 64-column group
   // MODE_HIST: per query row, bins b = floor(64 sqrt((d2 - hlo) * hinv)) for d2 <= htop, counted into
   // hist[row][64] (shared-memory counts flushed with global atomics per work unit)
@@ -377,6 +379,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* xfull_bar = aempty_bar + 1;      // [kXnSlots]
   uint64_t* xempty_bar = xfull_bar + kXnSlots;  // [kXnSlots]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty_bar + kXnSlots);
+  uint64_t* ufull_bar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kUnitSlots] (tile-major)
+  uint64_t* uempty_bar = ufull_bar + kUnitSlots;                     // [kUnitSlots]
+  int32_t* s_unit = reinterpret_cast<int32_t*>(uempty_bar + kUnitSlots);  // [kUnitSlots]
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
@@ -404,6 +409,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int x = 0; x < kXnSlots; ++x) {
       mbar_init(&xfull_bar[x], 1);
       mbar_init(&xempty_bar[x], kPP ? kNumEpiWarps / 2 : kNumEpiWarps);
+    }
+    if (tmajor) {
+      for (int x = 0; x < kUnitSlots; ++x) {
+        mbar_init(&ufull_bar[x], 1);
+        mbar_init(&uempty_bar[x], 1 + kNumEpiWarps);  // the MMA thread and every epilogue warp
+      }
     }
     fence_mbar_init();
   }
@@ -440,7 +451,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int uiter = 0;
       uint32_t titer = 0;
-      for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
+      // units are claimed dynamically (they differ in length: 1..many query blocks per tile) and
+      // published to the MMA / epilogue warps through a small ring; -1 ends the sweep
+      int uslot = 0;
+      uint32_t uph = 0;
+      for (;; ++uiter) {
+        int u = atomicAdd(p.unit_counter, 1);
+        if (u >= nunits) u = -1;
+        mbar_wait(&uempty_bar[uslot], uph ^ 1);
+        s_unit[uslot] = u;
+        mbar_arrive(&ufull_bar[uslot]);
+        if (++uslot == kUnitSlots) { uslot = 0; uph ^= 1; }
+        if (u < 0) break;
         const int col0 = __ldg(p.ulist + 3 * u) * kBN;
         const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
         DK_DCHECK(col0 >= 0 && col0 < p.n && i0 <= i1);
@@ -539,7 +561,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       int uiter = 0;
       const uint32_t a0 = smem_u32(smemA), b0 = smem_u32(smemB);
-      for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
+      int uslot = 0;
+      uint32_t uph = 0;
+      for (;; ++uiter) {
+        mbar_wait(&ufull_bar[uslot], uph);
+        const int u = s_unit[uslot];
+        mbar_arrive(&uempty_bar[uslot]);
+        if (++uslot == kUnitSlots) { uslot = 0; uph ^= 1; }
+        if (u < 0) break;
         const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
         mbar_wait(afull_bar, uiter & 1);
         tc_fence_after();
@@ -685,7 +714,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t titer = 0;
       const float m2s = *p.m2s;
       float mn_unused = 0.f;
-      for (int u = first_unit; u < nunits; u += unit_step) {
+      int uslot = 0;
+      uint32_t uph = 0;
+      for (;;) {
+        mbar_wait(&ufull_bar[uslot], uph);
+        const int u = s_unit[uslot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&uempty_bar[uslot]);
+        if (++uslot == kUnitSlots) { uslot = 0; uph ^= 1; }
+        if (u < 0) break;
         const int64_t cbase = int64_t(__ldg(p.ulist + 3 * u)) * kBN + cg * 64;
         const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
         const bool full = cbase + 64 <= p.n;
