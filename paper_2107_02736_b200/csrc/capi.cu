@@ -565,11 +565,18 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
         a.seg_tiles = seg_tiles;
         a.tmin = tmin;
         launch_sweep(a, h->num_sms, s);
-        launch_tau_from_tmin(tmin, nseg_g, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau, s);
+        // the global pass also sets each query's histogram range for (b): [min, k-th] of its
+        // segment minima
+        launch_tau_from_tmin(tmin, nseg_g, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau, s, nullptr, 0,
+                             at<float>(h->ws, L.hlo), at<float>(h->ws, L.hinv), at<float>(h->ws, L.htop));
       }
-      // (b) threshold from the block's own neighbourhood: 32-column segment minima over every hS-th
-      // tile and the tiles of the balls nearest to the block's queries (tens to hundreds of tiles
-      // per block instead of a quarter of the dataset); tau_q = k-th smallest + 2 eps_q as before
+      // (b) threshold from the block's own neighbourhood: per block of 128 ball-sorted queries a
+      // list of tiles — every hS-th tile and the tiles of the balls nearest to the block's
+      // queries and their neighbour balls (tens to hundreds of tiles instead of a quarter of the
+      // dataset) — swept once in MODE_HIST: each query's approx d2 of the listed rows counted
+      // into 64 quadratic bins over the range of (a); the bin where the count reaches k bounds
+      // the k-th distance (k distinct rows below its edge).  Segment minima of the same lists
+      // sit far above the k-th distance in high dimension (c5), the row histogram does not.
       int32_t* hl = at<int32_t>(h->ws, L.hlist);
       int32_t* hc = at<int32_t>(h->ws, L.hcnt);
       int32_t* hplan = ctr + 8;  // [0] units, [1] listed (block, tile) pairs, [2] U
@@ -577,33 +584,11 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
                              int64_t(L.hneed) * kBN, L.hmax, L.hlmax, hl, hc, s);
       launch_block_units(hc, nqb, L.hlmax, h->num_sms, at<int32_t>(h->ws, L.tstart), at<int32_t>(h->ws, L.ustart),
                          hplan, at<int32_t>(h->ws, L.ulist), int64_t(L.ulist_ints / 3), s);
-      float* tmin = at<float>(h->ws, L.tmin);
-      const int32_t nseg = L.hlmax * kListSegs;  // no fill: tau reads only the listed segments
-      SweepArgs a{};
-      a.mode = MODE_TILEMIN;
-      a.qop = &q;
-      a.enc = &h->kc->enc;
-      a.n = h->n;
-      a.n_pad = h->n_pad;
-      a.tile_stride = 1;
-      a.seg_tiles = 0;
-      a.tmin = tmin;
-      a.ulist = at<int32_t>(h->ws, L.ulist);
-      a.tlist = hl;
-      a.nunits_dev = hplan;
-      a.list_stride = L.hlmax;
-      launch_sweep(a, h->num_sms, s);
       float* hlo = at<float>(h->ws, L.hlo);
       float* hinv = at<float>(h->ws, L.hinv);
       float* htop = at<float>(h->ws, L.htop);
       uint32_t* hist = at<uint32_t>(h->ws, L.hist);
-      float* tau_h = at<float>(h->ws, L.tauh);
-      launch_tau_from_tmin(tmin, nseg, bn_pad, bn, k, q.qn, e.xn_max, e.eps_rel, tau_h, s, hc, kListSegs, hlo, hinv,
-                           htop);
-      // refinement: a second listed sweep counts, per query, the approx d2 of the listed rows in
-      // 64 bins over [min segment minimum, k-th segment minimum]; the bin where the count reaches
-      // k gives a tighter (still valid) tau_q — segment minima alone sit well above the k-th
-      // distance when few segments are near (high dimension, small balls)
+      float* tau_h = tau;  // the histogram bound tightens the global one
       DK_CUDA(cudaMemsetAsync(hist, 0, size_t(bn) * kHistBins * sizeof(uint32_t), s));
       {
         SweepArgs b{};
