@@ -512,8 +512,12 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
   const char* home_env = std::getenv("DK_KNN_HOME");
   const int64_t home_target = std::clamp<int64_t>(4 * int64_t(k), 256, 2048);
   const bool home_tau = home_env != nullptr ? std::atoi(home_env) != 0 : int64_t(ntiles) >= 32 * home_target;
-  for (int64_t b0 = 0; b0 < nq; b0 += bpad) {
-    const int64_t bn = std::min<int64_t>(bpad, nq - b0);
+  // equal batches (a call of 16,384 queries is not 15,872 + 512): a small remainder batch sweeps
+  // a large fraction of the tiles (its blocks span many balls) and would skew the pruning statistic
+  const int64_t nbatch = (nq + bpad - 1) / bpad;
+  const int64_t bstep = std::min<int64_t>(bpad, round_up((nq + nbatch - 1) / nbatch, 2 * kBM));
+  for (int64_t b0 = 0; b0 < nq; b0 += bstep) {
+    const int64_t bn = std::min<int64_t>(bstep, nq - b0);
     const int32_t bn_pad = int32_t(query_pad(bn));
     const int32_t nqb = bn_pad / kBM;
     const double* Qb = Qd + b0 * h->d;
@@ -697,7 +701,7 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
                      tmajor ? "tile-major" : "block-major", act, (long long)nqb * ntiles,
                      100.0 * double(act) / (double(nqb) * ntiles), int(h->kc->C));
     }
-    if (prune && b0 + bpad >= nq) {  // the swept fraction of the call's last batch, read next call
+    if (prune && b0 == 0) {  // the swept fraction of the call's first (largest) batch, read next call
       DK_CUDA(cudaMemcpyAsync(h->kc->stat_host, uplan + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaEventRecord(h->kc->stat_ev, s));
       h->kc->stat_total = double(nqb) * double(ntiles);
