@@ -275,6 +275,11 @@ dk_status dk_set_profiling(dk_handle h, int32_t on);
  * candidates per query, queries that took the exact-scan fallback. */
 dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t* cand_max,
                        int64_t* fallbacks);
+/* Exact-KDE diagnostics of this handle's two-precision path (dk_naive, gaussian, non-integer
+ * rows): queries it served, queries whose fp16 bound failed and were recomputed in split3, and
+ * the hot (query block, tile) pairs / all pairs of the last call's first batch (-1: not yet
+ * known).  No reference counterpart. */
+dk_status dk_kde_stats(dk_handle h, int64_t* queries, int64_t* fallbacks, int64_t* hot_pairs, int64_t* total_pairs);
 /* Diagnostics: time (ms, CUDA events) of one tile sweep of the given mode
  * (0 KDE-gauss, 1 KDE-exp, 2 segment-min, 3 filter, 4 null epilogue) with the
  * given operand encoding (0 exact, 1 split3, 2 fp16) — a pipeline probe. */

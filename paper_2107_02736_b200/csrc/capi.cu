@@ -738,6 +738,308 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
 }
 
 
+// ------------------------------------------------------------------ two-precision exact KDE
+// Exact gaussian KDE of non-integer data (hybrid.cu): the single-pass fp16 sweep over the
+// cluster-sorted rows (the k-NN operand) for every pair, the split3 sweep only over the (query
+// block, tile) pairs holding a tile half whose fp16 kernel sum exceeds kHybHotThr, an a-posteriori
+// bound per query (fp16 part) checked against kHybTol, exact split3 recomputation of the queries
+// that fail it.  Used for gaussian batches of >= kHybMinQueries on datasets of >= kPruneMinTiles
+// tiles under DK_PREC_AUTO; DK_KDE_HYBRID=0 turns it off, =1 forces it (read per call).
+constexpr int64_t kHybMinQueries = 2048;
+constexpr float kHybHotThr = 2.44140625e-04f;  // 2^-12 per 128-column half (kernel values in (0, 1])
+constexpr double kHybTol = 2e-6;                  // relative bound of the fp16 part
+constexpr double kHybUseless = 0.25;              // hot (block, tile) fraction above which it does not pay
+
+double env_double(const char* name, double def) {
+  const char* v = std::getenv(name);
+  return v ? std::atof(v) : def;
+}
+
+int hyb_env() {  // -1 auto, 0 off, 1 forced
+  const char* v = std::getenv("DK_KDE_HYBRID");
+  return v ? (std::atoi(v) != 0 ? 1 : 0) : -1;
+}
+
+bool hyb_eligible(const dk_dataset* h, int32_t family, int64_t nq) {
+  const int mode = hyb_env();
+  if (mode == 0 || family != DK_GAUSSIAN || h->precision != DK_PREC_AUTO || h->int_exact || h->kc_failed) return false;
+  if (h->n_pad / kBN < kPruneMinTiles || (h->kc != nullptr && h->kc->hyb_failed)) return false;
+  return mode == 1 || nq >= kHybMinQueries;
+}
+
+// the hot fraction of earlier calls, read without waiting (like knn_prune_decide)
+bool hyb_decide(dk_dataset* h) {
+  KnnClusters* kc = h->kc;
+  if (kc == nullptr || hyb_env() == 1) return true;
+  if (kc->hyb_stat_pending) {
+    const cudaError_t q = cudaEventQuery(kc->hyb_stat_ev);
+    if (q == cudaSuccess) {
+      kc->hyb_stat_pending = false;
+      const bool wide = double(kc->hyb_stat_host[0]) > kHybUseless * kc->hyb_stat_total;
+      if (wide) {
+        kc->hyb_useless = true;
+        kc->hyb_off_calls = 0;
+      }
+    } else if (q == cudaErrorNotReady) {
+      (void)cudaGetLastError();
+    } else {
+      DK_CUDA(q);
+    }
+  }
+  if (kc->hyb_useless) {
+    if (++kc->hyb_off_calls < 32) return false;
+    kc->hyb_useless = false;
+    kc->hyb_off_calls = 0;
+  }
+  return true;
+}
+
+// split3 operand of the cluster-sorted rows (first hybrid call); false when it does not fit
+bool ensure_sorted_split3(dk_dataset* h, cudaStream_t s) {
+  KnnClusters* kc = h->kc;
+  if (kc->enc3.mode == 1) return true;
+  if (kc->hyb_failed) return false;
+  const int32_t d = h->d;
+  const int32_t Kp = int32_t(round_up(3 * int64_t(d), kBK));
+  {
+    size_t free_b = 0, total_b = 0;
+    DK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (double(free_b) < double(h->n_pad) * (2.0 * Kp + 8.0) * 1.1 + double(64 << 20)) {
+      kc->hyb_failed = true;
+      return false;
+    }
+  }
+  ensure_mu(h, s);
+  Encoding& e = kc->enc3;
+  try {
+    DK_CUDA(cudaMalloc(&e.B, size_t(h->n_pad) * Kp * sizeof(__half)));
+    DK_CUDA(cudaMalloc(&e.xn, size_t(h->n_pad) * sizeof(float)));
+    DK_CUDA(cudaMalloc(&e.sx, 2 * sizeof(float)));
+    if (!kc->hyb_stat_host) {
+      DK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&kc->hyb_stat_host), 4 * sizeof(int32_t), cudaHostAllocDefault));
+      DK_CUDA(cudaEventCreateWithFlags(&kc->hyb_stat_ev, cudaEventDisableTiming));
+    }
+  } catch (const Error& err) {
+    for (void* p : {static_cast<void*>(e.B), static_cast<void*>(e.xn), static_cast<void*>(e.sx)})
+      if (p) cudaFree(p);
+    e = Encoding{};
+    cudaGetLastError();
+    if (err.code != DK_ENOMEM) throw;
+    kc->hyb_failed = true;
+    return false;
+  }
+  e.Kp = Kp;
+  e.d = d;
+  e.mu = h->mu;
+  launch_encode_rows(kc->xs, h->n, h->n_pad, d, 1, e.mu, Kp, e.B, e.xn, e.sx, reinterpret_cast<uint32_t*>(e.sx + 1),
+                     s);
+  e.xn_max = kc->enc.xn_max;
+  e.eps_rel = float(1.01 * (4.0 * std::ldexp(1.0, -22) + double(Kp + 4) * std::ldexp(1.0, -24)));
+  e.tmap = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(Kp), uint32_t(kBN));
+  e.tmap_half = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(Kp), uint32_t(kBN / 2));
+  e.mode = 1;
+  return true;
+}
+
+// whether this call runs two-precision (builds the sorted rows and their split3 operand once)
+bool hyb_prepare(dk_dataset* h, int32_t family, int64_t nq_chunk_min, cudaStream_t s) {
+  if (!hyb_eligible(h, family, nq_chunk_min) || !hyb_decide(h)) return false;
+  const Encoding& e = ensure_encoding(h, 2, s);
+  if (!ensure_knn_clusters(h, e, s)) return false;
+  return ensure_sorted_split3(h, s);
+}
+
+struct HybLayout {
+  size_t dq, near, near_s, iota, qperm, sort_tmp, qs, A16, qn16, sc16, A3, qn3, sc3, part, bits, tlist, tcnt, ubeg,
+      ucnt, ulist, phot, ctr, fail, fv;
+  size_t sort_tmp_bytes = 0, end = 0;
+  int32_t bpad = 0;
+};
+
+HybLayout hyb_layout(const dk_dataset* h, int64_t nq, size_t base) {
+  HybLayout L{};
+  Plan pl;
+  pl.off = base;
+  int64_t bmax = 16384;
+  if (const char* v = std::getenv("DK_HYB_BATCH")) bmax = std::max<int64_t>(2 * kBM, round_up(std::atoll(v), 2 * kBM));
+  L.bpad = int32_t(std::min<int64_t>(bmax, query_pad(nq)));
+  const int32_t bpad = L.bpad, nqb = bpad / kBM, ntiles = int32_t(h->n_pad / kBN);
+  const int32_t C = knn_cluster_count(h);
+  const int32_t Kp16 = int32_t(round_up(h->d, kBK)), Kp3 = int32_t(round_up(3 * int64_t(h->d), kBK));
+  L.dq = pl.add<double>(size_t(bpad) * C);
+  L.near = pl.add<int32_t>(bpad);
+  L.near_s = pl.add<int32_t>(bpad);
+  L.iota = pl.add<int32_t>(bpad);
+  L.qperm = pl.add<int32_t>(bpad);
+  L.sort_tmp_bytes = ball_sort_temp_bytes(bpad);
+  L.sort_tmp = pl.add<uint8_t>(L.sort_tmp_bytes);
+  L.qs = pl.add<double>(size_t(bpad) * h->d);
+  L.A16 = pl.add<__half>(size_t(bpad) * Kp16);
+  L.qn16 = pl.add<float>(bpad);
+  L.sc16 = pl.add<float>(4);
+  L.A3 = pl.add<__half>(size_t(bpad) * Kp3);
+  L.qn3 = pl.add<float>(bpad);
+  L.sc3 = pl.add<float>(4);
+  L.part = pl.add<double>(std::max(sweep_part_count(h->n_pad, bpad, h->num_sms, false),
+                                   sweep_part_count(h->n_pad, bpad, h->num_sms, true)));
+  L.bits = pl.add<uint32_t>(size_t(nqb) * ntiles * kHotWords);
+  L.tlist = pl.add<int32_t>(size_t(nqb) * ntiles);
+  L.tcnt = pl.add<int32_t>(nqb);
+  L.ubeg = pl.add<int32_t>(nqb);
+  L.ucnt = pl.add<int32_t>(nqb);
+  L.ulist = pl.add<int32_t>(size_t(3) * nqb * kHotUnitsPerBlock);
+  L.phot = pl.add<double>(size_t(nqb) * kHotUnitsPerBlock * kColGroups * kBM);
+  L.ctr = pl.add<int32_t>(16);
+  L.fail = pl.add<int32_t>(size_t(nq));
+  L.fv = pl.add<double>(bpad);
+  L.end = pl.off;
+  return L;
+}
+
+size_t hyb_ws_bytes(const dk_dataset* h, int64_t nq) { return hyb_layout(h, nq, 0).end + 4096; }
+
+// Two-precision exact gaussian KDE of nq device queries into od (device), means scaled by `scale`.
+// Enqueued without host waits except one read of the failure count at the end (and the fallback).
+void kde_hybrid(dk_dataset* h, const double* Qc, int64_t nq, double bw, double scale, double* od, cudaStream_t s,
+                size_t base) {
+  KnnClusters* kc = h->kc;
+  const HybLayout L = hyb_layout(h, nq, base);
+  if (L.end > h->ws.cap) throw Error{DK_ECUDA, "internal: hybrid KDE workspace under-reserved"};
+  const Encoding& e16 = kc->enc;
+  const Encoding& e3 = kc->enc3;
+  const double log2e = 1.4426950408889634;
+  const float negc = float(-log2e / (2.0 * bw * bw));
+  const double inv2h2 = 1.0 / (2.0 * bw * bw);
+  const float thr = float(env_double("DK_HYB_THR", kHybHotThr));
+  const double tol = env_double("DK_HYB_TOL", kHybTol);
+  const int32_t ntiles = int32_t(h->n_pad / kBN);
+  int32_t* ctr = at<int32_t>(h->ws, L.ctr);  // [0] failures, [4..5] split3 units / listed pairs
+  int32_t* fail = at<int32_t>(h->ws, L.fail);
+  DK_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), s));
+  int64_t rest = nq;  // queries from here on take the plain split3 sweep (early switch)
+  const int64_t nbatch = (nq + L.bpad - 1) / L.bpad;
+  const int64_t bstep = std::min<int64_t>(L.bpad, round_up((nq + nbatch - 1) / nbatch, 2 * kBM));
+  for (int64_t b0 = 0; b0 < nq; b0 += bstep) {
+    const int64_t bn = std::min<int64_t>(bstep, nq - b0);
+    const int32_t bn_pad = int32_t(query_pad(bn));
+    const int32_t nqb = bn_pad / kBM;
+    const double* Qb = Qc + b0 * h->d;
+    // ball-sorted batch: each block of 128 queries is local, so its hot tiles are few
+    int32_t* near = at<int32_t>(h->ws, L.near);
+    int32_t* qperm = at<int32_t>(h->ws, L.qperm);
+    launch_query_cluster_dist(Qb, bn, h->d, kc->cent, kc->C, at<double>(h->ws, L.dq), near, s);
+    launch_sort_queries_by_ball(near, bn, kc->C, at<int32_t>(h->ws, L.near_s), at<int32_t>(h->ws, L.iota), qperm,
+                                h->ws.base + L.sort_tmp, L.sort_tmp_bytes, s);
+    double* Qs = at<double>(h->ws, L.qs);
+    launch_gather_rows_f64(Qb, qperm, bn, h->d, Qs, s);
+    QueryOperand q16 = encode_queries(h, e16, Qs, bn, bn_pad, at<__half>(h->ws, L.A16), at<float>(h->ws, L.qn16),
+                                      at<float>(h->ws, L.sc16), s);
+    QueryOperand q3 = encode_queries(h, e3, Qs, bn, bn_pad, at<__half>(h->ws, L.A3), at<float>(h->ws, L.qn3),
+                                     at<float>(h->ws, L.sc3), s);
+    uint32_t* bits = at<uint32_t>(h->ws, L.bits);
+    int32_t ncc = 0;
+    {
+      SweepArgs a{};
+      a.mode = MODE_KDE_COLD;
+      a.qop = &q16;
+      a.enc = &e16;
+      a.n = h->n;
+      a.n_pad = h->n_pad;
+      a.tile_stride = 1;
+      a.negc = negc;
+      a.part = at<double>(h->ws, L.part);
+      a.ncc_out = &ncc;
+      a.hot_bits = bits;
+      a.hot_thr = thr;
+      ProfScope ps(h, s, 2.0 * double(h->d) * double(bn) * double(h->n), double(h->n_pad) * e16.Kp * 2, 1);
+      launch_sweep(a, h->num_sms, s);
+    }
+    int32_t* tlist = at<int32_t>(h->ws, L.tlist);
+    int32_t* tcnt = at<int32_t>(h->ws, L.tcnt);
+    int32_t* ubeg = at<int32_t>(h->ws, L.ubeg);
+    int32_t* ucnt = at<int32_t>(h->ws, L.ucnt);
+    int32_t* ulist = at<int32_t>(h->ws, L.ulist);
+    double* phot = at<double>(h->ws, L.phot);
+    launch_hot_lists(bits, nqb, ntiles, tlist, tcnt, s);
+    launch_hot_units(tcnt, nqb, ntiles, ubeg, ucnt, ctr + 4, ulist, s);
+    {
+      SweepArgs b{};
+      b.mode = MODE_KDE_HOT;
+      b.qop = &q3;
+      b.enc = &e3;
+      b.n = h->n;
+      b.n_pad = h->n_pad;
+      b.tile_stride = 1;
+      b.negc = negc;
+      b.part = phot;
+      b.hot_bits = bits;
+      b.ulist = ulist;
+      b.tlist = tlist;
+      b.nunits_dev = ctr + 4;
+      launch_sweep(b, h->num_sms, s);
+    }
+    launch_hyb_combine(at<double>(h->ws, L.part), ncc * kColGroups, bn_pad, bn, phot, ubeg, ucnt, q16.qn,
+                       e16.eps_rel, e16.xn_max, inv2h2, tol, scale, qperm, b0, od + b0, fail, ctr,
+                       nullptr, s);
+    if (b0 == 0) {  // hot (block, tile) pairs of the first batch, read at the next call
+      DK_CUDA(cudaMemcpyAsync(kc->hyb_stat_host, ctr + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      DK_CUDA(cudaEventRecord(kc->hyb_stat_ev, s));
+      kc->hyb_stat_total = double(nqb) * double(ntiles);
+      kc->hyb_stat_pending = true;
+      if (b0 + bn < nq && hyb_env() != 1) {
+        // a bandwidth that makes most pairs hot (a wide kernel: c5) costs 1 + 3 MMA passes: the
+        // rest of this call and the next 32 calls take the plain split3 sweep
+        DK_CUDA(cudaEventSynchronize(kc->hyb_stat_ev));
+        kc->hyb_stat_pending = false;
+        if (double(kc->hyb_stat_host[0]) > kHybUseless * kc->hyb_stat_total) {
+          kc->hyb_useless = true;
+          kc->hyb_off_calls = 0;
+          rest = b0 + bn;
+          break;
+        }
+      }
+    }
+  }
+  // queries whose fp16 bound failed (and the batches after an early switch): split3 sweeps over the
+  // sorted rows, gathered by index or a contiguous range
+  int32_t nf = 0;
+  DK_CUDA(cudaMemcpyAsync(&nf, ctr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  DK_CUDA(cudaStreamSynchronize(s));
+  h->hyb_queries += rest;
+  h->hyb_fallbacks += nf;
+  auto split3_rows = [&](const int32_t* idx, int64_t first, int64_t fn) {
+    const int32_t fpad = int32_t(query_pad(fn));
+    const double* Qf = Qc + first * h->d;
+    if (idx != nullptr) {
+      launch_gather_rows_f64(Qc, idx + first, fn, h->d, at<double>(h->ws, L.qs), s);
+      Qf = at<double>(h->ws, L.qs);
+    }
+    QueryOperand q = encode_queries(h, e3, Qf, fn, fpad, at<__half>(h->ws, L.A3), at<float>(h->ws, L.qn3),
+                                    at<float>(h->ws, L.sc3), s);
+    SweepArgs a{};
+    a.mode = MODE_KDE_GAUSS;
+    a.qop = &q;
+    a.enc = &e3;
+    a.n = h->n;
+    a.n_pad = h->n_pad;
+    a.tile_stride = 1;
+    a.negc = negc;
+    a.part = at<double>(h->ws, L.part);
+    int32_t ncc = 0;
+    a.ncc_out = &ncc;
+    launch_sweep(a, h->num_sms, s);
+    if (idx != nullptr) {
+      double* fv = at<double>(h->ws, L.fv);
+      launch_reduce_partials(a.part, ncc * kColGroups, fpad, fn, scale, fv, s);
+      launch_scatter_f64(fv, idx + first, fn, od, s);
+    } else {
+      launch_reduce_partials(a.part, ncc * kColGroups, fpad, fn, scale, od + first, s);
+    }
+  };
+  for (int64_t f0 = 0; f0 < nf; f0 += L.bpad) split3_rows(fail, f0, std::min<int64_t>(L.bpad, nf - f0));
+  for (int64_t r0 = rest; r0 < nq; r0 += L.bpad) split3_rows(nullptr, r0, std::min<int64_t>(L.bpad, nq - r0));
+}
+
 // ------------------------------------------------------------------ fit
 struct HandleDeleter {
   void operator()(dk_dataset* h) const { dk_free(h); }
@@ -1136,7 +1438,11 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       o_part[c] = pl.add<double>(sweep_part_count(h->n_pad, pad, h->num_sms));
       o_fl[c] = pl.add<uint32_t>(4);
     }
-    h->ws.reserve(pl.off);
+    // two-precision exact KDE (non-integer gaussian batches on large datasets): decided before the
+    // workspace is reserved (the first call builds the sorted rows' operands in their own memory)
+    const bool hyb = hyb_prepare(h, family, nq, s);
+    const size_t hyb_base = pl.off;
+    h->ws.reserve(pl.off + (hyb ? hyb_ws_bytes(h, std::max(c_cnt[0], c_cnt[1])) : 0));
     double* od = out_dev ? out : at<double>(h->ws, o_out);
     const double* Qd = Q;
     if (host_q) {
@@ -1193,6 +1499,11 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     };
     for (int c = 0; c < nchunks; ++c) {
       if (c == 1) DK_CUDA(cudaStreamWaitEvent(s, h->copy_done, 0));
+      if (hyb) {
+        kde_hybrid(h, Qd + size_t(c_beg[c]) * h->d, c_cnt[c], bandwidth, scale, od + c_beg[c], s, hyb_base);
+        if (!out_dev) copy_out(out + c_beg[c], od + c_beg[c], size_t(c_cnt[c]) * sizeof(double), s);
+        continue;
+      }
       if (h->precision == DK_PREC_AUTO && h->int_exact) {
         // Integer dataset: launch the exact-mode sweep without waiting for the query check.
         // The sweep reads the check's flags and skips itself for fractional queries; the host
@@ -1657,6 +1968,23 @@ dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t
     if (cand_sum) *cand_sum = h->knn_cand_sum;
     if (cand_max) *cand_max = h->knn_cand_max;
     if (fallbacks) *fallbacks = h->knn_fallbacks;
+  });
+}
+
+dk_status dk_kde_stats(dk_handle h, int64_t* queries, int64_t* fallbacks, int64_t* hot_pairs, int64_t* total_pairs) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr, "NULL handle");
+    DeviceGuard g(h->device);
+    if (queries) *queries = h->hyb_queries;
+    if (fallbacks) *fallbacks = h->hyb_fallbacks;
+    int64_t hot = -1, tot = -1;
+    if (h->kc != nullptr && h->kc->hyb_stat_host != nullptr && h->kc->hyb_stat_total > 0) {
+      DK_CUDA(cudaEventSynchronize(h->kc->hyb_stat_ev));
+      hot = h->kc->hyb_stat_host[0];
+      tot = int64_t(h->kc->hyb_stat_total);
+    }
+    if (hot_pairs) *hot_pairs = hot;
+    if (total_pairs) *total_pairs = tot;
   });
 }
 

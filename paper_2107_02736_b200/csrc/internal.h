@@ -146,6 +146,19 @@ struct KnnClusters {
   double stat_total = 0;         // (block, tile) pairs of that batch
   bool stat_pending = false;
   cudaEvent_t stat_ev = nullptr;
+  // two-precision exact KDE (capi.cu kde_hybrid): split3 operand of the sorted rows (same centring
+  // as the k-NN encoding), built on the first hybrid call; the hot fraction of each call's first
+  // batch is read back like the pruning statistic (at once when more batches follow), and a
+  // bandwidth that makes most (block, tile) pairs hot (a wide kernel: c5) turns the hybrid off for
+  // the rest of the call and the next 32 calls
+  Encoding enc3;
+  bool hyb_failed = false;     // the split3 copy did not fit in device memory
+  bool hyb_useless = false;
+  int hyb_off_calls = 0;
+  int32_t* hyb_stat_host = nullptr;  // pinned: [0] hot (block, tile) pairs of the last first batch
+  double hyb_stat_total = 0;
+  bool hyb_stat_pending = false;
+  cudaEvent_t hyb_stat_ev = nullptr;
 };
 
 // Growable device scratch, carved per call.
@@ -198,6 +211,7 @@ struct dk_dataset {
   bool kc_failed = false;          // the cluster build did not fit in device memory: unpruned sweeps
   bool knn_stats = false;
   int64_t knn_queries = 0, knn_cand_sum = 0, knn_cand_max = 0, knn_fallbacks = 0;
+  int64_t hyb_queries = 0, hyb_fallbacks = 0;  // two-precision exact KDE: queries served / recomputed in split3
 };
 
 namespace dk {
@@ -261,12 +275,28 @@ struct SweepArgs {
   int32_t tmajor;
   const int32_t* blist;
   int32_t* unit_counter;  // tile-major: dynamic unit claims (zeroed by the caller)
+  // two-precision exact KDE (MODE_KDE_COLD / MODE_KDE_HOT): [nqb][ntiles][8] hot lane masks
+  uint32_t* hot_bits;
+  float hot_thr;
 };
 // tile-major FILTER fits when the resident dataset tile (kblocks x 32 KB) leaves a >= 3-stage ring
 bool tile_major_fits(int32_t Kp);
-size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms);  // doubles needed for KDE partials
+// doubles needed for KDE partials (allow_pair = false: sweeps that never run as 2-CTA pairs)
+size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms, bool allow_pair = true);
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
 void set_pair_enabled(bool on);  // 2-CTA (cta_group::2) sweeps; off by default (DK_PAIR=1)
+
+// two-precision exact gaussian KDE (hybrid.cu)
+constexpr int32_t kHotUnitsPerBlock = 16;  // split3 work units per query block (partials: [units][4][128])
+void launch_hot_lists(const uint32_t* bits, int32_t nqb, int32_t ntiles, int32_t* tlist, int32_t* tcount,
+                      cudaStream_t s);
+void launch_hot_units(const int32_t* tcount, int32_t nqb, int32_t ntiles, int32_t* ubeg, int32_t* ucnt,
+                      int32_t* scal, int32_t* ulist, cudaStream_t s);
+void launch_hyb_combine(const double* part_cold, int32_t nparts, int32_t nq_pad, int64_t bn, const double* part_hot,
+                        const int32_t* ubeg, const int32_t* ucnt, const float* qn, float eps_rel, float xn_max,
+                        double inv2h2, double tol, double scale, const int32_t* qperm, int64_t qbase, double* out,
+                        int32_t* fail, int32_t* nfail, double* bound_out, cudaStream_t s);
+void launch_scatter_f64(const double* v, const int32_t* idx, int64_t n, double* out, cudaStream_t s);
 
 // L1 / laplacian exact KDE on CUDA cores
 size_t l1_part_count(int64_t n, int32_t nq);

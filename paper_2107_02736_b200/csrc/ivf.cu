@@ -1491,10 +1491,13 @@ void free_knn_clusters(KnnClusters& kc) {
                   static_cast<void*>(kc.xs), static_cast<void*>(kc.tclo), static_cast<void*>(kc.tchi),
                   static_cast<void*>(kc.off), static_cast<void*>(kc.nbr)})
     if (p) cudaFree(p);
-  for (void* p : {static_cast<void*>(kc.enc.B), static_cast<void*>(kc.enc.xn), static_cast<void*>(kc.enc.sx)})
+  for (void* p : {static_cast<void*>(kc.enc.B), static_cast<void*>(kc.enc.xn), static_cast<void*>(kc.enc.sx),
+                  static_cast<void*>(kc.enc3.B), static_cast<void*>(kc.enc3.xn), static_cast<void*>(kc.enc3.sx)})
     if (p) cudaFree(p);
   if (kc.stat_host) cudaFreeHost(kc.stat_host);
   if (kc.stat_ev) cudaEventDestroy(kc.stat_ev);
+  if (kc.hyb_stat_host) cudaFreeHost(kc.hyb_stat_host);
+  if (kc.hyb_stat_ev) cudaEventDestroy(kc.hyb_stat_ev);
   kc = KnnClusters{};
 }
 

@@ -165,10 +165,10 @@ bool tile_major_fits(int32_t Kp) {
 
 static bool use_pair(int nqb) { return g_pair_enabled && nqb >= 2 && nqb % 2 == 0; }
 
-size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms) {
+size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms, bool allow_pair) {
   const int ntiles = int(n_pad / kBN);
   const int nqb = nq_pad / kBM;
-  const bool pr = use_pair(nqb);
+  const bool pr = allow_pair && use_pair(nqb);
   const Plan pl = make_plan(1, ntiles, pr ? nqb / 2 : nqb, pr ? num_sms / 2 : num_sms, MODE_KDE_GAUSS, pr);
   return size_t(pl.ncc) * kColGroups * size_t(nq_pad);
 }
@@ -182,7 +182,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const int ntiles_all = int(a.n_pad / kBN);
   const int ntiles = (ntiles_all + a.tile_stride - 1) / a.tile_stride;
   const int nqb = q.nq_pad / kBM;
-  const bool pr = a.ulist == nullptr && use_pair(nqb);
+  const bool pr = a.ulist == nullptr && a.mode != MODE_KDE_COLD && use_pair(nqb);
   const int ngroups = pr ? nqb / 2 : nqb;
   const int nslots = pr ? num_sms / 2 : num_sms;  // CTAs (or CTA pairs) resident at once
   const bool tmajor = a.tmajor != 0;
@@ -230,6 +230,8 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.hinv = a.hinv;
   p.htop = a.htop;
   p.hist = a.hist;
+  p.hot_bits = a.hot_bits;
+  p.hot_thr = a.hot_thr;
   p.tmajor = tmajor ? 1 : 0;
   p.blist = a.blist;
   p.unit_counter = a.unit_counter;
@@ -240,8 +242,12 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   // a device-side unit count is unknown here: one CTA per SM, surplus CTAs find no unit
   const int nunits = a.ulist != nullptr ? (a.nunits_dev != nullptr ? nslots : a.nunits_list) : ngroups * pl.ncc;
   if (nunits <= 0) return;
-  if (a.ulist != nullptr && (pr || (a.mode != MODE_FILTER && a.mode != MODE_TILEMIN && a.mode != MODE_HIST)))
-    throw Error{DK_EINVAL, "internal: tile lists are k-NN sweeps only"};
+  if (a.ulist != nullptr &&
+      (pr || (a.mode != MODE_FILTER && a.mode != MODE_TILEMIN && a.mode != MODE_HIST && a.mode != MODE_KDE_HOT)))
+    throw Error{DK_EINVAL, "internal: tile lists are k-NN and two-precision KDE sweeps only"};
+  if ((a.mode == MODE_KDE_HOT && a.ulist == nullptr) ||
+      ((a.mode == MODE_KDE_HOT || a.mode == MODE_KDE_COLD) && a.hot_bits == nullptr))
+    throw Error{DK_EINVAL, "internal: two-precision KDE sweeps need a hot bitmap (and a list for the split3 pass)"};
   if (a.ulist != nullptr && a.mode == MODE_TILEMIN && a.seg_tiles != 0)
     throw Error{DK_EINVAL, "internal: listed TILEMIN sweeps use one segment per 64-column group"};
   const int grid = std::min(nunits, nslots) * (pr ? 2 : 1);
@@ -259,6 +265,8 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
     case MODE_TILEMIN: launch_any<MODE_TILEMIN>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_FILTER: launch_any<MODE_FILTER>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_NULL: launch_any<MODE_NULL>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_KDE_COLD: launch_mode<MODE_KDE_COLD, false>(q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_KDE_HOT: launch_mode<MODE_KDE_HOT, false>(q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_HIST:
       if (pr || a.ulist == nullptr) throw Error{DK_EINVAL, "internal: histogram sweeps are listed single-CTA sweeps"};
       launch_mode<MODE_HIST, false>(q.tmap, tb, p, grid, pl.smem, s);

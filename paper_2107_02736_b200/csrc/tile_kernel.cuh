@@ -56,12 +56,24 @@ enum TileMode : int {
   MODE_FILTER = 3,
   MODE_NULL = 4,
   MODE_KDE_GAUSS_MUFU = 5,  // gaussian with every exponential on MUFU (MMA-heavy encodings)
-  MODE_HIST = 6             // k-NN threshold refinement: per-query histogram of approx d2 (listed sweeps)
+  MODE_HIST = 6,            // k-NN threshold refinement: per-query histogram of approx d2 (listed sweeps)
+  // exact gaussian KDE in two precisions (capi.cu kde_hybrid): the single-pass fp16 sweep sums every
+  // 128-column tile half whose fp32 sum is at most hot_thr and marks the others in a bitmap; the
+  // split3 sweep over the listed (block, tile) pairs sums exactly the marked halves
+  MODE_KDE_COLD = 7,
+  MODE_KDE_HOT = 8
 };
 constexpr int kHistBins = 64;  // MODE_HIST bins per query (quadratic spacing over [lo_q, top_q])
 __host__ __device__ constexpr bool is_kde(int mode) {
-  return mode == MODE_KDE_GAUSS || mode == MODE_KDE_EXP || mode == MODE_KDE_GAUSS_MUFU;
+  return mode == MODE_KDE_GAUSS || mode == MODE_KDE_EXP || mode == MODE_KDE_GAUSS_MUFU || mode == MODE_KDE_COLD ||
+         mode == MODE_KDE_HOT;
 }
+// the per-element epilogue of a mode: the two-precision sweeps are gaussian (the split3 one with every
+// exponential on MUFU: it is MMA-bound)
+__host__ __device__ constexpr int epi_mode(int mode) {
+  return mode == MODE_KDE_COLD ? int(MODE_KDE_GAUSS) : mode == MODE_KDE_HOT ? int(MODE_KDE_GAUSS_MUFU) : mode;
+}
+constexpr int kHotWords = 8;  // hot bitmap words per (query block, tile): 4 lane quarters x 2 column halves
 
 constexpr int kBM = 128;           // query rows per tile (UMMA M)
 constexpr int kBN = 256;           // dataset columns per tile (UMMA N)
@@ -110,6 +122,10 @@ struct TileParams {
   const float* hinv;
   const float* htop;
   uint32_t* hist;
+  // MODE_KDE_COLD writes / MODE_KDE_HOT reads: [nqb][ntiles][kHotWords] lane masks, word quarter * 2 +
+  // half = rows quarter*32 + lane of the block, columns [128 half, 128 half + 128) of the tile
+  uint32_t* hot_bits;
+  float hot_thr;           // MODE_KDE_COLD: a tile half whose fp32 sum exceeds this is hot
   const float* xn;         // [n_pad] |x|^2 (encoding-consistent)
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
@@ -159,7 +175,8 @@ constexpr uint32_t kPolyPairs = DK_POLY_PAIRS;
 #endif
 template <int MODE, bool kPair>
 __host__ __device__ constexpr bool use_pingpong() {
-  return DK_PINGPONG != 0 && !kPair && (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU || MODE == MODE_KDE_EXP);
+  return DK_PINGPONG != 0 && !kPair &&
+         (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU || MODE == MODE_KDE_EXP || MODE == MODE_KDE_COLD);
 }
 
 // 2^t for a pair, t <= 0, on the FMA pipe: t = j + f (j = round(t), |f| <= 1/2),
@@ -688,15 +705,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[group]);
           }
-          epi_chunk<MODE>(r0, xsm + sub * 64, qn, m2s, negc, 0.f, full, cbase, p.n, a0, a1, mn_unused, p, row,
-                          nullptr, nullptr, lrow);
-          epi_chunk<MODE>(r1, xsm + sub * 64 + 32, qn, m2s, negc, 0.f, full, cbase + 32, p.n, a0, a1, mn_unused,
-                          p, row, nullptr, nullptr, lrow);
+          epi_chunk<epi_mode(MODE)>(r0, xsm + sub * 64, qn, m2s, negc, 0.f, full, cbase, p.n, a0, a1, mn_unused, p,
+                                    row, nullptr, nullptr, lrow);
+          epi_chunk<epi_mode(MODE)>(r1, xsm + sub * 64 + 32, qn, m2s, negc, 0.f, full, cbase + 32, p.n, a0, a1,
+                                    mn_unused, p, row, nullptr, nullptr, lrow);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         ph ^= 1u;
-        usum += double((a0.x + a0.y) + (a1.x + a1.y));
+        const float hs = (a0.x + a0.y) + (a1.x + a1.y);
+        if constexpr (MODE == MODE_KDE_COLD) {
+          // a half whose sum exceeds hot_thr is left to the split3 sweep (bit set); the others are summed here
+          const bool hot = hs > p.hot_thr && row < p.nq;
+          const uint32_t w = __ballot_sync(0xffffffffu, hot);
+          if (lane == 0) p.hot_bits[(size_t(qb) * p.ntiles + t) * kHotWords + quarter * 2 + half] = w;
+          if (!hot) usum += double(hs);
+        } else {
+          usum += double(hs);
+        }
       }
       p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
     }
@@ -790,6 +816,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int seg = MODE == MODE_TILEMIN ? t0 / segdiv : 0;
       for (int t = t0; t < t1; ++t, ++titer) {
         const uint32_t xs = titer % kXnSlots;
+        bool take = true;  // MODE_KDE_HOT: this row's half of the tile is hot (summed here)
+        if constexpr (MODE == MODE_KDE_HOT) {
+          const uint32_t w = p.hot_bits[(size_t(qb) * p.ntiles + p.tlist[t]) * kHotWords + quarter * 2 + (cg >> 1)];
+          take = ((w >> lane) & 1u) != 0u;
+        }
         if constexpr (MODE == MODE_TILEMIN) {
           if (p.seg_tiles > 0 && t / segdiv != seg) {
             atomicMin(reinterpret_cast<int*>(&p.tmin[size_t(seg) * p.nq_pad + row]), __float_as_int(fmaxf(mn, 0.f)));
@@ -825,14 +856,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* xsm = smemX + xs * kBN + cg * 64;
         const bool full = cbase + 64 <= p.n;
         float2 a0 = MODE == MODE_HIST ? hpar : make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f), b0 = a0;
-        epi_chunk<MODE>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf, lrow);
+        epi_chunk<epi_mode(MODE)>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf,
+                                  lrow);
         // TILEMIN returns the chunk's two 16-column minima in its first accumulator
-        epi_chunk<MODE>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n, MODE == MODE_TILEMIN ? b0 : a0, a1,
-                        mn, p, row, scnt, sbuf, lrow);
+        epi_chunk<epi_mode(MODE)>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n,
+                                  MODE == MODE_TILEMIN ? b0 : a0, a1, mn, p, row, scnt, sbuf, lrow);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         if constexpr (is_kde(MODE)) {
-          usum += double((a0.x + a0.y) + (a1.x + a1.y));
+          if (take) usum += double((a0.x + a0.y) + (a1.x + a1.y));
         } else if constexpr (MODE == MODE_TILEMIN) {
           if (p.tlist != nullptr) {
             // listed threshold sweep: 8 segments of 32 columns per tile (segment = list position x 8 + 32-column
@@ -848,7 +880,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if constexpr (is_kde(MODE)) {
+      if constexpr (MODE == MODE_KDE_HOT) {
+        p.part[(size_t(u) * kColGroups + cg) * kBM + lrow] = usum;  // listed: one partial per unit
+      } else if constexpr (is_kde(MODE)) {
         p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
       } else if constexpr (MODE == MODE_TILEMIN) {
         if (t1 > t0 && p.seg_tiles > 0)

@@ -66,6 +66,14 @@ def main():
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     stats = None
+    if args.op.startswith("naive"):
+        import ctypes
+
+        from paper_2107_02736_b200 import _lib
+
+        v = [ctypes.c_int64() for _ in range(4)]
+        _lib.check(_lib.load().dk_kde_stats(ds.handle, *[ctypes.byref(x) for x in v]))
+        stats = dict(zip(("hybrid_queries", "hybrid_fallbacks", "hot_pairs", "pairs"), (x.value for x in v)))
     if args.op.startswith(("knn", "deann")):
         import ctypes
 
