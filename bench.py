@@ -16,6 +16,9 @@ objects for the rest of BASELINE's metric ("exact & DEANN at n = 1M-8M"):
   deann  config 3 DEANN (exact k = 100 NN + m = 1,000 Philox samples): device value,
          e2e through `deann_batch` (pinned host queries, list of Estimates), per-kernel
          rooflines, clocks, oracle parity of the timed output, CPU baseline.
+  c3_exact  config 3 exact KDE (non-integer rows): the two-precision path (single-pass fp16
+         sweep of every pair, split3 sweep of the hot tile halves, per-query bound), its 1x
+         roofline fraction, the split3-only time beside it, e2e, parity, CPU baseline.
   c5     config 5 (n = 8M, 100,000 queries): exact KDE and DEANN (k = 100, m = 2,000);
          dataset-sharded over the ranks when N > 1 (all-reduce of partial sums,
          all-gather + merge of per-shard top-k, shared Philox stream).
@@ -491,7 +494,7 @@ def run_ours(args):
     ds.free()
     del W
     if ws == 1 and not args.no_secondary:
-        line["deann"] = measure_deann_c3(args, local, timer)
+        line["deann"], line["c3_exact"] = measure_deann_c3(args, local, timer)
     if not args.no_c5:
         c5 = measure_c5(args, ws, rank, local, dist, timer)
         if rank == 0:
@@ -555,6 +558,7 @@ def measure_deann_c3(args, local, timer):
                                 out.data_ptr(), None, None, None, stream.cuda_stream))
 
     steps, warm = max(3, min(args.steps, 20)), max(3, args.warmup)
+    exact = measure_c3_exact(args, local, timer, W, ds, spec, h, Qd, steps, warm)
     with ClockSampler(local) as clocks:
         ms = timer.run(step, steps, warm, clocks)
     launches = _launches(lib, ds)
@@ -610,7 +614,88 @@ def measure_deann_c3(args, local, timer):
         res["cpu_baseline"] = cpu_baseline(
             "oracle deann + brute_force_knn, numpy PCG64", _deann_oracle_fn(od, "gaussian", h, W.k, W.m),
             [(j, W.Q[j]) for j in range(256)], 1, 10.0, f"the first 256 of the {nq:,} queries")
-    return res
+        ref = O.naive_kde(od, "gaussian", h, W.Q[exact.pop("_parity_sel")])
+        exact["parity_max_rel"] = float(np.max(np.abs(exact.pop("_parity_vals") - ref) / ref))
+        exact["cpu_baseline"] = cpu_baseline(
+            "oracle/deann_oracle.naive_kde", lambda blk: O.naive_kde(od, "gaussian", h, blk),
+            [W.Q[i:i + 8] for i in range(0, 512, 8)], 8, 6.0,
+            f"blocks of 8 of the first 512 of the {nq:,} queries over all n={n:,} rows")
+    exact.pop("_parity_sel", None)
+    exact.pop("_parity_vals", None)
+    return res, exact
+
+
+def measure_c3_exact(args, local, timer, W, ds, spec, h, Qd, steps, warm):
+    """Exact KDE on config 3 (non-integer rows): the two-precision path (capi.cu kde_hybrid) —
+    single-pass fp16 sweep of every pair, split3 sweep of the hot (block, tile) pairs, per-query
+    bound — against the 1x roofline, with the split3-only time beside it."""
+    import ctypes
+
+    import torch
+
+    import paper_2107_02736_b200 as g
+    from paper_2107_02736_b200 import _lib
+
+    lib = _lib.load()
+    n, d = W.X.shape
+    nq = W.Q.shape[0]
+    stream = torch.cuda.current_stream()
+    out = torch.empty(nq, dtype=torch.float64, device=f"cuda:{local}")
+
+    def step(_i):
+        g.naive_kde_into(ds, spec, Qd, out, stream=stream.cuda_stream)
+
+    def stats():
+        v = [ctypes.c_int64() for _ in range(4)]
+        _lib.check(lib.dk_kde_stats(ds.handle, *[ctypes.byref(x) for x in v]))
+        return [x.value for x in v]
+
+    q0, f0, _, _ = stats()
+    with ClockSampler(local) as clocks:
+        for i in range(warm):
+            step(i)
+        q1, f1, _, _ = stats()
+        _lib.check(lib.dk_set_profiling(ds.handle, 1))
+        ms = timer.run(step, steps, 0, clocks)
+    kms = _kernel_ms(lib, ds)[0]  # the single-pass fp16 sweep (every pair)
+    _lib.check(lib.dk_set_profiling(ds.handle, 0))
+    launches = _launches(lib, ds)
+    q2, f2, hot, tot = stats()
+    vals = out.cpu().numpy()
+    os.environ["DK_KDE_HYBRID"] = "0"
+    try:
+        ms_split3 = timer.run(step, max(3, steps // 4), 2)
+    finally:
+        del os.environ["DK_KDE_HYBRID"]
+    Qh = torch.from_numpy(W.Q).pin_memory().numpy()
+    e2e_ms = timer.wall(lambda i: g.naive_kde(ds, spec, Qh).values, steps, 5)
+    peaks = _peaks()
+    flops, ex2 = 2.0 * d * nq * n, float(nq) * n
+    t_bound = max(flops / (peaks["bf16_tflops"] * 1e12), ex2 / _sfu_peak(peaks))
+    sel = list(np.random.default_rng(5).choice(nq, 16, replace=False))
+    return {
+        "metric": "KDE queries/sec (exact naive KDE, gaussian) at n=1.2M, d=100",
+        "value": nq / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
+        "higher_is_better": True, "gpu_launches": launches * steps,
+        "dtype": "fp16 single pass for every pair + fp16 split3 for the hot tile halves (fp32 accumulate, "
+                 "fp64 row sums), per-query a-posteriori bound of the fp16 part <= 2e-6",
+        "two_precision": {"queries_served": q2 - q1, "fallback_queries": f2 - f1, "hot_block_tile_pairs": hot,
+                          "block_tile_pairs": tot, "hot_fraction": hot / tot if tot > 0 else None,
+                          "warmup_calls_served": q1 - q0},
+        "split3_only": {"value": nq / (ms_split3 / 1e3), "ms_per_step": ms_split3,
+                        "note": "DK_KDE_HYBRID=0: every pair in split3 (round-1 path)"},
+        "roofline": {"bound": "sfu (1x: one exp2 per pair) / tensor (1x: one fp16 MMA pass)",
+                     "kernel_ms_fp16_sweep": kms, "frac_of_1x_binding": t_bound / (ms / 1e3),
+                     "fp16_sweep_frac_of_1x_binding": t_bound / (kms / 1e3),
+                     "t_bound_ms": t_bound * 1e3, "sfu_peak_tex2s": _sfu_peak(peaks) / 1e12,
+                     "tensor_peak_tflops": peaks["bf16_tflops"]},
+        "e2e": {"value": nq / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
+                "d2h_bytes_per_step": int(nq * 8), "api": "naive_kde(ds, KernelSpec, pinned host queries)"},
+        "clocks": clocks.summary(),
+        "config": {"workload": "c3: 1,200,000 x 100 L2-normalised rows, 10,000 queries, h by median-1e-3 rule",
+                   "bandwidth": h, "l2": "inputs larger than L2 (307 MB fp16 operand + 480 MB rows)"},
+        "_parity_sel": sel, "_parity_vals": vals[sel],
+    }
 
 
 def measure_c5(args, ws, rank, local, dist, timer):

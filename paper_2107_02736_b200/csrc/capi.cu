@@ -19,6 +19,7 @@
 #include <unistd.h>
 
 #include <map>
+#include <tuple>
 #include <mutex>
 
 #include "internal.h"
@@ -849,6 +850,24 @@ bool hyb_prepare(dk_dataset* h, int32_t family, int64_t nq_chunk_min, cudaStream
   return ensure_sorted_split3(h, s);
 }
 
+// KDE partials of any sweep of at most bpad queries (the batches and the fallback chunks): the
+// column-chunk count of the plan grows as the query-block count falls, so take the maximum over
+// every query padding up to bpad (cached per shape)
+size_t hyb_part_cap(const dk_dataset* h, int32_t bpad) {
+  static std::mutex mu;
+  static std::map<std::tuple<int64_t, int32_t, int>, size_t> cache;
+  const auto key = std::make_tuple(h->n_pad, bpad, h->num_sms);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  size_t cap = 0;
+  for (int32_t pad = kBM; pad <= bpad; pad = pad == kBM ? 2 * kBM : pad + 2 * kBM)
+    cap = std::max({cap, sweep_part_count(h->n_pad, pad, h->num_sms, false),
+                    sweep_part_count(h->n_pad, pad, h->num_sms, true)});
+  cache[key] = cap;
+  return cap;
+}
+
 struct HybLayout {
   size_t dq, near, near_s, iota, qperm, sort_tmp, qs, A16, qn16, sc16, A3, qn3, sc3, part, bits, tlist, tcnt, ubeg,
       ucnt, ulist, phot, ctr, fail, fv;
@@ -880,8 +899,7 @@ HybLayout hyb_layout(const dk_dataset* h, int64_t nq, size_t base) {
   L.A3 = pl.add<__half>(size_t(bpad) * Kp3);
   L.qn3 = pl.add<float>(bpad);
   L.sc3 = pl.add<float>(4);
-  L.part = pl.add<double>(std::max(sweep_part_count(h->n_pad, bpad, h->num_sms, false),
-                                   sweep_part_count(h->n_pad, bpad, h->num_sms, true)));
+  L.part = pl.add<double>(hyb_part_cap(h, bpad));
   L.bits = pl.add<uint32_t>(size_t(nqb) * ntiles * kHotWords);
   L.tlist = pl.add<int32_t>(size_t(nqb) * ntiles);
   L.tcnt = pl.add<int32_t>(nqb);

@@ -130,6 +130,23 @@ def test_host_queries_two_chunks_and_ragged_batch(data, monkeypatch):
     assert _rel(host[sel], O.naive_kde(od, "gaussian", H, Qr[sel])) < 1e-5
 
 
+def test_few_fallbacks_outlier_queries(data, monkeypatch):
+    """Queries far from every row (random unit directions) have no hot tile half: their value is
+    all fp16 and its bound fails, so they alone are recomputed in split3 (a fallback sweep of a
+    single 128-query block, whose partial-sum plan is the widest)."""
+    X, Q, ds, od = data
+    rng = np.random.default_rng(11)
+    out = rng.standard_normal((5, X.shape[1]))
+    out /= np.linalg.norm(out, axis=1, keepdims=True)
+    Qm = np.concatenate([Q[:2043], out])[rng.permutation(2048)]
+    ref = _split3(ds, Qm, monkeypatch)
+    q0, f0, _, _ = _stats(ds)
+    v = _naive_dev(ds, Qm)
+    q1, f1, _, _ = _stats(ds)
+    assert q1 - q0 == 2048 and 5 <= f1 - f0 < 128, f1 - f0
+    assert _rel(v, ref) < 1e-6
+
+
 def test_wide_bandwidth_turns_the_path_off(data, monkeypatch):
     """h = 1 on unit vectors: every (block, tile) pair is hot.  Still correct; after one such call
     the handle stops using the two-precision path (it would cost 1 + 3 MMA passes)."""
