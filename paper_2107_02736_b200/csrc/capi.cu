@@ -875,7 +875,8 @@ struct HybLayout {
   int32_t bpad = 0;
 };
 
-HybLayout hyb_layout(const dk_dataset* h, int64_t nq, size_t base) {
+// nq: the largest chunk of the call (batch size), nq_call: all its queries (failure list)
+HybLayout hyb_layout(const dk_dataset* h, int64_t nq, int64_t nq_call, size_t base) {
   HybLayout L{};
   Plan pl;
   pl.off = base;
@@ -908,20 +909,20 @@ HybLayout hyb_layout(const dk_dataset* h, int64_t nq, size_t base) {
   L.ulist = pl.add<int32_t>(size_t(3) * nqb * kHotUnitsPerBlock);
   L.phot = pl.add<double>(size_t(nqb) * kHotUnitsPerBlock * kColGroups * kBM);
   L.ctr = pl.add<int32_t>(16);
-  L.fail = pl.add<int32_t>(size_t(nq));
+  L.fail = pl.add<int32_t>(size_t(nq_call));
   L.fv = pl.add<double>(bpad);
   L.end = pl.off;
   return L;
 }
 
-size_t hyb_ws_bytes(const dk_dataset* h, int64_t nq) { return hyb_layout(h, nq, 0).end + 4096; }
 
-// Two-precision exact gaussian KDE of nq device queries into od (device), means scaled by `scale`.
-// Enqueued without host waits except one read of the failure count at the end (and the fallback).
-void kde_hybrid(dk_dataset* h, const double* Qc, int64_t nq, double bw, double scale, double* od, cudaStream_t s,
-                size_t base) {
+
+// Two-precision exact gaussian KDE of queries [q0, q0 + qn) of the call's device queries Q into od
+// (device, the call's base), means scaled by `scale`.  Enqueued without host waits; the last chunk
+// of a call (`last`) reads the failure count of the whole call once and recomputes those queries.
+void kde_hybrid(dk_dataset* h, const double* Q, int64_t q0, int64_t qn, double bw, double scale, double* od,
+                cudaStream_t s, const HybLayout& L, bool first, bool last) {
   KnnClusters* kc = h->kc;
-  const HybLayout L = hyb_layout(h, nq, base);
   if (L.end > h->ws.cap) throw Error{DK_ECUDA, "internal: hybrid KDE workspace under-reserved"};
   const Encoding& e16 = kc->enc;
   const Encoding& e3 = kc->enc3;
@@ -931,17 +932,48 @@ void kde_hybrid(dk_dataset* h, const double* Qc, int64_t nq, double bw, double s
   const float thr = float(env_double("DK_HYB_THR", kHybHotThr));
   const double tol = env_double("DK_HYB_TOL", kHybTol);
   const int32_t ntiles = int32_t(h->n_pad / kBN);
-  int32_t* ctr = at<int32_t>(h->ws, L.ctr);  // [0] failures, [4..5] split3 units / listed pairs
-  int32_t* fail = at<int32_t>(h->ws, L.fail);
-  DK_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), s));
-  int64_t rest = nq;  // queries from here on take the plain split3 sweep (early switch)
-  const int64_t nbatch = (nq + L.bpad - 1) / L.bpad;
-  const int64_t bstep = std::min<int64_t>(L.bpad, round_up((nq + nbatch - 1) / nbatch, 2 * kBM));
-  for (int64_t b0 = 0; b0 < nq; b0 += bstep) {
-    const int64_t bn = std::min<int64_t>(bstep, nq - b0);
+  int32_t* ctr = at<int32_t>(h->ws, L.ctr);  // [0] failures of the call, [4..5] split3 units / listed pairs
+  int32_t* fail = at<int32_t>(h->ws, L.fail);  // query ids relative to Q
+  if (first) DK_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), s));
+  // plain split3 sweep over the sorted rows for queries gathered by id (idx) or a contiguous range
+  auto split3_rows = [&](const int32_t* idx, int64_t first_q, int64_t fn) {
+    const int32_t fpad = int32_t(query_pad(fn));
+    const double* Qf = Q + first_q * h->d;
+    if (idx != nullptr) {
+      launch_gather_rows_f64(Q, idx + first_q, fn, h->d, at<double>(h->ws, L.qs), s);
+      Qf = at<double>(h->ws, L.qs);
+    }
+    QueryOperand q = encode_queries(h, e3, Qf, fn, fpad, at<__half>(h->ws, L.A3), at<float>(h->ws, L.qn3),
+                                    at<float>(h->ws, L.sc3), s);
+    SweepArgs a{};
+    a.mode = MODE_KDE_GAUSS;
+    a.qop = &q;
+    a.enc = &e3;
+    a.n = h->n;
+    a.n_pad = h->n_pad;
+    a.tile_stride = 1;
+    a.negc = negc;
+    a.part = at<double>(h->ws, L.part);
+    int32_t ncc = 0;
+    a.ncc_out = &ncc;
+    launch_sweep(a, h->num_sms, s);
+    if (idx != nullptr) {
+      double* fv = at<double>(h->ws, L.fv);
+      launch_reduce_partials(a.part, ncc * kColGroups, fpad, fn, scale, fv, s);
+      launch_scatter_f64(fv, idx + first_q, fn, od, s);
+    } else {
+      launch_reduce_partials(a.part, ncc * kColGroups, fpad, fn, scale, od + first_q, s);
+    }
+  };
+  // queries of this chunk from rest on take the plain split3 sweep (early switch in this call)
+  int64_t rest = (!first && kc->hyb_useless) ? 0 : qn;
+  const int64_t nbatch = (qn + L.bpad - 1) / L.bpad;
+  const int64_t bstep = std::min<int64_t>(L.bpad, round_up((qn + nbatch - 1) / nbatch, 2 * kBM));
+  for (int64_t b0 = 0; b0 < rest; b0 += bstep) {
+    const int64_t bn = std::min<int64_t>(bstep, qn - b0);
     const int32_t bn_pad = int32_t(query_pad(bn));
     const int32_t nqb = bn_pad / kBM;
-    const double* Qb = Qc + b0 * h->d;
+    const double* Qb = Q + (q0 + b0) * h->d;
     // ball-sorted batch: each block of 128 queries is local, so its hot tiles are few
     int32_t* near = at<int32_t>(h->ws, L.near);
     int32_t* qperm = at<int32_t>(h->ws, L.qperm);
@@ -997,14 +1029,14 @@ void kde_hybrid(dk_dataset* h, const double* Qc, int64_t nq, double bw, double s
       launch_sweep(b, h->num_sms, s);
     }
     launch_hyb_combine(at<double>(h->ws, L.part), ncc * kColGroups, bn_pad, bn, phot, ubeg, ucnt, q16.qn,
-                       e16.eps_rel, e16.xn_max, inv2h2, tol, scale, qperm, b0, od + b0, fail, ctr,
+                       e16.eps_rel, e16.xn_max, inv2h2, tol, scale, qperm, q0 + b0, od + q0 + b0, fail, ctr,
                        nullptr, s);
-    if (b0 == 0) {  // hot (block, tile) pairs of the first batch, read at the next call
+    if (b0 == 0 && first) {  // hot (block, tile) pairs of the call's first batch, read at the next call
       DK_CUDA(cudaMemcpyAsync(kc->hyb_stat_host, ctr + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       DK_CUDA(cudaEventRecord(kc->hyb_stat_ev, s));
       kc->hyb_stat_total = double(nqb) * double(ntiles);
       kc->hyb_stat_pending = true;
-      if (b0 + bn < nq && hyb_env() != 1) {
+      if (b0 + bn < qn && hyb_env() != 1) {
         // a bandwidth that makes most pairs hot (a wide kernel: c5) costs 1 + 3 MMA passes: the
         // rest of this call and the next 32 calls take the plain split3 sweep
         DK_CUDA(cudaEventSynchronize(kc->hyb_stat_ev));
@@ -1018,44 +1050,15 @@ void kde_hybrid(dk_dataset* h, const double* Qc, int64_t nq, double bw, double s
       }
     }
   }
-  // queries whose fp16 bound failed (and the batches after an early switch): split3 sweeps over the
-  // sorted rows, gathered by index or a contiguous range
+  h->hyb_queries += rest;
+  for (int64_t r0 = rest; r0 < qn; r0 += L.bpad) split3_rows(nullptr, q0 + r0, std::min<int64_t>(L.bpad, qn - r0));
+  if (!last) return;
+  // queries of the whole call whose fp16 bound failed: split3 sweeps gathered by id
   int32_t nf = 0;
   DK_CUDA(cudaMemcpyAsync(&nf, ctr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   DK_CUDA(cudaStreamSynchronize(s));
-  h->hyb_queries += rest;
   h->hyb_fallbacks += nf;
-  auto split3_rows = [&](const int32_t* idx, int64_t first, int64_t fn) {
-    const int32_t fpad = int32_t(query_pad(fn));
-    const double* Qf = Qc + first * h->d;
-    if (idx != nullptr) {
-      launch_gather_rows_f64(Qc, idx + first, fn, h->d, at<double>(h->ws, L.qs), s);
-      Qf = at<double>(h->ws, L.qs);
-    }
-    QueryOperand q = encode_queries(h, e3, Qf, fn, fpad, at<__half>(h->ws, L.A3), at<float>(h->ws, L.qn3),
-                                    at<float>(h->ws, L.sc3), s);
-    SweepArgs a{};
-    a.mode = MODE_KDE_GAUSS;
-    a.qop = &q;
-    a.enc = &e3;
-    a.n = h->n;
-    a.n_pad = h->n_pad;
-    a.tile_stride = 1;
-    a.negc = negc;
-    a.part = at<double>(h->ws, L.part);
-    int32_t ncc = 0;
-    a.ncc_out = &ncc;
-    launch_sweep(a, h->num_sms, s);
-    if (idx != nullptr) {
-      double* fv = at<double>(h->ws, L.fv);
-      launch_reduce_partials(a.part, ncc * kColGroups, fpad, fn, scale, fv, s);
-      launch_scatter_f64(fv, idx + first, fn, od, s);
-    } else {
-      launch_reduce_partials(a.part, ncc * kColGroups, fpad, fn, scale, od + first, s);
-    }
-  };
   for (int64_t f0 = 0; f0 < nf; f0 += L.bpad) split3_rows(fail, f0, std::min<int64_t>(L.bpad, nf - f0));
-  for (int64_t r0 = rest; r0 < nq; r0 += L.bpad) split3_rows(nullptr, r0, std::min<int64_t>(L.bpad, nq - r0));
 }
 
 // ------------------------------------------------------------------ fit
@@ -1459,8 +1462,8 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     // two-precision exact KDE (non-integer gaussian batches on large datasets): decided before the
     // workspace is reserved (the first call builds the sorted rows' operands in their own memory)
     const bool hyb = hyb_prepare(h, family, nq, s);
-    const size_t hyb_base = pl.off;
-    h->ws.reserve(pl.off + (hyb ? hyb_ws_bytes(h, std::max(c_cnt[0], c_cnt[1])) : 0));
+    const HybLayout HL = hyb ? hyb_layout(h, std::max(c_cnt[0], c_cnt[1]), nq, pl.off) : HybLayout{};
+    h->ws.reserve(hyb ? HL.end + 4096 : pl.off);
     double* od = out_dev ? out : at<double>(h->ws, o_out);
     const double* Qd = Q;
     if (host_q) {
@@ -1518,8 +1521,8 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     for (int c = 0; c < nchunks; ++c) {
       if (c == 1) DK_CUDA(cudaStreamWaitEvent(s, h->copy_done, 0));
       if (hyb) {
-        kde_hybrid(h, Qd + size_t(c_beg[c]) * h->d, c_cnt[c], bandwidth, scale, od + c_beg[c], s, hyb_base);
-        if (!out_dev) copy_out(out + c_beg[c], od + c_beg[c], size_t(c_cnt[c]) * sizeof(double), s);
+        kde_hybrid(h, Qd, c_beg[c], c_cnt[c], bandwidth, scale, od, s, HL, c == 0, c == nchunks - 1);
+        if (!out_dev && c == nchunks - 1) copy_out(out, od, size_t(nq) * sizeof(double), s);
         continue;
       }
       if (h->precision == DK_PREC_AUTO && h->int_exact) {
