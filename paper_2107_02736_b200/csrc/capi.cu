@@ -98,7 +98,7 @@ const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
   Encoding& e = enc_slot(h, mode);
   if (e.mode == mode) return e;
   const int32_t d = h->d;
-  e.Kp = int32_t(round_up(mode == 1 ? 3 * int64_t(d) : d, kBK));
+  e.Kp = enc_kp(d, mode);
   e.d = d;
   if (mode != 0) ensure_mu(h, s);
   e.mu = mode == 0 ? nullptr : h->mu;
@@ -119,7 +119,8 @@ const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
   // rounding, the add and the fma), using 2|q||x| <= |q|^2 + |x|^2.
   if (mode == 0) e.eps_rel = 0.f;                                                        // exact integers
   else if (mode == 1) e.eps_rel = float(1.01 * (4.0 * std::ldexp(1.0, -22) + double(e.Kp + 4) * u));  // split3
-  else e.eps_rel = float(1.01 * (2.002 * std::ldexp(1.0, -11) + double(e.Kp + 4) * u));             // fp16
+  // fp16: + 2^-20 for the norm columns' residual and subnormal operands (values < 2^-14 of 2^8)
+  else e.eps_rel = float(1.01 * (2.002 * std::ldexp(1.0, -11) + double(e.Kp + 4) * u + std::ldexp(1.0, -20)));
   e.tmap = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN));
   e.tmap_half = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN / 2));
   e.mode = mode;
@@ -160,15 +161,17 @@ int choose_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cu
 }
 
 QueryOperand encode_queries(dk_dataset* h, const Encoding& e, const double* Qd, int64_t nq, int32_t nq_pad,
-                            __half* A, float* qn, float* scal, cudaStream_t s, uint32_t* check_flags = nullptr) {
+                            __half* A, float* qn, float* scal, cudaStream_t s, uint32_t* check_flags = nullptr,
+                            bool aug = false) {
   QueryOperand q;
+  q.aug = aug && enc_has_aug(h->d, e.mode);
   q.nq = int32_t(nq);
   q.nq_pad = nq_pad;
   q.A = A;
   q.qn = qn;
   q.m2s = scal;
   launch_encode_queries(Qd, nq, nq_pad, h->d, e.mode, e.mu, e.Kp, e.sx, A, qn, scal,
-                        reinterpret_cast<uint32_t*>(scal + 1), s, check_flags);
+                        reinterpret_cast<uint32_t*>(scal + 1), s, check_flags, q.aug);
   q.tmap = make_tmap_2d_f16(A, uint64_t(nq_pad), uint64_t(e.Kp), uint32_t(kBM));
   return q;
 }
@@ -885,7 +888,7 @@ HybLayout hyb_layout(const dk_dataset* h, int64_t nq, int64_t nq_call, size_t ba
   L.bpad = int32_t(std::min<int64_t>(bmax, query_pad(nq)));
   const int32_t bpad = L.bpad, nqb = bpad / kBM, ntiles = int32_t(h->n_pad / kBN);
   const int32_t C = knn_cluster_count(h);
-  const int32_t Kp16 = int32_t(round_up(h->d, kBK)), Kp3 = int32_t(round_up(3 * int64_t(h->d), kBK));
+  const int32_t Kp16 = enc_kp(h->d, 2), Kp3 = enc_kp(h->d, 1);
   L.dq = pl.add<double>(size_t(bpad) * C);
   L.near = pl.add<int32_t>(bpad);
   L.near_s = pl.add<int32_t>(bpad);
@@ -983,7 +986,7 @@ void kde_hybrid(dk_dataset* h, const double* Q, int64_t q0, int64_t qn, double b
     double* Qs = at<double>(h->ws, L.qs);
     launch_gather_rows_f64(Qb, qperm, bn, h->d, Qs, s);
     QueryOperand q16 = encode_queries(h, e16, Qs, bn, bn_pad, at<__half>(h->ws, L.A16), at<float>(h->ws, L.qn16),
-                                      at<float>(h->ws, L.sc16), s);
+                                      at<float>(h->ws, L.sc16), s, nullptr, true);
     QueryOperand q3 = encode_queries(h, e3, Qs, bn, bn_pad, at<__half>(h->ws, L.A3), at<float>(h->ws, L.qn3),
                                      at<float>(h->ws, L.sc3), s);
     uint32_t* bits = at<uint32_t>(h->ws, L.bits);
@@ -1493,8 +1496,9 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       const double* Qc = Qd + size_t(q0) * h->d;
       const Encoding& e = ensure_encoding(h, mode, s);
       // speculative exact mode: the query encode also computes the exact-mode flags
+      // exact-mode gaussian sweeps carry the query norms in the operand (the MMA yields -d2/2)
       QueryOperand q = encode_queries(h, e, Qc, cn, pad, at<__half>(h->ws, o_A[c]), at<float>(h->ws, o_qn[c]),
-                                      at<float>(h->ws, o_scal[c]), s, guard_flags);
+                                      at<float>(h->ws, o_scal[c]), s, guard_flags, mode == 0 && family == DK_GAUSSIAN);
       if (guard_flags) {
         DK_CUDA(cudaMemcpyAsync(h->flag_host + c, guard_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         DK_CUDA(cudaEventRecord(h->flag_event, s));

@@ -105,6 +105,23 @@ inline void set_dynamic_smem(K* kernel, size_t bytes) {
     if (!(cond)) throw ::dk::Error{DK_EINVAL, (msg)};  \
   } while (0)
 
+// Norm columns of the exact / fp16 operands (prep.cu): 3 for the row norm, 3 for the query norm.
+// They ride in the K padding only.  Where they would open a K-block of their own (d within 6 of a
+// multiple of 64: c2, d = 128) they cost more than the epilogue work they save — measured on c2:
+// 2.67 ms without, 2.83 ms with a full third K-block, 3.74 ms with 136-half rows (unaligned TMA
+// rows), 2.69-2.98 ms with 192-half rows and a 134-column tensor-map extent (zero-filled box),
+// for 2 to 6 of 16 exponentials on the FMA pipe — so those operands go without them.
+constexpr int32_t kAugCols = 6;
+inline bool enc_has_aug(int32_t d, int mode) {
+  return mode != 1 && (int64_t(d) + kAugCols + 63) / 64 == (int64_t(d) + 63) / 64;
+}
+// padded K (row stride, a multiple of 64) of an encoding: split3 3d, exact / fp16 d (+ norm columns)
+inline int32_t enc_kp(int32_t d, int mode) {
+  const int64_t k = mode == 1 ? 3 * int64_t(d) : int64_t(d) + (enc_has_aug(d, mode) ? kAugCols : 0);
+  return int32_t((k + 63) / 64 * 64);
+}
+inline int32_t enc_kblocks(int32_t Kp) { return (Kp + 63) / 64; }
+
 // One operand encoding of the dataset for the tensor-core tile.
 struct Encoding {
   int mode = -1;            // 0 exact fp16, 1 split3, 2 fp16 single (lossy)
@@ -222,6 +239,7 @@ struct QueryOperand {
   __half* A = nullptr;        // [nq_pad][Kp]
   float* qn = nullptr;        // [nq_pad]
   float* m2s = nullptr;       // device scalar
+  bool aug = false;           // A carries the query-norm columns (KDE: the MMA yields -d2/2)
   CUtensorMap tmap;
 };
 
@@ -236,9 +254,10 @@ void launch_encode_rows(const float* X, int64_t n, int64_t n_pad, int32_t d, int
 // queries
 void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags, cudaStream_t s);
 // check_flags (mode 0 only, nullable): also OR query_check's exact-mode flags into *check_flags
+// aug (exact / fp16 modes): write the query-norm columns (the KDE sweeps; k-NN leaves them zero)
 void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
                            int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
-                           cudaStream_t s, uint32_t* check_flags = nullptr);
+                           cudaStream_t s, uint32_t* check_flags = nullptr, bool aug = false);
 void launch_reduce_partials(const double* part, int32_t nparts, int32_t nq_pad, int64_t nq, double scale,
                             double* out, cudaStream_t s);
 

@@ -8,7 +8,14 @@
 //   split3 : centred, power-of-two scaled fp16 hi/lo pairs, K-concatenated
 //            A=[Qh|Ql|Qh], B=[Xl|Xh|Xh] so one MMA chain with K = 3d gives
 //            Qh.Xl + Ql.Xh + Qh.Xh (~2^-22 relative)     -> Kp = roundup(3d, 64)
-//   fp16   : single-pass scaled fp16 (opt-in, lossy)       -> Kp = roundup(d, 64)
+//   fp16   : single-pass scaled fp16 (k-NN sweeps, the two-precision KDE's
+//            every-pair pass)                              -> Kp = roundup(d + 6, 64)
+// The exact and fp16 operands carry kAugCols = 6 norm columns after the d data columns:
+//   rows    B = [x | -b1 -b2 -b3 | w1 w2 w3],  queries A = [q | w1 w2 w3 | -b1 -b2 -b3]
+// with w1 b1 + w2 b2 + w3 b3 = |v|^2 / 2 (scaled), so the MMA itself accumulates
+//   q.x - (|q|^2 + |x|^2) / 2 = -d2 / 2
+// and the KDE epilogue needs one multiply per pair (no norm loads, no cancellation in fp32
+// outside the accumulator).  k-NN query operands leave the A norm columns zero (plain q.x).
 #include "internal.h"
 
 namespace dk {
@@ -102,21 +109,23 @@ __device__ __forceinline__ float pow2_scale(uint32_t maxabs_bits) {
   if (!(m > 0.f)) return 1.f;
   int e;
   frexpf(m, &e);                       // m < 2^e
-  int sh = 14 - e;                     // scaled max in [2^13, 2^14)
+  int sh = 8 - e;                      // scaled max in [2^7, 2^8): scaled |v|^2 / 2 fits w1 b1 (aug columns)
   sh = max(-100, min(100, sh));
   return ldexpf(1.f, sh);
 }
 
-// one warp per row: writes the operand row (Kp halves) and the encoding-consistent fp32 norm
+// one warp per row: writes the operand row (Kp halves) and the fp32 norm;
+// aug: 0 = norm columns zero (k-NN queries), 1 = row side [-b | w], 2 = query side [w | -b]
 template <class T>
 __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t rows_pad, int32_t d, int mode,
                               const double* __restrict__ mu, int32_t Kp, const uint32_t* __restrict__ maxabs_bits,
                               const float* __restrict__ other_scale, __half* __restrict__ out,
                               float* __restrict__ norms, float* __restrict__ scale_out,
-                              float* __restrict__ m2s_out, uint32_t* __restrict__ check_flags) {
+                              float* __restrict__ m2s_out, uint32_t* __restrict__ check_flags, int aug) {
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const float s = (mode == 0) ? 1.f : pow2_scale(*maxabs_bits);
+  // queries with norm columns share the dataset's scale (the norm terms must carry one scale)
+  const float s = (mode == 0) ? 1.f : (aug == 2 && other_scale ? *other_scale : pow2_scale(*maxabs_bits));
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (scale_out) *scale_out = s;
     if (m2s_out) *m2s_out = -2.f / (s * (other_scale ? *other_scale : 1.f));
@@ -152,7 +161,10 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
       else w = h;
       o[k] = w;
     } else {
-      if (k >= d) { o[k] = __float2half_rn(0.f); continue; }
+      if (k >= d) {
+        if (aug == 0 || k >= d + kAugCols) o[k] = __float2half_rn(0.f);  // norm columns: written below
+        continue;
+      }
       double x = double(v[k]);
       if (check_flags) f |= value_flags(x);
       if (mu) x -= mu[k];
@@ -162,6 +174,35 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
   }
   nrm = warp_sum_d(nrm);
   if (lane == 0) norms[row] = float(nrm);
+  if (mode != 1 && aug != 0 && lane < kAugCols) {
+    // |v|^2 / 2 (scaled) = w1 b1 + w2 b2 + w3 b3.  Exact integers: b from floor divisions (xn <
+    // 2^23: b1 < 2^11, b2 < 64, b3 < 32 half-integers, all exact in fp16).  Scaled fp16: each b the
+    // fp16 rounding of the remainder (residual <= 2^-33 relative); a query norm beyond the range
+    // (v >= 2^31, or inf) poisons its row with NaN (the two-precision KDE then recomputes it).
+    double w[3], b[3];
+    bool bad = false;
+    if (mode == 0) {
+      w[0] = 2048.0; w[1] = 32.0; w[2] = 1.0;
+      b[0] = floor(nrm / 4096.0);
+      const double rem = nrm - b[0] * 4096.0;
+      b[1] = floor(rem / 64.0);
+      b[2] = (rem - b[1] * 64.0) * 0.5;
+    } else {
+      w[0] = 32768.0; w[1] = 32.0; w[2] = 1.0;
+      const double v = nrm * double(s) * double(s) * 0.5;
+      bad = !(v < 2147483648.0);
+      b[0] = double(__half2float(__float2half_rn(float(v / 32768.0))));
+      double r = v - b[0] * 32768.0;
+      b[1] = double(__half2float(__float2half_rn(float(r / 32.0))));
+      r -= b[1] * 32.0;
+      b[2] = double(__half2float(__float2half_rn(float(r))));
+    }
+    float val;
+    if (aug == 1) val = lane < 3 ? float(-b[lane]) : float(w[lane - 3]);
+    else val = lane < 3 ? float(w[lane]) : float(-b[lane - 3]);
+    if (bad && aug == 2 && lane == 3) val = __int_as_float(0x7fc00000);
+    o[d + lane] = __float2half_rn(val);
+  }
   if (check_flags) {
     f = warp_or(f);
     if (lane == 0) {
@@ -251,7 +292,8 @@ void launch_encode_rows(const float* X, int64_t n, int64_t n_pad, int32_t d, int
   }
   const int64_t threads = n_pad * 32;
   encode_kernel<float><<<unsigned((threads + 255) / 256), 256, 0, s>>>(X, n, n_pad, d, mode, mu, Kp, maxabs_bits,
-                                                                      nullptr, B, xn, scale, nullptr, nullptr);
+                                                                      nullptr, B, xn, scale, nullptr, nullptr,
+                                                                      enc_has_aug(d, mode) ? 1 : 0);
   DK_CHECK_LAUNCH();
 }
 
@@ -263,7 +305,7 @@ void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags,
 
 void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
                            int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
-                           cudaStream_t s, uint32_t* check_flags) {
+                           cudaStream_t s, uint32_t* check_flags, bool aug) {
   if (mode != 0) {
     DK_CUDA(cudaMemsetAsync(maxabs_bits, 0, sizeof(uint32_t), s));
     const int64_t total = nq * d;
@@ -273,7 +315,8 @@ void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t 
   }
   const int64_t threads = int64_t(nq_pad) * 32;
   encode_kernel<double><<<unsigned((threads + 255) / 256), 256, 0, s>>>(
-      Q, nq, nq_pad, d, mode, mu, Kp, maxabs_bits, sx, A, qn, nullptr, m2s, mode == 0 ? check_flags : nullptr);
+      Q, nq, nq_pad, d, mode, mu, Kp, maxabs_bits, sx, A, qn, nullptr, m2s, mode == 0 ? check_flags : nullptr,
+      (aug && enc_has_aug(d, mode)) ? 2 : 0);
   DK_CHECK_LAUNCH();
 }
 

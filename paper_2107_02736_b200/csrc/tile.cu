@@ -160,7 +160,7 @@ CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint3
 }
 
 bool tile_major_fits(int32_t Kp) {
-  return tile_smem_bytes(Kp / kBK, 0, 3, MODE_FILTER, false, true) <= kMaxSmem;
+  return tile_smem_bytes(enc_kblocks(Kp), 0, 3, MODE_FILTER, false, true) <= kMaxSmem;
 }
 
 static bool use_pair(int nqb) { return g_pair_enabled && nqb >= 2 && nqb % 2 == 0; }
@@ -178,11 +178,11 @@ void set_pair_enabled(bool on) { g_pair_enabled = on; }
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const QueryOperand& q = *a.qop;
   const Encoding& e = *a.enc;
-  const int kblocks = e.Kp / kBK;
+  const int kblocks = enc_kblocks(e.Kp);
   const int ntiles_all = int(a.n_pad / kBN);
   const int ntiles = (ntiles_all + a.tile_stride - 1) / a.tile_stride;
   const int nqb = q.nq_pad / kBM;
-  const bool pr = a.ulist == nullptr && a.mode != MODE_KDE_COLD && use_pair(nqb);
+  const bool pr = a.ulist == nullptr && a.mode != MODE_KDE_COLD && !q.aug && use_pair(nqb);
   const int ngroups = pr ? nqb / 2 : nqb;
   const int nslots = pr ? num_sms / 2 : num_sms;  // CTAs (or CTA pairs) resident at once
   const bool tmajor = a.tmajor != 0;
@@ -204,7 +204,8 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
 #define DK_KSKIP 1
 #endif
   {
-    const int kused = e.mode == 1 ? 3 * e.d : e.d;  // columns holding data (the rest is zero padding)
+    // columns holding data (the rest is zero padding)
+    const int kused = e.mode == 1 ? 3 * e.d : e.d + (enc_has_aug(e.d, e.mode) ? kAugCols : 0);
     const int rem = kused - (kblocks - 1) * kBK;
     p.klast = DK_KSKIP && e.d > 0 && rem > 0 && rem <= kBK ? (rem + 15) / 16 : kBK / 16;
   }
@@ -256,8 +257,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
     case MODE_KDE_GAUSS:
       // MMA-heavy encodings (split3: >= 4 K-blocks per tile) leave no FMA-pipe slack for the
       // exp2 polynomial and run power-capped: every exponential on MUFU is faster there
-      // (c3: 6.6 vs 7.0 ms); the single-pass encodings offload 2 of 16 pairs (c2: 2.83 vs 2.98 ms).
-      if (kblocks >= 4) launch_any<MODE_KDE_GAUSS_MUFU>(pr, q.tmap, tb, p, grid, pl.smem, s);
+      // (c3: 6.6 vs 7.0 ms); the single-pass encodings offload 2 of 16 pairs (c2: 2.83 vs 2.98 ms),
+      // 4 of 16 with the norm columns (q.aug: one multiply per pair before the exponential)
+      if (q.aug) launch_mode<MODE_KDE_GAUSS_AUG, false>(q.tmap, tb, p, grid, pl.smem, s);
+      else if (kblocks >= 4) launch_any<MODE_KDE_GAUSS_MUFU>(pr, q.tmap, tb, p, grid, pl.smem, s);
       else launch_any<MODE_KDE_GAUSS>(pr, q.tmap, tb, p, grid, pl.smem, s);
       break;
     case MODE_KDE_GAUSS_MUFU: launch_any<MODE_KDE_GAUSS_MUFU>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
@@ -265,7 +268,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
     case MODE_TILEMIN: launch_any<MODE_TILEMIN>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_FILTER: launch_any<MODE_FILTER>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_NULL: launch_any<MODE_NULL>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
-    case MODE_KDE_COLD: launch_mode<MODE_KDE_COLD, false>(q.tmap, tb, p, grid, pl.smem, s); break;
+    case MODE_KDE_COLD:
+      if (q.aug) launch_mode<MODE_KDE_COLD_AUG, false>(q.tmap, tb, p, grid, pl.smem, s);
+      else launch_mode<MODE_KDE_COLD, false>(q.tmap, tb, p, grid, pl.smem, s);
+      break;
     case MODE_KDE_HOT: launch_mode<MODE_KDE_HOT, false>(q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_HIST:
       if (pr || a.ulist == nullptr) throw Error{DK_EINVAL, "internal: histogram sweeps are listed single-CTA sweeps"};

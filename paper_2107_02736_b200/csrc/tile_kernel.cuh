@@ -61,17 +61,26 @@ enum TileMode : int {
   // 128-column tile half whose fp32 sum is at most hot_thr and marks the others in a bitmap; the
   // split3 sweep over the listed (block, tile) pairs sums exactly the marked halves
   MODE_KDE_COLD = 7,
-  MODE_KDE_HOT = 8
+  MODE_KDE_HOT = 8,
+  // gaussian over operands with norm columns (prep.cu: exact / fp16 with A = [q | w | -b(q)], B =
+  // [x | -b(x) | w]): the accumulator already holds -d2/2, so t = S * (m2s * negc) (KDE_COLD too)
+  MODE_KDE_GAUSS_AUG = 9,
+  MODE_KDE_COLD_AUG = 10   // KDE_COLD over operands with norm columns
 };
 constexpr int kHistBins = 64;  // MODE_HIST bins per query (quadratic spacing over [lo_q, top_q])
 __host__ __device__ constexpr bool is_kde(int mode) {
   return mode == MODE_KDE_GAUSS || mode == MODE_KDE_EXP || mode == MODE_KDE_GAUSS_MUFU || mode == MODE_KDE_COLD ||
-         mode == MODE_KDE_HOT;
+         mode == MODE_KDE_HOT || mode == MODE_KDE_GAUSS_AUG || mode == MODE_KDE_COLD_AUG;
 }
+__host__ __device__ constexpr bool is_aug(int mode) { return mode == MODE_KDE_GAUSS_AUG || mode == MODE_KDE_COLD_AUG; }
+__host__ __device__ constexpr bool is_cold(int mode) { return mode == MODE_KDE_COLD || mode == MODE_KDE_COLD_AUG; }
 // the per-element epilogue of a mode: the two-precision sweeps are gaussian (the split3 one with every
 // exponential on MUFU: it is MMA-bound)
 __host__ __device__ constexpr int epi_mode(int mode) {
-  return mode == MODE_KDE_COLD ? int(MODE_KDE_GAUSS) : mode == MODE_KDE_HOT ? int(MODE_KDE_GAUSS_MUFU) : mode;
+  return mode == MODE_KDE_COLD       ? int(MODE_KDE_GAUSS)
+         : mode == MODE_KDE_COLD_AUG ? int(MODE_KDE_GAUSS_AUG)
+         : mode == MODE_KDE_HOT      ? int(MODE_KDE_GAUSS_MUFU)
+                                     : mode;
 }
 constexpr int kHotWords = 8;  // hot bitmap words per (query block, tile): 4 lane quarters x 2 column halves
 
@@ -161,6 +170,12 @@ __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, i
 #define DK_POLY_PAIRS 0x0808u
 #endif
 constexpr uint32_t kPolyPairs = DK_POLY_PAIRS;
+// the norm-column epilogue spends 2 packed FMA-pipe ops per 2 pairs (t = S c, the sum) instead of 4,
+// so more of the exponentials can move to the FMA pipe
+#ifndef DK_POLY_PAIRS_AUG
+#define DK_POLY_PAIRS_AUG 0x2222u
+#endif
+constexpr uint32_t kPolyPairsAug = DK_POLY_PAIRS_AUG;
 
 // Ping-pong epilogue for the KDE sweeps (single-CTA): the two accumulator buffers are
 // consumed by two different groups of 8 epilogue warps (group = accumulator), each warp
@@ -176,7 +191,8 @@ constexpr uint32_t kPolyPairs = DK_POLY_PAIRS;
 template <int MODE, bool kPair>
 __host__ __device__ constexpr bool use_pingpong() {
   return DK_PINGPONG != 0 && !kPair &&
-         (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU || MODE == MODE_KDE_EXP || MODE == MODE_KDE_COLD);
+         (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU || MODE == MODE_KDE_EXP || is_cold(MODE) ||
+          MODE == MODE_KDE_GAUSS_AUG);
 }
 
 // 2^t for a pair, t <= 0, on the FMA pipe: t = j + f (j = round(t), |f| <= 1/2),
@@ -212,7 +228,21 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
                                           uint32_t* scnt, unsigned long long* sbuf, int lrow) {
   const float4* x4 = reinterpret_cast<const float4*>(xs_smem);
   if (full || MODE == MODE_TILEMIN || MODE == MODE_FILTER || MODE == MODE_HIST) {
-    if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU) {
+    if constexpr (MODE == MODE_KDE_GAUSS_AUG) {
+      // the accumulator is q.x - (|q|^2 + |x|^2)/2 = -d2/2 (scaled): t = S * negc (negc = m2s x the
+      // exp2 scale, an exact power-of-two product), no column norms
+      (void)x4;
+      const float2 c2 = make_float2(negc, negc);
+#pragma unroll
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float2 ta = mul2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), c2);
+        const float2 tb = mul2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), c2);
+        const float2 ea = (kPolyPairsAug >> (2 * j4)) & 1 ? exp2_poly2(ta) : make_float2(ex2_approx(ta.x), ex2_approx(ta.y));
+        const float2 eb = (kPolyPairsAug >> (2 * j4 + 1)) & 1 ? exp2_poly2(tb) : make_float2(ex2_approx(tb.x), ex2_approx(tb.y));
+        acc0 = add2(acc0, ea);
+        acc1 = add2(acc1, eb);
+      }
+    } else if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU) {
       constexpr uint32_t poly = MODE == MODE_KDE_GAUSS ? kPolyPairs : 0u;
       // d2 = S * m2s + (qn + xn) in the cancellation-safe order, then t = d2 * negc
       const float2 q2 = make_float2(qn, qn), m2 = make_float2(m2s, m2s), c2 = make_float2(negc, negc);
@@ -341,6 +371,10 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       if (j >= lim) continue;
+      if constexpr (MODE == MODE_KDE_GAUSS_AUG) {
+        acc0.x += ex2_approx(__uint_as_float(r[j]) * negc);
+        continue;
+      }
       const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs_smem[j]);
       if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU) {
         acc0.x += ex2_approx(d2 * negc);
@@ -673,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0;  // phase of this group's accumulator barriers
     uint32_t titer = 0;
     const float m2s = *p.m2s;
-    const float negc = p.negc;
+    const float negc = is_aug(MODE) ? p.negc * m2s : p.negc;  // norm columns: t = S * m2s * negc
     float mn_unused = 0.f;
     for (int u = first_unit; u < nunits; u += unit_step) {
       const int qb = u % ngroups, cc = u / ngroups;
@@ -714,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         ph ^= 1u;
         const float hs = (a0.x + a0.y) + (a1.x + a1.y);
-        if constexpr (MODE == MODE_KDE_COLD) {
+        if constexpr (is_cold(MODE)) {
           // a half whose sum exceeds hot_thr is left to the split3 sweep (bit set); the others are summed here
           const bool hot = hs > p.hot_thr && row < p.nq;
           const uint32_t w = __ballot_sync(0xffffffffu, hot);
@@ -790,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     uint32_t titer = 0;
     const float m2s = *p.m2s;
-    const float negc = p.negc;
+    const float negc = is_aug(MODE) ? p.negc * m2s : p.negc;
 #ifdef DK_TIMING
     const long long tepi0 = clock64();
 #endif

@@ -1,0 +1,54 @@
+"""Operands with norm columns (prep.cu: A = [q | w | -b(q)], B = [x | -b(x) | w], the MMA yields
+-d2/2 and the gaussian epilogue multiplies once per pair; tile mode KDE_GAUSS_AUG / KDE_COLD_AUG).
+
+Exact integer rows: the norm split is exact, so d2 is exact and the KDE matches the fp64 oracle
+(naive_kde, estimators.py:144-149) to the exponential's own rounding — checked next to the exact-mode
+limit (squared norms just under 2^23, the largest b1).  d = 64 has no padding for the columns and
+keeps the plain epilogue (also for the two-precision sweep, KDE_COLD).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2107_02736_b200 as g  # noqa: E402
+import workloads  # noqa: E402
+from oracle import deann_oracle as O  # noqa: E402
+
+
+def _rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+@pytest.mark.parametrize("d", [50, 57, 64, 100])
+def test_exact_integer_rows_near_the_norm_limit(d):
+    rng = np.random.default_rng(d)
+    vmax = int(np.sqrt((2 ** 23 - 1) / d))  # squared norms up to just under 2^23
+    X = rng.integers(0, vmax + 1, size=(20_000, d)).astype(np.float32)
+    X[:64] = vmax  # rows at the limit: b1 = floor(|x|^2 / 4096) at its largest
+    Q = rng.integers(0, vmax + 1, size=(300, d)).astype(np.float64)
+    Q[:3] = vmax
+    ds = g.Dataset.from_array(X)
+    assert ds.exact_mode
+    h = 0.35 * vmax * np.sqrt(d)
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", h), Q).values
+    ref = O.naive_kde(O.Data(X), "gaussian", h, Q)
+    assert _rel(got, ref) < 2e-6
+
+
+def test_two_precision_without_norm_columns(monkeypatch):
+    """d = 64: the fp16 sweep of the two-precision KDE keeps the plain epilogue (KDE_COLD)."""
+    X = workloads._c3_rows(3, 160_000)[:, :64].copy()
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    Q = workloads._c3_rows(4, 2048).astype(np.float64)[:, :64].copy()
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    ds = g.Dataset.from_array(X)
+    h = 0.2
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", h), Q).values
+    monkeypatch.setenv("DK_KDE_HYBRID", "0")
+    ref3 = g.naive_kde(ds, g.KernelSpec("gaussian", h), Q).values
+    assert _rel(got, ref3) < 5e-6
+    sel = np.arange(0, 2048, 256)
+    assert _rel(got[sel], O.naive_kde(O.Data(X), "gaussian", h, Q[sel])) < 1e-5
