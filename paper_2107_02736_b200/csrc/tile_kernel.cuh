@@ -851,9 +851,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = t0; t < t1; ++t, ++titer) {
         const uint32_t xs = titer % kXnSlots;
         bool take = true;  // MODE_KDE_HOT: this row's half of the tile is hot (summed here)
+        bool any = true;   // MODE_KDE_HOT: some row of this warp's quarter is (else no epilogue math)
         if constexpr (MODE == MODE_KDE_HOT) {
           const uint32_t w = p.hot_bits[(size_t(qb) * p.ntiles + p.tlist[t]) * kHotWords + quarter * 2 + (cg >> 1)];
           take = ((w >> lane) & 1u) != 0u;
+          any = w != 0u;
         }
         if constexpr (MODE == MODE_TILEMIN) {
           if (p.seg_tiles > 0 && t / segdiv != seg) {
@@ -890,11 +892,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* xsm = smemX + xs * kBN + cg * 64;
         const bool full = cbase + 64 <= p.n;
         float2 a0 = MODE == MODE_HIST ? hpar : make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f), b0 = a0;
-        epi_chunk<epi_mode(MODE)>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf,
-                                  lrow);
-        // TILEMIN returns the chunk's two 16-column minima in its first accumulator
-        epi_chunk<epi_mode(MODE)>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n,
-                                  MODE == MODE_TILEMIN ? b0 : a0, a1, mn, p, row, scnt, sbuf, lrow);
+        if (any) {  // warp-uniform
+          epi_chunk<epi_mode(MODE)>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf,
+                                    lrow);
+          // TILEMIN returns the chunk's two 16-column minima in its first accumulator
+          epi_chunk<epi_mode(MODE)>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n,
+                                    MODE == MODE_TILEMIN ? b0 : a0, a1, mn, p, row, scnt, sbuf, lrow);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         if constexpr (is_kde(MODE)) {
