@@ -380,6 +380,87 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
       if (perm != nullptr) top[i].lo = static_cast<unsigned long long>(perm[col]);
     }
   }
+  __syncthreads();
+  {
+    // Of the ns exactly evaluated keys only the k smallest are output.  A histogram of their
+    // exact d2 finds the bin holding the k-th; the keys up to that bin (k plus a few) are ordered
+    // by counting ranks (ids are distinct, so ranks are) and the first k write themselves out:
+    // O(ns + m^2) work and a handful of barriers instead of sorting all ns keys (round 1: a
+    // bitonic network over pow2(ns) keys, ~40 barrier-separated stages; ns is a few hundred on c3).
+    if (threadIdx.x == 0) { s_lo = 0xffffffffu; s_hi = 0u; s_bstar = kSelHist - 1; s_ns = 0u; }
+    for (int i = threadIdx.x; i < kSelHist; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    // exact d2 >= 0: the fp32 value rounded up keeps the order of the fp64 keys (monotone binning)
+    auto f32_of = [&](unsigned long long hi) { return __double2float_ru(__longlong_as_double(static_cast<long long>(hi))); };
+    uint32_t lo2 = 0xffffffffu, hi2 = 0u;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+      const uint32_t b = __float_as_uint(f32_of(top[i].hi));
+      lo2 = min(lo2, b);
+      hi2 = max(hi2, b);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo2 = min(lo2, __shfl_xor_sync(0xffffffffu, lo2, o));
+      hi2 = max(hi2, __shfl_xor_sync(0xffffffffu, hi2, o));
+    }
+    if (lane == 0) { atomicMin(&s_lo, lo2); atomicMax(&s_hi, hi2); }
+    __syncthreads();
+    const float elo = __uint_as_float(s_lo), ehi = __uint_as_float(s_hi);
+    const float escale = ehi > elo ? float(kSelHist) / (ehi - elo) : 0.f;
+    auto ebin = [&](unsigned long long hi) {
+      return min(max(__float2int_rz((f32_of(hi) - elo) * escale), 0), kSelHist - 1);
+    };
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) atomicAdd(&hist[ebin(top[i].hi)], 1u);
+    __syncthreads();
+    {
+      const int t = threadIdx.x;
+      const uint32_t h0 = hist[4 * t], h1 = hist[4 * t + 1], h2 = hist[4 * t + 2], h3 = hist[4 * t + 3];
+      const uint32_t own = h0 + h1 + h2 + h3;
+      uint32_t incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      uint32_t cum = incl - own;
+      for (int w = 0; w < warp; ++w) cum += s_wsum[w];
+      const uint32_t hh[4] = {h0, h1, h2, h3};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (cum < uint32_t(k) && cum + hh[j] >= uint32_t(k)) s_bstar = uint32_t(4 * t + j);
+        cum += hh[j];
+      }
+    }
+    __syncthreads();
+    const int eb = int(s_bstar);
+    uint16_t* sel = reinterpret_cast<uint16_t*>(hist);  // the bins are no longer needed: [<= 2 kSelHist]
+    __syncthreads();
+    for (int i = threadIdx.x; i < ns; i += blockDim.x)
+      if (ebin(top[i].hi) <= eb) {
+        const uint32_t pos = atomicAdd(&s_ns, 1u);
+        if (pos < uint32_t(2 * kSelHist)) sel[pos] = uint16_t(i);
+      }
+    __syncthreads();
+    const int m = int(s_ns);
+    if (m <= 2 * kSelHist) {
+      for (int a = threadIdx.x; a < m; a += blockDim.x) {
+        const Key128 ki = top[sel[a]];
+        int r = 0;
+        for (int b = 0; b < m; ++b) {
+          const Key128 kj = top[sel[b]];
+          r += (kj.hi < ki.hi) | ((kj.hi == ki.hi) & (kj.lo < ki.lo));
+        }
+        if (r < k) {
+          idx_out[size_t(q) * k + r] = int64_t(ki.lo) + global_offset;
+          d2_out[size_t(q) * k + r] = __longlong_as_double(static_cast<long long>(ki.hi));
+        }
+      }
+      return;
+    }
+    __syncthreads();
+  }
   for (int i = ns + threadIdx.x; i < P; i += blockDim.x) top[i] = Key128{~0ull, ~0ull};
   bitonic_k128(top, P);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
@@ -638,23 +719,34 @@ __global__ void __launch_bounds__(256) block_tile_lists_kernel(
     const float* __restrict__ tau, const float* __restrict__ qn, float xn_max, float eps_rel,
     const double* __restrict__ rad, const int32_t* __restrict__ tclo, const int32_t* __restrict__ tchi,
     int32_t ntiles, int32_t* __restrict__ tlist, int32_t* __restrict__ tcount, uint32_t* __restrict__ bits) {
-  extern __shared__ uint8_t need[];
+  // need: one bit per cluster.  Each warp takes every 8th row of the block and sweeps that
+  // query's distances to all clusters with coalesced reads (lanes over clusters), OR-ing a ballot
+  // per 32 clusters into shared memory (round 1: one thread per cluster looping over the rows,
+  // latency-bound, 149 us on c3).
+  extern __shared__ uint32_t need[];
   __shared__ int s_wcnt[8];
   __shared__ int s_base;
   const int qb = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = int64_t(qb) * 128;
   const int rows = int(bn - r0 < 128 ? bn - r0 : 128);
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    bool nd = false;
-    const double rc = rad[c];
-    for (int i = 0; i < rows && !nd; ++i) {
-      const int64_t row = r0 + i;
-      const double thr = (double(tau[row]) + double(eps_rel) * (double(qn[row]) + double(xn_max))) * (1.0 + 1e-6);
-      const double lb = fmax(dq[int64_t(qperm[row]) * C + c] * (1.0 - 1e-12) - rc, 0.0);
-      nd = lb * lb <= thr;
+  const int nw = (C + 31) >> 5;
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) need[w] = 0u;
+  __syncthreads();
+  for (int i = warp; i < rows; i += 8) {
+    const int64_t row = r0 + i;
+    const double thr = (double(tau[row]) + double(eps_rel) * (double(qn[row]) + double(xn_max))) * (1.0 + 1e-6);
+    const double* dr = dq + int64_t(qperm[row]) * C;
+    for (int c0 = 0; c0 < C; c0 += 32) {
+      const int c = c0 + lane;
+      bool nd = false;
+      if (c < C) {
+        const double lb = fmax(dr[c] * (1.0 - 1e-12) - rad[c], 0.0);
+        nd = lb * lb <= thr;
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, nd);
+      if (lane == 0 && m) atomicOr(&need[c0 >> 5], m);
     }
-    need[c] = nd ? 1 : 0;
   }
   if (threadIdx.x == 0) s_base = 0;
   __syncthreads();
@@ -662,7 +754,7 @@ __global__ void __launch_bounds__(256) block_tile_lists_kernel(
     const int t = t0 + threadIdx.x;
     bool on = false;
     if (t < ntiles)
-      for (int c = tclo[t]; c <= tchi[t] && !on; ++c) on = need[c] != 0;
+      for (int c = tclo[t]; c <= tchi[t] && !on; ++c) on = ((need[c >> 5] >> (c & 31)) & 1u) != 0u;
     const uint32_t b = __ballot_sync(0xffffffffu, on);
     if (lane == 0) s_wcnt[warp] = __popc(b);
     // tile-major schedule: bit t of row qb (32 tiles per word)
@@ -915,9 +1007,10 @@ void launch_block_tile_lists(const double* dq, int32_t C, const int32_t* qperm, 
                              const float* tau, const float* qn, float xn_max, float eps_rel, const double* rad,
                              const int32_t* tclo, const int32_t* tchi, int32_t ntiles, int32_t* tlist,
                              int32_t* tcount, uint32_t* bits, cudaStream_t s) {
-  set_dynamic_smem(block_tile_lists_kernel, size_t(C));
-  block_tile_lists_kernel<<<unsigned(nqb), 256, size_t(C), s>>>(dq, C, qperm, bn, tau, qn, xn_max, eps_rel, rad,
-                                                                 tclo, tchi, ntiles, tlist, tcount, bits);
+  const size_t smem = size_t((C + 31) / 32) * 4;
+  set_dynamic_smem(block_tile_lists_kernel, smem);
+  block_tile_lists_kernel<<<unsigned(nqb), 256, smem, s>>>(dq, C, qperm, bn, tau, qn, xn_max, eps_rel, rad, tclo,
+                                                             tchi, ntiles, tlist, tcount, bits);
   DK_CHECK_LAUNCH();
 }
 
