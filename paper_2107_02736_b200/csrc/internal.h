@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -113,7 +114,11 @@ inline void set_dynamic_smem(K* kernel, size_t bytes) {
 // for 2 to 6 of 16 exponentials on the FMA pipe — so those operands go without them.
 constexpr int32_t kAugCols = 6;
 inline bool enc_has_aug(int32_t d, int mode) {
-  return mode != 1 && (int64_t(d) + kAugCols + 63) / 64 == (int64_t(d) + 63) / 64;
+  static const bool force = [] {  // A/B: norm columns even when they open a K-block
+    const char* v = std::getenv("DK_AUG_FORCE");
+    return v != nullptr && std::atoi(v) != 0;
+  }();
+  return mode != 1 && (force || (int64_t(d) + kAugCols + 63) / 64 == (int64_t(d) + 63) / 64);
 }
 // padded K (row stride, a multiple of 64) of an encoding: split3 3d, exact / fp16 d (+ norm columns)
 inline int32_t enc_kp(int32_t d, int mode) {
