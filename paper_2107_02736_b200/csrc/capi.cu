@@ -750,7 +750,9 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
 // that fail it.  Used for gaussian batches of >= kHybMinQueries on datasets of >= kPruneMinTiles
 // tiles under DK_PREC_AUTO; DK_KDE_HYBRID=0 turns it off, =1 forces it (read per call).
 constexpr int64_t kHybMinQueries = 2048;
-constexpr float kHybHotThr = 2.44140625e-04f;  // 2^-12 per 128-column half (kernel values in (0, 1])
+// 2^-11 per 128-column half (kernel values in (0, 1]); c3: 2^-12 -> 2^-11 hot pairs 2.7% -> 2.4%
+// (3.36 -> 3.33 ms), larger thresholds no further (the same-cluster tiles remain)
+constexpr float kHybHotThr = 4.8828125e-04f;
 constexpr double kHybTol = 2e-6;                  // relative bound of the fp16 part
 constexpr double kHybUseless = 0.25;              // hot (block, tile) fraction above which it does not pay
 
@@ -887,9 +889,8 @@ HybLayout hyb_layout(const dk_dataset* h, int64_t nq, int64_t nq_call, size_t ba
   if (const char* v = std::getenv("DK_HYB_BATCH")) bmax = std::max<int64_t>(2 * kBM, round_up(std::atoll(v), 2 * kBM));
   L.bpad = int32_t(std::min<int64_t>(bmax, query_pad(nq)));
   const int32_t bpad = L.bpad, nqb = bpad / kBM, ntiles = int32_t(h->n_pad / kBN);
-  const int32_t C = knn_cluster_count(h);
   const int32_t Kp16 = enc_kp(h->d, 2), Kp3 = enc_kp(h->d, 1);
-  L.dq = pl.add<double>(size_t(bpad) * C);
+  L.dq = pl.add<unsigned long long>(size_t(bpad));  // nearest-ball keys
   L.near = pl.add<int32_t>(bpad);
   L.near_s = pl.add<int32_t>(bpad);
   L.iota = pl.add<int32_t>(bpad);
@@ -980,7 +981,7 @@ void kde_hybrid(dk_dataset* h, const double* Q, int64_t q0, int64_t qn, double b
     // ball-sorted batch: each block of 128 queries is local, so its hot tiles are few
     int32_t* near = at<int32_t>(h->ws, L.near);
     int32_t* qperm = at<int32_t>(h->ws, L.qperm);
-    launch_query_cluster_dist(Qb, bn, h->d, kc->cent, kc->C, at<double>(h->ws, L.dq), near, s);
+    launch_nearest_ball_f32(Qb, bn, h->d, kc->cent, kc->C, at<unsigned long long>(h->ws, L.dq), near, s);
     launch_sort_queries_by_ball(near, bn, kc->C, at<int32_t>(h->ws, L.near_s), at<int32_t>(h->ws, L.iota), qperm,
                                 h->ws.base + L.sort_tmp, L.sort_tmp_bytes, s);
     double* Qs = at<double>(h->ws, L.qs);

@@ -345,6 +345,9 @@ void free_knn_clusters(KnnClusters& kc);
 // dq[j][c] = |q_j - cent_c| (fp64 direct difference), nearest[j] = argmin_c dq[j][c]
 void launch_query_cluster_dist(const double* Q, int64_t nq, int32_t d, const double* cent, int32_t C, double* dq,
                                int32_t* nearest, cudaStream_t s);
+// nearest[j] = argmin_c |q_j - cent_c| in fp32 (ordering heuristic; best: nq scratch keys)
+void launch_nearest_ball_f32(const double* Q, int64_t nq, int32_t d, const double* cent, int32_t C,
+                             unsigned long long* best, int32_t* nearest, cudaStream_t s);
 // per block of 128 permuted queries: the tiles whose clusters can hold a row with approx d2 <= tau_q
 void launch_block_tile_lists(const double* dq, int32_t C, const int32_t* qperm, int64_t bn, int32_t nqb,
                              const float* tau, const float* qn, float xn_max, float eps_rel, const double* rad,

@@ -689,6 +689,63 @@ __global__ void __launch_bounds__(256) query_cluster_dist_kernel(const double* _
   }
 }
 
+// Nearest ball in fp32 (an ordering heuristic only: the two-precision KDE sorts its batch by it;
+// the k-NN's pruning bounds need the fp64 dq above).  Same 32 x 64 tiling; each query's
+// (distance bits, ball) minimum over the block's 64 balls, then one 64-bit atomicMin per query
+// and tile (deterministic: a minimum).
+__global__ void __launch_bounds__(256) nearest_ball_f32_kernel(const double* __restrict__ Q, int64_t nq, int32_t d,
+                                                               const double* __restrict__ cent, int32_t C,
+                                                               unsigned long long* __restrict__ best) {
+  __shared__ float qs[32][33];
+  __shared__ float cs[64][33];
+  const int64_t q0 = int64_t(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 64;
+  const int tq = threadIdx.x >> 4, tc = threadIdx.x & 15;
+  float acc[2][4] = {};
+  for (int k0 = 0; k0 < d; k0 += 32) {
+    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+      const int r = i >> 5, k = i & 31;
+      qs[r][k] = (q0 + r < nq && k0 + k < d) ? float(Q[(q0 + r) * d + k0 + k]) : 0.f;
+    }
+    for (int i = threadIdx.x; i < 64 * 32; i += 256) {
+      const int r = i >> 5, k = i & 31;
+      cs[r][k] = (c0 + r < C && k0 + k < d) ? float(cent[size_t(c0 + r) * d + k0 + k]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const float a0 = qs[tq][k], a1 = qs[tq + 16][k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float b = cs[tc + 16 * i][k];
+        const float t0 = a0 - b, t1 = a1 - b;
+        acc[0][i] = fmaf(t0, t0, acc[0][i]);
+        acc[1][i] = fmaf(t1, t1, acc[1][i]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    unsigned long long key = ~0ull;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = c0 + tc + 16 * i;
+      if (c < C) key = min(key, (static_cast<unsigned long long>(__float_as_uint(acc[a][i])) << 32) | uint32_t(c));
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+    const int64_t q = q0 + tq + 16 * a;
+    if (tc == 0 && q < nq) atomicMin(best + q, key);
+  }
+}
+
+__global__ void best_to_ball_kernel(const unsigned long long* __restrict__ best, int64_t nq,
+                                    int32_t* __restrict__ nearest) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nq) nearest[i] = int32_t(best[i] & 0xffffffffull);
+}
+
 __global__ void nearest_cluster_kernel(const double* __restrict__ dq, int64_t nq, int32_t C,
                                        int32_t* __restrict__ nearest) {
   const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1000,6 +1057,17 @@ void launch_query_cluster_dist(const double* Q, int64_t nq, int32_t d, const dou
   query_cluster_dist_kernel<<<grid, 256, 0, s>>>(Q, nq, d, cent, C, dq);
   DK_CHECK_LAUNCH();
   nearest_cluster_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(dq, nq, C, nearest);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_nearest_ball_f32(const double* Q, int64_t nq, int32_t d, const double* cent, int32_t C,
+                             unsigned long long* best, int32_t* nearest, cudaStream_t s) {
+  if (nq <= 0) return;
+  DK_CUDA(cudaMemsetAsync(best, 0xff, size_t(nq) * sizeof(unsigned long long), s));
+  dim3 grid(unsigned((nq + 31) / 32), unsigned((C + 63) / 64));
+  nearest_ball_f32_kernel<<<grid, 256, 0, s>>>(Q, nq, d, cent, C, best);
+  DK_CHECK_LAUNCH();
+  best_to_ball_kernel<<<unsigned((nq + 255) / 256), 256, 0, s>>>(best, nq, nearest);
   DK_CHECK_LAUNCH();
 }
 

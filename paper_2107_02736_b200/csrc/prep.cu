@@ -306,7 +306,8 @@ void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags,
 void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
                            int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
                            cudaStream_t s, uint32_t* check_flags, bool aug) {
-  if (mode != 0) {
+  // fp16 queries with norm columns take the dataset's scale: no maximum to find
+  if (mode != 0 && !(mode == 2 && aug && enc_has_aug(d, mode))) {
     DK_CUDA(cudaMemsetAsync(maxabs_bits, 0, sizeof(uint32_t), s));
     const int64_t total = nq * d;
     const unsigned blocks = unsigned(std::min<int64_t>(1184, (total + 255) / 256 + 1));
