@@ -105,8 +105,9 @@ const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
   DK_CUDA(cudaMalloc(&e.B, size_t(h->n_pad) * e.Kp * sizeof(__half)));
   DK_CUDA(cudaMalloc(&e.xn, size_t(h->n_pad) * sizeof(float)));
   DK_CUDA(cudaMalloc(&e.sx, 2 * sizeof(float)));
+  if (enc_aug_tail(d, mode)) DK_CUDA(cudaMalloc(&e.T, size_t(h->n_pad) * kTailK * sizeof(__half)));
   uint32_t* maxabs = reinterpret_cast<uint32_t*>(e.sx + 1);
-  launch_encode_rows(h->X, h->n, h->n_pad, d, mode, e.mu, e.Kp, e.B, e.xn, e.sx, maxabs, s);
+  launch_encode_rows(h->X, h->n, h->n_pad, d, mode, e.mu, e.Kp, e.B, e.xn, e.sx, maxabs, s, e.T);
   std::vector<float> xn(static_cast<size_t>(h->n));
   DK_CUDA(cudaMemcpyAsync(xn.data(), e.xn, xn.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
   DK_CUDA(cudaStreamSynchronize(s));
@@ -123,12 +124,14 @@ const Encoding& ensure_encoding(dk_dataset* h, int mode, cudaStream_t s) {
   else e.eps_rel = float(1.01 * (2.002 * std::ldexp(1.0, -11) + double(e.Kp + 4) * u + std::ldexp(1.0, -20)));
   e.tmap = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN));
   e.tmap_half = make_tmap_2d_f16(e.B, uint64_t(h->n_pad), uint64_t(e.Kp), uint32_t(kBN / 2));
+  if (e.T) e.tmap_t = make_tmap_tail_f16(e.T, uint64_t(h->n_pad), uint32_t(kBN));
   e.mode = mode;
   return e;
 }
 
 void free_encoding(Encoding& e) {
   if (e.B) cudaFree(e.B);
+  if (e.T) cudaFree(e.T);
   if (e.xn) cudaFree(e.xn);
   if (e.sx) cudaFree(e.sx);
   e = Encoding{};
@@ -160,19 +163,24 @@ int choose_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cu
   return (f & 6u) ? 1 : 0;
 }
 
+// aug: the KDE sweeps' query-norm columns (in A when they fit its padding, else in `tail`,
+// kTailK halves per padded row, when the encoding has a tail and the caller passes the buffer)
 QueryOperand encode_queries(dk_dataset* h, const Encoding& e, const double* Qd, int64_t nq, int32_t nq_pad,
                             __half* A, float* qn, float* scal, cudaStream_t s, uint32_t* check_flags = nullptr,
-                            bool aug = false) {
+                            bool aug = false, __half* tail = nullptr) {
   QueryOperand q;
-  q.aug = aug && enc_has_aug(h->d, e.mode);
+  const bool use_tail = aug && e.T != nullptr && tail != nullptr;
+  q.aug = aug && (enc_aug_main(h->d, e.mode) || use_tail);
+  q.T = use_tail ? tail : nullptr;
   q.nq = int32_t(nq);
   q.nq_pad = nq_pad;
   q.A = A;
   q.qn = qn;
   q.m2s = scal;
   launch_encode_queries(Qd, nq, nq_pad, h->d, e.mode, e.mu, e.Kp, e.sx, A, qn, scal,
-                        reinterpret_cast<uint32_t*>(scal + 1), s, check_flags, q.aug);
+                        reinterpret_cast<uint32_t*>(scal + 1), s, check_flags, q.aug, q.T);
   q.tmap = make_tmap_2d_f16(A, uint64_t(nq_pad), uint64_t(e.Kp), uint32_t(kBM));
+  if (q.T) q.tmap_t = make_tmap_tail_f16(q.T, uint64_t(nq_pad), uint32_t(kBM));
   return q;
 }
 
@@ -383,14 +391,16 @@ bool ensure_knn_clusters(dk_dataset* h, const Encoding& e, cudaStream_t s) {
     DK_CUDA(cudaMalloc(&se.B, size_t(h->n_pad) * se.Kp * sizeof(__half)));
     DK_CUDA(cudaMalloc(&se.xn, size_t(h->n_pad) * sizeof(float)));
     DK_CUDA(cudaMalloc(&se.sx, 2 * sizeof(float)));
+    if (e.T) DK_CUDA(cudaMalloc(&se.T, size_t(h->n_pad) * kTailK * sizeof(__half)));
     // same rows, same centring: the power-of-two scale (from the max |value|) equals the k-NN
     // encoding's, so the encoded queries serve both operands
     launch_encode_rows(kc->xs, h->n, h->n_pad, h->d, e.mode, e.mu, se.Kp, se.B, se.xn, se.sx,
-                       reinterpret_cast<uint32_t*>(se.sx + 1), s);
+                       reinterpret_cast<uint32_t*>(se.sx + 1), s, se.T);
     se.xn_max = e.xn_max;
     se.eps_rel = e.eps_rel;
     se.tmap = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN));
     se.tmap_half = make_tmap_2d_f16(se.B, uint64_t(h->n_pad), uint64_t(se.Kp), uint32_t(kBN / 2));
+    if (se.T) se.tmap_t = make_tmap_tail_f16(se.T, uint64_t(h->n_pad), uint32_t(kBN));
     se.mode = e.mode;
     DK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&kc->stat_host), 4 * sizeof(int32_t), cudaHostAllocDefault));
     DK_CUDA(cudaEventCreateWithFlags(&kc->stat_ev, cudaEventDisableTiming));
@@ -874,7 +884,7 @@ size_t hyb_part_cap(const dk_dataset* h, int32_t bpad) {
 }
 
 struct HybLayout {
-  size_t dq, near, near_s, iota, qperm, sort_tmp, qs, A16, qn16, sc16, A3, qn3, sc3, part, bits, tlist, tcnt, ubeg,
+  size_t dq, near, near_s, iota, qperm, sort_tmp, qs, A16, At16, qn16, sc16, A3, qn3, sc3, part, bits, tlist, tcnt, ubeg,
       ucnt, ulist, phot, ctr, fail, fv;
   size_t sort_tmp_bytes = 0, end = 0;
   int32_t bpad = 0;
@@ -899,6 +909,7 @@ HybLayout hyb_layout(const dk_dataset* h, int64_t nq, int64_t nq_call, size_t ba
   L.sort_tmp = pl.add<uint8_t>(L.sort_tmp_bytes);
   L.qs = pl.add<double>(size_t(bpad) * h->d);
   L.A16 = pl.add<__half>(size_t(bpad) * Kp16);
+  L.At16 = pl.add<__half>(size_t(bpad) * kTailK);
   L.qn16 = pl.add<float>(bpad);
   L.sc16 = pl.add<float>(4);
   L.A3 = pl.add<__half>(size_t(bpad) * Kp3);
@@ -987,7 +998,7 @@ void kde_hybrid(dk_dataset* h, const double* Q, int64_t q0, int64_t qn, double b
     double* Qs = at<double>(h->ws, L.qs);
     launch_gather_rows_f64(Qb, qperm, bn, h->d, Qs, s);
     QueryOperand q16 = encode_queries(h, e16, Qs, bn, bn_pad, at<__half>(h->ws, L.A16), at<float>(h->ws, L.qn16),
-                                      at<float>(h->ws, L.sc16), s, nullptr, true);
+                                      at<float>(h->ws, L.sc16), s, nullptr, true, at<__half>(h->ws, L.At16));
     QueryOperand q3 = encode_queries(h, e3, Qs, bn, bn_pad, at<__half>(h->ws, L.A3), at<float>(h->ws, L.qn3),
                                      at<float>(h->ws, L.sc3), s);
     uint32_t* bits = at<uint32_t>(h->ws, L.bits);
@@ -1454,10 +1465,11 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     const int64_t c_cnt[2] = {split, nq - split};
     const int nchunks = c_cnt[1] > 0 ? 2 : 1;
     const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
-    size_t o_A[2], o_qn[2], o_scal[2], o_part[2], o_fl[2];
+    size_t o_A[2], o_At[2], o_qn[2], o_scal[2], o_part[2], o_fl[2];
     for (int c = 0; c < nchunks; ++c) {
       const int32_t pad = int32_t(query_pad(c_cnt[c]));
       o_A[c] = pl.add<__half>(size_t(pad) * Kp_max);
+      o_At[c] = pl.add<__half>(size_t(pad) * kTailK);
       o_qn[c] = pl.add<float>(pad);
       o_scal[c] = pl.add<float>(4);
       o_part[c] = pl.add<double>(sweep_part_count(h->n_pad, pad, h->num_sms));
@@ -1499,7 +1511,8 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       // speculative exact mode: the query encode also computes the exact-mode flags
       // exact-mode gaussian sweeps carry the query norms in the operand (the MMA yields -d2/2)
       QueryOperand q = encode_queries(h, e, Qc, cn, pad, at<__half>(h->ws, o_A[c]), at<float>(h->ws, o_qn[c]),
-                                      at<float>(h->ws, o_scal[c]), s, guard_flags, mode == 0 && family == DK_GAUSSIAN);
+                                      at<float>(h->ws, o_scal[c]), s, guard_flags, mode == 0 && family == DK_GAUSSIAN,
+                                      at<__half>(h->ws, o_At[c]));
       if (guard_flags) {
         DK_CUDA(cudaMemcpyAsync(h->flag_host + c, guard_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         DK_CUDA(cudaEventRecord(h->flag_event, s));

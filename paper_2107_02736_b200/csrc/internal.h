@@ -107,22 +107,26 @@ inline void set_dynamic_smem(K* kernel, size_t bytes) {
   } while (0)
 
 // Norm columns of the exact / fp16 operands (prep.cu): 3 for the row norm, 3 for the query norm.
-// They ride in the K padding only.  Where they would open a K-block of their own (d within 6 of a
-// multiple of 64: c2, d = 128) they cost more than the epilogue work they save — measured on c2:
-// 2.67 ms without, 2.83 ms with a full third K-block, 3.74 ms with 136-half rows (unaligned TMA
-// rows), 2.69-2.98 ms with 192-half rows and a 134-column tensor-map extent (zero-filled box),
-// for 2 to 6 of 16 exponentials on the FMA pipe — so those operands go without them.
+// They ride in the K padding when they fit (d = 100: 106 of 128).  When d is within 6 of a
+// multiple of 64 (c2, d = 128) they go to a separate 16-column "tail" operand instead — one
+// 16-wide MMA step on 32-byte-swizzled tiles (8 KB per dataset tile) — because a whole extra
+// 64-column K-block costs more feed than the epilogue saves (c2: 2.67 -> 2.83 ms).
 constexpr int32_t kAugCols = 6;
-inline bool enc_has_aug(int32_t d, int mode) {
-  static const bool force = [] {  // A/B: norm columns even when they open a K-block
-    const char* v = std::getenv("DK_AUG_FORCE");
-    return v != nullptr && std::atoi(v) != 0;
-  }();
-  return mode != 1 && (force || (int64_t(d) + kAugCols + 63) / 64 == (int64_t(d) + 63) / 64);
+constexpr int32_t kTailK = 16;
+inline bool enc_aug_main(int32_t d, int mode) {
+  return mode != 1 && (int64_t(d) + kAugCols + 63) / 64 == (int64_t(d) + 63) / 64;
 }
+inline bool enc_aug_tail(int32_t d, int mode) {
+  static const bool off = [] {  // A/B: DK_AUG_TAIL=0 leaves such operands without norm columns
+    const char* v = std::getenv("DK_AUG_TAIL");
+    return v != nullptr && std::atoi(v) == 0;
+  }();
+  return mode != 1 && !off && !enc_aug_main(d, mode);
+}
+inline bool enc_has_aug(int32_t d, int mode) { return enc_aug_main(d, mode) || enc_aug_tail(d, mode); }
 // padded K (row stride, a multiple of 64) of an encoding: split3 3d, exact / fp16 d (+ norm columns)
 inline int32_t enc_kp(int32_t d, int mode) {
-  const int64_t k = mode == 1 ? 3 * int64_t(d) : int64_t(d) + (enc_has_aug(d, mode) ? kAugCols : 0);
+  const int64_t k = mode == 1 ? 3 * int64_t(d) : int64_t(d) + (enc_aug_main(d, mode) ? kAugCols : 0);
   return int32_t((k + 63) / 64 * 64);
 }
 inline int32_t enc_kblocks(int32_t Kp) { return (Kp + 63) / 64; }
@@ -133,6 +137,8 @@ struct Encoding {
   int32_t Kp = 0;           // padded K (multiple of 64)
   int32_t d = 0;            // data columns per part (K used = d, or 3d for split3)
   __half* B = nullptr;      // [n_pad][Kp]
+  __half* T = nullptr;      // [n_pad][kTailK] norm-column tail (enc_aug_tail), else nullptr
+  CUtensorMap tmap_t;       // T boxes of 256 rows x 16 columns, 32-byte swizzle
   float* xn = nullptr;      // [n_pad] |x - mu|^2 in fp32
   double* mu = nullptr;     // [d] centring (nullptr = none)
   float* sx = nullptr;      // device scalar: power-of-two scale applied to x
@@ -245,24 +251,30 @@ struct QueryOperand {
   float* qn = nullptr;        // [nq_pad]
   float* m2s = nullptr;       // device scalar
   bool aug = false;           // A carries the query-norm columns (KDE: the MMA yields -d2/2)
+  __half* T = nullptr;        // [nq_pad][kTailK] query tail (the encoding has a tail)
   CUtensorMap tmap;
+  CUtensorMap tmap_t;
 };
 
 CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint32_t box_rows);
+// rows x kTailK halves, boxes of box_rows x 16 with 32-byte swizzle (the norm-column tail)
+CUtensorMap make_tmap_tail_f16(const void* base, uint64_t rows, uint32_t box_rows);
 
 // dataset prep
 void launch_row_stats(const float* X, int64_t n, int32_t d, double* xn64, uint32_t* flags, cudaStream_t s);
 void launch_column_mean(const float* X, int64_t n, int32_t d, double* partial, int32_t row_blocks, double* mu,
                         cudaStream_t s);
 void launch_encode_rows(const float* X, int64_t n, int64_t n_pad, int32_t d, int mode, const double* mu,
-                        int32_t Kp, __half* B, float* xn, float* scale, uint32_t* maxabs_bits, cudaStream_t s);
+                        int32_t Kp, __half* B, float* xn, float* scale, uint32_t* maxabs_bits, cudaStream_t s,
+                        __half* tail = nullptr);
 // queries
 void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags, cudaStream_t s);
 // check_flags (mode 0 only, nullable): also OR query_check's exact-mode flags into *check_flags
 // aug (exact / fp16 modes): write the query-norm columns (the KDE sweeps; k-NN leaves them zero)
 void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
                            int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
-                           cudaStream_t s, uint32_t* check_flags = nullptr, bool aug = false);
+                           cudaStream_t s, uint32_t* check_flags = nullptr, bool aug = false,
+                           __half* tail = nullptr);
 void launch_reduce_partials(const double* part, int32_t nparts, int32_t nq_pad, int64_t nq, double scale,
                             double* out, cudaStream_t s);
 

@@ -1492,6 +1492,7 @@ void free_knn_clusters(KnnClusters& kc) {
                   static_cast<void*>(kc.off), static_cast<void*>(kc.nbr)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(kc.enc.B), static_cast<void*>(kc.enc.xn), static_cast<void*>(kc.enc.sx),
+                  static_cast<void*>(kc.enc.T),
                   static_cast<void*>(kc.enc3.B), static_cast<void*>(kc.enc3.xn), static_cast<void*>(kc.enc3.sx)})
     if (p) cudaFree(p);
   if (kc.stat_host) cudaFreeHost(kc.stat_host);

@@ -121,7 +121,8 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
                               const double* __restrict__ mu, int32_t Kp, const uint32_t* __restrict__ maxabs_bits,
                               const float* __restrict__ other_scale, __half* __restrict__ out,
                               float* __restrict__ norms, float* __restrict__ scale_out,
-                              float* __restrict__ m2s_out, uint32_t* __restrict__ check_flags, int aug) {
+                              float* __restrict__ m2s_out, uint32_t* __restrict__ check_flags, int aug,
+                              __half* __restrict__ tail) {
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   // queries with norm columns share the dataset's scale (the norm terms must carry one scale)
@@ -134,6 +135,7 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
   __half* o = out + row * Kp;
   if (row >= rows) {
     for (int k = lane; k < Kp; k += 32) o[k] = __float2half_rn(0.f);
+    if (tail && lane < kTailK) tail[row * kTailK + lane] = __float2half_rn(0.f);
     if (lane == 0) norms[row] = 0.f;
     return;
   }
@@ -162,7 +164,7 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
       o[k] = w;
     } else {
       if (k >= d) {
-        if (aug == 0 || k >= d + kAugCols) o[k] = __float2half_rn(0.f);  // norm columns: written below
+        if (aug == 0 || tail || k >= d + kAugCols) o[k] = __float2half_rn(0.f);  // norm columns: below
         continue;
       }
       double x = double(v[k]);
@@ -174,6 +176,7 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
   }
   nrm = warp_sum_d(nrm);
   if (lane == 0) norms[row] = float(nrm);
+  if (tail && lane >= kAugCols && lane < kTailK) tail[row * kTailK + lane] = __float2half_rn(0.f);
   if (mode != 1 && aug != 0 && lane < kAugCols) {
     // |v|^2 / 2 (scaled) = w1 b1 + w2 b2 + w3 b3.  Exact integers: b from floor divisions (xn <
     // 2^23: b1 < 2^11, b2 < 64, b3 < 32 half-integers, all exact in fp16).  Scaled fp16: each b the
@@ -201,7 +204,8 @@ __global__ void encode_kernel(const T* __restrict__ V, int64_t rows, int64_t row
     if (aug == 1) val = lane < 3 ? float(-b[lane]) : float(w[lane - 3]);
     else val = lane < 3 ? float(w[lane]) : float(-b[lane - 3]);
     if (bad && aug == 2 && lane == 3) val = __int_as_float(0x7fc00000);
-    o[d + lane] = __float2half_rn(val);
+    if (tail) tail[row * kTailK + lane] = __float2half_rn(val);
+    else o[d + lane] = __float2half_rn(val);
   }
   if (check_flags) {
     f = warp_or(f);
@@ -284,16 +288,20 @@ void launch_column_mean(const float* X, int64_t n, int32_t d, double* partial, i
 }
 
 void launch_encode_rows(const float* X, int64_t n, int64_t n_pad, int32_t d, int mode, const double* mu, int32_t Kp,
-                        __half* B, float* xn, float* scale, uint32_t* maxabs_bits, cudaStream_t s) {
+                        __half* B, float* xn, float* scale, uint32_t* maxabs_bits, cudaStream_t s, __half* tail) {
   DK_CUDA(cudaMemsetAsync(maxabs_bits, 0, sizeof(uint32_t), s));
   if (mode != 0) {
     maxabs_kernel<float><<<1184, 256, 0, s>>>(X, n, d, mu, maxabs_bits);
     DK_CHECK_LAUNCH();
   }
+  // norm columns: in the main operand when they fit its padding, else in the tail (if given)
+  const bool in_main = enc_aug_main(d, mode);
+  if (in_main) tail = nullptr;
+  const bool row_aug = in_main || (enc_aug_tail(d, mode) && tail != nullptr);
   const int64_t threads = n_pad * 32;
   encode_kernel<float><<<unsigned((threads + 255) / 256), 256, 0, s>>>(X, n, n_pad, d, mode, mu, Kp, maxabs_bits,
                                                                       nullptr, B, xn, scale, nullptr, nullptr,
-                                                                      enc_has_aug(d, mode) ? 1 : 0);
+                                                                      row_aug ? 1 : 0, tail);
   DK_CHECK_LAUNCH();
 }
 
@@ -305,9 +313,11 @@ void launch_query_check(const double* Q, int64_t nq, int32_t d, uint32_t* flags,
 
 void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t d, int mode, const double* mu,
                            int32_t Kp, const float* sx, __half* A, float* qn, float* m2s, uint32_t* maxabs_bits,
-                           cudaStream_t s, uint32_t* check_flags, bool aug) {
+                           cudaStream_t s, uint32_t* check_flags, bool aug, __half* tail) {
+  const bool q_aug = aug && (enc_aug_main(d, mode) || (enc_aug_tail(d, mode) && tail != nullptr));
+  tail = (q_aug && !enc_aug_main(d, mode)) ? tail : nullptr;
   // fp16 queries with norm columns take the dataset's scale: no maximum to find
-  if (mode != 0 && !(mode == 2 && aug && enc_has_aug(d, mode))) {
+  if (mode != 0 && !(mode == 2 && q_aug)) {
     DK_CUDA(cudaMemsetAsync(maxabs_bits, 0, sizeof(uint32_t), s));
     const int64_t total = nq * d;
     const unsigned blocks = unsigned(std::min<int64_t>(1184, (total + 255) / 256 + 1));
@@ -317,7 +327,7 @@ void launch_encode_queries(const double* Q, int64_t nq, int32_t nq_pad, int32_t 
   const int64_t threads = int64_t(nq_pad) * 32;
   encode_kernel<double><<<unsigned((threads + 255) / 256), 256, 0, s>>>(
       Q, nq, nq_pad, d, mode, mu, Kp, maxabs_bits, sx, A, qn, nullptr, m2s, mode == 0 ? check_flags : nullptr,
-      (aug && enc_has_aug(d, mode)) ? 2 : 0);
+      q_aug ? 2 : 0, tail);
   DK_CHECK_LAUNCH();
 }
 

@@ -215,6 +215,18 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
   return d;
 }
 
+// Shared-memory matrix descriptor, K-major operand, 32-byte swizzle (16 fp16 per row: the
+// norm-column tail slice): 8-row groups 256 bytes apart, layout type 6 (SWIZZLE_32B).
+__device__ __forceinline__ uint64_t sw32_kmajor_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;            // LBO (ignored for swizzled K-major)
+  d |= static_cast<uint64_t>(256u >> 4) << 32;     // SBO
+  d |= static_cast<uint64_t>(1u) << 46;            // version
+  d |= static_cast<uint64_t>(6u) << 61;            // SWIZZLE_32B
+  return d;
+}
+
 // Instruction descriptor for kind::f16: fp16 A/B (format 0), fp32 D, K-major A and B.
 __host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N) {
   return (1u << 4)            // D format F32

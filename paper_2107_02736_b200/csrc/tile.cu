@@ -111,7 +111,7 @@ Plan make_plan(int kblocks, int ntiles, int ngroups, int nslots, int mode, bool 
 
 template <int MODE, bool kPair>
 void launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const TileParams& p, int grid, size_t smem,
-                 cudaStream_t s) {
+                 cudaStream_t s, const CUtensorMap* tat = nullptr, const CUtensorMap* tbt = nullptr) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -131,7 +131,7 @@ void launch_mode(const CUtensorMap& ta, const CUtensorMap& tb, const TileParams&
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DK_CUDA(cudaLaunchKernelEx(&cfg, tile_kernel<MODE, kPair>, ta, tb, p));
+  DK_CUDA(cudaLaunchKernelEx(&cfg, tile_kernel<MODE, kPair>, ta, tb, tat ? *tat : ta, tbt ? *tbt : tb, p));
   DK_CHECK_LAUNCH();
 }
 
@@ -159,6 +159,19 @@ CUtensorMap make_tmap_2d_f16(const void* base, uint64_t rows, uint64_t kp, uint3
   return m;
 }
 
+CUtensorMap make_tmap_tail_f16(const void* base, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {uint64_t(kTailK), rows};
+  cuuint64_t strides[1] = {uint64_t(kTailK) * 2};
+  cuuint32_t box[2] = {uint32_t(kTailK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error{DK_ECUDA, "cuTensorMapEncodeTiled (tail) failed: " + std::to_string(int(r))};
+  return m;
+}
+
 bool tile_major_fits(int32_t Kp) {
   return tile_smem_bytes(enc_kblocks(Kp), 0, 3, MODE_FILTER, false, true) <= kMaxSmem;
 }
@@ -182,13 +195,28 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   const int ntiles_all = int(a.n_pad / kBN);
   const int ntiles = (ntiles_all + a.tile_stride - 1) / a.tile_stride;
   const int nqb = q.nq_pad / kBM;
-  const bool pr = a.ulist == nullptr && a.mode != MODE_KDE_COLD && !q.aug && use_pair(nqb);
+  const bool pr = a.ulist == nullptr && a.mode != MODE_KDE_COLD && !q.aug && use_pair(nqb);  // never with norm columns
   const int ngroups = pr ? nqb / 2 : nqb;
   const int nslots = pr ? num_sms / 2 : num_sms;  // CTAs (or CTA pairs) resident at once
   const bool tmajor = a.tmajor != 0;
   if (tmajor && (a.mode != MODE_FILTER || a.ulist == nullptr || a.blist == nullptr))
     throw Error{DK_EINVAL, "internal: tile-major sweeps are FILTER tile lists"};
-  const Plan pl = make_plan(kblocks, ntiles, ngroups, nslots, a.mode, pr, tmajor);
+  // norm columns in tail operands: only the resident-A KDE sweeps (otherwise the plain epilogue:
+  // the main A of a tail-mode query operand is plain q)
+  const bool want_tail = q.aug && q.T != nullptr && e.T != nullptr && a.ulist == nullptr && !pr &&
+                         (a.mode == MODE_KDE_GAUSS || a.mode == MODE_KDE_COLD);
+  Plan pl = make_plan(kblocks, ntiles, ngroups, nslots, a.mode, pr, tmajor);
+  bool tail = false;
+  if (want_tail && pl.a_resident) {
+    int st = pl.stages;
+    while (st > 2 && tile_smem_bytes(kblocks, 1, st, a.mode, false, false, true) > kMaxSmem) --st;
+    if (tile_smem_bytes(kblocks, 1, st, a.mode, false, false, true) <= kMaxSmem) {
+      tail = true;
+      pl.stages = st;
+      pl.smem = tile_smem_bytes(kblocks, 1, st, a.mode, false, false, true);
+    }
+  }
+  const bool aug = q.aug && (q.T == nullptr || tail);  // norm columns usable by this sweep
 
   TileParams p{};
   p.nq = q.nq;
@@ -233,6 +261,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.hist = a.hist;
   p.hot_bits = a.hot_bits;
   p.hot_thr = a.hot_thr;
+  p.tail = tail ? 1 : 0;
   p.tmajor = tmajor ? 1 : 0;
   p.blist = a.blist;
   p.unit_counter = a.unit_counter;
@@ -259,7 +288,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
       // exp2 polynomial and run power-capped: every exponential on MUFU is faster there
       // (c3: 6.6 vs 7.0 ms); the single-pass encodings offload 2 of 16 pairs (c2: 2.83 vs 2.98 ms),
       // 4 of 16 with the norm columns (q.aug: one multiply per pair before the exponential)
-      if (q.aug) launch_mode<MODE_KDE_GAUSS_AUG, false>(q.tmap, tb, p, grid, pl.smem, s);
+      if (aug) launch_mode<MODE_KDE_GAUSS_AUG, false>(q.tmap, tb, p, grid, pl.smem, s, &q.tmap_t, &e.tmap_t);
       else if (kblocks >= 4) launch_any<MODE_KDE_GAUSS_MUFU>(pr, q.tmap, tb, p, grid, pl.smem, s);
       else launch_any<MODE_KDE_GAUSS>(pr, q.tmap, tb, p, grid, pl.smem, s);
       break;
@@ -269,7 +298,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
     case MODE_FILTER: launch_any<MODE_FILTER>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_NULL: launch_any<MODE_NULL>(pr, q.tmap, tb, p, grid, pl.smem, s); break;
     case MODE_KDE_COLD:
-      if (q.aug) launch_mode<MODE_KDE_COLD_AUG, false>(q.tmap, tb, p, grid, pl.smem, s);
+      if (aug) launch_mode<MODE_KDE_COLD_AUG, false>(q.tmap, tb, p, grid, pl.smem, s, &q.tmap_t, &e.tmap_t);
       else launch_mode<MODE_KDE_COLD, false>(q.tmap, tb, p, grid, pl.smem, s);
       break;
     case MODE_KDE_HOT: launch_mode<MODE_KDE_HOT, false>(q.tmap, tb, p, grid, pl.smem, s); break;

@@ -135,6 +135,10 @@ struct TileParams {
   // half = rows quarter*32 + lane of the block, columns [128 half, 128 half + 128) of the tile
   uint32_t* hot_bits;
   float hot_thr;           // MODE_KDE_COLD: a tile half whose fp32 sum exceeds this is hot
+  // norm-column tail (prep.cu, d within 6 of a multiple of 64): the query block's 16-column tail
+  // rides with the resident A, each tile's 256 x 16 tail takes the column-norm slot (8 KB), and
+  // one more 16-wide MMA step closes the accumulation (KDE_GAUSS_AUG / KDE_COLD_AUG only)
+  int32_t tail;
   const float* xn;         // [n_pad] |x|^2 (encoding-consistent)
   const float* qn;         // [nq_pad] |q|^2
   const float* m2s;        // device scalar: -2 / (scale_q * scale_x)
@@ -148,8 +152,11 @@ struct TileParams {
   const uint32_t* guard;     // optional: the sweep is skipped when (*guard & 6) != 0 (queries not exact-mode)
 };
 
+constexpr int kTailABytes = kBM * 16 * 2;  // 4 KB: the query block's norm-column tail
+constexpr int kTailBBytes = kBN * 16 * 2;  // 8 KB: a dataset tile's norm-column tail (a column-norm slot)
+
 __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode, bool pair,
-                                                  bool tmajor = false) {
+                                                  bool tmajor = false, bool tail = false) {
   size_t a = a_resident ? size_t(kblocks) * kABlockBytes : size_t(stages) * kABlockBytes;
   size_t b = size_t(stages) * (pair ? kBBlockBytes / 2 : kBBlockBytes);
   if (tmajor) {  // resident dataset tile + ring of query K-blocks
@@ -157,7 +164,8 @@ __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, i
     b = size_t(kblocks) * kBBlockBytes;
   }
   size_t stage = (mode == MODE_FILTER || mode == MODE_HIST) ? size_t(kBM) * kStageCap * 8 + kBM * 4 : 0;
-  return 1024 /*align slack*/ + a + b + size_t(kXnSlots) * kBN * 4 + stage + 512 /*barriers*/;
+  const size_t xslots = size_t(kXnSlots) * (tail ? kTailBBytes : kBN * 4) + (tail ? kTailABytes : 0);
+  return 1024 /*align slack*/ + a + b + xslots + stage + 512 /*barriers*/;
 }
 
 
@@ -397,6 +405,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"
 template <int MODE, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
+                const __grid_constant__ CUtensorMap tmapAt, const __grid_constant__ CUtensorMap tmapBt,
                 const TileParams p) {
   // speculative exact-mode launch (capi.cu dk_naive): the host has not waited for the query
   // check, so a batch that turned out fractional skips this sweep and is redone in split3
@@ -410,14 +419,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kBStage = kPair ? kBBlockBytes / 2 : kBBlockBytes;  // B bytes per CTA per stage
   const bool tmajor = MODE == MODE_FILTER && !kPair && p.tmajor != 0;
   uint8_t* smemA = smem;
-  uint8_t* smemB = smem + (p.a_resident ? size_t(p.kblocks) * kABlockBytes : size_t(stages) * kABlockBytes);
-  float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBStage);  // [kXnSlots][256]
+  const bool tail = is_aug(MODE) && p.tail != 0;
+  // [A: resident K-blocks or ring][A tail (tail mode)][B ring][column-norm / B-tail slots]
+  uint8_t* smemAt = smem + (p.a_resident ? size_t(p.kblocks) * kABlockBytes : size_t(stages) * kABlockBytes);
+  uint8_t* smemB = smemAt + (tail ? kTailABytes : 0);
+  float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBStage);  // [kXnSlots][xslot]
+  const int xslot = tail ? kTailBBytes / 4 : kBN;  // floats per slot
   if (tmajor) {  // [resident tile: kblocks x 32 KB][ring: stages x 16 KB query K-blocks][norms]
     smemB = smem;
     smemA = smem + size_t(p.kblocks) * kBBlockBytes;
     smemX = reinterpret_cast<float*>(smemA + size_t(stages) * kABlockBytes);
   }
-  unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smemX + kXnSlots * kBN);  // FILTER staging
+  unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smemX + kXnSlots * xslot);  // FILTER staging
   constexpr bool kStage = MODE == MODE_FILTER || MODE == MODE_HIST;  // FILTER staging / HIST bins
   uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (kStage ? kBM * kStageCap : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(scnt + (kStage ? kBM : 0));
@@ -555,9 +568,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < p.kblocks; ++kb)
               tma_load_2d_pair(smemA + size_t(kb) * kABlockBytes, &tmapA, afull_bar, kb * kBK, qb * kBM, pol_a);
           } else {
-            mbar_arrive_expect_tx(afull_bar, uint32_t(p.kblocks) * kABlockBytes);
+            mbar_arrive_expect_tx(afull_bar, uint32_t(p.kblocks) * kABlockBytes + (tail ? kTailABytes : 0u));
             for (int kb = 0; kb < p.kblocks; ++kb)
               tma_load_2d(smemA + size_t(kb) * kABlockBytes, &tmapA, afull_bar, kb * kBK, qb * kBM, pol_a);
+            if (tail) tma_load_2d(smemAt, &tmapAt, afull_bar, 0, qb * kBM, pol_a);
           }
         }
         // tile-list mode: the next tile id is loaded one tile ahead (off the issue path)
@@ -571,11 +585,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             col0 = t * p.tile_stride * kBN;
           }
-          {  // column norms of this tile -> own smem ring slot
+          {  // column norms of this tile (tail mode: its norm-column tail) -> own smem ring slot
             const uint32_t xs = titer % kXnSlots;
             mbar_wait(&xempty_bar[xs], ((titer / kXnSlots) & 1) ^ 1);
-            mbar_arrive_expect_tx(&xfull_bar[xs], kBN * 4);
-            bulk_load(smemX + xs * kBN, p.xn + col0, kBN * 4, &xfull_bar[xs]);
+            if (tail) {
+              mbar_arrive_expect_tx(&xfull_bar[xs], kTailBBytes);
+              tma_load_2d(smemX + xs * xslot, &tmapBt, &xfull_bar[xs], 0, col0, pol_b);
+            } else {
+              mbar_arrive_expect_tx(&xfull_bar[xs], kBN * 4);
+              bulk_load(smemX + xs * xslot, p.xn + col0, kBN * 4, &xfull_bar[xs]);
+            }
           }
           for (int kb = 0; kb < p.kblocks; ++kb) {
             DK_TWAIT(5, mbar_wait(&empty_bar[stage], phase ^ 1));
@@ -651,7 +670,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int uiter = 0;
+      uint32_t titer = 0;
       const uint32_t a0 = smem_u32(smemA), b0 = smem_u32(smemB);
+      const uint64_t at_desc = sw32_kmajor_desc(smem_u32(smemAt));
       for (int u = first_unit; u < nunits; u += unit_step, ++uiter) {
         const int cc = u / ngroups;
         int t0 = cc * p.tiles_per_unit;
@@ -684,6 +705,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             else mma_commit(&empty_bar[stage]);
             if (++stage == stages) { stage = 0; phase ^= 1; }
           }
+          if (tail) {  // the 16 norm columns: A tail (resident) x this tile's B tail (column-norm slot)
+            const uint32_t xs = titer % kXnSlots;
+            mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
+            tc_fence_after();
+            mma_f16_ss(d_tmem, at_desc, sw32_kmajor_desc(smem_u32(smemX + xs * xslot)), idesc, 1u);
+          }
+          ++titer;
           if constexpr (kPair) mma_commit_pair_mc(&tfull_bar[acc], uint16_t(0x3));
           else mma_commit(&tfull_bar[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -724,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         DK_TWAIT(1, mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1));
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(group * kBN + half * 128);
         const int64_t tbase = int64_t(t) * p.tile_stride * kBN + half * 128;
-        const float* xsm = smemX + xs * kBN + half * 128;
+        const float* xsm = smemX + xs * xslot + half * 128;
         float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
 #pragma unroll 1
         for (int sub = 0; sub < 2; ++sub) {
@@ -889,7 +917,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         const int64_t cbase = int64_t(p.tlist != nullptr ? p.tlist[t] : t * p.tile_stride) * kBN + cg * 64;
-        const float* xsm = smemX + xs * kBN + cg * 64;
+        const float* xsm = smemX + xs * xslot + cg * 64;
         const bool full = cbase + 64 <= p.n;
         float2 a0 = MODE == MODE_HIST ? hpar : make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f), b0 = a0;
         if (any) {  // warp-uniform
