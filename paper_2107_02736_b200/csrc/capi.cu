@@ -1460,7 +1460,11 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     // Host queries of a large batch run as two chunks: the copy of the second (3/4 of the
     // batch) overlaps the sweep of the first on a side stream, hiding most of the H2D time.
     const bool host_q = !is_device_ptr(Q);
-    const int64_t split = (host_q && nq >= 4096) ? round_up(nq / 4, 256) : nq;
+    static const int64_t split_div = [] {  // A/B: first chunk = 1/div of the batch
+      const char* v = std::getenv("DK_E2E_SPLIT");
+      return v ? std::max<int64_t>(2, std::atoll(v)) : int64_t(4);
+    }();
+    const int64_t split = (host_q && nq >= 4096) ? round_up(nq / split_div, 256) : nq;
     const int64_t c_beg[2] = {0, split};
     const int64_t c_cnt[2] = {split, nq - split};
     const int nchunks = c_cnt[1] > 0 ? 2 : 1;
@@ -1536,6 +1540,13 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       launch_reduce_partials(a.part, ncc * kColGroups, pad, cn, scale, od + q0, s);
       if (!out_dev) copy_out(out + q0, od + q0, size_t(cn) * sizeof(double), s);
     };
+    // Integer dataset: the exact-mode sweeps are launched without waiting for the query check.
+    // Each reads its chunk's flags and skips itself for fractional queries; the host waits for
+    // the flags only after every chunk is enqueued (the last record of flag_event follows both
+    // chunks' flag copies) and redoes a fractional chunk in split3.  No host round trip sits
+    // between the chunks (round 1 waited per chunk, so chunk 1's sweep was enqueued only after
+    // chunk 0's sweep had drained the stream) or between consecutive calls.
+    const bool speculative = !hyb && h->precision == DK_PREC_AUTO && h->int_exact;
     for (int c = 0; c < nchunks; ++c) {
       if (c == 1) DK_CUDA(cudaStreamWaitEvent(s, h->copy_done, 0));
       if (hyb) {
@@ -1543,22 +1554,20 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
         if (!out_dev && c == nchunks - 1) copy_out(out, od, size_t(nq) * sizeof(double), s);
         continue;
       }
-      if (h->precision == DK_PREC_AUTO && h->int_exact) {
-        // Integer dataset: launch the exact-mode sweep without waiting for the query check.
-        // The sweep reads the check's flags and skips itself for fractional queries; the host
-        // waits only for the (early) check result — overlapped with the sweep — and redoes a
-        // fractional chunk in split3.  No host round trip sits between consecutive calls.
+      if (speculative) {
         uint32_t* flags = at<uint32_t>(h->ws, o_fl[c]);
         DK_CUDA(cudaMemsetAsync(flags, 0, sizeof(uint32_t), s));
         run_sweep(c, 0, flags);
-        DK_CUDA(cudaEventSynchronize(h->flag_event));
-        const uint32_t f = h->flag_host[c];
-        DK_REQUIRE(!(f & 1u), "queries must be finite");
-        if (f & 6u) run_sweep(c, 1, nullptr);
       } else {
         run_sweep(c, choose_mode(h, Qd + size_t(c_beg[c]) * h->d, c_cnt[c], at<uint32_t>(h->ws, o_fl[c]), s),
                   nullptr);
       }
+    }
+    if (speculative) {
+      DK_CUDA(cudaEventSynchronize(h->flag_event));
+      for (int c = 0; c < nchunks; ++c) DK_REQUIRE(!(h->flag_host[c] & 1u), "queries must be finite");
+      for (int c = 0; c < nchunks; ++c)
+        if (h->flag_host[c] & 6u) run_sweep(c, 1, nullptr);
     }
     if (!out_dev) DK_CUDA(cudaStreamSynchronize(s));
   });
