@@ -3,8 +3,10 @@
 
 Exact integer rows: the norm split is exact, so d2 is exact and the KDE matches the fp64 oracle
 (naive_kde, estimators.py:144-149) to the exponential's own rounding — checked next to the exact-mode
-limit (squared norms just under 2^23, the largest b1).  d = 64 has no padding for the columns and
-keeps the plain epilogue (also for the two-precision sweep, KDE_COLD).
+limit (squared norms just under 2^23, the largest b1).  d = 50 / 57 / 100 keep the columns in the
+K padding; d = 64 has none, so they go to the 16-column tail operand (one more 16-wide MMA step on
+32-byte-swizzled tiles), also for the two-precision sweep's fp16 pass (KDE_COLD_AUG); DK_AUG_TAIL=0
+falls back to the plain epilogue.
 """
 
 import numpy as np
@@ -38,8 +40,8 @@ def test_exact_integer_rows_near_the_norm_limit(d):
     assert _rel(got, ref) < 2e-6
 
 
-def test_two_precision_without_norm_columns(monkeypatch):
-    """d = 64: the fp16 sweep of the two-precision KDE keeps the plain epilogue (KDE_COLD)."""
+def test_two_precision_with_tail_norm_columns(monkeypatch):
+    """d = 64: the fp16 pass of the two-precision KDE takes its norm columns from the tail operand."""
     X = workloads._c3_rows(3, 160_000)[:, :64].copy()
     X /= np.linalg.norm(X, axis=1, keepdims=True)
     Q = workloads._c3_rows(4, 2048).astype(np.float64)[:, :64].copy()
@@ -52,3 +54,34 @@ def test_two_precision_without_norm_columns(monkeypatch):
     assert _rel(got, ref3) < 5e-6
     sel = np.arange(0, 2048, 256)
     assert _rel(got[sel], O.naive_kde(O.Data(X), "gaussian", h, Q[sel])) < 1e-5
+
+
+def test_exact_tail_matches_plain_epilogue_in_a_fresh_process():
+    """The tail path (d = 128, c2's shape) against the plain epilogue of the same library
+    (DK_AUG_TAIL=0, read once per process: run in a subprocess) on integer rows: both exact d2,
+    so the values agree to the exponentials' rounding."""
+    import os
+    import subprocess
+    import sys
+
+    from dk_testutil import REPO
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_2107_02736_b200 as g\n"
+        "rng = np.random.default_rng(3)\n"
+        "X = rng.integers(0, 256, size=(30000, 128)).astype(np.float32)\n"
+        "Q = rng.integers(0, 256, size=(5000, 128)).astype(np.float64)\n"
+        "ds = g.Dataset.from_array(X)\n"
+        "np.save(sys.argv[1], g.naive_kde(ds, g.KernelSpec('gaussian', 900.0), Q).values)\n" % REPO
+    )
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        outs = []
+        for env_tail in ("1", "0"):
+            path = os.path.join(td, f"v{env_tail}.npy")
+            env = dict(os.environ, DK_AUG_TAIL=env_tail)
+            subprocess.run([sys.executable, "-c", code, path], check=True, env=env)
+            outs.append(np.load(path))
+    assert _rel(outs[0], outs[1]) < 2e-6
