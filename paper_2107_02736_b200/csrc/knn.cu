@@ -36,6 +36,10 @@ namespace dk {
 namespace {
 
 constexpr int kSelHist = 1024;  // histogram bins of the k-NN selection (4 per thread of a 256-thread block)
+// lanes per exactly re-ranked row in every selection path (one summation order, so a query's
+// distances are bit-identical whichever path serves it); 4 lanes (8 rows per warp step, 6-7 float4
+// loads per lane in flight) measured faster than 8 (c3 k-NN 1.65 -> 1.58 ms) and 16 (1.67 ms)
+constexpr int kExactG = 4;
 
 struct Key128 {
   unsigned long long hi;  // fp64 bits of d2 (>= 0, so bit order == numeric order)
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
   for (int j = threadIdx.x; j < d; j += blockDim.x) qv[j] = Q[size_t(q) * d + j];
   const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  constexpr int G = 8;  // lanes per candidate: 4 candidates per warp step
+  constexpr int G = kExactG;  // lanes per candidate: 32 / G candidates per warp step
   const int grp = lane / G, gl = lane % G;
   __shared__ uint32_t s_lo, s_hi, s_bstar, s_tmax, s_ns;
   __shared__ uint32_t s_wsum[32];
@@ -487,7 +491,7 @@ __global__ void __launch_bounds__(256) select_slow_kernel(
   Key128* top = reinterpret_cast<Key128*>(sbuf + B);
   double* qv = reinterpret_cast<double*>(top + Kp + W);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  constexpr int G = 8;
+  constexpr int G = kExactG;
   const int grp = lane / G, gl = lane % G;
   __shared__ int s_stop;
   for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
@@ -555,9 +559,9 @@ __global__ void exact_knn_kernel(const float* __restrict__ X, int64_t n, int64_t
     __syncthreads();
     for (int i = threadIdx.x; i < Kp; i += blockDim.x) buf[i] = Key128{~0ull, ~0ull};
     for (int64_t pos = 0; pos < n; pos += chunk) {
-      // 8 lanes per row with the selection's summation order (exact_d2_group<8>), so a query
+      // kExactG lanes per row with the selection's summation order (exact_d2_group), so a query
       // gets bit-identical distances whichever path served it
-      constexpr int G = 8;
+      constexpr int G = kExactG;
       const int grp = lane / G, gl = lane % G;
       for (int i0 = warp * (32 / G); i0 < chunk; i0 += nwarps * (32 / G)) {
         const int i = i0 + grp;
