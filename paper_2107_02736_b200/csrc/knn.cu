@@ -775,17 +775,19 @@ __global__ void nearest_cluster_kernel(const double* __restrict__ dq, int64_t nq
 // rad_c)^2 <= tau_q + eps_q (approx d2 >= exact d2 - eps_q); a tile is needed when any
 // cluster of its range is.  fp64 slack: dq shrunk by 1e-12 relative (rad is inflated at
 // build), the threshold grown by 1e-6 relative.
-__global__ void __launch_bounds__(256) block_tile_lists_kernel(
+constexpr int kListThreads = 1024;  // block_tile_lists: 32 warps, 4 rows each
+__global__ void __launch_bounds__(kListThreads) block_tile_lists_kernel(
     const double* __restrict__ dq, int32_t C, const int32_t* __restrict__ qperm, int64_t bn,
     const float* __restrict__ tau, const float* __restrict__ qn, float xn_max, float eps_rel,
     const double* __restrict__ rad, const int32_t* __restrict__ tclo, const int32_t* __restrict__ tchi,
     int32_t ntiles, int32_t* __restrict__ tlist, int32_t* __restrict__ tcount, uint32_t* __restrict__ bits) {
-  // need: one bit per cluster.  Each warp takes every 8th row of the block and sweeps that
-  // query's distances to all clusters with coalesced reads (lanes over clusters), OR-ing a ballot
-  // per 32 clusters into shared memory (round 1: one thread per cluster looping over the rows,
-  // latency-bound, 149 us on c3).
+  // need: one bit per cluster.  Each of the 32 warps takes every 32nd row of the block and sweeps
+  // that query's distances to all clusters with coalesced reads (lanes over clusters), OR-ing a
+  // ballot per 32 clusters into shared memory (round 1: one thread per cluster looping over the
+  // rows, latency-bound, 149 us on c3; 8 warps: 108 us on c3, 0.63 ms per c5 batch).
   extern __shared__ uint32_t need[];
-  __shared__ int s_wcnt[8];
+  constexpr int kW = kListThreads / 32;
+  __shared__ int s_wcnt[kW];
   __shared__ int s_base;
   const int qb = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -794,7 +796,7 @@ __global__ void __launch_bounds__(256) block_tile_lists_kernel(
   const int nw = (C + 31) >> 5;
   for (int w = threadIdx.x; w < nw; w += blockDim.x) need[w] = 0u;
   __syncthreads();
-  for (int i = warp; i < rows; i += 8) {
+  for (int i = warp; i < rows; i += kW) {
     const int64_t row = r0 + i;
     const double thr = (double(tau[row]) + double(eps_rel) * (double(qn[row]) + double(xn_max))) * (1.0 + 1e-6);
     const double* dr = dq + int64_t(qperm[row]) * C;
@@ -828,7 +830,7 @@ __global__ void __launch_bounds__(256) block_tile_lists_kernel(
     __syncthreads();
     if (threadIdx.x == 0) {
       int tot = 0;
-      for (int w = 0; w < 8; ++w) tot += s_wcnt[w];
+      for (int w = 0; w < kW; ++w) tot += s_wcnt[w];
       s_base += tot;
     }
     __syncthreads();
@@ -1081,8 +1083,8 @@ void launch_block_tile_lists(const double* dq, int32_t C, const int32_t* qperm, 
                              int32_t* tcount, uint32_t* bits, cudaStream_t s) {
   const size_t smem = size_t((C + 31) / 32) * 4;
   set_dynamic_smem(block_tile_lists_kernel, smem);
-  block_tile_lists_kernel<<<unsigned(nqb), 256, smem, s>>>(dq, C, qperm, bn, tau, qn, xn_max, eps_rel, rad, tclo,
-                                                             tchi, ntiles, tlist, tcount, bits);
+  block_tile_lists_kernel<<<unsigned(nqb), kListThreads, smem, s>>>(dq, C, qperm, bn, tau, qn, xn_max, eps_rel, rad,
+                                                                      tclo, tchi, ntiles, tlist, tcount, bits);
   DK_CHECK_LAUNCH();
 }
 
