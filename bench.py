@@ -596,14 +596,15 @@ def measure_deann_c3(args, local, timer):
         est = g.deann_batch(ds, spec, bf, Qh, W.k, W.m, rng=g.PhiloxSampler(seed0 + i))
         return est.values
 
-    e2e_ms = timer.wall(e2e_step, max(steps, 20), 10)  # the first ~20 host-buffer calls run slower
+    with ClockSampler(local) as clk_e2e:
+        e2e_ms = timer.wall(e2e_step, max(steps, 20), 10)  # the first ~20 host-buffer calls run slower
     res = {"metric": "DEANN queries/sec (exact k=100 NN + m=1000 Philox samples, gaussian) at n=1.2M, d=100",
            "value": nq / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
            "higher_is_better": True, "gpu_launches": launches * steps,
            "e2e": {"value": nq / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
                    "d2h_bytes_per_step": int(nq * 8),
                    "api": "deann_batch(ds, KernelSpec, BruteForceIndex(ds), pinned host queries, 100, 1000, "
-                          "rng=PhiloxSampler) -> list[Estimate]"},
+                          "rng=PhiloxSampler) -> list[Estimate]", "clocks": clk_e2e.summary()},
            "kernel_rooflines": kroof, "clocks": clocks.summary(),
            "config": {"workload": "c3: 1,200,000 x 100 L2-normalised rows, 10,000 queries, h by median-1e-3 rule",
                       "bandwidth": h, "k": W.k, "m": W.m, "l2": "inputs larger than L2 (480 MB rows)"}}
@@ -671,7 +672,8 @@ def measure_c3_exact(args, local, timer, W, ds, spec, h, Qd, steps, warm):
     finally:
         del os.environ["DK_KDE_HYBRID"]
     Qh = torch.from_numpy(W.Q).pin_memory().numpy()
-    e2e_ms = timer.wall(lambda i: g.naive_kde(ds, spec, Qh).values, steps, 5)
+    with ClockSampler(local) as clk_e2e:
+        e2e_ms = timer.wall(lambda i: g.naive_kde(ds, spec, Qh).values, steps, 5)
     peaks = _peaks()
     flops, ex2 = 2.0 * d * nq * n, float(nq) * n
     t_bound = max(flops / (peaks["bf16_tflops"] * 1e12), ex2 / _sfu_peak(peaks))
@@ -693,7 +695,8 @@ def measure_c3_exact(args, local, timer, W, ds, spec, h, Qd, steps, warm):
                      "t_bound_ms": t_bound * 1e3, "sfu_peak_tex2s": _sfu_peak(peaks) / 1e12,
                      "tensor_peak_tflops": peaks["bf16_tflops"]},
         "e2e": {"value": nq / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 8),
-                "d2h_bytes_per_step": int(nq * 8), "api": "naive_kde(ds, KernelSpec, pinned host queries)"},
+                "d2h_bytes_per_step": int(nq * 8), "api": "naive_kde(ds, KernelSpec, pinned host queries)",
+                "clocks": clk_e2e.summary()},
         "clocks": clocks.summary(),
         "config": {"workload": "c3: 1,200,000 x 100 L2-normalised rows, 10,000 queries, h by median-1e-3 rule",
                    "bandwidth": h, "l2": "inputs larger than L2 (307 MB fp16 operand + 480 MB rows)"},
