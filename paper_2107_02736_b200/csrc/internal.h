@@ -113,6 +113,8 @@ inline void set_dynamic_smem(K* kernel, size_t bytes) {
 // 64-column K-block costs more feed than the epilogue saves (c2: 2.67 -> 2.83 ms).
 constexpr int32_t kAugCols = 6;
 constexpr int32_t kTailK = 16;
+// K columns holding data: split3 3d (A=[Qh|Ql|Qh], B=[Xl|Xh|Xh]), exact / fp16 d
+inline int64_t enc_kdata(int32_t d, int mode) { return mode == 1 ? 3 * int64_t(d) : int64_t(d); }
 inline bool enc_aug_main(int32_t d, int mode) {
   return mode != 1 && (int64_t(d) + kAugCols + 63) / 64 == (int64_t(d) + 63) / 64;
 }

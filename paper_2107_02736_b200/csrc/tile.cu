@@ -232,8 +232,10 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
 #define DK_KSKIP 1
 #endif
   {
-    // columns holding data (the rest is zero padding)
-    const int kused = e.mode == 1 ? 3 * e.d : e.d + (enc_has_aug(e.d, e.mode) ? kAugCols : 0);
+    // columns holding data (the rest is zero padding); the norm columns of the main operand only
+    // when this sweep's A carries them (k-NN sweeps leave them zero: c5, d = 96, 6 MMA steps not 7)
+    const bool main_aug = aug && q.T == nullptr && enc_aug_main(e.d, e.mode);
+    const int kused = int(enc_kdata(e.d, e.mode)) + (main_aug ? kAugCols : 0);
     const int rem = kused - (kblocks - 1) * kBK;
     p.klast = DK_KSKIP && e.d > 0 && rem > 0 && rem <= kBK ? (rem + 15) / 16 : kBK / 16;
   }
