@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 import paper_2107_02736_b200 as g  # noqa: E402
 import workloads  # noqa: E402
 from oracle import deann_oracle as O  # noqa: E402
+from paper_2107_02736_b200 import _lib  # noqa: E402
 
 
 def _rel(a, b):
@@ -85,3 +86,42 @@ def test_exact_tail_matches_plain_epilogue_in_a_fresh_process():
             subprocess.run([sys.executable, "-c", code, path], check=True, env=env)
             outs.append(np.load(path))
     assert _rel(outs[0], outs[1]) < 2e-6
+
+
+def test_tail_integer_rows_with_fractional_and_host_query_chunks():
+    """d = 128 integer rows (the tail path): a host batch of two chunks whose second chunk has a
+    fractional query — that chunk's speculative exact sweep skips itself and is redone in split3
+    after both chunks are enqueued; the first chunk stays exact."""
+    rng = np.random.default_rng(17)
+    X = rng.integers(0, 256, size=(20_000, 128)).astype(np.float32)
+    Q = rng.integers(0, 256, size=(4096, 128)).astype(np.float64)
+    Q[4000] += 0.5
+    ds, od = g.Dataset.from_array(X), O.Data(X)
+    assert ds.exact_mode
+    h = 900.0
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", h), Q).values
+    sel = np.array([0, 1, 1023, 1024, 2048, 4000, 4095])
+    assert _rel(got[sel], O.naive_kde(od, "gaussian", h, Q[sel])) < 2e-6
+
+
+def test_two_precision_on_dataset_shards(monkeypatch):
+    """Dataset-sharded handles (global_offset / global_n, each shard >= 512 tiles) take the
+    two-precision path too: their contributions to the global mean add up to the whole dataset's."""
+    X = workloads._c3_rows(11, 2 * 140_000)
+    Q = workloads._c3_rows(12, 2048).astype(np.float64)
+    h = 0.2239
+    n = X.shape[0]
+    full = g.naive_kde(g.Dataset.from_array(X), g.KernelSpec("gaussian", h), Q).values
+    acc = np.zeros_like(full)
+    for lo, hi in ((0, n // 2), (n // 2, n)):
+        sh = g.Dataset.from_array(X[lo:hi], global_offset=lo, global_n=n)
+        acc += g.naive_kde(sh, g.KernelSpec("gaussian", h), Q).values
+        lib = _lib.load()
+        import ctypes
+
+        v = [ctypes.c_int64() for _ in range(4)]
+        _lib.check(lib.dk_kde_stats(sh.handle, *[ctypes.byref(x) for x in v]))
+        assert v[0].value == Q.shape[0]  # served two-precision
+    assert _rel(acc, full) < 5e-6
+    sel = np.arange(0, 2048, 512)
+    assert _rel(full[sel], O.naive_kde(O.Data(X), "gaussian", h, Q[sel])) < 1e-5
