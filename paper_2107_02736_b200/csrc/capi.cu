@@ -866,21 +866,13 @@ bool hyb_prepare(dk_dataset* h, int32_t family, int64_t nq_chunk_min, cudaStream
 }
 
 // KDE partials of any sweep of at most bpad queries (the batches and the fallback chunks): the
-// column-chunk count of the plan grows as the query-block count falls, so take the maximum over
-// every query padding up to bpad (cached per shape)
-size_t hyb_part_cap(const dk_dataset* h, int32_t bpad) {
-  static std::mutex mu;
-  static std::map<std::tuple<int64_t, int32_t, int>, size_t> cache;
-  const auto key = std::make_tuple(h->n_pad, bpad, h->num_sms);
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  size_t cap = 0;
-  for (int32_t pad = kBM; pad <= bpad; pad = pad == kBM ? 2 * kBM : pad + 2 * kBM)
-    cap = std::max({cap, sweep_part_count(h->n_pad, pad, h->num_sms, false),
-                    sweep_part_count(h->n_pad, pad, h->num_sms, true)});
-  cache[key] = cap;
-  return cap;
+// column-chunk count of the plan grows as the query-block count falls, so bound it over every
+// query padding up to bpad
+size_t hyb_part_cap(const dk_dataset* h, int32_t bpad) { return sweep_part_bound(h->n_pad, bpad, h->num_sms); }
+void check_part_cap(const dk_dataset* h, int32_t pad, int32_t bpad) {  // the bound above, checked
+  if (std::max(sweep_part_count(h->n_pad, pad, h->num_sms, false), sweep_part_count(h->n_pad, pad, h->num_sms, true)) >
+      hyb_part_cap(h, bpad))
+    throw Error{DK_ECUDA, "internal: KDE partial-sum bound exceeded"};
 }
 
 struct HybLayout {
@@ -953,6 +945,7 @@ void kde_hybrid(dk_dataset* h, const double* Q, int64_t q0, int64_t qn, double b
   // plain split3 sweep over the sorted rows for queries gathered by id (idx) or a contiguous range
   auto split3_rows = [&](const int32_t* idx, int64_t first_q, int64_t fn) {
     const int32_t fpad = int32_t(query_pad(fn));
+    check_part_cap(h, fpad, L.bpad);
     const double* Qf = Q + first_q * h->d;
     if (idx != nullptr) {
       launch_gather_rows_f64(Q, idx + first_q, fn, h->d, at<double>(h->ws, L.qs), s);
@@ -988,6 +981,7 @@ void kde_hybrid(dk_dataset* h, const double* Q, int64_t q0, int64_t qn, double b
     const int64_t bn = std::min<int64_t>(bstep, qn - b0);
     const int32_t bn_pad = int32_t(query_pad(bn));
     const int32_t nqb = bn_pad / kBM;
+    check_part_cap(h, bn_pad, L.bpad);
     const double* Qb = Q + (q0 + b0) * h->d;
     // ball-sorted batch: each block of 128 queries is local, so its hot tiles are few
     int32_t* near = at<int32_t>(h->ws, L.near);

@@ -321,6 +321,8 @@ struct SweepArgs {
 bool tile_major_fits(int32_t Kp);
 // doubles needed for KDE partials (allow_pair = false: sweeps that never run as 2-CTA pairs)
 size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms, bool allow_pair = true);
+// >= sweep_part_count for every query padding up to max_pad (no plan search)
+size_t sweep_part_bound(int64_t n_pad, int32_t max_pad, int num_sms);
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
 void set_pair_enabled(bool on);  // 2-CTA (cta_group::2) sweeps; off by default (DK_PAIR=1)
 

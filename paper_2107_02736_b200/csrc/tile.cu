@@ -186,6 +186,26 @@ size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms, bool allow_p
   return size_t(pl.ncc) * kColGroups * size_t(nq_pad);
 }
 
+// An upper bound of sweep_part_count over every query padding up to max_pad, from the plan's
+// chunk-length range alone (balanced_tiles_per_unit picks tiles_per_unit >= lo, so a plan has at
+// most ceil(ntiles / lo) column chunks) — no makespan search per padding.
+size_t sweep_part_bound(int64_t n_pad, int32_t max_pad, int num_sms) {
+  const int64_t ntiles = n_pad / kBN;
+  size_t cap = 0;
+  for (int32_t pad = kBM; pad <= max_pad; pad = pad == kBM ? 2 * kBM : pad + 2 * kBM) {
+    const int nqb = pad / kBM;
+    for (int pr = 0; pr < 2; ++pr) {
+      const int64_t ngroups = pr ? std::max(1, nqb / 2) : nqb;
+      const int64_t nslots = pr ? std::max(1, num_sms / 2) : num_sms;
+      const int64_t total = ntiles * ngroups;
+      const int64_t hi = std::min<int64_t>(std::max<int64_t>(1, total / (nslots * 12)), ntiles);
+      const int64_t lo = std::min(std::max<int64_t>(1, total / (nslots * 48)), hi);
+      cap = std::max(cap, size_t((ntiles + lo - 1) / lo) * kColGroups * size_t(pad));
+    }
+  }
+  return cap;
+}
+
 void set_pair_enabled(bool on) { g_pair_enabled = on; }
 
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
