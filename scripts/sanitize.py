@@ -5,7 +5,8 @@ synccheck / initcheck):
 
 Covers the fused tile sweep in every mode (exact-integer and split3 gaussian, exponential,
 TILEMIN / FILTER, the pruned FILTER in tile-major order on >= 512 tiles, the 2-CTA pair
-variant with --pair), the L1 kernel, the k-NN selection / fallback / big-k paths, the Philox
+variant with --pair; the norm-column epilogue in the K padding and in the 16-column tail; the
+two-precision KDE's fp16 and split3 passes, hot lists, combine and fallback), the L1 kernel, the k-NN selection / fallback / big-k paths, the Philox
 sampler, explicit-row evaluation, the permuted sampler, the IVF build and query, and the
 shard merge.  Each check also compares against a NumPy reference, so a run that the
 sanitizer lets through is still a correct one.
@@ -95,5 +96,23 @@ Qd = e0.queries(Qm[:32])
 a, b = e0.knn(Qd, 12), e1.knn(Qd, 12)
 mi, _ = e0.merge_topk(torch.stack([a[0], b[0]]), torch.stack([a[1], b[1]]), 12)
 check("merge topk", np.array_equal(mi.cpu().numpy()[0], O.brute_force_knn(odm, Qm[0], 12)[0]))
+# norm columns in the 16-column tail (d = 128 integer rows) and in the K padding (d = 100)
+for dd in (128, 100):
+    Xi = rng.integers(0, 64, size=(3000, dd)).astype(np.float32)
+    Qi = rng.integers(0, 64, size=(40, dd)).astype(np.float64)
+    got = g.naive_kde(g.Dataset.from_array(Xi), g.KernelSpec("gaussian", 60.0), Qi).values
+    check(f"norm columns d={dd}", np.max(np.abs(got - O.naive_kde(O.Data(Xi), "gaussian", 60.0, Qi)) /
+                                        O.naive_kde(O.Data(Xi), "gaussian", 60.0, Qi)) < 2e-6)
+# two-precision exact KDE (>= 512 tiles, >= 2,048 queries), with forced fallbacks for a few queries
+import workloads  # noqa: E402
+
+Xh = workloads._c3_rows(3, 140_000)
+Qh = workloads._c3_rows(4, 2048).astype(np.float64)
+Qh[:3] = rng.standard_normal((3, Xh.shape[1]))  # unit directions far from every cluster: the fp16
+Qh[:3] /= np.linalg.norm(Qh[:3], axis=1, keepdims=True)  # bound fails -> split3 fallback
+dsh = g.Dataset.from_array(Xh)
+vh = g.naive_kde(dsh, g.KernelSpec("gaussian", 0.2239), Qh).values
+refh = O.naive_kde(O.Data(Xh), "gaussian", 0.2239, Qh[:8])
+check("two-precision KDE", float(np.max(np.abs(vh[:8] - refh) / refh)) < 1e-5)
 torch.cuda.synchronize()
 print("sanitize workload done", flush=True)
