@@ -1458,7 +1458,12 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       const char* v = std::getenv("DK_E2E_SPLIT");
       return v ? std::max<int64_t>(2, std::atoll(v)) : int64_t(4);
     }();
-    const int64_t split = (host_q && nq >= 4096) ? round_up(nq / split_div, 256) : nq;
+    // two-precision exact KDE (non-integer gaussian batches on large datasets): decided first (the
+    // first call builds the sorted rows' operands in their own memory); it runs as ONE chunk — its
+    // per-batch passes (ball order, two query encodes, hot lists, split3 pass) cost more when split
+    // than the hidden copy saves (c3 end to end 4.47 -> 3.6 ms)
+    const bool hyb = hyb_prepare(h, family, nq, s);
+    const int64_t split = (host_q && nq >= 4096 && !hyb) ? round_up(nq / split_div, 256) : nq;
     const int64_t c_beg[2] = {0, split};
     const int64_t c_cnt[2] = {split, nq - split};
     const int nchunks = c_cnt[1] > 0 ? 2 : 1;
@@ -1473,9 +1478,6 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       o_part[c] = pl.add<double>(sweep_part_count(h->n_pad, pad, h->num_sms));
       o_fl[c] = pl.add<uint32_t>(4);
     }
-    // two-precision exact KDE (non-integer gaussian batches on large datasets): decided before the
-    // workspace is reserved (the first call builds the sorted rows' operands in their own memory)
-    const bool hyb = hyb_prepare(h, family, nq, s);
     const HybLayout HL = hyb ? hyb_layout(h, std::max(c_cnt[0], c_cnt[1]), nq, pl.off) : HybLayout{};
     h->ws.reserve(hyb ? HL.end + 4096 : pl.off);
     double* od = out_dev ? out : at<double>(h->ws, o_out);
