@@ -36,10 +36,12 @@ namespace dk {
 namespace {
 
 constexpr int kSelHist = 1024;  // histogram bins of the k-NN selection (4 per thread of a 256-thread block)
-// lanes per exactly re-ranked row in every selection path (one summation order, so a query's
-// distances are bit-identical whichever path serves it); 4 lanes (8 rows per warp step, 6-7 float4
-// loads per lane in flight) measured faster than 8 (c3 k-NN 1.65 -> 1.58 ms) and 16 (1.67 ms)
-constexpr int kExactG = 4;
+// lanes per exactly re-ranked row, the same in every selection path for a given d (one summation
+// order, so a query's distances are bit-identical whichever path serves it): 4 lanes (8 rows per
+// warp step, 6-7 float4 loads per lane in flight) for rows up to 160 dimensions — faster than 8 on
+// c3 (k-NN 1.65 -> 1.58 ms) and 16 (1.67 ms) — and 8 for wider rows (c4, d = 784: DEANN 10.5 ms
+// with 4 lanes against 6.7 ms with 8)
+inline int exact_group(int32_t d) { return d <= 160 ? 4 : 8; }
 
 struct Key128 {
   unsigned long long hi;  // fp64 bits of d2 (>= 0, so bit order == numeric order)
@@ -272,6 +274,7 @@ __device__ __forceinline__ double exact_d2_group(const float* __restrict__ x, co
 // Queries this path cannot finish are appended to device lists, so the host never waits:
 //   slow list: more than 2 pow2(k) keys within 2 eps of T' -> select_slow_kernel;
 //   ovf list : candidate list overflowed (> cap) or shorter than k -> exact fp64 scan.
+template <int G>
 __global__ void __launch_bounds__(256) select_fast_kernel(
     const float* __restrict__ X, int64_t global_offset, int32_t d, const double* __restrict__ Q, int64_t nq,
     int32_t k, const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt, int32_t cap,
@@ -296,7 +299,6 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
   for (int j = threadIdx.x; j < d; j += blockDim.x) qv[j] = Q[size_t(q) * d + j];
   const double eps = double(eps_rel) * (double(qn[q]) + double(xn_max));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  constexpr int G = kExactG;  // lanes per candidate: 32 / G candidates per warp step
   const int grp = lane / G, gl = lane % G;
   __shared__ uint32_t s_lo, s_hi, s_bstar, s_tmax, s_ns;
   __shared__ uint32_t s_wsum[32];
@@ -478,6 +480,7 @@ __global__ void __launch_bounds__(256) select_fast_kernel(
 // over the device list): all candidates bitonic-sorted by approx key in shared memory, then
 // re-ranked exactly W at a time in that order until the next approx key - eps exceeds the
 // current exact k-th distance.
+template <int G>
 __global__ void __launch_bounds__(256) select_slow_kernel(
     const float* __restrict__ X, int64_t global_offset, int32_t d, const double* __restrict__ Q, int32_t k,
     const unsigned long long* __restrict__ cand, const uint32_t* __restrict__ cnt, int32_t cap,
@@ -491,7 +494,6 @@ __global__ void __launch_bounds__(256) select_slow_kernel(
   Key128* top = reinterpret_cast<Key128*>(sbuf + B);
   double* qv = reinterpret_cast<double*>(top + Kp + W);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  constexpr int G = kExactG;
   const int grp = lane / G, gl = lane % G;
   __shared__ int s_stop;
   for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
@@ -543,6 +545,7 @@ __global__ void __launch_bounds__(256) select_slow_kernel(
 
 // exact fp64 full scan for the queries on the overflow list (rare / degenerate inputs);
 // persistent grid over the device list
+template <int G>
 __global__ void exact_knn_kernel(const float* __restrict__ X, int64_t n, int64_t global_offset, int32_t d,
                                  const double* __restrict__ Q, const int32_t* __restrict__ qlist,
                                  const int32_t* __restrict__ qcount, int32_t k, int32_t B,
@@ -559,9 +562,8 @@ __global__ void exact_knn_kernel(const float* __restrict__ X, int64_t n, int64_t
     __syncthreads();
     for (int i = threadIdx.x; i < Kp; i += blockDim.x) buf[i] = Key128{~0ull, ~0ull};
     for (int64_t pos = 0; pos < n; pos += chunk) {
-      // kExactG lanes per row with the selection's summation order (exact_d2_group), so a query
+      // G lanes per row (exact_group(d)) with the selection's summation order (exact_d2_group), so a query
       // gets bit-identical distances whichever path served it
-      constexpr int G = kExactG;
       const int grp = lane / G, gl = lane % G;
       for (int i0 = warp * (32 / G); i0 < chunk; i0 += nwarps * (32 / G)) {
         const int i = i0 + grp;
@@ -1209,18 +1211,21 @@ void launch_select(const float* X, int64_t global_offset, int32_t d, const doubl
   // of shared memory keeps 6 CTAs per SM)
   const int scap = std::max(2 * Kp, 2048);
   const size_t fast_smem = size_t(scap) * sizeof(Key128) + size_t(d) * sizeof(double) + kSelHist * sizeof(uint32_t);
-  set_dynamic_smem(select_fast_kernel, fast_smem);
+  const bool g4 = exact_group(d) == 4;
+  auto fast = g4 ? select_fast_kernel<4> : select_fast_kernel<8>;
+  set_dynamic_smem(fast, fast_smem);
   if (fast_smem > 232448) throw Error{DK_EINVAL, "k too large for the k-NN selection buffer"};
-  select_fast_kernel<<<unsigned(nq), 256, fast_smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn,
-                                                          xn_max, eps_rel, idx_out, d2_out, slow_list, counts,
-                                                          ovf_list, counts + 1, perm, scap);
+  fast<<<unsigned(nq), 256, fast_smem, s>>>(X, global_offset, d, Q, nq, k, cand, cand_cnt, cap, qn, xn_max, eps_rel,
+                                            idx_out, d2_out, slow_list, counts, ovf_list, counts + 1, perm, scap);
   DK_CHECK_LAUNCH();
   const int B = std::max(2, pow2_ceil(cap));
   const size_t slow_smem = size_t(B) * 8 + size_t(2 * Kp) * sizeof(Key128) + size_t(d) * sizeof(double);
   if (slow_smem > 232448) throw Error{DK_EINVAL, "k or candidate capacity too large for the k-NN selection buffer"};
-  set_dynamic_smem(select_slow_kernel, slow_smem);
-  select_slow_kernel<<<unsigned(std::max(1, 2 * num_sms)), 256, slow_smem, s>>>(
-      X, global_offset, d, Q, k, cand, cand_cnt, cap, qn, xn_max, eps_rel, B, idx_out, d2_out, slow_list, counts, perm);
+  auto slow = g4 ? select_slow_kernel<4> : select_slow_kernel<8>;
+  set_dynamic_smem(slow, slow_smem);
+  slow<<<unsigned(std::max(1, 2 * num_sms)), 256, slow_smem, s>>>(X, global_offset, d, Q, k, cand, cand_cnt, cap, qn,
+                                                                  xn_max, eps_rel, B, idx_out, d2_out, slow_list,
+                                                                  counts, perm);
   DK_CHECK_LAUNCH();
 }
 
@@ -1230,10 +1235,11 @@ void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_o
   const int Kp = pow2_ceil(k);
   const int B = std::max(1024, 2 * Kp);
   const size_t smem = size_t(B) * sizeof(Key128);
-  set_dynamic_smem(exact_knn_kernel, smem);
+  auto fb = exact_group(d) == 4 ? exact_knn_kernel<4> : exact_knn_kernel<8>;
+  set_dynamic_smem(fb, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "k too large for the exact k-NN fallback"};
-  exact_knn_kernel<<<unsigned(std::max(1, num_sms)), 256, smem, s>>>(X, n_local, global_offset, d, Q, qlist, qcount,
-                                                                     k, B, idx_out, d2_out);
+  fb<<<unsigned(std::max(1, num_sms)), 256, smem, s>>>(X, n_local, global_offset, d, Q, qlist, qcount, k, B, idx_out,
+                                                       d2_out);
   DK_CHECK_LAUNCH();
 }
 
