@@ -39,8 +39,7 @@ constexpr int kSelHist = 1024;  // histogram bins of the k-NN selection (4 per t
 // lanes per exactly re-ranked row, the same in every selection path for a given d (one summation
 // order, so a query's distances are bit-identical whichever path serves it): 4 lanes (8 rows per
 // warp step, 6-7 float4 loads per lane in flight) for rows up to 160 dimensions — faster than 8 on
-// c3 (k-NN 1.65 -> 1.58 ms) and 16 (1.67 ms) — and 8 for wider rows (c4, d = 784: DEANN 10.5 ms
-// with 4 lanes against 6.7 ms with 8)
+// c3 (k-NN 1.65 -> 1.58 ms) and 16 (1.67 ms) — and 8 (the round-1 choice) for wider rows
 inline int exact_group(int32_t d) { return d <= 160 ? 4 : 8; }
 
 struct Key128 {
