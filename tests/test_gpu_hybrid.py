@@ -177,3 +177,20 @@ def test_wide_bandwidth_switches_within_a_multi_batch_call(monkeypatch):
     q1, _, hot, tot = _stats(ds)
     assert hot > 0.25 * tot and q1 - q0 == 1024  # the first batch only
     assert _rel(v, ref) < 1e-6
+
+
+def test_handles_release_the_two_precision_operands():
+    """Fit -> two-precision KDE (ball-sorted rows, fp16 and split3 operands, workspace) -> free,
+    three times: the device memory comes back (no per-handle leak of the new operands)."""
+    X = workloads._c3_rows(21, 140_000)
+    Q = workloads._c3_rows(22, 2048).astype(np.float64)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(3):
+        ds = g.Dataset.from_array(X)
+        g.naive_kde(ds, g.KernelSpec("gaussian", H), Q)
+        assert _stats(ds)[0] == Q.shape[0]
+        ds.free()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 << 20, (free0, free1)
