@@ -36,6 +36,7 @@ constexpr size_t kMaxSmem = 232448;  // sm_100 opt-in dynamic shared memory per 
 
 struct Plan {
   int a_resident, stages, tiles_per_unit, ncc;
+  int tbufs;  // tile-major: resident tile buffers
   size_t smem;
 };
 
@@ -82,12 +83,20 @@ Plan make_plan(int kblocks, int ntiles, int ngroups, int nslots, int mode, bool 
   Plan pl{};
   if (tmajor) {
     pl.a_resident = 0;
+    // two tile buffers when they leave a >= 4-stage ring: the next unit's tile (a DRAM read) loads
+    // while the current one's query blocks stream past, instead of stalling the MMA once per unit
+    static const int want = [] {
+      const char* v = std::getenv("DK_KNN_TBUFS");  // A/B switch
+      return v != nullptr && std::atoi(v) == 1 ? 1 : 2;
+    }();
+    const int bufs = want == 2 && tile_smem_bytes(kblocks, 0, 4, mode, false, 2) <= kMaxSmem ? 2 : 1;
     int st = 3;
-    while (st < 8 && tile_smem_bytes(kblocks, 0, st + 1, mode, false, true) <= kMaxSmem) ++st;
+    while (st < 8 && tile_smem_bytes(kblocks, 0, st + 1, mode, false, bufs) <= kMaxSmem) ++st;
     pl.stages = st;
+    pl.tbufs = bufs;
     pl.tiles_per_unit = 1;
     pl.ncc = 1;
-    pl.smem = tile_smem_bytes(kblocks, 0, st, mode, false, true);
+    pl.smem = tile_smem_bytes(kblocks, 0, st, mode, false, bufs);
     return pl;
   }
   // keep the query block resident when it fits next to a >=3-stage ring
@@ -284,7 +293,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.hot_bits = a.hot_bits;
   p.hot_thr = a.hot_thr;
   p.tail = tail ? 1 : 0;
-  p.tmajor = tmajor ? 1 : 0;
+  p.tmajor = tmajor ? pl.tbufs : 0;
   p.blist = a.blist;
   p.unit_counter = a.unit_counter;
   if (tmajor && a.unit_counter == nullptr) throw Error{DK_EINVAL, "internal: tile-major sweeps need a unit counter"};

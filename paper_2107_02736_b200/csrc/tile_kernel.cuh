@@ -96,7 +96,11 @@ constexpr int kColGroups = 4;      // 64-column groups per tile (one per epilogu
 constexpr int kXnSlots = 4;        // column-norm staging ring (1 KB per tile)
 constexpr uint32_t kTmemCols = 512;  // 2 accumulator buffers x 256 fp32 columns
 constexpr int kStageCap = 32;      // FILTER: per-row smem candidate staging (entries)
-constexpr int kUnitSlots = 4;      // tile-major: ring of claimed unit ids (producer -> MMA / epilogue)
+constexpr int kUnitSlots = 4;
+// tile-major FILTER: per epilogue warp, each lane's 32 d2 values of a chunk with hits staged in shared
+// memory (row stride 36 floats: conflict-free 16-byte stores), so a hit's key is one shared load
+constexpr int kSdStride = 36;
+constexpr size_t kTmSdBytes = size_t(kNumEpiWarps) * 32 * kSdStride * 4;      // tile-major: ring of claimed unit ids (producer -> MMA / epilogue)
 
 struct TileParams {
   int32_t nq;              // valid query rows
@@ -120,7 +124,8 @@ struct TileParams {
   // tile-major FILTER (tmajor = 1): unit u = dataset tile ulist[3u] (resident in shared memory)
   // x query blocks blist[ulist[3u+1] .. ulist[3u+2]) streamed through the ring; the unit count
   // is read from device memory (built on the device, capi.cu knn_device)
-  int32_t tmajor;
+  int32_t tmajor;          // tile-major FILTER: resident dataset-tile buffers (1, or 2: the next unit's tile
+                           // loads while the current unit's query blocks stream past); 0 = block-major
   const int32_t* blist;
   const int32_t* nunits_dev;
   int32_t* unit_counter;   // tile-major: units are claimed dynamically (atomicAdd), zeroed per launch
@@ -156,14 +161,16 @@ constexpr int kTailABytes = kBM * 16 * 2;  // 4 KB: the query block's norm-colum
 constexpr int kTailBBytes = kBN * 16 * 2;  // 8 KB: a dataset tile's norm-column tail (a column-norm slot)
 
 __host__ __device__ inline size_t tile_smem_bytes(int kblocks, int a_resident, int stages, int mode, bool pair,
-                                                  bool tmajor = false, bool tail = false) {
+                                                  int tmajor = 0, bool tail = false) {
   size_t a = a_resident ? size_t(kblocks) * kABlockBytes : size_t(stages) * kABlockBytes;
   size_t b = size_t(stages) * (pair ? kBBlockBytes / 2 : kBBlockBytes);
-  if (tmajor) {  // resident dataset tile + ring of query K-blocks
+  if (tmajor) {  // resident dataset tile(s) + ring of query K-blocks; candidates go straight to global lists
     a = size_t(stages) * kABlockBytes;
-    b = size_t(kblocks) * kBBlockBytes;
+    b = size_t(tmajor) * size_t(kblocks) * kBBlockBytes;
   }
-  size_t stage = (mode == MODE_FILTER || mode == MODE_HIST) ? size_t(kBM) * kStageCap * 8 + kBM * 4 : 0;
+  size_t stage = ((mode == MODE_FILTER && !tmajor) || mode == MODE_HIST) ? size_t(kBM) * kStageCap * 8 + kBM * 4
+                 : (mode == MODE_FILTER && tmajor)                      ? kTmSdBytes
+                                                                        : 0;
   const size_t xslots = size_t(kXnSlots) * (tail ? kTailBBytes : kBN * 4) + (tail ? kTailABytes : 0);
   return 1024 /*align slack*/ + a + b + xslots + stage + 512 /*barriers*/;
 }
@@ -393,6 +400,61 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
   }
 }
 
+// Tile-major FILTER, one 32-column chunk: d2 exactly as epi_chunk's k-NN branch computes it (packed
+// FFMA2 of S * m2s + (|q|^2 + |x|^2)), a min tree to reject the chunk, and for the chunks of a warp
+// with hits the d2 row staged in shared memory (`sd`, this lane's row), from which each hit's key
+// is one load — no per-hit select chain over the registers.  Candidates go straight to the row's
+// global list (one atomic per row and chunk with hits).
+__device__ __forceinline__ void filter_chunk_tm(const uint32_t (&r)[32], const float* __restrict__ xs_smem, float qn,
+                                                float m2s, float tau, bool full, int64_t cbase, const TileParams& p,
+                                                int row, float* sd) {
+  const float4* x4 = reinterpret_cast<const float4*>(xs_smem);
+  const float2 q2 = make_float2(qn, qn), m2 = make_float2(m2s, m2s);
+  float d2v[32];
+#pragma unroll
+  for (int j4 = 0; j4 < 8; ++j4) {
+    const float4 xv = x4[j4];
+    const float2 da = fma2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), m2,
+                           add2(q2, make_float2(xv.x, xv.y)));
+    const float2 db = fma2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), m2,
+                           add2(q2, make_float2(xv.z, xv.w)));
+    d2v[4 * j4] = da.x; d2v[4 * j4 + 1] = da.y; d2v[4 * j4 + 2] = db.x; d2v[4 * j4 + 3] = db.y;
+  }
+  float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[2], m3 = d2v[3];
+#pragma unroll
+  for (int j = 4; j < 32; j += 4) {
+    m0 = fminf(m0, d2v[j]); m1 = fminf(m1, d2v[j + 1]);
+    m2_ = fminf(m2_, d2v[j + 2]); m3 = fminf(m3, d2v[j + 3]);
+  }
+  uint32_t hits = 0;
+  if (fminf(fminf(m0, m1), fminf(m2_, m3)) <= tau) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) hits |= (d2v[j] <= tau ? 1u : 0u) << j;
+  }
+  if (!full) {  // columns past n never hit
+    const int64_t lim = p.n - cbase;
+    hits &= lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : (1u << lim) - 1u);
+  }
+  if (__any_sync(0xffffffffu, hits != 0u)) {
+#pragma unroll
+    for (int j4 = 0; j4 < 8; ++j4)
+      reinterpret_cast<float4*>(sd)[j4] = make_float4(d2v[4 * j4], d2v[4 * j4 + 1], d2v[4 * j4 + 2], d2v[4 * j4 + 3]);
+    if (hits) {
+      uint32_t slot = atomicAdd(&p.cand_cnt[row], uint32_t(__popc(hits)));
+      unsigned long long* dst = p.cand + size_t(row) * p.cap;
+      while (hits) {
+        const int j = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(fmaxf(sd[j], 0.f))) << 32) |
+                                       static_cast<unsigned long long>(cbase + j);
+        if (slot < uint32_t(p.cap)) dst[slot] = key;
+        ++slot;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32) : "memory"); }
 
 // kPair: a 2-CTA cluster runs tcgen05.mma.cta_group::2 with M = 256 — the two CTAs
@@ -418,6 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stages = p.stages;
   constexpr int kBStage = kPair ? kBBlockBytes / 2 : kBBlockBytes;  // B bytes per CTA per stage
   const bool tmajor = MODE == MODE_FILTER && !kPair && p.tmajor != 0;
+  const int tbufs = tmajor ? p.tmajor : 1;  // tile-major: resident tile buffers
   uint8_t* smemA = smem;
   const bool tail = is_aug(MODE) && p.tail != 0;
   // [A: resident K-blocks or ring][A tail (tail mode)][B ring][column-norm / B-tail slots]
@@ -425,22 +488,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smemB = smemAt + (tail ? kTailABytes : 0);
   float* smemX = reinterpret_cast<float*>(smemB + size_t(stages) * kBStage);  // [kXnSlots][xslot]
   const int xslot = tail ? kTailBBytes / 4 : kBN;  // floats per slot
-  if (tmajor) {  // [resident tile: kblocks x 32 KB][ring: stages x 16 KB query K-blocks][norms]
+  if (tmajor) {  // [resident tiles: tbufs x kblocks x 32 KB][ring: stages x 16 KB query K-blocks][norms]
     smemB = smem;
-    smemA = smem + size_t(p.kblocks) * kBBlockBytes;
+    smemA = smem + size_t(tbufs) * p.kblocks * kBBlockBytes;
     smemX = reinterpret_cast<float*>(smemA + size_t(stages) * kABlockBytes);
   }
   unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smemX + kXnSlots * xslot);  // FILTER staging
-  constexpr bool kStage = MODE == MODE_FILTER || MODE == MODE_HIST;  // FILTER staging / HIST bins
-  uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (kStage ? kBM * kStageCap : 0));
+  const bool kStage = (MODE == MODE_FILTER && !tmajor) || MODE == MODE_HIST;  // FILTER staging / HIST bins
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sbuf + (kStage ? kBM * kStageCap : tmajor ? kTmSdBytes / 8 : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(scnt + (kStage ? kBM : 0));
   uint64_t* full_bar = bars;                 // [stages]   (leader's counts both CTAs' bytes)
   uint64_t* empty_bar = bars + stages;       // [stages]
   uint64_t* tfull_bar = bars + 2 * stages;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;      // [2]        (leader's counts both CTAs' warps)
-  uint64_t* afull_bar = tempty_bar + 2;      // [1]
-  uint64_t* aempty_bar = afull_bar + 1;      // [1]
-  uint64_t* xfull_bar = aempty_bar + 1;      // [kXnSlots]
+  uint64_t* afull_bar = tempty_bar + 2;      // [2]        (the second: tile-major's other tile buffer)
+  uint64_t* aempty_bar = afull_bar + 2;      // [2]
+  uint64_t* xfull_bar = aempty_bar + 2;      // [kXnSlots]
   uint64_t* xempty_bar = xfull_bar + kXnSlots;  // [kXnSlots]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty_bar + kXnSlots);
   uint64_t* ufull_bar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kUnitSlots] (tile-major)
@@ -468,8 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], kPair ? 2 * kNumEpiWarps : (kPP ? kNumEpiWarps / 2 : kNumEpiWarps));
     }
-    mbar_init(afull_bar, 1);
-    mbar_init(aempty_bar, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&afull_bar[a], 1);
+      mbar_init(&aempty_bar[a], 1);
+    }
     for (int x = 0; x < kXnSlots; ++x) {
       mbar_init(&xfull_bar[x], 1);
       mbar_init(&xempty_bar[x], kPP ? kNumEpiWarps / 2 : kNumEpiWarps);
@@ -483,7 +548,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if constexpr (MODE == MODE_FILTER) {
-    for (int i = threadIdx.x; i < kBM; i += blockDim.x) scnt[i] = 0;
+    if (!tmajor)
+      for (int i = threadIdx.x; i < kBM; i += blockDim.x) scnt[i] = 0;
   }
   if constexpr (MODE == MODE_HIST) {
     static_assert(kBM * kHistBins * 4 <= kBM * kStageCap * 8, "histogram bins must fit the staging area");
@@ -530,10 +596,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int col0 = __ldg(p.ulist + 3 * u) * kBN;
         const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
         DK_DCHECK(col0 >= 0 && col0 < p.n && i0 <= i1);
-        mbar_wait(aempty_bar, (uiter & 1) ^ 1);
-        mbar_arrive_expect_tx(afull_bar, uint32_t(p.kblocks) * kBBlockBytes);
+        // the unit's tile buffer (alternating with tbufs == 2: it fills while the previous unit computes)
+        const int tb = tbufs == 2 ? (uiter & 1) : 0;
+        const uint32_t tuse = tbufs == 2 ? uint32_t(uiter >> 1) : uint32_t(uiter);
+        mbar_wait(&aempty_bar[tb], (tuse & 1) ^ 1);
+        mbar_arrive_expect_tx(&afull_bar[tb], uint32_t(p.kblocks) * kBBlockBytes);
+        uint8_t* tbuf = smemB + size_t(tb) * p.kblocks * kBBlockBytes;
         for (int kb = 0; kb < p.kblocks; ++kb)
-          tma_load_2d(smemB + size_t(kb) * kBBlockBytes, &tmapB, afull_bar, kb * kBK, col0, pol_b);
+          tma_load_2d(tbuf + size_t(kb) * kBBlockBytes, &tmapB, &afull_bar[tb], kb * kBK, col0, pol_b);
         for (int i = i0; i < i1; ++i, ++titer) {
           const int qb = __ldg(p.blist + i);
           DK_DCHECK(qb >= 0 && qb < p.nqb);
@@ -640,7 +710,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++uslot == kUnitSlots) { uslot = 0; uph ^= 1; }
         if (u < 0) break;
         const int i0 = __ldg(p.ulist + 3 * u + 1), i1 = __ldg(p.ulist + 3 * u + 2);
-        mbar_wait(afull_bar, uiter & 1);
+        const int tb = tbufs == 2 ? (uiter & 1) : 0;
+        const uint32_t tuse = tbufs == 2 ? uint32_t(uiter >> 1) : uint32_t(uiter);
+        const uint32_t bt = b0 + uint32_t(tb) * uint32_t(p.kblocks) * kBBlockBytes;
+        mbar_wait(&afull_bar[tb], tuse & 1);
         tc_fence_after();
         for (int i = i0; i < i1; ++i) {
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -650,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
             const uint64_t ad = sw128_kmajor_desc(a0 + uint32_t(stage) * kABlockBytes);
-            const uint64_t bd = sw128_kmajor_desc(b0 + uint32_t(kb) * kBBlockBytes);
+            const uint64_t bd = sw128_kmajor_desc(bt + uint32_t(kb) * kBBlockBytes);
             const int ksteps = kb == p.kblocks - 1 ? p.klast : kBK / 16;
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
@@ -661,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&tfull_bar[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        mma_commit(aempty_bar);  // the resident tile may be replaced
+        mma_commit(&aempty_bar[tb]);  // the resident tile may be replaced
       }
     } else if (lane == 0 && leader) {
       constexpr uint32_t idesc = idesc_f16_f32(kPair ? 2 * kBM : kBM, kBN);
@@ -801,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       uint32_t titer = 0;
       const float m2s = *p.m2s;
-      float mn_unused = 0.f;
+      float* sd = reinterpret_cast<float*>(sbuf) + (size_t(ew) * 32 + lane) * kSdStride;  // this lane's d2 row
       int uslot = 0;
       uint32_t uph = 0;
       for (;;) {
@@ -832,11 +905,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
           const float* xsm = smemX + xs * kBN + cg * 64;
-          float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-          epi_chunk<MODE>(r0, xsm, qn, m2s, 0.f, tau, full, cbase, p.n, a0, a1, mn_unused, p, row, nullptr,
-                          nullptr, lrow);
-          epi_chunk<MODE>(r1, xsm + 32, qn, m2s, 0.f, tau, full, cbase + 32, p.n, a0, a1, mn_unused, p, row,
-                          nullptr, nullptr, lrow);
+          filter_chunk_tm(r0, xsm, qn, m2s, tau, full, cbase, p, row, sd);
+          filter_chunk_tm(r1, xsm + 32, qn, m2s, tau, full, cbase + 32, p, row, sd);
           __syncwarp();
           if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         }
