@@ -303,6 +303,17 @@ int knn_mode(dk_dataset* h, const double* Qd, int64_t nq, uint32_t* flags, cudaS
   return m == 0 ? 0 : 2;
 }
 
+// k-NN sweeps with norm columns (single-pass fp16 operands whose K padding holds them): the
+// accumulator is -d2/2, within the same eps_q (the bound's 2^-20 term covers the columns' residual).
+// DK_KNN_AUG=0: plain operands.
+bool knn_aug(const dk_dataset* h, const Encoding& e) {
+  static const bool off = [] {
+    const char* v = std::getenv("DK_KNN_AUG");  // A/B switch
+    return v != nullptr && std::atoi(v) == 0;
+  }();
+  return !off && e.mode == 2 && enc_aug_main(h->d, e.mode);
+}
+
 // Pruned FILTER pass (internal.h KnnClusters): for datasets of >= 512 tiles the rows are
 // grouped once by k-means into balls; each block of 128 queries (sorted by their nearest
 // ball) then sweeps only the tiles whose balls can hold a row inside some member's tau_q.
@@ -551,8 +562,10 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
       idx_b = at<int64_t>(h->ws, L.tidx);
       d2_b = at<double>(h->ws, L.td2);
     }
+    // fp16 operands with norm columns in the K padding: the query side carries its norm columns too,
+    // so the sweeps' accumulators are -d2/2 and their epilogues skip the norm arithmetic
     QueryOperand q = encode_queries(h, e, Qb, bn, bn_pad, at<__half>(h->ws, L.A), at<float>(h->ws, L.qn),
-                                    at<float>(h->ws, L.scal), s);
+                                    at<float>(h->ws, L.scal), s, nullptr, knn_aug(h, e));
     float* tau = at<float>(h->ws, L.tau);
     uint32_t* cnt = at<uint32_t>(h->ws, L.cnt);
     unsigned long long* cand = at<unsigned long long>(h->ws, L.cand);

@@ -293,6 +293,7 @@ void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s) {
   p.hot_bits = a.hot_bits;
   p.hot_thr = a.hot_thr;
   p.tail = tail ? 1 : 0;
+  p.knn_aug = aug && (a.mode == MODE_TILEMIN || a.mode == MODE_FILTER || a.mode == MODE_HIST) ? 1 : 0;
   p.tmajor = tmajor ? pl.tbufs : 0;
   p.blist = a.blist;
   p.unit_counter = a.unit_counter;

@@ -30,6 +30,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 #include "ptx.cuh"
 
 namespace dk {
@@ -124,6 +125,8 @@ struct TileParams {
   // tile-major FILTER (tmajor = 1): unit u = dataset tile ulist[3u] (resident in shared memory)
   // x query blocks blist[ulist[3u+1] .. ulist[3u+2]) streamed through the ring; the unit count
   // is read from device memory (built on the device, capi.cu knn_device)
+  int32_t knn_aug;         // k-NN sweeps over operands with norm columns: the accumulator is -d2/2
+                           // (scaled), d2 = S * m2s (no |q|^2 / |x|^2 terms in the epilogue)
   int32_t tmajor;          // tile-major FILTER: resident dataset-tile buffers (1, or 2: the next unit's tile
                            // loads while the current unit's query blocks stream past); 0 = block-major
   const int32_t* blist;
@@ -203,6 +206,10 @@ constexpr uint32_t kPolyPairsAug = DK_POLY_PAIRS_AUG;
 #ifndef DK_PINGPONG
 #define DK_PINGPONG 1
 #endif
+__host__ __device__ constexpr bool is_knn_sweep(int mode) {
+  return mode == MODE_TILEMIN || mode == MODE_FILTER || mode == MODE_HIST;
+}
+
 template <int MODE, bool kPair>
 __host__ __device__ constexpr bool use_pingpong() {
   return DK_PINGPONG != 0 && !kPair &&
@@ -235,8 +242,35 @@ __device__ __forceinline__ float2 exp2_poly2(float2 t) {
   return r;
 }
 
+// k-NN sweeps: the approximate d2 of a 32-column chunk.  Plain operands: S * m2s + (|q|^2 + |x|^2)
+// (packed FFMA2, the norms of the columns from shared memory).  Operands with norm columns (aug):
+// the accumulator already is -d2/2 in the operands' scale, d2 = S * m2s (an exact power-of-two
+// product); both are within the encoding's eps_q of the exact d2 (capi.cu make_encoding).
+__device__ __forceinline__ void knn_d2(const uint32_t (&r)[32], const float4* __restrict__ x4, float qn, float m2s,
+                                       bool aug, float (&d2v)[32]) {
+  const float2 m2 = make_float2(m2s, m2s);
+  if (aug) {
+#pragma unroll
+    for (int j2 = 0; j2 < 16; ++j2) {
+      const float2 v = mul2(make_float2(__uint_as_float(r[2 * j2]), __uint_as_float(r[2 * j2 + 1])), m2);
+      d2v[2 * j2] = v.x; d2v[2 * j2 + 1] = v.y;
+    }
+    return;
+  }
+  const float2 q2 = make_float2(qn, qn);
+#pragma unroll
+  for (int j4 = 0; j4 < 8; ++j4) {
+    const float4 xv = x4[j4];
+    const float2 da = fma2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), m2,
+                           add2(q2, make_float2(xv.x, xv.y)));
+    const float2 db = fma2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), m2,
+                           add2(q2, make_float2(xv.z, xv.w)));
+    d2v[4 * j4] = da.x; d2v[4 * j4 + 1] = da.y; d2v[4 * j4 + 2] = db.x; d2v[4 * j4 + 3] = db.y;
+  }
+}
+
 // One 32-column chunk of the epilogue.  `full` = all 32 columns valid (warp-uniform).
-template <int MODE>
+template <int MODE, bool kAug = false>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* __restrict__ xs_smem, float qn,
                                           float m2s, float negc, float tau, bool full, int64_t cbase, int64_t n,
                                           float2& acc0, float2& acc1, float& mn, const TileParams& p, int row,
@@ -289,17 +323,8 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
       }
     } else {
       // k-NN passes: packed distance arithmetic, branch-free hit mask
-      const float2 q2 = make_float2(qn, qn), m2 = make_float2(m2s, m2s);
       float d2v[32];
-#pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4) {
-        const float4 xv = x4[j4];
-        const float2 da = fma2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), m2,
-                               add2(q2, make_float2(xv.x, xv.y)));
-        const float2 db = fma2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), m2,
-                               add2(q2, make_float2(xv.z, xv.w)));
-        d2v[4 * j4] = da.x; d2v[4 * j4 + 1] = da.y; d2v[4 * j4 + 2] = db.x; d2v[4 * j4 + 3] = db.y;
-      }
+      knn_d2(r, x4, qn, m2s, kAug, d2v);
       if (!full) {  // columns past n: +inf never wins a min; NaN never passes a threshold (not even +inf)
         const int lim = int(min(int64_t(32), n - cbase));
         const float pad = MODE != MODE_TILEMIN ? __int_as_float(0x7fc00000) : __int_as_float(0x7f800000);
@@ -400,26 +425,17 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
   }
 }
 
-// Tile-major FILTER, one 32-column chunk: d2 exactly as epi_chunk's k-NN branch computes it (packed
+// Tile-major FILTER, one 32-column chunk: d2 exactly as epi_chunk's k-NN branch computes it (knn_d2, packed
 // FFMA2 of S * m2s + (|q|^2 + |x|^2)), a min tree to reject the chunk, and for the chunks of a warp
 // with hits the d2 row staged in shared memory (`sd`, this lane's row), from which each hit's key
 // is one load — no per-hit select chain over the registers.  Candidates go straight to the row's
 // global list (one atomic per row and chunk with hits).
+template <bool kAug>
 __device__ __forceinline__ void filter_chunk_tm(const uint32_t (&r)[32], const float* __restrict__ xs_smem, float qn,
                                                 float m2s, float tau, bool full, int64_t cbase, const TileParams& p,
                                                 int row, float* sd) {
-  const float4* x4 = reinterpret_cast<const float4*>(xs_smem);
-  const float2 q2 = make_float2(qn, qn), m2 = make_float2(m2s, m2s);
   float d2v[32];
-#pragma unroll
-  for (int j4 = 0; j4 < 8; ++j4) {
-    const float4 xv = x4[j4];
-    const float2 da = fma2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])), m2,
-                           add2(q2, make_float2(xv.x, xv.y)));
-    const float2 db = fma2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])), m2,
-                           add2(q2, make_float2(xv.z, xv.w)));
-    d2v[4 * j4] = da.x; d2v[4 * j4 + 1] = da.y; d2v[4 * j4 + 2] = db.x; d2v[4 * j4 + 3] = db.y;
-  }
+  knn_d2(r, reinterpret_cast<const float4*>(xs_smem), qn, m2s, kAug, d2v);
   float m0 = d2v[0], m1 = d2v[1], m2_ = d2v[2], m3 = d2v[3];
 #pragma unroll
   for (int j = 4; j < 32; j += 4) {
@@ -905,8 +921,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           mbar_wait(&xfull_bar[xs], (titer / kXnSlots) & 1);
           const float* xsm = smemX + xs * kBN + cg * 64;
-          filter_chunk_tm(r0, xsm, qn, m2s, tau, full, cbase, p, row, sd);
-          filter_chunk_tm(r1, xsm + 32, qn, m2s, tau, full, cbase + 32, p, row, sd);
+          if (p.knn_aug) {
+            filter_chunk_tm<true>(r0, xsm, qn, m2s, tau, full, cbase, p, row, sd);
+            filter_chunk_tm<true>(r1, xsm + 32, qn, m2s, tau, full, cbase + 32, p, row, sd);
+          } else {
+            filter_chunk_tm<false>(r0, xsm, qn, m2s, tau, full, cbase, p, row, sd);
+            filter_chunk_tm<false>(r1, xsm + 32, qn, m2s, tau, full, cbase + 32, p, row, sd);
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&xempty_bar[xs]);
         }
@@ -990,12 +1011,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* xsm = smemX + xs * xslot + cg * 64;
         const bool full = cbase + 64 <= p.n;
         float2 a0 = MODE == MODE_HIST ? hpar : make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f), b0 = a0;
-        if (any) {  // warp-uniform
-          epi_chunk<epi_mode(MODE)>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt, sbuf,
-                                    lrow);
+        // k-NN sweeps over operands with norm columns take the aug arithmetic (knn_d2), chosen per pass
+        auto chunks = [&](auto aug) {
+          constexpr bool kA = decltype(aug)::value;
+          epi_chunk<epi_mode(MODE), kA>(r0, xsm, qn, m2s, negc, tau, full, cbase, p.n, a0, a1, mn, p, row, scnt,
+                                        sbuf, lrow);
           // TILEMIN returns the chunk's two 16-column minima in its first accumulator
-          epi_chunk<epi_mode(MODE)>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n,
-                                    MODE == MODE_TILEMIN ? b0 : a0, a1, mn, p, row, scnt, sbuf, lrow);
+          epi_chunk<epi_mode(MODE), kA>(r1, xsm + 32, qn, m2s, negc, tau, full, cbase + 32, p.n,
+                                        MODE == MODE_TILEMIN ? b0 : a0, a1, mn, p, row, scnt, sbuf, lrow);
+        };
+        if (any) {  // warp-uniform
+          if (is_knn_sweep(MODE) && p.knn_aug) chunks(std::true_type{});
+          else chunks(std::false_type{});
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
