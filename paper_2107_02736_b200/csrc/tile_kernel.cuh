@@ -69,6 +69,7 @@ enum TileMode : int {
   MODE_KDE_COLD_AUG = 10   // KDE_COLD over operands with norm columns
 };
 constexpr int kHistBins = 64;  // MODE_HIST bins per query (quadratic spacing over [lo_q, top_q])
+constexpr int kHistStride = kHistBins + 1;  // shared-memory row stride of the bins (rows on distinct banks)
 __host__ __device__ constexpr bool is_kde(int mode) {
   return mode == MODE_KDE_GAUSS || mode == MODE_KDE_EXP || mode == MODE_KDE_GAUSS_MUFU || mode == MODE_KDE_COLD ||
          mode == MODE_KDE_HOT || mode == MODE_KDE_GAUSS_AUG || mode == MODE_KDE_COLD_AUG;
@@ -333,14 +334,17 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
       }
       if constexpr (MODE == MODE_HIST) {
         // tau holds htop; acc0 = (hlo, hinv) of this row (set by the caller); NaN pads never count
-        uint32_t* hrow = reinterpret_cast<uint32_t*>(sbuf) + lrow * kHistBins;
+        // bin b = floor(64 sqrt((d2 - lo) / (top - lo))): the approximate square root's ~2^-22 relative
+        // error sits far inside the 1e-5 slack of the bin edges (knn.cu tau_hist_kernel)
+        uint32_t* hrow = reinterpret_cast<uint32_t*>(sbuf) + lrow * kHistStride;
+        const float2 nlo = make_float2(-acc0.x, -acc0.x), hinv = make_float2(acc0.y, acc0.y);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (d2v[j] <= tau) {
-            const float u = fmaxf((d2v[j] - acc0.x) * acc0.y, 0.f);
-            const int b = min(kHistBins - 1, __float2int_rz(sqrtf(u) * float(kHistBins)));
-            atomicAdd(hrow + b, 1u);
-          }
+        for (int j2 = 0; j2 < 16; ++j2) {
+          const float2 u = mul2(add2(make_float2(d2v[2 * j2], d2v[2 * j2 + 1]), nlo), hinv);
+          if (d2v[2 * j2] <= tau)
+            atomicAdd(hrow + min(kHistBins - 1, __float2int_rz(sqrt_approx(fmaxf(u.x, 0.f)) * float(kHistBins))), 1u);
+          if (d2v[2 * j2 + 1] <= tau)
+            atomicAdd(hrow + min(kHistBins - 1, __float2int_rz(sqrt_approx(fmaxf(u.y, 0.f)) * float(kHistBins))), 1u);
         }
       } else if constexpr (MODE == MODE_TILEMIN) {
         // minima of the two 16-column halves (listed sweeps keep them as separate segments)
@@ -568,9 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = threadIdx.x; i < kBM; i += blockDim.x) scnt[i] = 0;
   }
   if constexpr (MODE == MODE_HIST) {
-    static_assert(kBM * kHistBins * 4 <= kBM * kStageCap * 8, "histogram bins must fit the staging area");
+    static_assert(kBM * kHistStride * 4 <= kBM * kStageCap * 8 + kBM * 4, "histogram bins must fit the staging area");
     uint32_t* hb = reinterpret_cast<uint32_t*>(sbuf);
-    for (int i = threadIdx.x; i < kBM * kHistBins; i += blockDim.x) hb[i] = 0u;
+    for (int i = threadIdx.x; i < kBM * kHistStride; i += blockDim.x) hb[i] = 0u;
   }
   if (warp == 2) {
     if constexpr (kPair) tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -1054,7 +1058,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // flush the unit's bins: one global atomic per nonzero (row, bin)
         epi_bar();
         if (cg == 0) {
-          uint32_t* hrow = reinterpret_cast<uint32_t*>(sbuf) + lrow * kHistBins;
+          uint32_t* hrow = reinterpret_cast<uint32_t*>(sbuf) + lrow * kHistStride;
           for (int b = 0; b < kHistBins; ++b) {
             const uint32_t v = hrow[b];
             if (v) {
