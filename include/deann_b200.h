@@ -280,6 +280,12 @@ dk_status dk_knn_stats(dk_handle h, int64_t* queries, int64_t* cand_sum, int64_t
  * the hot (query block, tile) pairs / all pairs of the last call's first batch (-1: not yet
  * known).  No reference counterpart. */
 dk_status dk_kde_stats(dk_handle h, int64_t* queries, int64_t* fallbacks, int64_t* hot_pairs, int64_t* total_pairs);
+/* Queries of the last dk_naive call on this handle that the guard of the split3 sweeps recomputed
+ * in fp64 direct differences, as the reference evaluates every pair (naive_kde estimators.py:144-149):
+ * exponential-kernel queries with a row closer than the distance under which the sweep's d2 error
+ * could move exp(-sqrt(d2)/h) by more than 1e-4, gaussian queries whose d2 error bound exceeds
+ * 5e-5 x 2h^2.  Waits for that call's work.  No reference counterpart. */
+dk_status dk_kde_redo_count(dk_handle h, int64_t* count);
 /* Diagnostics: time (ms, CUDA events) of one tile sweep of the given mode
  * (0 KDE-gauss, 1 KDE-exp, 2 segment-min, 3 filter, 4 null epilogue) with the
  * given operand encoding (0 exact, 1 split3, 2 fp16) — a pipeline probe. */

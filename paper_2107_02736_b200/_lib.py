@@ -28,7 +28,7 @@ EXPORTED = (
     "dk_info", "dk_sq_norms",
     "dk_naive", "dk_sqdist", "dk_knn", "dk_merge_topk", "dk_sample", "dk_eval_rows", "dk_kernel_values", "dk_deann",
     "dk_rsp_attach", "dk_rsp_walk", "dk_ivf_create", "dk_ivf_free", "dk_kmeanspp_seed", "dk_kmeanspp_pick",
-    "dk_kmeans_lloyd", "dk_ivf_get", "dk_ivf_set", "dk_ivf_query", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_kde_stats", "dk_sweep_probe",
+    "dk_kmeans_lloyd", "dk_ivf_get", "dk_ivf_set", "dk_ivf_query", "dk_last_kernel_ms", "dk_set_profiling", "dk_last_launch_count", "dk_knn_stats", "dk_kde_stats", "dk_kde_redo_count", "dk_sweep_probe",
     "dk_host_alloc", "dk_host_free", "dk_deann_ivf", "dk_deann_combine", "dk_mufu_probe",
 )
 
@@ -103,6 +103,7 @@ def _declare(lib):
                                 ctypes.POINTER(_i64)]),
         "dk_kde_stats": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                 ctypes.POINTER(_i64)]),
+        "dk_kde_redo_count": (_i32, [_vp, ctypes.POINTER(_i64)]),
         "dk_host_alloc": (_i32, [_i64, ctypes.POINTER(_vp)]),
         "dk_host_free": (_i32, [_vp]),
     }

@@ -784,6 +784,14 @@ double env_double(const char* name, double def) {
   return v ? std::atof(v) : def;
 }
 
+bool kde_guard_on() {  // A/B: DK_KDE_GUARD=0 leaves the split3 sweeps unguarded
+  static const bool on = [] {
+    const char* v = std::getenv("DK_KDE_GUARD");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int hyb_env() {  // -1 auto, 0 off, 1 forced
   const char* v = std::getenv("DK_KDE_HYBRID");
   return v ? (std::atoi(v) != 0 ? 1 : 0) : -1;
@@ -1115,6 +1123,8 @@ HandlePtr new_handle(int64_t n, int32_t d, const dk_fit_opts* opts) {
     DeviceGuard g(device);
     DK_CUDA(cudaHostAlloc(&h->flag_host, 2 * sizeof(uint32_t), cudaHostAllocDefault));
     DK_CUDA(cudaEventCreateWithFlags(&h->flag_event, cudaEventDisableTiming));
+    DK_CUDA(cudaHostAlloc(&h->redo_host, 2 * sizeof(int32_t), cudaHostAllocDefault));
+    DK_CUDA(cudaEventCreateWithFlags(&h->redo_event, cudaEventDisableTiming));
   }
   return h;
 }
@@ -1393,6 +1403,8 @@ dk_status dk_free(dk_handle h) {
     if (h->rsp_inverse) cudaFree(h->rsp_inverse);
     if (h->flag_host) cudaFreeHost(h->flag_host);
     if (h->flag_event) cudaEventDestroy(h->flag_event);
+    if (h->redo_host) cudaFreeHost(h->redo_host);
+    if (h->redo_event) cudaEventDestroy(h->redo_event);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     if (h->copy_ready) cudaEventDestroy(h->copy_ready);
     if (h->copy_done) cudaEventDestroy(h->copy_done);
@@ -1476,12 +1488,13 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     // per-batch passes (ball order, two query encodes, hot lists, split3 pass) cost more when split
     // than the hidden copy saves (c3 end to end 4.47 -> 3.6 ms)
     const bool hyb = hyb_prepare(h, family, nq, s);
+    h->redo_mask = 0;
     const int64_t split = (host_q && nq >= 4096 && !hyb) ? round_up(nq / split_div, 256) : nq;
     const int64_t c_beg[2] = {0, split};
     const int64_t c_cnt[2] = {split, nq - split};
     const int nchunks = c_cnt[1] > 0 ? 2 : 1;
     const int32_t Kp_max = int32_t(round_up(3 * int64_t(h->d), kBK));
-    size_t o_A[2], o_At[2], o_qn[2], o_scal[2], o_part[2], o_fl[2];
+    size_t o_A[2], o_At[2], o_qn[2], o_scal[2], o_part[2], o_fl[2], o_tau[2] = {}, o_gflag[2] = {}, o_rlist[2] = {}, o_rpart[2] = {};
     for (int c = 0; c < nchunks; ++c) {
       const int32_t pad = int32_t(query_pad(c_cnt[c]));
       o_A[c] = pl.add<__half>(size_t(pad) * Kp_max);
@@ -1490,6 +1503,12 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       o_scal[c] = pl.add<float>(4);
       o_part[c] = pl.add<double>(sweep_part_count(h->n_pad, pad, h->num_sms));
       o_fl[c] = pl.add<uint32_t>(4);
+      if (!hyb) {  // guard of the split3 sweeps (redo.cu)
+        o_tau[c] = pl.add<float>(pad);
+        o_gflag[c] = pl.add<uint32_t>(pad);
+        o_rlist[c] = pl.add<int32_t>(size_t(pad) + 4);
+        o_rpart[c] = pl.add<double>(size_t(c_cnt[c]) * kRedoChunks);
+      }
     }
     const HybLayout HL = hyb ? hyb_layout(h, std::max(c_cnt[0], c_cnt[1]), nq, pl.off) : HybLayout{};
     h->ws.reserve(hyb ? HL.end + 4096 : pl.off);
@@ -1540,6 +1559,24 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       a.negc = negc;
       a.part = at<double>(h->ws, o_part[c]);
       a.guard = guard_flags;
+      // split3 sweeps are guarded: the d2 of a pair is off by about delta_q = delta_rel (|q|^2 + max |x|^2)
+      // (operand rounding 2^-22 |q||x| plus the fp32 accumulation over Kp / 16 MMA steps, which
+      // truncates: measured on sparse d = 784 rows, gaussian, 2h^2 = 4: 4.5e-4 against this model's
+      // 4.9e-4).  Queries whose kernel values that error can move by more than the tolerance are
+      // recomputed in fp64 (redo.cu): every exponential-kernel row with an approximate d2 under
+      // (delta_q / (tol h))^2 (flagged by the sweep), every gaussian query with delta_q > tol 2h^2.
+      const bool guarded = mode == 1 && kde_guard_on();
+      uint32_t* gflag = nullptr;
+      if (guarded) {
+        const double delta_rel = 0.5 * (std::ldexp(1.0, -21) + double(e.Kp / 16) * std::ldexp(1.0, -24));
+        gflag = at<uint32_t>(h->ws, o_gflag[c]);
+        launch_guard_tau(q.qn, pad, cn, e.xn_max, delta_rel, family == DK_GAUSSIAN ? 5e-5 : 1e-4, bandwidth,
+                         family == DK_GAUSSIAN, at<float>(h->ws, o_tau[c]), gflag, s);
+        if (family != DK_GAUSSIAN) {
+          a.tau = at<float>(h->ws, o_tau[c]);
+          a.cand_cnt = gflag;
+        }
+      }
       int32_t ncc = 0;
       a.ncc_out = &ncc;
       {
@@ -1547,6 +1584,14 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
         launch_sweep(a, h->num_sms, s);
       }
       launch_reduce_partials(a.part, ncc * kColGroups, pad, cn, scale, od + q0, s);
+      if (guarded) {
+        int32_t* rlist = at<int32_t>(h->ws, o_rlist[c]);
+        launch_kde_redo(h->X, h->n, h->d, Qc, cn, family == DK_GAUSSIAN, bandwidth, gflag, rlist + 4, rlist,
+                        at<double>(h->ws, o_rpart[c]), scale, od + q0, h->num_sms, s);
+        DK_CUDA(cudaMemcpyAsync(h->redo_host + c, rlist, sizeof(int32_t), cudaMemcpyDeviceToHost, s));  // statistics
+        DK_CUDA(cudaEventRecord(h->redo_event, s));
+        h->redo_mask |= 1 << c;
+      }
       if (!out_dev) copy_out(out + q0, od + q0, size_t(cn) * sizeof(double), s);
     };
     // Integer dataset: the exact-mode sweeps are launched without waiting for the query check.
@@ -2042,6 +2087,20 @@ dk_status dk_kde_stats(dk_handle h, int64_t* queries, int64_t* fallbacks, int64_
     }
     if (hot_pairs) *hot_pairs = hot;
     if (total_pairs) *total_pairs = tot;
+  });
+}
+
+dk_status dk_kde_redo_count(dk_handle h, int64_t* count) {
+  return guard([&] {
+    DK_REQUIRE(h != nullptr && count != nullptr, "NULL argument");
+    DeviceGuard g(h->device);
+    int64_t c = 0;
+    if (h->redo_mask) {
+      DK_CUDA(cudaEventSynchronize(h->redo_event));
+      for (int i = 0; i < 2; ++i)
+        if (h->redo_mask & (1 << i)) c += h->redo_host[i];
+    }
+    *count = c;
   });
 }
 

@@ -229,6 +229,10 @@ struct dk_dataset {
   int64_t* rsp_inverse = nullptr;  // [n] original id -> permuted position (dk_rsp_attach)
   uint32_t* flag_host = nullptr;   // pinned words: query-check flags of the speculative sweeps (2 chunks)
   cudaEvent_t flag_event = nullptr;
+  // exact-KDE guard (redo.cu): queries of the last dk_naive call recomputed in fp64, per chunk (pinned)
+  int32_t* redo_host = nullptr;
+  cudaEvent_t redo_event = nullptr;
+  int redo_mask = 0;
   cudaStream_t copy_stream = nullptr;  // side stream for the overlapped host->device query copy
   cudaEvent_t copy_ready = nullptr, copy_done = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -325,6 +329,14 @@ size_t sweep_part_count(int64_t n_pad, int32_t nq_pad, int num_sms, bool allow_p
 size_t sweep_part_bound(int64_t n_pad, int32_t max_pad, int num_sms);
 void launch_sweep(const SweepArgs& a, int num_sms, cudaStream_t s);
 void set_pair_enabled(bool on);  // 2-CTA (cta_group::2) sweeps; off by default (DK_PAIR=1)
+
+// exact-KDE guard (redo.cu): per-query thresholds / flags, and the fp64 recomputation of flagged queries
+constexpr int32_t kRedoChunks = 64;  // row chunks per listed query (partials: [nq][kRedoChunks])
+void launch_guard_tau(const float* qn, int32_t nq_pad, int64_t nq, float xn_max, double delta_rel, double tol,
+                      double h, bool gaussian, float* tau, uint32_t* flag, cudaStream_t s);
+void launch_kde_redo(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, bool gaussian, double h,
+                     const uint32_t* flag, int32_t* list, int32_t* count, double* part, double scale, double* out,
+                     int num_sms, cudaStream_t s);
 
 // two-precision exact gaussian KDE (hybrid.cu)
 constexpr int32_t kHotUnitsPerBlock = 16;  // split3 work units per query block (partials: [units][4][128])

@@ -318,6 +318,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
         for (int jj = 0; jj < 4; ++jj) {
           const int j = j4 * 4 + jj;
           const float d2 = fmaf(__uint_as_float(r[j]), m2s, qn + xs[jj]);
+          mn = fminf(mn, d2);  // near-pair guard: the row's smallest approximate d2 (see the unit end)
           const float e = ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
           if (jj & 1) acc0.y += e; else acc0.x += e;
         }
@@ -423,9 +424,21 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float* 
       if constexpr (MODE == MODE_KDE_GAUSS || MODE == MODE_KDE_GAUSS_MUFU) {
         acc0.x += ex2_approx(d2 * negc);
       } else {
+        if constexpr (MODE == MODE_KDE_EXP) mn = fminf(mn, d2);
         acc0.x += ex2_approx(sqrt_approx(fmaxf(d2, 0.f)) * negc);
       }
     }
+  }
+}
+
+// Exponential kernel, near-pair guard: exp(-sqrt(d2)/h) amplifies the operand-rounding error of a small
+// d2 (|sqrt(a) - sqrt(b)| ~ |a - b| / (2 sqrt(b)), unbounded at a coincident pair).  A row whose smallest
+// approximate d2 falls under its threshold tau (capi.cu exp_guard: the d2 below which the error of
+// sqrt(d2)/h can exceed the tolerance) is flagged and re-evaluated in fp64 (redo.cu).
+template <int MODE>
+__device__ __forceinline__ void exp_guard_flag(const TileParams& p, int row, float mn) {
+  if constexpr (MODE == MODE_KDE_EXP) {
+    if (p.tau != nullptr && mn < p.tau[row]) p.cand_cnt[row] = 1u;
   }
 }
 
@@ -829,8 +842,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t titer = 0;
     const float m2s = *p.m2s;
     const float negc = is_aug(MODE) ? p.negc * m2s : p.negc;  // norm columns: t = S * m2s * negc
-    float mn_unused = 0.f;
     for (int u = first_unit; u < nunits; u += unit_step) {
+      float mn = __int_as_float(0x7f800000);  // MODE_KDE_EXP: smallest approximate d2 of the row in this unit
       const int qb = u % ngroups, cc = u / ngroups;
       const int t0 = cc * p.tiles_per_unit;
       const int t1 = min(p.ntiles, t0 + p.tiles_per_unit);
@@ -860,10 +873,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[group]);
           }
-          epi_chunk<epi_mode(MODE)>(r0, xsm + sub * 64, qn, m2s, negc, 0.f, full, cbase, p.n, a0, a1, mn_unused, p,
+          epi_chunk<epi_mode(MODE)>(r0, xsm + sub * 64, qn, m2s, negc, 0.f, full, cbase, p.n, a0, a1, mn, p,
                                     row, nullptr, nullptr, lrow);
           epi_chunk<epi_mode(MODE)>(r1, xsm + sub * 64 + 32, qn, m2s, negc, 0.f, full, cbase + 32, p.n, a0, a1,
-                                    mn_unused, p, row, nullptr, nullptr, lrow);
+                                    mn, p, row, nullptr, nullptr, lrow);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty_bar[xs]);
@@ -880,6 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
+      exp_guard_flag<MODE>(p, row, mn);
     }
   } else if (tmajor && warp >= kEpiWarp0) {
     // ===================== tile-major FILTER epilogue =====================
@@ -1051,6 +1065,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.part[(size_t(u) * kColGroups + cg) * kBM + lrow] = usum;  // listed: one partial per unit
       } else if constexpr (is_kde(MODE)) {
         p.part[(size_t(cc) * kColGroups + cg) * p.nq_pad + row] = usum;
+        exp_guard_flag<MODE>(p, row, mn);
       } else if constexpr (MODE == MODE_TILEMIN) {
         if (t1 > t0 && p.seg_tiles > 0)
           atomicMin(reinterpret_cast<int*>(&p.tmin[size_t(seg) * p.nq_pad + row]), __float_as_int(fmaxf(mn, 0.f)));

@@ -188,3 +188,67 @@ def test_pinned_result_buffers_lifecycle():
     idx2, d22 = g.knn_batch(ds, Q[:7], 100)    # small: numpy path
     np.testing.assert_array_equal(idx[:7], idx2)
     np.testing.assert_array_equal(d2[:7], d22)
+
+
+def _redo_count(ds) -> int:
+    import ctypes
+
+    from paper_2107_02736_b200 import _lib
+
+    c = ctypes.c_int64(-1)
+    _lib.check(_lib.load().dk_kde_redo_count(ds.handle, ctypes.byref(c)))
+    return int(c.value)
+
+
+@pytest.mark.parametrize("n,d,scale,h", [(392, 3, 1.0, 0.075), (219, 16, 1.0, 0.19), (5000, 129, 1.0, 2.4),
+                                         (13000, 16, 30.0, 25.0), (70000, 1, 1.0, 0.14)])
+def test_exponential_queries_on_data_points(n, d, scale, h):
+    """exp(-sqrt(d2)/h) at a (near-)coincident pair amplifies the sweep's d2 error to sqrt(eps)/h: the
+    guard re-evaluates those queries in fp64 direct differences (redo.cu), as naive_kde
+    (estimators.py:144-149) evaluates every pair.  Unguarded, these cases are off by 2e-4 .. 5e-3."""
+    rng = np.random.default_rng(n + d)
+    X = (rng.normal(size=(n, d)) * scale).astype(np.float32)
+    if d == 3:
+        X = np.where(rng.random((n, d)) < 0.8, 0.0, rng.random((n, d))).astype(np.float32)
+    Q = X[rng.integers(0, n, size=200)].astype(np.float64)
+    ds = g.Dataset.from_array(X)
+    got = g.naive_kde(ds, g.KernelSpec("exponential", h), Q).values
+    assert _redo_count(ds) == 200
+    ref = O.naive_kde(O.Data(X), "exponential", h, Q)
+    assert _rel(got, ref) < 5e-6  # the reference's own d2 (norms identity) is good to ~1e-15 |x|^2 at a coincident pair
+    if d == 1:
+        return  # 70,000 points on a line: every query has a row within any threshold
+    # queries away from the rows stay on the tensor-core sweep
+    far = Q + 3.0 * scale
+    got = g.naive_kde(ds, g.KernelSpec("exponential", 40.0 * h), far).values
+    assert _redo_count(ds) == 0
+    assert _rel(got, O.naive_kde(O.Data(X), "exponential", 40.0 * h, far)) < KDE_RTOL
+
+
+def test_gaussian_bandwidth_narrow_against_the_norms():
+    """2h^2 = 4 on sparse 784-dimensional rows (|x|^2 ~ 50, K = 2352): the fp32 accumulation error of
+    d2, ~5e-4, is 1.2e-4 of 2h^2, so the whole batch takes the fp64 path (1.1e-4 unguarded)."""
+    rng = np.random.default_rng(359)
+    n, d = 6000, 784
+    X = np.where(rng.random((n, d)) < 0.8, 0.0, rng.random((n, d))).astype(np.float32)
+    Q = np.where(rng.random((64, d)) < 0.8, 0.0, rng.random((64, d)))
+    ds = g.Dataset.from_array(X)
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", 1.42), Q).values
+    assert _redo_count(ds) == 64
+    assert _rel(got, O.naive_kde(O.Data(X), "gaussian", 1.42, Q)) < 1e-9
+    # a bandwidth in proportion to the data stays on the sweep
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", 6.0), Q).values
+    assert _redo_count(ds) == 0
+    assert _rel(got, O.naive_kde(O.Data(X), "gaussian", 6.0, Q)) < KDE_RTOL
+
+
+def test_guard_on_dataset_shards():
+    """A shard handle's recomputed queries carry the shard's sum scaled by the global row count."""
+    rng = np.random.default_rng(5)
+    n, d, h = 3000, 8, 0.3
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    Q = X[:50].astype(np.float64)
+    parts = [g.Dataset.from_array(X[lo:hi], global_offset=lo, global_n=n) for lo, hi in [(0, 1200), (1200, n)]]
+    total = sum(g.naive_kde(p, g.KernelSpec("exponential", h), Q).values for p in parts)
+    assert _redo_count(parts[0]) == 50
+    assert _rel(total, O.naive_kde(O.Data(X), "exponential", h, Q)) < 1e-6  # the unflagged shard is a sweep
