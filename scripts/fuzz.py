@@ -66,25 +66,30 @@ def tie_tolerant_equal(gi, gd, ri, rd):
 def trial(seed):
     rng = np.random.default_rng(seed)
     kind = KINDS[int(rng.integers(0, len(KINDS)))]
-    size = rng.choice(["small", "mid", "big"], p=[0.3, 0.45, 0.25])
+    size = rng.choice(["small", "mid", "big", "hyb"], p=[0.3, 0.4, 0.2, 0.1])
     if size == "small":
         n = int(rng.integers(1, 400))
     elif size == "mid":
         n = int(rng.integers(400, 30000))
-    else:
+    elif size == "big":
         n = int(rng.integers(66000, 260000))
+    else:  # large gaussian batches on non-integer rows: the two-precision exact KDE
+        n = int(rng.integers(131072, 400000))
+        kind = str(rng.choice(["normal", "mixture", "sparse", "unit", "offset"]))
     d = int(rng.choice([1, 2, 3, 7, 16, 31, 64, 96, 100, 128, 129, 200, 300, 784]))
-    if size == "big":
+    if size in ("big", "hyb"):
         d = min(d, 128)
     nq = int(rng.choice([1, 2, 33, 128, 129, 300, 700, 2500]))
     if size == "big":
         nq = min(nq, 700)
+    if size == "hyb":
+        nq = int(rng.choice([2048, 2500, 4097]))
     X = make_rows(rng, kind, n, d).astype(np.float32)
     Q = make_rows(rng, kind, nq, d)
     if rng.random() < 0.3:  # queries on data points
         take = rng.integers(0, n, size=nq)
         Q = X[take].astype(np.float64)
-    fam = str(rng.choice(["gaussian", "exponential", "laplacian"]))
+    fam = str(rng.choice(["gaussian", "exponential", "laplacian"])) if size != "hyb" else "gaussian"
     if fam == "laplacian" and n * nq * d > 4e10:
         fam = "gaussian"
     # bandwidth from a pilot so that values neither underflow nor saturate
@@ -102,8 +107,9 @@ def trial(seed):
     msgs = []
     ok = True
 
-    got = g.naive_kde(ds, spec, Q).values
-    ref = O.naive_kde(od, fam, h, Q)
+    chk = np.arange(nq) if float(n) * nq * d < 3e10 else np.sort(rng.choice(nq, size=64, replace=False))
+    got = g.naive_kde(ds, spec, Q).values[chk]
+    ref = O.naive_kde(od, fam, h, Q[chk])
     live = ref > 1e-280
     e_naive = float(np.max(np.abs(got[live] - ref[live]) / ref[live])) if live.any() else 0.0
     dead = float(np.max(np.abs(got[~live]))) if (~live).any() else 0.0
