@@ -1460,6 +1460,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     const size_t o_flags = pl.add<uint32_t>(4);
     if (family == DK_LAPLACIAN) {
       const size_t o_part = pl.add<double>(l1_part_count(h->n, int32_t(nq)));
+      const size_t o_q32 = pl.add<float>(size_t(l1_nq_pad(nq)) * h->d);
       h->ws.reserve(pl.off);
       const double* Qd = stage_queries(h, Q, nq, o_Q, s);
       int32_t nparts = 0;
@@ -1467,7 +1468,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       double* od = out_dev ? out : at<double>(h->ws, o_out);
       {
         ProfScope ps(h, s, 3.0 * double(h->d) * double(nq) * double(h->n), double(h->n) * h->d * 4, 1);
-        launch_l1_kde(h->X, h->n, h->d, Qd, nq, 1.0 / bandwidth, part, &nparts, nullptr, s);
+        launch_l1_kde(h->X, h->n, h->d, Qd, nq, 1.0 / bandwidth, part, &nparts, at<float>(h->ws, o_q32), s);
       }
       launch_reduce_partials(part, nparts, l1_nq_pad(nq), nq, scale, od, s);
       if (!out_dev) {
