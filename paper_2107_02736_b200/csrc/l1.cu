@@ -147,14 +147,22 @@ __global__ void __launch_bounds__(kL1Threads, kL1Blocks) l1_kde_kernel(const flo
 // The register-staged loads above cost the FADD2 pipe ~30% (ncu, c4: long-scoreboard waits on the
 // staged global loads before each shared-memory store, 2-way conflicts on those stores, one barrier
 // per 16 dimensions with 2 warps per scheduler).  Here each chunk of 32 dimensions goes global ->
-// shared memory with 4-byte cp.async (zero fill past n / d), two stages, issued one chunk ahead
+// shared memory with 4-byte cp.async (zero fill past n / d), three stages, issued two chunks ahead
 // across tile boundaries, so nothing waits on a scoreboard and there is one barrier per 32
 // dimensions.  The element -> (row, dim) map puts 8 consecutive dimensions x 4 rows in a warp: full
 // 32-byte sectors from global memory and 32 distinct banks on the transposed store.  Queries are
 // converted to fp32 once per call (q32) so they ride the same copies.
-constexpr int DK2 = 32;
+#ifndef DK_L1_DK2
+#define DK_L1_DK2 32
+#endif
+constexpr int DK2 = DK_L1_DK2;  // dimensions per chunk (32 or 64)
+constexpr int kL1KH = DK2 == 64 ? 3 : 2;  // thread-id bits (from bit 5) that index the chunk's 8-dimension groups
 constexpr int kL1Pitch = TX + XPAD;  // floats per dimension row (TQ == TX)
-constexpr size_t kL1SmemV2 = size_t(2) * 2 * DK2 * kL1Pitch * sizeof(float);
+#ifndef DK_L1_STAGES
+#define DK_L1_STAGES 3
+#endif
+constexpr int kL1Stages = DK_L1_STAGES;
+constexpr size_t kL1SmemV2 = size_t(kL1Stages) * 2 * DK2 * kL1Pitch * sizeof(float);
 
 __global__ void l1_q32_kernel(const double* __restrict__ Q, int64_t nq, int32_t d, int64_t total,
                               float* __restrict__ q32) {
@@ -178,8 +186,10 @@ __global__ void __launch_bounds__(256, 1) l1_kde_kernel_v2(const float* __restri
   const int total = ntl * nchunks;
   // this thread's 16 (row, dim) slots of a chunk: idx = r * 256 + tid, dim = idx[0:3) | idx[5:7) << 3,
   // row = idx[3:5) | idx[7:12) << 2
-  const int kk_t = (threadIdx.x & 7) | (((threadIdx.x >> 5) & 3) << 3);
-  const int row_t = ((threadIdx.x >> 3) & 3) | ((threadIdx.x >> 7) << 2);
+  static_assert(DK2 == 32 || DK2 == 64, "chunk widths of the index map");
+  const int kk_t = (threadIdx.x & 7) | (((threadIdx.x >> 5) & (DK2 / 8 - 1)) << 3);
+  const int row_t = ((threadIdx.x >> 3) & 3) | ((threadIdx.x >> (5 + kL1KH)) << 2);
+  constexpr int kRowStep = 4 << (3 - kL1KH);
   auto load = [&](int it, int st) {
     const int xt = it / nchunks, c = it - xt * nchunks;
     const int64_t x0 = (tile0 + xt) * TX;
@@ -188,8 +198,8 @@ __global__ void __launch_bounds__(256, 1) l1_kde_kernel_v2(const float* __restri
     float* qd = qs(st) + kk_t * kL1Pitch;
     float* xd = xs(st) + kk_t * kL1Pitch;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const int row = row_t + 8 * r;
+    for (int r = 0; r < TX / kRowStep; ++r) {
+      const int row = row_t + kRowStep * r;
       const int64_t xi = x0 + row;
       const bool xin = kin && xi < n;
       cp_async4(qd + row, kin ? Q32 + (q0 + row) * d + k : Q32, kin ? 4u : 0u);
@@ -202,15 +212,20 @@ __global__ void __launch_bounds__(256, 1) l1_kde_kernel_v2(const float* __restri
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-  if (total > 0) load(0, 0);
-  cp_async_commit();
-  int xt = 0, c = 0;
-  for (int it = 0; it < total; ++it) {
-    const int st = it & 1;
-    cp_async_wait<0>();
-    __syncthreads();  // chunk `it` visible to all; every warp is done reading stage st ^ 1
-    if (it + 1 < total) load(it + 1, st ^ 1);
+#pragma unroll
+  for (int p = 0; p < kL1Stages - 1; ++p) {
+    if (p < total) load(p, p);
     cp_async_commit();
+  }
+  int xt = 0, c = 0, st = 0;
+  for (int it = 0; it < total; ++it) {
+    cp_async_wait<kL1Stages - 2>();  // all but the newest kL1Stages - 2 groups: chunk `it` has landed
+    __syncthreads();  // ... for every thread's copies; every warp is done reading the stage refilled next
+    {
+      const int nx = it + kL1Stages - 1;
+      if (nx < total) load(nx, st == 0 ? kL1Stages - 1 : st - 1);
+      cp_async_commit();
+    }
     const float* Qb = qs(st);
     const float* Xb = xs(st);
     float2 part_acc[8][4];
@@ -258,6 +273,7 @@ __global__ void __launch_bounds__(256, 1) l1_kde_kernel_v2(const float* __restri
       c = 0;
       ++xt;
     }
+    if (++st == kL1Stages) st = 0;
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
