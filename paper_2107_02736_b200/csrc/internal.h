@@ -233,6 +233,7 @@ struct dk_dataset {
   int32_t* redo_host = nullptr;
   cudaEvent_t redo_event = nullptr;
   int redo_mask = 0;
+  int64_t knn_budget = 0;  // bytes of k-NN candidate storage per batch (set at fit from the free memory)
   cudaStream_t copy_stream = nullptr;  // side stream for the overlapped host->device query copy
   cudaEvent_t copy_ready = nullptr, copy_done = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
