@@ -770,6 +770,22 @@ size_t knn_ws_bytes(const dk_dataset* h, int32_t k, int64_t nq) {
   return knn_layout(h, kp, k, Kp_max, knn_prunable(h, kp), 0).end + 4096;
 }
 
+// Reserve the call's workspace; when the batch planned from the fit-time memory no longer fits
+// (other handles or the caller's tensors have taken it since), halve the candidate budget — the
+// batch shrinks with it — down to the round-1 plan, then give up with DK_ENOMEM.
+void reserve_knn_ws(dk_dataset* h, size_t base, int32_t k, int64_t nq) {
+  for (;;) {
+    try {
+      h->ws.reserve(base + knn_ws_bytes(h, k, nq));
+      return;
+    } catch (const Error& e) {
+      if (e.code != DK_ENOMEM || h->knn_budget <= (int64_t(1) << 30)) throw;
+      (void)cudaGetLastError();
+      h->knn_budget = std::max<int64_t>(int64_t(1) << 30, h->knn_budget / 2);
+    }
+  }
+}
+
 
 // ------------------------------------------------------------------ two-precision exact KDE
 // Exact gaussian KDE of non-integer data (hybrid.cu): the single-pass fp16 sweep over the
@@ -1658,7 +1674,7 @@ dk_status dk_knn(dk_handle h, const double* Q, int64_t nq, int32_t k, int64_t* i
     const size_t o_idx = pl.add<int64_t>(size_t(nq) * k);
     const size_t o_d2 = pl.add<double>(size_t(nq) * k);
     const size_t base = pl.off;
-    h->ws.reserve(base + knn_ws_bytes(h, k, nq));
+    reserve_knn_ws(h, base, k, nq);
     const double* Qd = stage_queries(h, Q, nq, o_Q, s);
     int64_t* idx_d = idx_dev ? idx_out : at<int64_t>(h->ws, o_idx);
     double* d2_d = d2_dev ? d2_out : at<double>(h->ws, o_d2);
@@ -1868,7 +1884,8 @@ dk_status dk_deann(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     const size_t seg_bytes = long_excl ? seg_sort_temp_bytes(k, nq) : 0;
     const size_t o_seg = pl.add<uint8_t>(seg_bytes);
     const size_t base = pl.off;
-    h->ws.reserve(base + (k > 0 ? knn_ws_bytes(h, k, nq) : 0));
+    if (k > 0) reserve_knn_ws(h, base, k, nq);
+    else h->ws.reserve(base);
     const double* Qd = stage_queries(h, Q, nq, o_Q, s);
     int64_t* idx = at<int64_t>(h->ws, o_idx);
     double* d2 = at<double>(h->ws, o_d2);
