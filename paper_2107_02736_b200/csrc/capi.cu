@@ -744,8 +744,9 @@ void knn_device(dk_dataset* h, const double* Qd, int64_t nq, int32_t k, int64_t*
     // pruned: candidates are positions in the cluster-sorted rows (read from there, reported as row ids)
     launch_select(prune ? h->kc->xs : h->X, h->global_offset, h->d, Qb, bn, k, cand, cnt, kp.cap, q.qn, e.xn_max,
                   e.eps_rel, idx_b, d2_b, lists, ctr, h->num_sms, s, prune ? h->kc->perm : nullptr);
+    // (the candidate lists are free once the selection has run: scratch for the fallback's row slices)
     launch_exact_knn_fallback(h->X, h->n, h->global_offset, h->d, Qb, lists + bn, ctr + 1, k, idx_b, d2_b,
-                              h->num_sms, s);
+                              h->num_sms, s, cand, size_t(kp.cap) * size_t(kp.batch) * sizeof(unsigned long long));
     if (h->knn_stats) {
       std::vector<uint32_t> c(static_cast<size_t>(bn));
       int32_t nf = 0;

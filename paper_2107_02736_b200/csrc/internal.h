@@ -428,7 +428,8 @@ void launch_select(const float* X, int64_t global_offset, int32_t d, const doubl
                    int num_sms, cudaStream_t s, const int64_t* perm = nullptr);
 void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
                                const int32_t* qlist, const int32_t* qcount, int32_t k, int64_t* idx_out,
-                               double* d2_out, int num_sms, cudaStream_t s);
+                               double* d2_out, int num_sms, cudaStream_t s, void* tmp = nullptr,
+                               size_t tmp_bytes = 0);  // tmp: scratch for row slices (>= 65,536 k bytes to use them)
 void launch_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_in, const double* d2_in,
                        int64_t* idx_out, double* d2_out, cudaStream_t s);
 void launch_kernel_values(int32_t family, double h, const double* dist, int64_t count, double* out, uint32_t* bad,

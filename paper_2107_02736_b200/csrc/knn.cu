@@ -548,37 +548,116 @@ template <int G>
 __global__ void exact_knn_kernel(const float* __restrict__ X, int64_t n, int64_t global_offset, int32_t d,
                                  const double* __restrict__ Q, const int32_t* __restrict__ qlist,
                                  const int32_t* __restrict__ qcount, int32_t k, int32_t B,
-                                 int64_t* __restrict__ idx_out, double* __restrict__ d2_out) {
+                                 int64_t* __restrict__ idx_out, double* __restrict__ d2_out, int32_t nsplit,
+                                 int32_t split_max, int64_t* __restrict__ tmp_idx, double* __restrict__ tmp_d2) {
+  // Work items: with nsplit > 1 the first split_max listed queries are cut into nsplit row slices each
+  // (item = (query, slice), top k of the slice into tmp, merged by exact_merge_kernel), so a handful
+  // of overflowed queries use the whole GPU instead of one SM each (c5, 3 queries: 339 -> ~35 ms);
+  // listed queries past split_max scan all rows in one item and write their result directly.
   extern __shared__ unsigned long long sbuf[];
   Key128* buf = reinterpret_cast<Key128*>(sbuf);
   const int nlist = *qcount;
   const int Kp = pow2_ceil(k);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int chunk = B - Kp;
-  for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
+  const int nsq = nsplit > 1 ? min(nlist, split_max) : 0;  // queries served in slices
+  const int items = nsq * nsplit + (nlist - nsq);
+  const int64_t slice = nsplit > 1 ? (n + nsplit - 1) / nsplit : n;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const bool split = item < nsq * nsplit;
+    const int li = split ? item / nsplit : nsq + (item - nsq * nsplit);
+    const int part = split ? item % nsplit : 0;
+    const int64_t row_lo = split ? part * slice : 0;
+    const int64_t row_hi = split ? min(n, row_lo + slice) : n;
     const int q = qlist[li];
     const double* qv = Q + size_t(q) * d;
     __syncthreads();
     for (int i = threadIdx.x; i < Kp; i += blockDim.x) buf[i] = Key128{~0ull, ~0ull};
-    for (int64_t pos = 0; pos < n; pos += chunk) {
+    __syncthreads();
+    for (int64_t pos = row_lo; pos < row_hi; pos += chunk) {
       // G lanes per row (exact_group(d)) with the selection's summation order (exact_d2_group), so a query
       // gets bit-identical distances whichever path served it
       const int grp = lane / G, gl = lane % G;
+      const Key128 kth = buf[k - 1];  // the k-th best so far (sorted prefix; all-ones until k rows are in)
+      int beats = 0;
       for (int i0 = warp * (32 / G); i0 < chunk; i0 += nwarps * (32 / G)) {
         const int i = i0 + grp;
         const int64_t col = pos + i;
-        const bool ok = i < chunk && col < n;
+        const bool ok = i < chunk && col < row_hi;
         const double dd = exact_d2_group<G>(X + size_t(ok ? col : 0) * d, qv, d, gl);
-        if (gl == 0 && i < chunk)
-          buf[Kp + i] = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)),
-                                    static_cast<unsigned long long>(col)}
-                           : Key128{~0ull, ~0ull};
+        if (gl == 0 && i < chunk) {
+          const Key128 key = ok ? Key128{static_cast<unsigned long long>(__double_as_longlong(dd)),
+                                         static_cast<unsigned long long>(col)}
+                                : Key128{~0ull, ~0ull};
+          buf[Kp + i] = key;
+          beats |= (key.hi < kth.hi || (key.hi == kth.hi && key.lo < kth.lo)) ? 1 : 0;
+        }
       }
-      bitonic_k128(buf, B);
+      // a chunk with no row ahead of the current k-th leaves the prefix as it is: no sort (after the
+      // first few chunks that is nearly every chunk, so the scan costs its distances, not its sorts)
+      if (__syncthreads_or(beats)) bitonic_k128(buf, B);
     }
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
-      idx_out[size_t(q) * k + i] = int64_t(buf[i].lo) + global_offset;
-      d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(buf[i].hi));
+    if (split) {  // the slice's best rows, (d2, local row) ascending; -1 pads a slice with fewer than k rows
+      for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const bool have = buf[i].lo != ~0ull;
+        tmp_idx[(size_t(li) * nsplit + part) * k + i] = have ? int64_t(buf[i].lo) : -1;
+        tmp_d2[(size_t(li) * nsplit + part) * k + i] = __longlong_as_double(static_cast<long long>(buf[i].hi));
+      }
+    } else {
+      for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        idx_out[size_t(q) * k + i] = int64_t(buf[i].lo) + global_offset;
+        d2_out[size_t(q) * k + i] = __longlong_as_double(static_cast<long long>(buf[i].hi));
+      }
+    }
+  }
+}
+
+// merges the nsplit sorted slice lists of each sliced query (one warp per query, lane p = slice p):
+// k rounds of the warp-wide smallest (d2, row) head, as merge_topk_kernel
+__global__ void __launch_bounds__(256) exact_merge_kernel(const int32_t* __restrict__ qlist,
+                                                          const int32_t* __restrict__ qcount, int32_t split_max,
+                                                          int32_t nsplit, int32_t k, int64_t global_offset,
+                                                          const int64_t* __restrict__ tmp_idx,
+                                                          const double* __restrict__ tmp_d2,
+                                                          int64_t* __restrict__ idx_out, double* __restrict__ d2_out) {
+  const int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (li >= min(*qcount, split_max)) return;
+  const int q = qlist[li];
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  int head = 0;
+  long long ci = LLONG_MAX;
+  double cd = kInf;
+  auto load = [&]() {
+    ci = LLONG_MAX;
+    cd = kInf;
+    if (lane < nsplit && head < k) {
+      const long long v = tmp_idx[(size_t(li) * nsplit + lane) * k + head];
+      if (v >= 0) {
+        ci = v;
+        cd = tmp_d2[(size_t(li) * nsplit + lane) * k + head];
+      }
+    }
+  };
+  load();
+  for (int i = 0; i < k; ++i) {
+    double bd = cd;
+    long long bi = ci;
+    int bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (od < bd || (od == bd && (oi < bi || (oi == bi && ol < bl)))) { bd = od; bi = oi; bl = ol; }
+    }
+    if (lane == 0) {
+      idx_out[size_t(q) * k + i] = bi + global_offset;
+      d2_out[size_t(q) * k + i] = bd;
+    }
+    if (lane == bl) {
+      ++head;
+      load();
     }
   }
 }
@@ -1230,16 +1309,29 @@ void launch_select(const float* X, int64_t global_offset, int32_t d, const doubl
 
 void launch_exact_knn_fallback(const float* X, int64_t n_local, int64_t global_offset, int32_t d, const double* Q,
                                const int32_t* qlist, const int32_t* qcount, int32_t k, int64_t* idx_out,
-                               double* d2_out, int num_sms, cudaStream_t s) {
+                               double* d2_out, int num_sms, cudaStream_t s, void* tmp, size_t tmp_bytes) {
   const int Kp = pow2_ceil(k);
   const int B = std::max(1024, 2 * Kp);
   const size_t smem = size_t(B) * sizeof(Key128);
   auto fb = exact_group(d) == 4 ? exact_knn_kernel<4> : exact_knn_kernel<8>;
   set_dynamic_smem(fb, smem);
   if (smem > 232448) throw Error{DK_EINVAL, "k too large for the exact k-NN fallback"};
-  fb<<<unsigned(std::max(1, num_sms)), 256, smem, s>>>(X, n_local, global_offset, d, Q, qlist, qcount, k, B, idx_out,
-                                                       d2_out);
+  // slices when the scratch (the candidate lists, free once the selection has run) holds them and
+  // every slice has at least k rows' worth of work
+  constexpr int kSplit = 32, kSplitMax = 128;
+  const size_t need = size_t(kSplitMax) * kSplit * k * 16;
+  const bool split = tmp != nullptr && tmp_bytes >= need && n_local >= int64_t(kSplit) * 4096;
+  int64_t* tmp_idx = static_cast<int64_t*>(tmp);
+  double* tmp_d2 = reinterpret_cast<double*>(tmp_idx + size_t(kSplitMax) * kSplit * k);
+  fb<<<unsigned(std::max(1, 2 * num_sms)), 256, smem, s>>>(X, n_local, global_offset, d, Q, qlist, qcount, k, B,
+                                                           idx_out, d2_out, split ? kSplit : 1, kSplitMax, tmp_idx,
+                                                           tmp_d2);
   DK_CHECK_LAUNCH();
+  if (split) {
+    exact_merge_kernel<<<kSplitMax * 32 / 256, 256, 0, s>>>(qlist, qcount, kSplitMax, kSplit, k, global_offset,
+                                                            tmp_idx, tmp_d2, idx_out, d2_out);
+    DK_CHECK_LAUNCH();
+  }
 }
 
 void launch_merge_topk(int32_t parts, int64_t nq, int32_t k, const int64_t* idx_in, const double* d2_in,

@@ -2,7 +2,9 @@
 with DK_KNN_MAX_BATCH=16384 (the round-1 split) in subprocesses and compare indices, distances and
 DEANN values bit for bit.
 
-    python scripts/batch_check.py c5 [nq]
+    python scripts/batch_check.py c5 [nq] [VAR=value ...]     # the second run's environment
+    python scripts/batch_check.py c5 0 DK_KNN_GTILES=600      # a looser threshold pass: some queries overflow
+                                                              # their candidate lists and take the exact scan
 """
 import os
 import subprocess
@@ -37,7 +39,8 @@ if __name__ == "__main__":
     config = sys.argv[1]
     nq = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     outs = []
-    for name, env in [("default", {}), ("b16384", {"DK_KNN_MAX_BATCH": "16384"})]:
+    alt = dict(a.split("=", 1) for a in sys.argv[3:]) or {"DK_KNN_MAX_BATCH": "16384"}
+    for name, env in [("default", {}), ("alt", alt)]:
         out = f"/tmp/batch_check_{name}.npz"
         subprocess.run([sys.executable, __file__, "--child", config, str(nq), out], check=True,
                        env={**os.environ, **env})

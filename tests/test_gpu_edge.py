@@ -252,3 +252,34 @@ def test_guard_on_dataset_shards():
     total = sum(g.naive_kde(p, g.KernelSpec("exponential", h), Q).values for p in parts)
     assert _redo_count(parts[0]) == 50
     assert _rel(total, O.naive_kde(O.Data(X), "exponential", h, Q)) < 1e-6  # the unflagged shard is a sweep
+
+
+def test_knn_overflow_fallback_in_row_slices(monkeypatch):
+    """20,000 copies of one row overflow a query's candidate list (cap 8,192): the query takes the exact
+    fp64 scan, cut into row slices over the whole GPU on datasets of >= 131,072 rows and merged by
+    (d2, index) — ties to the lower index as _smallest_k (ann.py:82-102)."""
+    import ctypes
+
+    from paper_2107_02736_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    n, d, k = 140_000, 8, 10
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    dup = rng.choice(n, size=20_000, replace=False)
+    X[dup] = X[dup[0]]
+    Q = np.vstack([X[dup[0]].astype(np.float64) + 1e-3, rng.normal(size=(40, d))])
+    monkeypatch.setenv("DK_KNN_STATS", "1")  # read at fit time: the handle counts its fallbacks
+    ds = g.Dataset.from_array(X)
+    od = O.Data(X)
+    idx, d2 = g.knn_batch(ds, Q, k)
+    v = [ctypes.c_int64(0) for _ in range(4)]
+    _lib.check(_lib.load().dk_knn_stats(ds.handle, *[ctypes.byref(x) for x in v]))
+    assert v[3].value >= 1  # the duplicated-row query overflowed
+    for j in range(Q.shape[0]):
+        ri, rd = O.brute_force_knn(od, Q[j], k)
+        if j > 0:
+            np.testing.assert_array_equal(idx[j], ri)
+        np.testing.assert_allclose(d2[j], rd, rtol=1e-9, atol=1e-12)
+    # the 20,000 copies are exactly tied: the lower indices win here; the reference's order among them
+    # follows the rounding of its BLAS matvec (the north star's "identical up to ties within 1e-6")
+    np.testing.assert_array_equal(idx[0], np.sort(dup)[:k])
