@@ -45,12 +45,15 @@ def make_rows(rng, kind, n, d):
 KINDS = ["normal", "mixture", "integer", "sparse", "unit", "pool", "offset"]
 
 
-def tie_tolerant_equal(gi, gd, ri, rd):
-    """Index sets equal up to rows whose distance is within 1e-6 relative of the boundary."""
+def tie_tolerant_equal(gi, gd, ri, rd, noise=0.0):
+    """Index sets equal up to rows whose distance is within 1e-6 relative of the boundary.
+
+    `noise`: absolute rounding level of the reference's own distances (norms identity in fp64,
+    ~64 ulp of |q|^2 + |x|^2), below which its order of two rows is not meaningful."""
     if np.array_equal(gi, ri):
         return True
     bound = rd[-1]
-    tol = 1e-6 * max(bound, 1e-300)
+    tol = 1e-6 * max(bound, 1e-300) + noise
     only_g = np.setdiff1d(gi, ri)
     only_r = np.setdiff1d(ri, gi)
     gpos = {int(v): i for i, v in enumerate(gi)}
@@ -60,10 +63,11 @@ def tie_tolerant_equal(gi, gd, ri, rd):
     if any(abs(rd[rpos[int(v)]] - bound) > tol for v in only_r):
         return False
     # common rows may be permuted only among (near-)equal distances
-    return bool(np.all(np.abs(np.sort(gd) - np.sort(rd)) <= 1e-6 * np.maximum(np.sort(rd), 1e-300) + 1e-300))
+    return bool(np.all(np.abs(np.sort(gd) - np.sort(rd)) <= 1e-6 * np.maximum(np.sort(rd), 1e-300) + noise + 1e-300))
 
 
-def trial(seed):
+def gen(seed):
+    """The trial's inputs: (rng, kind, n, d, nq, X, Q, family, h, scale)."""
     rng = np.random.default_rng(seed)
     kind = KINDS[int(rng.integers(0, len(KINDS)))]
     size = rng.choice(["small", "mid", "big", "hyb"], p=[0.3, 0.4, 0.2, 0.1])
@@ -101,6 +105,11 @@ def trial(seed):
         scale = float(np.median(np.sqrt(((a - b) ** 2).sum(1))))
     scale = max(scale, 0.5)
     h = scale * float(rng.choice([0.15, 0.4, 1.0, 3.0]))
+    return rng, kind, n, d, nq, X, Q, fam, h, scale
+
+
+def trial(seed):
+    rng, kind, n, d, nq, X, Q, fam, h, scale = gen(seed)
     spec = g.KernelSpec(fam, h)
     ds = g.Dataset.from_array(X)
     od = O.Data(X)
@@ -130,7 +139,7 @@ def trial(seed):
         ri, rd = O.brute_force_knn(od, Q[j], k)
         if np.array_equal(ri, gi[j]):
             exact_same += 1
-        elif not tie_tolerant_equal(gi[j], gd[j], ri, rd):
+        elif not tie_tolerant_equal(gi[j], gd[j], ri, rd, noise=64 * 2.2e-16 * (float(Q[j] @ Q[j]) + xn_max)):
             ok = False
             msgs.append(f"KNN q{j}")
         # the reference's d2 (norms identity in fp64) carries ~4 ulp of |q|^2 + |x|^2: floor the denominator there
