@@ -807,6 +807,10 @@ double env_double(const char* name, double def) {
   return v ? std::atof(v) : def;
 }
 
+// sweep values (as means over the global rows) under this are recomputed in fp64: the fp32 epilogue cannot
+// represent a term under ~1e-38
+constexpr double kUnderflow = 1e-30;
+
 bool kde_guard_on() {  // A/B: DK_KDE_GUARD=0 leaves the split3 sweeps unguarded
   static const bool on = [] {
     const char* v = std::getenv("DK_KDE_GUARD");
@@ -1489,6 +1493,8 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
     if (family == DK_LAPLACIAN) {
       const size_t o_part = pl.add<double>(l1_part_count(h->n, int32_t(nq)));
       const size_t o_q32 = pl.add<float>(size_t(l1_nq_pad(nq)) * h->d);
+      const size_t o_rlist = pl.add<int32_t>(size_t(nq) + 4);
+      const size_t o_rpart = pl.add<double>(size_t(nq) * kRedoChunks);
       h->ws.reserve(pl.off);
       const double* Qd = stage_queries(h, Q, nq, o_Q, s);
       int32_t nparts = 0;
@@ -1499,6 +1505,15 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
         launch_l1_kde(h->X, h->n, h->d, Qd, nq, 1.0 / bandwidth, part, &nparts, at<float>(h->ws, o_q32), s);
       }
       launch_reduce_partials(part, nparts, l1_nq_pad(nq), nq, scale, od, s);
+      h->redo_mask = 0;
+      if (kde_guard_on()) {  // queries under the fp32 epilogue's range: fp64 (redo.cu)
+        int32_t* rlist = at<int32_t>(h->ws, o_rlist);
+        launch_kde_redo(h->X, h->n, h->d, Qd, nq, family, bandwidth, nullptr, kUnderflow * scale * double(h->global_n),
+                        rlist + 4, rlist, at<double>(h->ws, o_rpart), scale, od, h->num_sms, s);
+        DK_CUDA(cudaMemcpyAsync(h->redo_host, rlist, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaEventRecord(h->redo_event, s));
+        h->redo_mask = 1;
+      }
       if (!out_dev) {
         copy_out(out, od, size_t(nq) * sizeof(double), s);
         DK_CUDA(cudaStreamSynchronize(s));
@@ -1615,8 +1630,8 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       launch_reduce_partials(a.part, ncc * kColGroups, pad, cn, scale, od + q0, s);
       if (guarded) {
         int32_t* rlist = at<int32_t>(h->ws, o_rlist[c]);
-        launch_kde_redo(h->X, h->n, h->d, Qc, cn, family == DK_GAUSSIAN, bandwidth, gflag, rlist + 4, rlist,
-                        at<double>(h->ws, o_rpart[c]), scale, od + q0, h->num_sms, s);
+        launch_kde_redo(h->X, h->n, h->d, Qc, cn, family, bandwidth, gflag, kUnderflow * scale * double(h->global_n),
+                        rlist + 4, rlist, at<double>(h->ws, o_rpart[c]), scale, od + q0, h->num_sms, s);
         DK_CUDA(cudaMemcpyAsync(h->redo_host + c, rlist, sizeof(int32_t), cudaMemcpyDeviceToHost, s));  // statistics
         DK_CUDA(cudaEventRecord(h->redo_event, s));
         h->redo_mask |= 1 << c;

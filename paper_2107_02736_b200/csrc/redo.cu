@@ -45,8 +45,11 @@ __global__ void guard_tau_kernel(const float* __restrict__ qn, int32_t nq_pad, i
   flag[row] = f;
 }
 
-// list the flagged rows (ascending); one CTA
-__global__ void __launch_bounds__(1024) redo_list_kernel(const uint32_t* __restrict__ flag, int64_t nq,
+// list the flagged rows (ascending), and the rows whose sweep value fell under `under`: the fp32
+// epilogue bottoms out near 2^-126 per term (ex2.approx flushes, the polynomial clamps: a query far from
+// every row comes back as ~1.5e-39 whatever its true 1e-50 is), the fp64 recomputation does not; one CTA
+__global__ void __launch_bounds__(1024) redo_list_kernel(const uint32_t* __restrict__ flag,
+                                                         const double* __restrict__ out, double under, int64_t nq,
                                                          int32_t* __restrict__ list, int32_t* __restrict__ count) {
   __shared__ int s_w[32];
   __shared__ int s_base;
@@ -55,7 +58,7 @@ __global__ void __launch_bounds__(1024) redo_list_kernel(const uint32_t* __restr
   __syncthreads();
   for (int64_t r0 = 0; r0 < nq; r0 += blockDim.x) {
     const int64_t r = r0 + threadIdx.x;
-    const bool on = r < nq && flag[r] != 0u;
+    const bool on = r < nq && ((flag != nullptr && flag[r] != 0u) || !(out[r] >= under));
     const uint32_t m = __ballot_sync(0xffffffffu, on);
     if (lane == 0) s_w[warp] = __popc(m);
     __syncthreads();
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(1024) redo_list_kernel(const uint32_t* __restr
 // groups are added in a fixed order into part[item].
 template <int G>
 __global__ void __launch_bounds__(kRedoThreads) redo_eval_kernel(const float* __restrict__ X, int64_t n, int32_t d,
-                                                                 const double* __restrict__ Q, int32_t gaussian,
+                                                                 const double* __restrict__ Q, int32_t family,
                                                                  double c, const int32_t* __restrict__ list,
                                                                  const int32_t* __restrict__ count, int32_t nchunks,
                                                                  int32_t q_smem, double* __restrict__ part) {
@@ -109,12 +112,12 @@ __global__ void __launch_bounds__(kRedoThreads) redo_eval_kernel(const float* __
         const float* x = X + size_t(r) * d;
         for (int i = gl; i < d; i += G) {
           const double df = qv[i] - double(x[i]);
-          s = fma(df, df, s);
+          s = family == DK_LAPLACIAN ? s + fabs(df) : fma(df, df, s);
         }
       }
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (gl == 0 && valid) acc += gaussian ? exp(s * c) : exp(sqrt(s) * c);
+      if (gl == 0 && valid) acc += family == DK_EXPONENTIAL ? exp(sqrt(s) * c) : exp(s * c);
     }
     if (gl == 0) sgrp[warp * R + grp] = acc;
     __syncthreads();
@@ -145,19 +148,19 @@ void launch_guard_tau(const float* qn, int32_t nq_pad, int64_t nq, float xn_max,
   DK_CHECK_LAUNCH();
 }
 
-void launch_kde_redo(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, bool gaussian, double h,
-                     const uint32_t* flag, int32_t* list, int32_t* count, double* part, double scale, double* out,
-                     int num_sms, cudaStream_t s) {
-  redo_list_kernel<<<1, 1024, 0, s>>>(flag, nq, list, count);
+void launch_kde_redo(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, int32_t family, double h,
+                     const uint32_t* flag, double under, int32_t* list, int32_t* count, double* part, double scale,
+                     double* out, int num_sms, cudaStream_t s) {
+  redo_list_kernel<<<1, 1024, 0, s>>>(flag, out, under, nq, list, count);
   DK_CHECK_LAUNCH();
-  const double c = gaussian ? -1.0 / (2.0 * h * h) : -1.0 / h;
+  const double c = family == DK_GAUSSIAN ? -1.0 / (2.0 * h * h) : -1.0 / h;
   const int grid = num_sms * 4;
   const int G = d >= 32 ? 32 : (d > 8 ? 16 : (d > 2 ? 4 : 1));
   const bool q_smem = d <= 16384;  // wider queries are read through L1
   const size_t smem = (size_t(q_smem ? d : 0) + kRedoWarps * 32) * sizeof(double);
   auto run = [&](auto kern) {
     if (smem > 48 * 1024) DK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<grid, kRedoThreads, smem, s>>>(X, n, d, Q, gaussian ? 1 : 0, c, list, count, kRedoChunks, q_smem ? 1 : 0, part);
+    kern<<<grid, kRedoThreads, smem, s>>>(X, n, d, Q, family, c, list, count, kRedoChunks, q_smem ? 1 : 0, part);
   };
   if (G == 32) run(redo_eval_kernel<32>);
   else if (G == 16) run(redo_eval_kernel<16>);

@@ -283,3 +283,20 @@ def test_knn_overflow_fallback_in_row_slices(monkeypatch):
     # the 20,000 copies are exactly tied: the lower indices win here; the reference's order among them
     # follows the rounding of its BLAS matvec (the north star's "identical up to ties within 1e-6")
     np.testing.assert_array_equal(idx[0], np.sort(dup)[:k])
+
+
+@pytest.mark.parametrize("family,h", [("gaussian", 1.2), ("exponential", 0.12), ("laplacian", 0.2)])
+def test_far_queries_below_the_fp32_range(family, h):
+    """KDE values under ~1e-38 cannot come out of the fp32 epilogue (flushed exponentials; the polynomial's
+    clamp leaves ~1.5e-39): such queries are recomputed in fp64 and match the reference's tiny values."""
+    rng = np.random.default_rng(77)
+    X = rng.normal(size=(3000, 3)).astype(np.float32)
+    Q = np.vstack([rng.normal(size=(20, 3)), rng.normal(size=(20, 3)) + 14.0])  # 20 ordinary, 20 far away
+    ds = g.Dataset.from_array(X)
+    got = g.naive_kde(ds, g.KernelSpec(family, h), Q).values
+    ref = O.naive_kde(O.Data(X), family, h, Q)
+    assert ref[20:].max() < 1e-40 and ref[20:].min() > 1e-290
+    assert _redo_count(ds) >= 20
+    assert _rel(got[20:], ref[20:]) < 1e-9
+    ordinary = ref[:20] > 1e-30
+    assert _rel(got[:20][ordinary], ref[:20][ordinary]) < KDE_RTOL
