@@ -285,7 +285,7 @@ dk_status dk_kde_stats(dk_handle h, int64_t* queries, int64_t* fallbacks, int64_
  * exponential-kernel queries with a row closer than the distance under which the sweep's d2 error
  * could move exp(-sqrt(d2)/h) by more than 1e-4, gaussian queries whose d2 error bound exceeds
  * 5e-5 x 2h^2, and (these and the laplacian kernel) queries whose KDE came back under 1e-30, below the
- * fp32 epilogue's range.  Integer datasets in exact mode and the two-precision path are not guarded.
+ * fp32 epilogue's range.  Integer datasets in exact mode are not guarded.
  * Waits for that call's work.  No reference counterpart. */
 dk_status dk_kde_redo_count(dk_handle h, int64_t* count);
 /* Diagnostics: time (ms, CUDA events) of one tile sweep of the given mode

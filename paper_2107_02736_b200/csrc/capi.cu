@@ -811,6 +811,9 @@ double env_double(const char* name, double def) {
 // represent a term under ~1e-38
 constexpr double kUnderflow = 1e-30;
 
+// d2 error model of a split3 sweep, relative to |q|^2 + max |x|^2 (see dk_naive)
+double guard_delta_rel(int32_t Kp) { return 0.5 * (std::ldexp(1.0, -21) + double(Kp / 16) * std::ldexp(1.0, -24)); }
+
 bool kde_guard_on() {  // A/B: DK_KDE_GUARD=0 leaves the split3 sweeps unguarded
   static const bool on = [] {
     const char* v = std::getenv("DK_KDE_GUARD");
@@ -1547,12 +1550,10 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       o_scal[c] = pl.add<float>(4);
       o_part[c] = pl.add<double>(sweep_part_count(h->n_pad, pad, h->num_sms));
       o_fl[c] = pl.add<uint32_t>(4);
-      if (!hyb) {  // guard of the split3 sweeps (redo.cu)
-        o_tau[c] = pl.add<float>(pad);
-        o_gflag[c] = pl.add<uint32_t>(pad);
-        o_rlist[c] = pl.add<int32_t>(size_t(pad) + 4);
-        o_rpart[c] = pl.add<double>(size_t(c_cnt[c]) * kRedoChunks);
-      }
+      if (!hyb) o_tau[c] = pl.add<float>(pad);  // guard of the split3 sweeps (redo.cu)
+      o_gflag[c] = pl.add<uint32_t>(pad);
+      o_rlist[c] = pl.add<int32_t>(size_t(pad) + 4);  // (the two-precision path: underflowed queries only)
+      o_rpart[c] = pl.add<double>(size_t(c_cnt[c]) * kRedoChunks);
     }
     const HybLayout HL = hyb ? hyb_layout(h, std::max(c_cnt[0], c_cnt[1]), nq, pl.off) : HybLayout{};
     h->ws.reserve(hyb ? HL.end + 4096 : pl.off);
@@ -1612,7 +1613,7 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       const bool guarded = mode == 1 && kde_guard_on();
       uint32_t* gflag = nullptr;
       if (guarded) {
-        const double delta_rel = 0.5 * (std::ldexp(1.0, -21) + double(e.Kp / 16) * std::ldexp(1.0, -24));
+        const double delta_rel = guard_delta_rel(e.Kp);
         gflag = at<uint32_t>(h->ws, o_gflag[c]);
         launch_guard_tau(q.qn, pad, cn, e.xn_max, delta_rel, family == DK_GAUSSIAN ? 5e-5 : 1e-4, bandwidth,
                          family == DK_GAUSSIAN, at<float>(h->ws, o_tau[c]), gflag, s);
@@ -1649,6 +1650,21 @@ dk_status dk_naive(dk_handle h, const double* Q, int64_t nq, int32_t family, dou
       if (c == 1) DK_CUDA(cudaStreamWaitEvent(s, h->copy_done, 0));
       if (hyb) {
         kde_hybrid(h, Qd, c_beg[c], c_cnt[c], bandwidth, scale, od, s, HL, c == 0, c == nchunks - 1);
+        if (kde_guard_on()) {
+          // the hot pairs run the same split3 arithmetic as the plain sweep: the same gaussian guard
+          // (d2 error against 2h^2), from the raw queries; and values under the fp32 epilogue's range
+          int32_t* rlist = at<int32_t>(h->ws, o_rlist[c]);
+          uint32_t* gflag = at<uint32_t>(h->ws, o_gflag[c]);
+          const Encoding& e3 = h->kc->enc3;
+          launch_guard_flag_raw(Qd + size_t(c_beg[c]) * h->d, h->mu, h->d, c_cnt[c], e3.xn_max, guard_delta_rel(e3.Kp),
+                                5e-5 * 2.0 * bandwidth * bandwidth, gflag, s);
+          launch_kde_redo(h->X, h->n, h->d, Qd + size_t(c_beg[c]) * h->d, c_cnt[c], family, bandwidth, gflag,
+                          kUnderflow * scale * double(h->global_n), rlist + 4, rlist, at<double>(h->ws, o_rpart[c]),
+                          scale, od + c_beg[c], h->num_sms, s);
+          DK_CUDA(cudaMemcpyAsync(h->redo_host + c, rlist, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+          DK_CUDA(cudaEventRecord(h->redo_event, s));
+          h->redo_mask |= 1 << c;
+        }
         if (!out_dev && c == nchunks - 1) copy_out(out, od, size_t(nq) * sizeof(double), s);
         continue;
       }

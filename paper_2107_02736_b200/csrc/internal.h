@@ -335,6 +335,8 @@ void set_pair_enabled(bool on);  // 2-CTA (cta_group::2) sweeps; off by default 
 constexpr int32_t kRedoChunks = 64;  // row chunks per listed query (partials: [nq][kRedoChunks])
 void launch_guard_tau(const float* qn, int32_t nq_pad, int64_t nq, float xn_max, double delta_rel, double tol,
                       double h, bool gaussian, float* tau, uint32_t* flag, cudaStream_t s);
+void launch_guard_flag_raw(const double* Q, const double* mu, int32_t d, int64_t nq, float xn_max, double delta_rel,
+                           double lim, uint32_t* flag, cudaStream_t s);
 // flag may be nullptr; rows whose value in `out` is under `under` are recomputed too (fp32 underflow)
 void launch_kde_redo(const float* X, int64_t n, int32_t d, const double* Q, int64_t nq, int32_t family, double h,
                      const uint32_t* flag, double under, int32_t* list, int32_t* count, double* part, double scale,

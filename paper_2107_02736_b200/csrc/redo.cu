@@ -45,6 +45,24 @@ __global__ void guard_tau_kernel(const float* __restrict__ qn, int32_t nq_pad, i
   flag[row] = f;
 }
 
+// the gaussian flag from the raw queries (the two-precision path keeps its operands in ball order): one warp
+// per query, |q - mu|^2 in fp64, flag = delta_rel (|q - mu|^2 + xn_max) > lim (= tol 2h^2)
+__global__ void guard_flag_raw_kernel(const double* __restrict__ Q, const double* __restrict__ mu, int32_t d,
+                                      int64_t nq, float xn_max, double delta_rel, double lim,
+                                      uint32_t* __restrict__ flag) {
+  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  double s = 0.0;
+  for (int i = lane; i < d; i += 32) {
+    const double t = Q[size_t(q) * d + i] - (mu != nullptr ? mu[i] : 0.0);
+    s = fma(t, t, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) flag[q] = delta_rel * (s + double(xn_max)) > lim ? 1u : 0u;
+}
+
 // list the flagged rows (ascending), and the rows whose sweep value fell under `under`: the fp32
 // epilogue bottoms out near 2^-126 per term (ex2.approx flushes, the polynomial clamps: a query far from
 // every row comes back as ~1.5e-39 whatever its true 1e-50 is), the fp64 recomputation does not; one CTA
@@ -145,6 +163,12 @@ void launch_guard_tau(const float* qn, int32_t nq_pad, int64_t nq, float xn_max,
                       double h, bool gaussian, float* tau, uint32_t* flag, cudaStream_t s) {
   guard_tau_kernel<<<(nq_pad + 255) / 256, 256, 0, s>>>(qn, nq_pad, nq, xn_max, delta_rel, tol, h, gaussian ? 1 : 0,
                                                         tau, flag);
+  DK_CHECK_LAUNCH();
+}
+
+void launch_guard_flag_raw(const double* Q, const double* mu, int32_t d, int64_t nq, float xn_max, double delta_rel,
+                           double lim, uint32_t* flag, cudaStream_t s) {
+  guard_flag_raw_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(Q, mu, d, nq, xn_max, delta_rel, lim, flag);
   DK_CHECK_LAUNCH();
 }
 

@@ -194,3 +194,25 @@ def test_handles_release_the_two_precision_operands():
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 < 64 << 20, (free0, free1)
+
+
+def test_far_queries_on_the_two_precision_path():
+    """A batch large enough for the two-precision path with queries far from every row: their values lie
+    under the fp32 epilogue's range and are recomputed in fp64 (redo.cu), as on the split3 path."""
+    rng = np.random.default_rng(3)
+    n, d = 140_000, 16
+    centers = rng.normal(scale=3.0, size=(40, d))
+    X = (centers[rng.integers(0, 40, n)] + 0.3 * rng.normal(size=(n, d))).astype(np.float32)
+    Q = centers[rng.integers(0, 40, 2304)] + 0.3 * rng.normal(size=(2304, d))
+    Q[:16] += 25.0
+    h = 0.9
+    ds = g.Dataset.from_array(X)
+    got = g.naive_kde(ds, g.KernelSpec("gaussian", h), Q).values
+    c = ctypes.c_int64(-1)
+    _lib.check(_lib.load().dk_kde_redo_count(ds.handle, ctypes.byref(c)))
+    sel = np.r_[0:16, 16:2304:97]
+    ref = O.naive_kde(O.Data(X), "gaussian", h, Q[sel])
+    assert ref[:16].max() < 1e-40 and c.value >= 16
+    np.testing.assert_allclose(got[sel][:16], ref[:16], rtol=1e-9)
+    live = ref[16:] > 1e-30
+    np.testing.assert_allclose(got[sel][16:][live], ref[16:][live], rtol=1e-5)
